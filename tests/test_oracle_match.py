@@ -1,0 +1,118 @@
+"""Pins for the oracle's NCC (a7) and PCE (a8): P:93; S:284-331;
+readings R-15..R-20."""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import match
+
+
+def brute_surface(R, T):
+    """Direct O(N^4) circular correlation of the mean-removed inputs."""
+    R = R - R.mean()
+    T = T - T.mean()
+    H, W = R.shape
+    C = np.zeros((H, W))
+    for dy in range(H):
+        for dx in range(W):
+            C[dy, dx] = np.sum(R * np.roll(T, (dy, dx), axis=(0, 1)))
+    return C
+
+
+@pytest.mark.parametrize("shape", [(8, 8), (13, 21), (32, 32)])
+def test_fft_surface_equals_brute_force(shape):
+    """S:292, S:322 (AC7): FFT surface == direct spatial computation."""
+    rng = np.random.default_rng(shape[0])
+    R, T = rng.normal(size=shape), rng.normal(size=shape)
+    np.testing.assert_allclose(oracle.correlation_surface(R, T), brute_surface(R, T), atol=1e-9)
+
+
+def test_shift_theorem_and_peak():
+    """R = T circularly shifted by (3, 5) -> peak at (3, 5)."""
+    rng = np.random.default_rng(0)
+    T = rng.normal(size=(40, 48))
+    R = np.roll(T, (3, 5), axis=(0, 1))
+    p, (dy, dx), peak = oracle.pce(R, T)
+    assert (dy, dx) == (3, 5)
+    assert p > 1e3
+    p2, shift2, _ = oracle.pce(np.roll(R, (7, 1), axis=(0, 1)), T)
+    assert shift2 == (10, 6)
+    assert abs(p2 - p) / p < 1e-9
+
+
+def test_scale_invariance():
+    """positive gains leave PCE unchanged."""
+    rng = np.random.default_rng(1)
+    R, T = rng.normal(size=(32, 32)), rng.normal(size=(32, 32))
+    R[0, 0] += 20
+    T[0, 0] += 20
+    a = oracle.pce(R, T)[0]
+    b = oracle.pce(3.5 * R + 2.0, 0.25 * T - 7.0)[0]
+    assert abs(a - b) / abs(a) < 1e-9
+
+
+def test_pce_closed_form_surface():
+    """Surface with C[2,3] = 10 and 1 elsewhere: the 11x11 neighbourhood holds 120
+    ones, background mean of C^2 = (255 - 120)/(256 - 121) = 1 -> PCE = 100."""
+    C = np.ones((16, 16))
+    C[2, 3] = 10.0
+    p, peak, v = match.pce_from_surface(C, 5)
+    assert peak == (2, 3) and v == 10.0
+    assert abs(p - 100.0) < 1e-12
+    C[2, 3] = -10.0                          # sign is kept
+    assert abs(match.pce_from_surface(C, 5)[0] + 100.0) < 1e-12
+
+
+def test_delta_surface_caps():
+    """delta surface -> zero background energy -> cap 1e12."""
+    C = np.zeros((16, 16))
+    C[0, 0] = 1.0
+    assert match.pce_from_surface(C, 5)[0] == match.PCE_CAP
+
+
+def test_argmax_tie_smallest_index():
+    C = np.zeros((20, 20))
+    C[3, 4] = -2.0
+    C[1, 7] = 2.0
+    C[15, 15] = 0.5
+    assert match.pce_from_surface(C, 2)[1] == (1, 7)
+
+
+def test_null_calibration():
+    """S:300, S:608 (AC8): independent random inputs -> P(PCE > 60) < 5%."""
+    rng = np.random.default_rng(7)
+    hits = 0
+    for _ in range(200):
+        R, T = rng.normal(size=(128, 128)), rng.normal(size=(128, 128))
+        hits += oracle.pce(R, T)[0] > match.PCE_THRESHOLD
+    assert hits / 200 < 0.05
+
+
+def test_ncc_properties():
+    rng = np.random.default_rng(2)
+    a = rng.normal(size=(20, 30))
+    assert abs(oracle.ncc(a, a) - 1) < 1e-15
+    assert abs(oracle.ncc(a, -a) + 1) < 1e-15
+    assert abs(oracle.ncc(a, 3 * a + 7) - 1) < 1e-14
+    assert abs(oracle.ncc(a, -0.5 * a + 1) + 1) < 1e-14
+    b = rng.normal(size=(20, 30))
+    # equals the value of the correlation surface at shift 0 normalised by the norms
+    C = oracle.correlation_surface(a, b)
+    a0, b0 = a - a.mean(), b - b.mean()
+    assert abs(C[0, 0] / np.sqrt((a0 ** 2).sum() * (b0 ** 2).sum()) - oracle.ncc(a, b)) < 1e-14
+    with pytest.raises(ValueError):
+        oracle.ncc(np.ones((4, 4)), a[:4, :4])
+
+
+def test_aligned_pce_uses_origin():
+    rng = np.random.default_rng(3)
+    T = rng.normal(size=(32, 32))
+    R = np.roll(T, (4, 4), axis=(0, 1))
+    p_al, peak, _ = oracle.pce(R, T, aligned=True)
+    assert peak == (0, 0)
+    assert p_al < oracle.pce(R, T)[0]
+
+
+def test_threshold_strict():
+    """pce exactly 60 -> no match (strict '>')."""
+    assert not (60.0 > match.PCE_THRESHOLD)
