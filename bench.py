@@ -1,0 +1,408 @@
+#!/usr/bin/env python
+"""bench.py — SDA-frame PRNU fingerprint extraction on B200 (BASELINE config 2).
+
+One step = the whole hot path over one synthetic 1800-frame
+1920x1080 u8 video resident in HBM:
+  * conventional fingerprint (depth 1: 1800 denoisings)            a2-a6
+  * SDA fingerprint (depth 50: averaging + 36 denoisings)          a1-a6
+  * NCC of both fingerprints against the true K                    a7
+  * residual of a fresh query frame + PCE vs both fingerprints     a2-a4, a8
+metric: denoised Full-HD frames/s (1836 fingerprint denoisings per step), with
+fingerprints/s per depth beside it.  `e2e` repeats the two extractions through
+the host-buffer C-ABI call (frames in pinned host memory, K back to the host).
+
+python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+N > 1 runs N independent replicas (one video per rank; DESIGN.md "replicas
+only"), launched by torchrun; timing is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["prnu", "reference"], default="prnu")
+    ap.add_argument("--frames", type=int, default=1800)
+    ap.add_argument("--height", type=int, default=1080)
+    ap.add_argument("--width", type=int, default=1920)
+    ap.add_argument("--depths", default="1,50")
+    ap.add_argument("--batch", type=int, default=16, help="SDA frames denoised per wave at depth 1")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the oracle sample")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ dist
+def dist_setup(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if torch.cuda.is_available() and dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """Samples SM clock + throttle reasons with NVML every 20 ms while active."""
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+                 "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4, "applications_clocks_setting": 0x2}
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(s)}
+
+
+# ------------------------------------------------------------------ roofline model
+def sub_len(n):
+    return (n + 7) // 2
+
+
+def algorithmic_bytes_per_step(name: str, H: int, W: int, levels: int, depths, m: int, n_query: int = 1):
+    """Algorithmic HBM bytes one step moves through kernel `name`:
+    each input read once and each output written once at real (unpadded) sizes;
+    NUM/DEN (fp64) read + written once per synth_acc launch (counted by caller).
+    Frames per step: depth-1 fingerprint m (u8 input), SDA fingerprints m//d
+    (fp32 input), query residual n_query (u8 input)."""
+    nH, nW = [H], [W]
+    for _ in range(levels):
+        nH.append(sub_len(nH[-1]))
+        nW.append(sub_len(nW[-1]))
+    n = [nH[l] * nW[l] for l in range(levels + 1)]
+    P = H * W
+    f_u8 = (m if 1 in depths else 0) + n_query          # level-1 u8 inputs
+    f_f32 = sum(m // d for d in depths if d > 1)        # SDA frames
+    f_all = f_u8 + f_f32
+    if name == "sda_average":
+        return sum((m // d) * (d * P + 4 * P) for d in depths if d > 1)
+    if name == "analysis_l1_u8":
+        return f_u8 * (1 * P + 4 * 4 * n[1])
+    if name == "analysis_l1_f32":
+        return f_f32 * (4 * P + 4 * 4 * n[1])
+    if name.startswith("analysis_l"):
+        l = int(name[-1])
+        return f_all * (4 * n[l - 1] + (4 if l < levels else 3) * 4 * n[l])
+    if name.startswith("synthesis_l") and name != "synthesis_l1":
+        l = int(name[-1])
+        return f_all * ((4 if l < levels else 3) * 4 * n[l] + 4 * n[l - 1])
+    if name == "synthesis_l1":
+        return n_query * (4 * 4 * n[1] + 4 * P)
+    if name == "synth_acc_l1_u8":
+        return (m if 1 in depths else 0) * (4 * 4 * n[1] + 1 * P)
+    if name == "synth_acc_l1_f32":
+        return f_f32 * (4 * 4 * n[1] + 4 * P)
+    return None
+
+
+# ------------------------------------------------------------------ reference arm / cpu baseline
+def oracle_sample(frames_host, depths, budget_s: float):
+    """Time the oracle (as it stands, single thread) on a bounded sample of the
+    workload: for each depth, extract a fingerprint from the first k*depth frames
+    with k grown until the budget is spent.  Returns (denoises/s, description)."""
+    import oracle
+    fr = frames_host
+    t_total, n_total, desc = 0.0, 0, []
+    per_depth = budget_s / len(depths)
+    for d in depths:
+        k = 1
+        t_d = 0.0
+        n_d = 0
+        while True:
+            t0 = time.perf_counter()
+            oracle.extract_fingerprint(fr[: k * d], d)
+            dt = time.perf_counter() - t0
+            t_d += dt
+            n_d += k
+            if t_d + 2 * dt > per_depth or (k + 1) * d > fr.shape[0]:
+                break
+            k += 1
+        t_total += t_d
+        n_total += n_d
+        desc.append(f"d={d}: {n_d} denoisings over {t_d:.1f}s")
+    return n_total / t_total, "; ".join(desc)
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the fp64 CPU oracle on the host cores (rank 0 only)."""
+    import numpy as np
+    import torch
+
+    import synth
+    if rank != 0:
+        return
+    depths = [int(x) for x in args.depths.split(",")]
+    m = min(args.frames, max(depths) * 2)
+    v = synth.video("drift", m, args.height, args.width, seed=0,
+                    device="cuda" if torch.cuda.is_available() else "cpu")
+    fr = v.frames.cpu().numpy()
+    per_step = max(2.0, min(args.cpu_seconds, 60.0) / max(1, args.steps + args.warmup))
+    for _ in range(args.warmup):
+        oracle_sample(fr, depths, per_step)
+    rates = []
+    t_all = 0.0
+    n_all = 0
+    desc = ""
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        r, desc = oracle_sample(fr, depths, per_step)
+        t_all += time.perf_counter() - t0
+        rates.append(r)
+    value = float(np.mean(rates))
+    line = {"impl": "reference", "metric": "denoised Full-HD frames/sec", "value": value,
+            "unit": "denoised FHD frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * t_all / max(1, args.steps), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C2 {args.frames}x{args.height}x{args.width} u8 video, depths {depths} "
+                                   "(bounded oracle sample per step)",
+                       "frames": args.frames, "H": args.height, "W": args.width, "depths": depths},
+            "cpu_baseline": {"value": value, "unit": "denoised FHD frames/s", "cores": 1, "kind": "oracle",
+                             "sample": desc},
+            "e2e": {"value": value, "unit": "denoised FHD frames/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ main arm
+def main():
+    args = parse()
+    rank, world, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import numpy as np
+    import torch
+
+    import paper_1909_04573_b200 as prnu
+    import synth
+
+    assert torch.cuda.is_available(), "bench.py needs a CUDA device"
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    depths = [int(x) for x in args.depths.split(",")]
+    m, H, W = args.frames, args.height, args.width
+
+    # ---- inputs: one synthetic video per rank (+1 query frame), resident in HBM
+    allf = torch.empty((m + 1, H, W), dtype=torch.uint8, device=dev)
+    v = synth.video("drift", m + 1, H, W, seed=rank, device=dev, out=allf)
+    frames, query = allf[:m], allf[m:]
+    K_true = v.K.contiguous()
+    torch.cuda.synchronize()
+
+    exs = {d: prnu.Extractor(H, W, d, batch=(args.batch if d == 1 else max(1, min(64, m // d))), device=dev)
+           for d in depths}
+    n_sda = {d: m // d for d in depths}
+    plan = prnu.PcePlan(H, W, len(depths), device=dev)
+
+    def step():
+        Ks = []
+        for d in depths:
+            Ks.append(exs[d](frames).K)
+        for K in Ks:
+            prnu.ncc(K, K_true)
+        Rq = prnu.residual(query, zero_mean=True)
+        T = prnu.pce_template(torch.stack(Ks), query.expand(len(depths), H, W).contiguous())
+        return plan(Rq.expand(len(depths), H, W).contiguous(), T)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = prnu.kernel_launches()
+    sampler = ClockSampler(dev.index)
+    barrier(world)
+    torch.cuda.synchronize()
+    with sampler:
+        e0.record(stream)
+        for _ in range(args.steps):
+            res = step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    ms = e0.elapsed_time(e1)
+    launches = prnu.kernel_launches() - launches0
+    ms_max = max_over_ranks(ms, world)
+    ms_step = ms_max / args.steps
+    denoise_per_step = sum(n_sda.values())
+    value = denoise_per_step * args.steps * world / (ms_max / 1000.0)
+    pce_vals = res.pce.cpu().tolist()
+
+    # ---- per-kernel event timing over the same K steps (separate pass)
+    roof, kernels = None, None
+    if not args.no_profile:
+        prnu._lib.prnu_profile_begin()
+        for _ in range(args.steps):
+            step()
+        torch.cuda.synchronize()
+        import ctypes
+        maxk = 64
+        names = ctypes.create_string_buffer(64 * maxk)
+        tot = (ctypes.c_double * maxk)()
+        cnt = (ctypes.c_int64 * maxk)()
+        nk = ctypes.c_int()
+        prnu._lib.prnu_profile_end(maxk, names, tot, cnt, ctypes.byref(nk))
+        kernels = {}
+        for k in range(min(nk.value, maxk)):
+            nm = names.raw[64 * k: 64 * k + 64].split(b"\0")[0].decode()
+            kernels[nm] = {"ms_per_step": tot[k] / args.steps, "launches_per_step": cnt[k] / args.steps}
+        tot_ms = sum(x["ms_per_step"] for x in kernels.values())
+        peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+        peaks = json.load(open(peaks_path)) if os.path.exists(peaks_path) else {}
+        peak = peaks.get("hbm_gbs", 6650.0)
+        for nm, x in kernels.items():
+            x["share"] = x["ms_per_step"] / tot_ms
+            by = algorithmic_bytes_per_step(nm, H, W, 4, depths, m)
+            if by is not None and nm.startswith("synth_acc"):
+                by += 32 * H * W * x["launches_per_step"]          # NUM/DEN read + write per launch
+            if by is not None:
+                x["alg_bytes_per_launch"] = by / x["launches_per_step"]
+                x["alg_GBps"] = by / (x["ms_per_step"] / 1000.0) / 1e9
+        # dominant kernel = largest share of kernel time
+        top = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
+        kt = kernels[top]
+        avg_ms = kt["ms_per_step"] / kt["launches_per_step"]
+        achieved = kt.get("alg_GBps")
+        roof = {"kernel": top, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": None,
+                "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback",
+                "bytes_per_launch": kt.get("alg_bytes_per_launch"), "avg_launch_ms": avg_ms,
+                "share_of_kernel_time": kt["share"]}
+
+    # ---- e2e through the host-buffer C-ABI call
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty((m, H, W), dtype=torch.uint8, pin_memory=True)
+        host.copy_(frames)
+        exh = {d: prnu.Extractor(H, W, d, batch=exs[d].batch, device=dev, host=True) for d in depths}
+        for _ in range(1):
+            for d in depths:
+                exh[d](host)
+        torch.cuda.synchronize()
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            for d in depths:
+                exh[d](host)
+        t = time.perf_counter() - t0
+        t = max_over_ranks(t, world)
+        e2e = {"value": denoise_per_step * args.e2e_steps * world / t, "unit": "denoised FHD frames/s",
+               "h2d_bytes_per_step": int(len(depths) * m * H * W), "d2h_bytes_per_step": int(len(depths) * H * W * 4),
+               "steps": args.e2e_steps, "fingerprints_per_s": len(depths) * args.e2e_steps * world / t}
+        del host
+
+    # ---- cpu baseline: the oracle on a bounded sample (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        fr = frames[: max(depths) * 2].cpu().numpy()
+        r, desc = oracle_sample(fr, depths, args.cpu_seconds)
+        cpu = {"value": r, "unit": "denoised FHD frames/s", "cores": 1, "kind": "oracle",
+               "sample": f"fp64 C oracle, single thread, first frames of the same video: {desc}"}
+
+    if rank == 0:
+        ncc_vals = [prnu.ncc(exs[d](frames).K, K_true).item() for d in depths]
+        line = {
+            "metric": "denoised Full-HD frames/sec (1800-frame video fingerprints, depths 1 and 50)",
+            "value": value, "unit": "denoised FHD frames/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 (fp64 accumulators; u8 input)", "data": "synthetic",
+            "config": {"workload": f"C2: {m}x{W}x{H} u8 video, fingerprints at depths {depths}, NCC vs true K, "
+                                   "query residual + PCE", "frames": m, "H": H, "W": W, "depths": depths,
+                       "batch": args.batch, "denoises_per_step": denoise_per_step,
+                       "l2": f"inputs ({m * H * W / 1e9:.2f} GB u8) larger than the 126 MB L2; no flush",
+                       "parallelism": f"replicas x{world}"},
+            "fingerprints_per_s": {f"depth{d}": 1000.0 / ms_step * world for d in depths},
+            "source_frames_per_s": len(depths) * m * world * 1000.0 / ms_step,
+            "ncc_vs_true_K": dict(zip([f"depth{d}" for d in depths], ncc_vals)),
+            "pce_query": pce_vals,
+            "gpu_launches": int(launches),
+            "clocks": sampler.summary(),
+            "roofline": roof,
+            "kernels": kernels,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    barrier(world)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,222 @@
+/*
+ * prnu.h — C ABI of libprnu.so, the B200 (sm_100a) hot path of SDA-frame PRNU
+ * fingerprint extraction (Taspinar, Mohanty, Memon, arXiv 1909.04573).
+ *
+ * Citations: P:<n> = PAPER.md line n; S:<n> = SPEC.md line n; R-<n> = a
+ * reading of the paper fixed in DESIGN.md §3 where the paper is silent.
+ *
+ * Conventions (all entry points):
+ *  - Every pointer is a DEVICE pointer owned by the caller unless the argument
+ *    name ends in `_host`.  The library never allocates or frees caller memory;
+ *    scratch space is the caller-owned `ws` of at least the size the matching
+ *    `*_workspace_bytes` query returns (256-byte aligned).
+ *  - Planes are row-major and contiguous: `[batch][H][W]`, H rows of W columns,
+ *    frames/batch outermost.  "1920x1080" means W = 1920, H = 1080.
+ *  - Calls are asynchronous on `stream` (a `cudaStream_t` passed as void*;
+ *    NULL = the legacy default stream).  Arguments are validated synchronously
+ *    before anything is launched; on a non-zero status nothing was launched
+ *    (except PRNU_CUDA_ERROR, which reports a failed launch).
+ *  - Results are deterministic: identical inputs give bit-identical outputs,
+ *    independent of `batch` (no atomics on any value-carrying path, fixed
+ *    reduction orders).
+ *  - `prnu_last_error()` returns a thread-local description of the last
+ *    failure of the calling thread.
+ */
+#ifndef PRNU_H
+#define PRNU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes (SPEC error names in brackets). */
+enum {
+    PRNU_OK = 0,
+    PRNU_INVALID_ARG = 1,          /* null pointer, non-positive size, batch < 1            */
+    PRNU_PLANE_TOO_SMALL = 2,      /* H or W < 2^levels                      [S:118]        */
+    PRNU_DEPTH_EXCEEDS_FRAMES = 3, /* depth > m or depth < 1                 [S:189]        */
+    PRNU_BAD_PARAMETER = 4,        /* sigma0_sq <= 0, levels outside 1..6, window not in
+                                      {3,5,7,9}, exclusion_half < 0        [S:110]        */
+    PRNU_DIMENSION_MISMATCH = 5,   /*                                        [S:198, S:207] */
+    PRNU_EMPTY_ACCUMULATOR = 6,    /* reserved (finalize cannot inspect device data
+                                      synchronously; see prnu_fingerprint_finalize) [S:216] */
+    PRNU_CONSTANT_INPUT = 7,       /* reserved (see prnu_ncc)                [S:288]        */
+    PRNU_DEGENERATE_SURFACE = 8,   /* reserved (see prnu_pce)                [S:297]        */
+    PRNU_WORKSPACE_TOO_SMALL = 9,
+    PRNU_CUDA_ERROR = 10           /* a launch / cuFFT call failed; see prnu_last_error() */
+};
+
+/* Parameters of the denoiser F (P:150, P:259 cite the Mihcak wavelet filter
+ * without internals; S:109-117 and S:149-150 parameterise it; R-1..R-8).
+ *   F = 8-tap Daubechies DWT (4 vanishing moments), `levels` levels,
+ *       half-sample symmetric extension, subband length floor((N+7)/2);
+ *       every detail coefficient c becomes c * v/(v + sigma0_sq) with
+ *       v = max(0, min_w mean_{w x w}(c^2) - sigma0_sq) over `windows`
+ *       (mirror-extended windows, divided by w^2); the approximation passes
+ *       through; inverse DWT.  The residual W = I - F(I).           */
+typedef struct {
+    float sigma0_sq;   /* base noise variance, [0,255]^2 units; default 9.0      */
+    int levels;        /* decomposition depth 1..6; default 4                    */
+    int n_windows;     /* number of valid entries in `windows` (1..4); default 4 */
+    int windows[4];    /* odd window sizes from {3,5,7,9}; default {3,5,7,9}     */
+} prnu_denoise_params;
+
+/* Fill *p with the defaults above. */
+int prnu_default_params(prnu_denoise_params* p);
+
+/* ---------------------------------------------------------------------------
+ * a1  SDA grouping and averaging — P:124 ("g non-intersecting equal-sized
+ * subgroups ... each with d = m/g frames"), P:170-175 (I_i^SDA =
+ * sum_{j=(i-1)d+1}^{id} I_j / d).
+ *
+ * prnu_sda_groups: *n_sda_host = floor(m / depth) (the m mod depth
+ *   trailing frames are dropped).  PRNU_DEPTH_EXCEEDS_FRAMES if depth > m or
+ *   depth < 1.
+ * prnu_sda_average: frames u8 [m][H][W] -> sda_out fp32 [floor(m/depth)][H][W].
+ *   Group i averages frames [i*depth, (i+1)*depth).  Each output is the exact
+ *   integer sum divided by depth, rounded once to the nearest fp32 (R-11):
+ *   bit-exact.  depth == 1 widens u8 to fp32.  n_sda_host (optional, host)
+ *   receives the group count.
+ * ------------------------------------------------------------------------- */
+int prnu_sda_groups(int64_t m, int64_t depth, int64_t* n_sda_host);
+int prnu_sda_average(const uint8_t* frames, int64_t m, int H, int W, int64_t depth,
+                     float* sda_out, int64_t* n_sda_host, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * a2-a4  Noise residual W = I - F(I) — P:83 (W_k = I_k - F(I_k))
+ * (W^SDA = I^SDA - F(I^SDA)).
+ *
+ * planes fp32 (or u8 for the _u8 variant) [batch][H][W] -> W_out fp32
+ * [batch][H][W].  zero_mean != 0 additionally subtracts each row's mean, then
+ * each column's mean (used for query residuals before PCE, R-9).  The
+ * residual is computed in the noise domain, W = IDWT(0, c - F(c)) (equal to
+ * I - F(I) in exact arithmetic, R-10), in fp32; max |error| vs the fp64 oracle
+ * <= 1e-3 intensity units (BASELINE tolerance).
+ * Errors: PLANE_TOO_SMALL (H or W < 2^levels), BAD_PARAMETER,
+ * WORKSPACE_TOO_SMALL.
+ * ------------------------------------------------------------------------- */
+size_t prnu_residual_workspace_bytes(int batch, int H, int W, const prnu_denoise_params* p);
+int prnu_residual(const float* planes, int batch, int H, int W, const prnu_denoise_params* p,
+                  int zero_mean, float* W_out, void* ws, size_t ws_bytes, void* stream);
+int prnu_residual_u8(const uint8_t* planes, int batch, int H, int W, const prnu_denoise_params* p,
+                     int zero_mean, float* W_out, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * a5  MLE accumulation — Eq. (2) P:151-155 and its SDA form P:200-203:
+ * K = sum_i W_i I_i / sum_i I_i^2.
+ * sum_WI[p] += W[b][p] * I[b][p], sum_I2[p] += I[b][p]^2 for b = 0..batch-1 in
+ * ascending order, products and sums in fp64 (a product of two
+ * fp32 values is exact in fp64).  sum_WI / sum_I2 are fp64 [H][W], in-out;
+ * the caller zeroes them before the first contribution.
+ * ------------------------------------------------------------------------- */
+int prnu_fingerprint_accumulate(const float* W, const float* I, int batch, int H, int Wd,
+                                double* sum_WI, double* sum_I2, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * a6  Finalize — S:212-220: K = sum_WI / max(sum_I2, eps) element-wise, then
+ * (zero_mean != 0) the row/column zero-mean of S:135 computed in fp64
+ * (K - rowmean - colmean + totalmean, R-13); K_out fp32 [H][W].
+ * An all-zero accumulator yields K = 0 (EMPTY_ACCUMULATOR cannot be detected
+ * without a device->host sync; the host wrapper tracks contribution counts).
+ * ------------------------------------------------------------------------- */
+size_t prnu_finalize_workspace_bytes(int H, int W);
+int prnu_fingerprint_finalize(const double* sum_WI, const double* sum_I2, int H, int W, double eps,
+                              int zero_mean, float* K_out, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * a1-a6 fused  Fingerprint extraction — the three steps of P:58-60 ("frame
+ * averaging, denoising, and noise averaging") and S:221-228.
+ * frames u8 [m][H][W] (device) -> K_out fp32 [H][W], sum_WI/sum_I2 fp64
+ * [H][W] (outputs, zeroed by the call), n_sda_host = floor(m/depth).
+ * `batch` SDA frames are denoised per wave (1 <= batch); the result does not
+ * depend on it.  depth == 1 is the conventional pipeline and is bit-identical
+ * to prnu_residual + prnu_fingerprint_accumulate + prnu_fingerprint_finalize
+ * on the widened frames.
+ * ------------------------------------------------------------------------- */
+size_t prnu_extract_workspace_bytes(int H, int W, int batch, int64_t depth, const prnu_denoise_params* p);
+int prnu_extract_fingerprint(const uint8_t* frames, int64_t m, int H, int W, int64_t depth,
+                             const prnu_denoise_params* p, int batch, double eps, float* K_out,
+                             double* sum_WI, double* sum_I2, int64_t* n_sda_host, void* ws,
+                             size_t ws_bytes, void* stream);
+
+/* Same, with the frames in (preferably page-locked) HOST memory and K written
+ * to HOST memory: frames are streamed host->device in chunks of
+ * `batch * depth` frames through a double-buffered staging area inside `ws`,
+ * overlapped with the denoising of the previous chunk (copy stream + events
+ * created internally).  Synchronous: returns after K_out_host is written.
+ * sum_WI/sum_I2 are device buffers as above. */
+size_t prnu_extract_host_workspace_bytes(int H, int W, int batch, int64_t depth,
+                                         const prnu_denoise_params* p);
+int prnu_extract_fingerprint_host(const uint8_t* frames_host, int64_t m, int H, int W, int64_t depth,
+                                  const prnu_denoise_params* p, int batch, double eps,
+                                  float* K_out_host, double* sum_WI, double* sum_I2,
+                                  int64_t* n_sda_host, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * a7  NCC — P:93, P:259 name it; S:284-287 fixes it (R-16): the Pearson
+ * correlation over all pixels at shift (0,0),
+ * rho = sum (a-abar)(b-bbar) / sqrt(sum (a-abar)^2 sum (b-bbar)^2),
+ * two-pass, fp64 sums, fixed reduction order.  a, b fp32 [batch][H][W];
+ * ncc_out fp64 [batch] (device).  A constant input yields NaN (ConstantInput,
+ * S:288, is reported in-band because detection would need a sync).
+ * ------------------------------------------------------------------------- */
+size_t prnu_ncc_workspace_bytes(int batch, int H, int W);
+int prnu_ncc(const float* a, const float* b, int batch, int H, int W, double* ncc_out, void* ws,
+             size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * a8  PCE — P:259 ("PCE ... A preset threshold of 60 ... Values higher than
+ * this threshold"), formula S:293-301 / S:328-331 (R-17..R-19).
+ *
+ * prnu_pce_template: T[b] = K[b or 0] (.) (float)Iq[b] (R-18);
+ *   K fp32 [k_batch][H][W] with k_batch in {1, batch}, Iq u8 [batch][H][W].
+ * prnu_pce: for each pair b, C = circular cross-correlation of the
+ *   mean-removed residual[b] and template[b] (C[dy,dx] = sum R0[y,x]
+ *   T0[y-dy, x-dx], via cuFFT R2C/C2R, fp32; mean removal = zeroing the DC
+ *   bin), peak p* = argmax |C| (ties: smallest row-major index) or (0,0) if
+ *   aligned != 0; PCE = sign(C[p*]) C[p*]^2 / mean of C^2 outside the circular
+ *   (2e+1)^2 neighbourhood of p* (e = exclusion_half, default 5), energies in
+ *   fp64; zero background energy -> +-1e12.  Outputs (device,
+ *   [batch]): pce fp64, peak_y/peak_x int32 (the shift (dy,dx)), peak fp64
+ *   (C[p*] in the units of the definition above).  The decision is pce > 60
+ *   (strict).
+ * prnu_pce_plan_create: cuFFT plans for [batch][H][W] (no auto-allocation);
+ *   *ws_bytes receives the workspace prnu_pce needs.  *plan is opaque, freed
+ *   by prnu_pce_plan_destroy.
+ * ------------------------------------------------------------------------- */
+int prnu_pce_template(const float* K, int k_batch, const uint8_t* Iq, int batch, int H, int W,
+                      float* T_out, void* stream);
+int prnu_pce_plan_create(int H, int W, int batch, size_t* ws_bytes, void** plan);
+int prnu_pce(void* plan, const float* residual, const float* template_, int batch, int exclusion_half,
+             int aligned, double* pce, int* peak_y, int* peak_x, double* peak, void* ws, size_t ws_bytes,
+             void* stream);
+int prnu_pce_plan_destroy(void* plan);
+
+/* ---------------------------------------------------------------------------
+ * Diagnostics.
+ * prnu_last_error: thread-local text of the last failure ("" if none).
+ * prnu_kernel_launches: process-wide count of kernels this library has
+ *   launched (cuFFT's internal kernels excluded), for launch accounting.
+ * prnu_version: library version string.
+ * ------------------------------------------------------------------------- */
+const char* prnu_last_error(void);
+uint64_t prnu_kernel_launches(void);
+const char* prnu_version(void);
+
+/* Per-kernel timing (diagnostic, process-wide).  Between prnu_profile_begin()
+ * and prnu_profile_end() every kernel launch of this library is bracketed by a
+ * CUDA event pair recorded on the launching stream.  prnu_profile_end waits
+ * for those events, disables timing and reports, per kernel name (at most
+ * max_kernels entries; names is max_kernels * 64 bytes, NUL-terminated
+ * entries): total milliseconds and launch counts; *n_kernels = number of
+ * distinct names seen.  Names are "<kernel>_l<level>" for per-level kernels. */
+int prnu_profile_begin(void);
+int prnu_profile_end(int max_kernels, char* names, double* ms_total, int64_t* launches, int* n_kernels);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PRNU_H */

@@ -132,7 +132,10 @@ void oracle_idwt1d(const double* a, const double* d, long istride, int n, int N,
     oracle_filters(NULL, NULL, rl, rh);
     for (int t = 0; t < N; ++t) {
         double s = 0.0;
-        for (int k = 0; k < n; ++k) {
+        /* only k with 0 <= t+6-2k <= 7 contribute: k in [floor(t/2), floor((t+6)/2)] */
+        int k0 = t / 2, k1 = (t + 6) / 2;
+        if (k1 > n - 1) k1 = n - 1;
+        for (int k = k0; k <= k1; ++k) {
             int f = t + 6 - 2 * k;
             if (f < 0 || f > 7) continue;
             s += a[(long)k * istride] * rl[f] + d[(long)k * istride] * rh[f];
@@ -188,16 +191,23 @@ void oracle_idwt2d(const double* aa, const double* da, const double* ad, const d
    mirrored with e_n, always w^2 samples, divided by w^2.       */
 void oracle_box_mean_sq(const double* c, int nH, int nW, int w, double* out) {
     int r = w / 2;
+    /* mirrored indices e_n(i) for i in [-r, n+r), tabulated once */
+    int* ey = (int*)malloc(sizeof(int) * (nH + 2 * r));
+    int* ex = (int*)malloc(sizeof(int) * (nW + 2 * r));
+    for (int i = -r; i < nH + r; ++i) ey[i + r] = oracle_ext(i, nH);
+    for (int i = -r; i < nW + r; ++i) ex[i + r] = oracle_ext(i, nW);
     for (int y = 0; y < nH; ++y)
         for (int x = 0; x < nW; ++x) {
             double s = 0.0;
             for (int dy = -r; dy <= r; ++dy)
                 for (int dx = -r; dx <= r; ++dx) {
-                    double v = c[(long)oracle_ext(y + dy, nH) * nW + oracle_ext(x + dx, nW)];
+                    double v = c[(long)ey[y + dy + r] * nW + ex[x + dx + r]];
                     s += v * v;
                 }
             out[(long)y * nW + x] = s / ((double)w * (double)w);
         }
+    free(ey);
+    free(ex);
 }
 
 /* "each detail coefficient c is attenuated by the local Wiener

@@ -1,0 +1,391 @@
+"""paper_1909_04573_b200 — B200 (sm_100a) hot path of SDA-frame PRNU fingerprint
+extraction (Taspinar, Mohanty, Memon, arXiv 1909.04573).
+
+A thin ctypes binding over ``libprnu.so`` (C ABI in ``include/prnu.h``).  This
+module only marshals arguments: it checks tensors, allocates outputs and
+workspaces with torch (device memory + the current CUDA stream), and calls
+the C entry points of the same name.  Every step of the path runs in the
+library's CUDA kernels; there is no CPU fallback, and importing fails loudly
+if the library has not been built (``python __graft_entry__.py`` or
+``paper_1909_04573_b200._build.build()``).
+
+Citations: P:<n> = PAPER.md line, S:<n> = SPEC.md line, R-<n> = DESIGN.md reading.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+from dataclasses import dataclass, field
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libprnu.so")
+HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "prnu.h")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python __graft_entry__.py build` "
+                      "(nvcc, sm_100a).  There is no CPU fallback.")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+STATUS = {0: "OK", 1: "INVALID_ARG", 2: "PLANE_TOO_SMALL", 3: "DEPTH_EXCEEDS_FRAMES", 4: "BAD_PARAMETER",
+          5: "DIMENSION_MISMATCH", 6: "EMPTY_ACCUMULATOR", 7: "CONSTANT_INPUT", 8: "DEGENERATE_SURFACE",
+          9: "WORKSPACE_TOO_SMALL", 10: "CUDA_ERROR"}
+PCE_THRESHOLD = 60.0   # P:259, strict ">"
+
+
+class PrnuError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        msg = _lib.prnu_last_error().decode(errors="replace")
+        super().__init__(f"{where}: {STATUS.get(code, code)} ({msg})")
+        self.code = code
+
+
+class _Params(ctypes.Structure):
+    _fields_ = [("sigma0_sq", ctypes.c_float), ("levels", ctypes.c_int), ("n_windows", ctypes.c_int),
+                ("windows", ctypes.c_int * 4)]
+
+
+@dataclass
+class DenoiseParams:
+    """Parameters of F (R-1..R-8): sigma0^2 = 9, 4 levels, windows {3,5,7,9}."""
+    sigma0_sq: float = 9.0
+    levels: int = 4
+    windows: tuple = field(default=(3, 5, 7, 9))
+
+    def c(self) -> _Params:
+        p = _Params()
+        p.sigma0_sq = float(self.sigma0_sq)
+        p.levels = int(self.levels)
+        p.n_windows = len(self.windows)
+        for i, w in enumerate(self.windows[:4]):
+            p.windows[i] = int(w)
+        return p
+
+
+_vp = ctypes.c_void_p
+_i = ctypes.c_int
+_i64 = ctypes.c_int64
+_sz = ctypes.c_size_t
+_d = ctypes.c_double
+_P = ctypes.POINTER(_Params)
+
+
+def _sig(name, res, *args):
+    f = getattr(_lib, name)
+    f.restype = res
+    f.argtypes = list(args)
+    return f
+
+
+_sig("prnu_default_params", _i, _P)
+_sig("prnu_sda_groups", _i, _i64, _i64, ctypes.POINTER(_i64))
+_sig("prnu_sda_average", _i, _vp, _i64, _i, _i, _i64, _vp, ctypes.POINTER(_i64), _vp)
+_sig("prnu_residual_workspace_bytes", _sz, _i, _i, _i, _P)
+_sig("prnu_residual", _i, _vp, _i, _i, _i, _P, _i, _vp, _vp, _sz, _vp)
+_sig("prnu_residual_u8", _i, _vp, _i, _i, _i, _P, _i, _vp, _vp, _sz, _vp)
+_sig("prnu_fingerprint_accumulate", _i, _vp, _vp, _i, _i, _i, _vp, _vp, _vp)
+_sig("prnu_finalize_workspace_bytes", _sz, _i, _i)
+_sig("prnu_fingerprint_finalize", _i, _vp, _vp, _i, _i, _d, _i, _vp, _vp, _sz, _vp)
+_sig("prnu_extract_workspace_bytes", _sz, _i, _i, _i, _i64, _P)
+_sig("prnu_extract_fingerprint", _i, _vp, _i64, _i, _i, _i64, _P, _i, _d, _vp, _vp, _vp, ctypes.POINTER(_i64), _vp,
+     _sz, _vp)
+_sig("prnu_extract_host_workspace_bytes", _sz, _i, _i, _i, _i64, _P)
+_sig("prnu_extract_fingerprint_host", _i, _vp, _i64, _i, _i, _i64, _P, _i, _d, _vp, _vp, _vp,
+     ctypes.POINTER(_i64), _vp, _sz, _vp)
+_sig("prnu_ncc_workspace_bytes", _sz, _i, _i, _i)
+_sig("prnu_ncc", _i, _vp, _vp, _i, _i, _i, _vp, _vp, _sz, _vp)
+_sig("prnu_pce_template", _i, _vp, _i, _vp, _i, _i, _i, _vp, _vp)
+_sig("prnu_pce_plan_create", _i, _i, _i, _i, ctypes.POINTER(_sz), ctypes.POINTER(_vp))
+_sig("prnu_pce", _i, _vp, _vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _sz, _vp)
+_sig("prnu_pce_plan_destroy", _i, _vp)
+_sig("prnu_last_error", ctypes.c_char_p)
+_sig("prnu_kernel_launches", ctypes.c_uint64)
+_sig("prnu_version", ctypes.c_char_p)
+
+
+def _check(rc: int, where: str):
+    if rc != 0:
+        raise PrnuError(rc, where)
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t: torch.Tensor):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _dev(t: torch.Tensor, dtype, name: str, ndim=(2, 3)):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if t.dim() not in ndim:
+        raise ValueError(f"{name} must have {ndim} dims, got {t.dim()}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
+def _ws(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+
+
+def _params(p):
+    return (p or DenoiseParams()).c()
+
+
+def kernel_launches() -> int:
+    """Kernels this library has launched so far (process-wide; cuFFT excluded)."""
+    return int(_lib.prnu_kernel_launches())
+
+
+def version() -> str:
+    return _lib.prnu_version().decode()
+
+
+# ---------------------------------------------------------------- a1
+def sda_groups(m: int, depth: int) -> int:
+    """floor(m/depth) SDA frames; DEPTH_EXCEEDS_FRAMES if depth > m."""
+    n = _i64()
+    _check(_lib.prnu_sda_groups(m, depth, ctypes.byref(n)), "prnu_sda_groups")
+    return int(n.value)
+
+
+def sda_average(frames: torch.Tensor, depth: int) -> torch.Tensor:
+    """u8 [m,H,W] -> fp32 [floor(m/depth),H,W] SDA frames, bit-exact."""
+    _dev(frames, torch.uint8, "frames", (3,))
+    m, H, W = frames.shape
+    ns = sda_groups(m, depth)
+    out = torch.empty((ns, H, W), dtype=torch.float32, device=frames.device)
+    _check(_lib.prnu_sda_average(_ptr(frames), m, H, W, depth, _ptr(out), None, _stream()), "prnu_sda_average")
+    return out
+
+
+prnu_sda_average = sda_average
+
+
+# ---------------------------------------------------------------- a2-a4
+def residual(planes: torch.Tensor, params: DenoiseParams | None = None, zero_mean: bool = False,
+             out: torch.Tensor | None = None) -> torch.Tensor:
+    """W = I - F(I) for fp32 or u8 planes [b,H,W] (or [H,W])."""
+    squeeze = planes.dim() == 2
+    if squeeze:
+        planes = planes.unsqueeze(0)
+    if planes.dtype not in (torch.float32, torch.uint8):
+        raise TypeError("planes must be float32 or uint8")
+    _dev(planes, planes.dtype, "planes", (3,))
+    b, H, W = planes.shape
+    p = _params(params)
+    nbytes = _lib.prnu_residual_workspace_bytes(b, H, W, ctypes.byref(p))
+    if nbytes == 0:
+        _check(_lib.prnu_residual(_ptr(planes), b, H, W, ctypes.byref(p), 0, None, None, 0, None), "prnu_residual")
+    ws = _ws(nbytes, planes.device)
+    if out is None:
+        out = torch.empty((b, H, W), dtype=torch.float32, device=planes.device)
+    fn = _lib.prnu_residual if planes.dtype == torch.float32 else _lib.prnu_residual_u8
+    _check(fn(_ptr(planes), b, H, W, ctypes.byref(p), int(zero_mean), _ptr(out), _ptr(ws), nbytes, _stream()),
+           "prnu_residual")
+    return out[0] if squeeze else out
+
+
+prnu_residual = residual
+
+
+# ---------------------------------------------------------------- a5-a6
+def fingerprint_accumulate(W: torch.Tensor, I: torch.Tensor, sum_WI: torch.Tensor, sum_I2: torch.Tensor):
+    """sum_WI += W*I, sum_I2 += I^2 over the batch in order (Eq. 2)."""
+    if W.dim() == 2:
+        W, I = W.unsqueeze(0), I.unsqueeze(0)
+    _dev(W, torch.float32, "W", (3,))
+    _dev(I, torch.float32, "I", (3,))
+    _dev(sum_WI, torch.float64, "sum_WI", (2,))
+    _dev(sum_I2, torch.float64, "sum_I2", (2,))
+    b, H, Wd = W.shape
+    if I.shape != W.shape or sum_WI.shape != (H, Wd) or sum_I2.shape != (H, Wd):
+        raise ValueError("dimension mismatch")
+    _check(_lib.prnu_fingerprint_accumulate(_ptr(W), _ptr(I), b, H, Wd, _ptr(sum_WI), _ptr(sum_I2), _stream()),
+           "prnu_fingerprint_accumulate")
+
+
+prnu_fingerprint_accumulate = fingerprint_accumulate
+
+
+def fingerprint_finalize(sum_WI: torch.Tensor, sum_I2: torch.Tensor, eps: float = 1e-6,
+                         zero_mean: bool = True) -> torch.Tensor:
+    """K = sum_WI / max(sum_I2, eps), then row/column zero-mean."""
+    _dev(sum_WI, torch.float64, "sum_WI", (2,))
+    _dev(sum_I2, torch.float64, "sum_I2", (2,))
+    H, W = sum_WI.shape
+    nbytes = _lib.prnu_finalize_workspace_bytes(H, W)
+    ws = _ws(nbytes, sum_WI.device)
+    K = torch.empty((H, W), dtype=torch.float32, device=sum_WI.device)
+    _check(_lib.prnu_fingerprint_finalize(_ptr(sum_WI), _ptr(sum_I2), H, W, float(eps), int(zero_mean), _ptr(K),
+                                          _ptr(ws), nbytes, _stream()), "prnu_fingerprint_finalize")
+    return K
+
+
+prnu_fingerprint_finalize = fingerprint_finalize
+
+
+@dataclass
+class Fingerprint:
+    K: torch.Tensor        # fp32 [H,W], zero-meaned K_hat
+    sum_WI: torch.Tensor   # fp64 [H,W]
+    sum_I2: torch.Tensor   # fp64 [H,W]
+    n_sda: int             # denoise operations = floor(m/depth)
+    depth: int
+    frames: int
+
+
+class Extractor:
+    """Reusable fingerprint extractor for fixed (H, W, depth, batch): owns the
+    workspace and accumulators so repeated calls allocate nothing."""
+
+    def __init__(self, H: int, W: int, depth: int, batch: int = 16, params: DenoiseParams | None = None,
+                 device="cuda", eps: float = 1e-6, host: bool = False):
+        self.H, self.W, self.depth, self.batch, self.eps, self.host = H, W, depth, batch, eps, host
+        self.p = _params(params)
+        q = _lib.prnu_extract_host_workspace_bytes if host else _lib.prnu_extract_workspace_bytes
+        self.nbytes = q(H, W, batch, depth, ctypes.byref(self.p))
+        if self.nbytes == 0:
+            raise PrnuError(4, "prnu_extract_workspace_bytes (invalid H/W/batch/depth/params)")
+        self.ws = _ws(self.nbytes, device)
+        self.sum_WI = torch.empty((H, W), dtype=torch.float64, device=device)
+        self.sum_I2 = torch.empty((H, W), dtype=torch.float64, device=device)
+        self.K = (torch.empty((H, W), dtype=torch.float32, pin_memory=True) if host
+                  else torch.empty((H, W), dtype=torch.float32, device=device))
+
+    def __call__(self, frames: torch.Tensor) -> Fingerprint:
+        if frames.dtype != torch.uint8 or frames.dim() != 3 or not frames.is_contiguous():
+            raise TypeError("frames must be a contiguous uint8 [m,H,W] tensor")
+        m, H, W = frames.shape
+        if (H, W) != (self.H, self.W):
+            raise ValueError("frame size differs from the extractor's")
+        ns = _i64()
+        if self.host:
+            if frames.is_cuda:
+                raise TypeError("host extractor takes CPU (pinned) frames")
+            rc = _lib.prnu_extract_fingerprint_host(_ptr(frames), m, H, W, self.depth, ctypes.byref(self.p),
+                                                    self.batch, self.eps, _ptr(self.K), _ptr(self.sum_WI),
+                                                    _ptr(self.sum_I2), ctypes.byref(ns), _ptr(self.ws), self.nbytes,
+                                                    _stream())
+            _check(rc, "prnu_extract_fingerprint_host")
+        else:
+            _dev(frames, torch.uint8, "frames", (3,))
+            rc = _lib.prnu_extract_fingerprint(_ptr(frames), m, H, W, self.depth, ctypes.byref(self.p), self.batch,
+                                               self.eps, _ptr(self.K), _ptr(self.sum_WI), _ptr(self.sum_I2),
+                                               ctypes.byref(ns), _ptr(self.ws), self.nbytes, _stream())
+            _check(rc, "prnu_extract_fingerprint")
+        return Fingerprint(self.K, self.sum_WI, self.sum_I2, int(ns.value), self.depth, m)
+
+
+def extract_fingerprint(frames: torch.Tensor, depth: int, params: DenoiseParams | None = None, batch: int = 16,
+                        eps: float = 1e-6) -> Fingerprint:
+    """The three steps of P:58-60 (average, denoise, MLE) + finalize, on device frames."""
+    m, H, W = frames.shape
+    sda_groups(m, depth)
+    return Extractor(H, W, depth, batch, params, frames.device, eps)(frames)
+
+
+prnu_extract_fingerprint = extract_fingerprint
+
+
+# ---------------------------------------------------------------- a7-a8
+def ncc(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """Aligned Pearson correlation per plane (R-16), fp64 [batch] (or 0-dim)."""
+    squeeze = a.dim() == 2
+    if squeeze:
+        a, b = a.unsqueeze(0), b.unsqueeze(0)
+    _dev(a, torch.float32, "a", (3,))
+    _dev(b, torch.float32, "b", (3,))
+    if a.shape != b.shape:
+        raise ValueError("dimension mismatch")
+    n, H, W = a.shape
+    nbytes = _lib.prnu_ncc_workspace_bytes(n, H, W)
+    ws = _ws(nbytes, a.device)
+    out = torch.empty((n,), dtype=torch.float64, device=a.device)
+    _check(_lib.prnu_ncc(_ptr(a), _ptr(b), n, H, W, _ptr(out), _ptr(ws), nbytes, _stream()), "prnu_ncc")
+    return out[0] if squeeze else out
+
+
+prnu_ncc = ncc
+
+
+def pce_template(K: torch.Tensor, Iq: torch.Tensor) -> torch.Tensor:
+    """T = K (.) Iq (R-18); K fp32 [H,W] or [b,H,W], Iq u8 [b,H,W] or [H,W]."""
+    if Iq.dim() == 2:
+        Iq = Iq.unsqueeze(0)
+    Kb = K.unsqueeze(0) if K.dim() == 2 else K
+    _dev(Kb, torch.float32, "K", (3,))
+    _dev(Iq, torch.uint8, "Iq", (3,))
+    b, H, W = Iq.shape
+    T = torch.empty((b, H, W), dtype=torch.float32, device=Iq.device)
+    _check(_lib.prnu_pce_template(_ptr(Kb), Kb.shape[0], _ptr(Iq), b, H, W, _ptr(T), _stream()),
+           "prnu_pce_template")
+    return T
+
+
+@dataclass
+class PceResult:
+    pce: torch.Tensor     # fp64 [b]
+    peak_y: torch.Tensor  # int32 [b]
+    peak_x: torch.Tensor  # int32 [b]
+    peak: torch.Tensor    # fp64 [b]
+
+    def decision(self) -> torch.Tensor:
+        return self.pce > PCE_THRESHOLD   # strict
+
+
+class PcePlan:
+    """cuFFT plans + workspace for [batch][H][W] residual/template pairs."""
+
+    def __init__(self, H: int, W: int, batch: int = 1, device="cuda"):
+        self.H, self.W, self.batch = H, W, batch
+        nb = _sz()
+        h = _vp()
+        _check(_lib.prnu_pce_plan_create(H, W, batch, ctypes.byref(nb), ctypes.byref(h)), "prnu_pce_plan_create")
+        self._h = h
+        self.nbytes = int(nb.value)
+        self.ws = _ws(self.nbytes, device)
+        self.out = PceResult(torch.empty(batch, dtype=torch.float64, device=device),
+                             torch.empty(batch, dtype=torch.int32, device=device),
+                             torch.empty(batch, dtype=torch.int32, device=device),
+                             torch.empty(batch, dtype=torch.float64, device=device))
+
+    def __call__(self, R: torch.Tensor, T: torch.Tensor, exclusion_half: int = 5, aligned: bool = False) -> PceResult:
+        if R.dim() == 2:
+            R, T = R.unsqueeze(0), T.unsqueeze(0)
+        _dev(R, torch.float32, "residual", (3,))
+        _dev(T, torch.float32, "template", (3,))
+        if R.shape != (self.batch, self.H, self.W) or T.shape != R.shape:
+            raise ValueError("dimension mismatch with the plan")
+        o = self.out
+        _check(_lib.prnu_pce(self._h, _ptr(R), _ptr(T), self.batch, exclusion_half, int(aligned), _ptr(o.pce),
+                             _ptr(o.peak_y), _ptr(o.peak_x), _ptr(o.peak), _ptr(self.ws), self.nbytes, _stream()),
+               "prnu_pce")
+        return PceResult(o.pce.clone(), o.peak_y.clone(), o.peak_x.clone(), o.peak.clone())
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _lib.prnu_pce_plan_destroy(h)
+            self._h = None
+
+
+def pce(R: torch.Tensor, T: torch.Tensor, exclusion_half: int = 5, aligned: bool = False) -> PceResult:
+    b = 1 if R.dim() == 2 else R.shape[0]
+    return PcePlan(R.shape[-2], R.shape[-1], b, R.device)(R, T, exclusion_half, aligned)
+
+
+prnu_pce = pce
+
+
+def header_symbols() -> list[str]:
+    """Every function declared in include/prnu.h."""
+    txt = open(HEADER_PATH).read()
+    return sorted(set(re.findall(r"\b(prnu_[a-z0-9_]+)\s*\(", txt)))

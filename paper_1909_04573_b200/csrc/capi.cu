@@ -1,0 +1,464 @@
+// capi.cu — the extern "C" boundary of libprnu.so (declared in include/prnu.h).
+// Validation happens here, synchronously, before anything is launched; the
+// kernels live in sda.cu / wavelet.cu / mle.cu / pce.cu.
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+
+namespace prnu {
+
+// ---------------------------------------------------------------- state
+static thread_local std::string t_err;
+static std::atomic<uint64_t> g_launches{0};
+
+void set_error(const std::string& msg) { t_err = msg; }
+int fail(int code, const std::string& msg) {
+    t_err = msg;
+    return code;
+}
+void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+int check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(PRNU_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+    return PRNU_OK;
+}
+
+// ---------------------------------------------------------------- profiler
+struct ProfRec {
+    const char* name;
+    cudaEvent_t a, b;
+};
+static std::mutex g_prof_mu;
+static bool g_prof_on = false;
+static std::vector<ProfRec> g_prof;
+static std::vector<cudaEvent_t> g_ev_pool;
+
+static cudaEvent_t pool_event() {
+    if (!g_ev_pool.empty()) {
+        cudaEvent_t e = g_ev_pool.back();
+        g_ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+KTimer::KTimer(const char* name, cudaStream_t s) : slot(-1), st(s) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    if (!g_prof_on) return;
+    ProfRec r{name, pool_event(), pool_event()};
+    cudaEventRecord(r.a, s);
+    slot = (int)g_prof.size();
+    g_prof.push_back(r);
+}
+
+KTimer::~KTimer() {
+    if (slot < 0) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    if (slot < (int)g_prof.size()) cudaEventRecord(g_prof[slot].b, st);
+}
+
+int validate_params(const prnu_denoise_params* p, int H, int W, ShrinkParams* sp) {
+    if (!p) return fail(PRNU_INVALID_ARG, "params is NULL");
+    if (!(p->sigma0_sq > 0.0f) || !(p->sigma0_sq < 3.0e38f)) return fail(PRNU_BAD_PARAMETER, "sigma0_sq must be > 0");
+    if (p->levels < 1 || p->levels > kMaxLevels) return fail(PRNU_BAD_PARAMETER, "levels must be in 1..6");
+    if (p->n_windows < 1 || p->n_windows > 4) return fail(PRNU_BAD_PARAMETER, "n_windows must be in 1..4");
+    int mask = 0;
+    for (int i = 0; i < p->n_windows; ++i) {
+        int w = p->windows[i];
+        if (w != 3 && w != 5 && w != 7 && w != 9)
+            return fail(PRNU_BAD_PARAMETER, "windows must be odd sizes from {3,5,7,9}");
+        mask |= 1 << ((w - 3) / 2);
+    }
+    if (H < (1 << p->levels) || W < (1 << p->levels))
+        return fail(PRNU_PLANE_TOO_SMALL, "H and W must be >= 2^levels");
+    if (sp) {
+        sp->sigma0_sq = p->sigma0_sq;
+        sp->wmask = mask;
+    }
+    return PRNU_OK;
+}
+
+// kernels / launchers defined in the other translation units
+int launch_sda_average(const uint8_t* frames, long long n_groups, long long P, int d, float* out, cudaStream_t st);
+size_t pyramid_floats_per_frame(const Pyramid& p);
+template <typename TIn>
+int run_residual(const TIn* in, int nb, int H, int W, const Pyramid& p, const ShrinkParams& sp, float* W_out,
+                 float* ws_pyr, cudaStream_t st);
+template <typename TIn>
+int run_residual_accumulate(const TIn* in, const TIn* I, int nb, int H, int W, const Pyramid& p,
+                            const ShrinkParams& sp, double* num, double* den, float* ws_pyr, cudaStream_t st);
+int launch_accumulate(const float* W, const float* I, int batch, long long P, double* num, double* den,
+                      cudaStream_t st);
+size_t zm_workspace_bytes(int H, int W);
+int launch_finalize(const double* num, const double* den, int H, int W, double eps, int zero_mean, float* K,
+                    void* ws, cudaStream_t st);
+int launch_zero_mean_f32(float* Wp, int H, int W, void* ws, cudaStream_t st);
+size_t ncc_workspace_bytes(int batch);
+int launch_ncc(const float* a, const float* b, int batch, long long P, double* out, void* ws, cudaStream_t st);
+int launch_pce_template(const float* K, int k_batch, const uint8_t* Iq, int batch, long long P, float* T,
+                        cudaStream_t st);
+int pce_plan_create(int H, int W, int batch, size_t* ws_bytes, void** out);
+int pce_plan_destroy(void* plan);
+int pce_plan_dims(void* plan, int* H, int* W, int* batch, size_t* ws_bytes);
+int run_pce(void* plan, const float* R, const float* T, int excl, int aligned, double* pce, int* py, int* px,
+            double* peak, void* ws, cudaStream_t st);
+
+static size_t residual_ws(int batch, int H, int W, const Pyramid& pyr) {
+    return align_up(sizeof(float) * pyramid_floats_per_frame(pyr) * (size_t)batch, 256) + zm_workspace_bytes(H, W);
+}
+
+static size_t extract_ws(int H, int W, int batch, int64_t depth, const Pyramid& pyr) {
+    size_t s = align_up(sizeof(float) * pyramid_floats_per_frame(pyr) * (size_t)batch, 256);
+    if (depth > 1) s += align_up(sizeof(float) * (size_t)H * W * batch, 256);
+    s += zm_workspace_bytes(H, W);
+    return s;
+}
+
+static int check_dims(int H, int W) {
+    if (H <= 0 || W <= 0) return fail(PRNU_INVALID_ARG, "H and W must be positive");
+    if ((long long)H * W > (1LL << 31) - 1) return fail(PRNU_INVALID_ARG, "H*W must fit in int32");
+    return PRNU_OK;
+}
+
+// Shared by the device and host extraction entry points: process SDA groups
+// [g0, g0+nb) whose frames start at `frames` (device).
+static int extract_chunk(const uint8_t* frames, int64_t nb, int H, int W, int64_t depth, const Pyramid& pyr,
+                         const ShrinkParams& sp, double* num, double* den, char* ws, cudaStream_t st) {
+    float* pyr_ws = reinterpret_cast<float*>(ws);
+    size_t pyr_bytes = align_up(sizeof(float) * pyramid_floats_per_frame(pyr) * (size_t)nb, 256);
+    if (depth == 1)
+        return run_residual_accumulate<uint8_t>(frames, frames, (int)nb, H, W, pyr, sp, num, den, pyr_ws, st);
+    float* S = reinterpret_cast<float*>(ws + pyr_bytes);
+    int rc = launch_sda_average(frames, nb, (long long)H * W, (int)depth, S, st);
+    if (rc) return rc;
+    return run_residual_accumulate<float>(S, S, (int)nb, H, W, pyr, sp, num, den, pyr_ws, st);
+}
+
+template <typename TIn>
+static int residual_impl(const TIn* planes, int batch, int H, int W, const prnu_denoise_params* p, int zero_mean,
+                         float* W_out, void* ws, size_t ws_bytes, void* stream) {
+    int rc;
+    if (!planes || !W_out || !ws) return fail(PRNU_INVALID_ARG, "null pointer");
+    if (batch < 1) return fail(PRNU_INVALID_ARG, "batch must be >= 1");
+    if ((rc = check_dims(H, W))) return rc;
+    ShrinkParams sp;
+    if ((rc = validate_params(p, H, W, &sp))) return rc;
+    Pyramid pyr = make_pyramid(H, W, p->levels);
+    if (ws_bytes < residual_ws(batch, H, W, pyr)) return fail(PRNU_WORKSPACE_TOO_SMALL, "workspace too small");
+    cudaStream_t st = as_stream(stream);
+    float* pyr_ws = reinterpret_cast<float*>(ws);
+    if ((rc = run_residual<TIn>(planes, batch, H, W, pyr, sp, W_out, pyr_ws, st))) return rc;
+    if (zero_mean) {
+        char* zm = reinterpret_cast<char*>(ws) +
+                   align_up(sizeof(float) * pyramid_floats_per_frame(pyr) * (size_t)batch, 256);
+        for (int b = 0; b < batch; ++b)
+            if ((rc = launch_zero_mean_f32(W_out + (size_t)b * H * W, H, W, zm, st))) return rc;
+    }
+    return PRNU_OK;
+}
+
+}  // namespace prnu
+
+using namespace prnu;
+
+extern "C" {
+
+int prnu_default_params(prnu_denoise_params* p) {
+    if (!p) return fail(PRNU_INVALID_ARG, "params is NULL");
+    p->sigma0_sq = 9.0f;
+    p->levels = 4;
+    p->n_windows = 4;
+    p->windows[0] = 3;
+    p->windows[1] = 5;
+    p->windows[2] = 7;
+    p->windows[3] = 9;
+    return PRNU_OK;
+}
+
+int prnu_sda_groups(int64_t m, int64_t depth, int64_t* n_sda_host) {
+    if (m < 1) return fail(PRNU_INVALID_ARG, "m must be >= 1");
+    if (depth < 1 || depth > m) return fail(PRNU_DEPTH_EXCEEDS_FRAMES, "depth must be in 1..m");
+    if (n_sda_host) *n_sda_host = m / depth;
+    return PRNU_OK;
+}
+
+int prnu_sda_average(const uint8_t* frames, int64_t m, int H, int W, int64_t depth, float* sda_out,
+                     int64_t* n_sda_host, void* stream) {
+    int rc;
+    if (!frames || !sda_out) return fail(PRNU_INVALID_ARG, "null pointer");
+    if ((rc = check_dims(H, W))) return rc;
+    int64_t ns;
+    if ((rc = prnu_sda_groups(m, depth, &ns))) return rc;
+    if (depth > 65793) return fail(PRNU_BAD_PARAMETER, "depth > 65793 (sum would exceed 2^24)");
+    if (n_sda_host) *n_sda_host = ns;
+    return launch_sda_average(frames, ns, (long long)H * W, (int)depth, sda_out, as_stream(stream));
+}
+
+size_t prnu_residual_workspace_bytes(int batch, int H, int W, const prnu_denoise_params* p) {
+    if (batch < 1 || H <= 0 || W <= 0 || validate_params(p, H, W, nullptr)) return 0;
+    return residual_ws(batch, H, W, make_pyramid(H, W, p->levels));
+}
+
+int prnu_residual(const float* planes, int batch, int H, int W, const prnu_denoise_params* p, int zero_mean,
+                  float* W_out, void* ws, size_t ws_bytes, void* stream) {
+    return residual_impl<float>(planes, batch, H, W, p, zero_mean, W_out, ws, ws_bytes, stream);
+}
+
+int prnu_residual_u8(const uint8_t* planes, int batch, int H, int W, const prnu_denoise_params* p, int zero_mean,
+                     float* W_out, void* ws, size_t ws_bytes, void* stream) {
+    return residual_impl<uint8_t>(planes, batch, H, W, p, zero_mean, W_out, ws, ws_bytes, stream);
+}
+
+int prnu_fingerprint_accumulate(const float* W, const float* I, int batch, int H, int Wd, double* sum_WI,
+                                double* sum_I2, void* stream) {
+    int rc;
+    if (!W || !I || !sum_WI || !sum_I2) return fail(PRNU_INVALID_ARG, "null pointer");
+    if (batch < 1) return fail(PRNU_INVALID_ARG, "batch must be >= 1");
+    if ((rc = check_dims(H, Wd))) return rc;
+    return launch_accumulate(W, I, batch, (long long)H * Wd, sum_WI, sum_I2, as_stream(stream));
+}
+
+size_t prnu_finalize_workspace_bytes(int H, int W) {
+    if (H <= 0 || W <= 0) return 0;
+    return zm_workspace_bytes(H, W);
+}
+
+int prnu_fingerprint_finalize(const double* sum_WI, const double* sum_I2, int H, int W, double eps, int zero_mean,
+                              float* K_out, void* ws, size_t ws_bytes, void* stream) {
+    int rc;
+    if (!sum_WI || !sum_I2 || !K_out) return fail(PRNU_INVALID_ARG, "null pointer");
+    if ((rc = check_dims(H, W))) return rc;
+    if (!(eps > 0.0)) return fail(PRNU_BAD_PARAMETER, "eps must be > 0");
+    if (zero_mean && (!ws || ws_bytes < zm_workspace_bytes(H, W)))
+        return fail(PRNU_WORKSPACE_TOO_SMALL, "workspace too small");
+    return launch_finalize(sum_WI, sum_I2, H, W, eps, zero_mean, K_out, ws, as_stream(stream));
+}
+
+size_t prnu_extract_workspace_bytes(int H, int W, int batch, int64_t depth, const prnu_denoise_params* p) {
+    if (batch < 1 || depth < 1 || H <= 0 || W <= 0 || validate_params(p, H, W, nullptr)) return 0;
+    return extract_ws(H, W, batch, depth, make_pyramid(H, W, p->levels));
+}
+
+int prnu_extract_fingerprint(const uint8_t* frames, int64_t m, int H, int W, int64_t depth,
+                             const prnu_denoise_params* p, int batch, double eps, float* K_out, double* sum_WI,
+                             double* sum_I2, int64_t* n_sda_host, void* ws, size_t ws_bytes, void* stream) {
+    int rc;
+    if (!frames || !K_out || !sum_WI || !sum_I2 || !ws) return fail(PRNU_INVALID_ARG, "null pointer");
+    if (batch < 1) return fail(PRNU_INVALID_ARG, "batch must be >= 1");
+    if ((rc = check_dims(H, W))) return rc;
+    int64_t ns;
+    if ((rc = prnu_sda_groups(m, depth, &ns))) return rc;
+    if (depth > 65793) return fail(PRNU_BAD_PARAMETER, "depth > 65793");
+    if (!(eps > 0.0)) return fail(PRNU_BAD_PARAMETER, "eps must be > 0");
+    ShrinkParams sp;
+    if ((rc = validate_params(p, H, W, &sp))) return rc;
+    Pyramid pyr = make_pyramid(H, W, p->levels);
+    if (ws_bytes < extract_ws(H, W, batch, depth, pyr)) return fail(PRNU_WORKSPACE_TOO_SMALL, "workspace too small");
+    if (n_sda_host) *n_sda_host = ns;
+    cudaStream_t st = as_stream(stream);
+    const size_t P = (size_t)H * W;
+    cudaError_t e1 = cudaMemsetAsync(sum_WI, 0, sizeof(double) * P, st);
+    cudaError_t e2 = cudaMemsetAsync(sum_I2, 0, sizeof(double) * P, st);
+    if (e1 != cudaSuccess || e2 != cudaSuccess) return fail(PRNU_CUDA_ERROR, "cudaMemsetAsync failed");
+    char* wsb = reinterpret_cast<char*>(ws);
+    for (int64_t g0 = 0; g0 < ns; g0 += batch) {
+        int64_t nb = std::min<int64_t>(batch, ns - g0);
+        if ((rc = extract_chunk(frames + (size_t)g0 * depth * P, nb, H, W, depth, pyr, sp, sum_WI, sum_I2, wsb, st)))
+            return rc;
+    }
+    char* zm = wsb + extract_ws(H, W, batch, depth, pyr) - zm_workspace_bytes(H, W);
+    return launch_finalize(sum_WI, sum_I2, H, W, eps, 1, K_out, zm, st);
+}
+
+size_t prnu_extract_host_workspace_bytes(int H, int W, int batch, int64_t depth, const prnu_denoise_params* p) {
+    size_t base = prnu_extract_workspace_bytes(H, W, batch, depth, p);
+    if (!base) return 0;
+    size_t chunk = (size_t)batch * depth * H * W;
+    return base + 2 * align_up(chunk, 256) + align_up(sizeof(float) * (size_t)H * W, 256);
+}
+
+int prnu_extract_fingerprint_host(const uint8_t* frames_host, int64_t m, int H, int W, int64_t depth,
+                                  const prnu_denoise_params* p, int batch, double eps, float* K_out_host,
+                                  double* sum_WI, double* sum_I2, int64_t* n_sda_host, void* ws, size_t ws_bytes,
+                                  void* stream) {
+    int rc;
+    if (!frames_host || !K_out_host || !sum_WI || !sum_I2 || !ws) return fail(PRNU_INVALID_ARG, "null pointer");
+    if (batch < 1) return fail(PRNU_INVALID_ARG, "batch must be >= 1");
+    if ((rc = check_dims(H, W))) return rc;
+    int64_t ns;
+    if ((rc = prnu_sda_groups(m, depth, &ns))) return rc;
+    if (depth > 65793) return fail(PRNU_BAD_PARAMETER, "depth > 65793");
+    if (!(eps > 0.0)) return fail(PRNU_BAD_PARAMETER, "eps must be > 0");
+    ShrinkParams sp;
+    if ((rc = validate_params(p, H, W, &sp))) return rc;
+    if (ws_bytes < prnu_extract_host_workspace_bytes(H, W, batch, depth, p))
+        return fail(PRNU_WORKSPACE_TOO_SMALL, "workspace too small");
+    if (n_sda_host) *n_sda_host = ns;
+    Pyramid pyr = make_pyramid(H, W, p->levels);
+    const size_t P = (size_t)H * W;
+    const size_t base = extract_ws(H, W, batch, depth, pyr);
+    const size_t chunk = (size_t)batch * depth * P;
+    char* wsb = reinterpret_cast<char*>(ws);
+    uint8_t* stage[2] = {reinterpret_cast<uint8_t*>(wsb + base),
+                         reinterpret_cast<uint8_t*>(wsb + base + align_up(chunk, 256))};
+    float* Kdev = reinterpret_cast<float*>(wsb + base + 2 * align_up(chunk, 256));
+    char* zm = wsb + base - zm_workspace_bytes(H, W);
+    cudaStream_t st = as_stream(stream);
+    cudaStream_t cp = nullptr;
+    cudaEvent_t ready[2] = {nullptr, nullptr}, freed[2] = {nullptr, nullptr};
+    cudaError_t e = cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking);
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+        e = cudaEventCreateWithFlags(&ready[i], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&freed[i], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaMemsetAsync(sum_WI, 0, sizeof(double) * P, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(sum_I2, 0, sizeof(double) * P, st);
+    // the copy stream must not overwrite a staging buffer the compute stream still reads
+    if (e == cudaSuccess) e = cudaEventRecord(freed[0], st);
+    if (e == cudaSuccess) e = cudaEventRecord(freed[1], st);
+    rc = (e == cudaSuccess) ? PRNU_OK : fail(PRNU_CUDA_ERROR, std::string("setup: ") + cudaGetErrorString(e));
+    int64_t c = 0;
+    for (int64_t g0 = 0; g0 < ns && rc == PRNU_OK; g0 += batch, ++c) {
+        int64_t nb = std::min<int64_t>(batch, ns - g0);
+        int k = (int)(c & 1);
+        size_t bytes = (size_t)nb * depth * P;
+        e = cudaStreamWaitEvent(cp, freed[k], 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(stage[k], frames_host + (size_t)g0 * depth * P, bytes, cudaMemcpyHostToDevice, cp);
+        if (e == cudaSuccess) e = cudaEventRecord(ready[k], cp);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ready[k], 0);
+        if (e != cudaSuccess) {
+            rc = fail(PRNU_CUDA_ERROR, std::string("H2D staging: ") + cudaGetErrorString(e));
+            break;
+        }
+        rc = extract_chunk(stage[k], nb, H, W, depth, pyr, sp, sum_WI, sum_I2, wsb, st);
+        if (rc == PRNU_OK && (e = cudaEventRecord(freed[k], st)) != cudaSuccess)
+            rc = fail(PRNU_CUDA_ERROR, cudaGetErrorString(e));
+    }
+    if (rc == PRNU_OK) rc = launch_finalize(sum_WI, sum_I2, H, W, eps, 1, Kdev, zm, st);
+    if (rc == PRNU_OK) {
+        e = cudaMemcpyAsync(K_out_host, Kdev, sizeof(float) * P, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) rc = fail(PRNU_CUDA_ERROR, std::string("D2H K: ") + cudaGetErrorString(e));
+    } else {
+        cudaStreamSynchronize(st);
+    }
+    cudaStreamSynchronize(cp);
+    for (int i = 0; i < 2; ++i) {
+        if (ready[i]) cudaEventDestroy(ready[i]);
+        if (freed[i]) cudaEventDestroy(freed[i]);
+    }
+    if (cp) cudaStreamDestroy(cp);
+    return rc;
+}
+
+size_t prnu_ncc_workspace_bytes(int batch, int H, int W) {
+    if (batch < 1 || H <= 0 || W <= 0) return 0;
+    return ncc_workspace_bytes(batch);
+}
+
+int prnu_ncc(const float* a, const float* b, int batch, int H, int W, double* ncc_out, void* ws, size_t ws_bytes,
+             void* stream) {
+    int rc;
+    if (!a || !b || !ncc_out || !ws) return fail(PRNU_INVALID_ARG, "null pointer");
+    if (batch < 1 || batch > 65535) return fail(PRNU_INVALID_ARG, "batch must be in 1..65535");
+    if ((rc = check_dims(H, W))) return rc;
+    if (ws_bytes < ncc_workspace_bytes(batch)) return fail(PRNU_WORKSPACE_TOO_SMALL, "workspace too small");
+    return launch_ncc(a, b, batch, (long long)H * W, ncc_out, ws, as_stream(stream));
+}
+
+int prnu_pce_template(const float* K, int k_batch, const uint8_t* Iq, int batch, int H, int W, float* T_out,
+                      void* stream) {
+    int rc;
+    if (!K || !Iq || !T_out) return fail(PRNU_INVALID_ARG, "null pointer");
+    if (batch < 1 || batch > 65535) return fail(PRNU_INVALID_ARG, "batch must be in 1..65535");
+    if (k_batch != 1 && k_batch != batch) return fail(PRNU_DIMENSION_MISMATCH, "k_batch must be 1 or batch");
+    if ((rc = check_dims(H, W))) return rc;
+    return launch_pce_template(K, k_batch, Iq, batch, (long long)H * W, T_out, as_stream(stream));
+}
+
+int prnu_pce_plan_create(int H, int W, int batch, size_t* ws_bytes, void** plan) {
+    int rc;
+    if (!ws_bytes || !plan) return fail(PRNU_INVALID_ARG, "null pointer");
+    if (batch < 1 || batch > 65535) return fail(PRNU_INVALID_ARG, "batch must be in 1..65535");
+    if ((rc = check_dims(H, W))) return rc;
+    return pce_plan_create(H, W, batch, ws_bytes, plan);
+}
+
+int prnu_pce(void* plan, const float* residual, const float* template_, int batch, int exclusion_half, int aligned,
+             double* pce, int* peak_y, int* peak_x, double* peak, void* ws, size_t ws_bytes, void* stream) {
+    if (!plan || !residual || !template_ || !pce || !peak_y || !peak_x || !peak || !ws)
+        return fail(PRNU_INVALID_ARG, "null pointer");
+    int H, W, pb;
+    size_t need;
+    pce_plan_dims(plan, &H, &W, &pb, &need);
+    if (batch != pb) return fail(PRNU_DIMENSION_MISMATCH, "batch differs from the plan's batch");
+    if (exclusion_half < 0) return fail(PRNU_BAD_PARAMETER, "exclusion_half must be >= 0");
+    if (ws_bytes < need) return fail(PRNU_WORKSPACE_TOO_SMALL, "workspace too small");
+    return run_pce(plan, residual, template_, exclusion_half, aligned, pce, peak_y, peak_x, peak, ws,
+                   as_stream(stream));
+}
+
+int prnu_pce_plan_destroy(void* plan) { return pce_plan_destroy(plan); }
+
+int prnu_profile_begin(void) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (auto& r : g_prof) {
+        g_ev_pool.push_back(r.a);
+        g_ev_pool.push_back(r.b);
+    }
+    g_prof.clear();
+    g_prof_on = true;
+    return PRNU_OK;
+}
+
+int prnu_profile_end(int max_kernels, char* names, double* ms_total, int64_t* launches, int* n_kernels) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof_on = false;
+    std::vector<std::string> nm;
+    std::vector<double> ms;
+    std::vector<int64_t> cnt;
+    int rc = PRNU_OK;
+    for (auto& r : g_prof) {
+        float t = 0.f;
+        cudaError_t e = cudaEventSynchronize(r.b);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&t, r.a, r.b);
+        if (e != cudaSuccess) {
+            rc = fail(PRNU_CUDA_ERROR, std::string("profile: ") + cudaGetErrorString(e));
+            break;
+        }
+        size_t k = 0;
+        while (k < nm.size() && nm[k] != r.name) ++k;
+        if (k == nm.size()) {
+            nm.push_back(r.name);
+            ms.push_back(0.0);
+            cnt.push_back(0);
+        }
+        ms[k] += t;
+        cnt[k] += 1;
+    }
+    int n = (int)std::min<size_t>(nm.size(), (size_t)std::max(max_kernels, 0));
+    for (int k = 0; k < n; ++k) {
+        if (names) {
+            std::strncpy(names + 64 * k, nm[k].c_str(), 63);
+            names[64 * k + 63] = 0;
+        }
+        if (ms_total) ms_total[k] = ms[k];
+        if (launches) launches[k] = cnt[k];
+    }
+    if (n_kernels) *n_kernels = (int)nm.size();
+    return rc;
+}
+
+const char* prnu_last_error(void) { return t_err.c_str(); }
+
+uint64_t prnu_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
+
+const char* prnu_version(void) { return "prnu-b200 0.1.0 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,90 @@
+// common.cuh — shared device/host helpers of libprnu.so (sm_100a).
+// Product code: never includes or links anything under oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stddef.h>
+#include <atomic>
+#include <string>
+#include <algorithm>
+
+#include "../../include/prnu.h"
+
+namespace prnu {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+void count_launch(int n = 1);
+int check_launch(const char* what);   // PRNU_OK or PRNU_CUDA_ERROR (cudaGetLastError)
+
+// Optional per-kernel CUDA-event timing (prnu_profile_begin/end): when
+// enabled, a KTimer records an event pair around one launch on its stream.
+struct KTimer {
+    int slot;
+    cudaStream_t st;
+    KTimer(const char* name, cudaStream_t s);
+    ~KTimer();
+};
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// ---------------------------------------------------------------- wavelet
+// 8-tap Daubechies (4 vanishing moments) in minimum-phase order (R-2, R-5):
+// analysis   a[c] = sum_i H_[i] x[2c-6+i],   d[c] = sum_i G_[i] x[2c-6+i]
+// synthesis  x[2s+e] = sum_{m=0..3} a[s+m] H_[6-2m+e] + d[s+m] G_[6-2m+e]
+// with G_[i] = (-1)^i H_[7-i].  (Equivalent to the analysis/synthesis pair of
+// DESIGN.md §3 R-5; perfect reconstruction is tested on the GPU.)
+#define PRNU_H0 0.2303778133088965f
+#define PRNU_H1 0.7148465705529157f
+#define PRNU_H2 0.6308807679298589f
+#define PRNU_H3 (-0.027983769416859854f)
+#define PRNU_H4 (-0.18703481171909309f)
+#define PRNU_H5 0.030841381835560764f
+#define PRNU_H6 0.0328830116668852f
+#define PRNU_H7 (-0.010597401785069032f)
+
+__host__ __device__ __forceinline__ constexpr float wl_h(int i) {
+    return i == 0 ? PRNU_H0 : i == 1 ? PRNU_H1 : i == 2 ? PRNU_H2 : i == 3 ? PRNU_H3
+         : i == 4 ? PRNU_H4 : i == 5 ? PRNU_H5 : i == 6 ? PRNU_H6 : PRNU_H7;
+}
+__host__ __device__ __forceinline__ constexpr float wl_g(int i) {
+    return (i & 1) ? -wl_h(7 - i) : wl_h(7 - i);
+}
+
+// subband length of the expansive symmetric DWT: floor((N + 7) / 2)
+__host__ __device__ __forceinline__ int sub_len(int N) { return (N + 7) >> 1; }
+
+// half-sample symmetric index map e_N (R-4), valid for any integer i.
+__host__ __device__ __forceinline__ int mirror(int i, int N) {
+    int P2 = 2 * N;
+    int r = i % P2;
+    if (r < 0) r += P2;
+    return r < N ? r : P2 - 1 - r;
+}
+
+constexpr int kMaxLevels = 6;
+constexpr int kHalo = 4;  // max window radius (9x9)
+
+// Geometry of one decomposition: level 0 is the input plane.
+struct Pyramid {
+    int levels;
+    int nH[kMaxLevels + 1], nW[kMaxLevels + 1];
+    int pitch[kMaxLevels + 1];        // floats per row of each subband plane (level >= 1)
+    size_t plane[kMaxLevels + 1];     // floats per subband plane (nH * pitch)
+};
+
+Pyramid make_pyramid(int H, int W, int levels);
+
+// Shrink constants passed by value to kernels.
+struct ShrinkParams {
+    float sigma0_sq;
+    int wmask;            // bit k set <=> window (2k+3) enabled, k = 0..3
+};
+
+int validate_params(const prnu_denoise_params* p, int H, int W, ShrinkParams* sp);
+
+}  // namespace prnu

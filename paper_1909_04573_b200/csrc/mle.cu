@@ -1,0 +1,269 @@
+// mle.cu — a5 MLE accumulation, a6 finalize + zero-mean, a7 NCC (sm_100a).
+//
+// Every reduction has a fixed shape (grid size, per-thread stride, tree) that
+// depends only on the problem size, so results are bit-reproducible run to run
+// and independent of batching.  fp64 throughout the sums.
+#include "common.cuh"
+
+namespace prnu {
+
+// ---------------------------------------------------------------- a5
+// sum_WI[p] += W_b[p] I_b[p]; sum_I2[p] += I_b[p]^2, b ascending (Eq. 2).
+__global__ void __launch_bounds__(256) k_accumulate(const float* __restrict__ Wr, const float* __restrict__ I,
+                                                     int batch, long long P, double* __restrict__ num,
+                                                     double* __restrict__ den) {
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < P;
+         p += (long long)gridDim.x * blockDim.x) {
+        double n = num[p], d = den[p];
+        for (int b = 0; b < batch; ++b) {
+            double w = (double)Wr[(size_t)b * P + p];
+            double i = (double)I[(size_t)b * P + p];
+            n += w * i;
+            d += i * i;
+        }
+        num[p] = n;
+        den[p] = d;
+    }
+}
+
+int launch_accumulate(const float* W, const float* I, int batch, long long P, double* num, double* den,
+                      cudaStream_t st) {
+    long long blocks = std::min<long long>((P + 255) / 256, 148LL * 16);
+    {
+        KTimer kt("accumulate", st);
+        k_accumulate<<<(unsigned)blocks, 256, 0, st>>>(W, I, batch, P, num, den);
+    }
+    count_launch();
+    return check_launch("k_accumulate");
+}
+
+// ---------------------------------------------------------------- a6
+// Deterministic block sum of one double per thread (blockDim.x == 256).
+__device__ __forceinline__ double block_sum_256(double v, double* sh) {
+    sh[threadIdx.x] = v;
+    __syncthreads();
+#pragma unroll
+    for (int s = 128; s > 0; s >>= 1) {
+        if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+        __syncthreads();
+    }
+    double r = sh[0];
+    __syncthreads();
+    return r;
+}
+
+struct FinalizeSrc {   // K = sum_WI / max(sum_I2, eps)
+    const double* num;
+    const double* den;
+    double eps;
+    __device__ __forceinline__ double operator()(size_t i) const {
+        double d = den[i];
+        return num[i] / (d > eps ? d : eps);
+    }
+};
+struct FloatSrc {      // a residual plane to be zero-meaned
+    const float* w;
+    __device__ __forceinline__ double operator()(size_t i) const { return (double)w[i]; }
+};
+
+// S:135 step 1: materialise x (fp64) and each row's mean.
+template <class Src>
+__global__ void __launch_bounds__(256) k_zm_rows(Src src, int H, int W, double* __restrict__ X,
+                                                  double* __restrict__ rowmean) {
+    __shared__ double sh[256];
+    const int y = blockIdx.x;
+    double s = 0.0;
+    for (int x = threadIdx.x; x < W; x += 256) {
+        double v = src((size_t)y * W + x);
+        X[(size_t)y * W + x] = v;
+        s += v;
+    }
+    double t = block_sum_256(s, sh);
+    if (threadIdx.x == 0) rowmean[y] = t / W;
+}
+
+// S:135 step 2: column means of the row-centred values.
+__global__ void __launch_bounds__(256) k_zm_cols(const double* __restrict__ X, const double* __restrict__ rowmean,
+                                                  int H, int W, double* __restrict__ colmean) {
+    __shared__ double sh[8][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int x = blockIdx.x * 32 + tx;
+    double s = 0.0;
+    if (x < W)
+        for (int y = ty; y < H; y += 8) s += X[(size_t)y * W + x] - rowmean[y];
+    sh[ty][tx] = s;
+    __syncthreads();
+    if (ty == 0 && x < W) {
+        double t = 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) t += sh[k][tx];
+        colmean[x] = t / H;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_zm_apply(const double* __restrict__ X, const double* __restrict__ rowmean,
+                                                   const double* __restrict__ colmean, int H, int W,
+                                                   float* __restrict__ out) {
+    long long P = (long long)H * W;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P;
+         i += (long long)gridDim.x * blockDim.x) {
+        int y = (int)(i / W), x = (int)(i - (long long)y * W);
+        out[i] = (float)((X[i] - rowmean[y]) - colmean[x]);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_finalize_plain(FinalizeSrc src, long long P, float* __restrict__ out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P;
+         i += (long long)gridDim.x * blockDim.x)
+        out[i] = (float)src((size_t)i);
+}
+
+size_t zm_workspace_bytes(int H, int W) {
+    return align_up(sizeof(double) * (size_t)H * W, 256) + align_up(sizeof(double) * H, 256) +
+           align_up(sizeof(double) * W, 256);
+}
+
+template <class Src>
+static int run_zero_mean(Src src, int H, int W, float* out, void* ws, cudaStream_t st) {
+    char* p = reinterpret_cast<char*>(ws);
+    double* X = reinterpret_cast<double*>(p);
+    p += align_up(sizeof(double) * (size_t)H * W, 256);
+    double* rm = reinterpret_cast<double*>(p);
+    p += align_up(sizeof(double) * H, 256);
+    double* cm = reinterpret_cast<double*>(p);
+    {
+        KTimer kt("zm_rows", st);
+        k_zm_rows<Src><<<H, 256, 0, st>>>(src, H, W, X, rm);
+    }
+    {
+        KTimer kt("zm_cols", st);
+        k_zm_cols<<<(W + 31) / 32, 256, 0, st>>>(X, rm, H, W, cm);
+    }
+    long long P = (long long)H * W;
+    long long blocks = std::min<long long>((P + 255) / 256, 148LL * 16);
+    {
+        KTimer kt("zm_apply", st);
+        k_zm_apply<<<(unsigned)blocks, 256, 0, st>>>(X, rm, cm, H, W, out);
+    }
+    count_launch(3);
+    return check_launch("zero_mean");
+}
+
+int launch_finalize(const double* num, const double* den, int H, int W, double eps, int zero_mean, float* K,
+                    void* ws, cudaStream_t st) {
+    FinalizeSrc src{num, den, eps};
+    if (zero_mean) return run_zero_mean(src, H, W, K, ws, st);
+    long long P = (long long)H * W;
+    long long blocks = std::min<long long>((P + 255) / 256, 148LL * 16);
+    {
+        KTimer kt("finalize_plain", st);
+        k_finalize_plain<<<(unsigned)blocks, 256, 0, st>>>(src, P, K);
+    }
+    count_launch();
+    return check_launch("k_finalize_plain");
+}
+
+int launch_zero_mean_f32(float* Wp, int H, int W, void* ws, cudaStream_t st) {
+    return run_zero_mean(FloatSrc{Wp}, H, W, Wp, ws, st);
+}
+
+// ---------------------------------------------------------------- a7 NCC
+constexpr int NCC_BLOCKS = 296;   // 2 x 148 SMs; fixed so the sum order is fixed
+
+size_t ncc_workspace_bytes(int batch) {
+    return align_up(sizeof(double) * (size_t)batch * NCC_BLOCKS * 2, 256) +
+           align_up(sizeof(double) * (size_t)batch * NCC_BLOCKS * 3, 256);
+}
+
+__global__ void __launch_bounds__(256) k_ncc_pass1(const float* __restrict__ a, const float* __restrict__ b,
+                                                    long long P, double* __restrict__ part) {
+    __shared__ double sh[256];
+    const int pb = blockIdx.y;
+    const float* A = a + (size_t)pb * P;
+    const float* B = b + (size_t)pb * P;
+    double sa = 0.0, sb = 0.0;
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < P; i += 256LL * NCC_BLOCKS) {
+        sa += (double)A[i];
+        sb += (double)B[i];
+    }
+    sa = block_sum_256(sa, sh);
+    sb = block_sum_256(sb, sh);
+    if (threadIdx.x == 0) {
+        part[((size_t)pb * NCC_BLOCKS + blockIdx.x) * 2 + 0] = sa;
+        part[((size_t)pb * NCC_BLOCKS + blockIdx.x) * 2 + 1] = sb;
+    }
+}
+
+__device__ __forceinline__ void ncc_means(const double* part1, int pb, long long P, double* ma, double* mb,
+                                          double* sh) {
+    double sa = 0.0, sb = 0.0;
+    for (int k = threadIdx.x; k < NCC_BLOCKS; k += 256) {
+        sa += part1[((size_t)pb * NCC_BLOCKS + k) * 2 + 0];
+        sb += part1[((size_t)pb * NCC_BLOCKS + k) * 2 + 1];
+    }
+    *ma = block_sum_256(sa, sh) / (double)P;
+    *mb = block_sum_256(sb, sh) / (double)P;
+}
+
+__global__ void __launch_bounds__(256) k_ncc_pass2(const float* __restrict__ a, const float* __restrict__ b,
+                                                    long long P, const double* __restrict__ part1,
+                                                    double* __restrict__ part2) {
+    __shared__ double sh[256];
+    const int pb = blockIdx.y;
+    double ma, mb;
+    ncc_means(part1, pb, P, &ma, &mb, sh);
+    const float* A = a + (size_t)pb * P;
+    const float* B = b + (size_t)pb * P;
+    double sab = 0.0, saa = 0.0, sbb = 0.0;
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < P; i += 256LL * NCC_BLOCKS) {
+        double da = (double)A[i] - ma, db = (double)B[i] - mb;
+        sab += da * db;
+        saa += da * da;
+        sbb += db * db;
+    }
+    sab = block_sum_256(sab, sh);
+    saa = block_sum_256(saa, sh);
+    sbb = block_sum_256(sbb, sh);
+    if (threadIdx.x == 0) {
+        double* o = part2 + ((size_t)pb * NCC_BLOCKS + blockIdx.x) * 3;
+        o[0] = sab;
+        o[1] = saa;
+        o[2] = sbb;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_ncc_final(const double* __restrict__ part2, double* __restrict__ out) {
+    __shared__ double sh[256];
+    const int pb = blockIdx.x;
+    double s[3] = {0.0, 0.0, 0.0};
+    for (int k = threadIdx.x; k < NCC_BLOCKS; k += 256)
+        for (int j = 0; j < 3; ++j) s[j] += part2[((size_t)pb * NCC_BLOCKS + k) * 3 + j];
+    double sab = block_sum_256(s[0], sh);
+    double saa = block_sum_256(s[1], sh);
+    double sbb = block_sum_256(s[2], sh);
+    if (threadIdx.x == 0) out[pb] = sab / sqrt(saa * sbb);   // NaN for a constant input
+}
+
+int launch_ncc(const float* a, const float* b, int batch, long long P, double* out, void* ws, cudaStream_t st) {
+    char* p = reinterpret_cast<char*>(ws);
+    double* part1 = reinterpret_cast<double*>(p);
+    p += align_up(sizeof(double) * (size_t)batch * NCC_BLOCKS * 2, 256);
+    double* part2 = reinterpret_cast<double*>(p);
+    dim3 grid(NCC_BLOCKS, batch);
+    {
+        KTimer kt("ncc_pass1", st);
+        k_ncc_pass1<<<grid, 256, 0, st>>>(a, b, P, part1);
+    }
+    {
+        KTimer kt("ncc_pass2", st);
+        k_ncc_pass2<<<grid, 256, 0, st>>>(a, b, P, part1, part2);
+    }
+    {
+        KTimer kt("ncc_final", st);
+        k_ncc_final<<<batch, 256, 0, st>>>(part2, out);
+    }
+    count_launch(3);
+    return check_launch("ncc");
+}
+
+}  // namespace prnu

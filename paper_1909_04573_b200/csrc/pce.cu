@@ -1,0 +1,284 @@
+// pce.cu — a8: PCE of residual/template pairs.
+//
+// C = IFFT2( FFT2(R) . conj(FFT2(T)) ) with the DC bin zeroed (= correlation of
+// the mean-removed inputs), cuFFT R2C/C2R in fp32 (BASELINE: cuFFT only here).
+// Peak search and energies are deterministic block reductions in fp64.
+#include <cufft.h>
+
+#include "common.cuh"
+
+namespace prnu {
+
+constexpr int PCE_BLOCKS = 148;   // partial blocks per pair (fixed => fixed sum order)
+constexpr double PCE_CAP = 1e12;
+
+struct PcePlan {
+    int H, W, batch;
+    cufftHandle r2c, c2r;
+    size_t work;       // bytes of cuFFT work area
+    size_t ws_bytes;   // total workspace prnu_pce needs
+};
+
+static size_t spectrum_elems(int H, int W) { return (size_t)H * (W / 2 + 1); }
+
+// ---------------------------------------------------------------- template
+__global__ void __launch_bounds__(256) k_pce_template(const float* __restrict__ K, int k_batch,
+                                                       const uint8_t* __restrict__ Iq, long long P,
+                                                       float* __restrict__ T) {
+    const int b = blockIdx.y;
+    const float* Kb = K + (size_t)(k_batch == 1 ? 0 : b) * P;
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < P; i += 256LL * gridDim.x)
+        T[(size_t)b * P + i] = Kb[i] * (float)Iq[(size_t)b * P + i];
+}
+
+int launch_pce_template(const float* K, int k_batch, const uint8_t* Iq, int batch, long long P, float* T,
+                        cudaStream_t st) {
+    unsigned blocks = (unsigned)std::min<long long>((P + 255) / 256, 148LL * 4);
+    {
+        KTimer kt("pce_template", st);
+        k_pce_template<<<dim3(blocks, batch), 256, 0, st>>>(K, k_batch, Iq, P, T);
+    }
+    count_launch();
+    return check_launch("k_pce_template");
+}
+
+// ---------------------------------------------------------------- spectra
+__global__ void __launch_bounds__(256) k_conj_mul(cufftComplex* __restrict__ R, const cufftComplex* __restrict__ T,
+                                                   long long n_per, int batch) {
+    long long n = n_per * batch;
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += 256LL * gridDim.x) {
+        cufftComplex r = R[i], t = T[i];
+        cufftComplex o;
+        o.x = r.x * t.x + r.y * t.y;       // r * conj(t)
+        o.y = r.y * t.x - r.x * t.y;
+        if (i % n_per == 0) o.x = o.y = 0.f;   // DC bin: mean removal of both inputs
+        R[i] = o;
+    }
+}
+
+// ---------------------------------------------------------------- reductions
+struct PeakE {
+    float a;      // |C| of the best candidate
+    int idx;      // its linear index (-1 = none)
+    double e;     // partial energy
+};
+
+__device__ __forceinline__ bool better(float a1, int i1, float a2, int i2) {
+    // larger |C| wins; ties -> smaller index; idx -1 always loses
+    if (i2 < 0) return i1 >= 0;
+    if (i1 < 0) return false;
+    return a1 > a2 || (a1 == a2 && i1 < i2);
+}
+
+__device__ void block_reduce_peak(float& a, int& idx, double& e) {
+    __shared__ float sa[256];
+    __shared__ int si[256];
+    __shared__ double se[256];
+    sa[threadIdx.x] = a;
+    si[threadIdx.x] = idx;
+    se[threadIdx.x] = e;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+            int o = threadIdx.x + s;
+            if (better(sa[o], si[o], sa[threadIdx.x], si[threadIdx.x])) {
+                sa[threadIdx.x] = sa[o];
+                si[threadIdx.x] = si[o];
+            }
+            se[threadIdx.x] += se[o];
+        }
+        __syncthreads();
+    }
+    a = sa[0];
+    idx = si[0];
+    e = se[0];
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_pce_partial(const float* __restrict__ C, long long P, PeakE* __restrict__ part) {
+    const int b = blockIdx.y;
+    const float* Cb = C + (size_t)b * P;
+    float best = -1.f;
+    int bi = -1;
+    double e = 0.0;
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < P; i += 256LL * PCE_BLOCKS) {
+        float c = Cb[i];
+        float a = fabsf(c);
+        if (a > best) {   // strict: keeps the first (smallest) index of this thread's sequence
+            best = a;
+            bi = (int)i;
+        }
+        e += (double)c * (double)c;
+    }
+    block_reduce_peak(best, bi, e);
+    if (threadIdx.x == 0) part[(size_t)b * PCE_BLOCKS + blockIdx.x] = PeakE{best, bi, e};
+}
+
+__global__ void __launch_bounds__(256) k_pce_final(const float* __restrict__ C, const PeakE* __restrict__ part,
+                                                    int H, int W, int excl, int aligned, double scale,
+                                                    double* __restrict__ pce, int* __restrict__ py,
+                                                    int* __restrict__ px, double* __restrict__ peak) {
+    const int b = blockIdx.x;
+    const long long P = (long long)H * W;
+    const float* Cb = C + (size_t)b * P;
+    float best = -1.f;
+    int bi = -1;
+    double e = 0.0;
+    for (int k = threadIdx.x; k < PCE_BLOCKS; k += 256) {
+        PeakE q = part[(size_t)b * PCE_BLOCKS + k];
+        if (better(q.a, q.idx, best, bi)) {
+            best = q.a;
+            bi = q.idx;
+        }
+        e += q.e;
+    }
+    block_reduce_peak(best, bi, e);
+    int p = aligned ? 0 : bi;
+    int y = p / W, x = p - (p / W) * W;
+    // circular (2e+1)^2 neighbourhood, distinct positions only (first min(H,2e+1) rows/cols)
+    const int nr = min(H, 2 * excl + 1), nc = min(W, 2 * excl + 1);
+    double en = 0.0;
+    for (int k = threadIdx.x; k < nr * nc; k += 256) {
+        int r = k / nc, c = k - r * nc;
+        int yy = ((y - excl + r) % H + H) % H;
+        int xx = ((x - excl + c) % W + W) % W;
+        double v = (double)Cb[(size_t)yy * W + xx];
+        en += v * v;
+    }
+    __shared__ double sh[256];
+    sh[threadIdx.x] = en;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        double v = (double)Cb[p];
+        double n_out = (double)(P - (long long)nr * nc);
+        double r;
+        double bg = n_out > 0 ? (e - sh[0]) / n_out : 0.0;
+        if (!(n_out > 0) || !(bg > 0.0)) r = (v >= 0.0) ? PCE_CAP : -PCE_CAP;
+        else r = (v >= 0.0 ? 1.0 : -1.0) * v * v / bg;   // scale-invariant ratio
+        pce[b] = r;
+        py[b] = y;
+        px[b] = x;
+        peak[b] = v * scale;
+    }
+}
+
+// ---------------------------------------------------------------- host
+static const char* cufft_str(cufftResult r) {
+    switch (r) {
+        case CUFFT_SUCCESS: return "CUFFT_SUCCESS";
+        case CUFFT_INVALID_PLAN: return "CUFFT_INVALID_PLAN";
+        case CUFFT_ALLOC_FAILED: return "CUFFT_ALLOC_FAILED";
+        case CUFFT_INVALID_VALUE: return "CUFFT_INVALID_VALUE";
+        case CUFFT_INTERNAL_ERROR: return "CUFFT_INTERNAL_ERROR";
+        case CUFFT_EXEC_FAILED: return "CUFFT_EXEC_FAILED";
+        case CUFFT_SETUP_FAILED: return "CUFFT_SETUP_FAILED";
+        case CUFFT_INVALID_SIZE: return "CUFFT_INVALID_SIZE";
+        default: return "cufft error";
+    }
+}
+
+int pce_plan_create(int H, int W, int batch, size_t* ws_bytes, void** out) {
+    PcePlan* p = new PcePlan{};
+    p->H = H;
+    p->W = W;
+    p->batch = batch;
+    int n[2] = {H, W};
+    size_t w1 = 0, w2 = 0;
+    cufftResult r;
+    if ((r = cufftCreate(&p->r2c)) || (r = cufftCreate(&p->c2r))) {
+        delete p;
+        return fail(PRNU_CUDA_ERROR, std::string("cufftCreate: ") + cufft_str(r));
+    }
+    cufftSetAutoAllocation(p->r2c, 0);
+    cufftSetAutoAllocation(p->c2r, 0);
+    int nf = W / 2 + 1;
+    int inembed_r[2] = {H, W}, onembed_c[2] = {H, nf};
+    r = cufftMakePlanMany(p->r2c, 2, n, inembed_r, 1, H * W, onembed_c, 1, H * nf, CUFFT_R2C, batch, &w1);
+    if (r == CUFFT_SUCCESS)
+        r = cufftMakePlanMany(p->c2r, 2, n, onembed_c, 1, H * nf, inembed_r, 1, H * W, CUFFT_C2R, batch, &w2);
+    if (r != CUFFT_SUCCESS) {
+        cufftDestroy(p->r2c);
+        cufftDestroy(p->c2r);
+        delete p;
+        return fail(PRNU_CUDA_ERROR, std::string("cufftMakePlanMany: ") + cufft_str(r));
+    }
+    p->work = std::max(w1, w2);
+    size_t spec = sizeof(cufftComplex) * spectrum_elems(H, W) * batch;
+    p->ws_bytes = align_up(p->work, 256) + 2 * align_up(spec, 256) +
+                  align_up(sizeof(float) * (size_t)H * W * batch, 256) +
+                  align_up(sizeof(PeakE) * (size_t)PCE_BLOCKS * batch, 256);
+    *ws_bytes = p->ws_bytes;
+    *out = p;
+    return PRNU_OK;
+}
+
+int pce_plan_destroy(void* plan) {
+    PcePlan* p = reinterpret_cast<PcePlan*>(plan);
+    if (!p) return PRNU_OK;
+    cufftDestroy(p->r2c);
+    cufftDestroy(p->c2r);
+    delete p;
+    return PRNU_OK;
+}
+
+int pce_plan_dims(void* plan, int* H, int* W, int* batch, size_t* ws_bytes) {
+    PcePlan* p = reinterpret_cast<PcePlan*>(plan);
+    *H = p->H;
+    *W = p->W;
+    *batch = p->batch;
+    *ws_bytes = p->ws_bytes;
+    return PRNU_OK;
+}
+
+int run_pce(void* plan, const float* R, const float* T, int excl, int aligned, double* pce, int* py, int* px,
+            double* peak, void* ws, cudaStream_t st) {
+    PcePlan* p = reinterpret_cast<PcePlan*>(plan);
+    const int H = p->H, W = p->W, batch = p->batch;
+    char* c = reinterpret_cast<char*>(ws);
+    void* work = c;
+    c += align_up(p->work, 256);
+    size_t spec = sizeof(cufftComplex) * spectrum_elems(H, W) * batch;
+    cufftComplex* Rf = reinterpret_cast<cufftComplex*>(c);
+    c += align_up(spec, 256);
+    cufftComplex* Tf = reinterpret_cast<cufftComplex*>(c);
+    c += align_up(spec, 256);
+    float* Cs = reinterpret_cast<float*>(c);
+    c += align_up(sizeof(float) * (size_t)H * W * batch, 256);
+    PeakE* part = reinterpret_cast<PeakE*>(c);
+
+    cufftResult r;
+    if ((r = cufftSetStream(p->r2c, st)) || (r = cufftSetStream(p->c2r, st)) || (r = cufftSetWorkArea(p->r2c, work)) ||
+        (r = cufftSetWorkArea(p->c2r, work)))
+        return fail(PRNU_CUDA_ERROR, std::string("cufft setup: ") + cufft_str(r));
+    if ((r = cufftExecR2C(p->r2c, const_cast<float*>(R), Rf)))
+        return fail(PRNU_CUDA_ERROR, std::string("cufftExecR2C: ") + cufft_str(r));
+    if ((r = cufftExecR2C(p->r2c, const_cast<float*>(T), Tf)))
+        return fail(PRNU_CUDA_ERROR, std::string("cufftExecR2C: ") + cufft_str(r));
+    long long n_per = (long long)spectrum_elems(H, W);
+    unsigned blocks = (unsigned)std::min<long long>((n_per * batch + 255) / 256, 148LL * 8);
+    {
+        KTimer kt("pce_conj_mul", st);
+        k_conj_mul<<<blocks, 256, 0, st>>>(Rf, Tf, n_per, batch);
+    }
+    count_launch();
+    if (int rc = check_launch("k_conj_mul")) return rc;
+    if ((r = cufftExecC2R(p->c2r, Rf, Cs)))
+        return fail(PRNU_CUDA_ERROR, std::string("cufftExecC2R: ") + cufft_str(r));
+    long long P = (long long)H * W;
+    {
+        KTimer kt("pce_partial", st);
+        k_pce_partial<<<dim3(PCE_BLOCKS, batch), 256, 0, st>>>(Cs, P, part);
+    }
+    {
+        KTimer kt("pce_final", st);
+        k_pce_final<<<batch, 256, 0, st>>>(Cs, part, H, W, excl, aligned, 1.0 / (double)P, pce, py, px, peak);
+    }
+    count_launch(2);
+    return check_launch("pce reductions");
+}
+
+}  // namespace prnu

@@ -1,0 +1,110 @@
+// sda.cu — a1: SDA averaging.
+//
+// S_i[p] = RN_fp32( sum_{j = i d}^{(i+1) d - 1} u8_j[p] / d ).
+// The sum is an exact uint32 (max 255 * d < 2^24 for d <= 65793, so the
+// int -> float conversion is exact too) and the division is one IEEE
+// correctly-rounded fp32 divide (__fdiv_rn; never a reciprocal multiply,
+// R-11).  Each thread owns 16 consecutive pixels (one 16-byte load per
+// frame), loops over the d frames of its group with 8 loads in flight, and
+// writes four float4.  HBM-bound: (d + 4) bytes per output pixel.
+#include "common.cuh"
+
+namespace prnu {
+
+constexpr int SDA_VEC = 16;
+
+// Packed accumulation: each 32-bit word holds two 16-bit partial sums (bytes
+// 0,2 and bytes 1,3 of a 4-pixel word), exact for up to 257 frames; every 256
+// frames the packed sums are flushed into 32-bit per-pixel totals.
+__device__ __forceinline__ void sda_add_packed(const uint4& v, uint32_t (&pe)[4], uint32_t (&po)[4]) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        pe[q] += w[q] & 0x00ff00ffu;
+        po[q] += (w[q] >> 8) & 0x00ff00ffu;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_sda_average_vec(const uint4* __restrict__ frames, long long P16, int d,
+                                                          float4* __restrict__ out) {
+    const int g = blockIdx.y;   // SDA group
+    const float fd = (float)d;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P16;
+         i += (long long)gridDim.x * blockDim.x) {
+        const uint4* src = frames + (size_t)g * d * P16 + i;
+        uint32_t s[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) s[k] = 0;
+        for (int j0 = 0; j0 < d; j0 += 256) {
+            const int j1 = min(d, j0 + 256);
+            uint32_t pe[4] = {0, 0, 0, 0}, po[4] = {0, 0, 0, 0};
+            int j = j0;
+            for (; j + 8 <= j1; j += 8) {
+                uint4 v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = __ldcs(src + (size_t)(j + u) * P16);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) sda_add_packed(v[u], pe, po);
+            }
+            for (; j < j1; ++j) sda_add_packed(__ldcs(src + (size_t)j * P16), pe, po);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {   // pixel 4q+0 = low half of pe, 4q+2 = high half, etc.
+                s[4 * q + 0] += pe[q] & 0xffffu;
+                s[4 * q + 2] += pe[q] >> 16;
+                s[4 * q + 1] += po[q] & 0xffffu;
+                s[4 * q + 3] += po[q] >> 16;
+            }
+        }
+        float4* dst = out + ((size_t)g * P16 + i) * 4;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            float4 o;
+            o.x = __fdiv_rn((float)s[4 * q + 0], fd);
+            o.y = __fdiv_rn((float)s[4 * q + 1], fd);
+            o.z = __fdiv_rn((float)s[4 * q + 2], fd);
+            o.w = __fdiv_rn((float)s[4 * q + 3], fd);
+            dst[q] = o;   // plain store: the SDA frame is re-read by the denoiser (keep in L2)
+        }
+    }
+}
+
+// Generic path (P not a multiple of 16 or unaligned): one pixel per thread.
+__global__ void __launch_bounds__(256) k_sda_average_scalar(const uint8_t* __restrict__ frames, long long P, int d,
+                                                             float* __restrict__ out) {
+    const int g = blockIdx.y;
+    const float fd = (float)d;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P;
+         i += (long long)gridDim.x * blockDim.x) {
+        const uint8_t* src = frames + (size_t)g * d * P + i;
+        uint32_t s = 0;
+        for (int j = 0; j < d; ++j) s += src[(size_t)j * P];
+        out[(size_t)g * P + i] = __fdiv_rn((float)s, fd);
+    }
+}
+
+int launch_sda_average(const uint8_t* frames, long long n_groups, long long P, int d, float* out,
+                       cudaStream_t st) {
+    if (n_groups <= 0) return PRNU_OK;
+    const bool vec = (P % SDA_VEC == 0) && ((uintptr_t)frames % 16 == 0) && ((uintptr_t)out % 16 == 0);
+    for (long long g0 = 0; g0 < n_groups; g0 += 65535) {
+        int ng = (int)std::min<long long>(65535, n_groups - g0);
+        KTimer kt("sda_average", st);
+        if (vec) {
+            long long P16 = P / SDA_VEC;
+            long long blocks = std::min<long long>((P16 + 255) / 256, 148LL * 8);
+            dim3 grid((unsigned)blocks, ng);
+            k_sda_average_vec<<<grid, 256, 0, st>>>(reinterpret_cast<const uint4*>(frames + g0 * d * P), P16, d,
+                                                    reinterpret_cast<float4*>(out + g0 * P));
+        } else {
+            long long blocks = std::min<long long>((P + 255) / 256, 148LL * 8);
+            dim3 grid((unsigned)blocks, ng);
+            k_sda_average_scalar<<<grid, 256, 0, st>>>(frames + g0 * d * P, P, d, out + g0 * P);
+        }
+        count_launch();
+        int rc = check_launch("k_sda_average");
+        if (rc) return rc;
+    }
+    return PRNU_OK;
+}
+
+}  // namespace prnu

@@ -1,0 +1,69 @@
+"""The C-ABI library loads and exports every symbol include/prnu.h declares;
+host-side validation and workspace queries work without a GPU (no compute)."""
+import ctypes
+
+import pytest
+
+import paper_1909_04573_b200 as prnu
+
+
+def test_library_exports_every_header_symbol():
+    syms = prnu.header_symbols()
+    assert len(syms) >= 20
+    lib = ctypes.CDLL(prnu.LIB_PATH)
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+
+
+def test_library_is_sm100a():
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", prnu.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_default_params_and_version():
+    p = prnu._Params()
+    assert prnu._lib.prnu_default_params(ctypes.byref(p)) == 0
+    assert abs(p.sigma0_sq - 9.0) < 1e-7 and p.levels == 4 and p.n_windows == 4
+    assert list(p.windows) == [3, 5, 7, 9]
+    assert "sm_100a" in prnu.version()
+
+
+def test_sda_groups_host():
+    # P:436 counts via the library's host-side planner
+    assert [prnu.sda_groups(1200, d) for d in (1, 5, 10, 30, 50, 200, 1200)] == [1200, 240, 120, 40, 24, 6, 1]
+    with pytest.raises(prnu.PrnuError) as e:
+        prnu.sda_groups(10, 11)
+    assert e.value.code == 3
+
+
+def test_validation_is_synchronous_and_precedes_launch():
+    p = prnu.DenoiseParams().c()
+    L = prnu._lib
+    # null pointers -> INVALID_ARG
+    assert L.prnu_residual(None, 1, 64, 64, ctypes.byref(p), 0, None, None, 0, None) == 1
+    # plane too small
+    dummy = ctypes.c_void_p(1 << 20)
+    assert L.prnu_residual(dummy, 1, 15, 64, ctypes.byref(p), 0, dummy, dummy, 1 << 30, None) == 2
+    # bad parameter
+    bad = prnu.DenoiseParams(windows=(4,)).c()
+    assert L.prnu_residual(dummy, 1, 64, 64, ctypes.byref(bad), 0, dummy, dummy, 1 << 30, None) == 4
+    bad = prnu.DenoiseParams(sigma0_sq=0.0).c()
+    assert L.prnu_residual(dummy, 1, 64, 64, ctypes.byref(bad), 0, dummy, dummy, 1 << 30, None) == 4
+    # workspace too small
+    assert L.prnu_residual(dummy, 1, 64, 64, ctypes.byref(p), 0, dummy, dummy, 16, None) == 9
+    # depth exceeds frames
+    assert L.prnu_sda_average(dummy, 10, 8, 8, 11, dummy, None, None) == 3
+    assert "depth" in L.prnu_last_error().decode()
+
+
+def test_workspace_queries():
+    p = prnu.DenoiseParams().c()
+    L = prnu._lib
+    a = L.prnu_residual_workspace_bytes(1, 1080, 1920, ctypes.byref(p))
+    b = L.prnu_residual_workspace_bytes(8, 1080, 1920, ctypes.byref(p))
+    assert a > 1080 * 1920 * 4 and b > 7 * (a - L.prnu_finalize_workspace_bytes(1080, 1920))
+    assert L.prnu_extract_workspace_bytes(1080, 1920, 16, 50, ctypes.byref(p)) > \
+        L.prnu_extract_workspace_bytes(1080, 1920, 16, 1, ctypes.byref(p))
+    assert L.prnu_residual_workspace_bytes(1, 8, 8, ctypes.byref(p)) == 0   # 8 < 2^4

@@ -1,0 +1,274 @@
+"""GPU <-> oracle parity through the C ABI (libprnu.so), on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star):
+  SDA mean        bit-exact
+  residual W      max |dW| <= 1e-3 intensity units
+  fingerprint K   max |dK| * sqrt(sum_I2 / n_sda) <= 1e-3 intensity units (R-14)
+  NCC             |d| <= 1e-5
+  PCE             relative <= 1e-3 (tie rule R-19)
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+W_TOL = 1e-3
+K_TOL = 1e-3
+NCC_TOL = 1e-5
+PCE_RTOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def prnu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1909_04573_b200 as m
+    return m
+
+
+def _rand_frames(m, H, W, seed, lo=0, hi=256):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    return torch.randint(lo, hi, (m, H, W), generator=g, dtype=torch.uint8)
+
+
+def _textured(b, H, W, seed):
+    """fp32 planes with structure on every scale + noise, in [0, 255]."""
+    g = np.random.default_rng(seed)
+    y, x = np.mgrid[0:H, 0:W]
+    out = []
+    for i in range(b):
+        f = 128 + 50 * np.sin(2 * np.pi * (x / g.uniform(5, 40) + y / g.uniform(5, 40)))
+        f += 20 * np.cos(2 * np.pi * y / g.uniform(3, 9)) + g.normal(0, 4, (H, W))
+        out.append(np.clip(f, 0, 255))
+    return np.stack(out).astype(np.float32)
+
+
+def k_metric(K_gpu, K_ref, den, n_sda):
+    """R-14: error of the implied PRNU term K I in intensity units."""
+    d = np.abs(K_gpu.astype(np.float64) - K_ref)
+    return float((d * np.sqrt(den / n_sda)).max()), float(255 * d.max())
+
+
+# ---------------------------------------------------------------- a1
+@pytest.mark.parametrize("m,H,W,d", [(16, 64, 64, 4), (16, 64, 64, 1), (10, 33, 47, 3), (300, 17, 16, 300),
+                                     (7, 5, 3, 2), (600, 24, 40, 257), (1, 1, 1, 1)])
+def test_sda_average_bit_exact(prnu, m, H, W, d):
+    fr = _rand_frames(m, H, W, m * 7 + d)
+    got = prnu.sda_average(fr.cuda(), d).cpu().numpy()
+    ref = oracle.sda_average(fr.numpy(), d)
+    assert got.shape == ref.shape
+    np.testing.assert_array_equal(got.view(np.uint32), ref.view(np.uint32))
+
+
+def test_sda_average_extremes_bit_exact(prnu):
+    """All-255 and alternating extremes at the largest config depth (3600)."""
+    d = 3600
+    fr = torch.full((d, 4, 16), 255, dtype=torch.uint8)
+    fr[::2, :, ::3] = 0
+    fr[::7, 1, :] = 1
+    got = prnu.sda_average(fr.cuda(), d).cpu().numpy()
+    np.testing.assert_array_equal(got.view(np.uint32), oracle.sda_average(fr.numpy(), d).view(np.uint32))
+
+
+# ---------------------------------------------------------------- a2-a4
+@pytest.mark.parametrize("b,H,W", [(1, 64, 64), (3, 37, 53), (2, 135, 240), (1, 16, 16), (2, 100, 333),
+                                   (1, 270, 480)])
+def test_residual_matches_oracle(prnu, b, H, W):
+    I = _textured(b, H, W, H * W + b)
+    got = prnu.residual(torch.from_numpy(I).cuda()).cpu().numpy()
+    for i in range(b):
+        ref = oracle.residual(I[i])
+        err = np.abs(got[i] - ref).max()
+        assert err <= W_TOL, (i, err)
+
+
+@pytest.mark.parametrize("levels,windows,s0", [(1, (3,), 9.0), (2, (5, 9), 4.0), (3, (3, 5, 7, 9), 25.0),
+                                               (5, (7,), 9.0), (6, (3, 9), 1.0)])
+def test_residual_params_match_oracle(prnu, levels, windows, s0):
+    I = _textured(1, 96, 130, levels)[0]
+    p = prnu.DenoiseParams(sigma0_sq=s0, levels=levels, windows=windows)
+    got = prnu.residual(torch.from_numpy(I).cuda(), p).cpu().numpy()
+    ref = oracle.residual(I, sigma0_sq=s0, windows=windows, levels=levels)
+    assert np.abs(got - ref).max() <= W_TOL
+
+
+def test_residual_u8_and_zero_mean(prnu):
+    fr = _rand_frames(2, 70, 90, 11, 30, 220)
+    got = prnu.residual(fr.cuda(), zero_mean=True).cpu().numpy()
+    for i in range(2):
+        ref = oracle.residual(fr[i].numpy().astype(np.float32), zero_mean=True)
+        assert np.abs(got[i] - ref).max() <= W_TOL
+        assert np.abs(got[i].astype(np.float64).mean(axis=0)).max() < 1e-4
+        assert np.abs(got[i].astype(np.float64).mean(axis=1)).max() < 1e-4
+
+
+def test_residual_invariants(prnu):
+    c = torch.full((2, 64, 96), 128.0, device="cuda")
+    assert prnu.residual(c).abs().max().item() < 1e-4             # S:120 constant -> 0
+    I = torch.from_numpy(np.round(_textured(1, 64, 96, 5))).cuda()
+    d = prnu.residual(I + 10.0) - prnu.residual(I)               # S:130 offset invariance
+    assert d.abs().max().item() < 1e-3
+    with pytest.raises(prnu.PrnuError) as e:
+        prnu.residual(torch.zeros((1, 15, 64), device="cuda"))
+    assert e.value.code == 2
+
+
+def test_residual_deterministic_and_batch_independent(prnu):
+    I = torch.from_numpy(_textured(4, 80, 120, 9)).cuda()
+    a = prnu.residual(I)
+    b = prnu.residual(I)
+    c = torch.cat([prnu.residual(I[i:i + 1]) for i in range(4)])
+    assert torch.equal(a, b) and torch.equal(a, c)
+
+
+# ---------------------------------------------------------------- a5-a6
+def test_accumulate_finalize_match_oracle(prnu):
+    H, W = 40, 56
+    g = np.random.default_rng(0)
+    Ws = g.normal(0, 2, (5, H, W)).astype(np.float32)
+    Is = g.uniform(0, 255, (5, H, W)).astype(np.float32)
+    Is[:, 0, 0] = 0.0   # eps floor
+    num = torch.zeros((H, W), dtype=torch.float64, device="cuda")
+    den = torch.zeros_like(num)
+    prnu.fingerprint_accumulate(torch.from_numpy(Ws).cuda(), torch.from_numpy(Is).cuda(), num, den)
+    rn, rd = np.zeros((H, W)), np.zeros((H, W))
+    for i in range(5):
+        oracle.mle_accumulate(Ws[i].astype(np.float64), Is[i], rn, rd)
+    # fp32 inputs: products exact in fp64, same ascending order -> bit-identical
+    assert np.array_equal(num.cpu().numpy(), rn) and np.array_equal(den.cpu().numpy(), rd)
+    for zm in (False, True):
+        K = prnu.fingerprint_finalize(num, den, zero_mean=zm).cpu().numpy()
+        Kr = oracle.finalize(rn, rd, zero_mean=zm)
+        assert np.abs(K - Kr).max() <= 1e-6 * max(1.0, np.abs(Kr).max())
+    K = prnu.fingerprint_finalize(num, den).cpu().numpy().astype(np.float64)
+    assert np.abs(K.mean(axis=0)).max() < 1e-6 and np.abs(K.mean(axis=1)).max() < 1e-6
+
+
+@pytest.mark.parametrize("depth,batch", [(4, 1), (4, 3), (1, 16), (1, 5), (16, 1), (3, 2)])
+def test_extract_config1_matches_oracle(prnu, depth, batch):
+    """BASELINE config 1: 16 frames 64x64, d = 4 (and d = 1, 16, 3 with a dropped frame)."""
+    v = synth.video("shift", 16, 64, 64, seed=0)
+    fp = prnu.extract_fingerprint(v.frames.cuda(), depth, batch=batch)
+    K, num, den, ns = oracle.extract_fingerprint(v.frames.numpy(), depth)
+    assert fp.n_sda == ns == 16 // depth
+    np.testing.assert_array_equal(fp.sum_I2.cpu().numpy(), den)     # DEN is exact on both sides
+    prim, sec = k_metric(fp.K.cpu().numpy(), K, den, ns)
+    assert prim <= K_TOL, (prim, sec)
+    ncc_true = prnu.ncc(fp.K, v.K.cuda()).item()
+    assert abs(ncc_true - oracle.ncc(K, v.K.numpy())) <= NCC_TOL
+    assert ncc_true > 0.5 and abs(prnu.ncc(fp.K, v.K_other.cuda()).item()) < 0.1
+
+
+def test_extract_depth1_bit_identical_to_conventional(prnu):
+    """S:227 / S:241 / P:344: the d = 1 pipeline equals residual + accumulate + finalize."""
+    v = synth.video("drift", 12, 72, 136, seed=4)
+    fr = v.frames.cuda()
+    fp = prnu.extract_fingerprint(fr, 1, batch=5)
+    I = fr.float()
+    Wr = prnu.residual(I)
+    num = torch.zeros((72, 136), dtype=torch.float64, device="cuda")
+    den = torch.zeros_like(num)
+    prnu.fingerprint_accumulate(Wr, I, num, den)
+    K = prnu.fingerprint_finalize(num, den)
+    assert torch.equal(fp.sum_WI, num) and torch.equal(fp.sum_I2, den) and torch.equal(fp.K, K)
+
+
+def test_extract_deterministic_across_batches(prnu):
+    v = synth.video("drift", 40, 64, 128, seed=2)
+    fr = v.frames.cuda()
+    ref = prnu.extract_fingerprint(fr, 2, batch=20).K.clone()
+    for b in (1, 7, 20, 64):
+        assert torch.equal(prnu.extract_fingerprint(fr, 2, batch=b).K, ref)
+
+
+def test_extract_host_matches_device(prnu):
+    v = synth.video("drift", 30, 64, 96, seed=8)
+    dev = prnu.extract_fingerprint(v.frames.cuda(), 3, batch=4).K.cpu()
+    ex = prnu.Extractor(64, 96, 3, batch=4, host=True)
+    host = ex(v.frames.pin_memory()).K.clone()
+    assert torch.equal(dev, host)
+
+
+# ---------------------------------------------------------------- a7-a8
+def test_ncc_matches_oracle(prnu):
+    g = np.random.default_rng(3)
+    a = g.normal(0.3, 1, (3, 123, 77)).astype(np.float32)
+    b = (0.2 * a + g.normal(0, 1, a.shape)).astype(np.float32)
+    got = prnu.ncc(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()).cpu().numpy()
+    for i in range(3):
+        assert abs(got[i] - oracle.ncc(a[i], b[i])) <= NCC_TOL
+    x = torch.from_numpy(a[0]).cuda()
+    assert abs(prnu.ncc(x, x).item() - 1) < 1e-12
+    assert abs(prnu.ncc(x, -3 * x + 1).item() + 1) < 1e-12
+    assert np.isnan(prnu.ncc(torch.ones_like(x), x).item())
+
+
+def _pce_check(prnu, R, T, excl=5):
+    res = prnu.pce(torch.from_numpy(R).cuda(), torch.from_numpy(T).cuda(), excl)
+    res_al = prnu.pce(torch.from_numpy(R).cuda(), torch.from_numpy(T).cuda(), excl, aligned=True)
+    for i in range(R.shape[0]):
+        C = oracle.correlation_surface(R[i], T[i])
+        p_al = oracle.match.pce_from_surface(C, excl, peak=(0, 0))[0]
+        assert abs(res_al.pce[i].item() - p_al) <= PCE_RTOL * abs(p_al)
+        gy, gx = res.peak_y[i].item(), res.peak_x[i].item()
+        p_ref, peak_ref, v_ref = oracle.match.pce_from_surface(C, excl)
+        if (gy, gx) != peak_ref:
+            # R-19: only acceptable when the oracle's top two |C| nearly tie
+            top = np.sort(np.abs(C).ravel())[-2:]
+            assert (top[1] - top[0]) / top[1] < 1e-4, ((gy, gx), peak_ref)
+            p_ref = oracle.match.pce_from_surface(C, excl, peak=(gy, gx))[0]
+        assert abs(res.pce[i].item() - p_ref) <= PCE_RTOL * abs(p_ref)
+        assert abs(res.peak[i].item() - C[gy, gx]) <= 1e-3 * np.abs(C).max()
+
+
+def test_pce_matches_oracle_shifted(prnu):
+    g = np.random.default_rng(5)
+    T = g.normal(0, 1, (3, 96, 160)).astype(np.float32)
+    R = np.stack([np.roll(T[i], (i * 7, i * 13 + 1), axis=(0, 1)) + g.normal(0, 3, T[i].shape)
+                  for i in range(3)]).astype(np.float32)
+    _pce_check(prnu, R, T)
+    res = prnu.pce(torch.from_numpy(R).cuda(), torch.from_numpy(T).cuda())
+    assert [(res.peak_y[i].item(), res.peak_x[i].item()) for i in range(3)] == [(0, 1), (7, 14), (14, 27)]
+
+
+def test_pce_matches_oracle_null(prnu):
+    g = np.random.default_rng(6)
+    R = g.normal(0, 1, (4, 64, 80)).astype(np.float32)
+    T = g.normal(0, 1, (4, 64, 80)).astype(np.float32)
+    _pce_check(prnu, R, T)
+    _pce_check(prnu, R[:1, :10, :9].copy(), T[:1, :10, :9].copy(), excl=5)   # neighbourhood wraps
+
+
+def test_camera_identification_small(prnu):
+    """Config-4 shape at small scale: 4 cameras, K_hat (.) I_q templates, PCE matrix;
+    diagonal > 60 > off-diagonal (directional) and parity of every entry."""
+    H, W, n = 128, 192, 4
+    fps, queries, qres = [], [], []
+    for c in range(n):
+        v = synth.video("drift", 61, H, W, seed=1, camera=c, sigma_n=2.0)
+        fps.append(prnu.extract_fingerprint(v.frames[:60].cuda(), 6).K)
+        queries.append(v.frames[60])
+    Iq = torch.stack(queries).cuda()
+    Rq = prnu.residual(Iq, zero_mean=True)
+    M = np.zeros((n, n))
+    for c in range(n):
+        T = prnu.pce_template(fps[c], Iq)
+        res = prnu.pce(Rq, T)
+        M[:, c] = res.pce.cpu().numpy()
+        for q in range(n):
+            Rr = oracle.residual(queries[q].numpy().astype(np.float32), zero_mean=True)
+            Tr = oracle.pce_template(fps[c].cpu().numpy(), queries[q].numpy())
+            ref = oracle.pce(Rr, Tr)[0]
+            assert abs(M[q, c] - ref) <= PCE_RTOL * abs(ref) + 1e-6
+    assert np.all(np.diag(M) > 60)
+    assert np.all(M[~np.eye(n, dtype=bool)] < 60)
+
+
+def test_launch_counter_advances(prnu):
+    before = prnu.kernel_launches()
+    prnu.residual(torch.zeros((1, 64, 64), device="cuda"))
+    assert prnu.kernel_launches() - before == 8   # 4 analysis + 4 synthesis
