@@ -182,8 +182,9 @@ def residual(planes: torch.Tensor, params: DenoiseParams | None = None, zero_mea
     b, H, W = planes.shape
     p = _params(params)
     nbytes = _lib.prnu_residual_workspace_bytes(b, H, W, ctypes.byref(p))
-    if nbytes == 0:
-        _check(_lib.prnu_residual(_ptr(planes), b, H, W, ctypes.byref(p), 0, None, None, 0, None), "prnu_residual")
+    if nbytes == 0:   # invalid size/params: let the library name the error
+        _check(_lib.prnu_residual(_ptr(planes), b, H, W, ctypes.byref(p), 0, _ptr(planes), _ptr(planes), 0, None),
+               "prnu_residual")
     ws = _ws(nbytes, planes.device)
     if out is None:
         out = torch.empty((b, H, W), dtype=torch.float32, device=planes.device)
