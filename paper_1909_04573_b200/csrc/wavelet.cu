@@ -75,10 +75,27 @@ __global__ void __launch_bounds__(256) k_analysis_shrink(AnalysisArgs a) {
     }
     __syncthreads();
 
-    // ---- load the mirrored input tile
-    for (int e = tid; e < AIN * AIN; e += nthr) {
-        int r = e / AIN, c = e - r * AIN;
-        s_in[r * AIN_P + c] = (float)in[(size_t)s_iy[r] * a.in_pitch + s_ix[c]];
+    // ---- load the mirrored input tile: every thread issues all its loads
+    // before the first shared-memory store, so they are in flight together.
+    {
+        constexpr int PER = (AIN * AIN + 255) / 256;
+        float v[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            int e = tid + 256 * k;
+            if (e < AIN * AIN) {
+                int r = e / AIN, c = e - r * AIN;
+                v[k] = (float)__ldg(in + (size_t)s_iy[r] * a.in_pitch + s_ix[c]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            int e = tid + 256 * k;
+            if (e < AIN * AIN) {
+                int r = e / AIN, c = e - r * AIN;
+                s_in[r * AIN_P + c] = v[k];
+            }
+        }
     }
     __syncthreads();
 
@@ -229,21 +246,45 @@ struct SynthArgs {
 
 // Reconstruct the ST_Y x ST_X output tile at (ty0, tx0) of frame b into
 // s_out[ST_Y][SO_P] (shared).  All threads participate; ends with a barrier.
-__device__ __forceinline__ void synth_tile(const SynthArgs& a, int b, int ty0, int tx0, float* smem) {
+constexpr int S_LOAD_PER = (4 * SC_Y * SC_X + 255) / 256;
+
+// Issue the loads of frame b's coefficient tile into registers (no smem write).
+__device__ __forceinline__ void synth_fetch(const SynthArgs& a, int b, int ty0, int tx0, float (&v)[S_LOAD_PER]) {
+    const int ky0 = ty0 >> 1, kx0 = tx0 >> 1;
+    const size_t boff = (size_t)b * a.c_bstride;
+#pragma unroll
+    for (int k = 0; k < S_LOAD_PER; ++k) {
+        int e = threadIdx.x + 256 * k;
+        v[k] = 0.0f;
+        if (e < 4 * SC_Y * SC_X) {
+            int p = e / (SC_Y * SC_X);
+            int rem = e - p * (SC_Y * SC_X);
+            int r = rem / SC_X, c = rem - r * SC_X;
+            int gy = min(ky0 + r, a.nH - 1), gx = min(kx0 + c, a.nW - 1);
+            const float* src = p == 0 ? a.A : p == 1 ? a.d0 : p == 2 ? a.d1 : a.d2;
+            if (src) v[k] = __ldg(src + boff + (size_t)gy * a.c_pitch + gx);
+        }
+    }
+}
+
+__device__ __forceinline__ void synth_commit(const float (&v)[S_LOAD_PER], float* smem) {
+#pragma unroll
+    for (int k = 0; k < S_LOAD_PER; ++k) {
+        int e = threadIdx.x + 256 * k;
+        if (e < 4 * SC_Y * SC_X) {
+            int p = e / (SC_Y * SC_X);
+            int rem = e - p * (SC_Y * SC_X);
+            int r = rem / SC_X, c = rem - r * SC_X;
+            smem[(p * SC_Y + r) * SC_P + c] = v[k];
+        }
+    }
+}
+
+// Reconstruct from the coefficient tile already committed to smem.
+__device__ __forceinline__ void synth_compute(float* smem) {
     float* s_c = smem;                              // [4][SC_Y][SC_P]
     float* s_L = smem + S_SMEM_COEF;                // [2][ST_Y][SL_P]  (Lx, Hx)
     const int tid = threadIdx.x, nthr = blockDim.x;
-    const int ky0 = ty0 >> 1, kx0 = tx0 >> 1;
-    const size_t boff = (size_t)b * a.c_bstride;
-
-    for (int e = tid; e < 4 * SC_Y * SC_X; e += nthr) {
-        int p = e / (SC_Y * SC_X);
-        int rem = e - p * (SC_Y * SC_X);
-        int r = rem / SC_X, c = rem - r * SC_X;
-        int gy = min(ky0 + r, a.nH - 1), gx = min(kx0 + c, a.nW - 1);
-        const float* src = p == 0 ? a.A : p == 1 ? a.d0 : p == 2 ? a.d1 : a.d2;
-        s_c[(p * SC_Y + r) * SC_P + c] = src ? __ldg(src + boff + (size_t)gy * a.c_pitch + gx) : 0.0f;
-    }
     __syncthreads();
 
     // column pass (along y): Lx = synth(A, ad), Hx = synth(da, dd); 4 output rows per item
@@ -312,7 +353,12 @@ __global__ void __launch_bounds__(256) k_synthesis(SynthArgs a) {
     extern __shared__ float smem[];
     const int b = blockIdx.z;
     const int ty0 = blockIdx.y * ST_Y, tx0 = blockIdx.x * ST_X;
-    synth_tile(a, b, ty0, tx0, smem);
+    {
+        float v[S_LOAD_PER];
+        synth_fetch(a, b, ty0, tx0, v);
+        synth_commit(v, smem);
+    }
+    synth_compute(smem);
     float* out = a.out + (size_t)b * a.out_bstride;
     for (int e = threadIdx.x; e < ST_Y * ST_X; e += blockDim.x) {
         int r = e / ST_X, c = e - r * ST_X;
@@ -328,7 +374,7 @@ __global__ void __launch_bounds__(256) k_synthesis(SynthArgs a) {
 constexpr int ACC_PER_THREAD = (ST_Y * ST_X) / 256;
 
 template <typename TI>
-__global__ void __launch_bounds__(256) k_synthesis_accumulate(SynthArgs a, const TI* I, long long i_bstride,
+__global__ void __launch_bounds__(256, 2) k_synthesis_accumulate(SynthArgs a, const TI* I, long long i_bstride,
                                                               int i_pitch, int nb, double* num, double* den,
                                                               int acc_pitch) {
     extern __shared__ float smem[];
@@ -343,9 +389,22 @@ __global__ void __launch_bounds__(256) k_synthesis_accumulate(SynthArgs a, const
         an[k] = ok ? num[(size_t)gy * acc_pitch + gx] : 0.0;
         ad[k] = ok ? den[(size_t)gy * acc_pitch + gx] : 0.0;
     }
+    float v[S_LOAD_PER];
+    synth_fetch(a, 0, ty0, tx0, v);
     for (int b = 0; b < nb; ++b) {
-        synth_tile(a, b, ty0, tx0, smem);
+        synth_commit(v, smem);
+        if (b + 1 < nb) synth_fetch(a, b + 1, ty0, tx0, v);   // prefetch the next frame's tile
+        // this frame's I values, issued before the reconstruction so they are in flight
         const TI* Ib = I + (size_t)b * i_bstride;
+        float iv[ACC_PER_THREAD];
+#pragma unroll
+        for (int k = 0; k < ACC_PER_THREAD; ++k) {
+            int e = threadIdx.x + 256 * k;
+            int r = e / ST_X, c = e - r * ST_X;
+            int gy = min(ty0 + r, a.NH - 1), gx = min(tx0 + c, a.NW - 1);
+            iv[k] = (float)Ib[(size_t)gy * i_pitch + gx];
+        }
+        synth_compute(smem);
 #pragma unroll
         for (int k = 0; k < ACC_PER_THREAD; ++k) {
             int e = threadIdx.x + 256 * k;
@@ -353,12 +412,12 @@ __global__ void __launch_bounds__(256) k_synthesis_accumulate(SynthArgs a, const
             int gy = ty0 + r, gx = tx0 + c;
             if (gy < a.NH && gx < a.NW) {
                 double w = (double)smem[r * SO_P + c];
-                double iv = (double)(float)Ib[(size_t)gy * i_pitch + gx];
-                an[k] += w * iv;      // exact product (fp32 x fp32 fits fp64), fp64 sum
-                ad[k] += iv * iv;
+                double x = (double)iv[k];
+                an[k] += w * x;      // exact product (fp32 x fp32 fits fp64), fp64 sum
+                ad[k] += x * x;
             }
         }
-        __syncthreads();   // s_out is overwritten by the next frame's coefficient load
+        __syncthreads();   // s_out is overwritten by the next frame's coefficient commit
     }
 #pragma unroll
     for (int k = 0; k < ACC_PER_THREAD; ++k) {
