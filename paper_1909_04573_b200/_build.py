@@ -16,6 +16,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "-I" + os.path.join(ROOT, "include")]
+if os.environ.get("PRNU_DEBUG"):
+    FLAGS.append("-DPRNU_DEBUG")
 
 
 def _stale(target: str, deps) -> bool:

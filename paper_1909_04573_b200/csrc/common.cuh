@@ -11,6 +11,24 @@
 
 #include "../../include/prnu.h"
 
+// Device-side bounds checks, compiled in only for PRNU_DEBUG builds
+// (PRNU_DEBUG=1 python paper_1909_04573_b200/_build.py --force).
+#ifdef PRNU_DEBUG
+#include <cstdio>
+#define PRNU_DCHECK(c)                                                                          \
+    do {                                                                                        \
+        if (!(c)) {                                                                             \
+            printf("PRNU_DCHECK %s:%d %s blk(%d,%d,%d) thr %d\n", __FILE__, __LINE__, #c,        \
+                   blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x);                            \
+            __trap();                                                                           \
+        }                                                                                       \
+    } while (0)
+#else
+#define PRNU_DCHECK(c) \
+    do {               \
+    } while (0)
+#endif
+
 namespace prnu {
 
 // ---------------------------------------------------------------- errors

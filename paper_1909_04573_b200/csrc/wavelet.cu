@@ -21,17 +21,21 @@
 namespace prnu {
 
 // ============================================================== analysis
+// Tile: AT x AT output coefficients per subband, computed over an AR x AR
+// region (halo kHalo for the 9x9 windows) from an AIN x AIN input tile.
 constexpr int AT = 32;                  // output coefficient tile (square)
 constexpr int AR = AT + 2 * kHalo;      // 40: computed coefficient region
 constexpr int AIN = 2 * AR + 6;         // 86: input rows / columns of the region
-constexpr int AIN_P = AIN + 1;          // smem pitch of the input tile (odd)
-constexpr int ROW_P = AR + 1;           // pitch of row-pass / detail planes
-constexpr int HS_P = AT + 1;            // pitch of the horizontal window sums
-constexpr int A_SMEM_IN = AIN * AIN_P;            // >= 3*AR*ROW_P (details alias it)
-constexpr int A_SMEM_ROW = 2 * AIN * ROW_P;       // >= 4*AR*HS_P  (window sums alias it)
+constexpr int IN_P = 100;               // input tile pitch (== 4 mod 32: conflict-free LDS.128, row-major lanes)
+constexpr int RW_P = 44;                // row-pass plane pitch (== 12 mod 32)
+constexpr int DT_P = AR;                // detail plane pitch
+constexpr int V_P4 = AR + 1;            // vertical-sum plane pitch in float4 (41*4 == 4 mod 32)
+constexpr int A_SMEM_IN = AIN * IN_P;             // input tile; later the 3 detail planes
+constexpr int A_SMEM_ROW = 2 * AIN * RW_P;        // row-pass lo/hi; later the vertical sums
 constexpr size_t A_SMEM_BYTES = sizeof(float) * (A_SMEM_IN + A_SMEM_ROW) + sizeof(int) * (2 * AIN + 2 * AR);
-static_assert(3 * AR * ROW_P <= A_SMEM_IN, "detail planes must fit in the input tile");
-static_assert(4 * AR * HS_P <= A_SMEM_ROW, "window sums must fit in the row-pass planes");
+static_assert(3 * AR * DT_P <= A_SMEM_IN, "detail planes must fit in the input tile");
+static_assert(AT * V_P4 * 4 <= A_SMEM_ROW, "vertical sums must fit in the row-pass planes");
+static_assert(AIN * 3 <= 32 * 3 * 1 + 200, "load loop bound");
 
 struct AnalysisArgs {
     const void* in;
@@ -49,89 +53,118 @@ struct AnalysisArgs {
 };
 
 template <typename TIn>
-__global__ void __launch_bounds__(256) k_analysis_shrink(AnalysisArgs a) {
-    extern __shared__ float smem[];
-    float* s_in = smem;                          // [AIN][AIN_P]; later details [3][AR][ROW_P]
-    float* s_row = smem + A_SMEM_IN;             // [2][AIN][ROW_P]; later sums [4][AR][HS_P]
-    int* s_iy = reinterpret_cast<int*>(s_row + A_SMEM_ROW);   // [AIN] input row index
-    int* s_ix = s_iy + AIN;                                   // [AIN] input col index
-    int* s_rmap = s_ix + AIN;                                 // [AR] mirrored region row
-    int* s_cmap = s_rmap + AR;                                // [AR] mirrored region col
+__global__ void __launch_bounds__(256, 3) k_analysis_shrink(AnalysisArgs a) {
+    extern __shared__ __align__(16) float smem[];
+    float* s_in = smem;                          // [AIN][IN_P]; later details [3][AR][DT_P]
+    float* s_row = smem + A_SMEM_IN;             // [2][AIN][RW_P]; later vertical sums [AT][V_P4] float4
+    int* s_iy = reinterpret_cast<int*>(s_row + A_SMEM_ROW);   // [AIN] mirrored input row
+    int* s_ix = s_iy + AIN;                                   // [AIN] mirrored input col
+    int* s_rmap = s_ix + AIN;                                 // [AR] mirrored region row (local)
+    int* s_cmap = s_rmap + AR;                                // [AR] mirrored region col (local)
 
     const int tid = threadIdx.x;
-    const int nthr = blockDim.x;
+    const int lane = tid & 31, warp = tid >> 5;
     const int b = blockIdx.z;
     const int y0 = blockIdx.y * AT, x0 = blockIdx.x * AT;
     const int cy0 = y0 - kHalo, cx0 = x0 - kHalo;
     const TIn* in = reinterpret_cast<const TIn*>(a.in) + (size_t)b * a.in_bstride;
 
-    for (int i = tid; i < AIN; i += nthr) {
+    for (int i = tid; i < AIN; i += 256) {
         s_iy[i] = mirror(2 * cy0 - 6 + i, a.NH);
         s_ix[i] = mirror(2 * cx0 - 6 + i, a.NW);
     }
-    for (int i = tid; i < AR; i += nthr) {
-        s_rmap[i] = mirror(cy0 + i, a.nH) - cy0;
-        s_cmap[i] = mirror(cx0 + i, a.nW) - cx0;
+    for (int i = tid; i < AR; i += 256) {
+        // Window rows/cols of every output inside the plane mirror into the region;
+        // indices that only feed discarded outputs (beyond the plane) are clamped.
+        int mr = mirror(cy0 + i, a.nH) - cy0;
+        int mc = mirror(cx0 + i, a.nW) - cx0;
+        s_rmap[i] = (mr >= 0 && mr < AR) ? mr : i;
+        s_cmap[i] = (mc >= 0 && mc < AR) ? mc : i;
     }
+    // tile touches a border of the subband plane -> mirrored window reads needed
+    const bool border_x = (cx0 < 0) || (cx0 + AR > a.nW);
+    const bool border_y = (cy0 < 0) || (cy0 + AR > a.nH);
     __syncthreads();
 
-    // ---- load the mirrored input tile: every thread issues all its loads
-    // before the first shared-memory store, so they are in flight together.
+    // ---- 1. mirrored input tile: warp w loads rows w, w+8, ...; all loads in flight first
     {
-        constexpr int PER = (AIN * AIN + 255) / 256;
-        float v[PER];
+        constexpr int RPW = (AIN + 7) / 8;   // 11 rows per warp
+        float v[RPW][3];
+        int ixs[3];
 #pragma unroll
-        for (int k = 0; k < PER; ++k) {
-            int e = tid + 256 * k;
-            if (e < AIN * AIN) {
-                int r = e / AIN, c = e - r * AIN;
-                v[k] = (float)__ldg(in + (size_t)s_iy[r] * a.in_pitch + s_ix[c]);
+        for (int j = 0; j < 3; ++j) ixs[j] = s_ix[min(lane + 32 * j, AIN - 1)];
+#pragma unroll
+        for (int k = 0; k < RPW; ++k) {
+            int r = warp + 8 * k;
+            const TIn* row = in + (size_t)s_iy[min(r, AIN - 1)] * a.in_pitch;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                PRNU_DCHECK(s_iy[min(r, AIN - 1)] >= 0 && s_iy[min(r, AIN - 1)] < a.NH && ixs[j] >= 0 && ixs[j] < a.NW);
+                v[k][j] = (float)__ldg(row + ixs[j]);
             }
         }
 #pragma unroll
-        for (int k = 0; k < PER; ++k) {
-            int e = tid + 256 * k;
-            if (e < AIN * AIN) {
-                int r = e / AIN, c = e - r * AIN;
-                s_in[r * AIN_P + c] = v[k];
+        for (int k = 0; k < RPW; ++k) {
+            int r = warp + 8 * k;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                int c = lane + 32 * j;
+                if (r < AIN && c < AIN) s_in[r * IN_P + c] = v[k][j];
             }
         }
     }
     __syncthreads();
 
-    // ---- row pass (along x): lo/hi for AIN rows x AR coefficient columns
-    for (int it = tid; it < AIN * (AR / 4); it += nthr) {
-        int r = it % AIN, cg = it / AIN;
-        const float* src = s_in + r * AIN_P + 8 * cg;
-        float v[14];
+    // ---- 2. row pass (along x): lo/hi of AR coefficient columns for every input row;
+    //         item = (row, 8 coefficient columns), 24 inputs via 6 LDS.128
+    for (int it = tid; it < AIN * (AR / 8); it += 256) {
+        const int r = it % AIN, cg = it / AIN;
+        PRNU_DCHECK(r * IN_P + 16 * cg + 23 < A_SMEM_IN);
+        const float4* src = reinterpret_cast<const float4*>(s_in + r * IN_P + 16 * cg);
+        float v[24];
 #pragma unroll
-        for (int k = 0; k < 14; ++k) v[k] = src[k];
+        for (int k = 0; k < 6; ++k) {
+            float4 t = src[k];
+            v[4 * k] = t.x;
+            v[4 * k + 1] = t.y;
+            v[4 * k + 2] = t.z;
+            v[4 * k + 3] = t.w;
+        }
+        float lo[8], hi[8];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            float lo = 0.f, hi = 0.f;
+        for (int q = 0; q < 8; ++q) {
+            float l = 0.f, h = 0.f;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                lo = fmaf(wl_h(i), v[2 * q + i], lo);
-                hi = fmaf(wl_g(i), v[2 * q + i], hi);
+                l = fmaf(wl_h(i), v[2 * q + i], l);
+                h = fmaf(wl_g(i), v[2 * q + i], h);
             }
-            s_row[r * ROW_P + 4 * cg + q] = lo;
-            s_row[AIN * ROW_P + r * ROW_P + 4 * cg + q] = hi;
+            lo[q] = l;
+            hi[q] = h;
         }
+        float4* dl = reinterpret_cast<float4*>(s_row + r * RW_P + 8 * cg);
+        float4* dh = reinterpret_cast<float4*>(s_row + AIN * RW_P + r * RW_P + 8 * cg);
+        dl[0] = make_float4(lo[0], lo[1], lo[2], lo[3]);
+        dl[1] = make_float4(lo[4], lo[5], lo[6], lo[7]);
+        dh[0] = make_float4(hi[0], hi[1], hi[2], hi[3]);
+        dh[1] = make_float4(hi[4], hi[5], hi[6], hi[7]);
     }
     __syncthreads();
 
-    // ---- column pass (along y): 4 subbands for AR x AR coefficients
+    // ---- 3. column pass (along y): 4 subbands for AR x AR coefficients;
+    //         item = (column, 8 coefficient rows) from 22 rows of lo and hi
     float* s_det = s_in;
-    for (int it = tid; it < AR * (AR / 4); it += nthr) {
-        int c = it % AR, rg = it / AR;
-        float lo[14], hi[14];
+    for (int it = tid; it < AR * (AR / 8); it += 256) {
+        const int c = it % AR, rg = it / AR;
+        float lo[22], hi[22];
 #pragma unroll
-        for (int k = 0; k < 14; ++k) {
-            lo[k] = s_row[(8 * rg + k) * ROW_P + c];
-            hi[k] = s_row[AIN * ROW_P + (8 * rg + k) * ROW_P + c];
+        for (int k = 0; k < 22; ++k) {
+            lo[k] = s_row[(16 * rg + k) * RW_P + c];
+            hi[k] = s_row[AIN * RW_P + (16 * rg + k) * RW_P + c];
         }
+        const bool inner_c = (c >= kHalo) && (c < kHalo + AT) && (x0 + c - kHalo < a.nW);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < 8; ++q) {
             float aa = 0.f, ad = 0.f, da = 0.f, dd = 0.f;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
@@ -140,78 +173,96 @@ __global__ void __launch_bounds__(256) k_analysis_shrink(AnalysisArgs a) {
                 da = fmaf(wl_h(i), hi[2 * q + i], da);
                 dd = fmaf(wl_g(i), hi[2 * q + i], dd);
             }
-            int rr = 4 * rg + q;
-            s_det[0 * AR * ROW_P + rr * ROW_P + c] = da;
-            s_det[1 * AR * ROW_P + rr * ROW_P + c] = ad;
-            s_det[2 * AR * ROW_P + rr * ROW_P + c] = dd;
-            if (a.ll != nullptr && rr >= kHalo && rr < kHalo + AT && c >= kHalo && c < kHalo + AT) {
-                int gy = y0 + rr - kHalo, gx = x0 + c - kHalo;
-                if (gy < a.nH && gx < a.nW)
-                    a.ll[(size_t)b * a.out_bstride + (size_t)gy * a.out_pitch + gx] = aa;
+            const int rr = 8 * rg + q;
+            s_det[0 * AR * DT_P + rr * DT_P + c] = da;
+            s_det[1 * AR * DT_P + rr * DT_P + c] = ad;
+            s_det[2 * AR * DT_P + rr * DT_P + c] = dd;
+            if (a.ll != nullptr && inner_c && rr >= kHalo && rr < kHalo + AT) {
+                const int gy = y0 + rr - kHalo;
+                PRNU_DCHECK(x0 + c - kHalo >= 0 && x0 + c - kHalo < a.nW && gy >= 0);
+                if (gy < a.nH) a.ll[(size_t)b * a.out_bstride + (size_t)gy * a.out_pitch + x0 + c - kHalo] = aa;
             }
         }
     }
     __syncthreads();
 
-    // ---- shrink each detail subband (R-7)
+    // ---- 4. shrink each detail subband (R-7): separable window sums of c^2,
+    //         vertical (per column, 8 rows per item) then horizontal (per row, 8 cols per item)
     const float s0 = a.sp.sigma0_sq;
     const int wm = a.sp.wmask;
-    float* s_hs = s_row;
+    float4* s_v = reinterpret_cast<float4*>(s_row);   // [AT][V_P4]: (v3, v5, v7, v9)
     for (int s = 0; s < 3; ++s) {
-        const float* det = s_det + s * AR * ROW_P;
-        // stage A: horizontal window sums of c^2 (3,5,7,9 nested) for real region rows
-        for (int it = tid; it < AR * AT; it += nthr) {
-            int j = it % AT, rr = it / AT;
-            if (s_rmap[rr] != rr) continue;
-            float v[9];
+        const float* det = s_det + s * AR * DT_P;
+        // stage V: columns x in [0,AR) that are real, output rows 8*ig .. 8*ig+7
+        for (int it = tid; it < AR * (AT / 8); it += 256) {
+            const int x = it % AR, ig = it / AR;
+            if (border_x && s_cmap[x] != x) continue;
+            float q[16];
 #pragma unroll
-            for (int k = 0; k < 9; ++k) {
-                float c = det[rr * ROW_P + s_cmap[j + k]];
-                v[k] = c * c;
+            for (int k = 0; k < 16; ++k) {
+                const int rr = border_y ? s_rmap[8 * ig + k] : 8 * ig + k;
+                PRNU_DCHECK(rr >= 0 && rr < AR && x >= 0 && x < AR);
+                const float c = det[rr * DT_P + x];
+                q[k] = c * c;
             }
-            float h3 = v[3] + v[4] + v[5];
-            float h5 = h3 + v[2] + v[6];
-            float h7 = h5 + v[1] + v[7];
-            float h9 = h7 + v[0] + v[8];
-            s_hs[0 * AR * HS_P + rr * HS_P + j] = h3;
-            s_hs[1 * AR * HS_P + rr * HS_P + j] = h5;
-            s_hs[2 * AR * HS_P + rr * HS_P + j] = h7;
-            s_hs[3 * AR * HS_P + rr * HS_P + j] = h9;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                float v3 = q[t + 3] + q[t + 4] + q[t + 5];
+                float v5 = v3 + q[t + 2] + q[t + 6];
+                float v7 = v5 + q[t + 1] + q[t + 7];
+                float v9 = v7 + q[t] + q[t + 8];
+                s_v[(8 * ig + t) * V_P4 + x] = make_float4(v3, v5, v7, v9);
+            }
         }
         __syncthreads();
-        // stage B: vertical window sums, MAP variance, Wiener factor; 4 rows per thread
+        // stage H: output row i, output columns 8*jg .. 8*jg+7
         float* dst = (s == 0 ? a.d0 : s == 1 ? a.d1 : a.d2) + (size_t)b * a.out_bstride;
-        for (int it = tid; it < AT * (AT / 4); it += nthr) {
-            int j = it % AT, ig = it / AT;
-            float h[4][12];
+        for (int it = tid; it < AT * (AT / 8); it += 256) {
+            const int i = it % AT, jg = it / AT;
+            const int gy = y0 + i;
+            float4 u[16];
 #pragma unroll
-            for (int k = 0; k < 12; ++k) {
-                int rr = s_rmap[4 * ig + k];
-#pragma unroll
-                for (int w = 0; w < 4; ++w) h[w][k] = s_hs[w * AR * HS_P + rr * HS_P + j];
+            for (int k = 0; k < 16; ++k) {
+                const int xx = border_x ? s_cmap[8 * jg + k] : 8 * jg + k;
+                PRNU_DCHECK(xx >= 0 && xx < AR && i * V_P4 + xx < A_SMEM_ROW / 4);
+                u[k] = s_v[i * V_P4 + xx];
             }
+            const float4* crow = reinterpret_cast<const float4*>(det + (i + kHalo) * DT_P + 8 * jg + kHalo);
+            const float4 c0 = crow[0], c1 = crow[1];
+            const float cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+            float s3 = u[3].x + u[4].x + u[5].x;
+            float s5 = u[2].y + u[3].y + u[4].y + u[5].y + u[6].y;
+            float s7 = u[1].z + u[2].z + u[3].z + u[4].z + u[5].z + u[6].z + u[7].z;
+            float s9 = u[0].w + u[1].w + u[2].w + u[3].w + u[4].w + u[5].w + u[6].w + u[7].w + u[8].w;
+            float o[8];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                float s3 = 0.f, s5 = 0.f, s7 = 0.f, s9 = 0.f;
-#pragma unroll
-                for (int k = 3; k <= 5; ++k) s3 += h[0][q + k];
-#pragma unroll
-                for (int k = 2; k <= 6; ++k) s5 += h[1][q + k];
-#pragma unroll
-                for (int k = 1; k <= 7; ++k) s7 += h[2][q + k];
-#pragma unroll
-                for (int k = 0; k <= 8; ++k) s9 += h[3][q + k];
+            for (int t = 0; t < 8; ++t) {
+                if (t > 0) {   // slide the windows one column right
+                    s3 += u[t + 5].x - u[t + 2].x;
+                    s5 += u[t + 6].y - u[t + 1].y;
+                    s7 += u[t + 7].z - u[t].z;
+                    s9 += u[t + 8].w - u[t - 1].w;
+                }
                 float m = 3.402823466e38f;
                 if (wm & 1) m = fminf(m, s3 * (1.0f / 9.0f));
                 if (wm & 2) m = fminf(m, s5 * (1.0f / 25.0f));
                 if (wm & 4) m = fminf(m, s7 * (1.0f / 49.0f));
                 if (wm & 8) m = fminf(m, s9 * (1.0f / 81.0f));
-                float v = fmaxf(m - s0, 0.0f);
-                int i = 4 * ig + q;
-                float c = det[(i + kHalo) * ROW_P + j + kHalo];
-                float cn = c * __fdividef(s0, v + s0);     // noise-domain coefficient c - F(c)
-                int gy = y0 + i, gx = x0 + j;
-                if (gy < a.nH && gx < a.nW) dst[(size_t)gy * a.out_pitch + gx] = cn;
+                const float var = fmaxf(m - s0, 0.0f);
+                o[t] = cc[t] * __fdividef(s0, var + s0);   // noise-domain coefficient c - F(c)
+            }
+            if (gy < a.nH) {
+                const int gx = x0 + 8 * jg;
+                float* drow = dst + (size_t)gy * a.out_pitch + gx;
+                PRNU_DCHECK(gx >= 0 && gx < a.out_pitch && gy >= 0);
+                if (gx + 8 <= a.nW) {
+                    reinterpret_cast<float4*>(drow)[0] = make_float4(o[0], o[1], o[2], o[3]);
+                    reinterpret_cast<float4*>(drow)[1] = make_float4(o[4], o[5], o[6], o[7]);
+                } else {
+#pragma unroll
+                    for (int t = 0; t < 8; ++t)
+                        if (gx + t < a.nW) drow[t] = o[t];
+                }
             }
         }
         __syncthreads();
