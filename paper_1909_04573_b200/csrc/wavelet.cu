@@ -17,6 +17,7 @@
 // Filters are compile-time immediates (FFMA-imm).  fp32 arithmetic; the
 // accumulators are fp64.
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace prnu {
 
@@ -35,7 +36,6 @@ constexpr int A_SMEM_ROW = 2 * AIN * RW_P;        // row-pass lo/hi; later the v
 constexpr size_t A_SMEM_BYTES = sizeof(float) * (A_SMEM_IN + A_SMEM_ROW) + sizeof(int) * (2 * AIN + 2 * AR);
 static_assert(3 * AR * DT_P <= A_SMEM_IN, "detail planes must fit in the input tile");
 static_assert(AT * V_P4 * 4 <= A_SMEM_ROW, "vertical sums must fit in the row-pass planes");
-static_assert(AIN * 3 <= 32 * 3 * 1 + 200, "load loop bound");
 
 struct AnalysisArgs {
     const void* in;
@@ -270,85 +270,59 @@ __global__ void __launch_bounds__(256, 3) k_analysis_shrink(AnalysisArgs a) {
 }
 
 // ============================================================== synthesis
+// Output tile ST_Y x ST_X; its coefficients (rows ky0 .. ky0+SC_Y, cols kx0 ..
+// kx0+SC_X of the four subband planes) arrive by TMA into a double-buffered
+// shared tile: thread 0 issues frame f+1's four box loads on an mbarrier while
+// the CTA reconstructs frame f.  TMA zero-fills coefficients beyond the plane;
+// only outputs beyond the plane depend on them (t < N uses k <= (N+5)/2 < n).
 constexpr int ST_Y = 32, ST_X = 64;     // output tile
 constexpr int SC_Y = ST_Y / 2 + 3;      // 19 coefficient rows
 constexpr int SC_X = ST_X / 2 + 3;      // 35 coefficient cols
-constexpr int SC_P = SC_X + 1;          // 36
+constexpr int SC_BW = 36;               // TMA box width (144 B, multiple of 16)
+constexpr int SC_PS = 704;              // plane stride in floats (>= 19*36, 128-B multiple)
+constexpr int SC_TILE = 4 * SC_PS;      // one frame's 4 planes (128-B multiple)
 constexpr int SL_P = SC_X + 2;          // 37 (odd) pitch of the column-pass planes
 constexpr int SO_P = ST_X + 1;          // 65 pitch of the output staging tile
-constexpr int S_SMEM_COEF = 4 * SC_Y * SC_P;          // coefficient tiles; output staging aliases it
-constexpr int S_SMEM_L = 2 * ST_Y * SL_P;
-constexpr size_t S_SMEM_BYTES = sizeof(float) * (S_SMEM_COEF + S_SMEM_L);
-static_assert(ST_Y * SO_P <= S_SMEM_COEF, "output staging must fit in the coefficient tiles");
+constexpr size_t S_SMEM_BYTES = sizeof(float) * (2 * SC_TILE + 2 * ST_Y * SL_P + ST_Y * SO_P) + 2 * sizeof(uint64_t);
+static_assert(SC_Y * SC_BW <= SC_PS && (SC_PS * 4) % 128 == 0, "TMA plane tile layout");
+static_assert(((2 * SC_TILE + 2 * ST_Y * SL_P + ST_Y * SO_P) * 4) % 8 == 0, "mbarrier alignment");
+constexpr int ACC_PER_THREAD = (ST_Y * ST_X) / 256;
 
-struct SynthArgs {
-    const float* A;     // approximation (nullable = 0)
-    const float* d0;    // da
-    const float* d1;    // ad
-    const float* d2;    // dd
-    long long c_bstride;
-    int c_pitch;
-    int nH, nW;
-    float* out;
-    long long out_bstride;
-    int out_pitch;
-    int NH, NW;
+struct SynthMaps {
+    CUtensorMap A, d0, d1, d2;   // approximation (unused if !has_A), da, ad, dd
 };
 
-// Reconstruct the ST_Y x ST_X output tile at (ty0, tx0) of frame b into
-// s_out[ST_Y][SO_P] (shared).  All threads participate; ends with a barrier.
-constexpr int S_LOAD_PER = (4 * SC_Y * SC_X + 255) / 256;
+struct SynthArgs {
+    int has_A;
+    int NH, NW;                  // output plane size
+    int nb;                      // frames
+    int frames_per_cta;          // MODE 0: frames per CTA along grid.z
+    float* out;                  // MODE 0 output [nb][NH][out_pitch]
+    long long out_bstride;
+    int out_pitch;
+    const void* I;               // MODE 1/2: frames the residuals come from
+    long long i_bstride;
+    int i_pitch;
+    double* num;                 // MODE 1/2: fp64 accumulators [NH][acc_pitch]
+    double* den;
+    int acc_pitch;
+};
 
-// Issue the loads of frame b's coefficient tile into registers (no smem write).
-__device__ __forceinline__ void synth_fetch(const SynthArgs& a, int b, int ty0, int tx0, float (&v)[S_LOAD_PER]) {
-    const int ky0 = ty0 >> 1, kx0 = tx0 >> 1;
-    const size_t boff = (size_t)b * a.c_bstride;
-#pragma unroll
-    for (int k = 0; k < S_LOAD_PER; ++k) {
-        int e = threadIdx.x + 256 * k;
-        v[k] = 0.0f;
-        if (e < 4 * SC_Y * SC_X) {
-            int p = e / (SC_Y * SC_X);
-            int rem = e - p * (SC_Y * SC_X);
-            int r = rem / SC_X, c = rem - r * SC_X;
-            int gy = min(ky0 + r, a.nH - 1), gx = min(kx0 + c, a.nW - 1);
-            const float* src = p == 0 ? a.A : p == 1 ? a.d0 : p == 2 ? a.d1 : a.d2;
-            if (src) v[k] = __ldg(src + boff + (size_t)gy * a.c_pitch + gx);
-        }
-    }
-}
-
-__device__ __forceinline__ void synth_commit(const float (&v)[S_LOAD_PER], float* smem) {
-#pragma unroll
-    for (int k = 0; k < S_LOAD_PER; ++k) {
-        int e = threadIdx.x + 256 * k;
-        if (e < 4 * SC_Y * SC_X) {
-            int p = e / (SC_Y * SC_X);
-            int rem = e - p * (SC_Y * SC_X);
-            int r = rem / SC_X, c = rem - r * SC_X;
-            smem[(p * SC_Y + r) * SC_P + c] = v[k];
-        }
-    }
-}
-
-// Reconstruct from the coefficient tile already committed to smem.
-__device__ __forceinline__ void synth_compute(float* smem) {
-    float* s_c = smem;                              // [4][SC_Y][SC_P]
-    float* s_L = smem + S_SMEM_COEF;                // [2][ST_Y][SL_P]  (Lx, Hx)
-    const int tid = threadIdx.x, nthr = blockDim.x;
-    __syncthreads();
-
-    // column pass (along y): Lx = synth(A, ad), Hx = synth(da, dd); 4 output rows per item
-    for (int it = tid; it < SC_X * (ST_Y / 4); it += nthr) {
-        int k = it % SC_X, sg = it / SC_X;
-        float va[5], vad[5], vda[5], vdd[5];
+// Column pass (along y) then row pass (along x) of one frame's tile in `c`
+// into s_out[ST_Y][SO_P].  Ends with a barrier (s_out complete).
+__device__ __forceinline__ void synth_compute(const float* c, float* s_L, float* s_out) {
+    const int tid = threadIdx.x;
+    // Lx = synth(A, ad), Hx = synth(da, dd); item = (coefficient column k, 4 output rows)
+    for (int it = tid; it < SC_X * (ST_Y / 4); it += 256) {
+        const int k = it % SC_X, sg = it / SC_X;
+        float va[5], vda[5], vad[5], vdd[5];
 #pragma unroll
         for (int m = 0; m < 5; ++m) {
-            int r = 2 * sg + m;
-            va[m] = s_c[(0 * SC_Y + r) * SC_P + k];
-            vda[m] = s_c[(1 * SC_Y + r) * SC_P + k];
-            vad[m] = s_c[(2 * SC_Y + r) * SC_P + k];
-            vdd[m] = s_c[(3 * SC_Y + r) * SC_P + k];
+            const int r = (2 * sg + m) * SC_BW + k;
+            va[m] = c[0 * SC_PS + r];
+            vda[m] = c[1 * SC_PS + r];
+            vad[m] = c[2 * SC_PS + r];
+            vdd[m] = c[3 * SC_PS + r];
         }
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
@@ -362,25 +336,22 @@ __device__ __forceinline__ void synth_compute(float* smem) {
                     h = fmaf(wl_h(6 - 2 * m + e), vda[q + m], h);
                     h = fmaf(wl_g(6 - 2 * m + e), vdd[q + m], h);
                 }
-                int t = 4 * sg + 2 * q + e;
+                const int t = 4 * sg + 2 * q + e;
                 s_L[t * SL_P + k] = l;
                 s_L[ST_Y * SL_P + t * SL_P + k] = h;
             }
         }
     }
     __syncthreads();
-
-    // row pass (along x): 8 output columns per item; stage into s_out (aliases s_c)
-    float* s_out = smem;
-    for (int it = tid; it < ST_Y * (ST_X / 8); it += nthr) {
-        int t = it % ST_Y, g = it / ST_Y;
+    // row pass: item = (output row t, 8 output columns)
+    for (int it = tid; it < ST_Y * (ST_X / 8); it += 256) {
+        const int t = it % ST_Y, g = it / ST_Y;
         float vl[7], vh[7];
 #pragma unroll
         for (int m = 0; m < 7; ++m) {
             vl[m] = s_L[t * SL_P + 4 * g + m];
             vh[m] = s_L[ST_Y * SL_P + t * SL_P + 4 * g + m];
         }
-        float o[8];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
 #pragma unroll
@@ -391,93 +362,116 @@ __device__ __forceinline__ void synth_compute(float* smem) {
                     x = fmaf(wl_h(6 - 2 * m + e), vl[q + m], x);
                     x = fmaf(wl_g(6 - 2 * m + e), vh[q + m], x);
                 }
-                o[2 * q + e] = x;
+                s_out[t * SO_P + 8 * g + 2 * q + e] = x;
             }
         }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) s_out[t * SO_P + 8 * g + k] = o[k];
     }
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) k_synthesis(SynthArgs a) {
-    extern __shared__ float smem[];
-    const int b = blockIdx.z;
+// MODE 0: write the reconstruction (grid.z = frame chunks).
+// MODE 1: level-1 reconstruction fused with the MLE accumulation over all nb
+//         frames (grid.z = 1), I of type TI; NUM/DEN read once, written once,
+//         per-pixel sums in ascending frame order.
+template <int MODE, typename TI>
+__global__ void __launch_bounds__(256, MODE == 0 ? 3 : 2) k_synth_tma(const __grid_constant__ SynthMaps maps, SynthArgs a) {
+    extern __shared__ __align__(128) float smem[];
+    float* cbuf0 = smem;
+    float* s_L = smem + 2 * SC_TILE;
+    float* s_out = s_L + 2 * ST_Y * SL_P;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(s_out + ST_Y * SO_P);
+    const int tid = threadIdx.x;
     const int ty0 = blockIdx.y * ST_Y, tx0 = blockIdx.x * ST_X;
-    {
-        float v[S_LOAD_PER];
-        synth_fetch(a, b, ty0, tx0, v);
-        synth_commit(v, smem);
+    const int ky0 = ty0 >> 1, kx0 = tx0 >> 1;
+    int f0 = 0, f1 = a.nb;
+    if (MODE == 0) {
+        f0 = blockIdx.z * a.frames_per_cta;
+        f1 = min(a.nb, f0 + a.frames_per_cta);
     }
-    synth_compute(smem);
-    float* out = a.out + (size_t)b * a.out_bstride;
-    for (int e = threadIdx.x; e < ST_Y * ST_X; e += blockDim.x) {
-        int r = e / ST_X, c = e - r * ST_X;
-        int gy = ty0 + r, gx = tx0 + c;
-        if (gy < a.NH && gx < a.NW) out[(size_t)gy * a.out_pitch + gx] = smem[r * SO_P + c];
+    const uint32_t tx_bytes = (a.has_A ? 4u : 3u) * SC_BW * SC_Y * 4u;
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
     }
-}
-
-// Level-1 synthesis fused with the MLE accumulation over `nb` frames.
-// I: the frames the residuals come from (the SDA frames, or the u8 frames at
-// depth 1), [nb][NH][NW] with pitch i_pitch.  num/den: fp64 [NH][NW] (pitch
-// acc_pitch), read once before the frame loop and written once after it.
-constexpr int ACC_PER_THREAD = (ST_Y * ST_X) / 256;
-
-template <typename TI>
-__global__ void __launch_bounds__(256, 2) k_synthesis_accumulate(SynthArgs a, const TI* I, long long i_bstride,
-                                                              int i_pitch, int nb, double* num, double* den,
-                                                              int acc_pitch) {
-    extern __shared__ float smem[];
-    const int ty0 = blockIdx.y * ST_Y, tx0 = blockIdx.x * ST_X;
-    double an[ACC_PER_THREAD], ad[ACC_PER_THREAD];
-#pragma unroll
-    for (int k = 0; k < ACC_PER_THREAD; ++k) {
-        int e = threadIdx.x + 256 * k;
-        int r = e / ST_X, c = e - r * ST_X;
-        int gy = ty0 + r, gx = tx0 + c;
-        bool ok = gy < a.NH && gx < a.NW;
-        an[k] = ok ? num[(size_t)gy * acc_pitch + gx] : 0.0;
-        ad[k] = ok ? den[(size_t)gy * acc_pitch + gx] : 0.0;
-    }
-    float v[S_LOAD_PER];
-    synth_fetch(a, 0, ty0, tx0, v);
-    for (int b = 0; b < nb; ++b) {
-        synth_commit(v, smem);
-        if (b + 1 < nb) synth_fetch(a, b + 1, ty0, tx0, v);   // prefetch the next frame's tile
-        // this frame's I values, issued before the reconstruction so they are in flight
-        const TI* Ib = I + (size_t)b * i_bstride;
-        float iv[ACC_PER_THREAD];
-#pragma unroll
-        for (int k = 0; k < ACC_PER_THREAD; ++k) {
-            int e = threadIdx.x + 256 * k;
-            int r = e / ST_X, c = e - r * ST_X;
-            int gy = min(ty0 + r, a.NH - 1), gx = min(tx0 + c, a.NW - 1);
-            iv[k] = (float)Ib[(size_t)gy * i_pitch + gx];
+    if (!a.has_A) {   // coarsest level: the approximation of the noise domain is 0 (R-10)
+        for (int i = tid; i < SC_PS; i += 256) {
+            cbuf0[i] = 0.f;
+            cbuf0[SC_TILE + i] = 0.f;
         }
-        synth_compute(smem);
+    }
+    __syncthreads();
+    auto issue = [&](int f, int buf) {
+        float* c = cbuf0 + buf * SC_TILE;
+        mbar_arrive_expect_tx(&bar[buf], tx_bytes);
+        if (a.has_A) tma_load_3d(c, &maps.A, kx0, ky0, f, &bar[buf]);
+        tma_load_3d(c + 1 * SC_PS, &maps.d0, kx0, ky0, f, &bar[buf]);
+        tma_load_3d(c + 2 * SC_PS, &maps.d1, kx0, ky0, f, &bar[buf]);
+        tma_load_3d(c + 3 * SC_PS, &maps.d2, kx0, ky0, f, &bar[buf]);
+    };
+    if (tid == 0 && f0 < f1) issue(f0, 0);
+
+    double an[ACC_PER_THREAD], ad[ACC_PER_THREAD];
+    if (MODE == 1) {
 #pragma unroll
         for (int k = 0; k < ACC_PER_THREAD; ++k) {
-            int e = threadIdx.x + 256 * k;
-            int r = e / ST_X, c = e - r * ST_X;
-            int gy = ty0 + r, gx = tx0 + c;
-            if (gy < a.NH && gx < a.NW) {
-                double w = (double)smem[r * SO_P + c];
-                double x = (double)iv[k];
-                an[k] += w * x;      // exact product (fp32 x fp32 fits fp64), fp64 sum
+            const int e = tid + 256 * k;
+            const int r = e / ST_X, cc = e - r * ST_X;
+            const int gy = ty0 + r, gx = tx0 + cc;
+            const bool ok = gy < a.NH && gx < a.NW;
+            an[k] = ok ? a.num[(size_t)gy * a.acc_pitch + gx] : 0.0;
+            ad[k] = ok ? a.den[(size_t)gy * a.acc_pitch + gx] : 0.0;
+        }
+    }
+    for (int f = f0; f < f1; ++f) {
+        const int it = f - f0, buf = it & 1;
+        if (tid == 0 && f + 1 < f1) {
+            fence_proxy_async();
+            issue(f + 1, buf ^ 1);   // buffer buf^1 was released by the barrier ending iteration it-1
+        }
+        float iv[ACC_PER_THREAD];
+        if (MODE == 1) {   // this frame's I values, in flight during the reconstruction
+            const TI* Ib = reinterpret_cast<const TI*>(a.I) + (size_t)f * a.i_bstride;
+#pragma unroll
+            for (int k = 0; k < ACC_PER_THREAD; ++k) {
+                const int e = tid + 256 * k;
+                const int r = e / ST_X, cc = e - r * ST_X;
+                const int gy = min(ty0 + r, a.NH - 1), gx = min(tx0 + cc, a.NW - 1);
+                iv[k] = (float)Ib[(size_t)gy * a.i_pitch + gx];
+            }
+        }
+        mbar_wait(&bar[buf], (it >> 1) & 1);
+        synth_compute(cbuf0 + buf * SC_TILE, s_L, s_out);
+        if (MODE == 0) {
+            float* out = a.out + (size_t)f * a.out_bstride;
+            for (int e = tid; e < ST_Y * ST_X; e += 256) {
+                const int r = e / ST_X, cc = e - r * ST_X;
+                const int gy = ty0 + r, gx = tx0 + cc;
+                if (gy < a.NH && gx < a.NW) out[(size_t)gy * a.out_pitch + gx] = s_out[r * SO_P + cc];
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < ACC_PER_THREAD; ++k) {
+                const int e = tid + 256 * k;
+                const int r = e / ST_X, cc = e - r * ST_X;
+                const double w = (double)s_out[r * SO_P + cc];
+                const double x = (double)iv[k];
+                an[k] += w * x;   // exact product (fp32 x fp32 fits fp64), fp64 sum
                 ad[k] += x * x;
             }
         }
-        __syncthreads();   // s_out is overwritten by the next frame's coefficient commit
+        __syncthreads();   // s_L / s_out / cbuf[buf] free for the next frame
     }
+    if (MODE == 1) {
 #pragma unroll
-    for (int k = 0; k < ACC_PER_THREAD; ++k) {
-        int e = threadIdx.x + 256 * k;
-        int r = e / ST_X, c = e - r * ST_X;
-        int gy = ty0 + r, gx = tx0 + c;
-        if (gy < a.NH && gx < a.NW) {
-            num[(size_t)gy * acc_pitch + gx] = an[k];
-            den[(size_t)gy * acc_pitch + gx] = ad[k];
+        for (int k = 0; k < ACC_PER_THREAD; ++k) {
+            const int e = tid + 256 * k;
+            const int r = e / ST_X, cc = e - r * ST_X;
+            const int gy = ty0 + r, gx = tx0 + cc;
+            if (gy < a.NH && gx < a.NW) {
+                a.num[(size_t)gy * a.acc_pitch + gx] = an[k];
+                a.den[(size_t)gy * a.acc_pitch + gx] = ad[k];
+            }
         }
     }
 }
@@ -533,6 +527,28 @@ static const char* kAnalysisName[kMaxLevels + 1] = {"", "analysis_l1", "analysis
 static const char* kSynthName[kMaxLevels + 1] = {"", "synthesis_l1", "synthesis_l2", "synthesis_l3",
                                                  "synthesis_l4", "synthesis_l5", "synthesis_l6"};
 
+bool encode_tensor_map_3d(CUtensorMap* map, CUtensorMapDataType dt, size_t elem_bytes, const void* base, uint64_t cols,
+                          uint64_t rows, uint64_t depth, uint64_t pitch_bytes, uint64_t plane_bytes, uint32_t box_w,
+                          uint32_t box_h) {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !p)
+            return false;
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    (void)elem_bytes;
+    cuuint64_t dims[3] = {cols, rows, depth};
+    cuuint64_t strides[2] = {pitch_bytes, plane_bytes};
+    cuuint32_t box[3] = {box_w, box_h, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(map, dt, 3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 static bool g_attr_done = false;
 
 static int setup_attributes() {
@@ -541,18 +557,40 @@ static int setup_attributes() {
                                           (int)A_SMEM_BYTES);
     cudaError_t e2 = cudaFuncSetAttribute(k_analysis_shrink<uint8_t>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)A_SMEM_BYTES);
-    if (e1 != cudaSuccess || e2 != cudaSuccess)
-        return fail(PRNU_CUDA_ERROR, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e1 ? e1 : e2));
+    cudaError_t e3 = cudaFuncSetAttribute(k_synth_tma<0, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)S_SMEM_BYTES);
+    cudaError_t e4 = cudaFuncSetAttribute(k_synth_tma<1, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)S_SMEM_BYTES);
+    cudaError_t e5 = cudaFuncSetAttribute(k_synth_tma<1, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)S_SMEM_BYTES);
+    cudaError_t e = e1 ? e1 : e2 ? e2 : e3 ? e3 : e4 ? e4 : e5;
+    if (e != cudaSuccess) return fail(PRNU_CUDA_ERROR, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
     g_attr_done = true;
     return PRNU_OK;
 }
 
-// Run the analysis of all levels and the synthesis of levels L..2 for `nb`
-// frames; leaves the level-1 noise-domain subbands + the level-1 synthesis
-// input ready.  Returns a SynthArgs for the final (level-1) synthesis.
+// Tensor maps over the four level-l planes of `nb` frames, box SC_BW x SC_Y.
+static int synth_maps(const Pyramid& p, const PyramidBuffers& pb, int l, int nb, bool has_A, SynthMaps* m) {
+    const uint64_t pitch = (uint64_t)p.pitch[l] * 4, plane = (uint64_t)pb.bstride[l] * 4;
+    const float* src[4] = {pb.approx[l], pb.det[l][0], pb.det[l][1], pb.det[l][2]};
+    CUtensorMap* dst[4] = {&m->A, &m->d0, &m->d1, &m->d2};
+    for (int i = 0; i < 4; ++i) {
+        if (i == 0 && !has_A) {
+            *dst[0] = CUtensorMap{};
+            continue;
+        }
+        if (!encode_tensor_map_3d(dst[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, src[i], p.nW[l], p.nH[l], nb, pitch,
+                                  plane, SC_BW, SC_Y))
+            return fail(PRNU_CUDA_ERROR, "cuTensorMapEncodeTiled failed");
+    }
+    return PRNU_OK;
+}
+
+// Analysis of all levels, then synthesis of levels L..2 (the level-1
+// synthesis is launched by the caller, fused or not with the accumulation).
 template <typename TIn>
 static int denoise_front(const TIn* in, long long in_bstride, int in_pitch, int nb, const Pyramid& p,
-                         const PyramidBuffers& pb, const ShrinkParams& sp, cudaStream_t st, SynthArgs* last) {
+                         const PyramidBuffers& pb, const ShrinkParams& sp, cudaStream_t st) {
     int rc = setup_attributes();
     if (rc) return rc;
     const int L = p.levels;
@@ -585,32 +623,26 @@ static int denoise_front(const TIn* in, long long in_bstride, int in_pitch, int 
         count_launch();
         if ((rc = check_launch("k_analysis_shrink"))) return rc;
     }
-    for (int l = L; l >= 1; --l) {
+    for (int l = L; l >= 2; --l) {
+        SynthMaps m;
+        if ((rc = synth_maps(p, pb, l, nb, l < L, &m))) return rc;
         SynthArgs s{};
-        s.A = (l < L) ? pb.approx[l] : nullptr;
-        s.d0 = pb.det[l][0];
-        s.d1 = pb.det[l][1];
-        s.d2 = pb.det[l][2];
-        s.c_bstride = (long long)pb.bstride[l];
-        s.c_pitch = p.pitch[l];
-        s.nH = p.nH[l];
-        s.nW = p.nW[l];
+        s.has_A = l < L;
         s.NH = p.nH[l - 1];
         s.NW = p.nW[l - 1];
-        if (l == 1) {
-            *last = s;   // out filled by the caller
-            break;
-        }
+        s.nb = nb;
         s.out = pb.approx[l - 1];
         s.out_bstride = (long long)pb.bstride[l - 1];
         s.out_pitch = p.pitch[l - 1];
-        dim3 grid((s.NW + ST_X - 1) / ST_X, (s.NH + ST_Y - 1) / ST_Y, nb);
+        const int tiles = ((s.NW + ST_X - 1) / ST_X) * ((s.NH + ST_Y - 1) / ST_Y);
+        s.frames_per_cta = std::max(1, std::min(4, tiles * nb / (148 * 6)));
+        dim3 grid((s.NW + ST_X - 1) / ST_X, (s.NH + ST_Y - 1) / ST_Y, (nb + s.frames_per_cta - 1) / s.frames_per_cta);
         {
             KTimer kt(kSynthName[l], st);
-            k_synthesis<<<grid, 256, S_SMEM_BYTES, st>>>(s);
+            k_synth_tma<0, float><<<grid, 256, S_SMEM_BYTES, st>>>(m, s);
         }
         count_launch();
-        if ((rc = check_launch("k_synthesis"))) return rc;
+        if ((rc = check_launch("k_synth_tma"))) return rc;
     }
     return PRNU_OK;
 }
@@ -619,35 +651,55 @@ template <typename TIn>
 int run_residual(const TIn* in, int nb, int H, int W, const Pyramid& p, const ShrinkParams& sp, float* W_out,
                  float* ws_pyr, cudaStream_t st) {
     PyramidBuffers pb = carve_pyramid(p, ws_pyr, nb);
-    SynthArgs s{};
-    int rc = denoise_front<TIn>(in, (long long)H * W, W, nb, p, pb, sp, st, &s);
+    int rc = denoise_front<TIn>(in, (long long)H * W, W, nb, p, pb, sp, st);
     if (rc) return rc;
+    SynthMaps m;
+    if ((rc = synth_maps(p, pb, 1, nb, p.levels > 1, &m))) return rc;
+    SynthArgs s{};
+    s.has_A = p.levels > 1;
+    s.NH = H;
+    s.NW = W;
+    s.nb = nb;
     s.out = W_out;
     s.out_bstride = (long long)H * W;
     s.out_pitch = W;
-    dim3 grid((W + ST_X - 1) / ST_X, (H + ST_Y - 1) / ST_Y, nb);
+    const int tiles = ((W + ST_X - 1) / ST_X) * ((H + ST_Y - 1) / ST_Y);
+    s.frames_per_cta = std::max(1, std::min(4, tiles * nb / (148 * 6)));
+    dim3 grid((W + ST_X - 1) / ST_X, (H + ST_Y - 1) / ST_Y, (nb + s.frames_per_cta - 1) / s.frames_per_cta);
     {
         KTimer kt("synthesis_l1", st);
-        k_synthesis<<<grid, 256, S_SMEM_BYTES, st>>>(s);
+        k_synth_tma<0, float><<<grid, 256, S_SMEM_BYTES, st>>>(m, s);
     }
     count_launch();
-    return check_launch("k_synthesis(level 1)");
+    return check_launch("k_synth_tma(level 1)");
 }
 
 template <typename TIn>
 int run_residual_accumulate(const TIn* in, const TIn* I, int nb, int H, int W, const Pyramid& p,
                             const ShrinkParams& sp, double* num, double* den, float* ws_pyr, cudaStream_t st) {
     PyramidBuffers pb = carve_pyramid(p, ws_pyr, nb);
-    SynthArgs s{};
-    int rc = denoise_front<TIn>(in, (long long)H * W, W, nb, p, pb, sp, st, &s);
+    int rc = denoise_front<TIn>(in, (long long)H * W, W, nb, p, pb, sp, st);
     if (rc) return rc;
+    SynthMaps m;
+    if ((rc = synth_maps(p, pb, 1, nb, p.levels > 1, &m))) return rc;
+    SynthArgs s{};
+    s.has_A = p.levels > 1;
+    s.NH = H;
+    s.NW = W;
+    s.nb = nb;
+    s.I = I;
+    s.i_bstride = (long long)H * W;
+    s.i_pitch = W;
+    s.num = num;
+    s.den = den;
+    s.acc_pitch = W;
     dim3 grid((W + ST_X - 1) / ST_X, (H + ST_Y - 1) / ST_Y, 1);
     {
         KTimer kt(sizeof(TIn) == 1 ? "synth_acc_l1_u8" : "synth_acc_l1_f32", st);
-        k_synthesis_accumulate<TIn><<<grid, 256, S_SMEM_BYTES, st>>>(s, I, (long long)H * W, W, nb, num, den, W);
+        k_synth_tma<1, TIn><<<grid, 256, S_SMEM_BYTES, st>>>(m, s);
     }
     count_launch();
-    return check_launch("k_synthesis_accumulate");
+    return check_launch("k_synth_tma(accumulate)");
 }
 
 template int run_residual<float>(const float*, int, int, int, const Pyramid&, const ShrinkParams&, float*, float*,
