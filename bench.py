@@ -79,6 +79,11 @@ def max_over_ranks(x: float, world: int) -> float:
     return float(t.item())
 
 
+def job_throughput(units_per_step: float, steps: int, world: int, ms_max: float) -> float:
+    """Whole-job throughput: units every rank processed / the slowest rank's time."""
+    return units_per_step * steps * world / (ms_max / 1000.0)
+
+
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
     """Samples SM clock + throttle reasons with NVML every 20 ms while active."""
@@ -303,7 +308,7 @@ def main():
     ms_max = max_over_ranks(ms, world)
     ms_step = ms_max / args.steps
     denoise_per_step = sum(n_sda.values())
-    value = denoise_per_step * args.steps * world / (ms_max / 1000.0)
+    value = job_throughput(denoise_per_step, args.steps, world, ms_max)
     pce_vals = res.pce.cpu().tolist()
 
     # ---- per-kernel event timing over the same K steps (separate pass)
