@@ -27,7 +27,7 @@ namespace prnu {
 constexpr int AT = 32;                  // output coefficient tile (square)
 constexpr int AR = AT + 2 * kHalo;      // 40: computed coefficient region
 constexpr int AIN = 2 * AR + 6;         // 86: input rows / columns of the region
-constexpr int IN_P = 100;               // input tile pitch (== 4 mod 32: conflict-free LDS.128, row-major lanes)
+constexpr int IN_P = 92;                // input tile pitch (== 28 mod 32: conflict-free LDS.128, row-major lanes)
 constexpr int RW_P = 44;                // row-pass plane pitch (== 12 mod 32)
 constexpr int DT_P = AR;                // detail plane pitch
 constexpr int V_P4 = AR + 1;            // vertical-sum plane pitch in float4 (41*4 == 4 mod 32)
@@ -155,7 +155,9 @@ __global__ void __launch_bounds__(256, 3) k_analysis_shrink(AnalysisArgs a) {
     //         item = (column, 8 coefficient rows) from 22 rows of lo and hi
     float* s_det = s_in;
     for (int it = tid; it < AR * (AR / 8); it += 256) {
-        const int c = it % AR, rg = it / AR;
+        // warps cover 32 consecutive columns of one row group (no bank-shifted wrap)
+        const int c = it < 32 * (AR / 8) ? (it & 31) : 32 + ((it - 32 * (AR / 8)) % (AR - 32));
+        const int rg = it < 32 * (AR / 8) ? (it >> 5) : (it - 32 * (AR / 8)) / (AR - 32);
         float lo[22], hi[22];
 #pragma unroll
         for (int k = 0; k < 22; ++k) {
@@ -195,7 +197,8 @@ __global__ void __launch_bounds__(256, 3) k_analysis_shrink(AnalysisArgs a) {
         const float* det = s_det + s * AR * DT_P;
         // stage V: columns x in [0,AR) that are real, output rows 8*ig .. 8*ig+7
         for (int it = tid; it < AR * (AT / 8); it += 256) {
-            const int x = it % AR, ig = it / AR;
+            const int x = it < 32 * (AT / 8) ? (it & 31) : 32 + ((it - 32 * (AT / 8)) % (AR - 32));
+            const int ig = it < 32 * (AT / 8) ? (it >> 5) : (it - 32 * (AT / 8)) / (AR - 32);
             if (border_x && s_cmap[x] != x) continue;
             float q[16];
 #pragma unroll
