@@ -38,7 +38,7 @@ def parse():
     ap.add_argument("--height", type=int, default=1080)
     ap.add_argument("--width", type=int, default=1920)
     ap.add_argument("--depths", default="1,50")
-    ap.add_argument("--batch", type=int, default=16, help="SDA frames denoised per wave at depth 1")
+    ap.add_argument("--batch", type=int, default=32, help="SDA frames denoised per wave at depth 1")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
@@ -311,7 +311,8 @@ def main():
     value = job_throughput(denoise_per_step, args.steps, world, ms_max)
     pce_vals = res.pce.cpu().tolist()
 
-    # ---- per-kernel event timing over the same K steps (separate pass)
+    # ---- per-kernel event timing over the same K steps (separate pass; the
+    #      library serialises its waves while timing so each kernel is measured alone)
     roof, kernels = None, None
     if not args.no_profile:
         prnu._lib.prnu_profile_begin()

@@ -18,6 +18,8 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", 
          "-I" + os.path.join(ROOT, "include")]
 if os.environ.get("PRNU_DEBUG"):
     FLAGS.append("-DPRNU_DEBUG")
+for _flag in os.environ.get("PRNU_NVCC_DEFS", "").split():
+    FLAGS.append("-D" + _flag)
 
 
 def _stale(target: str, deps) -> bool:

@@ -2,6 +2,7 @@
 // Validation happens here, synchronously, before anything is launched; the
 // kernels live in sda.cu / wavelet.cu / mle.cu / pce.cu.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -62,6 +63,11 @@ KTimer::~KTimer() {
     if (slot < (int)g_prof.size()) cudaEventRecord(g_prof[slot].b, st);
 }
 
+bool profiling_active() {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    return g_prof_on;
+}
+
 int validate_params(const prnu_denoise_params* p, int H, int W, ShrinkParams* sp) {
     if (!p) return fail(PRNU_INVALID_ARG, "params is NULL");
     if (!(p->sigma0_sq > 0.0f) || !(p->sigma0_sq < 3.0e38f)) return fail(PRNU_BAD_PARAMETER, "sigma0_sq must be > 0");
@@ -91,7 +97,8 @@ int run_residual(const TIn* in, int nb, int H, int W, const Pyramid& p, const Sh
                  float* ws_pyr, cudaStream_t st);
 template <typename TIn>
 int run_residual_accumulate(const TIn* in, const TIn* I, int nb, int H, int W, const Pyramid& p,
-                            const ShrinkParams& sp, double* num, double* den, float* ws_pyr, cudaStream_t st);
+                            const ShrinkParams& sp, double* num, double* den, float* ws_pyr, cudaStream_t st,
+                            cudaEvent_t acc_wait, cudaEvent_t acc_done);
 int launch_accumulate(const float* W, const float* I, int batch, long long P, double* num, double* den,
                       cudaStream_t st);
 size_t zm_workspace_bytes(int H, int W);
@@ -112,11 +119,26 @@ static size_t residual_ws(int batch, int H, int W, const Pyramid& pyr) {
     return align_up(sizeof(float) * pyramid_floats_per_frame(pyr) * (size_t)batch, 256) + zm_workspace_bytes(H, W);
 }
 
-static size_t extract_ws(int H, int W, int batch, int64_t depth, const Pyramid& pyr) {
+// Waves of SDA frames alternate between kExtractStreams streams (each with its
+// own pyramid/SDA workspace) so one wave's small levels overlap the next wave's
+// large ones; only the accumulating launches are chained (ascending order).
+static int extract_streams() {
+    static const int n = [] {
+        const char* e = getenv("PRNU_STREAMS");
+        int v = e ? atoi(e) : 2;
+        return v < 1 ? 1 : (v > 2 ? 2 : v);
+    }();
+    return n;
+}
+
+static size_t extract_wave_ws(int H, int W, int batch, int64_t depth, const Pyramid& pyr) {
     size_t s = align_up(sizeof(float) * pyramid_floats_per_frame(pyr) * (size_t)batch, 256);
     if (depth > 1) s += align_up(sizeof(float) * (size_t)H * W * batch, 256);
-    s += zm_workspace_bytes(H, W);
     return s;
+}
+
+static size_t extract_ws(int H, int W, int batch, int64_t depth, const Pyramid& pyr) {
+    return extract_streams() * extract_wave_ws(H, W, batch, depth, pyr) + zm_workspace_bytes(H, W);
 }
 
 static int check_dims(int H, int W) {
@@ -125,18 +147,20 @@ static int check_dims(int H, int W) {
     return PRNU_OK;
 }
 
-// Shared by the device and host extraction entry points: process SDA groups
-// [g0, g0+nb) whose frames start at `frames` (device).
+// Shared by the device and host extraction entry points: process nb SDA groups
+// whose frames start at `frames` (device), with wave workspace `ws`.
 static int extract_chunk(const uint8_t* frames, int64_t nb, int H, int W, int64_t depth, const Pyramid& pyr,
-                         const ShrinkParams& sp, double* num, double* den, char* ws, cudaStream_t st) {
+                         const ShrinkParams& sp, double* num, double* den, char* ws, cudaStream_t st,
+                         cudaEvent_t acc_wait = nullptr, cudaEvent_t acc_done = nullptr) {
     float* pyr_ws = reinterpret_cast<float*>(ws);
     size_t pyr_bytes = align_up(sizeof(float) * pyramid_floats_per_frame(pyr) * (size_t)nb, 256);
     if (depth == 1)
-        return run_residual_accumulate<uint8_t>(frames, frames, (int)nb, H, W, pyr, sp, num, den, pyr_ws, st);
+        return run_residual_accumulate<uint8_t>(frames, frames, (int)nb, H, W, pyr, sp, num, den, pyr_ws, st,
+                                                acc_wait, acc_done);
     float* S = reinterpret_cast<float*>(ws + pyr_bytes);
     int rc = launch_sda_average(frames, nb, (long long)H * W, (int)depth, S, st);
     if (rc) return rc;
-    return run_residual_accumulate<float>(S, S, (int)nb, H, W, pyr, sp, num, den, pyr_ws, st);
+    return run_residual_accumulate<float>(S, S, (int)nb, H, W, pyr, sp, num, den, pyr_ws, st, acc_wait, acc_done);
 }
 
 template <typename TIn>
@@ -266,13 +290,51 @@ int prnu_extract_fingerprint(const uint8_t* frames, int64_t m, int H, int W, int
     cudaError_t e2 = cudaMemsetAsync(sum_I2, 0, sizeof(double) * P, st);
     if (e1 != cudaSuccess || e2 != cudaSuccess) return fail(PRNU_CUDA_ERROR, "cudaMemsetAsync failed");
     char* wsb = reinterpret_cast<char*>(ws);
-    for (int64_t g0 = 0; g0 < ns; g0 += batch) {
-        int64_t nb = std::min<int64_t>(batch, ns - g0);
-        if ((rc = extract_chunk(frames + (size_t)g0 * depth * P, nb, H, W, depth, pyr, sp, sum_WI, sum_I2, wsb, st)))
-            return rc;
+    // per-kernel timing (prnu_profile_begin) serialises the waves so that each
+    // kernel's event pair measures that kernel alone
+    const int nst = extract_streams();
+    const bool serial = profiling_active();
+    const size_t wave = extract_wave_ws(H, W, batch, depth, pyr);
+    char* zm = wsb + nst * wave;
+    if (nst == 1 || serial || ns <= batch) {
+        for (int64_t g0 = 0; g0 < ns; g0 += batch) {
+            int64_t nb = std::min<int64_t>(batch, ns - g0);
+            if ((rc = extract_chunk(frames + (size_t)g0 * depth * P, nb, H, W, depth, pyr, sp, sum_WI, sum_I2, wsb,
+                                    st)))
+                return rc;
+        }
+        return launch_finalize(sum_WI, sum_I2, H, W, eps, 1, K_out, zm, st);
     }
-    char* zm = wsb + extract_ws(H, W, batch, depth, pyr) - zm_workspace_bytes(H, W);
-    return launch_finalize(sum_WI, sum_I2, H, W, eps, 1, K_out, zm, st);
+    // two streams: waves alternate; accumulations chained by events
+    cudaStream_t s1 = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_end = nullptr, acc[2] = {nullptr, nullptr};
+    cudaError_t e = cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_end, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&acc[0], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&acc[1], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(ev_start, st);            // s1 starts after the caller's prior work
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s1, ev_start, 0);
+    rc = (e == cudaSuccess) ? PRNU_OK : fail(PRNU_CUDA_ERROR, std::string("stream setup: ") + cudaGetErrorString(e));
+    cudaStream_t sts[2] = {st, s1};
+    int64_t k = 0;
+    for (int64_t g0 = 0; g0 < ns && rc == PRNU_OK; g0 += batch, ++k) {
+        int64_t nb = std::min<int64_t>(batch, ns - g0);
+        const int j = (int)(k & 1);
+        rc = extract_chunk(frames + (size_t)g0 * depth * P, nb, H, W, depth, pyr, sp, sum_WI, sum_I2,
+                           wsb + j * wave, sts[j], k > 0 ? acc[j ^ 1] : nullptr, acc[j]);
+    }
+    if (rc == PRNU_OK) {
+        e = cudaEventRecord(ev_end, s1);                               // the caller's stream sees all waves
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev_end, 0);
+        if (e != cudaSuccess) rc = fail(PRNU_CUDA_ERROR, std::string("stream join: ") + cudaGetErrorString(e));
+    }
+    if (rc == PRNU_OK) rc = launch_finalize(sum_WI, sum_I2, H, W, eps, 1, K_out, zm, st);
+    // destroying a stream/event with pending work is legal: resources are released on completion
+    if (s1) cudaStreamDestroy(s1);
+    for (cudaEvent_t ev : {ev_start, ev_end, acc[0], acc[1]})
+        if (ev) cudaEventDestroy(ev);
+    return rc;
 }
 
 size_t prnu_extract_host_workspace_bytes(int H, int W, int batch, int64_t depth, const prnu_denoise_params* p) {

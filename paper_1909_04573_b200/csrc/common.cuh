@@ -46,6 +46,8 @@ struct KTimer {
     ~KTimer();
 };
 
+bool profiling_active();
+
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -71,6 +73,18 @@ __host__ __device__ __forceinline__ constexpr float wl_h(int i) {
 }
 __host__ __device__ __forceinline__ constexpr float wl_g(int i) {
     return (i & 1) ? -wl_h(7 - i) : wl_h(7 - i);
+}
+
+// Packed fp32 FMA (sm_100a FFMA2): lane-wise RN fma, bit-identical to two fmaf.
+// A scalar first operand is broadcast to both lanes by the instruction itself.
+__device__ __forceinline__ float2 ffma2(float a, float2 b, float2 c) {
+    const float2 aa = make_float2(a, a);
+    unsigned long long ra = *reinterpret_cast<const unsigned long long*>(&aa);
+    unsigned long long rb = *reinterpret_cast<const unsigned long long*>(&b);
+    unsigned long long rc = *reinterpret_cast<const unsigned long long*>(&c);
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(ra), "l"(rb), "l"(rc));
+    return *reinterpret_cast<float2*>(&r);
 }
 
 // subband length of the expansive symmetric DWT: floor((N + 7) / 2)

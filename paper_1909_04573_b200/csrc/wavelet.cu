@@ -16,6 +16,8 @@
 //
 // Filters are compile-time immediates (FFMA-imm).  fp32 arithmetic; the
 // accumulators are fp64.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "tma.cuh"
 
@@ -29,13 +31,20 @@ constexpr int AR = AT + 2 * kHalo;      // 40: computed coefficient region
 constexpr int AIN = 2 * AR + 6;         // 86: input rows / columns of the region
 constexpr int IN_P = 92;                // input tile pitch (== 28 mod 32: conflict-free LDS.128, row-major lanes)
 constexpr int RW_P = 44;                // row-pass plane pitch (== 12 mod 32)
-constexpr int DT_P = AR;                // detail plane pitch
+constexpr int RW_PLANE = AIN * RW_P + 48;   // one row-pass plane incl. the row-block skew (<= 8*5)
+constexpr int DT_P = AR + 1;            // detail plane pitch (odd: conflict-free column walks)
 constexpr int V_P4 = AR + 1;            // vertical-sum plane pitch in float4 (41*4 == 4 mod 32)
+constexpr int V_PLANE4 = AT * V_P4;     // float4 per vertical-sum buffer
 constexpr int A_SMEM_IN = AIN * IN_P;             // input tile; later the 3 detail planes
-constexpr int A_SMEM_ROW = 2 * AIN * RW_P;        // row-pass lo/hi; later the vertical sums
+constexpr int A_SMEM_ROW = 2 * V_PLANE4 * 4;      // row-pass lo/hi; later two vertical-sum buffers
 constexpr size_t A_SMEM_BYTES = sizeof(float) * (A_SMEM_IN + A_SMEM_ROW) + sizeof(int) * (2 * AIN + 2 * AR);
 static_assert(3 * AR * DT_P <= A_SMEM_IN, "detail planes must fit in the input tile");
-static_assert(AT * V_P4 * 4 <= A_SMEM_ROW, "vertical sums must fit in the row-pass planes");
+static_assert(2 * RW_PLANE <= A_SMEM_ROW, "row-pass planes must fit");
+
+// Row r of a row-pass plane starts at r*RW_P plus a skew of 8 floats per block
+// of 16 rows (monotonic: rows never overlap), so column walks of different row groups (16 rows apart) fall in
+// different banks; the 16-byte alignment of row-pass stores is kept.
+__device__ __forceinline__ int rw_off(int r) { return r * RW_P + 8 * (r >> 4); }
 
 struct AnalysisArgs {
     const void* in;
@@ -52,41 +61,266 @@ struct AnalysisArgs {
     ShrinkParams sp;
 };
 
-template <typename TIn>
-__global__ void __launch_bounds__(256, 3) k_analysis_shrink(AnalysisArgs a) {
-    extern __shared__ __align__(16) float smem[];
-    float* s_in = smem;                          // [AIN][IN_P]; later details [3][AR][DT_P]
-    float* s_row = smem + A_SMEM_IN;             // [2][AIN][RW_P]; later vertical sums [AT][V_P4] float4
-    int* s_iy = reinterpret_cast<int*>(s_row + A_SMEM_ROW);   // [AIN] mirrored input row
-    int* s_ix = s_iy + AIN;                                   // [AIN] mirrored input col
-    int* s_rmap = s_ix + AIN;                                 // [AR] mirrored region row (local)
-    int* s_cmap = s_rmap + AR;                                // [AR] mirrored region col (local)
+// Geometry of one analysis tile.
+struct ATile {
+    int b, y0, x0, cy0, cx0;
+    bool bx, by;   // the window region crosses a subband border (mirrored reads)
+};
 
-    const int tid = threadIdx.x;
-    const int lane = tid & 31, warp = tid >> 5;
-    const int b = blockIdx.z;
-    const int y0 = blockIdx.y * AT, x0 = blockIdx.x * AT;
-    const int cy0 = y0 - kHalo, cx0 = x0 - kHalo;
-    const TIn* in = reinterpret_cast<const TIn*>(a.in) + (size_t)b * a.in_bstride;
+__device__ __forceinline__ ATile analysis_tile(const AnalysisArgs& a, int b, int ty, int tx) {
+    ATile g;
+    g.b = b;
+    g.y0 = ty * AT;
+    g.x0 = tx * AT;
+    g.cy0 = g.y0 - kHalo;
+    g.cx0 = g.x0 - kHalo;
+    g.bx = (g.cx0 < 0) || (g.cx0 + AR > a.nW);
+    g.by = (g.cy0 < 0) || (g.cy0 + AR > a.nH);
+    return g;
+}
 
-    for (int i = tid; i < AIN; i += 256) {
-        s_iy[i] = mirror(2 * cy0 - 6 + i, a.NH);
-        s_ix[i] = mirror(2 * cx0 - 6 + i, a.NW);
+// Mirror tables of a tile (R-4): input rows/cols of the AIN x AIN tile and the
+// region rows/cols the shrink windows read.  Window rows/cols of every output
+// inside the plane mirror into the region; indices that only feed discarded
+// outputs (beyond the plane) are clamped.  Caller synchronises.
+__device__ __forceinline__ void analysis_tables(const AnalysisArgs& a, const ATile& g, int* s_iy, int* s_ix,
+                                                int* s_rmap, int* s_cmap) {
+    for (int i = threadIdx.x; i < AIN; i += 256) {
+        s_iy[i] = mirror(2 * g.cy0 - 6 + i, a.NH);
+        s_ix[i] = mirror(2 * g.cx0 - 6 + i, a.NW);
     }
-    for (int i = tid; i < AR; i += 256) {
-        // Window rows/cols of every output inside the plane mirror into the region;
-        // indices that only feed discarded outputs (beyond the plane) are clamped.
-        int mr = mirror(cy0 + i, a.nH) - cy0;
-        int mc = mirror(cx0 + i, a.nW) - cx0;
+    for (int i = threadIdx.x; i < AR; i += 256) {
+        const int mr = mirror(g.cy0 + i, a.nH) - g.cy0;
+        const int mc = mirror(g.cx0 + i, a.nW) - g.cx0;
         s_rmap[i] = (mr >= 0 && mr < AR) ? mr : i;
         s_cmap[i] = (mc >= 0 && mc < AR) ? mc : i;
     }
-    // tile touches a border of the subband plane -> mirrored window reads needed
-    const bool border_x = (cx0 < 0) || (cx0 + AR > a.nW);
-    const bool border_y = (cy0 < 0) || (cy0 + AR > a.nH);
-    __syncthreads();
+}
 
-    // ---- 1. mirrored input tile: warp w loads rows w, w+8, ...; all loads in flight first
+// Row pass (along x) of the 8 coefficient columns 8cg..8cg+7 of input row r,
+// from 24 consecutive input values v (only v[0..21] contribute).
+__device__ __forceinline__ void rowpass_item(const float (&v)[24], float* s_row, int r, int cg) {
+    float lo[8], hi[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        float2 lh = make_float2(0.f, 0.f);   // (lo, hi) in one FFMA2 per tap
+#pragma unroll
+        for (int i = 0; i < 8; ++i) lh = ffma2(v[2 * q + i], make_float2(wl_h(i), wl_g(i)), lh);
+        lo[q] = lh.x;
+        hi[q] = lh.y;
+    }
+    float4* dl = reinterpret_cast<float4*>(s_row + rw_off(r) + 8 * cg);
+    float4* dh = reinterpret_cast<float4*>(s_row + RW_PLANE + rw_off(r) + 8 * cg);
+    dl[0] = make_float4(lo[0], lo[1], lo[2], lo[3]);
+    dl[1] = make_float4(lo[4], lo[5], lo[6], lo[7]);
+    dh[0] = make_float4(hi[0], hi[1], hi[2], hi[3]);
+    dh[1] = make_float4(hi[4], hi[5], hi[6], hi[7]);
+}
+
+// fp32 input tile [AIN][IN_P]: item = (row, 8 coefficient columns), 6 LDS.128
+__device__ __forceinline__ void rowpass_f32(const float* s_in, float* s_row) {
+    for (int it = threadIdx.x; it < AIN * (AR / 8); it += 256) {
+        const int r = it % AIN, cg = it / AIN;
+        const float4* src = reinterpret_cast<const float4*>(s_in + r * IN_P + 16 * cg);
+        float v[24];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            const float4 t = src[k];
+            v[4 * k] = t.x;
+            v[4 * k + 1] = t.y;
+            v[4 * k + 2] = t.z;
+            v[4 * k + 3] = t.w;
+        }
+        rowpass_item(v, s_row, r, cg);
+    }
+}
+
+// u8 input tile [AIN][U8_P] bytes: one LDS.128 + one LDS.64 per item; bytes are
+// widened exactly with the 2^23 trick: float(0x4B0000bb) - 2^23 = bb.
+constexpr int U8_P = 112;   // 28 words == 28 mod 32: conflict-free LDS.128 for row-major lanes
+__device__ __forceinline__ float u8_to_f32(uint32_t w, int k) {
+    return __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7540u | (uint32_t)k)) - 8388608.0f;
+}
+// The u8 tile row starts U8_OFF bytes before input column 2*cx0-6: u8 TMA boxes
+// must start on a 16-byte boundary (measured: other x offsets fault).
+constexpr int U8_OFF = 2;
+__device__ __forceinline__ void rowpass_u8(const uint8_t* s_in8, float* s_row) {
+    for (int it = threadIdx.x; it < AIN * (AR / 8); it += 256) {
+        const int r = it % AIN, cg = it / AIN;
+        const uint8_t* src = s_in8 + r * U8_P + 16 * cg;
+        const uint4 w0 = *reinterpret_cast<const uint4*>(src);
+        const uint2 w1 = *reinterpret_cast<const uint2*>(src + 16);
+        const uint32_t w[6] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y};
+        float v[24];
+#pragma unroll
+        for (int k = 0; k < 22; ++k) v[k] = u8_to_f32(w[(k + U8_OFF) >> 2], (k + U8_OFF) & 3);
+        v[22] = v[23] = 0.f;
+        rowpass_item(v, s_row, r, cg);
+    }
+}
+
+// Column pass (along y): 4 subbands for the AR x AR region; item = (column,
+// 8 coefficient rows) from 22 rows of lo and hi.  Details -> s_det, the inner
+// approximation -> global (next level's input).
+__device__ __forceinline__ void colpass(const AnalysisArgs& a, const ATile& g, const float* s_row, float* s_det) {
+    for (int it = threadIdx.x; it < AR * (AR / 8); it += 256) {
+        // warps cover 32 consecutive columns of one row group (no bank-shifted wrap)
+        const int c = it < 32 * (AR / 8) ? (it & 31) : 32 + ((it - 32 * (AR / 8)) % (AR - 32));
+        const int rg = it < 32 * (AR / 8) ? (it >> 5) : (it - 32 * (AR / 8)) / (AR - 32);
+        float lo[22], hi[22];
+#pragma unroll
+        for (int k = 0; k < 22; ++k) {
+            lo[k] = s_row[rw_off(16 * rg + k) + c];
+            hi[k] = s_row[RW_PLANE + rw_off(16 * rg + k) + c];
+        }
+        const bool inner_c = (c >= kHalo) && (c < kHalo + AT) && (g.x0 + c - kHalo < a.nW);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            float2 p_l = make_float2(0.f, 0.f), p_h = make_float2(0.f, 0.f);   // (aa, ad), (da, dd)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                p_l = ffma2(lo[2 * q + i], make_float2(wl_h(i), wl_g(i)), p_l);
+                p_h = ffma2(hi[2 * q + i], make_float2(wl_h(i), wl_g(i)), p_h);
+            }
+            const float aa = p_l.x, ad = p_l.y, da = p_h.x, dd = p_h.y;
+            const int rr = 8 * rg + q;
+            s_det[0 * AR * DT_P + rr * DT_P + c] = da;
+            s_det[1 * AR * DT_P + rr * DT_P + c] = ad;
+            s_det[2 * AR * DT_P + rr * DT_P + c] = dd;
+            if (a.ll != nullptr && inner_c && rr >= kHalo && rr < kHalo + AT) {
+                const int gy = g.y0 + rr - kHalo;
+                if (gy < a.nH) a.ll[(size_t)g.b * a.out_bstride + (size_t)gy * a.out_pitch + g.x0 + c - kHalo] = aa;
+            }
+        }
+    }
+}
+
+// Shrink of the three detail subbands (R-7): separable window sums of
+// c^2 — vertical (per column, 8 rows per item, nested 3/5/7/9) into a float4
+// plane, then horizontal (per row, 8 columns per item, sliding sums) — and the
+// Wiener factor; writes the noise-domain coefficients c sigma0^2/(v+sigma0^2).
+// Two vertical-sum buffers pipeline the subbands: phases V0 | H0+V1 | H1+V2 | H2.
+// Starts after a barrier that made s_det complete; ends with a barrier.
+__device__ __forceinline__ void shrink_v(const ATile& g, const float* det, float4* s_v, const int* s_rmap,
+                                         const int* s_cmap, int it) {
+    const int x = it < 32 * (AT / 8) ? (it & 31) : 32 + ((it - 32 * (AT / 8)) % (AR - 32));
+    const int ig = it < 32 * (AT / 8) ? (it >> 5) : (it - 32 * (AT / 8)) / (AR - 32);
+    if (g.bx && s_cmap[x] != x) return;
+    float q[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const int rr = g.by ? s_rmap[8 * ig + k] : 8 * ig + k;
+        const float c = det[rr * DT_P + x];
+        q[k] = __fmul_rn(c, c);   // no contraction into the sums: identical in every kernel
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        const float v3 = q[t + 3] + q[t + 4] + q[t + 5];
+        const float v5 = v3 + q[t + 2] + q[t + 6];
+        const float v7 = v5 + q[t + 1] + q[t + 7];
+        const float v9 = v7 + q[t] + q[t + 8];
+        s_v[(8 * ig + t) * V_P4 + x] = make_float4(v3, v5, v7, v9);
+    }
+}
+
+__device__ __forceinline__ void shrink_h(const AnalysisArgs& a, const ATile& g, const float* det, const float4* s_v,
+                                         const int* s_cmap, float* dst, int it) {
+    const float s0 = a.sp.sigma0_sq;
+    const int wm = a.sp.wmask;
+    const int i = it % AT, jg = it / AT;
+    const int gy = g.y0 + i;
+    float4 u[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const int xx = g.bx ? s_cmap[8 * jg + k] : 8 * jg + k;
+        u[k] = s_v[i * V_P4 + xx];
+    }
+    const float* crow = det + (i + kHalo) * DT_P + 8 * jg + kHalo;
+    float s3 = u[3].x + u[4].x + u[5].x;
+    float s5 = u[2].y + u[3].y + u[4].y + u[5].y + u[6].y;
+    float s7 = u[1].z + u[2].z + u[3].z + u[4].z + u[5].z + u[6].z + u[7].z;
+    float s9 = u[0].w + u[1].w + u[2].w + u[3].w + u[4].w + u[5].w + u[6].w + u[7].w + u[8].w;
+    float o[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        if (t > 0) {   // slide the windows one column right
+            s3 += u[t + 5].x - u[t + 2].x;
+            s5 += u[t + 6].y - u[t + 1].y;
+            s7 += u[t + 7].z - u[t].z;
+            s9 += u[t + 8].w - u[t - 1].w;
+        }
+        float m = 3.402823466e38f;
+        if (wm & 1) m = fminf(m, s3 * (1.0f / 9.0f));
+        if (wm & 2) m = fminf(m, s5 * (1.0f / 25.0f));
+        if (wm & 4) m = fminf(m, s7 * (1.0f / 49.0f));
+        if (wm & 8) m = fminf(m, s9 * (1.0f / 81.0f));
+        const float var = fmaxf(m - s0, 0.0f);
+        o[t] = crow[t] * __fdividef(s0, var + s0);   // noise-domain coefficient c - F(c)
+    }
+    if (gy < a.nH) {
+        const int gx = g.x0 + 8 * jg;
+        float* drow = dst + (size_t)gy * a.out_pitch + gx;
+        if (gx + 8 <= a.nW) {
+            reinterpret_cast<float4*>(drow)[0] = make_float4(o[0], o[1], o[2], o[3]);
+            reinterpret_cast<float4*>(drow)[1] = make_float4(o[4], o[5], o[6], o[7]);
+        } else {
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+                if (gx + t < a.nW) drow[t] = o[t];
+        }
+    }
+}
+
+__device__ __forceinline__ void shrink3(const AnalysisArgs& a, const ATile& g, const float* s_det, float4* s_v,
+                                        const int* s_rmap, const int* s_cmap) {
+    constexpr int VI = AR * (AT / 8);   // 160 vertical items per subband
+    constexpr int HI = AT * (AT / 8);   // 128 horizontal items per subband
+    const int tid = threadIdx.x;
+#ifdef PRNU_SEQ_SHRINK
+#pragma unroll 1
+    for (int s = 0; s < 3; ++s) {
+        for (int it = tid; it < VI; it += 256) shrink_v(g, s_det + s * AR * DT_P, s_v, s_rmap, s_cmap, it);
+        __syncthreads();
+        for (int it = tid; it < HI; it += 256)
+            shrink_h(a, g, s_det + s * AR * DT_P, s_v, s_cmap,
+                     (s == 0 ? a.d0 : s == 1 ? a.d1 : a.d2) + (size_t)g.b * a.out_bstride, it);
+        __syncthreads();
+    }
+    return;
+#endif
+    for (int it = tid; it < VI; it += 256) shrink_v(g, s_det, s_v, s_rmap, s_cmap, it);
+    __syncthreads();
+#pragma unroll 1
+    for (int s = 0; s < 3; ++s) {
+        // H of subband s (buffer s&1) together with V of subband s+1 (buffer (s+1)&1)
+        const int n = HI + (s < 2 ? VI : 0);
+        for (int it = tid; it < n; it += 256) {
+            if (it < HI)
+                shrink_h(a, g, s_det + s * AR * DT_P, s_v + (s & 1) * V_PLANE4, s_cmap,
+                         (s == 0 ? a.d0 : s == 1 ? a.d1 : a.d2) + (size_t)g.b * a.out_bstride, it);
+            else
+                shrink_v(g, s_det + (s + 1) * AR * DT_P, s_v + ((s + 1) & 1) * V_PLANE4, s_rmap, s_cmap, it - HI);
+        }
+        __syncthreads();
+    }
+}
+
+// Generic analysis kernel: one tile per CTA, mirrored input loaded with
+// ordinary loads (all in flight before the first shared store).
+template <typename TIn>
+__global__ void __launch_bounds__(256, 3) k_analysis_shrink(AnalysisArgs a) {
+    extern __shared__ __align__(128) float smem[];
+    float* s_in = smem;                          // [AIN][IN_P]; later details [3][AR][DT_P]
+    float* s_row = smem + A_SMEM_IN;             // [2][AIN][RW_P]; later vertical sums [AT][V_P4] float4
+    int* s_iy = reinterpret_cast<int*>(s_row + A_SMEM_ROW);
+    int* s_ix = s_iy + AIN;
+    int* s_rmap = s_ix + AIN;
+    int* s_cmap = s_rmap + AR;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const ATile g = analysis_tile(a, blockIdx.z, blockIdx.y, blockIdx.x);
+    const TIn* in = reinterpret_cast<const TIn*>(a.in) + (size_t)g.b * a.in_bstride;
+    analysis_tables(a, g, s_iy, s_ix, s_rmap, s_cmap);
+    __syncthreads();
     {
         constexpr int RPW = (AIN + 7) / 8;   // 11 rows per warp
         float v[RPW][3];
@@ -95,180 +329,107 @@ __global__ void __launch_bounds__(256, 3) k_analysis_shrink(AnalysisArgs a) {
         for (int j = 0; j < 3; ++j) ixs[j] = s_ix[min(lane + 32 * j, AIN - 1)];
 #pragma unroll
         for (int k = 0; k < RPW; ++k) {
-            int r = warp + 8 * k;
-            const TIn* row = in + (size_t)s_iy[min(r, AIN - 1)] * a.in_pitch;
+            const TIn* row = in + (size_t)s_iy[min(warp + 8 * k, AIN - 1)] * a.in_pitch;
 #pragma unroll
-            for (int j = 0; j < 3; ++j) {
-                PRNU_DCHECK(s_iy[min(r, AIN - 1)] >= 0 && s_iy[min(r, AIN - 1)] < a.NH && ixs[j] >= 0 && ixs[j] < a.NW);
-                v[k][j] = (float)__ldg(row + ixs[j]);
-            }
+            for (int j = 0; j < 3; ++j) v[k][j] = (float)__ldg(row + ixs[j]);
         }
 #pragma unroll
         for (int k = 0; k < RPW; ++k) {
-            int r = warp + 8 * k;
+            const int r = warp + 8 * k;
 #pragma unroll
             for (int j = 0; j < 3; ++j) {
-                int c = lane + 32 * j;
+                const int c = lane + 32 * j;
                 if (r < AIN && c < AIN) s_in[r * IN_P + c] = v[k][j];
             }
         }
     }
     __syncthreads();
-
-    // ---- 2. row pass (along x): lo/hi of AR coefficient columns for every input row;
-    //         item = (row, 8 coefficient columns), 24 inputs via 6 LDS.128
-    for (int it = tid; it < AIN * (AR / 8); it += 256) {
-        const int r = it % AIN, cg = it / AIN;
-        PRNU_DCHECK(r * IN_P + 16 * cg + 23 < A_SMEM_IN);
-        const float4* src = reinterpret_cast<const float4*>(s_in + r * IN_P + 16 * cg);
-        float v[24];
-#pragma unroll
-        for (int k = 0; k < 6; ++k) {
-            float4 t = src[k];
-            v[4 * k] = t.x;
-            v[4 * k + 1] = t.y;
-            v[4 * k + 2] = t.z;
-            v[4 * k + 3] = t.w;
-        }
-        float lo[8], hi[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            float l = 0.f, h = 0.f;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                l = fmaf(wl_h(i), v[2 * q + i], l);
-                h = fmaf(wl_g(i), v[2 * q + i], h);
-            }
-            lo[q] = l;
-            hi[q] = h;
-        }
-        float4* dl = reinterpret_cast<float4*>(s_row + r * RW_P + 8 * cg);
-        float4* dh = reinterpret_cast<float4*>(s_row + AIN * RW_P + r * RW_P + 8 * cg);
-        dl[0] = make_float4(lo[0], lo[1], lo[2], lo[3]);
-        dl[1] = make_float4(lo[4], lo[5], lo[6], lo[7]);
-        dh[0] = make_float4(hi[0], hi[1], hi[2], hi[3]);
-        dh[1] = make_float4(hi[4], hi[5], hi[6], hi[7]);
-    }
+    rowpass_f32(s_in, s_row);
     __syncthreads();
-
-    // ---- 3. column pass (along y): 4 subbands for AR x AR coefficients;
-    //         item = (column, 8 coefficient rows) from 22 rows of lo and hi
     float* s_det = s_in;
-    for (int it = tid; it < AR * (AR / 8); it += 256) {
-        // warps cover 32 consecutive columns of one row group (no bank-shifted wrap)
-        const int c = it < 32 * (AR / 8) ? (it & 31) : 32 + ((it - 32 * (AR / 8)) % (AR - 32));
-        const int rg = it < 32 * (AR / 8) ? (it >> 5) : (it - 32 * (AR / 8)) / (AR - 32);
-        float lo[22], hi[22];
-#pragma unroll
-        for (int k = 0; k < 22; ++k) {
-            lo[k] = s_row[(16 * rg + k) * RW_P + c];
-            hi[k] = s_row[AIN * RW_P + (16 * rg + k) * RW_P + c];
-        }
-        const bool inner_c = (c >= kHalo) && (c < kHalo + AT) && (x0 + c - kHalo < a.nW);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            float aa = 0.f, ad = 0.f, da = 0.f, dd = 0.f;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                aa = fmaf(wl_h(i), lo[2 * q + i], aa);
-                ad = fmaf(wl_g(i), lo[2 * q + i], ad);
-                da = fmaf(wl_h(i), hi[2 * q + i], da);
-                dd = fmaf(wl_g(i), hi[2 * q + i], dd);
-            }
-            const int rr = 8 * rg + q;
-            s_det[0 * AR * DT_P + rr * DT_P + c] = da;
-            s_det[1 * AR * DT_P + rr * DT_P + c] = ad;
-            s_det[2 * AR * DT_P + rr * DT_P + c] = dd;
-            if (a.ll != nullptr && inner_c && rr >= kHalo && rr < kHalo + AT) {
-                const int gy = y0 + rr - kHalo;
-                PRNU_DCHECK(x0 + c - kHalo >= 0 && x0 + c - kHalo < a.nW && gy >= 0);
-                if (gy < a.nH) a.ll[(size_t)b * a.out_bstride + (size_t)gy * a.out_pitch + x0 + c - kHalo] = aa;
-            }
-        }
+    colpass(a, g, s_row, s_det);
+    __syncthreads();
+    shrink3(a, g, s_det, reinterpret_cast<float4*>(s_row), s_rmap, s_cmap);
+}
+
+// Level-1 u8 analysis, persistent: each CTA walks tiles blockIdx.x, +gridDim.x,
+// ...; interior tiles arrive by TMA (box U8_P x AIN bytes) into a u8 tile that
+// is re-filled for the next tile as soon as the row pass has consumed it, so
+// the load overlaps the column pass and the shrink.  Border tiles (mirrored
+// input) are loaded with ordinary loads.
+constexpr int U8_TILE_BYTES = ((AIN * U8_P + 127) / 128) * 128;
+constexpr int A8_ROW_FLOATS = A_SMEM_ROW;          // row-pass planes; later the two vertical-sum buffers
+constexpr int A8_DET_FLOATS = 3 * AR * DT_P;
+constexpr size_t A8_SMEM_BYTES = U8_TILE_BYTES + sizeof(float) * (A8_ROW_FLOATS + A8_DET_FLOATS) +
+                                 sizeof(int) * (2 * AIN + 2 * AR) + 16;
+
+__device__ __forceinline__ bool u8_tile_interior(const AnalysisArgs& a, const ATile& g) {
+    const int iy = 2 * g.cy0 - 6, ix = 2 * g.cx0 - 6 - U8_OFF;   // ix: 16-byte aligned box start
+    return iy >= 0 && ix >= 0 && (ix & 15) == 0 && iy + AIN <= a.NH && ix + U8_OFF + AIN <= a.NW;
+}
+
+__global__ void __launch_bounds__(256, 3) k_analysis_u8_tma(const __grid_constant__ CUtensorMap in_map, AnalysisArgs a,
+                                                           int tiles_x, int tiles_y, int n_tiles) {
+    extern __shared__ __align__(128) unsigned char smem8[];
+    uint8_t* s_in8 = smem8;
+    float* s_row = reinterpret_cast<float*>(smem8 + U8_TILE_BYTES);
+    float* s_det = s_row + A8_ROW_FLOATS;
+    int* s_iy = reinterpret_cast<int*>(s_det + A8_DET_FLOATS);
+    int* s_ix = s_iy + AIN;
+    int* s_rmap = s_ix + AIN;
+    int* s_cmap = s_rmap + AR;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(s_cmap + AR + ((2 * AIN + 2 * AR) & 1));
+    const int tid = threadIdx.x;
+    const int per_frame = tiles_x * tiles_y;
+    auto tile_of = [&](int t) {
+        const int b = t / per_frame, r = t - b * per_frame;
+        return analysis_tile(a, b, r / tiles_x, r % tiles_x);
+    };
+    auto issue = [&](const ATile& g) {
+        mbar_arrive_expect_tx(bar, (uint32_t)(U8_P * AIN));
+        tma_load_3d(s_in8, &in_map, 2 * g.cx0 - 6 - U8_OFF, 2 * g.cy0 - 6, g.b, bar);
+    };
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
     }
     __syncthreads();
-
-    // ---- 4. shrink each detail subband (R-7): separable window sums of c^2,
-    //         vertical (per column, 8 rows per item) then horizontal (per row, 8 cols per item)
-    const float s0 = a.sp.sigma0_sq;
-    const int wm = a.sp.wmask;
-    float4* s_v = reinterpret_cast<float4*>(s_row);   // [AT][V_P4]: (v3, v5, v7, v9)
-    for (int s = 0; s < 3; ++s) {
-        const float* det = s_det + s * AR * DT_P;
-        // stage V: columns x in [0,AR) that are real, output rows 8*ig .. 8*ig+7
-        for (int it = tid; it < AR * (AT / 8); it += 256) {
-            const int x = it < 32 * (AT / 8) ? (it & 31) : 32 + ((it - 32 * (AT / 8)) % (AR - 32));
-            const int ig = it < 32 * (AT / 8) ? (it >> 5) : (it - 32 * (AT / 8)) / (AR - 32);
-            if (border_x && s_cmap[x] != x) continue;
-            float q[16];
-#pragma unroll
-            for (int k = 0; k < 16; ++k) {
-                const int rr = border_y ? s_rmap[8 * ig + k] : 8 * ig + k;
-                PRNU_DCHECK(rr >= 0 && rr < AR && x >= 0 && x < AR);
-                const float c = det[rr * DT_P + x];
-                q[k] = c * c;
+    uint32_t phase = 0;
+    int t = blockIdx.x;
+    if (t < n_tiles && tid == 0) {
+        const ATile g0 = tile_of(t);
+        if (u8_tile_interior(a, g0)) issue(g0);
+    }
+    for (; t < n_tiles; t += gridDim.x) {
+        const ATile g = tile_of(t);
+        analysis_tables(a, g, s_iy, s_ix, s_rmap, s_cmap);
+        if (u8_tile_interior(a, g)) {
+            mbar_wait(bar, phase);
+            phase ^= 1;
+            __syncthreads();   // tables visible
+        } else {
+            __syncthreads();   // tables visible
+            const uint8_t* in = reinterpret_cast<const uint8_t*>(a.in) + (size_t)g.b * a.in_bstride;
+            for (int e = tid; e < AIN * AIN; e += 256) {
+                const int r = e / AIN, c = e - r * AIN;
+                s_in8[r * U8_P + U8_OFF + c] = __ldg(in + (size_t)s_iy[r] * a.in_pitch + s_ix[c]);
             }
-#pragma unroll
-            for (int t = 0; t < 8; ++t) {
-                float v3 = q[t + 3] + q[t + 4] + q[t + 5];
-                float v5 = v3 + q[t + 2] + q[t + 6];
-                float v7 = v5 + q[t + 1] + q[t + 7];
-                float v9 = v7 + q[t] + q[t + 8];
-                s_v[(8 * ig + t) * V_P4 + x] = make_float4(v3, v5, v7, v9);
+            __syncthreads();
+        }
+        rowpass_u8(s_in8, s_row);
+        fence_proxy_async();   // order this thread's generic accesses of s_in8 before the next TMA write
+        __syncthreads();       // u8 tile consumed, s_row complete
+        const int tn = t + gridDim.x;
+        if (tid == 0 && tn < n_tiles) {
+            const ATile gn = tile_of(tn);
+            if (u8_tile_interior(a, gn)) {
+                fence_proxy_async();
+                issue(gn);   // lands while this tile's column pass and shrink run
             }
         }
+        colpass(a, g, s_row, s_det);
         __syncthreads();
-        // stage H: output row i, output columns 8*jg .. 8*jg+7
-        float* dst = (s == 0 ? a.d0 : s == 1 ? a.d1 : a.d2) + (size_t)b * a.out_bstride;
-        for (int it = tid; it < AT * (AT / 8); it += 256) {
-            const int i = it % AT, jg = it / AT;
-            const int gy = y0 + i;
-            float4 u[16];
-#pragma unroll
-            for (int k = 0; k < 16; ++k) {
-                const int xx = border_x ? s_cmap[8 * jg + k] : 8 * jg + k;
-                PRNU_DCHECK(xx >= 0 && xx < AR && i * V_P4 + xx < A_SMEM_ROW / 4);
-                u[k] = s_v[i * V_P4 + xx];
-            }
-            const float4* crow = reinterpret_cast<const float4*>(det + (i + kHalo) * DT_P + 8 * jg + kHalo);
-            const float4 c0 = crow[0], c1 = crow[1];
-            const float cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-            float s3 = u[3].x + u[4].x + u[5].x;
-            float s5 = u[2].y + u[3].y + u[4].y + u[5].y + u[6].y;
-            float s7 = u[1].z + u[2].z + u[3].z + u[4].z + u[5].z + u[6].z + u[7].z;
-            float s9 = u[0].w + u[1].w + u[2].w + u[3].w + u[4].w + u[5].w + u[6].w + u[7].w + u[8].w;
-            float o[8];
-#pragma unroll
-            for (int t = 0; t < 8; ++t) {
-                if (t > 0) {   // slide the windows one column right
-                    s3 += u[t + 5].x - u[t + 2].x;
-                    s5 += u[t + 6].y - u[t + 1].y;
-                    s7 += u[t + 7].z - u[t].z;
-                    s9 += u[t + 8].w - u[t - 1].w;
-                }
-                float m = 3.402823466e38f;
-                if (wm & 1) m = fminf(m, s3 * (1.0f / 9.0f));
-                if (wm & 2) m = fminf(m, s5 * (1.0f / 25.0f));
-                if (wm & 4) m = fminf(m, s7 * (1.0f / 49.0f));
-                if (wm & 8) m = fminf(m, s9 * (1.0f / 81.0f));
-                const float var = fmaxf(m - s0, 0.0f);
-                o[t] = cc[t] * __fdividef(s0, var + s0);   // noise-domain coefficient c - F(c)
-            }
-            if (gy < a.nH) {
-                const int gx = x0 + 8 * jg;
-                float* drow = dst + (size_t)gy * a.out_pitch + gx;
-                PRNU_DCHECK(gx >= 0 && gx < a.out_pitch && gy >= 0);
-                if (gx + 8 <= a.nW) {
-                    reinterpret_cast<float4*>(drow)[0] = make_float4(o[0], o[1], o[2], o[3]);
-                    reinterpret_cast<float4*>(drow)[1] = make_float4(o[4], o[5], o[6], o[7]);
-                } else {
-#pragma unroll
-                    for (int t = 0; t < 8; ++t)
-                        if (gx + t < a.nW) drow[t] = o[t];
-                }
-            }
-        }
-        __syncthreads();
+        shrink3(a, g, s_det, reinterpret_cast<float4*>(s_row), s_rmap, s_cmap);
     }
 }
 
@@ -329,20 +490,20 @@ __device__ __forceinline__ void synth_compute(const float* c, float* s_L, float*
         }
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
+            // outputs t = 2s (e = 0) and 2s+1 (e = 1) as one FFMA2 pair
+            float2 l = make_float2(0.f, 0.f), h = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                float l = 0.f, h = 0.f;
-#pragma unroll
-                for (int m = 0; m < 4; ++m) {
-                    l = fmaf(wl_h(6 - 2 * m + e), va[q + m], l);
-                    l = fmaf(wl_g(6 - 2 * m + e), vad[q + m], l);
-                    h = fmaf(wl_h(6 - 2 * m + e), vda[q + m], h);
-                    h = fmaf(wl_g(6 - 2 * m + e), vdd[q + m], h);
-                }
-                const int t = 4 * sg + 2 * q + e;
-                s_L[t * SL_P + k] = l;
-                s_L[ST_Y * SL_P + t * SL_P + k] = h;
+            for (int m = 0; m < 4; ++m) {
+                l = ffma2(va[q + m], make_float2(wl_h(6 - 2 * m), wl_h(7 - 2 * m)), l);
+                l = ffma2(vad[q + m], make_float2(wl_g(6 - 2 * m), wl_g(7 - 2 * m)), l);
+                h = ffma2(vda[q + m], make_float2(wl_h(6 - 2 * m), wl_h(7 - 2 * m)), h);
+                h = ffma2(vdd[q + m], make_float2(wl_g(6 - 2 * m), wl_g(7 - 2 * m)), h);
             }
+            const int t = 4 * sg + 2 * q;
+            s_L[t * SL_P + k] = l.x;
+            s_L[(t + 1) * SL_P + k] = l.y;
+            s_L[ST_Y * SL_P + t * SL_P + k] = h.x;
+            s_L[ST_Y * SL_P + (t + 1) * SL_P + k] = h.y;
         }
     }
     __syncthreads();
@@ -357,16 +518,14 @@ __device__ __forceinline__ void synth_compute(const float* c, float* s_L, float*
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
+            float2 x = make_float2(0.f, 0.f);   // outputs 2q (e = 0) and 2q+1 (e = 1)
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                float x = 0.f;
-#pragma unroll
-                for (int m = 0; m < 4; ++m) {
-                    x = fmaf(wl_h(6 - 2 * m + e), vl[q + m], x);
-                    x = fmaf(wl_g(6 - 2 * m + e), vh[q + m], x);
-                }
-                s_out[t * SO_P + 8 * g + 2 * q + e] = x;
+            for (int m = 0; m < 4; ++m) {
+                x = ffma2(vl[q + m], make_float2(wl_h(6 - 2 * m), wl_h(7 - 2 * m)), x);
+                x = ffma2(vh[q + m], make_float2(wl_g(6 - 2 * m), wl_g(7 - 2 * m)), x);
             }
+            s_out[t * SO_P + 8 * g + 2 * q] = x.x;
+            s_out[t * SO_P + 8 * g + 2 * q + 1] = x.y;
         }
     }
     __syncthreads();
@@ -566,7 +725,9 @@ static int setup_attributes() {
                                           (int)S_SMEM_BYTES);
     cudaError_t e5 = cudaFuncSetAttribute(k_synth_tma<1, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)S_SMEM_BYTES);
-    cudaError_t e = e1 ? e1 : e2 ? e2 : e3 ? e3 : e4 ? e4 : e5;
+    cudaError_t e6 = cudaFuncSetAttribute(k_analysis_u8_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)A8_SMEM_BYTES);
+    cudaError_t e = e1 ? e1 : e2 ? e2 : e3 ? e3 : e4 ? e4 : e5 ? e5 : e6;
     if (e != cudaSuccess) return fail(PRNU_CUDA_ERROR, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
     g_attr_done = true;
     return PRNU_OK;
@@ -616,7 +777,22 @@ static int denoise_front(const TIn* in, long long in_bstride, int in_pitch, int 
             a.in = in;
             a.in_bstride = in_bstride;
             a.in_pitch = in_pitch;
-            k_analysis_shrink<TIn><<<grid, 256, A_SMEM_BYTES, st>>>(a);
+            CUtensorMap map;
+            // The persistent TMA variant is correct but measured slower than the generic
+            // kernel on B200 (23.9 vs 21.5 ms/step, profiles/r01): opt-in only.
+            static const bool use_tma = getenv("PRNU_TMA_ANALYSIS") != nullptr;
+            const bool tma_ok = use_tma && sizeof(TIn) == 1 && (in_pitch % 16) == 0 && (in_bstride % 16) == 0 &&
+                                ((uintptr_t)in % 16) == 0 &&
+                                encode_tensor_map_3d(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, in, (uint64_t)a.NW,
+                                                     (uint64_t)a.NH, (uint64_t)nb, (uint64_t)in_pitch,
+                                                     (uint64_t)in_bstride, U8_P, AIN);
+            if (tma_ok) {
+                const int tx = (int)grid.x, ty = (int)grid.y, n_tiles = tx * ty * nb;
+                const int ctas = std::min(n_tiles, 148 * 3);
+                k_analysis_u8_tma<<<ctas, 256, A8_SMEM_BYTES, st>>>(map, a, tx, ty, n_tiles);
+            } else {
+                k_analysis_shrink<TIn><<<grid, 256, A_SMEM_BYTES, st>>>(a);
+            }
         } else {
             a.in = pb.approx[l - 1];
             a.in_bstride = (long long)pb.bstride[l - 1];
@@ -677,9 +853,12 @@ int run_residual(const TIn* in, int nb, int H, int W, const Pyramid& p, const Sh
     return check_launch("k_synth_tma(level 1)");
 }
 
+// acc_wait (optional): event the accumulating launch must wait for (the previous
+// wave's accumulation on another stream); acc_done (optional): recorded after it.
 template <typename TIn>
 int run_residual_accumulate(const TIn* in, const TIn* I, int nb, int H, int W, const Pyramid& p,
-                            const ShrinkParams& sp, double* num, double* den, float* ws_pyr, cudaStream_t st) {
+                            const ShrinkParams& sp, double* num, double* den, float* ws_pyr, cudaStream_t st,
+                            cudaEvent_t acc_wait, cudaEvent_t acc_done) {
     PyramidBuffers pb = carve_pyramid(p, ws_pyr, nb);
     int rc = denoise_front<TIn>(in, (long long)H * W, W, nb, p, pb, sp, st);
     if (rc) return rc;
@@ -697,12 +876,16 @@ int run_residual_accumulate(const TIn* in, const TIn* I, int nb, int H, int W, c
     s.den = den;
     s.acc_pitch = W;
     dim3 grid((W + ST_X - 1) / ST_X, (H + ST_Y - 1) / ST_Y, 1);
+    if (acc_wait && cudaStreamWaitEvent(st, acc_wait, 0) != cudaSuccess)
+        return fail(PRNU_CUDA_ERROR, "cudaStreamWaitEvent");
     {
         KTimer kt(sizeof(TIn) == 1 ? "synth_acc_l1_u8" : "synth_acc_l1_f32", st);
         k_synth_tma<1, TIn><<<grid, 256, S_SMEM_BYTES, st>>>(m, s);
     }
     count_launch();
-    return check_launch("k_synth_tma(accumulate)");
+    if ((rc = check_launch("k_synth_tma(accumulate)"))) return rc;
+    if (acc_done && cudaEventRecord(acc_done, st) != cudaSuccess) return fail(PRNU_CUDA_ERROR, "cudaEventRecord");
+    return PRNU_OK;
 }
 
 template int run_residual<float>(const float*, int, int, int, const Pyramid&, const ShrinkParams&, float*, float*,
@@ -710,8 +893,10 @@ template int run_residual<float>(const float*, int, int, int, const Pyramid&, co
 template int run_residual<uint8_t>(const uint8_t*, int, int, int, const Pyramid&, const ShrinkParams&, float*,
                                    float*, cudaStream_t);
 template int run_residual_accumulate<float>(const float*, const float*, int, int, int, const Pyramid&,
-                                            const ShrinkParams&, double*, double*, float*, cudaStream_t);
+                                            const ShrinkParams&, double*, double*, float*, cudaStream_t, cudaEvent_t,
+                                            cudaEvent_t);
 template int run_residual_accumulate<uint8_t>(const uint8_t*, const uint8_t*, int, int, int, const Pyramid&,
-                                              const ShrinkParams&, double*, double*, float*, cudaStream_t);
+                                              const ShrinkParams&, double*, double*, float*, cudaStream_t,
+                                              cudaEvent_t, cudaEvent_t);
 
 }  // namespace prnu
