@@ -186,18 +186,18 @@ def oracle_sample(frames_host, depths, budget_s: float):
     t_total, n_total, desc = 0.0, 0, []
     per_depth = budget_s / len(depths)
     for d in depths:
-        k = 1
-        t_d = 0.0
-        n_d = 0
-        while True:
+        k_max = fr.shape[0] // d
+        t0 = time.perf_counter()
+        oracle.extract_fingerprint(fr[:d], d)          # one SDA frame: calibrates the sample size
+        t_d = time.perf_counter() - t0
+        n_d = 1
+        k = max(1, min(k_max, int(per_depth / 3.0 / max(t_d, 1e-3))))
+        # fingerprints of k SDA frames until this depth's budget is spent
+        while t_d < per_depth:
             t0 = time.perf_counter()
             oracle.extract_fingerprint(fr[: k * d], d)
-            dt = time.perf_counter() - t0
-            t_d += dt
+            t_d += time.perf_counter() - t0
             n_d += k
-            if t_d + 2 * dt > per_depth or (k + 1) * d > fr.shape[0]:
-                break
-            k += 1
         t_total += t_d
         n_total += n_d
         desc.append(f"d={d}: {n_d} denoisings over {t_d:.1f}s")
@@ -347,8 +347,17 @@ def main():
         kt = kernels[top]
         avg_ms = kt["ms_per_step"] / kt["launches_per_step"]
         achieved = kt.get("alg_GBps")
+        # DRAM traffic per launch of that kernel from the committed ncu --set full capture
+        # (same kernel and launch configuration), else null
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "latest_traffic.json")
+        if os.path.exists(tpath):
+            t = json.load(open(tpath))
+            fpl = n_sda.get(1, 0) / max(1.0, kt["launches_per_step"]) if top.endswith("_u8") else None
+            if t.get("kernel") == top and fpl and abs(fpl - t["frames_per_launch"]) < 1.0:
+                traffic = t["dram_bytes_read"] + t["dram_bytes_write"]
         roof = {"kernel": top, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": (achieved / peak) if achieved else None, "traffic": None,
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback",
                 "bytes_per_launch": kt.get("alg_bytes_per_launch"), "avg_launch_ms": avg_ms,
                 "share_of_kernel_time": kt["share"]}
@@ -378,7 +387,7 @@ def main():
     # ---- cpu baseline: the oracle on a bounded sample (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        fr = frames[: max(depths) * 2].cpu().numpy()
+        fr = frames[: max(depths) * 2].cpu().numpy()   # 100 frames: 100 (d=1) / 2 (d=50) denoisings per pass
         r, desc = oracle_sample(fr, depths, args.cpu_seconds)
         cpu = {"value": r, "unit": "denoised FHD frames/s", "cores": 1, "kind": "oracle",
                "sample": f"fp64 C oracle, single thread, first frames of the same video: {desc}"}
