@@ -51,16 +51,19 @@ int oracle_sda_average(const uint8_t* frames, long m, int H, int W, long d, floa
     long ns = oracle_sda_groups(m, d);
     if (ns < 0) return 3;
     long P = (long)H * W;
+    int64_t* s = (int64_t*)malloc(sizeof(int64_t) * P);
     for (long i = 0; i < ns; ++i) {
-        for (long p = 0; p < P; ++p) {
-            int64_t s = 0;                       /* exact integer sum */
-            for (long j = i * d; j < (i + 1) * d; ++j) s += frames[j * P + p];
-            /* exact rational s/d -> fp32.  s < 2^53 so (double)s is exact;
-               the fp64 quotient is then rounded to fp32.  tests/ pin this
-               against IEEE fp32 division exhaustively for every depth used. */
-            out[i * P + p] = (float)((double)s / (double)d);
-        }
+        /* exact integer sum of the group (integer addition: the order of the
+           frames does not change the value), frame by frame for locality */
+        memset(s, 0, sizeof(int64_t) * P);
+        for (long j = i * d; j < (i + 1) * d; ++j)
+            for (long p = 0; p < P; ++p) s[p] += frames[j * P + p];
+        /* exact rational s/d -> fp32.  s < 2^53 so (double)s is exact;
+           the fp64 quotient is then rounded to fp32.  tests/ pin this
+           against IEEE fp32 division exhaustively for every depth used. */
+        for (long p = 0; p < P; ++p) out[i * P + p] = (float)((double)s[p] / (double)d);
     }
+    free(s);
     return 0;
 }
 

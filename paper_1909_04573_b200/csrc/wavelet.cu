@@ -321,7 +321,34 @@ __global__ void __launch_bounds__(256, 3) k_analysis_shrink(AnalysisArgs a) {
     const TIn* in = reinterpret_cast<const TIn*>(a.in) + (size_t)g.b * a.in_bstride;
     analysis_tables(a, g, s_iy, s_ix, s_rmap, s_cmap);
     __syncthreads();
-    {
+    const int ix0 = 2 * g.cx0 - 6, iy0 = 2 * g.cy0 - 6;
+    if (sizeof(TIn) == 1 && ix0 >= 2 && iy0 >= 0 && ix0 - 2 + 88 <= a.NW && iy0 + AIN <= a.NH &&
+        ((reinterpret_cast<uintptr_t>(in) + (size_t)ix0 - 2) & 3) == 0 && (a.in_pitch & 3) == 0) {
+        // interior u8 tile: each row is 22 aligned words covering input columns
+        // ix0-2 .. ix0+85; lane w widens its 4 bytes exactly (2^23 trick)
+        constexpr int RPW = (AIN + 7) / 8;
+        const uint8_t* base = reinterpret_cast<const uint8_t*>(in) + (size_t)iy0 * a.in_pitch + ix0 - 2;
+        uint32_t wv[RPW];
+#pragma unroll
+        for (int k = 0; k < RPW; ++k) {
+            const int r = min(warp + 8 * k, AIN - 1);
+            wv[k] = lane < 22 ? __ldg(reinterpret_cast<const uint32_t*>(base + (size_t)r * a.in_pitch) + lane) : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < RPW; ++k) {
+            const int r = warp + 8 * k;
+            if (r < AIN && lane < 22) {
+                const int c0 = 4 * lane - 2;   // tile column of byte 0
+                const float f0 = __uint_as_float(__byte_perm(wv[k], 0x4B000000u, 0x7540u)) - 8388608.0f;
+                const float f1 = __uint_as_float(__byte_perm(wv[k], 0x4B000000u, 0x7541u)) - 8388608.0f;
+                const float f2 = __uint_as_float(__byte_perm(wv[k], 0x4B000000u, 0x7542u)) - 8388608.0f;
+                const float f3 = __uint_as_float(__byte_perm(wv[k], 0x4B000000u, 0x7543u)) - 8388608.0f;
+                float* row = s_in + r * IN_P;
+                if (lane > 0) *reinterpret_cast<float2*>(row + c0) = make_float2(f0, f1);
+                *reinterpret_cast<float2*>(row + c0 + 2) = make_float2(f2, f3);   // c0 + 3 <= 85
+            }
+        }
+    } else {
         constexpr int RPW = (AIN + 7) / 8;   // 11 rows per warp
         float v[RPW][3];
         int ixs[3];

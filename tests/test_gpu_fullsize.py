@@ -1,0 +1,172 @@
+"""Full-size parity (BASELINE.json configs 2-5) through the C ABI, in the launch
+configuration bench.py times (batch 32, two streams), against the fp64 oracle on
+outputs it can compute in seconds, plus properties that hold at any size.
+
+Tolerances as in test_gpu_parity.py."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+W_TOL = 1e-3
+K_TOL = 1e-3
+NCC_TOL = 1e-5
+PCE_RTOL = 1e-3
+BENCH_BATCH = 32
+
+
+@pytest.fixture(scope="module")
+def prnu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1909_04573_b200 as m
+    return m
+
+
+def k_metric(K_gpu, K_ref, den, n_sda):
+    d = np.abs(K_gpu.astype(np.float64) - K_ref)
+    return float((d * np.sqrt(den / n_sda)).max())
+
+
+@pytest.fixture(scope="module")
+def video_c2():
+    """Config 2: 1800 (+1 query) frames 1920x1080, the drift recipe."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    v = synth.video("drift", 1801, 1080, 1920, seed=0, device="cuda")
+    return v
+
+
+def test_c2_depth50_full_oracle(prnu, video_c2):
+    """Config 2, SDA depth 50: the whole 36-frame fingerprint against the oracle."""
+    fr = video_c2.frames[:1800]
+    fp = prnu.extract_fingerprint(fr, 50, batch=36)
+    K_ref, num, den, ns = oracle.extract_fingerprint(fr.cpu().numpy(), 50)
+    assert fp.n_sda == ns == 36
+    np.testing.assert_array_equal(fp.sum_I2.cpu().numpy(), den)      # exact: same fp32 SDA frames, same order
+    assert k_metric(fp.K.cpu().numpy(), K_ref, den, ns) <= K_TOL
+    rho = prnu.ncc(fp.K, video_c2.K).item()
+    assert abs(rho - oracle.ncc(K_ref, video_c2.K.cpu().numpy())) <= NCC_TOL
+    assert rho > 0.9
+
+
+def test_c2_depth1_sampled(prnu, video_c2):
+    """Config 2, conventional (1800 denoisings) in the bench configuration:
+    sum_I2 equals the exact integer sum of squares; residuals of sampled frames
+    match the oracle; the first 32 frames' accumulator matches the oracle's."""
+    fr = video_c2.frames[:1800]
+    fp = prnu.extract_fingerprint(fr, 1, batch=BENCH_BATCH)
+    assert fp.n_sda == 1800
+    sq = torch.zeros((1080, 1920), dtype=torch.int64, device="cuda")
+    for i in range(0, 1800, 100):
+        x = fr[i:i + 100].to(torch.int64)
+        sq += (x * x).sum(0)
+    assert torch.equal(fp.sum_I2, sq.double())                       # exact (all sums < 2^53)
+    # residuals of sampled frames (same kernels, batch of 3)
+    idx = [0, 977, 1799]
+    Wg = prnu.residual(fr[idx].contiguous()).cpu().numpy()
+    for j, i in enumerate(idx):
+        Wr = oracle.residual(fr[i].cpu().numpy().astype(np.float32))
+        assert np.abs(Wg[j] - Wr).max() <= W_TOL
+    # one whole wave: the fingerprint of the first 32 frames against the oracle
+    sub = fr[:32].contiguous()
+    fp32 = prnu.extract_fingerprint(sub, 1, batch=BENCH_BATCH)
+    K_ref, num, den, ns = oracle.extract_fingerprint(sub.cpu().numpy(), 1)
+    assert k_metric(fp32.K.cpu().numpy(), K_ref, den, ns) <= K_TOL
+    assert prnu.ncc(fp.K, video_c2.K).item() > 0.9
+
+
+def test_c2_query_pce(prnu, video_c2):
+    """The bench's PCE leg: query frame 1800 against the depth-50 fingerprint."""
+    fr = video_c2.frames
+    fp = prnu.extract_fingerprint(fr[:1800], 50, batch=36)
+    q = fr[1800:1801]
+    R = prnu.residual(q, zero_mean=True)
+    res = prnu.pce(R, prnu.pce_template(fp.K, q))
+    K_ref, _, _, _ = oracle.extract_fingerprint(fr[:1800].cpu().numpy(), 50)
+    qn = q[0].cpu().numpy()
+    p_ref, peak_ref, _ = oracle.pce(oracle.residual(qn.astype(np.float32), zero_mean=True),
+                                    oracle.pce_template(K_ref, qn))
+    assert (res.peak_y.item(), res.peak_x.item()) == peak_ref == (0, 0)
+    assert abs(res.pce.item() - p_ref) <= PCE_RTOL * abs(p_ref)
+    assert res.decision().item()
+
+
+def test_c5_depth_sweep_sampled(prnu):
+    """Config 5 (3600 frames 1920x1080, shift recipe): every depth of the sweep
+    runs; d = 3600 and d = 300 are checked against the oracle in full; the
+    denoise counts follow floor(m/d)."""
+    v = synth.video("shift", 3600, 1080, 1920, seed=0, device="cuda")
+    fr = v.frames
+    host = None
+    for d in (1, 2, 5, 10, 25, 50, 100, 300, 3600):
+        fp = prnu.extract_fingerprint(fr, d, batch=BENCH_BATCH if d == 1 else max(1, min(64, 3600 // d)))
+        assert fp.n_sda == 3600 // d
+        assert prnu.ncc(fp.K, v.K).item() > 0.5
+        if d in (300, 3600):
+            if host is None:
+                host = fr.cpu().numpy()
+            K_ref, num, den, ns = oracle.extract_fingerprint(host, d)
+            np.testing.assert_array_equal(fp.sum_I2.cpu().numpy(), den)
+            assert k_metric(fp.K.cpu().numpy(), K_ref, den, ns) <= K_TOL
+
+
+def test_c3_stills_sampled(prnu):
+    """Config 3 shape (4000x3000 luma stills): residual parity on one still, the
+    depth-50 fingerprint of 200 stills against the oracle (4 SDA frames)."""
+    Y, K_luma = synth.stills(200, 3000, 4000, seed=0, device="cuda")
+    Wg = prnu.residual(Y[7:8].contiguous()).cpu().numpy()[0]
+    Wr = oracle.residual(Y[7].cpu().numpy().astype(np.float32))
+    assert np.abs(Wg - Wr).max() <= W_TOL
+    fp = prnu.extract_fingerprint(Y, 50, batch=4)
+    K_ref, num, den, ns = oracle.extract_fingerprint(Y.cpu().numpy(), 50)
+    assert ns == 4
+    assert k_metric(fp.K.cpu().numpy(), K_ref, den, ns) <= K_TOL
+    for d in (1, 5, 10, 20):
+        assert prnu.extract_fingerprint(Y, d, batch=BENCH_BATCH if d == 1 else 20).n_sda == 200 // d
+
+
+def test_c4_camera_id_sampled(prnu):
+    """Config 4: 64 cameras x 300 frames 1280x720, depth 30, 64 query residuals
+    against 64 fingerprints (4096 PCEs).  Diagonal > 60 > off-diagonal
+    (directional); sampled entries against the oracle."""
+    H, W, n = 720, 1280, 64
+    Ks, queries, cams = [], [], {}
+    for c in range(n):
+        v = synth.video("drift", 301, H, W, seed=4, camera=c, device="cuda")
+        Ks.append(prnu.extract_fingerprint(v.frames[:300], 30, batch=10).K.clone())
+        queries.append(v.frames[300])
+        if c < 2:
+            cams[c] = v.frames.cpu().numpy()
+    Iq = torch.stack(queries)
+    R = prnu.residual(Iq, zero_mean=True)
+    plan = prnu.PcePlan(H, W, n)
+    M = np.zeros((n, n))
+    PY = np.zeros((n, n), dtype=np.int64)
+    PX = np.zeros((n, n), dtype=np.int64)
+    for c in range(n):
+        res = plan(R, prnu.pce_template(Ks[c], Iq))
+        M[:, c] = res.pce.cpu().numpy()
+        PY[:, c] = res.peak_y.cpu().numpy()
+        PX[:, c] = res.peak_x.cpu().numpy()
+    off = M[~np.eye(n, dtype=bool)]
+    assert np.all(np.diag(M) > 60)
+    assert np.mean(off > 60) < 0.01
+    # oracle on sampled pairs: cameras 0 and 1 against queries 0, 1, 2 (R-19 tie rule)
+    for c in (0, 1):
+        K_ref, _, _, _ = oracle.extract_fingerprint(cams[c][:300], 30)
+        for q in (0, 1, 2):
+            qn = queries[q].cpu().numpy()
+            C = oracle.correlation_surface(oracle.residual(qn.astype(np.float32), zero_mean=True),
+                                           oracle.pce_template(K_ref, qn))
+            p_ref, peak_ref, _ = oracle.match.pce_from_surface(C)
+            gpk = (int(PY[q, c]), int(PX[q, c]))
+            if gpk != peak_ref:
+                top = np.sort(np.abs(C).ravel())[-2:]
+                assert (top[1] - top[0]) / top[1] < 1e-4, (q, c, gpk, peak_ref)
+                p_ref = oracle.match.pce_from_surface(C, peak=gpk)[0]
+            assert abs(M[q, c] - p_ref) <= PCE_RTOL * abs(p_ref) + 1e-3, (q, c, M[q, c], p_ref)
