@@ -505,7 +505,10 @@ __device__ __forceinline__ void synth_compute(const float* c, float* s_L, float*
     const int tid = threadIdx.x;
     // Lx = synth(A, ad), Hx = synth(da, dd); item = (coefficient column k, 4 output rows)
     for (int it = tid; it < SC_X * (ST_Y / 4); it += 256) {
-        const int k = it % SC_X, sg = it / SC_X;
+        // warps 0..7: columns 0..31 of one row group each; the last items take
+        // columns 32..34 of every group (no bank-shifted wrap inside a warp)
+        const int k = it < 32 * (ST_Y / 4) ? (it & 31) : 32 + (it - 32 * (ST_Y / 4)) % (SC_X - 32);
+        const int sg = it < 32 * (ST_Y / 4) ? (it >> 5) : (it - 32 * (ST_Y / 4)) / (SC_X - 32);
         float va[5], vda[5], vad[5], vdd[5];
 #pragma unroll
         for (int m = 0; m < 5; ++m) {
@@ -600,18 +603,22 @@ __global__ void __launch_bounds__(256, MODE == 0 ? 3 : 2) k_synth_tma(const __gr
     };
     if (tid == 0 && f0 < f1) issue(f0, 0);
 
+    // accumulate mapping: thread owns column cc of rows r0, r0+4, ..., r0+28 of the tile
+    static_assert(ST_X == 64 && ACC_PER_THREAD * 4 == ST_Y, "accumulate mapping");
+    const int r0 = tid >> 6, cc = tid & 63;
+    const int gx = tx0 + cc;
+    const int gxc = min(gx, a.NW - 1);
     double an[ACC_PER_THREAD], ad[ACC_PER_THREAD];
     if (MODE == 1) {
 #pragma unroll
         for (int k = 0; k < ACC_PER_THREAD; ++k) {
-            const int e = tid + 256 * k;
-            const int r = e / ST_X, cc = e - r * ST_X;
-            const int gy = ty0 + r, gx = tx0 + cc;
+            const int gy = ty0 + r0 + 4 * k;
             const bool ok = gy < a.NH && gx < a.NW;
             an[k] = ok ? a.num[(size_t)gy * a.acc_pitch + gx] : 0.0;
             ad[k] = ok ? a.den[(size_t)gy * a.acc_pitch + gx] : 0.0;
         }
     }
+
     for (int f = f0; f < f1; ++f) {
         const int it = f - f0, buf = it & 1;
         if (tid == 0 && f + 1 < f1) {
@@ -621,29 +628,25 @@ __global__ void __launch_bounds__(256, MODE == 0 ? 3 : 2) k_synth_tma(const __gr
         float iv[ACC_PER_THREAD];
         if (MODE == 1) {   // this frame's I values, in flight during the reconstruction
             const TI* Ib = reinterpret_cast<const TI*>(a.I) + (size_t)f * a.i_bstride;
-#pragma unroll
-            for (int k = 0; k < ACC_PER_THREAD; ++k) {
-                const int e = tid + 256 * k;
-                const int r = e / ST_X, cc = e - r * ST_X;
-                const int gy = min(ty0 + r, a.NH - 1), gx = min(tx0 + cc, a.NW - 1);
-                iv[k] = (float)Ib[(size_t)gy * a.i_pitch + gx];
-            }
+#pragma unroll   // rows clamped into the plane: values of pixels beyond it are read, never stored
+            for (int k = 0; k < ACC_PER_THREAD; ++k)
+                iv[k] = (float)__ldg(Ib + min(ty0 + r0 + 4 * k, a.NH - 1) * a.i_pitch + gxc);
         }
         mbar_wait(&bar[buf], (it >> 1) & 1);
         synth_compute(cbuf0 + buf * SC_TILE, s_L, s_out);
         if (MODE == 0) {
             float* out = a.out + (size_t)f * a.out_bstride;
-            for (int e = tid; e < ST_Y * ST_X; e += 256) {
-                const int r = e / ST_X, cc = e - r * ST_X;
-                const int gy = ty0 + r, gx = tx0 + cc;
-                if (gy < a.NH && gx < a.NW) out[(size_t)gy * a.out_pitch + gx] = s_out[r * SO_P + cc];
+            if (gx < a.NW) {
+#pragma unroll
+                for (int k = 0; k < ACC_PER_THREAD; ++k) {
+                    const int gy = ty0 + r0 + 4 * k;
+                    if (gy < a.NH) out[(size_t)gy * a.out_pitch + gx] = s_out[(r0 + 4 * k) * SO_P + cc];
+                }
             }
         } else {
 #pragma unroll
             for (int k = 0; k < ACC_PER_THREAD; ++k) {
-                const int e = tid + 256 * k;
-                const int r = e / ST_X, cc = e - r * ST_X;
-                const double w = (double)s_out[r * SO_P + cc];
+                const double w = (double)s_out[(r0 + 4 * k) * SO_P + cc];
                 const double x = (double)iv[k];
                 an[k] += w * x;   // exact product (fp32 x fp32 fits fp64), fp64 sum
                 ad[k] += x * x;
@@ -654,9 +657,7 @@ __global__ void __launch_bounds__(256, MODE == 0 ? 3 : 2) k_synth_tma(const __gr
     if (MODE == 1) {
 #pragma unroll
         for (int k = 0; k < ACC_PER_THREAD; ++k) {
-            const int e = tid + 256 * k;
-            const int r = e / ST_X, cc = e - r * ST_X;
-            const int gy = ty0 + r, gx = tx0 + cc;
+            const int gy = ty0 + r0 + 4 * k;
             if (gy < a.NH && gx < a.NW) {
                 a.num[(size_t)gy * a.acc_pitch + gx] = an[k];
                 a.den[(size_t)gy * a.acc_pitch + gx] = ad[k];
