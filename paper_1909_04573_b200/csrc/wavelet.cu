@@ -174,6 +174,10 @@ __device__ __forceinline__ void colpass(const AnalysisArgs& a, const ATile& g, c
             hi[k] = s_row[RW_PLANE + rw_off(16 * rg + k) + c];
         }
         const bool inner_c = (c >= kHalo) && (c < kHalo + AT) && (g.x0 + c - kHalo < a.nW);
+        // approximation of region row rr goes to plane row y0 + rr - kHalo
+        float* llc = a.ll ? a.ll + (size_t)g.b * a.out_bstride + (ptrdiff_t)(g.y0 - kHalo) * a.out_pitch + g.x0 + c -
+                                kHalo
+                          : nullptr;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             float2 p_l = make_float2(0.f, 0.f), p_h = make_float2(0.f, 0.f);   // (aa, ad), (da, dd)
@@ -187,10 +191,8 @@ __device__ __forceinline__ void colpass(const AnalysisArgs& a, const ATile& g, c
             s_det[0 * AR * DT_P + rr * DT_P + c] = da;
             s_det[1 * AR * DT_P + rr * DT_P + c] = ad;
             s_det[2 * AR * DT_P + rr * DT_P + c] = dd;
-            if (a.ll != nullptr && inner_c && rr >= kHalo && rr < kHalo + AT) {
-                const int gy = g.y0 + rr - kHalo;
-                if (gy < a.nH) a.ll[(size_t)g.b * a.out_bstride + (size_t)gy * a.out_pitch + g.x0 + c - kHalo] = aa;
-            }
+            if (llc != nullptr && inner_c && rr >= kHalo && rr < kHalo + AT && g.y0 + rr - kHalo < a.nH)
+                llc[(ptrdiff_t)rr * a.out_pitch] = aa;
         }
     }
 }
@@ -201,15 +203,16 @@ __device__ __forceinline__ void colpass(const AnalysisArgs& a, const ATile& g, c
 // Wiener factor; writes the noise-domain coefficients c sigma0^2/(v+sigma0^2).
 // Two vertical-sum buffers pipeline the subbands: phases V0 | H0+V1 | H1+V2 | H2.
 // Starts after a barrier that made s_det complete; ends with a barrier.
-__device__ __forceinline__ void shrink_v(const ATile& g, const float* det, float4* s_v, const int* s_rmap,
-                                         const int* s_cmap, int it) {
+template <bool BY>
+__device__ __forceinline__ void shrink_v_t(const ATile& g, const float* det, float4* s_v, const int* s_rmap,
+                                           const int* s_cmap, int it) {
     const int x = it < 32 * (AT / 8) ? (it & 31) : 32 + ((it - 32 * (AT / 8)) % (AR - 32));
     const int ig = it < 32 * (AT / 8) ? (it >> 5) : (it - 32 * (AT / 8)) / (AR - 32);
     if (g.bx && s_cmap[x] != x) return;
     float q[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
-        const int rr = g.by ? s_rmap[8 * ig + k] : 8 * ig + k;
+        const int rr = BY ? s_rmap[8 * ig + k] : 8 * ig + k;
         const float c = det[rr * DT_P + x];
         q[k] = __fmul_rn(c, c);   // no contraction into the sums: identical in every kernel
     }
@@ -223,8 +226,15 @@ __device__ __forceinline__ void shrink_v(const ATile& g, const float* det, float
     }
 }
 
-__device__ __forceinline__ void shrink_h(const AnalysisArgs& a, const ATile& g, const float* det, const float4* s_v,
-                                         const int* s_cmap, float* dst, int it) {
+__device__ __forceinline__ void shrink_v(const ATile& g, const float* det, float4* s_v, const int* s_rmap,
+                                         const int* s_cmap, int it) {
+    if (g.by) shrink_v_t<true>(g, det, s_v, s_rmap, s_cmap, it);
+    else shrink_v_t<false>(g, det, s_v, s_rmap, s_cmap, it);
+}
+
+template <bool BX>
+__device__ __forceinline__ void shrink_h_t(const AnalysisArgs& a, const ATile& g, const float* det,
+                                           const float4* s_v, const int* s_cmap, float* dst, int it) {
     const float s0 = a.sp.sigma0_sq;
     const int wm = a.sp.wmask;
     const int i = it % AT, jg = it / AT;
@@ -232,7 +242,7 @@ __device__ __forceinline__ void shrink_h(const AnalysisArgs& a, const ATile& g, 
     float4 u[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
-        const int xx = g.bx ? s_cmap[8 * jg + k] : 8 * jg + k;
+        const int xx = BX ? s_cmap[8 * jg + k] : 8 * jg + k;
         u[k] = s_v[i * V_P4 + xx];
     }
     const float* crow = det + (i + kHalo) * DT_P + 8 * jg + kHalo;
@@ -269,6 +279,12 @@ __device__ __forceinline__ void shrink_h(const AnalysisArgs& a, const ATile& g, 
                 if (gx + t < a.nW) drow[t] = o[t];
         }
     }
+}
+
+__device__ __forceinline__ void shrink_h(const AnalysisArgs& a, const ATile& g, const float* det, const float4* s_v,
+                                         const int* s_cmap, float* dst, int it) {
+    if (g.bx) shrink_h_t<true>(a, g, det, s_v, s_cmap, dst, it);
+    else shrink_h_t<false>(a, g, det, s_v, s_cmap, dst, it);
 }
 
 __device__ __forceinline__ void shrink3(const AnalysisArgs& a, const ATile& g, const float* s_det, float4* s_v,
