@@ -27,6 +27,11 @@ namespace prnu {
 // Tile: AT x AT output coefficients per subband, computed over an AR x AR
 // region (halo kHalo for the 9x9 windows) from an AIN x AIN input tile.
 constexpr int AT = 32;                  // output coefficient tile (square)
+#ifndef PRNU_ANALYSIS_THREADS
+#define PRNU_ANALYSIS_THREADS 288
+#endif
+constexpr int A_NT = PRNU_ANALYSIS_THREADS;   // threads per analysis CTA (9 warps: measured best of 256/288/320/384)
+constexpr int A_NW = A_NT / 32;
 constexpr int AR = AT + 2 * kHalo;      // 40: computed coefficient region
 constexpr int AIN = 2 * AR + 6;         // 86: input rows / columns of the region
 constexpr int IN_P = 92;                // input tile pitch (== 28 mod 32: conflict-free LDS.128, row-major lanes)
@@ -85,11 +90,11 @@ __device__ __forceinline__ ATile analysis_tile(const AnalysisArgs& a, int b, int
 // outputs (beyond the plane) are clamped.  Caller synchronises.
 __device__ __forceinline__ void analysis_tables(const AnalysisArgs& a, const ATile& g, int* s_iy, int* s_ix,
                                                 int* s_rmap, int* s_cmap) {
-    for (int i = threadIdx.x; i < AIN; i += 256) {
+    for (int i = threadIdx.x; i < AIN; i += A_NT) {
         s_iy[i] = mirror(2 * g.cy0 - 6 + i, a.NH);
         s_ix[i] = mirror(2 * g.cx0 - 6 + i, a.NW);
     }
-    for (int i = threadIdx.x; i < AR; i += 256) {
+    for (int i = threadIdx.x; i < AR; i += A_NT) {
         const int mr = mirror(g.cy0 + i, a.nH) - g.cy0;
         const int mc = mirror(g.cx0 + i, a.nW) - g.cx0;
         s_rmap[i] = (mr >= 0 && mr < AR) ? mr : i;
@@ -119,7 +124,7 @@ __device__ __forceinline__ void rowpass_item(const float (&v)[24], float* s_row,
 
 // fp32 input tile [AIN][IN_P]: item = (row, 8 coefficient columns), 6 LDS.128
 __device__ __forceinline__ void rowpass_f32(const float* s_in, float* s_row) {
-    for (int it = threadIdx.x; it < AIN * (AR / 8); it += 256) {
+    for (int it = threadIdx.x; it < AIN * (AR / 8); it += A_NT) {
         const int r = it % AIN, cg = it / AIN;
         const float4* src = reinterpret_cast<const float4*>(s_in + r * IN_P + 16 * cg);
         float v[24];
@@ -145,7 +150,7 @@ __device__ __forceinline__ float u8_to_f32(uint32_t w, int k) {
 // must start on a 16-byte boundary (measured: other x offsets fault).
 constexpr int U8_OFF = 2;
 __device__ __forceinline__ void rowpass_u8(const uint8_t* s_in8, float* s_row) {
-    for (int it = threadIdx.x; it < AIN * (AR / 8); it += 256) {
+    for (int it = threadIdx.x; it < AIN * (AR / 8); it += A_NT) {
         const int r = it % AIN, cg = it / AIN;
         const uint8_t* src = s_in8 + r * U8_P + 16 * cg;
         const uint4 w0 = *reinterpret_cast<const uint4*>(src);
@@ -163,15 +168,17 @@ __device__ __forceinline__ void rowpass_u8(const uint8_t* s_in8, float* s_row) {
 // 8 coefficient rows) from 22 rows of lo and hi.  Details -> s_det, the inner
 // approximation -> global (next level's input).
 __device__ __forceinline__ void colpass(const AnalysisArgs& a, const ATile& g, const float* s_row, float* s_det) {
-    for (int it = threadIdx.x; it < AR * (AR / 8); it += 256) {
+    for (int it = threadIdx.x; it < AR * (AR / 8); it += A_NT) {
         // warps cover 32 consecutive columns of one row group (no bank-shifted wrap)
         const int c = it < 32 * (AR / 8) ? (it & 31) : 32 + ((it - 32 * (AR / 8)) % (AR - 32));
         const int rg = it < 32 * (AR / 8) ? (it >> 5) : (it - 32 * (AR / 8)) / (AR - 32);
         float lo[22], hi[22];
+        // rw_off(16 rg + k) = (16 RW_P + 8) rg + RW_P k + 8 (k >> 4) for k < 32
+        const float* lo_base = s_row + (16 * RW_P + 8) * rg + c;
 #pragma unroll
         for (int k = 0; k < 22; ++k) {
-            lo[k] = s_row[rw_off(16 * rg + k) + c];
-            hi[k] = s_row[RW_PLANE + rw_off(16 * rg + k) + c];
+            lo[k] = lo_base[RW_P * k + 8 * (k >> 4)];
+            hi[k] = lo_base[RW_PLANE + RW_P * k + 8 * (k >> 4)];
         }
         const bool inner_c = (c >= kHalo) && (c < kHalo + AT) && (g.x0 + c - kHalo < a.nW);
         // approximation of region row rr goes to plane row y0 + rr - kHalo
@@ -295,22 +302,22 @@ __device__ __forceinline__ void shrink3(const AnalysisArgs& a, const ATile& g, c
 #ifdef PRNU_SEQ_SHRINK
 #pragma unroll 1
     for (int s = 0; s < 3; ++s) {
-        for (int it = tid; it < VI; it += 256) shrink_v(g, s_det + s * AR * DT_P, s_v, s_rmap, s_cmap, it);
+        for (int it = tid; it < VI; it += A_NT) shrink_v(g, s_det + s * AR * DT_P, s_v, s_rmap, s_cmap, it);
         __syncthreads();
-        for (int it = tid; it < HI; it += 256)
+        for (int it = tid; it < HI; it += A_NT)
             shrink_h(a, g, s_det + s * AR * DT_P, s_v, s_cmap,
                      (s == 0 ? a.d0 : s == 1 ? a.d1 : a.d2) + (size_t)g.b * a.out_bstride, it);
         __syncthreads();
     }
     return;
 #endif
-    for (int it = tid; it < VI; it += 256) shrink_v(g, s_det, s_v, s_rmap, s_cmap, it);
+    for (int it = tid; it < VI; it += A_NT) shrink_v(g, s_det, s_v, s_rmap, s_cmap, it);
     __syncthreads();
 #pragma unroll 1
     for (int s = 0; s < 3; ++s) {
         // H of subband s (buffer s&1) together with V of subband s+1 (buffer (s+1)&1)
         const int n = HI + (s < 2 ? VI : 0);
-        for (int it = tid; it < n; it += 256) {
+        for (int it = tid; it < n; it += A_NT) {
             if (it < HI)
                 shrink_h(a, g, s_det + s * AR * DT_P, s_v + (s & 1) * V_PLANE4, s_cmap,
                          (s == 0 ? a.d0 : s == 1 ? a.d1 : a.d2) + (size_t)g.b * a.out_bstride, it);
@@ -324,7 +331,7 @@ __device__ __forceinline__ void shrink3(const AnalysisArgs& a, const ATile& g, c
 // Generic analysis kernel: one tile per CTA, mirrored input loaded with
 // ordinary loads (all in flight before the first shared store).
 template <typename TIn>
-__global__ void __launch_bounds__(256, 3) k_analysis_shrink(AnalysisArgs a) {
+__global__ void __launch_bounds__(A_NT, 3) k_analysis_shrink(AnalysisArgs a) {
     extern __shared__ __align__(128) float smem[];
     float* s_in = smem;                          // [AIN][IN_P]; later details [3][AR][DT_P]
     float* s_row = smem + A_SMEM_IN;             // [2][AIN][RW_P]; later vertical sums [AT][V_P4] float4
@@ -335,24 +342,29 @@ __global__ void __launch_bounds__(256, 3) k_analysis_shrink(AnalysisArgs a) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const ATile g = analysis_tile(a, blockIdx.z, blockIdx.y, blockIdx.x);
     const TIn* in = reinterpret_cast<const TIn*>(a.in) + (size_t)g.b * a.in_bstride;
-    analysis_tables(a, g, s_iy, s_ix, s_rmap, s_cmap);
-    __syncthreads();
     const int ix0 = 2 * g.cx0 - 6, iy0 = 2 * g.cy0 - 6;
-    if (sizeof(TIn) == 1 && ix0 >= 2 && iy0 >= 0 && ix0 - 2 + 88 <= a.NW && iy0 + AIN <= a.NH &&
-        ((reinterpret_cast<uintptr_t>(in) + (size_t)ix0 - 2) & 3) == 0 && (a.in_pitch & 3) == 0) {
+    const bool fast_u8 = sizeof(TIn) == 1 && ix0 >= 2 && iy0 >= 0 && ix0 - 2 + 88 <= a.NW && iy0 + AIN <= a.NH &&
+                         ((reinterpret_cast<uintptr_t>(in) + (size_t)ix0 - 2) & 3) == 0 && (a.in_pitch & 3) == 0;
+    if (!fast_u8 || g.bx || g.by) {   // mirror tables: only tiles that read mirrored samples need them
+        analysis_tables(a, g, s_iy, s_ix, s_rmap, s_cmap);
+        __syncthreads();
+    }
+    if (fast_u8) {
         // interior u8 tile: each row is 22 aligned words covering input columns
         // ix0-2 .. ix0+85; lane w widens its 4 bytes exactly (2^23 trick)
-        constexpr int RPW = (AIN + 7) / 8;
-        const uint8_t* base = reinterpret_cast<const uint8_t*>(in) + (size_t)iy0 * a.in_pitch + ix0 - 2;
+        constexpr int RPW = (AIN + A_NW - 1) / A_NW;
+        const uint32_t* wp = reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(in) +
+                                                               (size_t)(iy0 + warp) * a.in_pitch + ix0 - 2) +
+                             min(lane, 21);
+        const size_t wstep = (size_t)A_NW * a.in_pitch / 4;   // A_NW rows, in 32-bit words
         uint32_t wv[RPW];
 #pragma unroll
-        for (int k = 0; k < RPW; ++k) {
-            const int r = min(warp + 8 * k, AIN - 1);
-            wv[k] = lane < 22 ? __ldg(reinterpret_cast<const uint32_t*>(base + (size_t)r * a.in_pitch) + lane) : 0u;
+        for (int k = 0; k < RPW; ++k) {   // rows warp + A_NW k (the last exists for some warps only)
+            wv[k] = (warp + A_NW * k < AIN) ? __ldg(wp + k * wstep) : 0u;
         }
 #pragma unroll
         for (int k = 0; k < RPW; ++k) {
-            const int r = warp + 8 * k;
+            const int r = warp + A_NW * k;
             if (r < AIN && lane < 22) {
                 const int c0 = 4 * lane - 2;   // tile column of byte 0
                 const float f0 = __uint_as_float(__byte_perm(wv[k], 0x4B000000u, 0x7540u)) - 8388608.0f;
@@ -365,20 +377,20 @@ __global__ void __launch_bounds__(256, 3) k_analysis_shrink(AnalysisArgs a) {
             }
         }
     } else {
-        constexpr int RPW = (AIN + 7) / 8;   // 11 rows per warp
+        constexpr int RPW = (AIN + A_NW - 1) / A_NW;   // rows per warp
         float v[RPW][3];
         int ixs[3];
 #pragma unroll
         for (int j = 0; j < 3; ++j) ixs[j] = s_ix[min(lane + 32 * j, AIN - 1)];
 #pragma unroll
         for (int k = 0; k < RPW; ++k) {
-            const TIn* row = in + (size_t)s_iy[min(warp + 8 * k, AIN - 1)] * a.in_pitch;
+            const TIn* row = in + (size_t)s_iy[min(warp + A_NW * k, AIN - 1)] * a.in_pitch;
 #pragma unroll
             for (int j = 0; j < 3; ++j) v[k][j] = (float)__ldg(row + ixs[j]);
         }
 #pragma unroll
         for (int k = 0; k < RPW; ++k) {
-            const int r = warp + 8 * k;
+            const int r = warp + A_NW * k;
 #pragma unroll
             for (int j = 0; j < 3; ++j) {
                 const int c = lane + 32 * j;
@@ -411,7 +423,7 @@ __device__ __forceinline__ bool u8_tile_interior(const AnalysisArgs& a, const AT
     return iy >= 0 && ix >= 0 && (ix & 15) == 0 && iy + AIN <= a.NH && ix + U8_OFF + AIN <= a.NW;
 }
 
-__global__ void __launch_bounds__(256, 3) k_analysis_u8_tma(const __grid_constant__ CUtensorMap in_map, AnalysisArgs a,
+__global__ void __launch_bounds__(A_NT, 3) k_analysis_u8_tma(const __grid_constant__ CUtensorMap in_map, AnalysisArgs a,
                                                            int tiles_x, int tiles_y, int n_tiles) {
     extern __shared__ __align__(128) unsigned char smem8[];
     uint8_t* s_in8 = smem8;
@@ -453,7 +465,7 @@ __global__ void __launch_bounds__(256, 3) k_analysis_u8_tma(const __grid_constan
         } else {
             __syncthreads();   // tables visible
             const uint8_t* in = reinterpret_cast<const uint8_t*>(a.in) + (size_t)g.b * a.in_bstride;
-            for (int e = tid; e < AIN * AIN; e += 256) {
+            for (int e = tid; e < AIN * AIN; e += A_NT) {
                 const int r = e / AIN, c = e - r * AIN;
                 s_in8[r * U8_P + U8_OFF + c] = __ldg(in + (size_t)s_iy[r] * a.in_pitch + s_ix[c]);
             }
@@ -833,15 +845,15 @@ static int denoise_front(const TIn* in, long long in_bstride, int in_pitch, int 
             if (tma_ok) {
                 const int tx = (int)grid.x, ty = (int)grid.y, n_tiles = tx * ty * nb;
                 const int ctas = std::min(n_tiles, 148 * 3);
-                k_analysis_u8_tma<<<ctas, 256, A8_SMEM_BYTES, st>>>(map, a, tx, ty, n_tiles);
+                k_analysis_u8_tma<<<ctas, A_NT, A8_SMEM_BYTES, st>>>(map, a, tx, ty, n_tiles);
             } else {
-                k_analysis_shrink<TIn><<<grid, 256, A_SMEM_BYTES, st>>>(a);
+                k_analysis_shrink<TIn><<<grid, A_NT, A_SMEM_BYTES, st>>>(a);
             }
         } else {
             a.in = pb.approx[l - 1];
             a.in_bstride = (long long)pb.bstride[l - 1];
             a.in_pitch = p.pitch[l - 1];
-            k_analysis_shrink<float><<<grid, 256, A_SMEM_BYTES, st>>>(a);
+            k_analysis_shrink<float><<<grid, A_NT, A_SMEM_BYTES, st>>>(a);
         }
         count_launch();
         if ((rc = check_launch("k_analysis_shrink"))) return rc;
