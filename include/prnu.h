@@ -196,6 +196,23 @@ int prnu_pce(void* plan, const float* residual, const float* template_, int batc
 int prnu_pce_plan_destroy(void* plan);
 
 /* ---------------------------------------------------------------------------
+ * f1  Block-wise matching — P:266 ("divided each full resolution fingerprint
+ * into 500x500 disjoint blocks"), P:321, S:275-278 (BlockGrid).
+ * The H x W frame is cut into disjoint block x block tiles in row-major order
+ * (edge tiles smaller, kept; n_tiles = ceil(H/block) * ceil(W/block)).  For each
+ * tile: the aligned PCE (peak fixed at (0,0) of the tile's own circular
+ * correlation surface of the mean-removed residual and template tiles, as
+ * prnu_pce with aligned = 1) and the aligned NCC of the tile (as prnu_ncc).
+ * residual, template_: fp32 [H][W] (device); pce, ncc: fp64 [n_tiles] (device).
+ * prnu_block_plan_create: cuFFT plans for the (at most four) tile sizes;
+ *   *n_tiles_host and *ws_bytes (host) receive the tile count and workspace.
+ * ------------------------------------------------------------------------- */
+int prnu_block_plan_create(int H, int W, int block, int* n_tiles_host, size_t* ws_bytes, void** plan);
+int prnu_block_match(void* plan, const float* residual, const float* template_, int exclusion_half, double* pce,
+                     double* ncc, void* ws, size_t ws_bytes, void* stream);
+int prnu_block_plan_destroy(void* plan);
+
+/* ---------------------------------------------------------------------------
  * Diagnostics.
  * prnu_last_error: thread-local text of the last failure ("" if none).
  * prnu_kernel_launches: process-wide count of kernels this library has

@@ -78,3 +78,27 @@ def pce(R, T, exclusion_half: int = 5, aligned: bool = False):
     """Returns (pce, (dy, dx), peak_value).  aligned=True fixes the peak at (0,0)."""
     C = correlation_surface(R, T)
     return pce_from_surface(C, exclusion_half, peak=(0, 0) if aligned else None)
+
+
+def block_grid(H: int, W: int, block: int = 500):
+    """S:275-278 BlockGrid: disjoint block x block tiles covering the frame in
+    row-major order; edge tiles are smaller and kept (never empty).
+    Returns [(y, x, h, w)]."""
+    if block < 1:
+        raise ValueError("block must be >= 1")
+    return [(y, x, min(block, H - y), min(block, W - x)) for y in range(0, H, block) for x in range(0, W, block)]
+
+
+def blockwise_match(R, T, block: int = 500, exclusion_half: int = 5):
+    """S:311-314 ("500x500 disjoint blocks"): one aligned
+    correlation per tile (no shift search): PCE with the peak fixed at (0,0) of
+    the tile's own circular correlation surface, and the aligned NCC of the
+    tile.  Returns [(y, x, h, w, pce, ncc)] in row-major tile order."""
+    R = np.asarray(R, dtype=np.float64)
+    T = np.asarray(T, dtype=np.float64)
+    out = []
+    for (y, x, h, w) in block_grid(R.shape[0], R.shape[1], block):
+        r, t = R[y:y + h, x:x + w], T[y:y + h, x:x + w]
+        p, _, _ = pce(r, t, exclusion_half, aligned=True)
+        out.append((y, x, h, w, p, ncc(r, t)))
+    return out

@@ -101,6 +101,11 @@ _sig("prnu_pce_template", _i, _vp, _i, _vp, _i, _i, _i, _vp, _vp)
 _sig("prnu_pce_plan_create", _i, _i, _i, _i, ctypes.POINTER(_sz), ctypes.POINTER(_vp))
 _sig("prnu_pce", _i, _vp, _vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _sz, _vp)
 _sig("prnu_pce_plan_destroy", _i, _vp)
+_sig("prnu_block_plan_create", _i, _i, _i, _i, ctypes.POINTER(_i), ctypes.POINTER(_sz), ctypes.POINTER(_vp))
+_sig("prnu_block_match", _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _sz, _vp)
+_sig("prnu_block_plan_destroy", _i, _vp)
+_sig("prnu_profile_begin", _i)
+_sig("prnu_profile_end", _i, _i, ctypes.c_char_p, ctypes.POINTER(_d), ctypes.POINTER(_i64), ctypes.POINTER(_i))
 _sig("prnu_last_error", ctypes.c_char_p)
 _sig("prnu_kernel_launches", ctypes.c_uint64)
 _sig("prnu_version", ctypes.c_char_p)
@@ -384,6 +389,54 @@ def pce(R: torch.Tensor, T: torch.Tensor, exclusion_half: int = 5, aligned: bool
 
 
 prnu_pce = pce
+
+
+class BlockPlan:
+    """f1 block-wise matching: per-tile aligned PCE and
+    NCC over block x block tiles (edge tiles kept), row-major tile order."""
+
+    def __init__(self, H: int, W: int, block: int = 500, device="cuda"):
+        self.H, self.W, self.block = H, W, block
+        n = _i()
+        nb = _sz()
+        h = _vp()
+        _check(_lib.prnu_block_plan_create(H, W, block, ctypes.byref(n), ctypes.byref(nb), ctypes.byref(h)),
+               "prnu_block_plan_create")
+        self._h = h
+        self.n_tiles = int(n.value)
+        self.nbytes = int(nb.value)
+        self.ws = _ws(self.nbytes, device)
+        self.device = device
+
+    def tiles(self):
+        """[(y, x, h, w)] in row-major order."""
+        b = self.block
+        return [(y, x, min(b, self.H - y), min(b, self.W - x)) for y in range(0, self.H, b)
+                for x in range(0, self.W, b)]
+
+    def __call__(self, R: torch.Tensor, T: torch.Tensor, exclusion_half: int = 5):
+        _dev(R, torch.float32, "residual", (2,))
+        _dev(T, torch.float32, "template", (2,))
+        if R.shape != (self.H, self.W) or T.shape != R.shape:
+            raise ValueError("dimension mismatch with the plan")
+        pce = torch.empty(self.n_tiles, dtype=torch.float64, device=R.device)
+        ncc = torch.empty(self.n_tiles, dtype=torch.float64, device=R.device)
+        _check(_lib.prnu_block_match(self._h, _ptr(R), _ptr(T), exclusion_half, _ptr(pce), _ptr(ncc), _ptr(self.ws),
+                                     self.nbytes, _stream()), "prnu_block_match")
+        return pce, ncc
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _lib.prnu_block_plan_destroy(h)
+            self._h = None
+
+
+def block_match(R: torch.Tensor, T: torch.Tensor, block: int = 500, exclusion_half: int = 5):
+    return BlockPlan(R.shape[-2], R.shape[-1], block, R.device)(R, T, exclusion_half)
+
+
+prnu_block_match = block_match
 
 
 def header_symbols() -> list[str]:

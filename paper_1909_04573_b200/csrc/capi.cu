@@ -114,6 +114,11 @@ int pce_plan_destroy(void* plan);
 int pce_plan_dims(void* plan, int* H, int* W, int* batch, size_t* ws_bytes);
 int run_pce(void* plan, const float* R, const float* T, int excl, int aligned, double* pce, int* py, int* px,
             double* peak, void* ws, cudaStream_t st);
+int block_plan_create(int H, int W, int block, int* n_tiles, size_t* ws_bytes, void** out);
+int block_plan_destroy(void* plan);
+int block_plan_dims(void* plan, int* H, int* W, int* n_tiles, size_t* ws_bytes);
+int run_block_match(void* plan, const float* R, const float* T, int excl, double* pce_out, double* ncc_out, void* ws,
+                    cudaStream_t st);
 
 static size_t residual_ws(int batch, int H, int W, const Pyramid& pyr) {
     return align_up(sizeof(float) * pyramid_floats_per_frame(pyr) * (size_t)batch, 256) + zm_workspace_bytes(H, W);
@@ -467,6 +472,27 @@ int prnu_pce(void* plan, const float* residual, const float* template_, int batc
 }
 
 int prnu_pce_plan_destroy(void* plan) { return pce_plan_destroy(plan); }
+
+int prnu_block_plan_create(int H, int W, int block, int* n_tiles_host, size_t* ws_bytes, void** plan) {
+    int rc;
+    if (!n_tiles_host || !ws_bytes || !plan) return fail(PRNU_INVALID_ARG, "null pointer");
+    if ((rc = check_dims(H, W))) return rc;
+    if (block < 2) return fail(PRNU_BAD_PARAMETER, "block must be >= 2");
+    return block_plan_create(H, W, block, n_tiles_host, ws_bytes, plan);
+}
+
+int prnu_block_match(void* plan, const float* residual, const float* template_, int exclusion_half, double* pce,
+                     double* ncc, void* ws, size_t ws_bytes, void* stream) {
+    if (!plan || !residual || !template_ || !pce || !ncc || !ws) return fail(PRNU_INVALID_ARG, "null pointer");
+    int H, W, n;
+    size_t need;
+    block_plan_dims(plan, &H, &W, &n, &need);
+    if (exclusion_half < 0) return fail(PRNU_BAD_PARAMETER, "exclusion_half must be >= 0");
+    if (ws_bytes < need) return fail(PRNU_WORKSPACE_TOO_SMALL, "workspace too small");
+    return run_block_match(plan, residual, template_, exclusion_half, pce, ncc, ws, as_stream(stream));
+}
+
+int prnu_block_plan_destroy(void* plan) { return block_plan_destroy(plan); }
 
 int prnu_profile_begin(void) {
     std::lock_guard<std::mutex> lk(g_prof_mu);

@@ -281,4 +281,155 @@ int run_pce(void* plan, const float* R, const float* T, int excl, int aligned, d
     return check_launch("pce reductions");
 }
 
+// ---------------------------------------------------------------- f1: block-wise matching
+// P:266 ("divided each full resolution fingerprint into 500x500 disjoint
+// blocks"); S:275-278 (BlockGrid: disjoint tiles, edge tiles kept),
+// S:311-314 (one aligned correlation per tile, no shift search).  Tiles fall in
+// at most four size classes (full/last row x full/last column); each class is
+// gathered into a contiguous batch and runs the PCE pipeline with the peak
+// fixed at (0,0) of the tile's own surface, plus the aligned NCC of the tile.
+struct BlockClass {
+    int h, w, ty0, tx0, nty, ntx, count;
+    void* plan;          // PcePlan for [count][h][w]
+    size_t pce_ws;
+};
+
+struct BlockPlan {
+    int H, W, block, n_ty, n_tx, n_tiles, n_classes;
+    BlockClass cls[4];
+    size_t gather_bytes;   // largest class: R and T batches
+    size_t pce_ws;         // largest class PCE workspace
+    size_t ws_bytes;
+};
+
+size_t ncc_workspace_bytes(int batch);
+int launch_ncc(const float* a, const float* b, int batch, long long P, double* out, void* ws, cudaStream_t st);
+
+__global__ void __launch_bounds__(256) k_gather_tiles(const float* __restrict__ src, int W, int block, int ty0,
+                                                       int tx0, int ntx, int h, int w, float* __restrict__ dst) {
+    const int i = blockIdx.y;
+    const int ty = ty0 + i / ntx, tx = tx0 + i % ntx;
+    const float* s0 = src + (size_t)ty * block * W + (size_t)tx * block;
+    float* d0 = dst + (size_t)i * h * w;
+    for (int e = blockIdx.x * 256 + threadIdx.x; e < h * w; e += 256 * gridDim.x) {
+        const int y = e / w, x = e - y * w;
+        d0[e] = s0[(size_t)y * W + x];
+    }
+}
+
+__global__ void k_scatter_tiles(const double* __restrict__ pce_c, const double* __restrict__ ncc_c, int count,
+                                int ty0, int tx0, int ntx, int n_tx, double* __restrict__ pce_out,
+                                double* __restrict__ ncc_out) {
+    for (int i = threadIdx.x; i < count; i += blockDim.x) {
+        const int id = (ty0 + i / ntx) * n_tx + tx0 + i % ntx;
+        pce_out[id] = pce_c[i];
+        ncc_out[id] = ncc_c[i];
+    }
+}
+
+int block_plan_create(int H, int W, int block, int* n_tiles, size_t* ws_bytes, void** out) {
+    BlockPlan* bp = new BlockPlan{};
+    bp->H = H;
+    bp->W = W;
+    bp->block = block;
+    bp->n_ty = (H + block - 1) / block;
+    bp->n_tx = (W + block - 1) / block;
+    bp->n_tiles = bp->n_ty * bp->n_tx;
+    const int fy = H / block, fx = W / block;          // full tiles per column / row
+    const int ry = H - fy * block, rx = W - fx * block; // remainders (0: none)
+    const int ys[2][3] = {{block, 0, fy}, {ry, fy, ry ? 1 : 0}};   // (h, ty0, nty)
+    const int xs[2][3] = {{block, 0, fx}, {rx, fx, rx ? 1 : 0}};
+    int rc = PRNU_OK;
+    for (int a = 0; a < 2 && rc == PRNU_OK; ++a)
+        for (int c = 0; c < 2 && rc == PRNU_OK; ++c) {
+            BlockClass k{};
+            k.h = ys[a][0];
+            k.ty0 = ys[a][1];
+            k.nty = ys[a][2];
+            k.w = xs[c][0];
+            k.tx0 = xs[c][1];
+            k.ntx = xs[c][2];
+            k.count = k.nty * k.ntx;
+            if (k.count == 0 || k.h == 0 || k.w == 0) continue;
+            rc = pce_plan_create(k.h, k.w, k.count, &k.pce_ws, &k.plan);
+            if (rc) break;
+            bp->cls[bp->n_classes++] = k;
+            bp->gather_bytes = std::max(bp->gather_bytes, 2 * align_up(sizeof(float) * k.count * k.h * k.w, 256));
+            bp->pce_ws = std::max(bp->pce_ws, k.pce_ws);
+        }
+    if (rc) {
+        for (int i = 0; i < bp->n_classes; ++i) pce_plan_destroy(bp->cls[i].plan);
+        delete bp;
+        return rc;
+    }
+    // per-class outputs: pce, peak (fp64), peak_y, peak_x (int32), ncc (fp64)
+    const size_t outs = 3 * align_up(sizeof(double) * bp->n_tiles, 256) + 2 * align_up(sizeof(int) * bp->n_tiles, 256);
+    bp->ws_bytes = bp->gather_bytes + bp->pce_ws + align_up(ncc_workspace_bytes(bp->n_tiles), 256) + outs;
+    *n_tiles = bp->n_tiles;
+    *ws_bytes = bp->ws_bytes;
+    *out = bp;
+    return PRNU_OK;
+}
+
+int block_plan_destroy(void* plan) {
+    BlockPlan* bp = reinterpret_cast<BlockPlan*>(plan);
+    if (!bp) return PRNU_OK;
+    for (int i = 0; i < bp->n_classes; ++i) pce_plan_destroy(bp->cls[i].plan);
+    delete bp;
+    return PRNU_OK;
+}
+
+int block_plan_dims(void* plan, int* H, int* W, int* n_tiles, size_t* ws_bytes) {
+    BlockPlan* bp = reinterpret_cast<BlockPlan*>(plan);
+    *H = bp->H;
+    *W = bp->W;
+    *n_tiles = bp->n_tiles;
+    *ws_bytes = bp->ws_bytes;
+    return PRNU_OK;
+}
+
+int run_block_match(void* plan, const float* R, const float* T, int excl, double* pce_out, double* ncc_out, void* ws,
+                    cudaStream_t st) {
+    BlockPlan* bp = reinterpret_cast<BlockPlan*>(plan);
+    char* c = reinterpret_cast<char*>(ws);
+    float* Rg = reinterpret_cast<float*>(c);
+    float* Tg = reinterpret_cast<float*>(c + bp->gather_bytes / 2);
+    c += bp->gather_bytes;
+    void* pce_ws = c;
+    c += bp->pce_ws;
+    void* ncc_ws = c;
+    c += align_up(ncc_workspace_bytes(bp->n_tiles), 256);
+    double* pc = reinterpret_cast<double*>(c);
+    c += align_up(sizeof(double) * bp->n_tiles, 256);
+    double* pk = reinterpret_cast<double*>(c);
+    c += align_up(sizeof(double) * bp->n_tiles, 256);
+    double* nc = reinterpret_cast<double*>(c);
+    c += align_up(sizeof(double) * bp->n_tiles, 256);
+    int* py = reinterpret_cast<int*>(c);
+    c += align_up(sizeof(int) * bp->n_tiles, 256);
+    int* px = reinterpret_cast<int*>(c);
+    int rc;
+    for (int i = 0; i < bp->n_classes; ++i) {
+        const BlockClass& k = bp->cls[i];
+        const long long P = (long long)k.h * k.w;
+        dim3 grid((unsigned)std::min<long long>((P + 255) / 256, 64), k.count);
+        {
+            KTimer kt("block_gather", st);
+            k_gather_tiles<<<grid, 256, 0, st>>>(R, bp->W, bp->block, k.ty0, k.tx0, k.ntx, k.h, k.w, Rg);
+            k_gather_tiles<<<grid, 256, 0, st>>>(T, bp->W, bp->block, k.ty0, k.tx0, k.ntx, k.h, k.w, Tg);
+        }
+        count_launch(2);
+        if ((rc = check_launch("k_gather_tiles"))) return rc;
+        if ((rc = run_pce(k.plan, Rg, Tg, excl, 1, pc, py, px, pk, pce_ws, st))) return rc;
+        if ((rc = launch_ncc(Rg, Tg, k.count, P, nc, ncc_ws, st))) return rc;
+        {
+            KTimer kt("block_scatter", st);
+            k_scatter_tiles<<<1, 256, 0, st>>>(pc, nc, k.count, k.ty0, k.tx0, k.ntx, bp->n_tx, pce_out, ncc_out);
+        }
+        count_launch();
+        if ((rc = check_launch("k_scatter_tiles"))) return rc;
+    }
+    return PRNU_OK;
+}
+
 }  // namespace prnu

@@ -272,3 +272,38 @@ def test_launch_counter_advances(prnu):
     before = prnu.kernel_launches()
     prnu.residual(torch.zeros((1, 64, 64), device="cuda"))
     assert prnu.kernel_launches() - before == 8   # 4 analysis + 4 synthesis
+
+
+# ---------------------------------------------------------------- f1 block-wise
+@pytest.mark.parametrize("H,W,block", [(130, 170, 50), (512, 1024, 500), (96, 64, 32)])
+def test_block_match_matches_oracle(prnu, H, W, block):
+    """per-tile aligned PCE and NCC, edge tiles kept."""
+    g = np.random.default_rng(H + W)
+    T = g.normal(0, 1, (H, W)).astype(np.float32)
+    R = (0.2 * T + g.normal(0, 1, (H, W))).astype(np.float32)
+    plan = prnu.BlockPlan(H, W, block)
+    pce, ncc = plan(torch.from_numpy(R).cuda(), torch.from_numpy(T).cuda())
+    ref = oracle.blockwise_match(R, T, block)
+    assert plan.n_tiles == len(ref) and plan.tiles() == [r[:4] for r in ref]
+    pce, ncc = pce.cpu().numpy(), ncc.cpu().numpy()
+    for i, (y, x, h, w, p, c) in enumerate(ref):
+        assert abs(pce[i] - p) <= PCE_RTOL * abs(p), (i, pce[i], p)
+        assert abs(ncc[i] - c) <= NCC_TOL
+
+
+def test_block_match_fhd_directional(prnu):
+    """Full-HD query vs its camera's fingerprint, 500x500 blocks (12 tiles incl.
+    80-row and 420-column edge tiles): matched blocks exceed the threshold."""
+    v = synth.video("drift", 201, 1080, 1920, seed=6, sigma_n=2.0, device="cuda")
+    fp = prnu.extract_fingerprint(v.frames[:200], 10, batch=20)
+    q = v.frames[200:201]
+    R = prnu.residual(q, zero_mean=True)[0]
+    T = prnu.pce_template(fp.K, q)[0]
+    pce, ncc = prnu.block_match(R, T, 500)
+    assert pce.numel() == 12
+    full = [i for i, (y, x, h, w) in enumerate(prnu.BlockPlan(1080, 1920, 500).tiles()) if h == 500 and w == 500]
+    assert (pce[full] > 60).all()
+    ref = oracle.blockwise_match(R.cpu().numpy(), T.cpu().numpy(), 500)
+    for i, r in enumerate(ref):
+        assert abs(pce[i].item() - r[4]) <= PCE_RTOL * abs(r[4])
+        assert abs(ncc[i].item() - r[5]) <= NCC_TOL

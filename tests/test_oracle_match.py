@@ -116,3 +116,28 @@ def test_aligned_pce_uses_origin():
 def test_threshold_strict():
     """pce exactly 60 -> no match (strict '>')."""
     assert not (60.0 > match.PCE_THRESHOLD)
+
+
+def test_block_grid_spec_examples():
+    """1000x500 frame, block 500 -> 2 tiles; 1024x512 -> edge tiles kept."""
+    g = match.block_grid(500, 1000, 500)      # H=500 rows, W=1000 cols
+    assert g == [(0, 0, 500, 500), (0, 500, 500, 500)]
+    g = match.block_grid(512, 1024, 500)
+    assert len(g) == 6 and (0, 1000, 500, 24) in g and (500, 1000, 12, 24) in g
+    assert sum(h * w for (_, _, h, w) in g) == 512 * 1024             # disjoint cover
+    assert len(match.block_grid(1000, 1000, 500)) == 4               # S:557
+
+
+def test_blockwise_equals_per_tile_aligned_pce():
+    rng = np.random.default_rng(9)
+    T = rng.normal(size=(70, 90))
+    R = 0.3 * T + rng.normal(size=T.shape)
+    res = match.blockwise_match(R, T, block=32)
+    assert len(res) == 3 * 3
+    for (y, x, h, w, p, c) in res:
+        r, t = R[y:y + h, x:x + w], T[y:y + h, x:x + w]
+        C = brute_surface(r, t)                       # direct correlation of the tile
+        pp = match.pce_from_surface(C, 5, peak=(0, 0))[0]
+        assert abs(p - pp) <= 1e-9 * abs(pp)
+        assert abs(c - oracle.ncc(r, t)) < 1e-12
+        assert p > 0 and c > 0.1                      # matched tiles correlate
