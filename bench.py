@@ -38,7 +38,7 @@ def parse():
     ap.add_argument("--height", type=int, default=1080)
     ap.add_argument("--width", type=int, default=1920)
     ap.add_argument("--depths", default="1,50")
-    ap.add_argument("--batch", type=int, default=32, help="SDA frames denoised per wave at depth 1")
+    ap.add_argument("--batch", type=int, default=64, help="SDA frames denoised per wave at depth 1")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true")

@@ -127,11 +127,13 @@ static size_t residual_ws(int batch, int H, int W, const Pyramid& pyr) {
 // Waves of SDA frames alternate between kExtractStreams streams (each with its
 // own pyramid/SDA workspace) so one wave's small levels overlap the next wave's
 // large ones; only the accumulating launches are chained (ascending order).
+constexpr int kMaxExtractStreams = 4;
+
 static int extract_streams() {
     static const int n = [] {
         const char* e = getenv("PRNU_STREAMS");
         int v = e ? atoi(e) : 2;
-        return v < 1 ? 1 : (v > 2 ? 2 : v);
+        return v < 1 ? 1 : (v > kMaxExtractStreams ? kMaxExtractStreams : v);
     }();
     return n;
 }
@@ -310,35 +312,40 @@ int prnu_extract_fingerprint(const uint8_t* frames, int64_t m, int H, int W, int
         }
         return launch_finalize(sum_WI, sum_I2, H, W, eps, 1, K_out, zm, st);
     }
-    // two streams: waves alternate; accumulations chained by events
-    cudaStream_t s1 = nullptr;
-    cudaEvent_t ev_start = nullptr, ev_end = nullptr, acc[2] = {nullptr, nullptr};
-    cudaError_t e = cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_end, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&acc[0], cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&acc[1], cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventRecord(ev_start, st);            // s1 starts after the caller's prior work
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(s1, ev_start, 0);
+    // nst streams: waves rotate over them; each wave's accumulation waits for the
+    // previous wave's (events), so the per-pixel order stays ascending
+    cudaStream_t sts[kMaxExtractStreams] = {st, nullptr, nullptr, nullptr};
+    cudaEvent_t ev_start = nullptr, ev_end[kMaxExtractStreams] = {}, acc[kMaxExtractStreams] = {};
+    cudaError_t e = cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
+    for (int j = 0; j < nst && e == cudaSuccess; ++j) {
+        if (j > 0) e = cudaStreamCreateWithFlags(&sts[j], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_end[j], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&acc[j], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(ev_start, st);   // helper streams start after the caller's prior work
+    for (int j = 1; j < nst && e == cudaSuccess; ++j) e = cudaStreamWaitEvent(sts[j], ev_start, 0);
     rc = (e == cudaSuccess) ? PRNU_OK : fail(PRNU_CUDA_ERROR, std::string("stream setup: ") + cudaGetErrorString(e));
-    cudaStream_t sts[2] = {st, s1};
     int64_t k = 0;
     for (int64_t g0 = 0; g0 < ns && rc == PRNU_OK; g0 += batch, ++k) {
         int64_t nb = std::min<int64_t>(batch, ns - g0);
-        const int j = (int)(k & 1);
+        const int j = (int)(k % nst), jp = (int)((k + nst - 1) % nst);
         rc = extract_chunk(frames + (size_t)g0 * depth * P, nb, H, W, depth, pyr, sp, sum_WI, sum_I2,
-                           wsb + j * wave, sts[j], k > 0 ? acc[j ^ 1] : nullptr, acc[j]);
+                           wsb + j * wave, sts[j], k > 0 ? acc[jp] : nullptr, acc[j]);
     }
-    if (rc == PRNU_OK) {
-        e = cudaEventRecord(ev_end, s1);                               // the caller's stream sees all waves
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev_end, 0);
+    for (int j = 1; j < nst && rc == PRNU_OK; ++j) {   // the caller's stream sees all waves
+        e = cudaEventRecord(ev_end[j], sts[j]);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev_end[j], 0);
         if (e != cudaSuccess) rc = fail(PRNU_CUDA_ERROR, std::string("stream join: ") + cudaGetErrorString(e));
     }
     if (rc == PRNU_OK) rc = launch_finalize(sum_WI, sum_I2, H, W, eps, 1, K_out, zm, st);
     // destroying a stream/event with pending work is legal: resources are released on completion
-    if (s1) cudaStreamDestroy(s1);
-    for (cudaEvent_t ev : {ev_start, ev_end, acc[0], acc[1]})
-        if (ev) cudaEventDestroy(ev);
+    for (int j = 1; j < nst; ++j)
+        if (sts[j]) cudaStreamDestroy(sts[j]);
+    if (ev_start) cudaEventDestroy(ev_start);
+    for (int j = 0; j < nst; ++j) {
+        if (ev_end[j]) cudaEventDestroy(ev_end[j]);
+        if (acc[j]) cudaEventDestroy(acc[j]);
+    }
     return rc;
 }
 

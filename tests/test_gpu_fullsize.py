@@ -16,7 +16,7 @@ W_TOL = 1e-3
 K_TOL = 1e-3
 NCC_TOL = 1e-5
 PCE_RTOL = 1e-3
-BENCH_BATCH = 32
+BENCH_BATCH = 64
 
 
 @pytest.fixture(scope="module")
