@@ -142,6 +142,15 @@ int prnu_extract_fingerprint(const uint8_t* frames, int64_t m, int H, int W, int
                              double* sum_WI, double* sum_I2, int64_t* n_sda_host, void* ws,
                              size_t ws_bytes, void* stream);
 
+/* f4 I-frame emulation ("I-frames only"): stride selection.
+ * Frames 0, stride, 2 stride, ... < m are denoised one by one and accumulated
+ * exactly as the conventional pipeline; *n_used_host = ceil(m / stride).  The
+ * workspace is prnu_extract_workspace_bytes(H, W, batch, 1, p). */
+int prnu_extract_fingerprint_stride(const uint8_t* frames, int64_t m, int H, int W, int64_t stride,
+                                    const prnu_denoise_params* p, int batch, double eps, float* K_out,
+                                    double* sum_WI, double* sum_I2, int64_t* n_used_host, void* ws, size_t ws_bytes,
+                                    void* stream);
+
 /* Same, with the frames in (preferably page-locked) HOST memory and K written
  * to HOST memory: frames are streamed host->device in chunks of
  * `batch * depth` frames through a double-buffered staging area inside `ws`,

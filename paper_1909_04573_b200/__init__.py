@@ -92,6 +92,8 @@ _sig("prnu_fingerprint_finalize", _i, _vp, _vp, _i, _i, _d, _i, _vp, _vp, _sz, _
 _sig("prnu_extract_workspace_bytes", _sz, _i, _i, _i, _i64, _P)
 _sig("prnu_extract_fingerprint", _i, _vp, _i64, _i, _i, _i64, _P, _i, _d, _vp, _vp, _vp, ctypes.POINTER(_i64), _vp,
      _sz, _vp)
+_sig("prnu_extract_fingerprint_stride", _i, _vp, _i64, _i, _i, _i64, _P, _i, _d, _vp, _vp, _vp, ctypes.POINTER(_i64),
+     _vp, _sz, _vp)
 _sig("prnu_extract_host_workspace_bytes", _sz, _i, _i, _i, _i64, _P)
 _sig("prnu_extract_fingerprint_host", _i, _vp, _i64, _i, _i, _i64, _P, _i, _d, _vp, _vp, _vp,
      ctypes.POINTER(_i64), _vp, _sz, _vp)
@@ -299,6 +301,28 @@ def extract_fingerprint(frames: torch.Tensor, depth: int, params: DenoiseParams 
 
 
 prnu_extract_fingerprint = extract_fingerprint
+
+
+def extract_fingerprint_stride(frames: torch.Tensor, stride: int, params: DenoiseParams | None = None,
+                               batch: int = 16, eps: float = 1e-6) -> Fingerprint:
+    """f4 I-frame emulation: conventional fingerprint of the
+    frames 0, stride, 2 stride, ... (n = ceil(m / stride) denoisings)."""
+    _dev(frames, torch.uint8, "frames", (3,))
+    m, H, W = frames.shape
+    p = _params(params)
+    nbytes = _lib.prnu_extract_workspace_bytes(H, W, batch, 1, ctypes.byref(p))
+    ws = _ws(nbytes, frames.device)
+    s_wi = torch.empty((H, W), dtype=torch.float64, device=frames.device)
+    s_i2 = torch.empty_like(s_wi)
+    K = torch.empty((H, W), dtype=torch.float32, device=frames.device)
+    n = _i64()
+    _check(_lib.prnu_extract_fingerprint_stride(_ptr(frames), m, H, W, stride, ctypes.byref(p), batch, eps, _ptr(K),
+                                                _ptr(s_wi), _ptr(s_i2), ctypes.byref(n), _ptr(ws), nbytes, _stream()),
+           "prnu_extract_fingerprint_stride")
+    return Fingerprint(K, s_wi, s_i2, int(n.value), 1, m)
+
+
+prnu_extract_fingerprint_stride = extract_fingerprint_stride
 
 
 # ---------------------------------------------------------------- a7-a8

@@ -98,7 +98,7 @@ int run_residual(const TIn* in, int nb, int H, int W, const Pyramid& p, const Sh
 template <typename TIn>
 int run_residual_accumulate(const TIn* in, const TIn* I, int nb, int H, int W, const Pyramid& p,
                             const ShrinkParams& sp, double* num, double* den, float* ws_pyr, cudaStream_t st,
-                            cudaEvent_t acc_wait, cudaEvent_t acc_done);
+                            cudaEvent_t acc_wait, cudaEvent_t acc_done, long long frame_stride);
 int launch_accumulate(const float* W, const float* I, int batch, long long P, double* num, double* den,
                       cudaStream_t st);
 size_t zm_workspace_bytes(int H, int W);
@@ -156,18 +156,21 @@ static int check_dims(int H, int W) {
 
 // Shared by the device and host extraction entry points: process nb SDA groups
 // whose frames start at `frames` (device), with wave workspace `ws`.
+// depth > 0: SDA groups of `depth` consecutive frames.  depth < 0: stride
+// selection (f4), the frames are every |depth|-th frame, denoised one by one.
 static int extract_chunk(const uint8_t* frames, int64_t nb, int H, int W, int64_t depth, const Pyramid& pyr,
                          const ShrinkParams& sp, double* num, double* den, char* ws, cudaStream_t st,
                          cudaEvent_t acc_wait = nullptr, cudaEvent_t acc_done = nullptr) {
     float* pyr_ws = reinterpret_cast<float*>(ws);
     size_t pyr_bytes = align_up(sizeof(float) * pyramid_floats_per_frame(pyr) * (size_t)nb, 256);
-    if (depth == 1)
+    const long long P = (long long)H * W;
+    if (depth == 1 || depth < 0)
         return run_residual_accumulate<uint8_t>(frames, frames, (int)nb, H, W, pyr, sp, num, den, pyr_ws, st,
-                                                acc_wait, acc_done);
+                                                acc_wait, acc_done, depth < 0 ? -depth * P : P);
     float* S = reinterpret_cast<float*>(ws + pyr_bytes);
-    int rc = launch_sda_average(frames, nb, (long long)H * W, (int)depth, S, st);
+    int rc = launch_sda_average(frames, nb, P, (int)depth, S, st);
     if (rc) return rc;
-    return run_residual_accumulate<float>(S, S, (int)nb, H, W, pyr, sp, num, den, pyr_ws, st, acc_wait, acc_done);
+    return run_residual_accumulate<float>(S, S, (int)nb, H, W, pyr, sp, num, den, pyr_ws, st, acc_wait, acc_done, P);
 }
 
 template <typename TIn>
@@ -275,21 +278,26 @@ size_t prnu_extract_workspace_bytes(int H, int W, int batch, int64_t depth, cons
     return extract_ws(H, W, batch, depth, make_pyramid(H, W, p->levels));
 }
 
-int prnu_extract_fingerprint(const uint8_t* frames, int64_t m, int H, int W, int64_t depth,
-                             const prnu_denoise_params* p, int batch, double eps, float* K_out, double* sum_WI,
-                             double* sum_I2, int64_t* n_sda_host, void* ws, size_t ws_bytes, void* stream) {
+// mode 0: SDA depth `depth` (1 = conventional); mode 1: stride selection with
+// step `depth` (frames 0, depth, 2 depth, ... < m), each frame denoised.
+static int extract_impl(const uint8_t* frames, int64_t m, int H, int W, int64_t depth, int mode,
+                        const prnu_denoise_params* p, int batch, double eps, float* K_out, double* sum_WI,
+                        double* sum_I2, int64_t* n_sda_host, void* ws, size_t ws_bytes, void* stream) {
     int rc;
     if (!frames || !K_out || !sum_WI || !sum_I2 || !ws) return fail(PRNU_INVALID_ARG, "null pointer");
     if (batch < 1) return fail(PRNU_INVALID_ARG, "batch must be >= 1");
     if ((rc = check_dims(H, W))) return rc;
     int64_t ns;
     if ((rc = prnu_sda_groups(m, depth, &ns))) return rc;
-    if (depth > 65793) return fail(PRNU_BAD_PARAMETER, "depth > 65793");
+    if (mode == 1) ns = (m + depth - 1) / depth;   // frames 0, depth, 2 depth, ... < m
+    const int64_t unit = mode == 1 ? 1 : depth;      // frames per unit in the workspace sizing
+    const int64_t dsel = mode == 1 ? -depth : depth; // extract_chunk's depth argument
+    if (mode == 0 && depth > 65793) return fail(PRNU_BAD_PARAMETER, "depth > 65793");
     if (!(eps > 0.0)) return fail(PRNU_BAD_PARAMETER, "eps must be > 0");
     ShrinkParams sp;
     if ((rc = validate_params(p, H, W, &sp))) return rc;
     Pyramid pyr = make_pyramid(H, W, p->levels);
-    if (ws_bytes < extract_ws(H, W, batch, depth, pyr)) return fail(PRNU_WORKSPACE_TOO_SMALL, "workspace too small");
+    if (ws_bytes < extract_ws(H, W, batch, unit, pyr)) return fail(PRNU_WORKSPACE_TOO_SMALL, "workspace too small");
     if (n_sda_host) *n_sda_host = ns;
     cudaStream_t st = as_stream(stream);
     const size_t P = (size_t)H * W;
@@ -301,12 +309,12 @@ int prnu_extract_fingerprint(const uint8_t* frames, int64_t m, int H, int W, int
     // kernel's event pair measures that kernel alone
     const int nst = extract_streams();
     const bool serial = profiling_active();
-    const size_t wave = extract_wave_ws(H, W, batch, depth, pyr);
+    const size_t wave = extract_wave_ws(H, W, batch, unit, pyr);
     char* zm = wsb + nst * wave;
     if (nst == 1 || serial || ns <= batch) {
         for (int64_t g0 = 0; g0 < ns; g0 += batch) {
             int64_t nb = std::min<int64_t>(batch, ns - g0);
-            if ((rc = extract_chunk(frames + (size_t)g0 * depth * P, nb, H, W, depth, pyr, sp, sum_WI, sum_I2, wsb,
+            if ((rc = extract_chunk(frames + (size_t)g0 * depth * P, nb, H, W, dsel, pyr, sp, sum_WI, sum_I2, wsb,
                                     st)))
                 return rc;
         }
@@ -329,7 +337,7 @@ int prnu_extract_fingerprint(const uint8_t* frames, int64_t m, int H, int W, int
     for (int64_t g0 = 0; g0 < ns && rc == PRNU_OK; g0 += batch, ++k) {
         int64_t nb = std::min<int64_t>(batch, ns - g0);
         const int j = (int)(k % nst), jp = (int)((k + nst - 1) % nst);
-        rc = extract_chunk(frames + (size_t)g0 * depth * P, nb, H, W, depth, pyr, sp, sum_WI, sum_I2,
+        rc = extract_chunk(frames + (size_t)g0 * depth * P, nb, H, W, dsel, pyr, sp, sum_WI, sum_I2,
                            wsb + j * wave, sts[j], k > 0 ? acc[jp] : nullptr, acc[j]);
     }
     for (int j = 1; j < nst && rc == PRNU_OK; ++j) {   // the caller's stream sees all waves
@@ -347,6 +355,21 @@ int prnu_extract_fingerprint(const uint8_t* frames, int64_t m, int H, int W, int
         if (acc[j]) cudaEventDestroy(acc[j]);
     }
     return rc;
+}
+
+int prnu_extract_fingerprint(const uint8_t* frames, int64_t m, int H, int W, int64_t depth,
+                             const prnu_denoise_params* p, int batch, double eps, float* K_out, double* sum_WI,
+                             double* sum_I2, int64_t* n_sda_host, void* ws, size_t ws_bytes, void* stream) {
+    return extract_impl(frames, m, H, W, depth, 0, p, batch, eps, K_out, sum_WI, sum_I2, n_sda_host, ws, ws_bytes,
+                        stream);
+}
+
+int prnu_extract_fingerprint_stride(const uint8_t* frames, int64_t m, int H, int W, int64_t stride,
+                                    const prnu_denoise_params* p, int batch, double eps, float* K_out,
+                                    double* sum_WI, double* sum_I2, int64_t* n_used_host, void* ws, size_t ws_bytes,
+                                    void* stream) {
+    return extract_impl(frames, m, H, W, stride, 1, p, batch, eps, K_out, sum_WI, sum_I2, n_used_host, ws, ws_bytes,
+                        stream);
 }
 
 size_t prnu_extract_host_workspace_bytes(int H, int W, int batch, int64_t depth, const prnu_denoise_params* p) {

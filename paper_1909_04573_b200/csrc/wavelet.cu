@@ -89,12 +89,12 @@ __device__ __forceinline__ ATile analysis_tile(const AnalysisArgs& a, int b, int
 // inside the plane mirror into the region; indices that only feed discarded
 // outputs (beyond the plane) are clamped.  Caller synchronises.
 __device__ __forceinline__ void analysis_tables(const AnalysisArgs& a, const ATile& g, int* s_iy, int* s_ix,
-                                                int* s_rmap, int* s_cmap) {
-    for (int i = threadIdx.x; i < AIN; i += A_NT) {
+                                                int* s_rmap, int* s_cmap, int tid = threadIdx.x, int nthr = A_NT) {
+    for (int i = tid; i < AIN; i += nthr) {
         s_iy[i] = mirror(2 * g.cy0 - 6 + i, a.NH);
         s_ix[i] = mirror(2 * g.cx0 - 6 + i, a.NW);
     }
-    for (int i = threadIdx.x; i < AR; i += A_NT) {
+    for (int i = tid; i < AR; i += nthr) {
         const int mr = mirror(g.cy0 + i, a.nH) - g.cy0;
         const int mc = mirror(g.cx0 + i, a.nW) - g.cx0;
         s_rmap[i] = (mr >= 0 && mr < AR) ? mr : i;
@@ -123,8 +123,9 @@ __device__ __forceinline__ void rowpass_item(const float (&v)[24], float* s_row,
 }
 
 // fp32 input tile [AIN][IN_P]: item = (row, 8 coefficient columns), 6 LDS.128
-__device__ __forceinline__ void rowpass_f32(const float* s_in, float* s_row) {
-    for (int it = threadIdx.x; it < AIN * (AR / 8); it += A_NT) {
+__device__ __forceinline__ void rowpass_f32(const float* s_in, float* s_row, int tid = threadIdx.x,
+                                            int nthr = A_NT) {
+    for (int it = tid; it < AIN * (AR / 8); it += nthr) {
         const int r = it % AIN, cg = it / AIN;
         const float4* src = reinterpret_cast<const float4*>(s_in + r * IN_P + 16 * cg);
         float v[24];
@@ -149,8 +150,9 @@ __device__ __forceinline__ float u8_to_f32(uint32_t w, int k) {
 // The u8 tile row starts U8_OFF bytes before input column 2*cx0-6: u8 TMA boxes
 // must start on a 16-byte boundary (measured: other x offsets fault).
 constexpr int U8_OFF = 2;
-__device__ __forceinline__ void rowpass_u8(const uint8_t* s_in8, float* s_row) {
-    for (int it = threadIdx.x; it < AIN * (AR / 8); it += A_NT) {
+__device__ __forceinline__ void rowpass_u8(const uint8_t* s_in8, float* s_row, int tid = threadIdx.x,
+                                           int nthr = A_NT) {
+    for (int it = tid; it < AIN * (AR / 8); it += nthr) {
         const int r = it % AIN, cg = it / AIN;
         const uint8_t* src = s_in8 + r * U8_P + 16 * cg;
         const uint4 w0 = *reinterpret_cast<const uint4*>(src);
@@ -167,8 +169,9 @@ __device__ __forceinline__ void rowpass_u8(const uint8_t* s_in8, float* s_row) {
 // Column pass (along y): 4 subbands for the AR x AR region; item = (column,
 // 8 coefficient rows) from 22 rows of lo and hi.  Details -> s_det, the inner
 // approximation -> global (next level's input).
-__device__ __forceinline__ void colpass(const AnalysisArgs& a, const ATile& g, const float* s_row, float* s_det) {
-    for (int it = threadIdx.x; it < AR * (AR / 8); it += A_NT) {
+__device__ __forceinline__ void colpass(const AnalysisArgs& a, const ATile& g, const float* s_row, float* s_det,
+                                        int tid = threadIdx.x, int nthr = A_NT) {
+    for (int it = tid; it < AR * (AR / 8); it += nthr) {
         // warps cover 32 consecutive columns of one row group (no bank-shifted wrap)
         const int c = it < 32 * (AR / 8) ? (it & 31) : 32 + ((it - 32 * (AR / 8)) % (AR - 32));
         const int rg = it < 32 * (AR / 8) ? (it >> 5) : (it - 32 * (AR / 8)) / (AR - 32);
@@ -294,77 +297,62 @@ __device__ __forceinline__ void shrink_h(const AnalysisArgs& a, const ATile& g, 
     else shrink_h_t<false>(a, g, det, s_v, s_cmap, dst, it);
 }
 
+// CTA-wide barrier, or a named barrier over a warp group (bar.sync id, count).
+struct CtaBar {
+    __device__ __forceinline__ void sync() const { __syncthreads(); }
+};
+struct NamedBar {
+    int id, count;
+    __device__ __forceinline__ void sync() const {
+        asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+    }
+};
+
+template <class Bar>
 __device__ __forceinline__ void shrink3(const AnalysisArgs& a, const ATile& g, const float* s_det, float4* s_v,
-                                        const int* s_rmap, const int* s_cmap) {
+                                        const int* s_rmap, const int* s_cmap, Bar bar, int tid = threadIdx.x,
+                                        int nthr = A_NT) {
     constexpr int VI = AR * (AT / 8);   // 160 vertical items per subband
     constexpr int HI = AT * (AT / 8);   // 128 horizontal items per subband
-    const int tid = threadIdx.x;
-#ifdef PRNU_SEQ_SHRINK
-#pragma unroll 1
-    for (int s = 0; s < 3; ++s) {
-        for (int it = tid; it < VI; it += A_NT) shrink_v(g, s_det + s * AR * DT_P, s_v, s_rmap, s_cmap, it);
-        __syncthreads();
-        for (int it = tid; it < HI; it += A_NT)
-            shrink_h(a, g, s_det + s * AR * DT_P, s_v, s_cmap,
-                     (s == 0 ? a.d0 : s == 1 ? a.d1 : a.d2) + (size_t)g.b * a.out_bstride, it);
-        __syncthreads();
-    }
-    return;
-#endif
-    for (int it = tid; it < VI; it += A_NT) shrink_v(g, s_det, s_v, s_rmap, s_cmap, it);
-    __syncthreads();
+    for (int it = tid; it < VI; it += nthr) shrink_v(g, s_det, s_v, s_rmap, s_cmap, it);
+    bar.sync();
 #pragma unroll 1
     for (int s = 0; s < 3; ++s) {
         // H of subband s (buffer s&1) together with V of subband s+1 (buffer (s+1)&1)
         const int n = HI + (s < 2 ? VI : 0);
-        for (int it = tid; it < n; it += A_NT) {
+        for (int it = tid; it < n; it += nthr) {
             if (it < HI)
                 shrink_h(a, g, s_det + s * AR * DT_P, s_v + (s & 1) * V_PLANE4, s_cmap,
                          (s == 0 ? a.d0 : s == 1 ? a.d1 : a.d2) + (size_t)g.b * a.out_bstride, it);
             else
                 shrink_v(g, s_det + (s + 1) * AR * DT_P, s_v + ((s + 1) & 1) * V_PLANE4, s_rmap, s_cmap, it - HI);
         }
-        __syncthreads();
+        bar.sync();
     }
 }
 
-// Generic analysis kernel: one tile per CTA, mirrored input loaded with
-// ordinary loads (all in flight before the first shared store).
-template <typename TIn>
-__global__ void __launch_bounds__(A_NT, 3) k_analysis_shrink(AnalysisArgs a) {
-    extern __shared__ __align__(128) float smem[];
-    float* s_in = smem;                          // [AIN][IN_P]; later details [3][AR][DT_P]
-    float* s_row = smem + A_SMEM_IN;             // [2][AIN][RW_P]; later vertical sums [AT][V_P4] float4
-    int* s_iy = reinterpret_cast<int*>(s_row + A_SMEM_ROW);
-    int* s_ix = s_iy + AIN;
-    int* s_rmap = s_ix + AIN;
-    int* s_cmap = s_rmap + AR;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const ATile g = analysis_tile(a, blockIdx.z, blockIdx.y, blockIdx.x);
+// Input tile of one analysis tile into s_in [AIN][IN_P] (fp32), by NWARPS warps
+// (warp = 0..NWARPS-1).  Interior u8 tiles: each row is 22 aligned words covering
+// input columns ix0-2 .. ix0+85, widened exactly (2^23 trick); otherwise mirrored
+// element loads via the tables (which the caller computed and synchronised).
+// Returns nothing; the caller synchronises before the row pass.
+template <typename TIn, int NWARPS>
+__device__ __forceinline__ void load_tile(const AnalysisArgs& a, const ATile& g, bool fast_u8, float* s_in,
+                                          const int* s_iy, const int* s_ix, int warp, int lane) {
     const TIn* in = reinterpret_cast<const TIn*>(a.in) + (size_t)g.b * a.in_bstride;
-    const int ix0 = 2 * g.cx0 - 6, iy0 = 2 * g.cy0 - 6;
-    const bool fast_u8 = sizeof(TIn) == 1 && ix0 >= 2 && iy0 >= 0 && ix0 - 2 + 88 <= a.NW && iy0 + AIN <= a.NH &&
-                         ((reinterpret_cast<uintptr_t>(in) + (size_t)ix0 - 2) & 3) == 0 && (a.in_pitch & 3) == 0;
-    if (!fast_u8 || g.bx || g.by) {   // mirror tables: only tiles that read mirrored samples need them
-        analysis_tables(a, g, s_iy, s_ix, s_rmap, s_cmap);
-        __syncthreads();
-    }
+    constexpr int RPW = (AIN + NWARPS - 1) / NWARPS;   // rows per warp
     if (fast_u8) {
-        // interior u8 tile: each row is 22 aligned words covering input columns
-        // ix0-2 .. ix0+85; lane w widens its 4 bytes exactly (2^23 trick)
-        constexpr int RPW = (AIN + A_NW - 1) / A_NW;
+        const int ix0 = 2 * g.cx0 - 6, iy0 = 2 * g.cy0 - 6;
         const uint32_t* wp = reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(in) +
                                                                (size_t)(iy0 + warp) * a.in_pitch + ix0 - 2) +
                              min(lane, 21);
-        const size_t wstep = (size_t)A_NW * a.in_pitch / 4;   // A_NW rows, in 32-bit words
+        const size_t wstep = (size_t)NWARPS * a.in_pitch / 4;   // NWARPS rows, in 32-bit words
         uint32_t wv[RPW];
 #pragma unroll
-        for (int k = 0; k < RPW; ++k) {   // rows warp + A_NW k (the last exists for some warps only)
-            wv[k] = (warp + A_NW * k < AIN) ? __ldg(wp + k * wstep) : 0u;
-        }
+        for (int k = 0; k < RPW; ++k) wv[k] = (warp + NWARPS * k < AIN) ? __ldg(wp + k * wstep) : 0u;
 #pragma unroll
         for (int k = 0; k < RPW; ++k) {
-            const int r = warp + A_NW * k;
+            const int r = warp + NWARPS * k;
             if (r < AIN && lane < 22) {
                 const int c0 = 4 * lane - 2;   // tile column of byte 0
                 const float f0 = __uint_as_float(__byte_perm(wv[k], 0x4B000000u, 0x7540u)) - 8388608.0f;
@@ -377,20 +365,19 @@ __global__ void __launch_bounds__(A_NT, 3) k_analysis_shrink(AnalysisArgs a) {
             }
         }
     } else {
-        constexpr int RPW = (AIN + A_NW - 1) / A_NW;   // rows per warp
         float v[RPW][3];
         int ixs[3];
 #pragma unroll
         for (int j = 0; j < 3; ++j) ixs[j] = s_ix[min(lane + 32 * j, AIN - 1)];
 #pragma unroll
         for (int k = 0; k < RPW; ++k) {
-            const TIn* row = in + (size_t)s_iy[min(warp + A_NW * k, AIN - 1)] * a.in_pitch;
+            const TIn* row = in + (size_t)s_iy[min(warp + NWARPS * k, AIN - 1)] * a.in_pitch;
 #pragma unroll
             for (int j = 0; j < 3; ++j) v[k][j] = (float)__ldg(row + ixs[j]);
         }
 #pragma unroll
         for (int k = 0; k < RPW; ++k) {
-            const int r = warp + A_NW * k;
+            const int r = warp + NWARPS * k;
 #pragma unroll
             for (int j = 0; j < 3; ++j) {
                 const int c = lane + 32 * j;
@@ -398,13 +385,112 @@ __global__ void __launch_bounds__(A_NT, 3) k_analysis_shrink(AnalysisArgs a) {
             }
         }
     }
+}
+
+template <typename TIn>
+__device__ __forceinline__ bool tile_fast_u8(const AnalysisArgs& a, const ATile& g) {
+    const TIn* in = reinterpret_cast<const TIn*>(a.in) + (size_t)g.b * a.in_bstride;
+    const int ix0 = 2 * g.cx0 - 6, iy0 = 2 * g.cy0 - 6;
+    return sizeof(TIn) == 1 && ix0 >= 2 && iy0 >= 0 && ix0 - 2 + 88 <= a.NW && iy0 + AIN <= a.NH &&
+           ((reinterpret_cast<uintptr_t>(in) + (size_t)ix0 - 2) & 3) == 0 && (a.in_pitch & 3) == 0;
+}
+
+// Generic analysis kernel: one tile per CTA.
+template <typename TIn>
+__global__ void __launch_bounds__(A_NT, 3) k_analysis_shrink(AnalysisArgs a) {
+    extern __shared__ __align__(128) float smem[];
+    float* s_in = smem;                          // [AIN][IN_P]; later details [3][AR][DT_P]
+    float* s_row = smem + A_SMEM_IN;             // [2][AIN][RW_P]; later vertical sums
+    int* s_iy = reinterpret_cast<int*>(s_row + A_SMEM_ROW);
+    int* s_ix = s_iy + AIN;
+    int* s_rmap = s_ix + AIN;
+    int* s_cmap = s_rmap + AR;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const ATile g = analysis_tile(a, blockIdx.z, blockIdx.y, blockIdx.x);
+    const bool fast_u8 = tile_fast_u8<TIn>(a, g);
+    if (!fast_u8 || g.bx || g.by) {   // mirror tables: only tiles that read mirrored samples need them
+        analysis_tables(a, g, s_iy, s_ix, s_rmap, s_cmap);
+        __syncthreads();
+    }
+    load_tile<TIn, A_NW>(a, g, fast_u8, s_in, s_iy, s_ix, warp, lane);
     __syncthreads();
     rowpass_f32(s_in, s_row);
     __syncthreads();
     float* s_det = s_in;
     colpass(a, g, s_row, s_det);
     __syncthreads();
-    shrink3(a, g, s_det, reinterpret_cast<float4*>(s_row), s_rmap, s_cmap);
+    shrink3(a, g, s_det, reinterpret_cast<float4*>(s_row), s_rmap, s_cmap, CtaBar{});
+}
+
+// Warp-specialized persistent analysis: WS_NP producer warps (tables, input
+// tile, row pass, column pass) and WS_NC consumer warps (shrink) hand tiles over
+// through a two-slot ring of detail tiles, with named barriers: FULL[slot]
+// (producer arrives, consumer syncs) and EMPTY[slot] (consumer arrives,
+// producer syncs before reusing the slot).  One CTA per SM walks tiles
+// blockIdx.x, +gridDim.x, ...; while one group waits at its internal
+// barriers the other group keeps the SM issuing.
+#ifndef PRNU_WS_NP
+#define PRNU_WS_NP 12
+#endif
+#ifndef PRNU_WS_NC
+#define PRNU_WS_NC 12
+#endif
+constexpr int WS_NP = PRNU_WS_NP, WS_NC = PRNU_WS_NC;
+constexpr int WS_PT = 32 * WS_NP, WS_CT = 32 * WS_NC, WS_T = WS_PT + WS_CT;
+constexpr int WS_DET = 3 * AR * DT_P;               // one detail slot
+constexpr int WS_FLOATS = A_SMEM_IN + 2 * RW_PLANE + 2 * WS_DET + 2 * V_PLANE4 * 4;
+constexpr size_t WS_SMEM_BYTES = sizeof(float) * WS_FLOATS + sizeof(int) * (2 * AIN + 4 * AR);
+enum { BAR_PROD = 1, BAR_CONS = 2, BAR_FULL0 = 3, BAR_EMPTY0 = 5 };
+
+__device__ __forceinline__ void named_arrive(int id, int count) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+template <typename TIn>
+__global__ void __launch_bounds__(WS_T, 1) k_analysis_ws(AnalysisArgs a, int tiles_x, int tiles_y, int n_tiles) {
+    extern __shared__ __align__(128) float smem[];
+    float* s_in = smem;
+    float* s_row = s_in + A_SMEM_IN;
+    float* s_det0 = s_row + 2 * RW_PLANE;
+    float4* s_v = reinterpret_cast<float4*>(s_det0 + 2 * WS_DET);
+    int* s_iy = reinterpret_cast<int*>(smem + WS_FLOATS);
+    int* s_ix = s_iy + AIN;
+    int* s_rmap0 = s_ix + AIN;        // [2][AR]
+    int* s_cmap0 = s_rmap0 + 2 * AR;  // [2][AR]
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int per_frame = tiles_x * tiles_y;
+    auto tile_of = [&](int t) {
+        const int b = t / per_frame, r = t - b * per_frame;
+        return analysis_tile(a, b, r / tiles_x, r % tiles_x);
+    };
+    if (warp < WS_NP) {   // ---------------- producer
+        int k = 0;
+        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++k) {
+            const int slot = k & 1;
+            const ATile g = tile_of(t);
+            if (k >= 2) NamedBar{BAR_EMPTY0 + slot, WS_T}.sync();   // consumer released tile k-2's slot
+            const bool fast_u8 = tile_fast_u8<TIn>(a, g);
+            analysis_tables(a, g, s_iy, s_ix, s_rmap0 + slot * AR, s_cmap0 + slot * AR, tid, WS_PT);
+            NamedBar{BAR_PROD, WS_PT}.sync();
+            load_tile<TIn, WS_NP>(a, g, fast_u8, s_in, s_iy, s_ix, warp, lane);
+            NamedBar{BAR_PROD, WS_PT}.sync();
+            rowpass_f32(s_in, s_row, tid, WS_PT);
+            NamedBar{BAR_PROD, WS_PT}.sync();
+            colpass(a, g, s_row, s_det0 + slot * WS_DET, tid, WS_PT);
+            named_arrive(BAR_FULL0 + slot, WS_T);                  // details of tile k complete
+        }
+    } else {              // ---------------- consumer
+        const int ctid = tid - WS_PT;
+        int k = 0;
+        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++k) {
+            const int slot = k & 1;
+            const ATile g = tile_of(t);
+            NamedBar{BAR_FULL0 + slot, WS_T}.sync();
+            shrink3(a, g, s_det0 + slot * WS_DET, s_v, s_rmap0 + slot * AR, s_cmap0 + slot * AR,
+                    NamedBar{BAR_CONS, WS_CT}, ctid, WS_CT);
+            if (t + 2 * (int)gridDim.x < n_tiles) named_arrive(BAR_EMPTY0 + slot, WS_T);   // slot free for k+2
+        }
+    }
 }
 
 // Level-1 u8 analysis, persistent: each CTA walks tiles blockIdx.x, +gridDim.x,
@@ -484,7 +570,7 @@ __global__ void __launch_bounds__(A_NT, 3) k_analysis_u8_tma(const __grid_consta
         }
         colpass(a, g, s_row, s_det);
         __syncthreads();
-        shrink3(a, g, s_det, reinterpret_cast<float4*>(s_row), s_rmap, s_cmap);
+        shrink3(a, g, s_det, reinterpret_cast<float4*>(s_row), s_rmap, s_cmap, CtaBar{});
     }
 }
 
@@ -783,7 +869,11 @@ static int setup_attributes() {
                                           (int)S_SMEM_BYTES);
     cudaError_t e6 = cudaFuncSetAttribute(k_analysis_u8_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)A8_SMEM_BYTES);
-    cudaError_t e = e1 ? e1 : e2 ? e2 : e3 ? e3 : e4 ? e4 : e5 ? e5 : e6;
+    cudaError_t e7 = cudaFuncSetAttribute(k_analysis_ws<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)WS_SMEM_BYTES);
+    cudaError_t e8 = cudaFuncSetAttribute(k_analysis_ws<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)WS_SMEM_BYTES);
+    cudaError_t e = e1 ? e1 : e2 ? e2 : e3 ? e3 : e4 ? e4 : e5 ? e5 : e6 ? e6 : e7 ? e7 : e8;
     if (e != cudaSuccess) return fail(PRNU_CUDA_ERROR, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
     g_attr_done = true;
     return PRNU_OK;
@@ -842,10 +932,14 @@ static int denoise_front(const TIn* in, long long in_bstride, int in_pitch, int 
                                 encode_tensor_map_3d(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, in, (uint64_t)a.NW,
                                                      (uint64_t)a.NH, (uint64_t)nb, (uint64_t)in_pitch,
                                                      (uint64_t)in_bstride, U8_P, AIN);
+            static const bool use_ws = getenv("PRNU_WS_ANALYSIS") != nullptr;   // A/B switch
             if (tma_ok) {
                 const int tx = (int)grid.x, ty = (int)grid.y, n_tiles = tx * ty * nb;
                 const int ctas = std::min(n_tiles, 148 * 3);
                 k_analysis_u8_tma<<<ctas, A_NT, A8_SMEM_BYTES, st>>>(map, a, tx, ty, n_tiles);
+            } else if (use_ws) {
+                const int tx = (int)grid.x, ty = (int)grid.y, n_tiles = tx * ty * nb;
+                k_analysis_ws<TIn><<<std::min(n_tiles, 148), WS_T, WS_SMEM_BYTES, st>>>(a, tx, ty, n_tiles);
             } else {
                 k_analysis_shrink<TIn><<<grid, A_NT, A_SMEM_BYTES, st>>>(a);
             }
@@ -911,12 +1005,14 @@ int run_residual(const TIn* in, int nb, int H, int W, const Pyramid& p, const Sh
 
 // acc_wait (optional): event the accumulating launch must wait for (the previous
 // wave's accumulation on another stream); acc_done (optional): recorded after it.
+// frame_stride: elements between consecutive frames of `in`/`I` (H*W for a
+// contiguous stack; k*H*W selects every k-th frame, f4 stride emulation).
 template <typename TIn>
 int run_residual_accumulate(const TIn* in, const TIn* I, int nb, int H, int W, const Pyramid& p,
                             const ShrinkParams& sp, double* num, double* den, float* ws_pyr, cudaStream_t st,
-                            cudaEvent_t acc_wait, cudaEvent_t acc_done) {
+                            cudaEvent_t acc_wait, cudaEvent_t acc_done, long long frame_stride) {
     PyramidBuffers pb = carve_pyramid(p, ws_pyr, nb);
-    int rc = denoise_front<TIn>(in, (long long)H * W, W, nb, p, pb, sp, st);
+    int rc = denoise_front<TIn>(in, frame_stride, W, nb, p, pb, sp, st);
     if (rc) return rc;
     SynthMaps m;
     if ((rc = synth_maps(p, pb, 1, nb, p.levels > 1, &m))) return rc;
@@ -926,7 +1022,7 @@ int run_residual_accumulate(const TIn* in, const TIn* I, int nb, int H, int W, c
     s.NW = W;
     s.nb = nb;
     s.I = I;
-    s.i_bstride = (long long)H * W;
+    s.i_bstride = frame_stride;
     s.i_pitch = W;
     s.num = num;
     s.den = den;
@@ -950,9 +1046,9 @@ template int run_residual<uint8_t>(const uint8_t*, int, int, int, const Pyramid&
                                    float*, cudaStream_t);
 template int run_residual_accumulate<float>(const float*, const float*, int, int, int, const Pyramid&,
                                             const ShrinkParams&, double*, double*, float*, cudaStream_t, cudaEvent_t,
-                                            cudaEvent_t);
+                                            cudaEvent_t, long long);
 template int run_residual_accumulate<uint8_t>(const uint8_t*, const uint8_t*, int, int, int, const Pyramid&,
                                               const ShrinkParams&, double*, double*, float*, cudaStream_t,
-                                              cudaEvent_t, cudaEvent_t);
+                                              cudaEvent_t, cudaEvent_t, long long);
 
 }  // namespace prnu
