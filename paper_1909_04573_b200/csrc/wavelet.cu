@@ -331,6 +331,8 @@ __device__ __forceinline__ void shrink3(const AnalysisArgs& a, const ATile& g, c
     }
 }
 
+__device__ __forceinline__ bool fast_f32(const AnalysisArgs& a, const ATile& g);
+
 // Input tile of one analysis tile into s_in [AIN][IN_P] (fp32), by NWARPS warps
 // (warp = 0..NWARPS-1).  Interior u8 tiles: each row is 22 aligned words covering
 // input columns ix0-2 .. ix0+85, widened exactly (2^23 trick); otherwise mirrored
@@ -364,6 +366,28 @@ __device__ __forceinline__ void load_tile(const AnalysisArgs& a, const ATile& g,
                 *reinterpret_cast<float2*>(row + c0 + 2) = make_float2(f2, f3);   // c0 + 3 <= 85
             }
         }
+    } else if (sizeof(TIn) == 4 && fast_f32(a, g)) {
+        // interior fp32 tile: each row is 43 aligned float2 (input columns ix0 .. ix0+85)
+        const int ix0 = 2 * g.cx0 - 6, iy0 = 2 * g.cy0 - 6;
+        const float2* rp = reinterpret_cast<const float2*>(reinterpret_cast<const float*>(in) +
+                                                           (size_t)(iy0 + warp) * a.in_pitch + ix0);
+        const size_t rstep = (size_t)NWARPS * a.in_pitch / 2;   // NWARPS rows, in float2
+        float2 v0[RPW], v1[RPW];
+#pragma unroll
+        for (int k = 0; k < RPW; ++k) {
+            const bool ok = warp + NWARPS * k < AIN;
+            v0[k] = ok ? __ldg(rp + k * rstep + lane) : make_float2(0.f, 0.f);
+            v1[k] = (ok && lane < AIN / 2 - 32) ? __ldg(rp + k * rstep + 32 + lane) : make_float2(0.f, 0.f);
+        }
+#pragma unroll
+        for (int k = 0; k < RPW; ++k) {
+            const int r = warp + NWARPS * k;
+            if (r < AIN) {
+                float2* row = reinterpret_cast<float2*>(s_in + r * IN_P);
+                row[lane] = v0[k];
+                if (lane < AIN / 2 - 32) row[32 + lane] = v1[k];
+            }
+        }
     } else {
         float v[RPW][3];
         int ixs[3];
@@ -387,6 +411,14 @@ __device__ __forceinline__ void load_tile(const AnalysisArgs& a, const ATile& g,
     }
 }
 
+// interior fp32 tile whose rows can be read as aligned float2 (no mirroring)
+__device__ __forceinline__ bool fast_f32(const AnalysisArgs& a, const ATile& g) {
+    const int ix0 = 2 * g.cx0 - 6, iy0 = 2 * g.cy0 - 6;
+    const float* in = reinterpret_cast<const float*>(a.in) + (size_t)g.b * a.in_bstride;
+    return ix0 >= 0 && iy0 >= 0 && ix0 + AIN <= a.NW && iy0 + AIN <= a.NH && (ix0 & 1) == 0 &&
+           (a.in_pitch & 1) == 0 && ((reinterpret_cast<uintptr_t>(in) & 7) == 0);
+}
+
 template <typename TIn>
 __device__ __forceinline__ bool tile_fast_u8(const AnalysisArgs& a, const ATile& g) {
     const TIn* in = reinterpret_cast<const TIn*>(a.in) + (size_t)g.b * a.in_bstride;
@@ -408,7 +440,8 @@ __global__ void __launch_bounds__(A_NT, 3) k_analysis_shrink(AnalysisArgs a) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const ATile g = analysis_tile(a, blockIdx.z, blockIdx.y, blockIdx.x);
     const bool fast_u8 = tile_fast_u8<TIn>(a, g);
-    if (!fast_u8 || g.bx || g.by) {   // mirror tables: only tiles that read mirrored samples need them
+    const bool fast = fast_u8 || (sizeof(TIn) == 4 && fast_f32(a, g));
+    if (!fast || g.bx || g.by) {   // mirror tables: only tiles that read mirrored samples need them
         analysis_tables(a, g, s_iy, s_ix, s_rmap, s_cmap);
         __syncthreads();
     }
