@@ -66,6 +66,14 @@ struct AnalysisArgs {
     ShrinkParams sp;
 };
 
+// Filter pairs in constant memory: FFMA2 takes them as c[][] / uniform-register
+// operands instead of re-materialising immediate pairs with MOVs at every use.
+__constant__ float2 c_hg[8] = {{PRNU_H0, PRNU_H7}, {PRNU_H1, -PRNU_H6}, {PRNU_H2, PRNU_H5}, {PRNU_H3, -PRNU_H4},
+                               {PRNU_H4, PRNU_H3}, {PRNU_H5, -PRNU_H2}, {PRNU_H6, PRNU_H1}, {PRNU_H7, -PRNU_H0}};
+// synthesis: (H(6-2m), H(7-2m)) and (G(6-2m), G(7-2m)), m = 0..3
+__constant__ float2 c_sh[4] = {{PRNU_H6, PRNU_H7}, {PRNU_H4, PRNU_H5}, {PRNU_H2, PRNU_H3}, {PRNU_H0, PRNU_H1}};
+__constant__ float2 c_sg[4] = {{PRNU_H1, -PRNU_H0}, {PRNU_H3, -PRNU_H2}, {PRNU_H5, -PRNU_H4}, {PRNU_H7, -PRNU_H6}};
+
 // Geometry of one analysis tile.
 struct ATile {
     int b, y0, x0, cy0, cx0;
@@ -242,7 +250,7 @@ __device__ __forceinline__ void shrink_v(const ATile& g, const float* det, float
     else shrink_v_t<false>(g, det, s_v, s_rmap, s_cmap, it);
 }
 
-template <bool BX>
+template <bool BX, bool ALL4>
 __device__ __forceinline__ void shrink_h_t(const AnalysisArgs& a, const ATile& g, const float* det,
                                            const float4* s_v, const int* s_cmap, float* dst, int it) {
     const float s0 = a.sp.sigma0_sq;
@@ -269,11 +277,16 @@ __device__ __forceinline__ void shrink_h_t(const AnalysisArgs& a, const ATile& g
             s7 += u[t + 7].z - u[t].z;
             s9 += u[t + 8].w - u[t - 1].w;
         }
-        float m = 3.402823466e38f;
-        if (wm & 1) m = fminf(m, s3 * (1.0f / 9.0f));
-        if (wm & 2) m = fminf(m, s5 * (1.0f / 25.0f));
-        if (wm & 4) m = fminf(m, s7 * (1.0f / 49.0f));
-        if (wm & 8) m = fminf(m, s9 * (1.0f / 81.0f));
+        float m;
+        if (ALL4) {   // the default window set {3,5,7,9}: no per-window selects
+            m = fminf(fminf(s3 * (1.0f / 9.0f), s5 * (1.0f / 25.0f)), fminf(s7 * (1.0f / 49.0f), s9 * (1.0f / 81.0f)));
+        } else {
+            m = 3.402823466e38f;
+            if (wm & 1) m = fminf(m, s3 * (1.0f / 9.0f));
+            if (wm & 2) m = fminf(m, s5 * (1.0f / 25.0f));
+            if (wm & 4) m = fminf(m, s7 * (1.0f / 49.0f));
+            if (wm & 8) m = fminf(m, s9 * (1.0f / 81.0f));
+        }
         const float var = fmaxf(m - s0, 0.0f);
         o[t] = crow[t] * __fdividef(s0, var + s0);   // noise-domain coefficient c - F(c)
     }
@@ -293,8 +306,14 @@ __device__ __forceinline__ void shrink_h_t(const AnalysisArgs& a, const ATile& g
 
 __device__ __forceinline__ void shrink_h(const AnalysisArgs& a, const ATile& g, const float* det, const float4* s_v,
                                          const int* s_cmap, float* dst, int it) {
-    if (g.bx) shrink_h_t<true>(a, g, det, s_v, s_cmap, dst, it);
-    else shrink_h_t<false>(a, g, det, s_v, s_cmap, dst, it);
+    const bool all4 = a.sp.wmask == 15;
+    if (g.bx) {
+        if (all4) shrink_h_t<true, true>(a, g, det, s_v, s_cmap, dst, it);
+        else shrink_h_t<true, false>(a, g, det, s_v, s_cmap, dst, it);
+    } else {
+        if (all4) shrink_h_t<false, true>(a, g, det, s_v, s_cmap, dst, it);
+        else shrink_h_t<false, false>(a, g, det, s_v, s_cmap, dst, it);
+    }
 }
 
 // CTA-wide barrier, or a named barrier over a warp group (bar.sync id, count).
@@ -671,10 +690,10 @@ __device__ __forceinline__ void synth_compute(const float* c, float* s_L, float*
             float2 l = make_float2(0.f, 0.f), h = make_float2(0.f, 0.f);
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
-                l = ffma2(va[q + m], make_float2(wl_h(6 - 2 * m), wl_h(7 - 2 * m)), l);
-                l = ffma2(vad[q + m], make_float2(wl_g(6 - 2 * m), wl_g(7 - 2 * m)), l);
-                h = ffma2(vda[q + m], make_float2(wl_h(6 - 2 * m), wl_h(7 - 2 * m)), h);
-                h = ffma2(vdd[q + m], make_float2(wl_g(6 - 2 * m), wl_g(7 - 2 * m)), h);
+                l = ffma2(va[q + m], c_sh[m], l);
+                l = ffma2(vad[q + m], c_sg[m], l);
+                h = ffma2(vda[q + m], c_sh[m], h);
+                h = ffma2(vdd[q + m], c_sg[m], h);
             }
             const int t = 4 * sg + 2 * q;
             s_L[t * SL_P + k] = l.x;
@@ -698,8 +717,8 @@ __device__ __forceinline__ void synth_compute(const float* c, float* s_L, float*
             float2 x = make_float2(0.f, 0.f);   // outputs 2q (e = 0) and 2q+1 (e = 1)
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
-                x = ffma2(vl[q + m], make_float2(wl_h(6 - 2 * m), wl_h(7 - 2 * m)), x);
-                x = ffma2(vh[q + m], make_float2(wl_g(6 - 2 * m), wl_g(7 - 2 * m)), x);
+                x = ffma2(vl[q + m], c_sh[m], x);
+                x = ffma2(vh[q + m], c_sg[m], x);
             }
             s_out[t * SO_P + 8 * g + 2 * q] = x.x;
             s_out[t * SO_P + 8 * g + 2 * q + 1] = x.y;
