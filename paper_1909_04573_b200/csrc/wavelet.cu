@@ -732,7 +732,10 @@ __device__ __forceinline__ void synth_compute(const float* c, float* s_L, float*
 //         frames (grid.z = 1), I of type TI; NUM/DEN read once, written once,
 //         per-pixel sums in ascending frame order.
 template <int MODE, typename TI>
-__global__ void __launch_bounds__(256, MODE == 0 ? 3 : 2) k_synth_tma(const __grid_constant__ SynthMaps maps, SynthArgs a) {
+#ifndef PRNU_SYNTH_ACC_MINB
+#define PRNU_SYNTH_ACC_MINB 3
+#endif
+__global__ void __launch_bounds__(256, MODE == 0 ? 3 : PRNU_SYNTH_ACC_MINB) k_synth_tma(const __grid_constant__ SynthMaps maps, SynthArgs a) {
     extern __shared__ __align__(128) float smem[];
     float* cbuf0 = smem;
     float* s_L = smem + 2 * SC_TILE;
