@@ -362,27 +362,27 @@ def main():
                 "bytes_per_launch": kt.get("alg_bytes_per_launch"), "avg_launch_ms": avg_ms,
                 "share_of_kernel_time": kt["share"]}
 
-    # ---- e2e through the host-buffer C-ABI call
+    # ---- e2e through the host-buffer C-ABI call: the frames start in pinned host
+    #      memory; one upload per step feeds every depth (prnu_extract_multi_host),
+    #      the fingerprints come back to host memory
     e2e = None
     if not args.no_e2e:
         host = torch.empty((m, H, W), dtype=torch.uint8, pin_memory=True)
         host.copy_(frames)
-        exh = {d: prnu.Extractor(H, W, d, batch=exs[d].batch, device=dev, host=True) for d in depths}
-        for _ in range(1):
-            for d in depths:
-                exh[d](host)
+        mx = prnu.MultiExtractor(m, H, W, depths, batch=args.batch, device=dev)
+        mx(host)
         torch.cuda.synchronize()
         barrier(world)
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            for d in depths:
-                exh[d](host)
+            mx(host)
         t = time.perf_counter() - t0
         t = max_over_ranks(t, world)
         e2e = {"value": denoise_per_step * args.e2e_steps * world / t, "unit": "denoised FHD frames/s",
-               "h2d_bytes_per_step": int(len(depths) * m * H * W), "d2h_bytes_per_step": int(len(depths) * H * W * 4),
-               "steps": args.e2e_steps, "fingerprints_per_s": len(depths) * args.e2e_steps * world / t}
-        del host
+               "h2d_bytes_per_step": int(m * H * W), "d2h_bytes_per_step": int(len(depths) * H * W * 4),
+               "steps": args.e2e_steps, "fingerprints_per_s": len(depths) * args.e2e_steps * world / t,
+               "api": "prnu_extract_multi_host (one upload per step for all depths)"}
+        del host, mx
 
     # ---- cpu baseline: the oracle on a bounded sample (rank 0, N = 1 only)
     cpu = None

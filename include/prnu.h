@@ -164,6 +164,20 @@ int prnu_extract_fingerprint_host(const uint8_t* frames_host, int64_t m, int H, 
                                   float* K_out_host, double* sum_WI, double* sum_I2,
                                   int64_t* n_sda_host, void* ws, size_t ws_bytes, void* stream);
 
+/* Several SDA depths from ONE upload of a host frame stack (e.g. the paper's
+ * depth sweeps).  The whole u8 stack [m][H][W] is copied to the
+ * device workspace in chunks of 128 frames on an internal copy stream; each
+ * wave of each depth waits only for the chunk holding its last frame, so the
+ * upload overlaps the denoising.  Outputs: K_out_host fp32 [n_depths][H][W]
+ * (host), sums fp64 [n_depths][2][H][W] (device: sum_WI then sum_I2 per depth),
+ * n_sda_host int64 [n_depths] (host).  Each depth's result is bit-identical to
+ * prnu_extract_fingerprint on the same frames.  Synchronous. */
+size_t prnu_extract_multi_host_workspace_bytes(int64_t m, int H, int W, int batch, const int64_t* depths_host,
+                                               int n_depths, const prnu_denoise_params* p);
+int prnu_extract_multi_host(const uint8_t* frames_host, int64_t m, int H, int W, const int64_t* depths_host,
+                            int n_depths, const prnu_denoise_params* p, int batch, double eps, float* K_out_host,
+                            double* sums, int64_t* n_sda_host, void* ws, size_t ws_bytes, void* stream);
+
 /* ---------------------------------------------------------------------------
  * a7  NCC — P:93, P:259 name it; S:284-287 fixes it (R-16): the Pearson
  * correlation over all pixels at shift (0,0),

@@ -95,6 +95,9 @@ _sig("prnu_extract_fingerprint", _i, _vp, _i64, _i, _i, _i64, _P, _i, _d, _vp, _
 _sig("prnu_extract_fingerprint_stride", _i, _vp, _i64, _i, _i, _i64, _P, _i, _d, _vp, _vp, _vp, ctypes.POINTER(_i64),
      _vp, _sz, _vp)
 _sig("prnu_extract_host_workspace_bytes", _sz, _i, _i, _i, _i64, _P)
+_sig("prnu_extract_multi_host_workspace_bytes", _sz, _i64, _i, _i, _i, ctypes.POINTER(_i64), _i, _P)
+_sig("prnu_extract_multi_host", _i, _vp, _i64, _i, _i, ctypes.POINTER(_i64), _i, _P, _i, _d, _vp, _vp,
+     ctypes.POINTER(_i64), _vp, _sz, _vp)
 _sig("prnu_extract_fingerprint_host", _i, _vp, _i64, _i, _i, _i64, _P, _i, _d, _vp, _vp, _vp,
      ctypes.POINTER(_i64), _vp, _sz, _vp)
 _sig("prnu_ncc_workspace_bytes", _sz, _i, _i, _i)
@@ -290,6 +293,39 @@ class Extractor:
                                                ctypes.byref(ns), _ptr(self.ws), self.nbytes, _stream())
             _check(rc, "prnu_extract_fingerprint")
         return Fingerprint(self.K, self.sum_WI, self.sum_I2, int(ns.value), self.depth, m)
+
+
+class MultiExtractor:
+    """Fingerprints at several SDA depths from ONE upload of a host (pinned) frame
+    stack [m][H][W]; owns the device workspace (which holds the whole stack)."""
+
+    def __init__(self, m: int, H: int, W: int, depths, batch: int = 64, params: DenoiseParams | None = None,
+                 device="cuda", eps: float = 1e-6):
+        self.m, self.H, self.W, self.batch, self.eps = m, H, W, batch, eps
+        self.depths = [int(d) for d in depths]
+        self.p = _params(params)
+        self._d = (_i64 * len(self.depths))(*self.depths)
+        self.nbytes = _lib.prnu_extract_multi_host_workspace_bytes(m, H, W, batch, self._d, len(self.depths),
+                                                                   ctypes.byref(self.p))
+        if self.nbytes == 0:
+            raise PrnuError(4, "prnu_extract_multi_host_workspace_bytes (invalid m/H/W/batch/depths/params)")
+        self.ws = _ws(self.nbytes, device)
+        self.sums = torch.empty((len(self.depths), 2, H, W), dtype=torch.float64, device=device)
+        self.K = torch.empty((len(self.depths), H, W), dtype=torch.float32, pin_memory=True)
+        self.n_sda = [0] * len(self.depths)
+
+    def __call__(self, frames_host: torch.Tensor) -> torch.Tensor:
+        if frames_host.is_cuda or frames_host.dtype != torch.uint8 or not frames_host.is_contiguous():
+            raise TypeError("frames must be a contiguous uint8 CPU (pinned) tensor")
+        if tuple(frames_host.shape) != (self.m, self.H, self.W):
+            raise ValueError("frame stack shape differs from the extractor's")
+        ns = (_i64 * len(self.depths))()
+        _check(_lib.prnu_extract_multi_host(_ptr(frames_host), self.m, self.H, self.W, self._d, len(self.depths),
+                                            ctypes.byref(self.p), self.batch, self.eps, _ptr(self.K),
+                                            _ptr(self.sums), ns, _ptr(self.ws), self.nbytes, _stream()),
+               "prnu_extract_multi_host")
+        self.n_sda = list(ns)
+        return self.K
 
 
 def extract_fingerprint(frames: torch.Tensor, depth: int, params: DenoiseParams | None = None, batch: int = 16,

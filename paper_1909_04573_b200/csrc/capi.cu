@@ -454,6 +454,109 @@ int prnu_extract_fingerprint_host(const uint8_t* frames_host, int64_t m, int H, 
     return rc;
 }
 
+// ---------------------------------------------------------------- multi-depth, one upload
+static constexpr int64_t kMultiChunk = 128;   // frames per H2D chunk (event granularity)
+
+static size_t multi_layout(int64_t m, int H, int W, int batch, const int64_t* depths, int n, const Pyramid& pyr,
+                           size_t* off_waves, size_t* off_K, size_t* off_zm) {
+    const size_t P = (size_t)H * W;
+    size_t o = align_up((size_t)m * P, 256);                      // the whole u8 stack on the device
+    *off_waves = o;
+    size_t wmax = 0;
+    for (int i = 0; i < n; ++i) wmax = std::max(wmax, extract_wave_ws(H, W, batch, depths[i], pyr));
+    o += wmax;                                                     // one wave workspace, reused per depth
+    *off_K = o;
+    o += align_up(sizeof(float) * P * n, 256);
+    *off_zm = o;
+    o += zm_workspace_bytes(H, W);
+    return o;
+}
+
+size_t prnu_extract_multi_host_workspace_bytes(int64_t m, int H, int W, int batch, const int64_t* depths_host,
+                                               int n_depths, const prnu_denoise_params* p) {
+    if (m < 1 || H <= 0 || W <= 0 || batch < 1 || n_depths < 1 || !depths_host || validate_params(p, H, W, nullptr))
+        return 0;
+    for (int i = 0; i < n_depths; ++i)
+        if (depths_host[i] < 1 || depths_host[i] > m) return 0;
+    size_t a, b, c;
+    return multi_layout(m, H, W, batch, depths_host, n_depths, make_pyramid(H, W, p->levels), &a, &b, &c);
+}
+
+int prnu_extract_multi_host(const uint8_t* frames_host, int64_t m, int H, int W, const int64_t* depths_host,
+                            int n_depths, const prnu_denoise_params* p, int batch, double eps, float* K_out_host,
+                            double* sums, int64_t* n_sda_host, void* ws, size_t ws_bytes, void* stream) {
+    int rc;
+    if (!frames_host || !depths_host || !K_out_host || !sums || !ws) return fail(PRNU_INVALID_ARG, "null pointer");
+    if (batch < 1 || n_depths < 1) return fail(PRNU_INVALID_ARG, "batch and n_depths must be >= 1");
+    if ((rc = check_dims(H, W))) return rc;
+    for (int i = 0; i < n_depths; ++i) {
+        int64_t ns;
+        if ((rc = prnu_sda_groups(m, depths_host[i], &ns))) return rc;
+        if (depths_host[i] > 65793) return fail(PRNU_BAD_PARAMETER, "depth > 65793");
+        if (n_sda_host) n_sda_host[i] = ns;
+    }
+    if (!(eps > 0.0)) return fail(PRNU_BAD_PARAMETER, "eps must be > 0");
+    ShrinkParams sp;
+    if ((rc = validate_params(p, H, W, &sp))) return rc;
+    Pyramid pyr = make_pyramid(H, W, p->levels);
+    size_t off_w, off_K, off_zm;
+    if (ws_bytes < multi_layout(m, H, W, batch, depths_host, n_depths, pyr, &off_w, &off_K, &off_zm))
+        return fail(PRNU_WORKSPACE_TOO_SMALL, "workspace too small");
+    const size_t P = (size_t)H * W;
+    char* wsb = reinterpret_cast<char*>(ws);
+    uint8_t* fdev = reinterpret_cast<uint8_t*>(wsb);
+    float* Kdev = reinterpret_cast<float*>(wsb + off_K);
+    cudaStream_t st = as_stream(stream), cp = nullptr;
+    const int64_t n_chunks = (m + kMultiChunk - 1) / kMultiChunk;
+    std::vector<cudaEvent_t> ev((size_t)n_chunks, nullptr);
+    cudaEvent_t ev_start = nullptr;
+    cudaError_t e = cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
+    for (int64_t c = 0; c < n_chunks && e == cudaSuccess; ++c) e = cudaEventCreateWithFlags(&ev[c], cudaEventDisableTiming);
+    // the upload starts after the caller's prior work on `stream` (it owns the workspace)
+    if (e == cudaSuccess) e = cudaEventRecord(ev_start, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cp, ev_start, 0);
+    for (int64_t c = 0; c < n_chunks && e == cudaSuccess; ++c) {
+        const int64_t f0 = c * kMultiChunk, nf = std::min<int64_t>(kMultiChunk, m - f0);
+        e = cudaMemcpyAsync(fdev + (size_t)f0 * P, frames_host + (size_t)f0 * P, (size_t)nf * P,
+                            cudaMemcpyHostToDevice, cp);
+        if (e == cudaSuccess) e = cudaEventRecord(ev[c], cp);
+    }
+    rc = (e == cudaSuccess) ? PRNU_OK : fail(PRNU_CUDA_ERROR, std::string("upload: ") + cudaGetErrorString(e));
+    int64_t waited = -1;   // highest chunk the compute stream already waits for
+    for (int i = 0; i < n_depths && rc == PRNU_OK; ++i) {
+        const int64_t d = depths_host[i], ns = m / d;
+        double* num = sums + (size_t)2 * i * P;
+        double* den = num + P;
+        e = cudaMemsetAsync(num, 0, sizeof(double) * 2 * P, st);
+        if (e != cudaSuccess) rc = fail(PRNU_CUDA_ERROR, "cudaMemsetAsync failed");
+        for (int64_t g0 = 0; g0 < ns && rc == PRNU_OK; g0 += batch) {
+            const int64_t nb = std::min<int64_t>(batch, ns - g0);
+            const int64_t need = ((g0 + nb) * d - 1) / kMultiChunk;   // chunk holding the wave's last frame
+            for (; waited < need && rc == PRNU_OK; ++waited)
+                if (cudaStreamWaitEvent(st, ev[waited + 1], 0) != cudaSuccess)
+                    rc = fail(PRNU_CUDA_ERROR, "cudaStreamWaitEvent");
+            if (rc == PRNU_OK)
+                rc = extract_chunk(fdev + (size_t)g0 * d * P, nb, H, W, d, pyr, sp, num, den, wsb + off_w, st);
+        }
+        if (rc == PRNU_OK) rc = launch_finalize(num, den, H, W, eps, 1, Kdev + (size_t)i * P, wsb + off_zm, st);
+        if (rc == PRNU_OK &&
+            (e = cudaMemcpyAsync(K_out_host + (size_t)i * P, Kdev + (size_t)i * P, sizeof(float) * P,
+                                 cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+            rc = fail(PRNU_CUDA_ERROR, std::string("D2H K: ") + cudaGetErrorString(e));
+    }
+    // never leave the upload running into memory the caller may reuse
+    for (; waited + 1 < n_chunks && rc == PRNU_OK; ++waited) cudaStreamWaitEvent(st, ev[waited + 1], 0);
+    cudaError_t es = cudaStreamSynchronize(st);
+    if (rc == PRNU_OK && es != cudaSuccess) rc = fail(PRNU_CUDA_ERROR, std::string("sync: ") + cudaGetErrorString(es));
+    cudaStreamSynchronize(cp);
+    for (cudaEvent_t x : ev)
+        if (x) cudaEventDestroy(x);
+    if (ev_start) cudaEventDestroy(ev_start);
+    if (cp) cudaStreamDestroy(cp);
+    return rc;
+}
+
 size_t prnu_ncc_workspace_bytes(int batch, int H, int W) {
     if (batch < 1 || H <= 0 || W <= 0) return 0;
     return ncc_workspace_bytes(batch);

@@ -74,6 +74,13 @@ __constant__ float2 c_hg[8] = {{PRNU_H0, PRNU_H7}, {PRNU_H1, -PRNU_H6}, {PRNU_H2
 __constant__ float2 c_sh[4] = {{PRNU_H6, PRNU_H7}, {PRNU_H4, PRNU_H5}, {PRNU_H2, PRNU_H3}, {PRNU_H0, PRNU_H1}};
 __constant__ float2 c_sg[4] = {{PRNU_H1, -PRNU_H0}, {PRNU_H3, -PRNU_H2}, {PRNU_H5, -PRNU_H4}, {PRNU_H7, -PRNU_H6}};
 
+// Analysis (lo, hi) tap pairs: immediates (default) or constant-memory pairs.
+#ifdef PRNU_HG_CONST
+#define PRNU_HG(i) c_hg[i]
+#else
+#define PRNU_HG(i) make_float2(wl_h(i), wl_g(i))
+#endif
+
 // Geometry of one analysis tile.
 struct ATile {
     int b, y0, x0, cy0, cx0;
@@ -118,7 +125,7 @@ __device__ __forceinline__ void rowpass_item(const float (&v)[24], float* s_row,
     for (int q = 0; q < 8; ++q) {
         float2 lh = make_float2(0.f, 0.f);   // (lo, hi) in one FFMA2 per tap
 #pragma unroll
-        for (int i = 0; i < 8; ++i) lh = ffma2(v[2 * q + i], make_float2(wl_h(i), wl_g(i)), lh);
+        for (int i = 0; i < 8; ++i) lh = ffma2(v[2 * q + i], PRNU_HG(i), lh);
         lo[q] = lh.x;
         hi[q] = lh.y;
     }
@@ -201,8 +208,8 @@ __device__ __forceinline__ void colpass(const AnalysisArgs& a, const ATile& g, c
             float2 p_l = make_float2(0.f, 0.f), p_h = make_float2(0.f, 0.f);   // (aa, ad), (da, dd)
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                p_l = ffma2(lo[2 * q + i], make_float2(wl_h(i), wl_g(i)), p_l);
-                p_h = ffma2(hi[2 * q + i], make_float2(wl_h(i), wl_g(i)), p_h);
+                p_l = ffma2(lo[2 * q + i], PRNU_HG(i), p_l);
+                p_h = ffma2(hi[2 * q + i], PRNU_HG(i), p_h);
             }
             const float aa = p_l.x, ad = p_l.y, da = p_h.x, dd = p_h.y;
             const int rr = 8 * rg + q;

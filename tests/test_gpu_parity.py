@@ -333,3 +333,18 @@ def test_stride_vs_sda_directional(prnu):
     f_str = prnu.extract_fingerprint_stride(v.frames, 30, batch=20)
     assert f_sda.n_sda == f_str.n_sda == 20
     assert prnu.ncc(f_sda.K, v.K).item() > prnu.ncc(f_str.K, v.K).item() + 0.05
+
+
+def test_multi_depth_one_upload_matches_device(prnu):
+    """prnu_extract_multi_host: one chunked upload, several depths; each fingerprint
+    bit-identical to the device-frame extraction (waves straddle upload chunks)."""
+    v = synth.video("drift", 300, 72, 96, seed=11)
+    host = v.frames.pin_memory()
+    depths = [1, 50, 7, 300]
+    mx = prnu.MultiExtractor(300, 72, 96, depths, batch=16)
+    K = mx(host).clone()
+    assert mx.n_sda == [300, 6, 42, 1]
+    for i, d in enumerate(depths):
+        ref = prnu.extract_fingerprint(v.frames.cuda(), d, batch=16)
+        assert torch.equal(K[i], ref.K.cpu()), d
+        assert torch.equal(mx.sums[i, 1], ref.sum_I2)
