@@ -28,9 +28,9 @@ namespace prnu {
 // region (halo kHalo for the 9x9 windows) from an AIN x AIN input tile.
 constexpr int AT = 32;                  // output coefficient tile (square)
 #ifndef PRNU_ANALYSIS_THREADS
-#define PRNU_ANALYSIS_THREADS 288
+#define PRNU_ANALYSIS_THREADS 256
 #endif
-constexpr int A_NT = PRNU_ANALYSIS_THREADS;   // threads per analysis CTA (9 warps: measured best of 256/288/320/384)
+constexpr int A_NT = PRNU_ANALYSIS_THREADS;   // threads per analysis CTA (8 warps x 4 CTAs/SM: measured best, profiles/r01)
 constexpr int A_NW = A_NT / 32;
 constexpr int AR = AT + 2 * kHalo;      // 40: computed coefficient region
 constexpr int AIN = 2 * AR + 6;         // 86: input rows / columns of the region
@@ -42,7 +42,6 @@ constexpr int V_P4 = AR + 1;            // vertical-sum plane pitch in float4 (4
 constexpr int V_PLANE4 = AT * V_P4;     // float4 per vertical-sum buffer
 constexpr int A_SMEM_IN = AIN * IN_P;             // input tile; later the 3 detail planes
 constexpr int A_SMEM_ROW = 2 * V_PLANE4 * 4;      // row-pass lo/hi; later two vertical-sum buffers
-constexpr size_t A_SMEM_BYTES = sizeof(float) * (A_SMEM_IN + A_SMEM_ROW) + sizeof(int) * (2 * AIN + 2 * AR);
 static_assert(3 * AR * DT_P <= A_SMEM_IN, "detail planes must fit in the input tile");
 static_assert(2 * RW_PLANE <= A_SMEM_ROW, "row-pass planes must fit");
 
@@ -357,6 +356,23 @@ __device__ __forceinline__ void shrink3(const AnalysisArgs& a, const ATile& g, c
     }
 }
 
+// One vertical-sum buffer: V0 | H0 | V1 | H1 | V2 | H2 (smaller footprint).
+__device__ __forceinline__ void shrink3_single(const AnalysisArgs& a, const ATile& g, const float* s_det, float4* s_v,
+                                               const int* s_rmap, const int* s_cmap, int tid = threadIdx.x,
+                                               int nthr = A_NT) {
+    constexpr int VI = AR * (AT / 8);
+    constexpr int HI = AT * (AT / 8);
+#pragma unroll 1
+    for (int s = 0; s < 3; ++s) {
+        for (int it = tid; it < VI; it += nthr) shrink_v(g, s_det + s * AR * DT_P, s_v, s_rmap, s_cmap, it);
+        __syncthreads();
+        for (int it = tid; it < HI; it += nthr)
+            shrink_h(a, g, s_det + s * AR * DT_P, s_v, s_cmap,
+                     (s == 0 ? a.d0 : s == 1 ? a.d1 : a.d2) + (size_t)g.b * a.out_bstride, it);
+        __syncthreads();
+    }
+}
+
 __device__ __forceinline__ bool fast_f32(const AnalysisArgs& a, const ATile& g);
 
 // Input tile of one analysis tile into s_in [AIN][IN_P] (fp32), by NWARPS warps
@@ -454,12 +470,86 @@ __device__ __forceinline__ bool tile_fast_u8(const AnalysisArgs& a, const ATile&
 }
 
 // Generic analysis kernel: one tile per CTA.
+// u8 input tile kept as bytes [AIN][U8_P] (row = input columns 2*cx0-6-U8_OFF ..):
+// interior tiles store the 22 aligned words of each row as loaded (one STS.32
+// per lane); border tiles store mirrored bytes through the tables.
+template <int NWARPS>
+__device__ __forceinline__ void load_tile_u8(const AnalysisArgs& a, const ATile& g, bool fast_u8, uint8_t* s_in8,
+                                             const int* s_iy, const int* s_ix, int warp, int lane) {
+    const uint8_t* in = reinterpret_cast<const uint8_t*>(a.in) + (size_t)g.b * a.in_bstride;
+    constexpr int RPW = (AIN + NWARPS - 1) / NWARPS;
+    if (fast_u8) {
+        const int ix0 = 2 * g.cx0 - 6, iy0 = 2 * g.cy0 - 6;
+        const uint32_t* wp =
+            reinterpret_cast<const uint32_t*>(in + (size_t)(iy0 + warp) * a.in_pitch + ix0 - U8_OFF) + min(lane, 21);
+        const size_t wstep = (size_t)NWARPS * a.in_pitch / 4;
+        uint32_t wv[RPW];
+#pragma unroll
+        for (int k = 0; k < RPW; ++k) wv[k] = (warp + NWARPS * k < AIN) ? __ldg(wp + k * wstep) : 0u;
+#pragma unroll
+        for (int k = 0; k < RPW; ++k) {
+            const int r = warp + NWARPS * k;
+            if (r < AIN && lane < 22) reinterpret_cast<uint32_t*>(s_in8 + r * U8_P)[lane] = wv[k];
+        }
+    } else {
+        uint8_t v[RPW][3];
+        int ixs[3];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) ixs[j] = s_ix[min(lane + 32 * j, AIN - 1)];
+#pragma unroll
+        for (int k = 0; k < RPW; ++k) {
+            const uint8_t* row = in + (size_t)s_iy[min(warp + NWARPS * k, AIN - 1)] * a.in_pitch;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) v[k][j] = __ldg(row + ixs[j]);
+        }
+#pragma unroll
+        for (int k = 0; k < RPW; ++k) {
+            const int r = warp + NWARPS * k;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const int c = lane + 32 * j;
+                if (r < AIN && c < AIN) s_in8[r * U8_P + U8_OFF + c] = v[k][j];
+            }
+        }
+    }
+}
+
+// Shared-memory layout of the generic analysis kernel per input type: the
+// input tile (fp32 [AIN][IN_P], or u8 [AIN][U8_P] bytes when PRNU_U8_FLOAT_TILE
+// is not set) later holds the detail planes; the row-pass planes later hold the
+// vertical-sum buffer(s).
+#ifndef PRNU_U8_FLOAT_TILE
+constexpr bool kU8Bytes = true;
+#else
+constexpr bool kU8Bytes = false;
+#endif
+#ifdef PRNU_DOUBLE_V
+constexpr bool kDoubleV = true;    // two vertical-sum buffers (pipelined V/H phases, 3 CTAs/SM)
+#else
+constexpr bool kDoubleV = false;   // one buffer: u8 kernel fits 4 CTAs/SM (measured faster)
+#endif
 template <typename TIn>
-__global__ void __launch_bounds__(A_NT, 3) k_analysis_shrink(AnalysisArgs a) {
+__host__ __device__ constexpr int a_in_floats() {
+    return (sizeof(TIn) == 1 && kU8Bytes) ? (3 * AR * DT_P > (AIN * U8_P + 3) / 4 ? 3 * AR * DT_P : (AIN * U8_P + 3) / 4)
+                                          : A_SMEM_IN;
+}
+__host__ __device__ constexpr int a_row_floats() {
+    return kDoubleV ? A_SMEM_ROW : (2 * RW_PLANE > V_PLANE4 * 4 ? 2 * RW_PLANE : V_PLANE4 * 4);
+}
+template <typename TIn>
+constexpr size_t a_smem_bytes() {
+    return sizeof(float) * (a_in_floats<TIn>() + a_row_floats()) + sizeof(int) * (2 * AIN + 2 * AR);
+}
+#ifndef PRNU_ANALYSIS_MINB
+#define PRNU_ANALYSIS_MINB 4
+#endif
+
+template <typename TIn>
+__global__ void __launch_bounds__(A_NT, PRNU_ANALYSIS_MINB) k_analysis_shrink(AnalysisArgs a) {
     extern __shared__ __align__(128) float smem[];
-    float* s_in = smem;                          // [AIN][IN_P]; later details [3][AR][DT_P]
-    float* s_row = smem + A_SMEM_IN;             // [2][AIN][RW_P]; later vertical sums
-    int* s_iy = reinterpret_cast<int*>(s_row + A_SMEM_ROW);
+    float* s_in = smem;                              // input tile; later details [3][AR][DT_P]
+    float* s_row = smem + a_in_floats<TIn>();        // [2][AIN][RW_P]; later vertical sums
+    int* s_iy = reinterpret_cast<int*>(s_row + a_row_floats());
     int* s_ix = s_iy + AIN;
     int* s_rmap = s_ix + AIN;
     int* s_cmap = s_rmap + AR;
@@ -471,14 +561,21 @@ __global__ void __launch_bounds__(A_NT, 3) k_analysis_shrink(AnalysisArgs a) {
         analysis_tables(a, g, s_iy, s_ix, s_rmap, s_cmap);
         __syncthreads();
     }
-    load_tile<TIn, A_NW>(a, g, fast_u8, s_in, s_iy, s_ix, warp, lane);
-    __syncthreads();
-    rowpass_f32(s_in, s_row);
+    if (sizeof(TIn) == 1 && kU8Bytes) {
+        load_tile_u8<A_NW>(a, g, fast_u8, reinterpret_cast<uint8_t*>(s_in), s_iy, s_ix, warp, lane);
+        __syncthreads();
+        rowpass_u8(reinterpret_cast<const uint8_t*>(s_in), s_row);
+    } else {
+        load_tile<TIn, A_NW>(a, g, fast_u8, s_in, s_iy, s_ix, warp, lane);
+        __syncthreads();
+        rowpass_f32(s_in, s_row);
+    }
     __syncthreads();
     float* s_det = s_in;
     colpass(a, g, s_row, s_det);
     __syncthreads();
-    shrink3(a, g, s_det, reinterpret_cast<float4*>(s_row), s_rmap, s_cmap, CtaBar{});
+    if (kDoubleV) shrink3(a, g, s_det, reinterpret_cast<float4*>(s_row), s_rmap, s_cmap, CtaBar{});
+    else shrink3_single(a, g, s_det, reinterpret_cast<float4*>(s_row), s_rmap, s_cmap);
 }
 
 // Warp-specialized persistent analysis: WS_NP producer warps (tables, input
@@ -920,9 +1017,9 @@ static bool g_attr_done = false;
 static int setup_attributes() {
     if (g_attr_done) return PRNU_OK;
     cudaError_t e1 = cudaFuncSetAttribute(k_analysis_shrink<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)A_SMEM_BYTES);
+                                          (int)a_smem_bytes<float>());
     cudaError_t e2 = cudaFuncSetAttribute(k_analysis_shrink<uint8_t>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)A_SMEM_BYTES);
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a_smem_bytes<uint8_t>());
     cudaError_t e3 = cudaFuncSetAttribute(k_synth_tma<0, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)S_SMEM_BYTES);
     cudaError_t e4 = cudaFuncSetAttribute(k_synth_tma<1, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1003,13 +1100,13 @@ static int denoise_front(const TIn* in, long long in_bstride, int in_pitch, int 
                 const int tx = (int)grid.x, ty = (int)grid.y, n_tiles = tx * ty * nb;
                 k_analysis_ws<TIn><<<std::min(n_tiles, 148), WS_T, WS_SMEM_BYTES, st>>>(a, tx, ty, n_tiles);
             } else {
-                k_analysis_shrink<TIn><<<grid, A_NT, A_SMEM_BYTES, st>>>(a);
+                k_analysis_shrink<TIn><<<grid, A_NT, a_smem_bytes<TIn>(), st>>>(a);
             }
         } else {
             a.in = pb.approx[l - 1];
             a.in_bstride = (long long)pb.bstride[l - 1];
             a.in_pitch = p.pitch[l - 1];
-            k_analysis_shrink<float><<<grid, A_NT, A_SMEM_BYTES, st>>>(a);
+            k_analysis_shrink<float><<<grid, A_NT, a_smem_bytes<float>(), st>>>(a);
         }
         count_launch();
         if ((rc = check_launch("k_analysis_shrink"))) return rc;
