@@ -76,14 +76,20 @@ __host__ __device__ __forceinline__ constexpr float wl_g(int i) {
 }
 
 // Packed fp32 FMA (sm_100a FFMA2): lane-wise RN fma, bit-identical to two fmaf.
-// A scalar first operand is broadcast to both lanes by the instruction itself.
+// The scalar first operand is broadcast inside the asm (mov.b64 {a, a}), which
+// ptxas folds into the instruction's .F32 broadcast operand: no MOVs.
 __device__ __forceinline__ float2 ffma2(float a, float2 b, float2 c) {
-    const float2 aa = make_float2(a, a);
-    unsigned long long ra = *reinterpret_cast<const unsigned long long*>(&aa);
     unsigned long long rb = *reinterpret_cast<const unsigned long long*>(&b);
     unsigned long long rc = *reinterpret_cast<const unsigned long long*>(&c);
     unsigned long long r;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(ra), "l"(rb), "l"(rc));
+    asm("{.reg .b64 aa; mov.b64 aa, {%1, %1}; fma.rn.f32x2 %0, aa, %2, %3;}" : "=l"(r) : "f"(a), "l"(rb), "l"(rc));
+    return *reinterpret_cast<float2*>(&r);
+}
+// Packed product of a broadcast scalar and a pair (FMUL2), == ffma2(a, b, 0).
+__device__ __forceinline__ float2 fmul2s(float a, float2 b) {
+    unsigned long long rb = *reinterpret_cast<const unsigned long long*>(&b);
+    unsigned long long r;
+    asm("{.reg .b64 aa; mov.b64 aa, {%1, %1}; mul.rn.f32x2 %0, aa, %2;}" : "=l"(r) : "f"(a), "l"(rb));
     return *reinterpret_cast<float2*>(&r);
 }
 
@@ -118,5 +124,13 @@ struct ShrinkParams {
 };
 
 int validate_params(const prnu_denoise_params* p, int H, int W, ShrinkParams* sp);
+
+// strip.cu: column-streaming analysis + shrink of one level (see strip.cu)
+int launch_analysis_strip_u8(const uint8_t* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll,
+                             float* d0, float* d1, float* d2, long long out_bstride, int out_pitch, int nH, int nW,
+                             const ShrinkParams& sp, int nb, cudaStream_t st);
+int launch_analysis_strip_f32(const float* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll,
+                              float* d0, float* d1, float* d2, long long out_bstride, int out_pitch, int nH, int nW,
+                              const ShrinkParams& sp, int nb, cudaStream_t st);
 
 }  // namespace prnu

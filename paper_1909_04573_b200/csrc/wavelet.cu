@@ -1055,6 +1055,21 @@ static int synth_maps(const Pyramid& p, const PyramidBuffers& pb, int l, int nb,
     return PRNU_OK;
 }
 
+// Column-streaming strip analysis (strip.cu) unless PRNU_STRIP=0 (A/B switch
+// back to the tile kernel k_analysis_shrink).
+static bool use_strip() {
+    static const bool on = !(getenv("PRNU_STRIP") && getenv("PRNU_STRIP")[0] == '0');
+    return on;
+}
+
+// Deepest level analysed by the strip kernel (PRNU_STRIP_MAXL, default 1): the
+// coarser levels have too few strips x segments to fill the GPU with the
+// strip kernel's sequential blocks; the tile kernel is faster there (measured).
+static int strip_max_level() {
+    static const int l = getenv("PRNU_STRIP_MAXL") ? atoi(getenv("PRNU_STRIP_MAXL")) : 1;
+    return l;
+}
+
 // Analysis of all levels, then synthesis of levels L..2 (the level-1
 // synthesis is launched by the caller, fused or not with the accumulation).
 template <typename TIn>
@@ -1092,7 +1107,16 @@ static int denoise_front(const TIn* in, long long in_bstride, int in_pitch, int 
                                                      (uint64_t)a.NH, (uint64_t)nb, (uint64_t)in_pitch,
                                                      (uint64_t)in_bstride, U8_P, AIN);
             static const bool use_ws = getenv("PRNU_WS_ANALYSIS") != nullptr;   // A/B switch
-            if (tma_ok) {
+            if (use_strip()) {
+                rc = sizeof(TIn) == 1
+                         ? launch_analysis_strip_u8(reinterpret_cast<const uint8_t*>(in), in_bstride, in_pitch, a.NH,
+                                                    a.NW, a.ll, a.d0, a.d1, a.d2, a.out_bstride, a.out_pitch, a.nH,
+                                                    a.nW, sp, nb, st)
+                         : launch_analysis_strip_f32(reinterpret_cast<const float*>(in), in_bstride, in_pitch, a.NH,
+                                                     a.NW, a.ll, a.d0, a.d1, a.d2, a.out_bstride, a.out_pitch, a.nH,
+                                                     a.nW, sp, nb, st);
+                if (rc) return rc;
+            } else if (tma_ok) {
                 const int tx = (int)grid.x, ty = (int)grid.y, n_tiles = tx * ty * nb;
                 const int ctas = std::min(n_tiles, 148 * 3);
                 k_analysis_u8_tma<<<ctas, A_NT, A8_SMEM_BYTES, st>>>(map, a, tx, ty, n_tiles);
@@ -1106,7 +1130,13 @@ static int denoise_front(const TIn* in, long long in_bstride, int in_pitch, int 
             a.in = pb.approx[l - 1];
             a.in_bstride = (long long)pb.bstride[l - 1];
             a.in_pitch = p.pitch[l - 1];
-            k_analysis_shrink<float><<<grid, A_NT, a_smem_bytes<float>(), st>>>(a);
+            if (use_strip() && l <= strip_max_level()) {
+                rc = launch_analysis_strip_f32(pb.approx[l - 1], a.in_bstride, a.in_pitch, a.NH, a.NW, a.ll, a.d0,
+                                               a.d1, a.d2, a.out_bstride, a.out_pitch, a.nH, a.nW, sp, nb, st);
+                if (rc) return rc;
+            } else {
+                k_analysis_shrink<float><<<grid, A_NT, a_smem_bytes<float>(), st>>>(a);
+            }
         }
         count_launch();
         if ((rc = check_launch("k_analysis_shrink"))) return rc;
