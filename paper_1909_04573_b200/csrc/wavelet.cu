@@ -939,6 +939,192 @@ __global__ void __launch_bounds__(256, MODE == 0 ? 3 : PRNU_SYNTH_ACC_MINB) k_sy
     }
 }
 
+// ============================================================== synthesis + accumulate, v2
+// Level-1 inverse fused with the MLE accumulation (a4 + a5):
+// one CTA owns a 32 x 64 pixel tile for every frame of the wave.  Per frame:
+//   * the four coefficient tiles AND the frame's I tile arrive by TMA into a
+//     two-stage ring (frame f+1 lands while f is reconstructed);
+//   * column pass (along y) into a double-buffered pair of L/H planes;
+//   * ONE barrier; the row pass (along x) of 8 pixels per thread feeds the
+//     accumulation straight from registers: NUM += W I (fp64 FMA of the exact
+//     fp32 x fp32 product), DEN += I^2 — for u8 frames an exact integer
+//     sum added to the fp64 accumulator at the end (bit-identical to the
+//     sequential fp64 sum, every partial sum being an integer < 2^53).
+// Per-pixel order is ascending frame order, as in k_synth_tma<1>.
+constexpr int SA_STAGE_COEF = 4 * SC_PS;           // floats per stage (4 planes)
+template <int TY, typename TI>
+constexpr size_t sacc_smem_bytes() {
+    return 2 * SA_STAGE_COEF * sizeof(float) + 3 * TY * ST_X * sizeof(TI) + 2 * 2 * TY * SL_P * sizeof(float) +
+           2 * sizeof(uint64_t);
+}
+
+template <int TY, typename TI>
+#ifndef PRNU_SACC_MINB
+#define PRNU_SACC_MINB 4
+#endif
+__global__ void __launch_bounds__(256, PRNU_SACC_MINB) k_synth_acc2(const __grid_constant__ SynthMaps maps,
+                                                       const __grid_constant__ CUtensorMap imap, SynthArgs a) {
+    constexpr int CY = TY / 2 + 3;   // coefficient rows of a TY-row tile
+    static_assert(TY % 4 == 0 && TY <= 32, "tile height");
+    extern __shared__ __align__(128) float smem[];
+    // coefficient ring of 2 stages (frame f in stage f & 1, released after its
+    // column pass), I-tile ring of 3 (frame f in f % 3, released after its row
+    // pass): frame f+2 is issued at the barrier of frame f, two frames ahead.
+    float* coef0 = smem;                                                      // [2][4][SC_PS]
+    TI* itile0 = reinterpret_cast<TI*>(smem + 2 * SA_STAGE_COEF);             // [3][TY][ST_X]
+    float* sL0 = reinterpret_cast<float*>(itile0 + 3 * TY * ST_X);          // [2][2][TY][SL_P]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sL0 + 2 * 2 * TY * SL_P);
+    const int tid = threadIdx.x;
+    const int ty0 = blockIdx.y * TY, tx0 = blockIdx.x * ST_X;
+    const int ky0 = ty0 >> 1, kx0 = tx0 >> 1;
+    const int nb = a.nb;
+    const uint32_t tx_bytes = (a.has_A ? 4u : 3u) * SC_BW * CY * 4u + (uint32_t)(TY * ST_X * sizeof(TI));
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    if (!a.has_A) {   // coarsest level: the approximation of the noise domain is 0 (R-10)
+        for (int i = tid; i < SC_PS; i += 256) {
+            coef0[i] = 0.f;
+            coef0[SA_STAGE_COEF + i] = 0.f;
+        }
+    }
+    __syncthreads();
+    auto issue = [&](int f) {
+        const int st = f & 1;
+        float* c = coef0 + st * SA_STAGE_COEF;
+        mbar_arrive_expect_tx(&bar[st], tx_bytes);
+        if (a.has_A) tma_load_3d(c, &maps.A, kx0, ky0, f, &bar[st]);
+        tma_load_3d(c + 1 * SC_PS, &maps.d0, kx0, ky0, f, &bar[st]);
+        tma_load_3d(c + 2 * SC_PS, &maps.d1, kx0, ky0, f, &bar[st]);
+        tma_load_3d(c + 3 * SC_PS, &maps.d2, kx0, ky0, f, &bar[st]);
+        tma_load_3d(itile0 + (f % 3) * TY * ST_X, &imap, tx0, ty0, f, &bar[st]);
+    };
+    if (tid == 0) {
+        if (nb > 0) issue(0);
+        if (nb > 1) issue(1);
+    }
+
+    // row pass / accumulate mapping: warp w rows 4w .. 4w+3, lane -> (row 4w + (lane & 3), 8 columns at 8 (lane >> 2))
+    const int lane = tid & 31, warp = tid >> 5;
+    const int rt = 4 * warp + (lane & 3), rg = lane >> 2;
+    const int gy = ty0 + rt, gx = tx0 + 8 * rg;
+    const bool rowact = rt < TY;            // warp-uniform: the last warp idles in the row pass when TY = 28
+    const bool rowok = rowact && gy < a.NH;
+    double num[8];
+    uint32_t den_i[8];
+    double den_d[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        num[k] = (rowok && gx + k < a.NW) ? a.num[(size_t)gy * a.acc_pitch + gx + k] : 0.0;
+        den_i[k] = 0u;
+        den_d[k] = 0.0;
+    }
+    if (sizeof(TI) == 4) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) den_d[k] = (rowok && gx + k < a.NW) ? a.den[(size_t)gy * a.acc_pitch + gx + k] : 0.0;
+    }
+
+    for (int f = 0; f < nb; ++f) {
+        const int st = f & 1;
+        mbar_wait(&bar[st], (f >> 1) & 1);
+        const float* c = coef0 + st * SA_STAGE_COEF;
+        float* sLo = sL0 + (f & 1) * 2 * TY * SL_P;
+        float* sHi = sLo + TY * SL_P;
+        // column pass: Lx = synth_y(A, ad), Hx = synth_y(da, dd); item = (coefficient column k, 4 output rows)
+        for (int it = tid; it < SC_X * (TY / 4); it += 256) {
+            const int k = it < 32 * (TY / 4) ? (it & 31) : 32 + (it - 32 * (TY / 4)) % (SC_X - 32);
+            const int sg = it < 32 * (TY / 4) ? (it >> 5) : (it - 32 * (TY / 4)) / (SC_X - 32);
+            float va[5], vda[5], vad[5], vdd[5];
+#pragma unroll
+            for (int m = 0; m < 5; ++m) {
+                const int r = (2 * sg + m) * SC_BW + k;
+                va[m] = c[0 * SC_PS + r];
+                vda[m] = c[1 * SC_PS + r];
+                vad[m] = c[2 * SC_PS + r];
+                vdd[m] = c[3 * SC_PS + r];
+            }
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                float2 l = fmul2s(va[q], c_sh[0]), h = fmul2s(vda[q], c_sh[0]);
+                l = ffma2(vad[q], c_sg[0], l);
+                h = ffma2(vdd[q], c_sg[0], h);
+#pragma unroll
+                for (int m = 1; m < 4; ++m) {
+                    l = ffma2(va[q + m], c_sh[m], l);
+                    l = ffma2(vad[q + m], c_sg[m], l);
+                    h = ffma2(vda[q + m], c_sh[m], h);
+                    h = ffma2(vdd[q + m], c_sg[m], h);
+                }
+                const int t = 4 * sg + 2 * q;
+                sLo[t * SL_P + k] = l.x;
+                sLo[(t + 1) * SL_P + k] = l.y;
+                sHi[t * SL_P + k] = h.x;
+                sHi[(t + 1) * SL_P + k] = h.y;
+            }
+        }
+        __syncthreads();   // L/H planes of frame f complete; every thread is past frame f-1
+        if (tid == 0 && f + 2 < nb) {
+            fence_proxy_async();
+            issue(f + 2);   // coefficient stage of frame f, I stage of frame f-1: both consumed
+        }
+        if (!rowact) continue;
+        // row pass of 8 pixels + accumulation
+        float vl[7], vh[7];
+#pragma unroll
+        for (int m = 0; m < 7; ++m) {
+            vl[m] = sLo[rt * SL_P + 4 * rg + m];
+            vh[m] = sHi[rt * SL_P + 4 * rg + m];
+        }
+        float w[8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            float2 x = fmul2s(vl[q], c_sh[0]);
+            x = ffma2(vh[q], c_sg[0], x);
+#pragma unroll
+            for (int m = 1; m < 4; ++m) {
+                x = ffma2(vl[q + m], c_sh[m], x);
+                x = ffma2(vh[q + m], c_sg[m], x);
+            }
+            w[2 * q] = x.x;
+            w[2 * q + 1] = x.y;
+        }
+        const TI* irow = itile0 + (f % 3) * TY * ST_X + rt * ST_X + 8 * rg;
+        if (sizeof(TI) == 1) {
+            const uint2 iv = *reinterpret_cast<const uint2*>(irow);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t xb = __byte_perm(k < 4 ? iv.x : iv.y, 0, 0x4440u | (uint32_t)(k & 3));
+                den_i[k] += xb * xb;
+                // exact integer -> double: (2^52 + x) - 2^52
+                const double xd = __hiloint2double(0x43300000, (int)xb) - 4503599627370496.0;
+                num[k] = fma((double)w[k], xd, num[k]);   // exact product, one fp64 rounding
+            }
+        } else {
+            const float4 i0 = *reinterpret_cast<const float4*>(irow);
+            const float4 i1 = *reinterpret_cast<const float4*>(irow + 4);
+            const float iv[8] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const double xd = (double)iv[k];
+                num[k] = fma((double)w[k], xd, num[k]);
+                den_d[k] = fma(xd, xd, den_d[k]);
+            }
+        }
+    }
+    if (rowok) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (gx + k < a.NW) {
+                a.num[(size_t)gy * a.acc_pitch + gx + k] = num[k];
+                double* dp = a.den + (size_t)gy * a.acc_pitch + gx + k;
+                *dp = sizeof(TI) == 1 ? *dp + (double)den_i[k] : den_d[k];
+            }
+        }
+    }
+}
+
 // ============================================================== host side
 Pyramid make_pyramid(int H, int W, int levels) {
     Pyramid p{};
@@ -1219,9 +1405,60 @@ int run_residual_accumulate(const TIn* in, const TIn* I, int nb, int H, int W, c
     dim3 grid((W + ST_X - 1) / ST_X, (H + ST_Y - 1) / ST_Y, 1);
     if (acc_wait && cudaStreamWaitEvent(st, acc_wait, 0) != cudaSuccess)
         return fail(PRNU_CUDA_ERROR, "cudaStreamWaitEvent");
+    // v2 (TMA-staged I tiles, one barrier per frame) unless PRNU_SACC2=0 or the
+    // frames violate the TMA stride/alignment rules.  Tile height 32 or 28 rows,
+    // whichever fills the last wave of 4 CTAs/SM better.
+    static const bool sacc2 = !(getenv("PRNU_SACC2") && getenv("PRNU_SACC2")[0] == '0');
+    const int slots = 148 * 4;
+    auto waste = [&](int ty) {
+        const long n = (long)((W + ST_X - 1) / ST_X) * ((H + ty - 1) / ty);
+        return (double)((n + slots - 1) / slots) * ty / ((double)n * ty / slots);   // waves rounded up / exact
+    };
+    const int TYsel = waste(28) < waste(32) - 1e-9 ? 28 : 32;
+    CUtensorMap imap;
+    SynthMaps m2;
+    const size_t es = sizeof(TIn);
+    bool v2 = sacc2 && ((size_t)W * es) % 16 == 0 && ((size_t)frame_stride * es) % 16 == 0 &&
+              ((uintptr_t)I % 16) == 0 &&
+              encode_tensor_map_3d(&imap, sizeof(TIn) == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                   es, I, (uint64_t)W, (uint64_t)H, (uint64_t)nb, (uint64_t)W * es,
+                                   (uint64_t)frame_stride * es, ST_X, TYsel);
+    if (v2) {
+        const uint64_t pitch = (uint64_t)p.pitch[1] * 4, plane = (uint64_t)pb.bstride[1] * 4;
+        const float* src[4] = {pb.approx[1], pb.det[1][0], pb.det[1][1], pb.det[1][2]};
+        CUtensorMap* dst[4] = {&m2.A, &m2.d0, &m2.d1, &m2.d2};
+        for (int i = 0; i < 4 && v2; ++i) {
+            if (i == 0 && !s.has_A) {
+                *dst[0] = CUtensorMap{};
+                continue;
+            }
+            v2 = encode_tensor_map_3d(dst[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, src[i], p.nW[1], p.nH[1], nb, pitch,
+                                      plane, SC_BW, TYsel / 2 + 3);
+        }
+    }
     {
         KTimer kt(sizeof(TIn) == 1 ? "synth_acc_l1_u8" : "synth_acc_l1_f32", st);
-        k_synth_tma<1, TIn><<<grid, 256, S_SMEM_BYTES, st>>>(m, s);
+        if (v2) {
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(k_synth_acc2<32, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sacc_smem_bytes<32, uint8_t>());
+                cudaFuncSetAttribute(k_synth_acc2<32, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sacc_smem_bytes<32, float>());
+                cudaFuncSetAttribute(k_synth_acc2<28, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sacc_smem_bytes<28, uint8_t>());
+                cudaFuncSetAttribute(k_synth_acc2<28, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sacc_smem_bytes<28, float>());
+                attr = true;
+            }
+            dim3 g2((W + ST_X - 1) / ST_X, (H + TYsel - 1) / TYsel, 1);
+            if (TYsel == 28)
+                k_synth_acc2<28, TIn><<<g2, 256, sacc_smem_bytes<28, TIn>(), st>>>(m2, imap, s);
+            else
+                k_synth_acc2<32, TIn><<<g2, 256, sacc_smem_bytes<32, TIn>(), st>>>(m2, imap, s);
+        } else {
+            k_synth_tma<1, TIn><<<grid, 256, S_SMEM_BYTES, st>>>(m, s);
+        }
     }
     count_launch();
     if ((rc = check_launch("k_synth_tma(accumulate)"))) return rc;
