@@ -354,13 +354,14 @@ def main():
         achieved = kt.get("alg_GBps")
         # DRAM traffic per launch of that kernel from the committed ncu --set full capture
         # (same kernel and launch configuration), else null
+        # (bytes per frame of the capture x this run's average frames per launch)
         traffic = None
         tpath = os.path.join(ROOT, "profiles", "latest_traffic.json")
         if os.path.exists(tpath):
             t = json.load(open(tpath))
-            fpl = n_sda.get(1, 0) / max(1.0, kt["launches_per_step"]) if top.endswith("_u8") else None
-            if t.get("kernel") == top and fpl and abs(fpl - t["frames_per_launch"]) < 1.0:
-                traffic = t["dram_bytes_read"] + t["dram_bytes_write"]
+            fpl = (n_sda.get(1, 0) + 1) / max(1.0, kt["launches_per_step"]) if top.endswith("_u8") else None
+            if t.get("kernel") == top and fpl and t.get("H") == H and t.get("W") == W:
+                traffic = (t["dram_bytes_read"] + t["dram_bytes_write"]) / t["frames_per_launch"] * fpl
         roof = {"kernel": top, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback",

@@ -74,6 +74,7 @@ __constant__ float2 c_sh[4] = {{PRNU_H6, PRNU_H7}, {PRNU_H4, PRNU_H5}, {PRNU_H2,
 __constant__ float2 c_sg[4] = {{PRNU_H1, -PRNU_H0}, {PRNU_H3, -PRNU_H2}, {PRNU_H5, -PRNU_H4}, {PRNU_H7, -PRNU_H6}};
 
 // Analysis (lo, hi) tap pairs: immediates (default) or constant-memory pairs.
+// (immediates measured faster than constant-memory pairs in this kernel, profiles/r01)
 #ifdef PRNU_HG_CONST
 #define PRNU_HG(i) c_hg[i]
 #else
@@ -122,9 +123,9 @@ __device__ __forceinline__ void rowpass_item(const float (&v)[24], float* s_row,
     float lo[8], hi[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-        float2 lh = make_float2(0.f, 0.f);   // (lo, hi) in one FFMA2 per tap
+        float2 lh = fmul2s(v[2 * q], PRNU_HG(0));   // (lo, hi) in one FFMA2 per tap
 #pragma unroll
-        for (int i = 0; i < 8; ++i) lh = ffma2(v[2 * q + i], PRNU_HG(i), lh);
+        for (int i = 1; i < 8; ++i) lh = ffma2(v[2 * q + i], PRNU_HG(i), lh);
         lo[q] = lh.x;
         hi[q] = lh.y;
     }
@@ -204,9 +205,9 @@ __device__ __forceinline__ void colpass(const AnalysisArgs& a, const ATile& g, c
                           : nullptr;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            float2 p_l = make_float2(0.f, 0.f), p_h = make_float2(0.f, 0.f);   // (aa, ad), (da, dd)
+            float2 p_l = fmul2s(lo[2 * q], PRNU_HG(0)), p_h = fmul2s(hi[2 * q], PRNU_HG(0));   // (aa, ad), (da, dd)
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
+            for (int i = 1; i < 8; ++i) {
                 p_l = ffma2(lo[2 * q + i], PRNU_HG(i), p_l);
                 p_h = ffma2(hi[2 * q + i], PRNU_HG(i), p_h);
             }
@@ -293,8 +294,10 @@ __device__ __forceinline__ void shrink_h_t(const AnalysisArgs& a, const ATile& g
             if (wm & 4) m = fminf(m, s7 * (1.0f / 49.0f));
             if (wm & 8) m = fminf(m, s9 * (1.0f / 81.0f));
         }
-        const float var = fmaxf(m - s0, 0.0f);
-        o[t] = crow[t] * __fdividef(s0, var + s0);   // noise-domain coefficient c - F(c)
+        // noise-domain coefficient c - F(c) = c s0 / (max(m - s0, 0) + s0) = c s0 / max(m, s0)
+        float r;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(fmaxf(m, s0)));
+        o[t] = crow[t] * s0 * r;
     }
     if (gy < a.nH) {
         const int gx = g.x0 + 8 * jg;
