@@ -162,6 +162,16 @@ def algorithmic_bytes_per_step(name: str, H: int, W: int, levels: int, depths, m
     f_all = f_u8 + f_f32
     if name == "sda_average":
         return sum((m // d) * (d * P + 4 * P) for d in depths if d > 1)
+    if name == "dwt_l1_u8":
+        return f_u8 * (1 * P + 4 * 4 * n[1])
+    if name == "dwt_l1_f32":
+        return f_f32 * (4 * P + 4 * 4 * n[1])
+    if name.startswith("dwt_l"):
+        l = int(name[-1])
+        return f_all * (4 * n[l - 1] + (4 if l < levels else 3) * 4 * n[l])
+    if name.startswith("shrink_l"):
+        l = int(name[-1])
+        return f_all * 2 * 3 * 4 * n[l]          # raw details read once, c - F(c) written once
     if name == "analysis_l1_u8":
         return f_u8 * (1 * P + 4 * 4 * n[1])
     if name == "analysis_l1_f32":

@@ -125,6 +125,16 @@ struct ShrinkParams {
 
 int validate_params(const prnu_denoise_params* p, int H, int W, ShrinkParams* sp);
 
+// split.cu: one level as a streaming DWT kernel + a streaming shrink kernel
+int launch_dwt_strip_u8(const uint8_t* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll, float* c0,
+                        float* c1, float* c2, long long out_bstride, int out_pitch, int nH, int nW, int nb,
+                        cudaStream_t st);
+int launch_dwt_strip_f32(const float* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll, float* c0,
+                         float* c1, float* c2, long long out_bstride, int out_pitch, int nH, int nW, int nb,
+                         cudaStream_t st);
+int launch_shrink_strip(const float* const src[3], float* const dst[3], long long bstride, int pitch, int nH, int nW,
+                        const ShrinkParams& sp, int nb, cudaStream_t st);
+
 // strip.cu: column-streaming analysis + shrink of one level (see strip.cu)
 int launch_analysis_strip_u8(const uint8_t* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll,
                              float* d0, float* d1, float* d2, long long out_bstride, int out_pitch, int nH, int nW,

@@ -548,6 +548,11 @@ bool encode_tensor_map_3d(CUtensorMap* map, CUtensorMapDataType dt, size_t elem_
                           uint32_t box_h);
 
 static bool g_strip_attr = false;
+// A/B experiment knob: extra dynamic shared memory per CTA (lowers occupancy)
+static int smem_pad() {
+    static const int p = getenv("PRNU_STRIP_SMEM_PAD") ? atoi(getenv("PRNU_STRIP_SMEM_PAD")) : 0;
+    return p;
+}
 constexpr int MINB = 3;
 
 template <typename T>
@@ -557,13 +562,13 @@ static int strip_launch(const T* in, long long in_bstride, int in_pitch, int NH,
     if (!g_strip_attr) {
         cudaError_t e[4] = {
             cudaFuncSetAttribute(k_analysis_strip<uint8_t, MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)strip_smem_bytes<uint8_t>()),
+                                 (int)strip_smem_bytes<uint8_t>() + smem_pad()),
             cudaFuncSetAttribute(k_analysis_strip<uint8_t, MINB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)strip_smem_bytes<uint8_t>()),
+                                 (int)strip_smem_bytes<uint8_t>() + smem_pad()),
             cudaFuncSetAttribute(k_analysis_strip<float, MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)strip_smem_bytes<float>()),
+                                 (int)strip_smem_bytes<float>() + smem_pad()),
             cudaFuncSetAttribute(k_analysis_strip<float, MINB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)strip_smem_bytes<float>())};
+                                 (int)strip_smem_bytes<float>() + smem_pad())};
         for (cudaError_t x : e)
             if (x != cudaSuccess)
                 return fail(PRNU_CUDA_ERROR, std::string("cudaFuncSetAttribute(strip): ") + cudaGetErrorString(x));
@@ -601,9 +606,9 @@ static int strip_launch(const T* in, long long in_bstride, int in_pitch, int NH,
     if (no_tma) a.use_tma = 0;
     dim3 grid(S, nseg, nb);
     if (sp.wmask == 15)
-        k_analysis_strip<T, MINB, true><<<grid, SR_NT, strip_smem_bytes<T>(), st>>>(map, a);
+        k_analysis_strip<T, MINB, true><<<grid, SR_NT, strip_smem_bytes<T>() + smem_pad(), st>>>(map, a);
     else
-        k_analysis_strip<T, MINB, false><<<grid, SR_NT, strip_smem_bytes<T>(), st>>>(map, a);
+        k_analysis_strip<T, MINB, false><<<grid, SR_NT, strip_smem_bytes<T>() + smem_pad(), st>>>(map, a);
     return PRNU_OK;
 }
 

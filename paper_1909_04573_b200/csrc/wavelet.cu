@@ -1150,13 +1150,14 @@ Pyramid make_pyramid(int H, int W, int levels) {
 size_t pyramid_floats_per_frame(const Pyramid& p) {
     size_t f = 0;
     for (int l = 1; l <= p.levels; ++l) f += 4 * p.plane[l];
-    return f;
+    return f + 3 * p.plane[1];   // + raw detail scratch of the split analysis (level-1 size, reused by every level)
 }
 
 struct PyramidBuffers {
     float* approx[kMaxLevels + 1];   // level-l approximation, reused for the synthesis output of level l+1
     float* det[kMaxLevels + 1][3];
     size_t bstride[kMaxLevels + 1];  // floats between frames within a level buffer
+    float* raw[3];                   // raw detail scratch (split analysis), batch x plane[1] floats each
 };
 
 PyramidBuffers carve_pyramid(const Pyramid& p, float* base, int batch) {
@@ -1170,6 +1171,10 @@ PyramidBuffers carve_pyramid(const Pyramid& p, float* base, int batch) {
             pb.det[l][s] = cur;
             cur += (size_t)batch * p.plane[l];
         }
+    }
+    for (int s = 0; s < 3; ++s) {
+        pb.raw[s] = cur;
+        cur += (size_t)batch * p.plane[1];
     }
     return pb;
 }
@@ -1251,6 +1256,27 @@ static bool use_strip() {
     return on;
 }
 
+// Split analysis (split.cu: streaming DWT + streaming shrink) unless PRNU_SPLIT=0.
+static bool use_split() {
+    static const bool on = !(getenv("PRNU_SPLIT") && getenv("PRNU_SPLIT")[0] == '0');
+    return on;
+}
+// First level analysed by the split kernels (PRNU_SPLIT_MINL, default 2): level 1
+// stays with the fused strip kernel (12.0 vs 13.6 ms/step split, profiles/r01).
+static int split_min_level() {
+    static const int l = getenv("PRNU_SPLIT_MINL") ? atoi(getenv("PRNU_SPLIT_MINL")) : 2;
+    return l;
+}
+// Last level analysed by the split kernels (PRNU_SPLIT_MAXL, default 2): on the
+// small coarse planes the tile kernel is faster (profiles/r01).
+static int split_max_level() {
+    static const int l = getenv("PRNU_SPLIT_MAXL") ? atoi(getenv("PRNU_SPLIT_MAXL")) : 2;
+    return l;
+}
+static const char* kDwtName[kMaxLevels + 1] = {"", "dwt_l1", "dwt_l2", "dwt_l3", "dwt_l4", "dwt_l5", "dwt_l6"};
+static const char* kShrinkName[kMaxLevels + 1] = {"", "shrink_l1", "shrink_l2", "shrink_l3",
+                                                  "shrink_l4", "shrink_l5", "shrink_l6"};
+
 // Deepest level analysed by the strip kernel (PRNU_STRIP_MAXL, default 1): the
 // coarser levels have too few strips x segments to fill the GPU with the
 // strip kernel's sequential blocks; the tile kernel is faster there (measured).
@@ -1281,6 +1307,33 @@ static int denoise_front(const TIn* in, long long in_bstride, int in_pitch, int 
         a.nW = p.nW[l];
         a.sp = sp;
         dim3 grid((p.nW[l] + AT - 1) / AT, (p.nH[l] + AT - 1) / AT, nb);
+        if (use_split() && l >= split_min_level() && l <= split_max_level()) {   // streaming DWT kernel + streaming shrink kernel (split.cu)
+            {
+                KTimer kt(l == 1 ? (sizeof(TIn) == 1 ? "dwt_l1_u8" : "dwt_l1_f32") : kDwtName[l], st);
+                if (l == 1 && sizeof(TIn) == 1)
+                    rc = launch_dwt_strip_u8(reinterpret_cast<const uint8_t*>(in), in_bstride, in_pitch, a.NH, a.NW,
+                                             a.ll, pb.raw[0], pb.raw[1], pb.raw[2], a.out_bstride, a.out_pitch, a.nH,
+                                             a.nW, nb, st);
+                else
+                    rc = launch_dwt_strip_f32(l == 1 ? reinterpret_cast<const float*>(in) : pb.approx[l - 1],
+                                              l == 1 ? in_bstride : (long long)pb.bstride[l - 1],
+                                              l == 1 ? in_pitch : p.pitch[l - 1], a.NH, a.NW, a.ll, pb.raw[0],
+                                              pb.raw[1], pb.raw[2], a.out_bstride, a.out_pitch, a.nH, a.nW, nb, st);
+                if (rc) return rc;
+            }
+            count_launch();
+            if ((rc = check_launch("k_dwt_strip"))) return rc;
+            {
+                KTimer kt(kShrinkName[l], st);
+                const float* src[3] = {pb.raw[0], pb.raw[1], pb.raw[2]};
+                float* dst[3] = {a.d0, a.d1, a.d2};
+                rc = launch_shrink_strip(src, dst, a.out_bstride, a.out_pitch, a.nH, a.nW, sp, nb, st);
+                if (rc) return rc;
+            }
+            count_launch();
+            if ((rc = check_launch("k_shrink_strip"))) return rc;
+            continue;
+        }
         KTimer kt(l == 1 ? (sizeof(TIn) == 1 ? "analysis_l1_u8" : "analysis_l1_f32") : kAnalysisName[l], st);
         if (l == 1) {
             a.in = in;

@@ -271,7 +271,9 @@ def test_camera_identification_small(prnu):
 def test_launch_counter_advances(prnu):
     before = prnu.kernel_launches()
     prnu.residual(torch.zeros((1, 64, 64), device="cuda"))
-    assert prnu.kernel_launches() - before == 8   # 4 analysis + 4 synthesis
+    n = prnu.kernel_launches() - before
+    # 4 synthesis launches; per analysis level 1 launch (fused) or 2 (DWT + shrink, split levels)
+    assert 8 <= n <= 12, n
 
 
 # ---------------------------------------------------------------- f1 block-wise
