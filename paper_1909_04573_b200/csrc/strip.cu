@@ -37,26 +37,43 @@
 
 namespace prnu {
 
+// Phase-time probes (build with -DPRNU_STRIP_PROFILE; read with prnu_debug_strip_profile):
+// per warp, clock64 cycles spent in each phase of a block, summed over warps and CTAs.
+#ifdef PRNU_STRIP_PROFILE
+__device__ unsigned long long g_strip_prof[16];
+#define SPROBE(i)                                         \
+    do {                                                  \
+        const long long now_ = clock64();                 \
+        pacc[i] += (unsigned long long)(now_ - plast);    \
+        plast = now_;                                     \
+    } while (0)
+#else
+#define SPROBE(i) \
+    do {          \
+    } while (0)
+#endif
+
 constexpr int SR_NT = 128;                  // threads per CTA == region columns
 constexpr int SR_RW = 128;                  // region width (O + 8 <= 128)
-constexpr int SR_OMAX = SR_RW - 8;          // max output columns per strip
+constexpr int SR_OMAX = 112;                // max output columns per strip (O + 8 <= SR_P2: the V planes hold ncols columns)
 constexpr int SR_BK = 8;                    // coefficient rows per block
 constexpr int SR_IR = 2 * SR_BK;            // input rows per block
-constexpr int SR_HALF = SR_RW / 2 + 16;     // Filter tap pairs (H_[i], G_[i]) and window scales in constant memory: FFMA2 /
+// Filter tap pairs (H_[i], G_[i]) and window scales in constant memory: FFMA2 /
 // FMUL2 read them as uniform operands (no per-use MOVs of immediate pairs).
 __constant__ float2 c_st_hg[8] = {{PRNU_H0, PRNU_H7}, {PRNU_H1, -PRNU_H6}, {PRNU_H2, PRNU_H5}, {PRNU_H3, -PRNU_H4},
                                   {PRNU_H4, PRNU_H3}, {PRNU_H5, -PRNU_H2}, {PRNU_H6, PRNU_H1}, {PRNU_H7, -PRNU_H0}};
 __constant__ float2 c_st_ws[2] = {{1.0f / 9.0f, 1.0f / 25.0f}, {1.0f / 49.0f, 1.0f / 81.0f}};
 
-// row-buffer column permutation: second half offset (== 16 mod 32)
-constexpr int SR_RBP = 164;                 // row-buffer pitch (== 4 mod 32: conflict-free STS.128, lanes over rows)
+constexpr int SR_RBP = 132;                 // row-buffer pitch (== 4 mod 32: conflict-free STS.128, lanes over rows)
 constexpr int SR_RB_FLOATS = 2 * SR_IR * SR_RBP;
-constexpr int SR_P2 = SR_RW + 1;            // float2 pitch of the vertical-sum planes (8 B mod 128 B)
-constexpr int SR_CP = SR_RW + 4;            // float pitch of coefficient rows (16 B mod 128 B)
+constexpr int SR_P2 = 121;                  // float2 pitch of the vertical-sum planes (== 1 mod 8: conflict-free LDS.64)
+constexpr int SR_CP = 124;                  // float pitch of coefficient rows (496 B == 112 mod 128)
 // V/c buffer of one subband: (v3, v5) plane [8][SR_P2] float2, (v7, v9) plane, c plane [8][SR_CP]
 constexpr int SR_VC_FLOATS = 2 * SR_BK * SR_P2 * 2 + SR_BK * SR_CP;
 constexpr int SR_A_FLOATS = SR_RB_FLOATS > SR_VC_FLOATS ? SR_RB_FLOATS : SR_VC_FLOATS;
-static_assert(SR_HALF + SR_RW / 2 <= SR_RBP, "row buffer pitch");
+constexpr int SR_NSTG = 3;                  // staging buffers: TMA two blocks ahead
+static_assert(8 * 16 <= SR_RBP, "row-buffer columns of the 16 row-pass groups");
+static_assert(SR_OMAX + 8 <= SR_P2 && SR_OMAX + 8 <= SR_CP, "V/c planes hold every region column");
 
 // Staging: two TMA boxes per block, box 0 = logical columns [0, BOXW), box 1 =
 // [128, 128 + BOXW), each [16 rows][BOXW] dense.  A row-pass group g reads
@@ -81,7 +98,7 @@ __host__ __device__ constexpr int strip_stage_elems() { return 2 * SR_IR * Strip
 
 template <typename T>
 constexpr size_t strip_smem_bytes() {
-    return 2 * strip_stage_elems<T>() * sizeof(T) + sizeof(float) * (SR_A_FLOATS + 2 * SR_VC_FLOATS) + 16;
+    return SR_NSTG * strip_stage_elems<T>() * sizeof(T) + sizeof(float) * (SR_A_FLOATS + 2 * SR_VC_FLOATS) + 32;
 }
 
 struct StripArgs {
@@ -102,8 +119,6 @@ struct StripArgs {
     int use_tma;
 };
 
-// row-buffer column permutation: columns 8g..8g+3 at 4g.., 8g+4..8g+7 at HALF + 4g..
-__device__ __forceinline__ int sr_pos(int c) { return ((c & 4) ? SR_HALF : 0) + 4 * (c >> 3) + (c & 3); }
 
 template <typename T>
 __device__ __forceinline__ float stg_at(const T* s, int r, int x) {
@@ -185,7 +200,7 @@ __global__ void __launch_bounds__(SR_NT, MINB) k_analysis_strip(const __grid_con
     constexpr int STG = strip_stage_elems<T>();
     extern __shared__ __align__(128) unsigned char smem[];
     T* stg0 = reinterpret_cast<T*>(smem);
-    float* regA = reinterpret_cast<float*>(smem + 2 * STG * sizeof(T));   // row buffer, later V/c buffer A
+    float* regA = reinterpret_cast<float*>(smem + SR_NSTG * STG * sizeof(T));   // row buffer, later V/c buffer A
     float* regB = regA + SR_A_FLOATS;                                      // V/c buffer of subband 0
     float* regC = regB + SR_VC_FLOATS;                                     // V/c buffer of subband 2
     uint64_t* bar = reinterpret_cast<uint64_t*>(regC + SR_VC_FLOATS);
@@ -205,7 +220,7 @@ __global__ void __launch_bounds__(SR_NT, MINB) k_analysis_strip(const __grid_con
     // column-pass source: in-plane columns read their own row-pass column; the
     // mirrored halo columns outside the subband read their partner (R-4)
     const int src_t = (gc < 0 || gc >= a.nW) ? min(max(mirror(gc, a.nW) - cx0 + 4, 0), SR_RW - 1) : t;
-    const int pos = sr_pos(src_t);
+    const int pos = src_t;   // row-buffer column (plain layout)
     const bool inner = (t >= 4) && (t < 4 + a.O) && (gc < a.nW);
     // row-pass items of this thread: row rr of groups ga and ga + 8 (skipped when
     // every column of the group lies beyond the subband)
@@ -219,8 +234,7 @@ __global__ void __launch_bounds__(SR_NT, MINB) k_analysis_strip(const __grid_con
     const bool hfull = hx + 8 <= a.nW;
 
     if (t == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+        for (int k = 0; k < SR_NSTG; ++k) mbar_init(&bar[k], 1);
         fence_mbar_init();
     }
 
@@ -246,17 +260,30 @@ __global__ void __launch_bounds__(SR_NT, MINB) k_analysis_strip(const __grid_con
         }
     }
 
+    // block i (i = -1: the prologue) is staged in buffer (i + 3) % 3; blocks load input
+    // rows 2K .. 2K+15, the prologue rows 2K0-6 .. 2K0-1 as rows 10..15 of a box at 2K0-16
+    auto stg_of = [&](int i) { return (i + SR_NSTG) % SR_NSTG; };
+    auto box_y = [&](int i) { return i < 0 ? 2 * K0 - 16 : 2 * (K0 + SR_BK * i); };
+    // blocks whose rows lie inside the plane are staged by TMA (a 16-row box pair; the
+    // prologue box starts 10 rows early); blocks whose rows mirror (R-4) are loaded
+    // by the threads (u8 TMA boxes cannot target single 144-byte rows: the shared
+    // destination of a box must be 128-byte aligned)
     auto tma_ok = [&](int i) {
-        const int y = 2 * (K0 + SR_BK * i);
+        const int y = box_y(i);
         return a.use_tma && y >= 0 && y + SR_IR <= a.NH;
     };
     auto issue = [&](int i) {   // thread 0 only
-        T* s = stg0 + (i & 1) * STG;
-        const int y = 2 * (K0 + SR_BK * i);
-        mbar_arrive_expect_tx(&bar[i & 1], (uint32_t)(2 * SR_IR * BW * sizeof(T)));
-        tma_load_3d(s, &map, xs, y, b, &bar[i & 1]);
-        tma_load_3d(s + SR_IR * BW, &map, xs + 128, y, b, &bar[i & 1]);
+        const int k = stg_of(i);
+        T* s = stg0 + k * STG;
+        const int y = box_y(i);
+        mbar_arrive_expect_tx(&bar[k], (uint32_t)(2 * SR_IR * BW * sizeof(T)));
+        tma_load_3d(s, &map, xs, y, b, &bar[k]);
+        tma_load_3d(s + SR_IR * BW, &map, xs + 128, y, b, &bar[k]);
     };
+    if (t == 0) {   // prologue and blocks 0, 1 in flight before anything else
+        for (int i = -1; i < 2 && i < nblk; ++i)
+            if (tma_ok(i)) issue(i);
+    }
     // Thread loads of nr rows starting at input row y0, rows and columns
     // mirrored (R-4), 16-byte chunks, all of a thread's chunks in flight first.
     const bool vec_ok = ((reinterpret_cast<uintptr_t>(in) & 15) == 0) && ((a.in_pitch * sizeof(T)) % 16 == 0);
@@ -295,13 +322,13 @@ __global__ void __launch_bounds__(SR_NT, MINB) k_analysis_strip(const __grid_con
     };
     // Row pass (along x) of row rr < nr of the staged rows into the row buffer
     // (regA): lo plane rows [0, 16), hi plane rows [16, 32), columns permuted.
-    auto rowpass = [&](const T* s, int nr) {
+    auto rowpass = [&](const T* s, int r0, int nr) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int g = ga + 8 * h;
             if ((h == 0 ? doA : doB) && rr < nr) {
                 float v[24];
-                stg_row22(s, rr, g, v);
+                stg_row22(s, r0 + rr, g, v);
                 float lo[8], hi[8];
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
@@ -311,12 +338,12 @@ __global__ void __launch_bounds__(SR_NT, MINB) k_analysis_strip(const __grid_con
                     lo[q] = lh.x;
                     hi[q] = lh.y;
                 }
-                float* dl = regA + rr * SR_RBP + 4 * g;
+                float* dl = regA + rr * SR_RBP + 8 * g;
                 float* dh = dl + SR_IR * SR_RBP;
                 *reinterpret_cast<float4*>(dl) = make_float4(lo[0], lo[1], lo[2], lo[3]);
-                *reinterpret_cast<float4*>(dl + SR_HALF) = make_float4(lo[4], lo[5], lo[6], lo[7]);
+                *reinterpret_cast<float4*>(dl + 4) = make_float4(lo[4], lo[5], lo[6], lo[7]);
                 *reinterpret_cast<float4*>(dh) = make_float4(hi[0], hi[1], hi[2], hi[3]);
-                *reinterpret_cast<float4*>(dh + SR_HALF) = make_float4(hi[4], hi[5], hi[6], hi[7]);
+                *reinterpret_cast<float4*>(dh + 4) = make_float4(hi[4], hi[5], hi[6], hi[7]);
             }
         }
     };
@@ -339,18 +366,22 @@ __global__ void __launch_bounds__(SR_NT, MINB) k_analysis_strip(const __grid_con
     float* const llb = a.ll ? a.ll + (size_t)b * a.out_bstride + gc : nullptr;
     const size_t dst_off = (size_t)b * a.out_bstride + hx;
 
+#ifdef PRNU_STRIP_PROFILE
+    unsigned long long pacc[16] = {};
+    long long plast = clock64();
+#endif
     // i = -1: prologue (the 6 row-pass rows preceding block 0: input rows 2K0-6 .. 2K0-1)
 #pragma unroll 1
     for (int i = -1; i < nblk; ++i) {
         const bool pro = i < 0;
         const int K = K0 + SR_BK * i;
-        T* s = stg0 + (i & 1) * STG;
-        if (pro) {
-            manual(s, 2 * K0 - 6, 6);
-            __syncthreads();
-        } else if (tma_ok(i)) {
-            mbar_wait(&bar[i & 1], (phase >> (i & 1)) & 1);
-            phase ^= 1u << (i & 1);
+        const int sk = stg_of(i);
+        T* s = stg0 + sk * STG;
+        int r0 = 0;
+        if (tma_ok(i)) {
+            mbar_wait(&bar[sk], (phase >> sk) & 1);
+            phase ^= 1u << sk;
+            if (pro) r0 = 10;
             if (edge) {
 #pragma unroll
                 for (int k = 0; k < SR_FIX; ++k) {
@@ -361,17 +392,17 @@ __global__ void __launch_bounds__(SR_NT, MINB) k_analysis_strip(const __grid_con
                 __syncthreads();
             }
         } else {
-            manual(s, 2 * K, SR_IR);
+            manual(s, pro ? 2 * K0 - 6 : 2 * K, pro ? 6 : SR_IR);
             __syncthreads();
         }
-        rowpass(s, pro ? 6 : SR_IR);
+        SPROBE(0);
+        rowpass(s, r0, pro ? 6 : SR_IR);
         fence_proxy_async();
+        SPROBE(1);
         __syncthreads();   // B1: row buffer complete, staging buffer s consumed
+        SPROBE(2);
+        if (t == 0 && i + 3 < nblk && tma_ok(i + 3)) issue(i + 3);   // into the buffer just consumed
         if (pro) {
-            if (t == 0) {
-                if (tma_ok(0)) issue(0);
-                if (nblk > 1 && tma_ok(1)) issue(1);
-            }
 #pragma unroll
             for (int r = 0; r < 6; ++r) {
                 lo_c[r] = regA[r * SR_RBP + pos];
@@ -380,7 +411,6 @@ __global__ void __launch_bounds__(SR_NT, MINB) k_analysis_strip(const __grid_con
             __syncthreads();
             continue;
         }
-        if (t == 0 && i + 2 < nblk && tma_ok(i + 2)) issue(i + 2);
 
         // ---- column pass of this thread's column: coefficient rows K .. K+7
         float q[16][3], cc[8][3];
@@ -462,11 +492,16 @@ __global__ void __launch_bounds__(SR_NT, MINB) k_analysis_strip(const __grid_con
                     C[j * SR_CP + t] = j < 4 ? c_c[j][sb] : cc[j - 4][sb];
                 }
             };
+            SPROBE(3);
             write_vc(regB, 0);
             write_vc(regC, 2);
+            SPROBE(4);
             __syncthreads();   // B2: every thread is done reading the row buffer
+            SPROBE(5);
             write_vc(regA, 1);
+            SPROBE(6);
             __syncthreads();   // B3: V/c of all three subbands ready
+            SPROBE(7);
             if (hv && K - 4 + hj < ky1) {
 #pragma unroll 1
                 for (int sb = 0; sb < 3; ++sb) {
@@ -530,7 +565,9 @@ __global__ void __launch_bounds__(SR_NT, MINB) k_analysis_strip(const __grid_con
                 }
             }
         }
+        SPROBE(8);
         __syncthreads();   // B4: V/c buffers and the row buffer free for the next block
+        SPROBE(9);
 #pragma unroll
         for (int k = 0; k < 8; ++k)
 #pragma unroll
@@ -540,6 +577,10 @@ __global__ void __launch_bounds__(SR_NT, MINB) k_analysis_strip(const __grid_con
 #pragma unroll
             for (int s2 = 0; s2 < 3; ++s2) c_c[k][s2] = cc[4 + k][s2];
     }
+#ifdef PRNU_STRIP_PROFILE
+    if ((t & 31) == 0)
+        for (int k = 0; k < 10; ++k) atomicAdd(&g_strip_prof[k], pacc[k]);
+#endif
 }
 
 // ------------------------------------------------------------------ host
@@ -598,9 +639,9 @@ static int strip_launch(const T* in, long long in_bstride, int in_pitch, int NH,
     nseg = (nH + a.SH - 1) / a.SH;
     CUtensorMap map{};
     const size_t es = sizeof(T);
+    const CUtensorMapDataType dt = sizeof(T) == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     a.use_tma = ((in_pitch * es) % 16 == 0) && ((in_bstride * es) % 16 == 0) && ((uintptr_t)in % 16 == 0) &&
-                encode_tensor_map_3d(&map, sizeof(T) == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                                     es, in, (uint64_t)NW, (uint64_t)NH, (uint64_t)nb, (uint64_t)in_pitch * es,
+                encode_tensor_map_3d(&map, dt, es, in, (uint64_t)NW, (uint64_t)NH, (uint64_t)nb, (uint64_t)in_pitch * es,
                                      (uint64_t)in_bstride * es, StripStage<T>::BOXW, SR_IR);
     static const bool no_tma = getenv("PRNU_STRIP_NO_TMA") != nullptr;
     if (no_tma) a.use_tma = 0;
@@ -610,6 +651,23 @@ static int strip_launch(const T* in, long long in_bstride, int in_pitch, int NH,
     else
         k_analysis_strip<T, MINB, false><<<grid, SR_NT, strip_smem_bytes<T>() + smem_pad(), st>>>(map, a);
     return PRNU_OK;
+}
+
+// Debug: phase cycle counters of k_analysis_strip (all zero unless built with
+// -DPRNU_STRIP_PROFILE).  out[0..15]; reset != 0 clears them afterwards.
+extern "C" int prnu_debug_strip_profile(unsigned long long* out, int reset) {
+#ifdef PRNU_STRIP_PROFILE
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, g_strip_prof, sizeof(unsigned long long) * 16);
+    if (reset) {
+        unsigned long long z[16] = {};
+        cudaMemcpyToSymbol(g_strip_prof, z, sizeof(z));
+    }
+#else
+    for (int k = 0; k < 16; ++k) out[k] = 0;
+    (void)reset;
+#endif
+    return 0;
 }
 
 int launch_analysis_strip_u8(const uint8_t* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll,

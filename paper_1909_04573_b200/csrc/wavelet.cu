@@ -955,13 +955,15 @@ __global__ void __launch_bounds__(256, MODE == 0 ? 3 : PRNU_SYNTH_ACC_MINB) k_sy
 //     sequential fp64 sum, every partial sum being an integer < 2^53).
 // Per-pixel order is ascending frame order, as in k_synth_tma<1>.
 constexpr int SA_STAGE_COEF = 4 * SC_PS;           // floats per stage (4 planes)
-template <int TY, typename TI>
+template <int TY, typename TI, int MODE = 1>
 constexpr size_t sacc_smem_bytes() {
-    return 2 * SA_STAGE_COEF * sizeof(float) + 3 * TY * ST_X * sizeof(TI) + 2 * 2 * TY * SL_P * sizeof(float) +
-           2 * sizeof(uint64_t);
+    return 2 * SA_STAGE_COEF * sizeof(float) + (MODE ? 3 * TY * ST_X * sizeof(TI) : 0) +
+           2 * 2 * TY * SL_P * sizeof(float) + 2 * sizeof(uint64_t);
 }
 
-template <int TY, typename TI>
+// MODE 1: accumulate (frames 0 .. nb-1, one CTA per tile); MODE 0: plain inverse
+// level written to a.out (frames [z * frames_per_cta, ...) per CTA, no I tiles).
+template <int TY, typename TI, int MODE = 1>
 #ifndef PRNU_SACC_MINB
 #define PRNU_SACC_MINB 4
 #endif
@@ -974,14 +976,15 @@ __global__ void __launch_bounds__(256, PRNU_SACC_MINB) k_synth_acc2(const __grid
     // column pass), I-tile ring of 3 (frame f in f % 3, released after its row
     // pass): frame f+2 is issued at the barrier of frame f, two frames ahead.
     float* coef0 = smem;                                                      // [2][4][SC_PS]
-    TI* itile0 = reinterpret_cast<TI*>(smem + 2 * SA_STAGE_COEF);             // [3][TY][ST_X]
-    float* sL0 = reinterpret_cast<float*>(itile0 + 3 * TY * ST_X);          // [2][2][TY][SL_P]
+    TI* itile0 = reinterpret_cast<TI*>(smem + 2 * SA_STAGE_COEF);             // [3][TY][ST_X] (MODE 1)
+    float* sL0 = reinterpret_cast<float*>(itile0 + (MODE ? 3 * TY * ST_X : 0));   // [2][2][TY][SL_P]
     uint64_t* bar = reinterpret_cast<uint64_t*>(sL0 + 2 * 2 * TY * SL_P);
     const int tid = threadIdx.x;
     const int ty0 = blockIdx.y * TY, tx0 = blockIdx.x * ST_X;
     const int ky0 = ty0 >> 1, kx0 = tx0 >> 1;
-    const int nb = a.nb;
-    const uint32_t tx_bytes = (a.has_A ? 4u : 3u) * SC_BW * CY * 4u + (uint32_t)(TY * ST_X * sizeof(TI));
+    const int f0 = MODE ? 0 : blockIdx.z * a.frames_per_cta;
+    const int nb = MODE ? a.nb : min(a.nb - f0, a.frames_per_cta);   // frames of this CTA: f0 .. f0+nb-1
+    const uint32_t tx_bytes = (a.has_A ? 4u : 3u) * SC_BW * CY * 4u + (MODE ? (uint32_t)(TY * ST_X * sizeof(TI)) : 0u);
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
@@ -998,11 +1001,11 @@ __global__ void __launch_bounds__(256, PRNU_SACC_MINB) k_synth_acc2(const __grid
         const int st = f & 1;
         float* c = coef0 + st * SA_STAGE_COEF;
         mbar_arrive_expect_tx(&bar[st], tx_bytes);
-        if (a.has_A) tma_load_3d(c, &maps.A, kx0, ky0, f, &bar[st]);
-        tma_load_3d(c + 1 * SC_PS, &maps.d0, kx0, ky0, f, &bar[st]);
-        tma_load_3d(c + 2 * SC_PS, &maps.d1, kx0, ky0, f, &bar[st]);
-        tma_load_3d(c + 3 * SC_PS, &maps.d2, kx0, ky0, f, &bar[st]);
-        tma_load_3d(itile0 + (f % 3) * TY * ST_X, &imap, tx0, ty0, f, &bar[st]);
+        if (a.has_A) tma_load_3d(c, &maps.A, kx0, ky0, f0 + f, &bar[st]);
+        tma_load_3d(c + 1 * SC_PS, &maps.d0, kx0, ky0, f0 + f, &bar[st]);
+        tma_load_3d(c + 2 * SC_PS, &maps.d1, kx0, ky0, f0 + f, &bar[st]);
+        tma_load_3d(c + 3 * SC_PS, &maps.d2, kx0, ky0, f0 + f, &bar[st]);
+        if (MODE) tma_load_3d(itile0 + (f % 3) * TY * ST_X, &imap, tx0, ty0, f, &bar[st]);
     };
     if (tid == 0) {
         if (nb > 0) issue(0);
@@ -1020,11 +1023,11 @@ __global__ void __launch_bounds__(256, PRNU_SACC_MINB) k_synth_acc2(const __grid
     double den_d[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-        num[k] = (rowok && gx + k < a.NW) ? a.num[(size_t)gy * a.acc_pitch + gx + k] : 0.0;
+        num[k] = (MODE && rowok && gx + k < a.NW) ? a.num[(size_t)gy * a.acc_pitch + gx + k] : 0.0;
         den_i[k] = 0u;
         den_d[k] = 0.0;
     }
-    if (sizeof(TI) == 4) {
+    if (MODE && sizeof(TI) == 4) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) den_d[k] = (rowok && gx + k < a.NW) ? a.den[(size_t)gy * a.acc_pitch + gx + k] : 0.0;
     }
@@ -1093,6 +1096,20 @@ __global__ void __launch_bounds__(256, PRNU_SACC_MINB) k_synth_acc2(const __grid
             w[2 * q] = x.x;
             w[2 * q + 1] = x.y;
         }
+        if (MODE == 0) {   // plain inverse level: write this thread's 8 outputs
+            if (rowok) {
+                float* orow = a.out + (size_t)(f0 + f) * a.out_bstride + (size_t)gy * a.out_pitch + gx;
+                if (gx + 8 <= a.NW && ((a.out_pitch & 3) == 0)) {
+                    reinterpret_cast<float4*>(orow)[0] = make_float4(w[0], w[1], w[2], w[3]);
+                    reinterpret_cast<float4*>(orow)[1] = make_float4(w[4], w[5], w[6], w[7]);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        if (gx + k < a.NW) orow[k] = w[k];
+                }
+            }
+            continue;
+        }
         const TI* irow = itile0 + (f % 3) * TY * ST_X + rt * ST_X + 8 * rg;
         if (sizeof(TI) == 1) {
             const uint2 iv = *reinterpret_cast<const uint2*>(irow);
@@ -1116,7 +1133,7 @@ __global__ void __launch_bounds__(256, PRNU_SACC_MINB) k_synth_acc2(const __grid
             }
         }
     }
-    if (rowok) {
+    if (MODE && rowok) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             if (gx + k < a.NW) {
@@ -1394,10 +1411,24 @@ static int denoise_front(const TIn* in, long long in_bstride, int in_pitch, int 
         s.out = pb.approx[l - 1];
         s.out_bstride = (long long)pb.bstride[l - 1];
         s.out_pitch = p.pitch[l - 1];
-        const int tiles = ((s.NW + ST_X - 1) / ST_X) * ((s.NH + ST_Y - 1) / ST_Y);
-        s.frames_per_cta = std::max(1, std::min(4, tiles * nb / (148 * 6)));
-        dim3 grid((s.NW + ST_X - 1) / ST_X, (s.NH + ST_Y - 1) / ST_Y, (nb + s.frames_per_cta - 1) / s.frames_per_cta);
-        {
+        static const bool synth2 = !(getenv("PRNU_SYNTH2") && getenv("PRNU_SYNTH2")[0] == '0');
+        if (synth2) {   // v2 pipeline (2-frame-deep TMA prefetch, one barrier per frame), 32-row tiles
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(k_synth_acc2<32, float, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sacc_smem_bytes<32, float, 0>());
+                attr = true;
+            }
+            const int tiles = ((s.NW + ST_X - 1) / ST_X) * ((s.NH + 31) / 32);
+            // frames per CTA: enough CTAs for ~4 waves of 4 CTAs/SM, at least 4 frames to amortise the pipeline
+            s.frames_per_cta = std::max(4, std::min(nb, (int)((long long)tiles * nb / (148 * 4 * 4))));
+            dim3 grid((s.NW + ST_X - 1) / ST_X, (s.NH + 31) / 32, (nb + s.frames_per_cta - 1) / s.frames_per_cta);
+            KTimer kt(kSynthName[l], st);
+            k_synth_acc2<32, float, 0><<<grid, 256, sacc_smem_bytes<32, float, 0>(), st>>>(m, CUtensorMap{}, s);
+        } else {
+            const int tiles = ((s.NW + ST_X - 1) / ST_X) * ((s.NH + ST_Y - 1) / ST_Y);
+            s.frames_per_cta = std::max(1, std::min(4, tiles * nb / (148 * 6)));
+            dim3 grid((s.NW + ST_X - 1) / ST_X, (s.NH + ST_Y - 1) / ST_Y, (nb + s.frames_per_cta - 1) / s.frames_per_cta);
             KTimer kt(kSynthName[l], st);
             k_synth_tma<0, float><<<grid, 256, S_SMEM_BYTES, st>>>(m, s);
         }
