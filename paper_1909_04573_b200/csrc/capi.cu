@@ -132,7 +132,7 @@ constexpr int kMaxExtractStreams = 4;
 static int extract_streams() {
     static const int n = [] {
         const char* e = getenv("PRNU_STREAMS");
-        int v = e ? atoi(e) : 2;
+        int v = e ? atoi(e) : 3;
         return v < 1 ? 1 : (v > kMaxExtractStreams ? kMaxExtractStreams : v);
     }();
     return n;

@@ -71,7 +71,11 @@ constexpr int SR_CP = 124;                  // float pitch of coefficient rows (
 // V/c buffer of one subband: (v3, v5) plane [8][SR_P2] float2, (v7, v9) plane, c plane [8][SR_CP]
 constexpr int SR_VC_FLOATS = 2 * SR_BK * SR_P2 * 2 + SR_BK * SR_CP;
 constexpr int SR_A_FLOATS = SR_RB_FLOATS > SR_VC_FLOATS ? SR_RB_FLOATS : SR_VC_FLOATS;
-constexpr int SR_NSTG = 3;                  // staging buffers: TMA two blocks ahead
+constexpr int SR_NSTG = 3;
+#ifndef PRNU_H_UNROLL
+#define PRNU_H_UNROLL 3
+#endif
+constexpr int kStripHUnroll = PRNU_H_UNROLL;   // subband items of the H pass unrolled (A/B knob)                  // staging buffers: TMA two blocks ahead
 static_assert(8 * 16 <= SR_RBP, "row-buffer columns of the 16 row-pass groups");
 static_assert(SR_OMAX + 8 <= SR_P2 && SR_OMAX + 8 <= SR_CP, "V/c planes hold every region column");
 
@@ -284,6 +288,7 @@ __global__ void __launch_bounds__(SR_NT, MINB) k_analysis_strip(const __grid_con
         for (int i = -1; i < 2 && i < nblk; ++i)
             if (tma_ok(i)) issue(i);
     }
+    __syncthreads();   // mbarrier initialisation visible to every thread before any wait
     // Thread loads of nr rows starting at input row y0, rows and columns
     // mirrored (R-4), 16-byte chunks, all of a thread's chunks in flight first.
     const bool vec_ok = ((reinterpret_cast<uintptr_t>(in) & 15) == 0) && ((a.in_pitch * sizeof(T)) % 16 == 0);
@@ -503,7 +508,7 @@ __global__ void __launch_bounds__(SR_NT, MINB) k_analysis_strip(const __grid_con
             __syncthreads();   // B3: V/c of all three subbands ready
             SPROBE(7);
             if (hv && K - 4 + hj < ky1) {
-#pragma unroll 1
+#pragma unroll kStripHUnroll
                 for (int sb = 0; sb < 3; ++sb) {
                     // horizontal sums (sliding), Wiener factor, store: outputs 8hg .. 8hg+7 of row hj
                     const float* buf = sb == 0 ? regB : sb == 1 ? regA : regC;

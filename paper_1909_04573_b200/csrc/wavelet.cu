@@ -1398,7 +1398,7 @@ static int denoise_front(const TIn* in, long long in_bstride, int in_pitch, int 
             }
         }
         count_launch();
-        if ((rc = check_launch("k_analysis_shrink"))) return rc;
+        if ((rc = check_launch(l == 1 ? "k_analysis_strip" : "k_analysis_shrink"))) return rc;
     }
     for (int l = L; l >= 2; --l) {
         SynthMaps m;
