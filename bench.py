@@ -38,7 +38,8 @@ def parse():
     ap.add_argument("--height", type=int, default=1080)
     ap.add_argument("--width", type=int, default=1920)
     ap.add_argument("--depths", default="1,50")
-    ap.add_argument("--batch", type=int, default=64, help="SDA frames denoised per wave at depth 1")
+    ap.add_argument("--batch", type=int, default=0,
+                    help="SDA frames denoised per wave at depth 1 (0: waves of <= 256 frames, equal sizes)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
@@ -285,6 +286,9 @@ def main():
     K_true = v.K.contiguous()
     torch.cuda.synchronize()
 
+    if args.batch <= 0:   # equal waves of at most 256 frames (1800 -> 8 waves of 225)
+        nw = -(-m // 256)
+        args.batch = -(-m // nw)
     exs = {d: prnu.Extractor(H, W, d, batch=(args.batch if d == 1 else max(1, min(64, m // d))), device=dev)
            for d in depths}
     n_sda = {d: m // d for d in depths}

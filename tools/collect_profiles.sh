@@ -10,7 +10,7 @@ python tools/launch_summary.py $O/ncu_launches.csv > $O/ncu_launches_summary.txt
 gzip -f $O/ncu_launches.csv
 python tools/profile_extract.py 64 64 > /dev/null 2>&1
 timeout 1200 ncu --set full --clock-control none --import-source on \
-  -k "regex:k_analysis_strip|k_synth_acc2|k_analysis_shrink|k_synth_tma" -c 8 -f -o $O/full \
+  -k "regex:k_analysis_strip|k_synth_acc2|k_analysis_shrink|k_synth_tma|k_dwt_strip|k_shrink_hfirst" -c 9 -f -o $O/full \
   python tools/profile_extract.py 64 64 > $O/ncu_full_run.log 2>&1; echo "ncu full rc $?"
 python tools/ncu_summary.py $O/full.ncu-rep > $O/ncu_full_summary.txt
 python tools/ncu_traffic.py $O/full.ncu-rep "k_analysis_strip<unsigned char" analysis_l1_u8 64 1080 1920 \

@@ -16,10 +16,10 @@ for r in rows[1:]:
     v = float(r[vi].replace(",", ""))
     scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
     name = r[ki]
-    if "prnu::" not in name:
+    if "prnu::" not in name and "splitk::" not in name:
         other += v * scale
         continue
-    short = name.split("(")[0].replace("void ", "").replace("prnu::", "")
+    short = name.split("(")[0].replace("void ", "").replace("prnu::", "").replace("splitk::", "")
     tot[short] += v * scale
     cnt[short] += 1
 T = sum(tot.values())
