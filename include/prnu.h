@@ -86,6 +86,21 @@ int prnu_sda_average(const uint8_t* frames, int64_t m, int H, int W, int64_t dep
                      float* sda_out, int64_t* n_sda_host, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * f4  RGB -> luminance with the BT.601 weights BASELINE
+ * config 3 names ("converted to luminance (0.299/0.587/0.114)").
+ *
+ * prnu_rgb_to_luma: rgb u8, layout 0 = planar [n][3][H][W] (R, G, B planes),
+ *   layout 1 = interleaved [n][H][W][3]; luma_out [n][H][W].  With the exact
+ *   integer s = 299 R + 587 G + 114 B:
+ *     rounding 0: fp32 luma = RN_fp32(s / 1000) (correctly rounded; bit-exact);
+ *     rounding 1: u8 luma = s / 1000 rounded half to even (exact rule).
+ *   H*W must be a multiple of 4; rgb 4-byte aligned; luma_out 16-byte (fp32)
+ *   or 4-byte (u8) aligned.  Errors: INVALID_ARG, BAD_PARAMETER.
+ * ------------------------------------------------------------------------- */
+int prnu_rgb_to_luma(const uint8_t* rgb, int64_t n, int H, int W, int layout, int rounding, void* luma_out,
+                     void* stream);
+
+/* ---------------------------------------------------------------------------
  * a2-a4  Noise residual W = I - F(I) — P:83 (W_k = I_k - F(I_k))
  * (W^SDA = I^SDA - F(I^SDA)).
  *

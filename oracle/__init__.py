@@ -119,6 +119,29 @@ def sda_average(frames: np.ndarray, depth: int) -> np.ndarray:
     return out
 
 
+# ---------------------------------------------------------------- f4 luma
+def rgb_to_luma(rgb: np.ndarray, layout: str = "planar", rounding: str = "fp32") -> np.ndarray:
+    """BT.601 luma Y = 0.299 R + 0.587 G + 0.114 B (BASELINE config 3).
+
+    Plain definition: the exact integer s = 299 R + 587 G + 114 B (Y = s / 1000
+    exactly); "fp32" returns the correctly rounded fp32 of s / 1000 (an IEEE
+    fp32 division of two exactly representable operands), "u8" rounds s / 1000
+    half to even in integer arithmetic."""
+    rgb = np.asarray(rgb, dtype=np.uint8)
+    if layout == "planar":
+        r, g, b = (rgb[:, k].astype(np.int64) for k in range(3))
+    elif layout == "interleaved":
+        r, g, b = (rgb[..., k].astype(np.int64) for k in range(3))
+    else:
+        raise ValueError(layout)
+    s = 299 * r + 587 * g + 114 * b
+    if rounding == "fp32":
+        return s.astype(np.float32) / np.float32(1000.0)
+    q, rem = np.divmod(s, 1000)
+    q = q + ((rem > 500) | ((rem == 500) & (q % 2 == 1)))
+    return q.astype(np.uint8)
+
+
 # ---------------------------------------------------------------- a2-a4
 def filters():
     """(dec_lo, dec_hi, rec_lo, rec_hi), each float64[8]."""

@@ -83,6 +83,7 @@ def _sig(name, res, *args):
 _sig("prnu_default_params", _i, _P)
 _sig("prnu_sda_groups", _i, _i64, _i64, ctypes.POINTER(_i64))
 _sig("prnu_sda_average", _i, _vp, _i64, _i, _i, _i64, _vp, ctypes.POINTER(_i64), _vp)
+_sig("prnu_rgb_to_luma", _i, _vp, _i64, _i, _i, _i, _i, _vp, _vp)
 _sig("prnu_residual_workspace_bytes", _sz, _i, _i, _i, _P)
 _sig("prnu_residual", _i, _vp, _i, _i, _i, _P, _i, _vp, _vp, _sz, _vp)
 _sig("prnu_residual_u8", _i, _vp, _i, _i, _i, _P, _i, _vp, _vp, _sz, _vp)
@@ -177,6 +178,34 @@ def sda_average(frames: torch.Tensor, depth: int) -> torch.Tensor:
 
 
 prnu_sda_average = sda_average
+
+
+# ---------------------------------------------------------------- f4 luma
+def rgb_to_luma(rgb: torch.Tensor, layout: str = "planar", dtype: torch.dtype = torch.float32) -> torch.Tensor:
+    """u8 RGB -> luma [n,H,W] with the BT.601 weights (BASELINE config 3).
+
+    layout "planar": rgb [n,3,H,W]; "interleaved": rgb [n,H,W,3].  dtype float32:
+    RN_fp32((299R + 587G + 114B) / 1000); dtype uint8: the same rounded half to even."""
+    _dev(rgb, torch.uint8, "rgb", (4,))
+    if layout == "planar":
+        n, c, H, W = rgb.shape
+        lay = 0
+    elif layout == "interleaved":
+        n, H, W, c = rgb.shape
+        lay = 1
+    else:
+        raise ValueError("layout must be 'planar' or 'interleaved'")
+    if c != 3:
+        raise ValueError("rgb must have 3 channels")
+    if dtype not in (torch.float32, torch.uint8):
+        raise ValueError("dtype must be float32 or uint8")
+    out = torch.empty((n, H, W), dtype=dtype, device=rgb.device)
+    _check(_lib.prnu_rgb_to_luma(_ptr(rgb), n, H, W, lay, 0 if dtype == torch.float32 else 1, _ptr(out), _stream()),
+           "prnu_rgb_to_luma")
+    return out
+
+
+prnu_rgb_to_luma = rgb_to_luma
 
 
 # ---------------------------------------------------------------- a2-a4
@@ -449,6 +478,41 @@ def pce(R: torch.Tensor, T: torch.Tensor, exclusion_half: int = 5, aligned: bool
 
 
 prnu_pce = pce
+
+
+# ---------------------------------------------------------------- f4: H0/H1 detection rates (host logic)
+PCE_THRESHOLD = 60.0   # P:259 "PCE higher than 60" -> match; strict (R-20)
+
+
+def detection_rates(pce_matrix, threshold: float = PCE_THRESHOLD) -> dict:
+    """Camera-identification decisions from a square PCE matrix M[q, c] (query q
+    against fingerprint c; the diagonal are the H1 pairs, the rest H0): TPR =
+    share of H1 pairs with PCE > threshold, FPR = share of H0 pairs with
+    PCE > threshold (strict, R-20).  Host-side bookkeeping over device results."""
+    import numpy as np
+    M = np.asarray(pce_matrix, dtype=np.float64)
+    if M.ndim != 2 or M.shape[0] != M.shape[1]:
+        raise ValueError("pce_matrix must be square [queries, fingerprints]")
+    eye = np.eye(M.shape[0], dtype=bool)
+    h1, h0 = M[eye], M[~eye]
+    return {"tpr": float(np.mean(h1 > threshold)), "fpr": float(np.mean(h0 > threshold)) if h0.size else 0.0,
+            "n_h1": int(h1.size), "n_h0": int(h0.size)}
+
+
+def roc(pce_h1, pce_h0):
+    """ROC of the PCE detector: thresholds at every observed score (descending),
+    returns (fpr, tpr, auc) with the decision PCE > threshold; AUC by the
+    trapezoid rule from (0, 0) to (1, 1)."""
+    import numpy as np
+    h1 = np.asarray(pce_h1, dtype=np.float64).ravel()
+    h0 = np.asarray(pce_h0, dtype=np.float64).ravel()
+    if h1.size == 0 or h0.size == 0:
+        raise ValueError("need H1 and H0 scores")
+    th = np.unique(np.concatenate([h1, h0]))[::-1]
+    tpr = np.array([0.0] + [float(np.mean(h1 >= t)) for t in th])
+    fpr = np.array([0.0] + [float(np.mean(h0 >= t)) for t in th])
+    auc = float(np.sum((fpr[1:] - fpr[:-1]) * (tpr[1:] + tpr[:-1]) / 2.0))
+    return fpr, tpr, auc
 
 
 class BlockPlan:

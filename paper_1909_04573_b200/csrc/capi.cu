@@ -91,6 +91,8 @@ int validate_params(const prnu_denoise_params* p, int H, int W, ShrinkParams* sp
 
 // kernels / launchers defined in the other translation units
 int launch_sda_average(const uint8_t* frames, long long n_groups, long long P, int d, float* out, cudaStream_t st);
+int launch_rgb_to_luma(const uint8_t* rgb, long long n, long long P, int layout, int rounding, void* out,
+                       cudaStream_t st);
 size_t pyramid_floats_per_frame(const Pyramid& p);
 template <typename TIn>
 int run_residual(const TIn* in, int nb, int H, int W, const Pyramid& p, const ShrinkParams& sp, float* W_out,
@@ -231,6 +233,21 @@ int prnu_sda_average(const uint8_t* frames, int64_t m, int H, int W, int64_t dep
     if (depth > 65793) return fail(PRNU_BAD_PARAMETER, "depth > 65793 (sum would exceed 2^24)");
     if (n_sda_host) *n_sda_host = ns;
     return launch_sda_average(frames, ns, (long long)H * W, (int)depth, sda_out, as_stream(stream));
+}
+
+int prnu_rgb_to_luma(const uint8_t* rgb, int64_t n, int H, int W, int layout, int rounding, void* luma_out,
+                     void* stream) {
+    int rc;
+    if (!rgb || !luma_out) return fail(PRNU_INVALID_ARG, "null pointer");
+    if (n < 1) return fail(PRNU_INVALID_ARG, "n must be >= 1");
+    if ((rc = check_dims(H, W))) return rc;
+    if (layout != 0 && layout != 1) return fail(PRNU_BAD_PARAMETER, "layout must be 0 (planar) or 1 (interleaved)");
+    if (rounding != 0 && rounding != 1) return fail(PRNU_BAD_PARAMETER, "rounding must be 0 (fp32) or 1 (u8)");
+    const long long P = (long long)H * W;
+    if (P % 4) return fail(PRNU_BAD_PARAMETER, "H*W must be a multiple of 4");
+    if (((uintptr_t)rgb & 3) || ((uintptr_t)luma_out & (rounding ? 3 : 15)))
+        return fail(PRNU_INVALID_ARG, "rgb must be 4-byte aligned, luma_out 16-byte (fp32) / 4-byte (u8) aligned");
+    return launch_rgb_to_luma(rgb, n, P, layout, rounding, luma_out, as_stream(stream));
 }
 
 size_t prnu_residual_workspace_bytes(int batch, int H, int W, const prnu_denoise_params* p) {

@@ -108,3 +108,81 @@ int launch_sda_average(const uint8_t* frames, long long n_groups, long long P, i
 }
 
 }  // namespace prnu
+
+// ---------------------------------------------------------------- f4: RGB -> luma
+// Y = 0.299 R + 0.587 G + 0.114 B (the BT.601 weights BASELINE
+// config 3 names), from the exact integer s = 299 R + 587 G + 114 B:
+//   rounding 0: fp32 Y = RN_fp32(s / 1000)  (one IEEE divide, s < 2^24 exact)
+//   rounding 1: u8   Y = s / 1000 rounded half to even (exact integer rule).
+// layout 0: planar [n][3][H][W]; layout 1: interleaved [n][H][W][3].
+// HBM-bound: 3 bytes in, 4 (or 1) out per pixel; 4 pixels per thread-iteration.
+namespace prnu {
+
+__device__ __forceinline__ uint32_t luma_s(uint32_t r, uint32_t g, uint32_t b) { return 299u * r + 587u * g + 114u * b; }
+
+template <int LAYOUT, int ROUND>
+__global__ void __launch_bounds__(256) k_rgb_to_luma(const uint8_t* __restrict__ rgb, long long n, long long P,
+                                                     void* __restrict__ out) {
+    const long long P4 = P / 4;   // P % 4 == 0 on this path
+    const long long total = n * P4;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long f = i / P4, q = i - f * P4;
+        uint32_t r[4], g[4], b[4];
+        if (LAYOUT == 0) {
+            const uint8_t* base = rgb + (size_t)f * 3 * P + 4 * q;
+            const uint32_t wr = __ldg(reinterpret_cast<const uint32_t*>(base));
+            const uint32_t wg = __ldg(reinterpret_cast<const uint32_t*>(base + P));
+            const uint32_t wb = __ldg(reinterpret_cast<const uint32_t*>(base + 2 * P));
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                r[k] = (wr >> (8 * k)) & 0xffu;
+                g[k] = (wg >> (8 * k)) & 0xffu;
+                b[k] = (wb >> (8 * k)) & 0xffu;
+            }
+        } else {
+            const uint32_t* base = reinterpret_cast<const uint32_t*>(rgb + ((size_t)f * P + 4 * q) * 3);
+            const uint32_t w0 = __ldg(base), w1 = __ldg(base + 1), w2 = __ldg(base + 2);
+            const uint32_t by[12] = {w0 & 0xffu, (w0 >> 8) & 0xffu, (w0 >> 16) & 0xffu, w0 >> 24,
+                                     w1 & 0xffu, (w1 >> 8) & 0xffu, (w1 >> 16) & 0xffu, w1 >> 24,
+                                     w2 & 0xffu, (w2 >> 8) & 0xffu, (w2 >> 16) & 0xffu, w2 >> 24};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                r[k] = by[3 * k];
+                g[k] = by[3 * k + 1];
+                b[k] = by[3 * k + 2];
+            }
+        }
+        if (ROUND == 0) {
+            float y[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) y[k] = __fdiv_rn((float)luma_s(r[k], g[k], b[k]), 1000.0f);
+            reinterpret_cast<float4*>(out)[i] = make_float4(y[0], y[1], y[2], y[3]);
+        } else {
+            uint32_t w = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t s = luma_s(r[k], g[k], b[k]);
+                uint32_t qv = s / 1000u;
+                const uint32_t rem = s - 1000u * qv;
+                if (rem > 500u || (rem == 500u && (qv & 1u))) ++qv;   // half to even
+                w |= qv << (8 * k);
+            }
+            reinterpret_cast<uint32_t*>(out)[i] = w;
+        }
+    }
+}
+
+int launch_rgb_to_luma(const uint8_t* rgb, long long n, long long P, int layout, int rounding, void* out,
+                       cudaStream_t st) {
+    const long long total = n * (P / 4);
+    const int blocks = (int)std::max(1LL, std::min((total + 255) / 256, 148LL * 16));
+    if (layout == 0 && rounding == 0) k_rgb_to_luma<0, 0><<<blocks, 256, 0, st>>>(rgb, n, P, out);
+    else if (layout == 0) k_rgb_to_luma<0, 1><<<blocks, 256, 0, st>>>(rgb, n, P, out);
+    else if (rounding == 0) k_rgb_to_luma<1, 0><<<blocks, 256, 0, st>>>(rgb, n, P, out);
+    else k_rgb_to_luma<1, 1><<<blocks, 256, 0, st>>>(rgb, n, P, out);
+    count_launch();
+    return check_launch("k_rgb_to_luma");
+}
+
+}  // namespace prnu

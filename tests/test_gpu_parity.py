@@ -266,6 +266,10 @@ def test_camera_identification_small(prnu):
             assert abs(M[q, c] - ref) <= PCE_RTOL * abs(ref) + 1e-6
     assert np.all(np.diag(M) > 60)
     assert np.all(M[~np.eye(n, dtype=bool)] < 60)
+    # f4 H0/H1 harness on the same matrix: perfect separation at the paper's threshold
+    rates = prnu.detection_rates(M)
+    assert rates["tpr"] == 1.0 and rates["fpr"] == 0.0 and rates["n_h0"] == n * (n - 1)
+    assert prnu.roc(np.diag(M), M[~np.eye(n, dtype=bool)])[2] == 1.0
 
 
 def test_launch_counter_advances(prnu):
@@ -350,3 +354,25 @@ def test_multi_depth_one_upload_matches_device(prnu):
         ref = prnu.extract_fingerprint(v.frames.cuda(), d, batch=16)
         assert torch.equal(K[i], ref.K.cpu()), d
         assert torch.equal(mx.sums[i, 1], ref.sum_I2)
+
+
+# ---------------------------------------------------------------- f4 luma
+@pytest.mark.gpu
+@pytest.mark.parametrize("layout", ["planar", "interleaved"])
+@pytest.mark.parametrize("n,H,W", [(1, 4, 4), (3, 37, 52), (2, 270, 480)])
+def test_rgb_to_luma_bit_exact(prnu, layout, n, H, W):
+    g = torch.Generator().manual_seed(11 + H)
+    shape = (n, 3, H, W) if layout == "planar" else (n, H, W, 3)
+    rgb = torch.randint(0, 256, shape, generator=g, dtype=torch.uint8)
+    rgb[0].view(-1)[:8] = 255
+    rgb[-1].view(-1)[-8:] = 0
+    for dt, rnd in ((torch.float32, "fp32"), (torch.uint8, "u8")):
+        y = prnu.rgb_to_luma(rgb.cuda(), layout, dt).cpu().numpy()
+        ref = oracle.rgb_to_luma(rgb.numpy(), layout, rnd)
+        assert y.dtype == ref.dtype and np.array_equal(y.view(np.uint8), ref.view(np.uint8))
+
+
+@pytest.mark.gpu
+def test_rgb_to_luma_errors(prnu):
+    with pytest.raises(prnu.PrnuError):
+        prnu.rgb_to_luma(torch.zeros((1, 3, 3, 3), dtype=torch.uint8, device="cuda"))   # H*W not a multiple of 4

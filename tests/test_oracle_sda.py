@@ -105,3 +105,39 @@ def test_averaging_noise_law(d):
         v = oracle.sda_average(fr, d)[0].astype(np.float64).var()
         ratios.append(v / ((sigma ** 2 + 1.0 / 12.0) / d))
     assert abs(np.mean(ratios) - 1.0) < 0.2
+
+
+# ---------------------------------------------------------------- f4: RGB -> luma
+def test_luma_gray_is_identity():
+    v = np.arange(256, dtype=np.uint8)
+    rgb = np.stack([v, v, v])[None, :, None, :]          # planar [1,3,1,256]
+    assert np.array_equal(oracle.rgb_to_luma(rgb, "planar", "fp32")[0, 0], v.astype(np.float32))
+    assert np.array_equal(oracle.rgb_to_luma(rgb, "planar", "u8")[0, 0], v)
+
+
+def test_luma_matches_fp64_formula_and_layouts():
+    rng = np.random.default_rng(5)
+    rgb = rng.integers(0, 256, size=(3, 3, 7, 9), dtype=np.uint8)
+    y64 = 0.299 * rgb[:, 0].astype(np.float64) + 0.587 * rgb[:, 1] + 0.114 * rgb[:, 2]
+    y = oracle.rgb_to_luma(rgb, "planar", "fp32")
+    assert np.max(np.abs(y - y64)) <= 2 ** -24 * 256        # within fp32 rounding of the exact value
+    inter = np.ascontiguousarray(np.moveaxis(rgb, 1, -1))
+    assert np.array_equal(oracle.rgb_to_luma(inter, "interleaved", "fp32"), y)
+    u = oracle.rgb_to_luma(rgb, "planar", "u8").astype(np.float64)
+    assert np.max(np.abs(u - y64)) <= 0.5 + 1e-9
+
+
+def test_luma_ties_round_half_to_even():
+    # s = 299 R + 587 G + 114 B with s mod 1000 == 500 exactly
+    ties = []
+    for r in range(256):
+        for g in range(0, 256, 5):
+            for b in range(0, 256, 7):
+                s = 299 * r + 587 * g + 114 * b
+                if s % 1000 == 500:
+                    ties.append((r, g, b, s // 1000))
+    assert len(ties) > 10
+    rgb = np.array([[t[0] for t in ties], [t[1] for t in ties], [t[2] for t in ties]], dtype=np.uint8)
+    out = oracle.rgb_to_luma(rgb[None, :, None, :], "planar", "u8")[0, 0]
+    expect = np.array([q + (q % 2) for (_, _, _, q) in ties], dtype=np.uint8)   # half to even
+    assert np.array_equal(out, expect)
