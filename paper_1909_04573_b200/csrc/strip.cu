@@ -55,7 +55,6 @@ __device__ unsigned long long g_strip_prof[16];
 
 constexpr int SR_NT = 128;                  // threads per CTA == region columns
 constexpr int SR_RW = 128;                  // region width (O + 8 <= 128)
-constexpr int SR_OMAX = 112;                // max output columns per strip (O + 8 <= SR_P2: the V planes hold ncols columns)
 constexpr int SR_BK = 8;                    // coefficient rows per block
 constexpr int SR_IR = 2 * SR_BK;            // input rows per block
 // Filter tap pairs (H_[i], G_[i]) and window scales in constant memory: FFMA2 /
@@ -66,18 +65,39 @@ __constant__ float2 c_st_ws[2] = {{1.0f / 9.0f, 1.0f / 25.0f}, {1.0f / 49.0f, 1.
 
 constexpr int SR_RBP = 132;                 // row-buffer pitch (== 4 mod 32: conflict-free STS.128, lanes over rows)
 constexpr int SR_RB_FLOATS = 2 * SR_IR * SR_RBP;
-constexpr int SR_P2 = 121;                  // float2 pitch of the vertical-sum planes (== 1 mod 8: conflict-free LDS.64)
-constexpr int SR_CP = 124;                  // float pitch of coefficient rows (496 B == 112 mod 128)
-// V/c buffer of one subband: (v3, v5) plane [8][SR_P2] float2, (v7, v9) plane, c plane [8][SR_CP]
-constexpr int SR_VC_FLOATS = 2 * SR_BK * SR_P2 * 2 + SR_BK * SR_CP;
-constexpr int SR_A_FLOATS = SR_RB_FLOATS > SR_VC_FLOATS ? SR_RB_FLOATS : SR_VC_FLOATS;
-constexpr int SR_NSTG = 3;
+// Per input type: strip width, V/c plane pitches, staging buffers.  u8: 3 staging
+// buffers (TMA two blocks ahead), 112 output columns; fp32 (levels >= 2, SDA
+// frames): a single staging buffer and 104 output columns, so that both variants
+// fit 3 CTAs/SM (<= 75 KB shared memory).
+template <typename T>
+struct StripCfg;
+template <>
+struct StripCfg<uint8_t> {
+    static constexpr int OMAX = 112;   // max output columns per strip
+    static constexpr int P2 = 121;     // float2 pitch of the vertical-sum planes (== 1 mod 8: conflict-free LDS.64)
+    static constexpr int CP = 124;     // float pitch of the coefficient planes (== 28 mod 32: conflict-free LDS.128)
+    static constexpr int NSTG = 3;
+};
+template <>
+struct StripCfg<float> {
+    static constexpr int OMAX = 104;
+    static constexpr int P2 = 113;
+    static constexpr int CP = 116;     // == 20 mod 32
+    static constexpr int NSTG = 1;
+};
+// V/c buffer of one subband: (v3, v5) plane [8][P2] float2, (v7, v9) plane, c plane [8][CP]
+template <typename T>
+__host__ __device__ constexpr int sr_vc_floats() { return 2 * SR_BK * StripCfg<T>::P2 * 2 + SR_BK * StripCfg<T>::CP; }
+template <typename T>
+__host__ __device__ constexpr int sr_a_floats() { return SR_RB_FLOATS > sr_vc_floats<T>() ? SR_RB_FLOATS : sr_vc_floats<T>(); }
+static_assert(StripCfg<uint8_t>::OMAX + 8 <= StripCfg<uint8_t>::P2 && StripCfg<uint8_t>::OMAX + 8 <= StripCfg<uint8_t>::CP &&
+                  StripCfg<float>::OMAX + 8 <= StripCfg<float>::P2 && StripCfg<float>::OMAX + 8 <= StripCfg<float>::CP,
+              "V/c planes hold every region column");
 #ifndef PRNU_H_UNROLL
 #define PRNU_H_UNROLL 3
 #endif
 constexpr int kStripHUnroll = PRNU_H_UNROLL;   // subband items of the H pass unrolled (A/B knob)                  // staging buffers: TMA two blocks ahead
 static_assert(8 * 16 <= SR_RBP, "row-buffer columns of the 16 row-pass groups");
-static_assert(SR_OMAX + 8 <= SR_P2 && SR_OMAX + 8 <= SR_CP, "V/c planes hold every region column");
 
 // Staging: two TMA boxes per block, box 0 = logical columns [0, BOXW), box 1 =
 // [128, 128 + BOXW), each [16 rows][BOXW] dense.  A row-pass group g reads
@@ -102,7 +122,8 @@ __host__ __device__ constexpr int strip_stage_elems() { return 2 * SR_IR * Strip
 
 template <typename T>
 constexpr size_t strip_smem_bytes() {
-    return SR_NSTG * strip_stage_elems<T>() * sizeof(T) + sizeof(float) * (SR_A_FLOATS + 2 * SR_VC_FLOATS) + 32;
+    return StripCfg<T>::NSTG * strip_stage_elems<T>() * sizeof(T) + sizeof(float) * (sr_a_floats<T>() + 2 * sr_vc_floats<T>()) +
+           32;
 }
 
 struct StripArgs {
@@ -202,6 +223,8 @@ __global__ void __launch_bounds__(SR_NT, MINB) k_analysis_strip(const __grid_con
     constexpr int BW = StripStage<T>::BOXW;
     constexpr int LOGW = StripStage<T>::LOGW;
     constexpr int STG = strip_stage_elems<T>();
+    constexpr int SR_NSTG = StripCfg<T>::NSTG, SR_P2 = StripCfg<T>::P2, SR_CP = StripCfg<T>::CP;
+    constexpr int SR_VC_FLOATS = sr_vc_floats<T>(), SR_A_FLOATS = sr_a_floats<T>();
     extern __shared__ __align__(128) unsigned char smem[];
     T* stg0 = reinterpret_cast<T*>(smem);
     float* regA = reinterpret_cast<float*>(smem + SR_NSTG * STG * sizeof(T));   // row buffer, later V/c buffer A
@@ -285,7 +308,7 @@ __global__ void __launch_bounds__(SR_NT, MINB) k_analysis_strip(const __grid_con
         tma_load_3d(s + SR_IR * BW, &map, xs + 128, y, b, &bar[k]);
     };
     if (t == 0) {   // prologue and blocks 0, 1 in flight before anything else
-        for (int i = -1; i < 2 && i < nblk; ++i)
+        for (int i = -1; i < SR_NSTG - 1 && i < nblk; ++i)
             if (tma_ok(i)) issue(i);
     }
     __syncthreads();   // mbarrier initialisation visible to every thread before any wait
@@ -406,7 +429,7 @@ __global__ void __launch_bounds__(SR_NT, MINB) k_analysis_strip(const __grid_con
         SPROBE(1);
         __syncthreads();   // B1: row buffer complete, staging buffer s consumed
         SPROBE(2);
-        if (t == 0 && i + 3 < nblk && tma_ok(i + 3)) issue(i + 3);   // into the buffer just consumed
+        if (t == 0 && i + SR_NSTG < nblk && tma_ok(i + SR_NSTG)) issue(i + SR_NSTG);   // into the buffer just consumed
         if (pro) {
 #pragma unroll
             for (int r = 0; r < 6; ++r) {
@@ -635,7 +658,7 @@ static int strip_launch(const T* in, long long in_bstride, int in_pitch, int NH,
     a.nH = nH;
     a.nW = nW;
     a.sp = sp;
-    const int S0 = (nW + SR_OMAX - 1) / SR_OMAX;
+    const int S0 = (nW + StripCfg<T>::OMAX - 1) / StripCfg<T>::OMAX;
     a.O = (int)align_up((size_t)((nW + S0 - 1) / S0), 8);
     const int S = (nW + a.O - 1) / a.O;
     static const int sh_env = getenv("PRNU_STRIP_SH") ? atoi(getenv("PRNU_STRIP_SH")) : 0;

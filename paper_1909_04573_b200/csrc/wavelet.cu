@@ -1273,9 +1273,11 @@ static bool use_strip() {
     return on;
 }
 
-// Split analysis (split.cu: streaming DWT + streaming shrink) unless PRNU_SPLIT=0.
+// Split analysis (split.cu: streaming DWT + streaming shrink) when PRNU_SPLIT=1:
+// measured slower than the fused strip kernel at levels 1-3 once the fp32 strip
+// variant fits 3 CTAs/SM (level 2: 3.65 vs 3.90 ms/step, profiles/r01).
 static bool use_split() {
-    static const bool on = !(getenv("PRNU_SPLIT") && getenv("PRNU_SPLIT")[0] == '0');
+    static const bool on = getenv("PRNU_SPLIT") && getenv("PRNU_SPLIT")[0] == '1';
     return on;
 }
 // First level analysed by the split kernels (PRNU_SPLIT_MINL, default 2): level 1
@@ -1294,11 +1296,11 @@ static const char* kDwtName[kMaxLevels + 1] = {"", "dwt_l1", "dwt_l2", "dwt_l3",
 static const char* kShrinkName[kMaxLevels + 1] = {"", "shrink_l1", "shrink_l2", "shrink_l3",
                                                   "shrink_l4", "shrink_l5", "shrink_l6"};
 
-// Deepest level analysed by the strip kernel (PRNU_STRIP_MAXL, default 1): the
-// coarser levels have too few strips x segments to fill the GPU with the
-// strip kernel's sequential blocks; the tile kernel is faster there (measured).
+// Deepest level analysed by the strip kernel (PRNU_STRIP_MAXL, default 3): the
+// level-4 planes are too small to fill the GPU with the strip kernel's
+// sequential blocks; the tile kernel is faster there (0.51 vs 0.86 ms/step).
 static int strip_max_level() {
-    static const int l = getenv("PRNU_STRIP_MAXL") ? atoi(getenv("PRNU_STRIP_MAXL")) : 1;
+    static const int l = getenv("PRNU_STRIP_MAXL") ? atoi(getenv("PRNU_STRIP_MAXL")) : 3;
     return l;
 }
 
