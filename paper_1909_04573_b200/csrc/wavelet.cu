@@ -1503,7 +1503,8 @@ int run_residual_accumulate(const TIn* in, const TIn* I, int nb, int H, int W, c
         const long n = (long)((W + ST_X - 1) / ST_X) * ((H + ty - 1) / ty);
         return (double)((n + slots - 1) / slots) * ty / ((double)n * ty / slots);   // waves rounded up / exact
     };
-    const int TYsel = waste(28) < waste(32) - 1e-9 ? 28 : 32;
+    static const int ty_env = getenv("PRNU_SACC_TY") ? atoi(getenv("PRNU_SACC_TY")) : 0;
+    const int TYsel = ty_env == 28 || ty_env == 32 ? ty_env : (waste(28) < waste(32) - 1e-9 ? 28 : 32);
     CUtensorMap imap;
     SynthMaps m2;
     const size_t es = sizeof(TIn);
