@@ -669,7 +669,10 @@ static int strip_launch(const T* in, long long in_bstride, int in_pitch, int NH,
     a.O = (int)align_up((size_t)((nW + S0 - 1) / S0), 8);
     const int S = (nW + a.O - 1) / a.O;
     static const int sh_env = getenv("PRNU_STRIP_SH") ? atoi(getenv("PRNU_STRIP_SH")) : 0;
-    int nseg = (nH + 127) / 128;
+    // segments of ~184 rows (prologue overhead ~4%), more of them while the grid
+    // holds fewer than 6 waves of 3 CTAs/SM (small planes; measured, profiles/r01)
+    int nseg = (nH + 183) / 184;
+    while ((long long)S * nseg * nb < 6LL * 148 * MINB && (nH + nseg) / (nseg + 1) >= 32) ++nseg;
     a.SH = sh_env > 0 ? (int)align_up((size_t)sh_env, 8) : (int)align_up((size_t)((nH + nseg - 1) / nseg), 8);
     nseg = (nH + a.SH - 1) / a.SH;
     CUtensorMap map{};
