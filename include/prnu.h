@@ -234,6 +234,21 @@ int prnu_pce(void* plan, const float* residual, const float* template_, int batc
 int prnu_pce_plan_destroy(void* plan);
 
 /* ---------------------------------------------------------------------------
+ * f2  Wiener filtering of fingerprints in the DFT domain —
+ * S:151 (an off-by-default option the paper does not specify; reading R-23).
+ * For each zero-mean K [batch][H][W]:  F = DFT2(K), A = |F|/sqrt(HW),
+ * s2 = mean(K^2), m = min over windows {3,5,7,9} of the mirror-extended box mean
+ * of A^2 (R-7), K_out = IDFT2(F * s2 / max(m, s2)).  cuFFT R2C/C2R in fp32.
+ * prnu_wdft_plan_create: cuFFT plans (no auto-allocation), *ws_bytes = the
+ *   workspace prnu_wdft needs; freed by prnu_wdft_plan_destroy.
+ * prnu_wdft: K and K_out device [batch][H][W] (K_out may alias K).  Errors:
+ *   INVALID_ARG, PLANE_TOO_SMALL (H or W < 4), WORKSPACE_TOO_SMALL, CUDA_ERROR.
+ * ------------------------------------------------------------------------- */
+int prnu_wdft_plan_create(int H, int W, int batch, size_t* ws_bytes, void** plan);
+int prnu_wdft(void* plan, const float* K, float* K_out, void* ws, size_t ws_bytes, void* stream);
+int prnu_wdft_plan_destroy(void* plan);
+
+/* ---------------------------------------------------------------------------
  * f1  Block-wise matching — P:266 ("divided each full resolution fingerprint
  * into 500x500 disjoint blocks"), P:321, S:275-278 (BlockGrid).
  * The H x W frame is cut into disjoint block x block tiles in row-major order

@@ -301,4 +301,4 @@ def extract_fingerprint(frames, depth: int, sigma0_sq: float = DEFAULT_SIGMA0_SQ
     return K, num, den, sda_groups(m, depth)
 
 
-from .match import ncc, pce, correlation_surface, pce_template, block_grid, blockwise_match  # noqa: E402,F401
+from .match import ncc, pce, correlation_surface, pce_template, block_grid, blockwise_match, wiener_dft  # noqa: E402,F401

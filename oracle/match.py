@@ -102,3 +102,28 @@ def blockwise_match(R, T, block: int = 500, exclusion_half: int = 5):
         p, _, _ = pce(r, t, exclusion_half, aligned=True)
         out.append((y, x, h, w, p, ncc(r, t)))
     return out
+
+
+def wiener_dft(K, windows=(3, 5, 7, 9)):
+    """f2 (S:151 option; reading R-23): Wiener filtering of a zero-mean fingerprint
+    in the DFT domain, written out step by step:
+      F = DFT2(K); A = |F| / sqrt(HW); s2 = mean(K^2);
+      m = min over w of the w x w box mean of A^2 with mirror (half-sample
+          symmetric) extension (the denoiser's window rule, R-7);
+      K' = real(IDFT2(F * s2 / max(m, s2)))
+    (the mirror windows make the gain not exactly symmetric under k -> -k; the
+    real part keeps its Hermitian part, as any real-to-real implementation must).
+    numpy's FFT and scipy's mirror box mean ('reflect', pinned equal to the e_N
+    windows in tests) are library primitives."""
+    from scipy.ndimage import uniform_filter
+    K = np.asarray(K, dtype=np.float64)
+    H, W = K.shape
+    F = np.fft.fft2(K)
+    A2 = (np.abs(F) ** 2) / (H * W)
+    s2 = float(np.mean(K * K))
+    if s2 == 0.0:
+        return np.zeros_like(K)
+    m = np.full(K.shape, np.inf)
+    for w in windows:
+        m = np.minimum(m, uniform_filter(A2, size=w, mode="reflect"))
+    return np.real(np.fft.ifft2(F * (s2 / np.maximum(m, s2))))

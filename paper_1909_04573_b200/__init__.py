@@ -107,6 +107,9 @@ _sig("prnu_pce_template", _i, _vp, _i, _vp, _i, _i, _i, _vp, _vp)
 _sig("prnu_pce_plan_create", _i, _i, _i, _i, ctypes.POINTER(_sz), ctypes.POINTER(_vp))
 _sig("prnu_pce", _i, _vp, _vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _sz, _vp)
 _sig("prnu_pce_plan_destroy", _i, _vp)
+_sig("prnu_wdft_plan_create", _i, _i, _i, _i, ctypes.POINTER(_sz), ctypes.POINTER(_vp))
+_sig("prnu_wdft", _i, _vp, _vp, _vp, _vp, _sz, _vp)
+_sig("prnu_wdft_plan_destroy", _i, _vp)
 _sig("prnu_block_plan_create", _i, _i, _i, _i, ctypes.POINTER(_i), ctypes.POINTER(_sz), ctypes.POINTER(_vp))
 _sig("prnu_block_match", _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _sz, _vp)
 _sig("prnu_block_plan_destroy", _i, _vp)
@@ -470,6 +473,46 @@ class PcePlan:
         if h is not None and h.value:
             _lib.prnu_pce_plan_destroy(h)
             self._h = None
+
+
+class WdftPlan:
+    """f2: Wiener filtering of [batch][H][W] zero-mean fingerprints in the DFT domain
+    (S:151 option; R-23): K' = IDFT2(F * s2 / max(m, s2)) with F = DFT2(K),
+    s2 = mean(K^2), m = min over windows 3..9 of the box mean of |F|^2 / (HW)."""
+
+    def __init__(self, H: int, W: int, batch: int = 1, device="cuda"):
+        self.H, self.W, self.batch = H, W, batch
+        nb = _sz()
+        h = _vp()
+        _check(_lib.prnu_wdft_plan_create(H, W, batch, ctypes.byref(nb), ctypes.byref(h)), "prnu_wdft_plan_create")
+        self._h = h
+        self.nbytes = int(nb.value)
+        self.ws = _ws(self.nbytes, device)
+
+    def __call__(self, K: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        squeeze = K.dim() == 2
+        if squeeze:
+            K = K.unsqueeze(0)
+        _dev(K, torch.float32, "K", (3,))
+        if K.shape != (self.batch, self.H, self.W):
+            raise ValueError("dimension mismatch with the plan")
+        out = torch.empty_like(K) if out is None else out
+        _check(_lib.prnu_wdft(self._h, _ptr(K), _ptr(out), _ptr(self.ws), self.nbytes, _stream()), "prnu_wdft")
+        return out[0] if squeeze else out
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.prnu_wdft_plan_destroy(h)
+            self._h = None
+
+
+def wdft(K: torch.Tensor) -> torch.Tensor:
+    b = 1 if K.dim() == 2 else K.shape[0]
+    return WdftPlan(K.shape[-2], K.shape[-1], b, K.device)(K)
+
+
+prnu_wdft = wdft
 
 
 def pce(R: torch.Tensor, T: torch.Tensor, exclusion_half: int = 5, aligned: bool = False) -> PceResult:

@@ -112,6 +112,10 @@ int launch_ncc(const float* a, const float* b, int batch, long long P, double* o
 int launch_pce_template(const float* K, int k_batch, const uint8_t* Iq, int batch, long long P, float* T,
                         cudaStream_t st);
 int pce_plan_create(int H, int W, int batch, size_t* ws_bytes, void** out);
+int wdft_plan_create(int H, int W, int batch, size_t* ws_bytes, void** out);
+int wdft_plan_destroy(void* plan);
+int wdft_plan_dims(void* plan, int* H, int* W, int* batch, size_t* ws_bytes);
+int run_wdft(void* plan, const float* K, float* K_out, void* ws, cudaStream_t st);
 int pce_plan_destroy(void* plan);
 int pce_plan_dims(void* plan, int* H, int* W, int* batch, size_t* ws_bytes);
 int run_pce(void* plan, const float* R, const float* T, int excl, int aligned, double* pce, int* py, int* px,
@@ -622,6 +626,26 @@ int prnu_pce(void* plan, const float* residual, const float* template_, int batc
 }
 
 int prnu_pce_plan_destroy(void* plan) { return pce_plan_destroy(plan); }
+
+int prnu_wdft_plan_create(int H, int W, int batch, size_t* ws_bytes, void** plan) {
+    int rc;
+    if (!ws_bytes || !plan) return fail(PRNU_INVALID_ARG, "null pointer");
+    if ((rc = check_dims(H, W))) return rc;
+    if (batch < 1) return fail(PRNU_INVALID_ARG, "batch must be >= 1");
+    if (H < 4 || W < 4) return fail(PRNU_PLANE_TOO_SMALL, "WDFT needs H, W >= 4");
+    return wdft_plan_create(H, W, batch, ws_bytes, plan);
+}
+
+int prnu_wdft(void* plan, const float* K, float* K_out, void* ws, size_t ws_bytes, void* stream) {
+    if (!plan || !K || !K_out || !ws) return fail(PRNU_INVALID_ARG, "null pointer");
+    int H, W, b;
+    size_t need;
+    wdft_plan_dims(plan, &H, &W, &b, &need);
+    if (ws_bytes < need) return fail(PRNU_WORKSPACE_TOO_SMALL, "workspace too small");
+    return run_wdft(plan, K, K_out, ws, as_stream(stream));
+}
+
+int prnu_wdft_plan_destroy(void* plan) { return wdft_plan_destroy(plan); }
 
 int prnu_block_plan_create(int H, int W, int block, int* n_tiles_host, size_t* ws_bytes, void** plan) {
     int rc;

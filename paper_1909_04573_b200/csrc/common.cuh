@@ -133,7 +133,7 @@ int launch_dwt_strip_f32(const float* in, long long in_bstride, int in_pitch, in
                          float* c1, float* c2, long long out_bstride, int out_pitch, int nH, int nW, int nb,
                          cudaStream_t st);
 int launch_shrink_strip(const float* const src[3], float* const dst[3], long long bstride, int pitch, int nH, int nW,
-                        const ShrinkParams& sp, int nb, cudaStream_t st);
+                        const ShrinkParams& sp, int nb, cudaStream_t st, int nsub = 3, const float* s0_dev = nullptr);
 
 // strip.cu: column-streaming analysis + shrink of one level (see strip.cu)
 int launch_analysis_strip_u8(const uint8_t* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll,

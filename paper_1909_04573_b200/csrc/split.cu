@@ -358,6 +358,8 @@ struct ShrinkArgs {
     ShrinkParams sp;
     int O;                 // output columns per strip (multiple of 8, <= SO_MAX)
     int SH;                // output rows per segment (multiple of BK)
+    int nsub;              // planes per frame (3 detail subbands; 1 for the WDFT magnitude)
+    const float* s0_dev;   // per-frame sigma0^2 on the device (nullable: sp.sigma0_sq)
 };
 
 template <bool ALL4>
@@ -368,7 +370,7 @@ __global__ void __launch_bounds__(NT, 5) k_shrink_strip(ShrinkArgs a) {
     float* const C = vc + 4 * BK * P2;
 
     const int t = threadIdx.x;
-    const int sb = blockIdx.z % 3, b = blockIdx.z / 3;
+    const int sb = blockIdx.z % a.nsub, b = blockIdx.z / a.nsub;
     const int cx0 = blockIdx.x * a.O;
     const int ky0 = blockIdx.y * a.SH;
     const int ky1 = min(ky0 + a.SH, a.nH);
@@ -384,7 +386,7 @@ __global__ void __launch_bounds__(NT, 5) k_shrink_strip(ShrinkArgs a) {
     const bool hv = t < a.O && hx < a.nW;
     const bool hfull = hx + 8 <= a.nW;
     float* const dst = (sb == 0 ? a.dst[0] : sb == 1 ? a.dst[1] : a.dst[2]) + (size_t)b * a.bstride + hx;
-    const float s0 = a.sp.sigma0_sq;
+    const float s0 = a.s0_dev ? a.s0_dev[b] : a.sp.sigma0_sq;
     const int wm = a.sp.wmask;
 
     // prefetch: the coefficients of the next two blocks in flight (rows mirrored, R-4;
@@ -529,7 +531,7 @@ template <bool ALL4>
 __global__ void __launch_bounds__(NT, 4) k_shrink_hfirst(ShrinkArgs a) {
     __shared__ __align__(16) float qb[2][BK][QP];
     const int t = threadIdx.x;
-    const int sb = blockIdx.z % 3, b = blockIdx.z / 3;
+    const int sb = blockIdx.z % a.nsub, b = blockIdx.z / a.nsub;
     const int cx0 = blockIdx.x * a.O;
     const int ky0 = blockIdx.y * a.SH;
     const int ky1 = min(ky0 + a.SH, a.nH);
@@ -541,7 +543,7 @@ __global__ void __launch_bounds__(NT, 4) k_shrink_hfirst(ShrinkArgs a) {
     const int nblk = 1 + (ky1 - ky0 + BK - 1) / BK;   // block 0 = prologue (rows ky0-4 .. ky0+3)
     const int K0 = ky0 - 4;
     const bool outc = t >= 4 && t < 4 + a.O && gc < nW;   // this thread's column is an output column
-    const float s0 = a.sp.sigma0_sq;
+    const float s0 = a.s0_dev ? a.s0_dev[b] : a.sp.sigma0_sq;
     const int wm = a.sp.wmask;
 
     float pf[BK], pf2[BK];
@@ -713,13 +715,15 @@ int launch_dwt_strip_f32(const float* in, long long in_bstride, int in_pitch, in
 }
 
 int launch_shrink_strip(const float* const src[3], float* const dst[3], long long bstride, int pitch, int nH, int nW,
-                        const ShrinkParams& sp, int nb, cudaStream_t st) {
+                        const ShrinkParams& sp, int nb, cudaStream_t st, int nsub, const float* s0_dev) {
     using namespace splitk;
     ShrinkArgs a{};
     for (int s = 0; s < 3; ++s) {
         a.src[s] = src[s];
         a.dst[s] = dst[s];
     }
+    a.nsub = nsub;
+    a.s0_dev = s0_dev;
     a.bstride = bstride;
     a.pitch = pitch;
     a.nH = nH;
@@ -730,9 +734,9 @@ int launch_shrink_strip(const float* const src[3], float* const dst[3], long lon
     a.O = (int)align_up((size_t)((nW + S0 - 1) / S0), 8);
     const int S = (nW + a.O - 1) / a.O;
     static const int sh_env = getenv("PRNU_SHRINK_SH") ? atoi(getenv("PRNU_SHRINK_SH")) : 0;
-    a.SH = sh_env > 0 ? (int)align_up((size_t)sh_env, BK) : seg_rows(nH, 136, BK, 3LL * S * nb, 2LL * 148 * 5);
+    a.SH = sh_env > 0 ? (int)align_up((size_t)sh_env, BK) : seg_rows(nH, 136, BK, (long long)nsub * S * nb, 2LL * 148 * 5);
     const int nseg = (nH + a.SH - 1) / a.SH;
-    dim3 grid(S, nseg, 3 * nb);
+    dim3 grid(S, nseg, nsub * nb);
     static const bool vfirst = getenv("PRNU_SHRINK_VFIRST") != nullptr;   // A/B: vertical-sums-first variant
     if (vfirst) {
         if (sp.wmask == 15) k_shrink_strip<true><<<grid, NT, 0, st>>>(a);

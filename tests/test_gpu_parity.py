@@ -376,3 +376,34 @@ def test_rgb_to_luma_bit_exact(prnu, layout, n, H, W):
 def test_rgb_to_luma_errors(prnu):
     with pytest.raises(prnu.PrnuError):
         prnu.rgb_to_luma(torch.zeros((1, 3, 3, 3), dtype=torch.uint8, device="cuda"))   # H*W not a multiple of 4
+
+
+# ---------------------------------------------------------------- f2 WDFT (R-23)
+@pytest.mark.gpu
+@pytest.mark.parametrize("B,H,W", [(1, 16, 24), (2, 130, 170), (1, 270, 480)])
+def test_wdft_matches_oracle(prnu, B, H, W):
+    rng = np.random.default_rng(H * W)
+    y, x = np.mgrid[0:H, 0:W]
+    Ks = []
+    for b in range(B):
+        K = rng.normal(0, 0.01, (H, W)) + 0.03 * np.cos(2 * np.pi * (3 * y / H + 7 * x / W + 0.3 * b))
+        Ks.append((K - K.mean()).astype(np.float32))
+    Kt = torch.from_numpy(np.stack(Ks)).cuda()
+    out = prnu.WdftPlan(H, W, B)(Kt).cpu().numpy()
+    for b in range(B):
+        ref = oracle.wiener_dft(Ks[b].astype(np.float64))
+        err = np.max(np.abs(out[b] - ref)) / np.max(np.abs(Ks[b]))
+        assert err <= 1e-4, err
+
+
+@pytest.mark.gpu
+def test_wdft_fingerprint_fhd(prnu):
+    """On a real (synthetic-camera) fingerprint at FHD: parity and it keeps the PRNU
+    (NCC with the true K does not drop)."""
+    v = synth.video("drift", 100, 1080, 1920, seed=3)
+    fp = prnu.extract_fingerprint(v.frames.cuda(), 50, batch=2)
+    Kw = prnu.wdft(fp.K)
+    ref = oracle.wiener_dft(fp.K.cpu().numpy().astype(np.float64))
+    err = np.max(np.abs(Kw.cpu().numpy() - ref)) / float(fp.K.abs().max())
+    assert err <= 1e-4, err
+    assert prnu.ncc(Kw, v.K.cuda()).item() >= prnu.ncc(fp.K, v.K.cuda()).item() - 0.02

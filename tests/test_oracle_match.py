@@ -141,3 +141,62 @@ def test_blockwise_equals_per_tile_aligned_pce():
         assert abs(p - pp) <= 1e-9 * abs(pp)
         assert abs(c - oracle.ncc(r, t)) < 1e-12
         assert p > 0 and c > 0.1                      # matched tiles correlate
+
+
+# ---------------------------------------------------------------- f2: Wiener filtering in the DFT domain (R-23)
+def test_wdft_delta_is_fixed_point():
+    """A unit impulse has a flat magnitude spectrum: A^2 = 1/(HW) = s2 everywhere,
+    so every box mean equals s2 and the gain s2/max(m, s2) is exactly 1."""
+    K = np.zeros((16, 24))
+    K[3, 5] = 1.0
+    assert np.max(np.abs(oracle.wiener_dft(K) - K)) < 1e-12
+
+
+def test_wdft_homogeneous_and_real():
+    rng = np.random.default_rng(1)
+    K = rng.normal(0, 0.01, (20, 28))
+    K -= K.mean()
+    a = oracle.wiener_dft(K)
+    assert np.max(np.abs(oracle.wiener_dft(3.5 * K) - 3.5 * a)) < 1e-12   # gain is scale-free
+    assert np.isrealobj(a) and abs(a.mean()) < 1e-12                     # zero-mean stays zero-mean
+
+
+def test_wdft_attenuates_a_periodic_component_not_the_noise():
+    """A strong periodic pattern (a spectral peak, the artefact WDFT targets) is
+    attenuated; the white part passes with gain <= 1 and keeps most of its energy."""
+    rng = np.random.default_rng(2)
+    H, W = 64, 64
+    noise = rng.normal(0, 0.01, (H, W))
+    y, x = np.mgrid[0:H, 0:W]
+    periodic = 0.05 * np.cos(2 * np.pi * (5 * y / H + 9 * x / W))
+    K = noise + periodic
+    K -= K.mean()
+    out = oracle.wiener_dft(K)
+    def peak(z):
+        return np.abs(np.fft.fft2(z))[5, 9]
+    assert peak(out) < 0.2 * peak(K)
+    rest = out - (np.sum(out * periodic) / np.sum(periodic * periodic)) * periodic
+    assert 0.5 * np.sum(noise ** 2) < np.sum(rest ** 2) <= 1.01 * np.sum(noise ** 2)
+
+
+def test_wdft_gain_matches_brute_force_windows():
+    """The box means inside wiener_dft use scipy 'reflect' = the e_N mirror windows
+    (R-7): brute force on a tiny plane."""
+    rng = np.random.default_rng(3)
+    K = rng.normal(0, 1, (5, 6))
+    K -= K.mean()
+    H, W = K.shape
+    F = np.fft.fft2(K)
+    A2 = np.abs(F) ** 2 / (H * W)
+    s2 = np.mean(K * K)
+    def e(i, N):
+        r = i % (2 * N)
+        return r if r < N else 2 * N - 1 - r
+    m = np.full((H, W), np.inf)
+    for w in (3, 5, 7, 9):
+        h = w // 2
+        box = np.array([[np.mean([A2[e(u + dy, H), e(v + dx, W)] for dy in range(-h, h + 1)
+                                  for dx in range(-h, h + 1)]) for v in range(W)] for u in range(H)])
+        m = np.minimum(m, box)
+    ref = np.real(np.fft.ifft2(F * (s2 / np.maximum(m, s2))))
+    assert np.max(np.abs(oracle.wiener_dft(K) - ref)) < 1e-12

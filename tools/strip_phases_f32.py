@@ -1,0 +1,16 @@
+"""Phase breakdown of k_analysis_strip<float> (needs a -DPRNU_STRIP_PROFILE build): fp32 planes."""
+import ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_1909_04573_b200 as prnu
+x = torch.rand(64, 1080, 1920, device="cuda") * 255
+prnu.residual(x); torch.cuda.synchronize()
+buf = (ctypes.c_ulonglong * 16)()
+prnu._lib.prnu_debug_strip_profile(buf, 1)
+prnu.residual(x); torch.cuda.synchronize()
+prnu._lib.prnu_debug_strip_profile(buf, 1)
+names = ["stage(wait TMA/manual/fixup)", "row pass", "B1 wait", "column pass", "V0,V2 write", "B2 wait",
+         "V1 write", "B3 wait", "H pass", "B4 wait"]
+tot = sum(buf[k] for k in range(10))
+for k in range(10):
+    print(f"{names[k]:32s} {100.0 * buf[k] / tot:6.2f}%")
