@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the NEXT-row measurements (f1, f2, f4)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the oracle sample")
     return ap.parse_args()
 
@@ -355,6 +356,37 @@ def main():
                 "bytes_per_launch": kt.get("alg_bytes_per_launch"), "avg_launch_ms": avg_ms,
                 "share_of_kernel_time": kt["share"]}
 
+    # ---- NEXT rows, measured outside the step: f2 WDFT of the two
+    #      fingerprints, f1 500x500 block matching of the query, f4 RGB->luma
+    next_rows = None
+    if not args.no_extras:
+        def timed(fn, reps=5):
+            fn()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(torch.cuda.current_stream())
+            for _ in range(reps):
+                fn()
+            b.record(torch.cuda.current_stream())
+            torch.cuda.synchronize()
+            return a.elapsed_time(b) / reps
+        Ks2 = torch.stack([exs[d](frames).K for d in depths])
+        wplan = prnu.WdftPlan(H, W, len(depths), device=dev)
+        t_wdft = timed(lambda: wplan(Ks2))
+        Rq = prnu.residual(query, zero_mean=True)[0]
+        Tq = prnu.pce_template(Ks2[0], query)[0]
+        bplan = prnu.BlockPlan(H, W, 500, device=dev)
+        t_blk = timed(lambda: bplan(Rq, Tq))
+        rgb = torch.randint(0, 256, (16, 3, H, W), dtype=torch.uint8, device=dev)
+        t_luma = timed(lambda: prnu.rgb_to_luma(rgb))
+        luma_bytes = 16 * H * W * (3 + 4)
+        pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
+        peak_hbm = json.load(open(pk)).get("hbm_gbs", 6650.0) if os.path.exists(pk) else 6650.0
+        next_rows = {"f2_wdft_ms_per_fingerprint": t_wdft / len(depths),
+                     "f1_block_match_ms": t_blk, "f1_tiles": bplan.n_tiles,
+                     "f4_rgb_to_luma_GBps": luma_bytes / (t_luma / 1000.0) / 1e9,
+                     "f4_rgb_to_luma_frac_hbm": luma_bytes / (t_luma / 1000.0) / 1e9 / peak_hbm}
+
     # ---- e2e through the host-buffer C-ABI call: the frames start in pinned host
     #      memory; one upload per step feeds every depth (prnu_extract_multi_host),
     #      the fingerprints come back to host memory
@@ -409,6 +441,7 @@ def main():
             "kernels": kernels,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "next_rows": next_rows,
         }
         print(json.dumps(line), flush=True)
     barrier(world)

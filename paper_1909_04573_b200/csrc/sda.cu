@@ -173,8 +173,87 @@ __global__ void __launch_bounds__(256) k_rgb_to_luma(const uint8_t* __restrict__
     }
 }
 
+// 16 pixels per thread-iteration: 16-byte loads of each plane (planar) or three
+// 16-byte loads of 48 interleaved bytes, 16-byte stores.  Requires P % 16 == 0
+// (else the 4-pixel kernel below runs).
+template <int LAYOUT, int ROUND>
+__global__ void __launch_bounds__(256) k_rgb_to_luma16(const uint8_t* __restrict__ rgb, long long n, long long P,
+                                                       void* __restrict__ out) {
+    const long long P16 = P / 16;
+    const long long total = n * P16;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long f = i / P16, q = i - f * P16;
+        uint32_t w[12];
+        if (LAYOUT == 0) {
+            const uint8_t* base = rgb + (size_t)f * 3 * P + 16 * q;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(base + c * P));
+                w[4 * c] = v.x;
+                w[4 * c + 1] = v.y;
+                w[4 * c + 2] = v.z;
+                w[4 * c + 3] = v.w;
+            }
+        } else {
+            const uint4* base = reinterpret_cast<const uint4*>(rgb + ((size_t)f * P + 16 * q) * 3);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const uint4 v = __ldg(base + c);
+                w[4 * c] = v.x;
+                w[4 * c + 1] = v.y;
+                w[4 * c + 2] = v.z;
+                w[4 * c + 3] = v.w;
+            }
+        }
+        uint32_t s[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            uint32_t r, g, b;
+            if (LAYOUT == 0) {
+                r = (w[k >> 2] >> (8 * (k & 3))) & 0xffu;
+                g = (w[4 + (k >> 2)] >> (8 * (k & 3))) & 0xffu;
+                b = (w[8 + (k >> 2)] >> (8 * (k & 3))) & 0xffu;
+            } else {
+                const int o = 3 * k;
+                r = (w[o >> 2] >> (8 * (o & 3))) & 0xffu;
+                g = (w[(o + 1) >> 2] >> (8 * ((o + 1) & 3))) & 0xffu;
+                b = (w[(o + 2) >> 2] >> (8 * ((o + 2) & 3))) & 0xffu;
+            }
+            s[k] = luma_s(r, g, b);
+        }
+        if (ROUND == 0) {
+            float4* o4 = reinterpret_cast<float4*>(out) + 4 * i;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                o4[k] = make_float4(__fdiv_rn((float)s[4 * k], 1000.0f), __fdiv_rn((float)s[4 * k + 1], 1000.0f),
+                                    __fdiv_rn((float)s[4 * k + 2], 1000.0f), __fdiv_rn((float)s[4 * k + 3], 1000.0f));
+        } else {
+            uint32_t ow[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                uint32_t qv = s[k] / 1000u;
+                const uint32_t rem = s[k] - 1000u * qv;
+                if (rem > 500u || (rem == 500u && (qv & 1u))) ++qv;   // half to even
+                ow[k >> 2] |= qv << (8 * (k & 3));
+            }
+            reinterpret_cast<uint4*>(out)[i] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+        }
+    }
+}
+
 int launch_rgb_to_luma(const uint8_t* rgb, long long n, long long P, int layout, int rounding, void* out,
                        cudaStream_t st) {
+    if (P % 16 == 0 && ((uintptr_t)rgb & 15) == 0 && ((uintptr_t)out & 15) == 0) {
+        const long long total = n * (P / 16);
+        const int blocks = (int)std::max(1LL, std::min((total + 255) / 256, 148LL * 16));
+        if (layout == 0 && rounding == 0) k_rgb_to_luma16<0, 0><<<blocks, 256, 0, st>>>(rgb, n, P, out);
+        else if (layout == 0) k_rgb_to_luma16<0, 1><<<blocks, 256, 0, st>>>(rgb, n, P, out);
+        else if (rounding == 0) k_rgb_to_luma16<1, 0><<<blocks, 256, 0, st>>>(rgb, n, P, out);
+        else k_rgb_to_luma16<1, 1><<<blocks, 256, 0, st>>>(rgb, n, P, out);
+        count_launch();
+        return check_launch("k_rgb_to_luma16");
+    }
     const long long total = n * (P / 4);
     const int blocks = (int)std::max(1LL, std::min((total + 255) / 256, 148LL * 16));
     if (layout == 0 && rounding == 0) k_rgb_to_luma<0, 0><<<blocks, 256, 0, st>>>(rgb, n, P, out);

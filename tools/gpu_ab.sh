@@ -7,7 +7,7 @@ else timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q 2>&1 | t
 i=0
 for envs in "$@"; do
   i=$((i+1))
-  env $envs timeout 600 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ab_$i.json 2> gpurun_out/ab_$i.err
+  env $envs timeout 600 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --no-extras > gpurun_out/ab_$i.json 2> gpurun_out/ab_$i.err
   echo "== [$envs] rc $?"; tail -2 gpurun_out/ab_$i.err
   python tools/show_bench.py gpurun_out/ab_$i.json | head -8
 done

@@ -7,7 +7,7 @@ i=0
 for defs in "$@"; do
   i=$((i+1))
   PRNU_NVCC_DEFS="$defs" python paper_1909_04573_b200/_build.py --force > gpurun_out/var_build_$i.log 2>&1 || { echo "build $i failed"; tail -5 gpurun_out/var_build_$i.log; continue; }
-  timeout 600 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/var_$i.json 2> gpurun_out/var_$i.err
+  timeout 600 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --no-extras > gpurun_out/var_$i.json 2> gpurun_out/var_$i.err
   echo "== [$defs] rc $?"; tail -2 gpurun_out/var_$i.err
   python tools/show_bench.py gpurun_out/var_$i.json 2>/dev/null | head -8
 done
