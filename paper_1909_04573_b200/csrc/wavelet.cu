@@ -581,158 +581,6 @@ __global__ void __launch_bounds__(A_NT, PRNU_ANALYSIS_MINB) k_analysis_shrink(An
     else shrink3_single(a, g, s_det, reinterpret_cast<float4*>(s_row), s_rmap, s_cmap);
 }
 
-// Warp-specialized persistent analysis: WS_NP producer warps (tables, input
-// tile, row pass, column pass) and WS_NC consumer warps (shrink) hand tiles over
-// through a two-slot ring of detail tiles, with named barriers: FULL[slot]
-// (producer arrives, consumer syncs) and EMPTY[slot] (consumer arrives,
-// producer syncs before reusing the slot).  One CTA per SM walks tiles
-// blockIdx.x, +gridDim.x, ...; while one group waits at its internal
-// barriers the other group keeps the SM issuing.
-#ifndef PRNU_WS_NP
-#define PRNU_WS_NP 12
-#endif
-#ifndef PRNU_WS_NC
-#define PRNU_WS_NC 12
-#endif
-constexpr int WS_NP = PRNU_WS_NP, WS_NC = PRNU_WS_NC;
-constexpr int WS_PT = 32 * WS_NP, WS_CT = 32 * WS_NC, WS_T = WS_PT + WS_CT;
-constexpr int WS_DET = 3 * AR * DT_P;               // one detail slot
-constexpr int WS_FLOATS = A_SMEM_IN + 2 * RW_PLANE + 2 * WS_DET + 2 * V_PLANE4 * 4;
-constexpr size_t WS_SMEM_BYTES = sizeof(float) * WS_FLOATS + sizeof(int) * (2 * AIN + 4 * AR);
-enum { BAR_PROD = 1, BAR_CONS = 2, BAR_FULL0 = 3, BAR_EMPTY0 = 5 };
-
-__device__ __forceinline__ void named_arrive(int id, int count) {
-    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-
-template <typename TIn>
-__global__ void __launch_bounds__(WS_T, 1) k_analysis_ws(AnalysisArgs a, int tiles_x, int tiles_y, int n_tiles) {
-    extern __shared__ __align__(128) float smem[];
-    float* s_in = smem;
-    float* s_row = s_in + A_SMEM_IN;
-    float* s_det0 = s_row + 2 * RW_PLANE;
-    float4* s_v = reinterpret_cast<float4*>(s_det0 + 2 * WS_DET);
-    int* s_iy = reinterpret_cast<int*>(smem + WS_FLOATS);
-    int* s_ix = s_iy + AIN;
-    int* s_rmap0 = s_ix + AIN;        // [2][AR]
-    int* s_cmap0 = s_rmap0 + 2 * AR;  // [2][AR]
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int per_frame = tiles_x * tiles_y;
-    auto tile_of = [&](int t) {
-        const int b = t / per_frame, r = t - b * per_frame;
-        return analysis_tile(a, b, r / tiles_x, r % tiles_x);
-    };
-    if (warp < WS_NP) {   // ---------------- producer
-        int k = 0;
-        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++k) {
-            const int slot = k & 1;
-            const ATile g = tile_of(t);
-            if (k >= 2) NamedBar{BAR_EMPTY0 + slot, WS_T}.sync();   // consumer released tile k-2's slot
-            const bool fast_u8 = tile_fast_u8<TIn>(a, g);
-            analysis_tables(a, g, s_iy, s_ix, s_rmap0 + slot * AR, s_cmap0 + slot * AR, tid, WS_PT);
-            NamedBar{BAR_PROD, WS_PT}.sync();
-            load_tile<TIn, WS_NP>(a, g, fast_u8, s_in, s_iy, s_ix, warp, lane);
-            NamedBar{BAR_PROD, WS_PT}.sync();
-            rowpass_f32(s_in, s_row, tid, WS_PT);
-            NamedBar{BAR_PROD, WS_PT}.sync();
-            colpass(a, g, s_row, s_det0 + slot * WS_DET, tid, WS_PT);
-            named_arrive(BAR_FULL0 + slot, WS_T);                  // details of tile k complete
-        }
-    } else {              // ---------------- consumer
-        const int ctid = tid - WS_PT;
-        int k = 0;
-        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++k) {
-            const int slot = k & 1;
-            const ATile g = tile_of(t);
-            NamedBar{BAR_FULL0 + slot, WS_T}.sync();
-            shrink3(a, g, s_det0 + slot * WS_DET, s_v, s_rmap0 + slot * AR, s_cmap0 + slot * AR,
-                    NamedBar{BAR_CONS, WS_CT}, ctid, WS_CT);
-            if (t + 2 * (int)gridDim.x < n_tiles) named_arrive(BAR_EMPTY0 + slot, WS_T);   // slot free for k+2
-        }
-    }
-}
-
-// Level-1 u8 analysis, persistent: each CTA walks tiles blockIdx.x, +gridDim.x,
-// ...; interior tiles arrive by TMA (box U8_P x AIN bytes) into a u8 tile that
-// is re-filled for the next tile as soon as the row pass has consumed it, so
-// the load overlaps the column pass and the shrink.  Border tiles (mirrored
-// input) are loaded with ordinary loads.
-constexpr int U8_TILE_BYTES = ((AIN * U8_P + 127) / 128) * 128;
-constexpr int A8_ROW_FLOATS = A_SMEM_ROW;          // row-pass planes; later the two vertical-sum buffers
-constexpr int A8_DET_FLOATS = 3 * AR * DT_P;
-constexpr size_t A8_SMEM_BYTES = U8_TILE_BYTES + sizeof(float) * (A8_ROW_FLOATS + A8_DET_FLOATS) +
-                                 sizeof(int) * (2 * AIN + 2 * AR) + 16;
-
-__device__ __forceinline__ bool u8_tile_interior(const AnalysisArgs& a, const ATile& g) {
-    const int iy = 2 * g.cy0 - 6, ix = 2 * g.cx0 - 6 - U8_OFF;   // ix: 16-byte aligned box start
-    return iy >= 0 && ix >= 0 && (ix & 15) == 0 && iy + AIN <= a.NH && ix + U8_OFF + AIN <= a.NW;
-}
-
-__global__ void __launch_bounds__(A_NT, 3) k_analysis_u8_tma(const __grid_constant__ CUtensorMap in_map, AnalysisArgs a,
-                                                           int tiles_x, int tiles_y, int n_tiles) {
-    extern __shared__ __align__(128) unsigned char smem8[];
-    uint8_t* s_in8 = smem8;
-    float* s_row = reinterpret_cast<float*>(smem8 + U8_TILE_BYTES);
-    float* s_det = s_row + A8_ROW_FLOATS;
-    int* s_iy = reinterpret_cast<int*>(s_det + A8_DET_FLOATS);
-    int* s_ix = s_iy + AIN;
-    int* s_rmap = s_ix + AIN;
-    int* s_cmap = s_rmap + AR;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(s_cmap + AR + ((2 * AIN + 2 * AR) & 1));
-    const int tid = threadIdx.x;
-    const int per_frame = tiles_x * tiles_y;
-    auto tile_of = [&](int t) {
-        const int b = t / per_frame, r = t - b * per_frame;
-        return analysis_tile(a, b, r / tiles_x, r % tiles_x);
-    };
-    auto issue = [&](const ATile& g) {
-        mbar_arrive_expect_tx(bar, (uint32_t)(U8_P * AIN));
-        tma_load_3d(s_in8, &in_map, 2 * g.cx0 - 6 - U8_OFF, 2 * g.cy0 - 6, g.b, bar);
-    };
-    if (tid == 0) {
-        mbar_init(bar, 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-    uint32_t phase = 0;
-    int t = blockIdx.x;
-    if (t < n_tiles && tid == 0) {
-        const ATile g0 = tile_of(t);
-        if (u8_tile_interior(a, g0)) issue(g0);
-    }
-    for (; t < n_tiles; t += gridDim.x) {
-        const ATile g = tile_of(t);
-        analysis_tables(a, g, s_iy, s_ix, s_rmap, s_cmap);
-        if (u8_tile_interior(a, g)) {
-            mbar_wait(bar, phase);
-            phase ^= 1;
-            __syncthreads();   // tables visible
-        } else {
-            __syncthreads();   // tables visible
-            const uint8_t* in = reinterpret_cast<const uint8_t*>(a.in) + (size_t)g.b * a.in_bstride;
-            for (int e = tid; e < AIN * AIN; e += A_NT) {
-                const int r = e / AIN, c = e - r * AIN;
-                s_in8[r * U8_P + U8_OFF + c] = __ldg(in + (size_t)s_iy[r] * a.in_pitch + s_ix[c]);
-            }
-            __syncthreads();
-        }
-        rowpass_u8(s_in8, s_row);
-        fence_proxy_async();   // order this thread's generic accesses of s_in8 before the next TMA write
-        __syncthreads();       // u8 tile consumed, s_row complete
-        const int tn = t + gridDim.x;
-        if (tid == 0 && tn < n_tiles) {
-            const ATile gn = tile_of(tn);
-            if (u8_tile_interior(a, gn)) {
-                fence_proxy_async();
-                issue(gn);   // lands while this tile's column pass and shrink run
-            }
-        }
-        colpass(a, g, s_row, s_det);
-        __syncthreads();
-        shrink3(a, g, s_det, reinterpret_cast<float4*>(s_row), s_rmap, s_cmap, CtaBar{});
-    }
-}
-
 // ============================================================== synthesis
 // Output tile ST_Y x ST_X; its coefficients (rows ky0 .. ky0+SC_Y, cols kx0 ..
 // kx0+SC_X of the four subband planes) arrive by TMA into a double-buffered
@@ -1237,13 +1085,7 @@ static int setup_attributes() {
                                           (int)S_SMEM_BYTES);
     cudaError_t e5 = cudaFuncSetAttribute(k_synth_tma<1, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)S_SMEM_BYTES);
-    cudaError_t e6 = cudaFuncSetAttribute(k_analysis_u8_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)A8_SMEM_BYTES);
-    cudaError_t e7 = cudaFuncSetAttribute(k_analysis_ws<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)WS_SMEM_BYTES);
-    cudaError_t e8 = cudaFuncSetAttribute(k_analysis_ws<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)WS_SMEM_BYTES);
-    cudaError_t e = e1 ? e1 : e2 ? e2 : e3 ? e3 : e4 ? e4 : e5 ? e5 : e6 ? e6 : e7 ? e7 : e8;
+    cudaError_t e = e1 ? e1 : e2 ? e2 : e3 ? e3 : e4 ? e4 : e5;
     if (e != cudaSuccess) return fail(PRNU_CUDA_ERROR, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
     g_attr_done = true;
     return PRNU_OK;
@@ -1358,16 +1200,6 @@ static int denoise_front(const TIn* in, long long in_bstride, int in_pitch, int 
             a.in = in;
             a.in_bstride = in_bstride;
             a.in_pitch = in_pitch;
-            CUtensorMap map;
-            // The persistent TMA variant is correct but measured slower than the generic
-            // kernel on B200 (23.9 vs 21.5 ms/step, profiles/r01): opt-in only.
-            static const bool use_tma = getenv("PRNU_TMA_ANALYSIS") != nullptr;
-            const bool tma_ok = use_tma && sizeof(TIn) == 1 && (in_pitch % 16) == 0 && (in_bstride % 16) == 0 &&
-                                ((uintptr_t)in % 16) == 0 &&
-                                encode_tensor_map_3d(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, in, (uint64_t)a.NW,
-                                                     (uint64_t)a.NH, (uint64_t)nb, (uint64_t)in_pitch,
-                                                     (uint64_t)in_bstride, U8_P, AIN);
-            static const bool use_ws = getenv("PRNU_WS_ANALYSIS") != nullptr;   // A/B switch
             if (use_strip()) {
                 rc = sizeof(TIn) == 1
                          ? launch_analysis_strip_u8(reinterpret_cast<const uint8_t*>(in), in_bstride, in_pitch, a.NH,
@@ -1377,14 +1209,7 @@ static int denoise_front(const TIn* in, long long in_bstride, int in_pitch, int 
                                                      a.NW, a.ll, a.d0, a.d1, a.d2, a.out_bstride, a.out_pitch, a.nH,
                                                      a.nW, sp, nb, st);
                 if (rc) return rc;
-            } else if (tma_ok) {
-                const int tx = (int)grid.x, ty = (int)grid.y, n_tiles = tx * ty * nb;
-                const int ctas = std::min(n_tiles, 148 * 3);
-                k_analysis_u8_tma<<<ctas, A_NT, A8_SMEM_BYTES, st>>>(map, a, tx, ty, n_tiles);
-            } else if (use_ws) {
-                const int tx = (int)grid.x, ty = (int)grid.y, n_tiles = tx * ty * nb;
-                k_analysis_ws<TIn><<<std::min(n_tiles, 148), WS_T, WS_SMEM_BYTES, st>>>(a, tx, ty, n_tiles);
-            } else {
+            } else {   // PRNU_STRIP=0: the tile kernel
                 k_analysis_shrink<TIn><<<grid, A_NT, a_smem_bytes<TIn>(), st>>>(a);
             }
         } else {
