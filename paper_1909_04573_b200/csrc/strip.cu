@@ -71,12 +71,20 @@ constexpr int SR_RB_FLOATS = 2 * SR_IR * SR_RBP;
 // fit 3 CTAs/SM (<= 75 KB shared memory).
 template <typename T>
 struct StripCfg;
+#ifndef PRNU_U8_OMAX   // build-time A/B knobs of the u8 configuration (defaults: measured best)
+#define PRNU_U8_OMAX 112
+#define PRNU_U8_P2 121
+#define PRNU_U8_CP 124
+#define PRNU_U8_NSTG 3
+#define PRNU_U8_MINB 3
+#endif
 template <>
 struct StripCfg<uint8_t> {
-    static constexpr int OMAX = 112;   // max output columns per strip
-    static constexpr int P2 = 121;     // float2 pitch of the vertical-sum planes (== 1 mod 8: conflict-free LDS.64)
-    static constexpr int CP = 124;     // float pitch of the coefficient planes (== 28 mod 32: conflict-free LDS.128)
-    static constexpr int NSTG = 3;
+    static constexpr int OMAX = PRNU_U8_OMAX;   // max output columns per strip
+    static constexpr int P2 = PRNU_U8_P2;       // float2 pitch of the vertical-sum planes (== 1 mod 8: conflict-free LDS.64)
+    static constexpr int CP = PRNU_U8_CP;       // float pitch of the coefficient planes (== 28 mod 32: conflict-free LDS.128)
+    static constexpr int NSTG = PRNU_U8_NSTG;
+    static constexpr int MINB = PRNU_U8_MINB;   // CTAs per SM the register budget targets
 };
 template <>
 struct StripCfg<float> {
@@ -84,6 +92,7 @@ struct StripCfg<float> {
     static constexpr int P2 = 113;
     static constexpr int CP = 116;     // == 20 mod 32
     static constexpr int NSTG = 1;
+    static constexpr int MINB = 3;
 };
 // V/c buffer of one subband: (v3, v5) plane [8][P2] float2, (v7, v9) plane, c plane [8][CP]
 template <typename T>
@@ -629,7 +638,6 @@ static int smem_pad() {
     static const int p = getenv("PRNU_STRIP_SMEM_PAD") ? atoi(getenv("PRNU_STRIP_SMEM_PAD")) : 0;
     return p;
 }
-constexpr int MINB = 3;
 
 template <typename T>
 static int strip_launch(const T* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll, float* d0,
@@ -637,13 +645,13 @@ static int strip_launch(const T* in, long long in_bstride, int in_pitch, int NH,
                         const ShrinkParams& sp, int nb, cudaStream_t st) {
     if (!g_strip_attr) {
         cudaError_t e[4] = {
-            cudaFuncSetAttribute(k_analysis_strip<uint8_t, MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cudaFuncSetAttribute(k_analysis_strip<uint8_t, StripCfg<uint8_t>::MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)strip_smem_bytes<uint8_t>() + smem_pad()),
-            cudaFuncSetAttribute(k_analysis_strip<uint8_t, MINB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cudaFuncSetAttribute(k_analysis_strip<uint8_t, StripCfg<uint8_t>::MINB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)strip_smem_bytes<uint8_t>() + smem_pad()),
-            cudaFuncSetAttribute(k_analysis_strip<float, MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cudaFuncSetAttribute(k_analysis_strip<float, StripCfg<float>::MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)strip_smem_bytes<float>() + smem_pad()),
-            cudaFuncSetAttribute(k_analysis_strip<float, MINB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cudaFuncSetAttribute(k_analysis_strip<float, StripCfg<float>::MINB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)strip_smem_bytes<float>() + smem_pad())};
         for (cudaError_t x : e)
             if (x != cudaSuccess)
@@ -672,7 +680,7 @@ static int strip_launch(const T* in, long long in_bstride, int in_pitch, int NH,
     // segments of ~184 rows (prologue overhead ~4%), more of them while the grid
     // holds fewer than 6 waves of 3 CTAs/SM (small planes; measured, profiles/r01)
     int nseg = (nH + 183) / 184;
-    while ((long long)S * nseg * nb < 6LL * 148 * MINB && (nH + nseg) / (nseg + 1) >= 32) ++nseg;
+    while ((long long)S * nseg * nb < 6LL * 148 * StripCfg<T>::MINB && (nH + nseg) / (nseg + 1) >= 32) ++nseg;
     a.SH = sh_env > 0 ? (int)align_up((size_t)sh_env, 8) : (int)align_up((size_t)((nH + nseg - 1) / nseg), 8);
     nseg = (nH + a.SH - 1) / a.SH;
     CUtensorMap map{};
@@ -685,9 +693,9 @@ static int strip_launch(const T* in, long long in_bstride, int in_pitch, int NH,
     if (no_tma) a.use_tma = 0;
     dim3 grid(S, nseg, nb);
     if (sp.wmask == 15)
-        k_analysis_strip<T, MINB, true><<<grid, SR_NT, strip_smem_bytes<T>() + smem_pad(), st>>>(map, a);
+        k_analysis_strip<T, StripCfg<T>::MINB, true><<<grid, SR_NT, strip_smem_bytes<T>() + smem_pad(), st>>>(map, a);
     else
-        k_analysis_strip<T, MINB, false><<<grid, SR_NT, strip_smem_bytes<T>() + smem_pad(), st>>>(map, a);
+        k_analysis_strip<T, StripCfg<T>::MINB, false><<<grid, SR_NT, strip_smem_bytes<T>() + smem_pad(), st>>>(map, a);
     return PRNU_OK;
 }
 
