@@ -679,8 +679,12 @@ static int strip_launch(const T* in, long long in_bstride, int in_pitch, int NH,
     static const int sh_env = getenv("PRNU_STRIP_SH") ? atoi(getenv("PRNU_STRIP_SH")) : 0;
     // segments of ~184 rows (prologue overhead ~4%), more of them while the grid
     // holds fewer than 6 waves of 3 CTAs/SM (small planes; measured, profiles/r01)
-    int nseg = (nH + 183) / 184;
-    while ((long long)S * nseg * nb < 6LL * 148 * StripCfg<T>::MINB && (nH + nseg) / (nseg + 1) >= 32) ++nseg;
+    static const int seg_rows = getenv("PRNU_STRIP_SEGROWS") ? atoi(getenv("PRNU_STRIP_SEGROWS")) : 184;
+    static const int waves_u8 = getenv("PRNU_STRIP_WAVES_U8") ? atoi(getenv("PRNU_STRIP_WAVES_U8")) : 6;
+    static const int waves_f32 = getenv("PRNU_STRIP_WAVES_F32") ? atoi(getenv("PRNU_STRIP_WAVES_F32")) : 6;
+    const long long waves = sizeof(T) == 1 ? waves_u8 : waves_f32;
+    int nseg = (nH + seg_rows - 1) / seg_rows;
+    while ((long long)S * nseg * nb < waves * 148 * StripCfg<T>::MINB && (nH + nseg) / (nseg + 1) >= 32) ++nseg;
     a.SH = sh_env > 0 ? (int)align_up((size_t)sh_env, 8) : (int)align_up((size_t)((nH + nseg - 1) / nseg), 8);
     nseg = (nH + a.SH - 1) / a.SH;
     CUtensorMap map{};

@@ -15,4 +15,5 @@ names = ["stage(wait TMA/manual/fixup)", "row pass", "B1 wait", "column pass", "
          "V1 write", "B3 wait", "H pass", "B4 wait"]
 tot = sum(buf[k] for k in range(10))
 for k in range(10):
-    print(f"{names[k]:32s} {100.0 * buf[k] / tot:6.2f}%")
+    print(f"{names[k]:32s} {100.0 * buf[k] / tot:6.2f}%  {buf[k] / 1e9:8.3f} Gcyc")
+print(f"{'total':32s} {100.0:6.2f}%  {tot / 1e9:8.3f} Gcyc")
