@@ -8,6 +8,8 @@ never imports the product path: the two share no code.
 * a1-a6 (SDA mean, DWT, shrink, IDWT, MLE, finalize) live in ``oracle.c``
   (plain loops, fp64), loaded here through ctypes.
 * a7-a8 (NCC, PCE) live in :mod:`oracle.match` (numpy fp64, ``numpy.fft``).
+* f3 denoiser variants (db8, pad + periodic, undecimated) live in
+  :mod:`oracle.variants` (numpy fp64, step by step; shrink from ``oracle.c``).
 
 Citations: ``P:<n>`` PAPER.md line, ``S:<n>`` SPEC.md line, ``R-<n>`` a
 reading listed in DESIGN.md.
