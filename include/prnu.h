@@ -266,6 +266,43 @@ int prnu_block_match(void* plan, const float* residual, const float* template_, 
 int prnu_block_plan_destroy(void* plan);
 
 /* ---------------------------------------------------------------------------
+ * f3  Denoiser variants — S:117 ("Daubechies-8 ...
+ * undecimated-boundary-safe", garbled) and S:150; readings
+ * R-24..R-26 of DESIGN.md.  The method of prnu_residual (decomposition, the
+ * local-variance Wiener shrink of every detail subband with the params' sigma0^2
+ * and mirror windows, approximation passed through, W = I - F(I)) with:
+ *   taps       8 (the default 8-tap Daubechies filter) or 16 (db8, 8 vanishing
+ *              moments; Daubechies 1992 Table 6.1);
+ *   boundary   0: half-sample symmetric extension, expansive subbands
+ *              floor((N + taps - 1)/2) (the default);  1: the plane is padded
+ *              (bottom/right, half-sample symmetric) to multiples of 2^levels,
+ *              transformed with periodic extension (subbands N/2), and W is
+ *              cropped back to H x W;
+ *   transform  0: decimated DWT;  1: undecimated (stationary) DWT — level l
+ *              filters with taps dilated by 2^(l-1), no decimation, circular
+ *              extension (requires boundary = 1), synthesis = adjoint / 2 per axis.
+ * {8, 0, 0} is the default denoiser (same result as prnu_residual up to fp32
+ * rounding; this generic path is slower).
+ * planes, W_out: fp32 device [batch][H][W]; zero_mean as prnu_residual.
+ * Errors: INVALID_ARG, PLANE_TOO_SMALL (H or W < 2^levels), BAD_PARAMETER
+ * (params, or a variant field out of range), WORKSPACE_TOO_SMALL, CUDA_ERROR.
+ * prnu_wavelet_filter: the library's lowpass filter for `taps` (8 or 16) in
+ *   minimum-phase order, as the fp32 values the kernels use, widened to double
+ *   (host call, no device work).
+ * ------------------------------------------------------------------------- */
+typedef struct {
+    int taps;        /* 8 (default) or 16                        */
+    int boundary;    /* 0 symmetric (default) or 1 pad + periodic */
+    int transform;   /* 0 decimated (default) or 1 undecimated    */
+} prnu_denoise_variant;
+size_t prnu_residual_variant_workspace_bytes(int batch, int H, int W, const prnu_denoise_params* p,
+                                             const prnu_denoise_variant* v);
+int prnu_residual_variant(const float* planes, int batch, int H, int W, const prnu_denoise_params* p,
+                          const prnu_denoise_variant* v, int zero_mean, float* W_out, void* ws, size_t ws_bytes,
+                          void* stream);
+int prnu_wavelet_filter(int taps, double* h_out);
+
+/* ---------------------------------------------------------------------------
  * Diagnostics.
  * prnu_last_error: thread-local text of the last failure ("" if none).
  * prnu_kernel_launches: process-wide count of kernels this library has

@@ -105,14 +105,15 @@ def dwt_sym(x, lo, hi):
 
 def idwt_sym(a, d, rl, rh, N: int):
     """Expansive symmetric synthesis: x[t] = sum_k a[k] rl[t+L-2-2k] + d[k] rh[t+L-2-2k],
-    terms whose filter index lies in [0, L) (oracle.c's offset 6 for L = 8)."""
+    terms whose filter index lies in [0, L) (oracle.c's offset 6 for L = 8).  Summed
+    per filter index f: coefficient k lands on t = 2k + f - (L-2), kept when 0 <= t < N."""
     n, L = a.shape[0], len(rl)
     x = np.zeros((N,) + a.shape[1:])
-    for t in range(N):
-        for k in range(n):
-            f = t + L - 2 - 2 * k
-            if 0 <= f < L:
-                x[t] += a[k] * rl[f] + d[k] * rh[f]
+    k = np.arange(n)
+    for f in range(L):
+        t = 2 * k + f - (L - 2)
+        ok = (t >= 0) & (t < N)
+        x[t[ok]] += a[ok] * rl[f] + d[ok] * rh[f]
     return x
 
 

@@ -65,6 +65,25 @@ class DenoiseParams:
         return p
 
 
+class _Variant(ctypes.Structure):
+    _fields_ = [("taps", ctypes.c_int), ("boundary", ctypes.c_int), ("transform", ctypes.c_int)]
+
+
+@dataclass
+class DenoiseVariant:
+    """f3 denoiser variant (R-24..R-26; include/prnu.h): taps 8 or 16 (db8),
+    boundary 0 (half-sample symmetric) or 1 (pad + periodic), transform 0 (decimated) or
+    1 (undecimated; circular, so boundary must be 1)."""
+    taps: int = 8
+    boundary: int = 0
+    transform: int = 0
+
+    def c(self) -> _Variant:
+        v = _Variant()
+        v.taps, v.boundary, v.transform = int(self.taps), int(self.boundary), int(self.transform)
+        return v
+
+
 _vp = ctypes.c_void_p
 _i = ctypes.c_int
 _i64 = ctypes.c_int64
@@ -113,6 +132,10 @@ _sig("prnu_wdft_plan_destroy", _i, _vp)
 _sig("prnu_block_plan_create", _i, _i, _i, _i, ctypes.POINTER(_i), ctypes.POINTER(_sz), ctypes.POINTER(_vp))
 _sig("prnu_block_match", _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _sz, _vp)
 _sig("prnu_block_plan_destroy", _i, _vp)
+_VP = ctypes.POINTER(_Variant)
+_sig("prnu_residual_variant_workspace_bytes", _sz, _i, _i, _i, _P, _VP)
+_sig("prnu_residual_variant", _i, _vp, _i, _i, _i, _P, _VP, _i, _vp, _vp, _sz, _vp)
+_sig("prnu_wavelet_filter", _i, _i, ctypes.POINTER(_d))
 _sig("prnu_profile_begin", _i)
 _sig("prnu_profile_end", _i, _i, ctypes.c_char_p, ctypes.POINTER(_d), ctypes.POINTER(_i64), ctypes.POINTER(_i))
 _sig("prnu_last_error", ctypes.c_char_p)
@@ -237,6 +260,39 @@ def residual(planes: torch.Tensor, params: DenoiseParams | None = None, zero_mea
 
 
 prnu_residual = residual
+
+
+def residual_variant(planes: torch.Tensor, variant: DenoiseVariant, params: DenoiseParams | None = None,
+                     zero_mean: bool = False, out: torch.Tensor | None = None) -> torch.Tensor:
+    """f3: W = I - F(I) with a denoiser variant (db8 / pad + periodic / undecimated) for
+    fp32 planes [b,H,W] (or [H,W]); same shrink and parameters as residual()."""
+    squeeze = planes.dim() == 2
+    if squeeze:
+        planes = planes.unsqueeze(0)
+    _dev(planes, torch.float32, "planes", (3,))
+    b, H, W = planes.shape
+    p = _params(params)
+    v = variant.c()
+    nbytes = _lib.prnu_residual_variant_workspace_bytes(b, H, W, ctypes.byref(p), ctypes.byref(v))
+    if nbytes == 0:   # invalid size/params/variant: let the library name the error
+        _check(_lib.prnu_residual_variant(_ptr(planes), b, H, W, ctypes.byref(p), ctypes.byref(v), 0,
+                                          _ptr(planes), _ptr(planes), 0, None), "prnu_residual_variant")
+    ws = _ws(nbytes, planes.device)
+    if out is None:
+        out = torch.empty((b, H, W), dtype=torch.float32, device=planes.device)
+    _check(_lib.prnu_residual_variant(_ptr(planes), b, H, W, ctypes.byref(p), ctypes.byref(v), int(zero_mean),
+                                      _ptr(out), _ptr(ws), nbytes, _stream()), "prnu_residual_variant")
+    return out[0] if squeeze else out
+
+
+prnu_residual_variant = residual_variant
+
+
+def wavelet_filter(taps: int = 8) -> list:
+    """The library's minimum-phase lowpass (the fp32 values its kernels use), host call."""
+    h = (ctypes.c_double * taps)()
+    _check(_lib.prnu_wavelet_filter(taps, h), "prnu_wavelet_filter")
+    return list(h)
 
 
 # ---------------------------------------------------------------- a5-a6

@@ -125,6 +125,24 @@ int block_plan_destroy(void* plan);
 int block_plan_dims(void* plan, int* H, int* W, int* n_tiles, size_t* ws_bytes);
 int run_block_match(void* plan, const float* R, const float* T, int excl, double* pce_out, double* ncc_out, void* ws,
                     cudaStream_t st);
+size_t variant_workspace_bytes(int batch, int H, int W, int levels, int taps, int boundary, int transform);
+int run_residual_variant(const float* in, int nb, int H, int W, int levels, int taps, int boundary, int transform,
+                         const ShrinkParams& sp, float* W_out, float* ws, cudaStream_t st);
+int variant_filter(int taps, double* h);
+
+static int validate_variant(const prnu_denoise_variant* v) {
+    if (!v) return fail(PRNU_INVALID_ARG, "variant is NULL");
+    if (v->taps != 8 && v->taps != 16) return fail(PRNU_BAD_PARAMETER, "variant taps must be 8 or 16");
+    if (v->boundary != 0 && v->boundary != 1) return fail(PRNU_BAD_PARAMETER, "variant boundary must be 0 or 1");
+    if (v->transform != 0 && v->transform != 1) return fail(PRNU_BAD_PARAMETER, "variant transform must be 0 or 1");
+    if (v->transform == 1 && v->boundary != 1)
+        return fail(PRNU_BAD_PARAMETER, "the undecimated transform is circular: boundary must be 1");
+    return PRNU_OK;
+}
+static size_t variant_ws(int batch, int H, int W, const prnu_denoise_params* p, const prnu_denoise_variant* v) {
+    return variant_workspace_bytes(batch, H, W, p->levels, v->taps, v->boundary, v->transform) +
+           zm_workspace_bytes(H, W);
+}
 
 static size_t residual_ws(int batch, int H, int W, const Pyramid& pyr) {
     return align_up(sizeof(float) * pyramid_floats_per_frame(pyr) * (size_t)batch, 256) + zm_workspace_bytes(H, W);
@@ -667,6 +685,41 @@ int prnu_block_match(void* plan, const float* residual, const float* template_, 
 }
 
 int prnu_block_plan_destroy(void* plan) { return block_plan_destroy(plan); }
+
+size_t prnu_residual_variant_workspace_bytes(int batch, int H, int W, const prnu_denoise_params* p,
+                                             const prnu_denoise_variant* v) {
+    if (batch < 1 || H <= 0 || W <= 0 || validate_params(p, H, W, nullptr) || validate_variant(v)) return 0;
+    return variant_ws(batch, H, W, p, v);
+}
+
+int prnu_residual_variant(const float* planes, int batch, int H, int W, const prnu_denoise_params* p,
+                          const prnu_denoise_variant* v, int zero_mean, float* W_out, void* ws, size_t ws_bytes,
+                          void* stream) {
+    int rc;
+    if (!planes || !W_out || !ws) return fail(PRNU_INVALID_ARG, "null pointer");
+    if (batch < 1) return fail(PRNU_INVALID_ARG, "batch must be >= 1");
+    if ((rc = check_dims(H, W))) return rc;
+    ShrinkParams sp;
+    if ((rc = validate_params(p, H, W, &sp))) return rc;
+    if ((rc = validate_variant(v))) return rc;
+    if (ws_bytes < variant_ws(batch, H, W, p, v)) return fail(PRNU_WORKSPACE_TOO_SMALL, "workspace too small");
+    cudaStream_t st = as_stream(stream);
+    if ((rc = run_residual_variant(planes, batch, H, W, p->levels, v->taps, v->boundary, v->transform, sp, W_out,
+                                   reinterpret_cast<float*>(ws), st)))
+        return rc;
+    if (zero_mean) {
+        char* zm = reinterpret_cast<char*>(ws) +
+                   variant_workspace_bytes(batch, H, W, p->levels, v->taps, v->boundary, v->transform);
+        for (int b = 0; b < batch; ++b)
+            if ((rc = launch_zero_mean_f32(W_out + (size_t)b * H * W, H, W, zm, st))) return rc;
+    }
+    return PRNU_OK;
+}
+
+int prnu_wavelet_filter(int taps, double* h_out) {
+    if (!h_out) return fail(PRNU_INVALID_ARG, "null pointer");
+    return variant_filter(taps, h_out);
+}
 
 int prnu_profile_begin(void) {
     std::lock_guard<std::mutex> lk(g_prof_mu);

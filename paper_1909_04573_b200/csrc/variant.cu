@@ -1,0 +1,363 @@
+// variant.cu — f3: the denoiser variants of Q2-Q4 (R-24..R-26).
+//
+//   taps = 16        db8 (8 vanishing moments) instead of the 8-tap filter (Q2)
+//   boundary = 1     pad to a multiple of 2^levels by e_N, periodic DWT, crop (Q4, R-24)
+//   transform = 1    undecimated (stationary) DWT, circular, dilation 2^(l-1) (Q3, R-25)
+//
+// Same method as the default path (decomposition, local-variance Wiener shrink of
+// every detail subband with mirror windows, noise-domain reconstruction
+// W = I - F(I), R-10), built from separable one-dimensional passes:
+//
+//   k_var_ana<T, MODE, AX>   one analysis pass along x (AX = 0) or y (AX = 1)
+//   launch_shrink_strip      split.cu's streaming shrink, reused unchanged
+//   k_var_syn<T, MODE, AX>   one synthesis pass (gather form); a null approximation is zero
+//
+// Filter convention (GPU side; R-5 generalised to T taps): H_ is the
+// minimum-phase lowpass in common.cuh's order (PRNU_H0..7 for T = 8),
+// G_[i] = (-1)^i H_[T-1-i], and
+//   decimated analysis   a[c] = sum_i H_[i] x[map(2c - (T-2) + i)]        (d with G_)
+//   decimated synthesis  x[t] = sum_m H_[e+2m] a[k] + G_[e+2m] d[k],  e = t & 1,
+//                        k = (t-e)/2 + (T-2)/2 - m: dropped outside [0, n) for the
+//                        symmetric transform, taken mod n for the periodic one (its
+//                        synthesis is the transpose of its orthogonal analysis)
+//   undecimated          a[t] = sum_i H_[i] x[(t - s (T-1-i)) mod N],
+//                        x[t] = 1/2 sum_i H_[i] a[(t + s (T-1-i)) mod N] + G_[i] d[...]
+// The passes are gathers, one thread per output, coalesced along x; they are
+// HBM/L2-bound (algorithmic bytes in DESIGN.md §6).
+#include "common.cuh"
+
+namespace prnu {
+
+// db8: Daubechies, "Ten Lectures on Wavelets" (1992), Table 6.1, N = 8, normalised
+// to sum sqrt(2), minimum-phase order.  8 taps: common.cuh's PRNU_H0..7.
+#define PRNU_DB8                                                                                             \
+    0.05441584224308161, 0.3128715909144659, 0.6756307362980128, 0.5853546836548691, -0.015829105256023893,  \
+        -0.2840155429624281, 0.00047248457399797254, 0.128747426620186, -0.01736930100202211,               \
+        -0.04408825393106472, 0.013981027917015516, 0.008746094047015655, -0.00487035299301066,             \
+        -0.0003917403729959771, 0.0006754494059985568, -0.00011747678400228192
+static constexpr double kDb8[16] = {PRNU_DB8};
+__constant__ float c_var_h[2][16] = {
+    {PRNU_H0, PRNU_H1, PRNU_H2, PRNU_H3, PRNU_H4, PRNU_H5, PRNU_H6, PRNU_H7, 0, 0, 0, 0, 0, 0, 0, 0},
+    {(float)kDb8[0], (float)kDb8[1], (float)kDb8[2], (float)kDb8[3], (float)kDb8[4], (float)kDb8[5],
+     (float)kDb8[6], (float)kDb8[7], (float)kDb8[8], (float)kDb8[9], (float)kDb8[10], (float)kDb8[11],
+     (float)kDb8[12], (float)kDb8[13], (float)kDb8[14], (float)kDb8[15]}};
+
+enum VarMode { VM_SYM = 0, VM_PER = 1, VM_SWT = 2 };
+
+__device__ __forceinline__ int var_mod(int i, int n) {
+    const int r = i % n;
+    return r < 0 ? r + n : r;
+}
+// where analysis input sample i of a length-N axis comes from (R-4, R-24, R-25)
+template <int MODE>
+__device__ __forceinline__ int var_map(int i, int N, int Np) {
+    if (MODE == VM_SYM) return mirror(i, N);
+    if (MODE == VM_PER) {
+        const int r = var_mod(i, Np);       // periodic over the padded length Np ...
+        return r < N ? r : mirror(r, N);    // ... whose samples beyond N mirror the plane
+    }
+    return var_mod(i, N);
+}
+
+struct VarPass {
+    const float* in[4];   // analysis: plane pl reads in[pl]; synthesis: (in[2pl], in[2pl+1]) = (a, d)
+    float* out[4];        // analysis: plane pl writes (out[2pl], out[2pl+1]) = (lo, hi); synthesis: out[pl]
+    long long in_bstride, out_bstride;   // floats between frames
+    int in_pitch, out_pitch;             // floats between rows
+    int N, Np;     // analysis: real / periodic length of the input axis; synthesis: n (coefficients)
+    int nout;      // outputs along the axis
+    int other;     // extent along the other axis
+    int s;         // undecimated dilation 2^(l-1)
+    int nplanes;
+};
+
+template <int AX>
+__device__ __forceinline__ size_t var_at(int k, int o, int pitch) {
+    return AX == 0 ? (size_t)o * pitch + k : (size_t)k * pitch + o;
+}
+
+// grid: x over the x extent (128 per CTA), y over the y extent, z = frame * nplanes + plane
+template <int T, int MODE, int AX>
+__global__ void __launch_bounds__(128) k_var_ana(VarPass p) {
+    const int pl = blockIdx.z % p.nplanes, b = blockIdx.z / p.nplanes;
+    const int x = blockIdx.x * 128 + threadIdx.x, y = blockIdx.y;
+    const int k = AX == 0 ? x : y, o = AX == 0 ? y : x;
+    if (k >= p.nout || o >= p.other) return;
+    const float* in = p.in[pl] + (size_t)b * p.in_bstride;
+    const float* H = c_var_h[T == 16];
+    float a = 0.f, d = 0.f;
+#pragma unroll
+    for (int i = 0; i < T; ++i) {
+        const int src = MODE == VM_SWT ? k - p.s * (T - 1 - i) : 2 * k - (T - 2) + i;
+        const float v = in[var_at<AX>(var_map<MODE>(src, p.N, p.Np), o, p.in_pitch)];
+        const float g = (i & 1) ? -H[T - 1 - i] : H[T - 1 - i];
+        a = fmaf(H[i], v, a);
+        d = fmaf(g, v, d);
+    }
+    const size_t oi = (size_t)b * p.out_bstride + var_at<AX>(k, o, p.out_pitch);
+    p.out[2 * pl][oi] = a;
+    p.out[2 * pl + 1][oi] = d;
+}
+
+template <int T, int MODE, int AX>
+__global__ void __launch_bounds__(128) k_var_syn(VarPass p) {
+    const int pl = blockIdx.z % p.nplanes, b = blockIdx.z / p.nplanes;
+    const int x = blockIdx.x * 128 + threadIdx.x, y = blockIdx.y;
+    const int t = AX == 0 ? x : y, o = AX == 0 ? y : x;
+    if (t >= p.nout || o >= p.other) return;
+    const float* A = p.in[2 * pl] ? p.in[2 * pl] + (size_t)b * p.in_bstride : nullptr;   // null: zero approximation
+    const float* D = p.in[2 * pl + 1] + (size_t)b * p.in_bstride;
+    const float* H = c_var_h[T == 16];
+    const int n = p.N;
+    float acc = 0.f;
+    if (MODE == VM_SWT) {
+#pragma unroll
+        for (int i = 0; i < T; ++i) {
+            const size_t at = var_at<AX>(var_mod(t + p.s * (T - 1 - i), n), o, p.in_pitch);
+            const float g = (i & 1) ? -H[T - 1 - i] : H[T - 1 - i];
+            if (A) acc = fmaf(H[i], A[at], acc);
+            acc = fmaf(g, D[at], acc);
+        }
+        acc *= 0.5f;
+    } else {
+        const int e = t & 1, base = (t - e) / 2 + (T - 2) / 2;
+#pragma unroll
+        for (int m = 0; m < T / 2; ++m) {
+            int k = base - m;
+            if (MODE == VM_SYM) {
+                if (k < 0 || k >= n) continue;
+            } else {
+                k = var_mod(k, n);
+            }
+            const int f = e + 2 * m;
+            const float g = e ? -H[T - 1 - f] : H[T - 1 - f];
+            const size_t at = var_at<AX>(k, o, p.in_pitch);
+            if (A) acc = fmaf(H[f], A[at], acc);
+            acc = fmaf(g, D[at], acc);
+        }
+    }
+    p.out[pl][(size_t)b * p.out_bstride + var_at<AX>(t, o, p.out_pitch)] = acc;
+}
+
+template <int T, int MODE>
+static void var_launch(bool syn, int ax, const VarPass& p, int nb, cudaStream_t st) {
+    const int ex = ax == 0 ? p.nout : p.other, ey = ax == 0 ? p.other : p.nout;
+    const dim3 grid((unsigned)((ex + 127) / 128), (unsigned)ey, (unsigned)(nb * p.nplanes));
+    if (syn) {
+        if (ax == 0) k_var_syn<T, MODE, 0><<<grid, 128, 0, st>>>(p);
+        else k_var_syn<T, MODE, 1><<<grid, 128, 0, st>>>(p);
+    } else {
+        if (ax == 0) k_var_ana<T, MODE, 0><<<grid, 128, 0, st>>>(p);
+        else k_var_ana<T, MODE, 1><<<grid, 128, 0, st>>>(p);
+    }
+}
+
+static void var_dispatch(int taps, int mode, bool syn, int ax, const VarPass& p, int nb, cudaStream_t st) {
+    if (taps == 8) {
+        if (mode == VM_SYM) var_launch<8, VM_SYM>(syn, ax, p, nb, st);
+        else if (mode == VM_PER) var_launch<8, VM_PER>(syn, ax, p, nb, st);
+        else var_launch<8, VM_SWT>(syn, ax, p, nb, st);
+    } else {
+        if (mode == VM_SYM) var_launch<16, VM_SYM>(syn, ax, p, nb, st);
+        else if (mode == VM_PER) var_launch<16, VM_PER>(syn, ax, p, nb, st);
+        else var_launch<16, VM_SWT>(syn, ax, p, nb, st);
+    }
+}
+
+// ------------------------------------------------------------------ geometry / workspace
+struct VarGeom {
+    int T, mode, L;
+    int H, W;
+    int inH[8], inW[8];     // real input extent of level l (l = 1..L)
+    int perH[8], perW[8];   // period of the level's input (== real except padded level 1)
+    int nH[8], nW[8];       // subband extent of level l
+    size_t sub_off[8];      // offset of level l's three noise planes (floats, per frame)
+    size_t scratch, approx, noise;   // floats per frame: one scratch plane, one approximation plane, all noise
+};
+
+static VarGeom var_geom(int H, int W, int levels, int taps, int boundary, int transform) {
+    VarGeom g{};
+    g.T = taps;
+    g.mode = transform ? VM_SWT : boundary ? VM_PER : VM_SYM;
+    g.L = levels;
+    g.H = H;
+    g.W = W;
+    const int m = 1 << levels;
+    int h = H, w = W;
+    size_t off = 0;
+    for (int l = 1; l <= levels; ++l) {
+        g.inH[l] = h;
+        g.inW[l] = w;
+        g.perH[l] = (g.mode == VM_PER && l == 1) ? (H + m - 1) / m * m : h;
+        g.perW[l] = (g.mode == VM_PER && l == 1) ? (W + m - 1) / m * m : w;
+        if (g.mode == VM_SWT) {
+            g.nH[l] = h;
+            g.nW[l] = w;
+        } else if (g.mode == VM_PER) {
+            g.nH[l] = g.perH[l] / 2;
+            g.nW[l] = g.perW[l] / 2;
+        } else {
+            g.nH[l] = (h + taps - 1) / 2;
+            g.nW[l] = (w + taps - 1) / 2;
+        }
+        g.sub_off[l] = off;
+        off += 3 * (size_t)g.nH[l] * g.nW[l];
+        h = g.nH[l];
+        w = g.nW[l];
+    }
+    g.noise = off;
+    size_t sc = 0, ap = 0;
+    for (int l = 1; l <= levels; ++l) {
+        sc = std::max(sc, (size_t)std::max(g.inH[l], g.perH[l]) * g.nW[l]);
+        ap = std::max(ap, (size_t)g.nH[l] * g.nW[l]);
+    }
+    g.scratch = align_up(sc, 64);
+    g.approx = align_up(ap, 64);
+    g.noise = align_up(g.noise, 64);
+    return g;
+}
+
+// per frame: 2 scratch + 2 approximation (ping-pong) + 3 raw details + all noise planes
+static size_t var_floats_per_frame(const VarGeom& g) { return 2 * g.scratch + 5 * g.approx + g.noise; }
+
+size_t variant_workspace_bytes(int batch, int H, int W, int levels, int taps, int boundary, int transform) {
+    const VarGeom g = var_geom(H, W, levels, taps, boundary, transform);
+    return align_up(sizeof(float) * var_floats_per_frame(g) * (size_t)batch, 256);
+}
+
+int variant_filter(int taps, double* h) {
+    if (taps == 8) {
+        const float h8[8] = {PRNU_H0, PRNU_H1, PRNU_H2, PRNU_H3, PRNU_H4, PRNU_H5, PRNU_H6, PRNU_H7};
+        for (int i = 0; i < 8; ++i) h[i] = h8[i];
+        return PRNU_OK;
+    }
+    if (taps == 16) {
+        for (int i = 0; i < 16; ++i) h[i] = (double)(float)kDb8[i];
+        return PRNU_OK;
+    }
+    return fail(PRNU_BAD_PARAMETER, "taps must be 8 or 16");
+}
+
+int run_residual_variant(const float* in, int nb, int H, int W, int levels, int taps, int boundary, int transform,
+                         const ShrinkParams& sp, float* W_out, float* ws, cudaStream_t st) {
+    const VarGeom g = var_geom(H, W, levels, taps, boundary, transform);
+    // each buffer holds nb frames; a plane of level l is stored densely, frame stride
+    // nH_l nW_l (the buffers are sized for level 1, the largest)
+    float* X[2] = {ws, ws + g.scratch * nb};
+    float* A[2] = {ws + 2 * g.scratch * nb, ws + (2 * g.scratch + g.approx) * nb};
+    float* R[3] = {A[1] + g.approx * nb, A[1] + 2 * g.approx * nb, A[1] + 3 * g.approx * nb};
+    float* NZ = A[1] + 4 * g.approx * nb;
+    auto noise = [&](int l, int k) { return NZ + (g.sub_off[l] + (size_t)k * g.nH[l] * g.nW[l]) * nb; };
+    int rc;
+    const float* cur = in;
+    long long cur_bs = (long long)H * W;
+    int cur_pitch = W;
+    for (int l = 1; l <= levels; ++l) {
+        const int s = 1 << (l - 1);
+        const int nHl = g.nH[l], nWl = g.nW[l];
+        {   // rows: cur [inH][inW] -> X0 = lo_x, X1 = hi_x  [inH][nW]
+            VarPass p{};
+            p.in[0] = cur;
+            p.out[0] = X[0];
+            p.out[1] = X[1];
+            p.in_bstride = cur_bs;
+            p.in_pitch = cur_pitch;
+            p.out_bstride = (long long)g.scratch;
+            p.out_pitch = nWl;
+            p.N = g.inW[l];
+            p.Np = g.perW[l];
+            p.nout = nWl;
+            p.other = g.inH[l];
+            p.s = s;
+            p.nplanes = 1;
+            KTimer kt("variant_ana_x", st);
+            var_dispatch(taps, g.mode, false, 0, p, nb, st);
+        }
+        count_launch();
+        if ((rc = check_launch("k_var_ana (x)"))) return rc;
+        {   // columns: X0 -> (aa, ad), X1 -> (da, dd)   [nH][nW]
+            VarPass p{};
+            p.in[0] = X[0];
+            p.in[1] = X[1];
+            p.out[0] = A[l & 1];
+            p.out[1] = R[1];
+            p.out[2] = R[0];
+            p.out[3] = R[2];
+            p.in_bstride = (long long)g.scratch;
+            p.in_pitch = nWl;
+            p.out_bstride = (long long)nHl * nWl;
+            p.out_pitch = nWl;
+            p.N = g.inH[l];
+            p.Np = g.perH[l];
+            p.nout = nHl;
+            p.other = nWl;
+            p.s = s;
+            p.nplanes = 2;
+            KTimer kt("variant_ana_y", st);
+            var_dispatch(taps, g.mode, false, 1, p, nb, st);
+        }
+        count_launch();
+        if ((rc = check_launch("k_var_ana (y)"))) return rc;
+        {   // shrink: raw (da, ad, dd) -> noise-domain planes of level l (R-10)
+            const float* src[3] = {R[0], R[1], R[2]};
+            float* dst[3] = {noise(l, 0), noise(l, 1), noise(l, 2)};
+            KTimer kt("variant_shrink", st);
+            if ((rc = launch_shrink_strip(src, dst, (long long)nHl * nWl, nWl, nHl, nWl, sp, nb, st))) return rc;
+        }
+        count_launch();
+        if ((rc = check_launch("k_shrink (variant)"))) return rc;
+        cur = A[l & 1];
+        cur_bs = (long long)nHl * nWl;
+        cur_pitch = nWl;
+    }
+    for (int l = levels; l >= 1; --l) {
+        const int s = 1 << (l - 1);
+        const int nHl = g.nH[l], nWl = g.nW[l];
+        const int outH = l == 1 ? H : g.inH[l], outW = l == 1 ? W : g.inW[l];
+        const float* approx = l == levels ? nullptr : A[l & 1];
+        {   // columns: (approx, ad) -> X0, (da, dd) -> X1   [outH][nW]
+            VarPass p{};
+            p.in[0] = approx;
+            p.in[1] = noise(l, 1);
+            p.in[2] = noise(l, 0);
+            p.in[3] = noise(l, 2);
+            p.out[0] = X[0];
+            p.out[1] = X[1];
+            p.in_bstride = (long long)nHl * nWl;
+            p.in_pitch = nWl;
+            p.out_bstride = (long long)g.scratch;
+            p.out_pitch = nWl;
+            p.N = nHl;
+            p.nout = outH;
+            p.other = nWl;
+            p.s = s;
+            p.nplanes = 2;
+            KTimer kt("variant_syn_y", st);
+            var_dispatch(taps, g.mode, true, 1, p, nb, st);
+        }
+        count_launch();
+        if ((rc = check_launch("k_var_syn (y)"))) return rc;
+        {   // rows: (X0, X1) -> approx of level l-1 (or W at l = 1)   [outH][outW]
+            VarPass p{};
+            p.in[0] = X[0];
+            p.in[1] = X[1];
+            p.out[0] = l == 1 ? W_out : A[(l - 1) & 1];
+            p.in_bstride = (long long)g.scratch;
+            p.in_pitch = nWl;
+            p.out_bstride = l == 1 ? (long long)H * W : (long long)outH * outW;
+            p.out_pitch = outW;
+            p.N = nWl;
+            p.nout = outW;
+            p.other = outH;
+            p.s = s;
+            p.nplanes = 1;
+            KTimer kt("variant_syn_x", st);
+            var_dispatch(taps, g.mode, true, 0, p, nb, st);
+        }
+        count_launch();
+        if ((rc = check_launch("k_var_syn (x)"))) return rc;
+    }
+    return PRNU_OK;
+}
+
+}  // namespace prnu

@@ -67,3 +67,27 @@ def test_workspace_queries():
     assert L.prnu_extract_workspace_bytes(1080, 1920, 16, 50, ctypes.byref(p)) > \
         L.prnu_extract_workspace_bytes(1080, 1920, 16, 1, ctypes.byref(p))
     assert L.prnu_residual_workspace_bytes(1, 8, 8, ctypes.byref(p)) == 0   # 8 < 2^4
+
+
+def test_variant_filters_match_oracle_factorisation():
+    """f3: the library's 8- and 16-tap lowpass (fp32 constants, host call) equal the
+    oracle's spectral factorisation (minimum-phase order = reversed dec_lo) to fp32 rounding."""
+    import numpy as np
+    from oracle import variants as V
+    for taps, p in ((8, 4), (16, 8)):
+        got = np.array(prnu.wavelet_filter(taps))
+        ref = V.daubechies(p)[::-1]
+        assert np.abs(got - ref.astype(np.float32).astype(np.float64)).max() == 0.0, taps
+    with pytest.raises(prnu.PrnuError) as e:
+        prnu.wavelet_filter(12)
+    assert e.value.code == 4
+
+
+def test_variant_validation_host():
+    """Variant fields are validated before any launch (workspace query returns 0)."""
+    p = prnu.DenoiseParams().c()
+    for v, ok in (((8, 0, 0), True), ((16, 1, 0), True), ((8, 1, 1), True), ((16, 1, 1), True),
+                  ((12, 0, 0), False), ((8, 2, 0), False), ((8, 0, 1), False), ((8, 0, 2), False)):
+        vv = prnu.DenoiseVariant(*v).c()
+        n = prnu._lib.prnu_residual_variant_workspace_bytes(2, 64, 96, ctypes.byref(p), ctypes.byref(vv))
+        assert (n > 0) == ok, v
