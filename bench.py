@@ -235,6 +235,34 @@ def run_reference(args, rank, world):
 
 
 # ------------------------------------------------------------------ main arm
+def variant_alg_bytes(H, W, levels, taps, boundary, transform):
+    """Algorithmic HBM bytes of one f3 variant residual (csrc/variant.cu): every pass reads
+    its input planes once and writes its outputs once (fp32)."""
+    m = 1 << levels
+    h, w = H, W
+    tot = 0
+    dims = []
+    for l in range(1, levels + 1):
+        ph = (h + m - 1) // m * m if (boundary and not transform and l == 1) else h
+        pw = (w + m - 1) // m * m if (boundary and not transform and l == 1) else w
+        if transform:
+            nh, nw = h, w
+        elif boundary:
+            nh, nw = ph // 2, pw // 2
+        else:
+            nh, nw = (h + taps - 1) // 2, (w + taps - 1) // 2
+        dims.append((h, w, nh, nw))
+        tot += h * w + 2 * h * nw            # rows pass
+        tot += 2 * h * nw + 4 * nh * nw      # columns pass
+        tot += 6 * nh * nw                   # shrink (3 in, 3 out)
+        h, w = nh, nw
+    for l in range(levels, 0, -1):
+        ih, iw, nh, nw = dims[l - 1]
+        tot += (3 if l == levels else 4) * nh * nw + 2 * ih * nw   # synthesis columns
+        tot += 2 * ih * nw + ih * iw                               # synthesis rows
+    return 4 * tot
+
+
 def main():
     args = parse()
     rank, world, local = dist_setup(args)
@@ -382,7 +410,18 @@ def main():
         luma_bytes = 16 * H * W * (3 + 4)
         pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
         peak_hbm = json.load(open(pk)).get("hbm_gbs", 6650.0) if os.path.exists(pk) else 6650.0
-        next_rows = {"f2_wdft_ms_per_fingerprint": t_wdft / len(depths),
+        # f3 denoiser variants: residual of 8 FHD SDA-like fp32 frames per call
+        Ivar = frames[:8].float()
+        f3 = {}
+        for name, v in (("db8_sym", (16, 0, 0)), ("db4_per", (8, 1, 0)), ("db8_per", (16, 1, 0)),
+                        ("db4_swt", (8, 1, 1)), ("db8_swt", (16, 1, 1))):
+            var = prnu.DenoiseVariant(*v)
+            out = torch.empty_like(Ivar)
+            t = timed(lambda: prnu.residual_variant(Ivar, var, out=out), reps=3)
+            gb = variant_alg_bytes(H, W, 4, *v) * Ivar.shape[0] / (t / 1000.0) / 1e9
+            f3[name] = {"ms_per_frame": t / Ivar.shape[0], "alg_GBps": gb}
+        next_rows = {"f3_variants": f3,
+                     "f2_wdft_ms_per_fingerprint": t_wdft / len(depths),
                      "f1_block_match_ms": t_blk, "f1_tiles": bplan.n_tiles,
                      "f4_rgb_to_luma_GBps": luma_bytes / (t_luma / 1000.0) / 1e9,
                      "f4_rgb_to_luma_frac_hbm": luma_bytes / (t_luma / 1000.0) / 1e9 / peak_hbm}

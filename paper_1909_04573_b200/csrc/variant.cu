@@ -76,47 +76,118 @@ __device__ __forceinline__ size_t var_at(int k, int o, int pitch) {
     return AX == 0 ? (size_t)o * pitch + k : (size_t)k * pitch + o;
 }
 
-// grid: x over the x extent (128 per CTA), y over the y extent, z = frame * nplanes + plane
+// grid: x over the x extent (128 threads per CTA), y over the y extent in runs of
+// VAR_RY rows per thread (amortises the index set-up and the CTA launch; the rows
+// a run shares hit L1), z = frame * nplanes + plane
+constexpr int VAR_RY = 8;
+
 template <int T, int MODE, int AX>
 __global__ void __launch_bounds__(128) k_var_ana(VarPass p) {
     const int pl = blockIdx.z % p.nplanes, b = blockIdx.z / p.nplanes;
-    const int x = blockIdx.x * 128 + threadIdx.x, y = blockIdx.y;
-    const int k = AX == 0 ? x : y, o = AX == 0 ? y : x;
-    if (k >= p.nout || o >= p.other) return;
+    const int x = blockIdx.x * 128 + threadIdx.x;
+    const int ey = AX == 0 ? p.other : p.nout;
+    if (x >= (AX == 0 ? p.nout : p.other)) return;
     const float* in = p.in[pl] + (size_t)b * p.in_bstride;
+    float* lo = p.out[2 * pl] + (size_t)b * p.out_bstride;
+    float* hi = p.out[2 * pl + 1] + (size_t)b * p.out_bstride;
     const float* H = c_var_h[T == 16];
-    float a = 0.f, d = 0.f;
+    const int y0 = blockIdx.y * VAR_RY, y1 = min(y0 + VAR_RY, ey);
+    if (AX == 1 && MODE != VM_SWT) {
+        // decimated, along y: the run's outputs k0 .. k0+7 read input rows
+        // 2 k0 - (T-2) .. 2 k0 + 15: each loaded once into registers
+        constexpr int NR = 2 * VAR_RY + T - 2;
+        float v[NR];
 #pragma unroll
-    for (int i = 0; i < T; ++i) {
-        const int src = MODE == VM_SWT ? k - p.s * (T - 1 - i) : 2 * k - (T - 2) + i;
-        const float v = in[var_at<AX>(var_map<MODE>(src, p.N, p.Np), o, p.in_pitch)];
-        const float g = (i & 1) ? -H[T - 1 - i] : H[T - 1 - i];
-        a = fmaf(H[i], v, a);
-        d = fmaf(g, v, d);
+        for (int j = 0; j < NR; ++j)
+            v[j] = __ldg(in + var_at<AX>(var_map<MODE>(2 * y0 - (T - 2) + j, p.N, p.Np), x, p.in_pitch));
+#pragma unroll
+        for (int r = 0; r < VAR_RY; ++r) {
+            if (y0 + r >= y1) break;
+            float a = 0.f, d = 0.f;
+#pragma unroll
+            for (int i = 0; i < T; ++i) {
+                const float g = (i & 1) ? -H[T - 1 - i] : H[T - 1 - i];
+                a = fmaf(H[i], v[2 * r + i], a);
+                d = fmaf(g, v[2 * r + i], d);
+            }
+            const size_t oi = var_at<AX>(y0 + r, x, p.out_pitch);
+            lo[oi] = a;
+            hi[oi] = d;
+        }
+        return;
     }
-    const size_t oi = (size_t)b * p.out_bstride + var_at<AX>(k, o, p.out_pitch);
-    p.out[2 * pl][oi] = a;
-    p.out[2 * pl + 1][oi] = d;
+    for (int y = y0; y < y1; ++y) {
+        const int k = AX == 0 ? x : y, o = AX == 0 ? y : x;
+        float a = 0.f, d = 0.f;
+#pragma unroll
+        for (int i = 0; i < T; ++i) {
+            const int src = MODE == VM_SWT ? k - p.s * (T - 1 - i) : 2 * k - (T - 2) + i;
+            const float v = __ldg(in + var_at<AX>(var_map<MODE>(src, p.N, p.Np), o, p.in_pitch));
+            const float g = (i & 1) ? -H[T - 1 - i] : H[T - 1 - i];
+            a = fmaf(H[i], v, a);
+            d = fmaf(g, v, d);
+        }
+        const size_t oi = var_at<AX>(k, o, p.out_pitch);
+        lo[oi] = a;
+        hi[oi] = d;
+    }
 }
 
 template <int T, int MODE, int AX>
 __global__ void __launch_bounds__(128) k_var_syn(VarPass p) {
     const int pl = blockIdx.z % p.nplanes, b = blockIdx.z / p.nplanes;
-    const int x = blockIdx.x * 128 + threadIdx.x, y = blockIdx.y;
-    const int t = AX == 0 ? x : y, o = AX == 0 ? y : x;
-    if (t >= p.nout || o >= p.other) return;
+    const int x = blockIdx.x * 128 + threadIdx.x;
+    const int ey = AX == 0 ? p.other : p.nout;
+    if (x >= (AX == 0 ? p.nout : p.other)) return;
     const float* A = p.in[2 * pl] ? p.in[2 * pl] + (size_t)b * p.in_bstride : nullptr;   // null: zero approximation
     const float* D = p.in[2 * pl + 1] + (size_t)b * p.in_bstride;
+    float* out = p.out[pl] + (size_t)b * p.out_bstride;
     const float* H = c_var_h[T == 16];
     const int n = p.N;
+    const int y0 = blockIdx.y * VAR_RY, y1 = min(y0 + VAR_RY, ey);
+    if (AX == 1 && MODE != VM_SWT) {
+        // decimated, along y: outputs t0 .. t0+7 (t0 even) gather coefficient rows
+        // k = t0/2 .. t0/2 + NK - 1: each loaded once into registers (rows outside
+        // [0, n) are dropped for the symmetric transform, wrapped for the periodic one)
+        constexpr int NK = VAR_RY / 2 + T / 2 - 1;
+        float ca[NK], cd[NK];
+#pragma unroll
+        for (int j = 0; j < NK; ++j) {
+            int k = y0 / 2 + j;
+            bool ok = true;
+            if (MODE == VM_SYM) ok = k < n;
+            else k = var_mod(k, n);
+            const size_t at = var_at<AX>(ok ? k : 0, x, p.in_pitch);
+            ca[j] = (ok && A) ? __ldg(A + at) : 0.f;
+            cd[j] = ok ? __ldg(D + at) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < VAR_RY; ++u) {
+            if (y0 + u >= y1) break;
+            const int e = u & 1;
+            float acc = 0.f;
+#pragma unroll
+            for (int m = 0; m < T / 2; ++m) {
+                const int j = (u - e) / 2 + (T - 2) / 2 - m;   // k - t0/2
+                const int f = e + 2 * m;
+                const float g = e ? -H[T - 1 - f] : H[T - 1 - f];
+                acc = fmaf(H[f], ca[j], acc);
+                acc = fmaf(g, cd[j], acc);
+            }
+            out[var_at<AX>(y0 + u, x, p.out_pitch)] = acc;
+        }
+        return;
+    }
+    for (int y = y0; y < y1; ++y) {
+    const int t = AX == 0 ? x : y, o = AX == 0 ? y : x;
     float acc = 0.f;
     if (MODE == VM_SWT) {
 #pragma unroll
         for (int i = 0; i < T; ++i) {
             const size_t at = var_at<AX>(var_mod(t + p.s * (T - 1 - i), n), o, p.in_pitch);
             const float g = (i & 1) ? -H[T - 1 - i] : H[T - 1 - i];
-            if (A) acc = fmaf(H[i], A[at], acc);
-            acc = fmaf(g, D[at], acc);
+            if (A) acc = fmaf(H[i], __ldg(A + at), acc);
+            acc = fmaf(g, __ldg(D + at), acc);
         }
         acc *= 0.5f;
     } else {
@@ -132,17 +203,18 @@ __global__ void __launch_bounds__(128) k_var_syn(VarPass p) {
             const int f = e + 2 * m;
             const float g = e ? -H[T - 1 - f] : H[T - 1 - f];
             const size_t at = var_at<AX>(k, o, p.in_pitch);
-            if (A) acc = fmaf(H[f], A[at], acc);
-            acc = fmaf(g, D[at], acc);
+            if (A) acc = fmaf(H[f], __ldg(A + at), acc);
+            acc = fmaf(g, __ldg(D + at), acc);
         }
     }
-    p.out[pl][(size_t)b * p.out_bstride + var_at<AX>(t, o, p.out_pitch)] = acc;
+    out[var_at<AX>(t, o, p.out_pitch)] = acc;
+    }
 }
 
 template <int T, int MODE>
 static void var_launch(bool syn, int ax, const VarPass& p, int nb, cudaStream_t st) {
     const int ex = ax == 0 ? p.nout : p.other, ey = ax == 0 ? p.other : p.nout;
-    const dim3 grid((unsigned)((ex + 127) / 128), (unsigned)ey, (unsigned)(nb * p.nplanes));
+    const dim3 grid((unsigned)((ex + 127) / 128), (unsigned)((ey + VAR_RY - 1) / VAR_RY), (unsigned)(nb * p.nplanes));
     if (syn) {
         if (ax == 0) k_var_syn<T, MODE, 0><<<grid, 128, 0, st>>>(p);
         else k_var_syn<T, MODE, 1><<<grid, 128, 0, st>>>(p);
