@@ -449,6 +449,30 @@ def extract_fingerprint_stride(frames: torch.Tensor, stride: int, params: Denois
 prnu_extract_fingerprint_stride = extract_fingerprint_stride
 
 
+def extract_fingerprint_variant(frames: torch.Tensor, depth: int, variant: DenoiseVariant,
+                                params: DenoiseParams | None = None, batch: int = 16,
+                                eps: float = 1e-6) -> Fingerprint:
+    """f3: the fingerprint pipeline (SDA average, denoise, MLE, finalize) with a
+    denoiser variant, composed from the C-ABI calls prnu_sda_average ->
+    prnu_residual_variant -> prnu_fingerprint_accumulate (ascending group order) ->
+    prnu_fingerprint_finalize, one wave of `batch` SDA frames at a time."""
+    _dev(frames, torch.uint8, "frames", (3,))
+    m, H, W = frames.shape
+    n_s = sda_groups(m, depth)
+    s_wi = torch.zeros((H, W), dtype=torch.float64, device=frames.device)
+    s_i2 = torch.zeros_like(s_wi)
+    Wbuf = None
+    for g0 in range(0, n_s, batch):
+        g1 = min(g0 + batch, n_s)
+        S = sda_average(frames[g0 * depth: g1 * depth], depth)
+        if Wbuf is None or Wbuf.shape[0] != S.shape[0]:
+            Wbuf = torch.empty_like(S)
+        residual_variant(S, variant, params, out=Wbuf)
+        fingerprint_accumulate(Wbuf, S, s_wi, s_i2)
+    K = fingerprint_finalize(s_wi, s_i2, eps)
+    return Fingerprint(K, s_wi, s_i2, n_s, depth, m)
+
+
 # ---------------------------------------------------------------- a7-a8
 def ncc(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
     """Aligned Pearson correlation per plane (R-16), fp64 [batch] (or 0-dim)."""

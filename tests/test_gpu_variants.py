@@ -109,3 +109,24 @@ def test_variant_full_hd(prnu, v, kw):
     I = _textured(1, 1080, 1920, 77)
     got = prnu.residual_variant(torch.from_numpy(I).cuda(), prnu.DenoiseVariant(*v)).cpu().numpy()[0]
     assert np.abs(got - V.residual(I[0], **kw)).max() <= W_TOL
+
+
+@pytest.mark.parametrize("v,kw", [VARIANTS[0], VARIANTS[3], VARIANTS[5]], ids=[IDS[0], IDS[3], IDS[5]])
+@pytest.mark.parametrize("depth", [1, 4])
+def test_variant_fingerprint_matches_oracle(prnu, v, kw, depth):
+    """f3 fingerprint (SDA -> variant residual -> MLE -> finalize) vs the oracle's
+    composition of the same steps; R-14 metric <= 1e-3 (as the default path)."""
+    import oracle
+    g = torch.Generator().manual_seed(5 + depth)
+    fr = torch.randint(20, 236, (16, 64, 80), generator=g, dtype=torch.uint8)
+    fp = prnu.extract_fingerprint_variant(fr.cuda(), depth, prnu.DenoiseVariant(*v), batch=3)
+    S = oracle.sda_average(fr.numpy(), depth)
+    num = np.zeros((64, 80))
+    den = np.zeros((64, 80))
+    for i in range(S.shape[0]):
+        oracle.mle_accumulate(V.residual(S[i], **kw), S[i], num, den)
+    K = oracle.finalize(num, den)
+    assert fp.n_sda == S.shape[0]
+    np.testing.assert_array_equal(fp.sum_I2.cpu().numpy(), den)     # exact fp64 sums of exact products
+    d = np.abs(fp.K.cpu().numpy().astype(np.float64) - K)
+    assert float((d * np.sqrt(den / S.shape[0])).max()) <= W_TOL
