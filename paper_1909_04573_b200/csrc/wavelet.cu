@@ -803,10 +803,16 @@ __global__ void __launch_bounds__(256, MODE == 0 ? 3 : PRNU_SYNTH_ACC_MINB) k_sy
 //     sequential fp64 sum, every partial sum being an integer < 2^53).
 // Per-pixel order is ascending frame order, as in k_synth_tma<1>.
 constexpr int SA_STAGE_COEF = 4 * SC_PS;           // floats per stage (4 planes)
+#ifndef PRNU_SACC_VEC
+#define PRNU_SACC_VEC 1   // row pass reads its 7 L/H values with two LDS.128 (pitch 40); 0: scalar, pitch 37
+#endif
+// L/H plane pitch: 40 == 8 mod 32 makes the row pass's LDS.128 (8 lanes: rows 4w+(l&3),
+// columns 4 (l>>2)) conflict-free; the column pass stores consecutive columns (any pitch)
+constexpr int SA_LP = PRNU_SACC_VEC ? 40 : SL_P;
 template <int TY, typename TI, int MODE = 1>
 constexpr size_t sacc_smem_bytes() {
     return 2 * SA_STAGE_COEF * sizeof(float) + (MODE ? 3 * TY * ST_X * sizeof(TI) : 0) +
-           2 * 2 * TY * SL_P * sizeof(float) + 2 * sizeof(uint64_t);
+           2 * 2 * TY * SA_LP * sizeof(float) + 2 * sizeof(uint64_t);
 }
 
 // MODE 1: accumulate (frames 0 .. nb-1, one CTA per tile); MODE 0: plain inverse
@@ -825,8 +831,8 @@ __global__ void __launch_bounds__(256, PRNU_SACC_MINB) k_synth_acc2(const __grid
     // pass): frame f+2 is issued at the barrier of frame f, two frames ahead.
     float* coef0 = smem;                                                      // [2][4][SC_PS]
     TI* itile0 = reinterpret_cast<TI*>(smem + 2 * SA_STAGE_COEF);             // [3][TY][ST_X] (MODE 1)
-    float* sL0 = reinterpret_cast<float*>(itile0 + (MODE ? 3 * TY * ST_X : 0));   // [2][2][TY][SL_P]
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sL0 + 2 * 2 * TY * SL_P);
+    float* sL0 = reinterpret_cast<float*>(itile0 + (MODE ? 3 * TY * ST_X : 0));   // [2][2][TY][SA_LP]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sL0 + 2 * 2 * TY * SA_LP);
     const int tid = threadIdx.x;
     const int ty0 = blockIdx.y * TY, tx0 = blockIdx.x * ST_X;
     const int ky0 = ty0 >> 1, kx0 = tx0 >> 1;
@@ -879,17 +885,22 @@ __global__ void __launch_bounds__(256, PRNU_SACC_MINB) k_synth_acc2(const __grid
 #pragma unroll
         for (int k = 0; k < 8; ++k) den_d[k] = (rowok && gx + k < a.NW) ? a.den[(size_t)gy * a.acc_pitch + gx + k] : 0.0;
     }
+    // column-pass items (frame-invariant): item it = (coefficient column k, output rows 4 sg .. 4 sg + 3);
+    // with at most one item per thread (TY <= 28) it is computed once here
+    constexpr int NITEM = SC_X * (TY / 4);
+    auto item_k = [](int it) { return it < 32 * (TY / 4) ? (it & 31) : 32 + (it - 32 * (TY / 4)) % (SC_X - 32); };
+    auto item_sg = [](int it) { return it < 32 * (TY / 4) ? (it >> 5) : (it - 32 * (TY / 4)) / (SC_X - 32); };
+    const int ck = item_k(tid), csg = item_sg(tid);
 
     for (int f = 0; f < nb; ++f) {
         const int st = f & 1;
         mbar_wait(&bar[st], (f >> 1) & 1);
         const float* c = coef0 + st * SA_STAGE_COEF;
-        float* sLo = sL0 + (f & 1) * 2 * TY * SL_P;
-        float* sHi = sLo + TY * SL_P;
+        float* sLo = sL0 + (f & 1) * 2 * TY * SA_LP;
+        float* sHi = sLo + TY * SA_LP;
         // column pass: Lx = synth_y(A, ad), Hx = synth_y(da, dd); item = (coefficient column k, 4 output rows)
-        for (int it = tid; it < SC_X * (TY / 4); it += 256) {
-            const int k = it < 32 * (TY / 4) ? (it & 31) : 32 + (it - 32 * (TY / 4)) % (SC_X - 32);
-            const int sg = it < 32 * (TY / 4) ? (it >> 5) : (it - 32 * (TY / 4)) / (SC_X - 32);
+        for (int it = tid; it < NITEM; it += 256) {
+            const int k = NITEM <= 256 ? ck : item_k(it), sg = NITEM <= 256 ? csg : item_sg(it);
             float va[5], vda[5], vad[5], vdd[5];
 #pragma unroll
             for (int m = 0; m < 5; ++m) {
@@ -912,10 +923,10 @@ __global__ void __launch_bounds__(256, PRNU_SACC_MINB) k_synth_acc2(const __grid
                     h = ffma2(vdd[q + m], c_sg[m], h);
                 }
                 const int t = 4 * sg + 2 * q;
-                sLo[t * SL_P + k] = l.x;
-                sLo[(t + 1) * SL_P + k] = l.y;
-                sHi[t * SL_P + k] = h.x;
-                sHi[(t + 1) * SL_P + k] = h.y;
+                sLo[t * SA_LP + k] = l.x;
+                sLo[(t + 1) * SA_LP + k] = l.y;
+                sHi[t * SA_LP + k] = h.x;
+                sHi[(t + 1) * SA_LP + k] = h.y;
             }
         }
         __syncthreads();   // L/H planes of frame f complete; every thread is past frame f-1
@@ -925,12 +936,22 @@ __global__ void __launch_bounds__(256, PRNU_SACC_MINB) k_synth_acc2(const __grid
         }
         if (!rowact) continue;
         // row pass of 8 pixels + accumulation
-        float vl[7], vh[7];
+        float vl[8], vh[8];
+#if PRNU_SACC_VEC
+        {   // columns 4 rg .. 4 rg + 7 (the 8th unused): two LDS.128 per plane
+            const float4* pl = reinterpret_cast<const float4*>(sLo + rt * SA_LP + 4 * rg);
+            const float4* ph = reinterpret_cast<const float4*>(sHi + rt * SA_LP + 4 * rg);
+            const float4 l0 = pl[0], l1 = pl[1], h0 = ph[0], h1 = ph[1];
+            vl[0] = l0.x; vl[1] = l0.y; vl[2] = l0.z; vl[3] = l0.w; vl[4] = l1.x; vl[5] = l1.y; vl[6] = l1.z; vl[7] = l1.w;
+            vh[0] = h0.x; vh[1] = h0.y; vh[2] = h0.z; vh[3] = h0.w; vh[4] = h1.x; vh[5] = h1.y; vh[6] = h1.z; vh[7] = h1.w;
+        }
+#else
 #pragma unroll
         for (int m = 0; m < 7; ++m) {
-            vl[m] = sLo[rt * SL_P + 4 * rg + m];
-            vh[m] = sHi[rt * SL_P + 4 * rg + m];
+            vl[m] = sLo[rt * SA_LP + 4 * rg + m];
+            vh[m] = sHi[rt * SA_LP + 4 * rg + m];
         }
+#endif
         float w[8];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
