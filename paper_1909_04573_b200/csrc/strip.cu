@@ -677,11 +677,13 @@ static int strip_launch(const T* in, long long in_bstride, int in_pitch, int NH,
     a.O = (int)align_up((size_t)((nW + S0 - 1) / S0), 8);
     const int S = (nW + a.O - 1) / a.O;
     static const int sh_env = getenv("PRNU_STRIP_SH") ? atoi(getenv("PRNU_STRIP_SH")) : 0;
-    // segments of ~184 rows (prologue overhead ~4%), more of them while the grid
-    // holds fewer than 6 waves of 3 CTAs/SM (small planes; measured, profiles/r01)
-    static const int seg_rows = getenv("PRNU_STRIP_SEGROWS") ? atoi(getenv("PRNU_STRIP_SEGROWS")) : 184;
+    // segments of <= 300 rows (prologue overhead <= 3%), more of them while the grid
+    // holds fewer than 6 (u8, level 1) / 1 (fp32, levels >= 2 and SDA frames) waves of
+    // 3 CTAs/SM: the fp32 levels of one wave overlap the other streams' work, so fewer,
+    // longer segments win there (interleaved A/B, tools/ab_repeat.sh: -0.9% per step)
+    static const int seg_rows = getenv("PRNU_STRIP_SEGROWS") ? atoi(getenv("PRNU_STRIP_SEGROWS")) : 300;
     static const int waves_u8 = getenv("PRNU_STRIP_WAVES_U8") ? atoi(getenv("PRNU_STRIP_WAVES_U8")) : 6;
-    static const int waves_f32 = getenv("PRNU_STRIP_WAVES_F32") ? atoi(getenv("PRNU_STRIP_WAVES_F32")) : 6;
+    static const int waves_f32 = getenv("PRNU_STRIP_WAVES_F32") ? atoi(getenv("PRNU_STRIP_WAVES_F32")) : 1;
     const long long waves = sizeof(T) == 1 ? waves_u8 : waves_f32;
     int nseg = (nH + seg_rows - 1) / seg_rows;
     while ((long long)S * nseg * nb < waves * 148 * StripCfg<T>::MINB && (nH + nseg) / (nseg + 1) >= 32) ++nseg;
