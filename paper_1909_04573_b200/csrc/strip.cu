@@ -303,18 +303,31 @@ __global__ void __launch_bounds__(SR_NT, MINB) k_analysis_strip(const __grid_con
         }
     }
 
-    // block i (i = -1: the prologue) is staged in buffer (i + 3) % 3; blocks load input
-    // rows 2K .. 2K+15, the prologue rows 2K0-6 .. 2K0-1 as rows 10..15 of a box at 2K0-16
+    // block i (i = -1: the prologue) is staged in buffer (i + 3) % 3; blocks need input
+    // rows 2K .. 2K+15, the prologue rows 2K0-6 .. 2K0-1
     auto stg_of = [&](int i) { return (i + SR_NSTG) % SR_NSTG; };
-    auto box_y = [&](int i) { return i < 0 ? 2 * K0 - 16 : 2 * (K0 + SR_BK * i); };
-    // blocks whose rows lie inside the plane are staged by TMA (a 16-row box pair; the
-    // prologue box starts 10 rows early); blocks whose rows mirror (R-4) are loaded
-    // by the threads (u8 TMA boxes cannot target single 144-byte rows: the shared
-    // destination of a box must be 128-byte aligned)
-    auto tma_ok = [&](int i) {
-        const int y = box_y(i);
-        return a.use_tma && y >= 0 && y + SR_IR <= a.NH;
+    // block i needs input rows y0(i) .. y0(i) + nrows(i) - 1 (mirrored into the plane, R-4);
+    // they all lie in one 16-row window [box_y, box_y + 16) of the plane unless the plane
+    // is shorter than 16 rows: the window is staged by TMA and the row pass reads
+    // physical row mirror(y) - box_y (so mirrored blocks are staged asynchronously too)
+    auto y0_of = [&](int i) { return i < 0 ? 2 * K0 - 6 : 2 * (K0 + SR_BK * i); };
+    // rows y in [-16, NH + 32) mirror by one reflection when NH >= 32 (no integer modulo)
+    const bool refl1 = a.NH >= 32;
+    auto mirror_row = [&](int y) {
+        return refl1 ? (y < 0 ? -1 - y : (y >= a.NH ? 2 * a.NH - 1 - y : y)) : mirror(y, a.NH);
     };
+    auto inside = [&](int i) { const int y0 = y0_of(i); return y0 >= 0 && y0 + SR_IR <= a.NH; };
+    auto box_y = [&](int i) {
+        const int y0 = y0_of(i);
+        if (inside(i)) return y0;
+        const int y1 = y0 + (i < 0 ? 6 : SR_IR) - 1;
+        int lo = min(mirror_row(y0), mirror_row(y1));
+        if (y0 < 0 && y1 >= 0) lo = 0;   // the range folds at the top edge
+        return min(lo, a.NH - SR_IR);
+    };
+    // every block is staged by TMA (a 16-row box pair at box_y) when the plane has at
+    // least 16 rows; otherwise (and without a tensor map) the threads load the rows
+    auto tma_ok = [&](int i) { return a.use_tma && a.NH >= SR_IR; };
     auto issue = [&](int i) {   // thread 0 only
         const int k = stg_of(i);
         T* s = stg0 + k * STG;
@@ -366,13 +379,13 @@ __global__ void __launch_bounds__(SR_NT, MINB) k_analysis_strip(const __grid_con
     };
     // Row pass (along x) of row rr < nr of the staged rows into the row buffer
     // (regA): lo plane rows [0, 16), hi plane rows [16, 32), columns permuted.
-    auto rowpass = [&](const T* s, int r0, int nr) {
+    auto rowpass = [&](const T* s, int prow, int nr) {   // prow: physical staged row of row rr
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int g = ga + 8 * h;
             if ((h == 0 ? doA : doB) && rr < nr) {
                 float v[24];
-                stg_row22(s, r0 + rr, g, v);
+                stg_row22(s, prow, g, v);
                 float lo[8], hi[8];
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
@@ -421,12 +434,14 @@ __global__ void __launch_bounds__(SR_NT, MINB) k_analysis_strip(const __grid_con
         const int K = K0 + SR_BK * i;
         const int sk = stg_of(i);
         T* s = stg0 + sk * STG;
-        int r0 = 0;
+        int prow = -1;   // physical staged row of this thread's row-pass row (TMA blocks)
         if (tma_ok(i)) {
+            SPROBE(10);   // carries of the previous block, loop head
             mbar_wait(&bar[sk], (phase >> sk) & 1);
+            SPROBE(11);   // TMA wait
             phase ^= 1u << sk;
-            if (pro) r0 = 10;
-            if (edge) {
+            prow = inside(i) ? rr : mirror_row(y0_of(i) + rr) - box_y(i);
+            if (edge) {   // (sequential: measured faster than loads-then-stores)
 #pragma unroll
                 for (int k = 0; k < SR_FIX; ++k) {
                     const float v = fix_dst[k] >= 0 ? stg_at(s, fix_dst[k] >> 9, fix_src[k]) : 0.f;
@@ -435,12 +450,15 @@ __global__ void __launch_bounds__(SR_NT, MINB) k_analysis_strip(const __grid_con
                 }
                 __syncthreads();
             }
+            SPROBE(13);   // edge fix-ups
         } else {
+            SPROBE(12);   // carries of the previous block, loop head (thread-loaded block)
             manual(s, pro ? 2 * K0 - 6 : 2 * K, pro ? 6 : SR_IR);
+            prow = rr;
             __syncthreads();
         }
-        SPROBE(0);
-        rowpass(s, r0, pro ? 6 : SR_IR);
+        SPROBE(0);        // thread loads of mirrored rows
+        rowpass(s, prow, pro ? 6 : SR_IR);
         fence_proxy_async();
         SPROBE(1);
         __syncthreads();   // B1: row buffer complete, staging buffer s consumed
@@ -623,7 +641,7 @@ __global__ void __launch_bounds__(SR_NT, MINB) k_analysis_strip(const __grid_con
     }
 #ifdef PRNU_STRIP_PROFILE
     if ((t & 31) == 0)
-        for (int k = 0; k < 10; ++k) atomicAdd(&g_strip_prof[k], pacc[k]);
+        for (int k = 0; k < 14; ++k) atomicAdd(&g_strip_prof[k], pacc[k]);
 #endif
 }
 

@@ -11,9 +11,10 @@ buf = (ctypes.c_ulonglong * 16)()
 prnu._lib.prnu_debug_strip_profile(buf, 1)
 ex(v.frames); torch.cuda.synchronize()
 prnu._lib.prnu_debug_strip_profile(buf, 1)
-names = ["stage(wait TMA/manual/fixup)", "row pass", "B1 wait", "column pass", "V0,V2 write", "B2 wait",
-         "V1 write", "B3 wait", "H pass", "B4 wait"]
-tot = sum(buf[k] for k in range(10))
-for k in range(10):
+names = ["thread loads (mirrored rows)", "row pass", "B1 wait", "column pass", "V0,V2 write", "B2 wait",
+         "V1 write", "B3 wait", "H pass", "B4 wait", "carries, loop head", "TMA wait", "carries (manual blocks)",
+         "edge fix-ups"]
+tot = sum(buf[k] for k in range(14))
+for k in range(14):
     print(f"{names[k]:32s} {100.0 * buf[k] / tot:6.2f}%  {buf[k] / 1e9:8.3f} Gcyc")
 print(f"{'total':32s} {100.0:6.2f}%  {tot / 1e9:8.3f} Gcyc")
