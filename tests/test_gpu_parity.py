@@ -76,7 +76,11 @@ def test_sda_average_extremes_bit_exact(prnu):
 
 # ---------------------------------------------------------------- a2-a4
 @pytest.mark.parametrize("b,H,W", [(1, 64, 64), (3, 37, 53), (2, 135, 240), (1, 16, 16), (2, 100, 333),
-                                   (1, 270, 480)])
+                                   (1, 270, 480),
+                                   # strip staging: 16 <= H < 32 (mirrored rows, generic reflection),
+                                   # H = 31/32/33 around the single-reflection threshold, wide and narrow
+                                   (1, 17, 700), (2, 20, 333), (1, 31, 500), (1, 32, 257), (1, 33, 1000),
+                                   (1, 300, 17)])
 def test_residual_matches_oracle(prnu, b, H, W):
     I = _textured(b, H, W, H * W + b)
     got = prnu.residual(torch.from_numpy(I).cuda()).cpu().numpy()
@@ -104,6 +108,15 @@ def test_residual_u8_and_zero_mean(prnu):
         assert np.abs(got[i] - ref).max() <= W_TOL
         assert np.abs(got[i].astype(np.float64).mean(axis=0)).max() < 1e-4
         assert np.abs(got[i].astype(np.float64).mean(axis=1)).max() < 1e-4
+
+
+@pytest.mark.parametrize("H,W", [(17, 700), (31, 500), (33, 1000), (64, 64), (135, 241)])
+def test_residual_u8_sizes(prnu, H, W):
+    """u8 input (the level-1 u8 strip kernel) at heights around the staging thresholds."""
+    fr = _rand_frames(2, H, W, H + W, 10, 245)
+    got = prnu.residual(fr.cuda()).cpu().numpy()
+    for i in range(2):
+        assert np.abs(got[i] - oracle.residual(fr[i].numpy().astype(np.float32))).max() <= W_TOL
 
 
 def test_residual_invariants(prnu):
