@@ -147,6 +147,28 @@ def sub_len(n):
     return (n + 7) // 2
 
 
+# FP32-pipe lane-operations the method needs per level-l coefficient position:
+# DWT 2 x (2 rows x 2 outputs x 8 taps) = 64 FMA; shrink of 3 detail coefficients,
+# each c^2 (1) + nested vertical (8) + sliding horizontal (8) window sums + 4 scalings
+# + the Wiener product (2) = 23 -> 69.  min / max / rcp run on other pipes (not counted).
+ALU_OPS_PER_POSITION = 64 + 3 * 23
+FP32_LANES_PER_SM = 128
+
+
+def algorithmic_ops_per_step(name: str, H: int, W: int, levels: int, depths, m: int, n_query: int = 1):
+    """FP32 lane-ops one step needs in an analysis kernel (fused DWT + shrink) of `name`."""
+    if not name.startswith("analysis_l"):
+        return None
+    l = int(name[len("analysis_l")])
+    nH, nW = H, W
+    for _ in range(l):
+        nH, nW = sub_len(nH), sub_len(nW)
+    f_u8 = (m if 1 in depths else 0) + n_query
+    f_f32 = sum(m // d for d in depths if d > 1)
+    frames = f_u8 if name.endswith("_u8") else (f_f32 if name.endswith("_f32") else f_u8 + f_f32)
+    return frames * nH * nW * ALU_OPS_PER_POSITION
+
+
 def algorithmic_bytes_per_step(name: str, H: int, W: int, levels: int, depths, m: int, n_query: int = 1):
     """Algorithmic HBM bytes one step moves through kernel `name`:
     each input read once and each output written once at real (unpadded) sizes;
@@ -378,11 +400,24 @@ def main():
             fpl = (n_sda.get(1, 0) + 1) / max(1.0, kt["launches_per_step"]) if top.endswith("_u8") else None
             if t.get("kernel") == top and fpl and t.get("H") == H and t.get("W") == W:
                 traffic = (t["dram_bytes_read"] + t["dram_bytes_write"]) / t["frames_per_launch"] * fpl
-        roof = {"kernel": top, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback",
-                "bytes_per_launch": kt.get("alg_bytes_per_launch"), "avg_launch_ms": avg_ms,
-                "share_of_kernel_time": kt["share"]}
+        hbm_view = {"achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                    "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback",
+                    "bytes_per_launch": kt.get("alg_bytes_per_launch")}
+        ops = algorithmic_ops_per_step(top, H, W, 4, depths, m)
+        if ops is not None:
+            # the fused analysis is bound by FP32 issue, not HBM: its roofline is
+            # the FP32 pipe, 148 SMs x 128 lanes x the max SM clock (B200_PROFILING.md units)
+            sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+            alu_peak = 148 * FP32_LANES_PER_SM * sm_mhz * 1e6 / 1e12
+            alu_ach = ops / (kt["ms_per_step"] / 1000.0) / 1e12
+            roof = {"kernel": top, "bound": "alu", "achieved": alu_ach, "peak": alu_peak,
+                    "unit": "T fp32 lane-op/s", "frac": alu_ach / alu_peak, "traffic": traffic,
+                    "peak_source": "derived: 148 SM x 128 FP32 lanes x %.0f MHz" % sm_mhz,
+                    "ops_per_launch": ops / kt["launches_per_step"], "avg_launch_ms": avg_ms,
+                    "share_of_kernel_time": kt["share"], "hbm_view": hbm_view}
+        else:
+            roof = dict(kernel=top, bound="hbm", avg_launch_ms=avg_ms, share_of_kernel_time=kt["share"], **hbm_view)
 
     # ---- NEXT rows, measured outside the step: f2 WDFT of the two
     #      fingerprints, f1 500x500 block matching of the query, f4 RGB->luma
