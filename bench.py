@@ -454,7 +454,7 @@ def main():
             out = torch.empty_like(Ivar)
             t = timed(lambda: prnu.residual_variant(Ivar, var, out=out), reps=3)
             gb = variant_alg_bytes(H, W, 4, *v) * Ivar.shape[0] / (t / 1000.0) / 1e9
-            f3[name] = {"ms_per_frame": t / Ivar.shape[0], "alg_GBps": gb}
+            f3[name] = {"ms_per_frame": t / Ivar.shape[0], "alg_GBps": gb, "frac_hbm": gb / peak_hbm}
         next_rows = {"f3_variants": f3,
                      "f2_wdft_ms_per_fingerprint": t_wdft / len(depths),
                      "f1_block_match_ms": t_blk, "f1_tiles": bplan.n_tiles,

@@ -92,6 +92,34 @@ __global__ void __launch_bounds__(128) k_var_ana(VarPass p) {
     float* hi = p.out[2 * pl + 1] + (size_t)b * p.out_bstride;
     const float* H = c_var_h[T == 16];
     const int y0 = blockIdx.y * VAR_RY, y1 = min(y0 + VAR_RY, ey);
+    if (AX == 1 && MODE == VM_SWT) {
+        // undecimated, along y, dilation s: run r = q s + ph holds the outputs
+        // t_u = 8 s q + ph + s u (one polyphase component), which read input rows
+        // 8 s q + ph + s j, j = u + i - (T-1): T + 7 rows, each loaded once
+        const int s_ = p.s, q = blockIdx.y / s_, ph = blockIdx.y - q * s_;
+        const int tb = 8 * s_ * q + ph;
+        if (tb >= p.nout) return;
+        float v[T + 7];
+#pragma unroll
+        for (int j = 0; j < T + 7; ++j)
+            v[j] = __ldg(in + var_at<AX>(var_mod(tb + s_ * (j - (T - 1)), p.N), x, p.in_pitch));
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int t = tb + s_ * u;
+            if (t >= p.nout) break;
+            float a = 0.f, d = 0.f;
+#pragma unroll
+            for (int i = 0; i < T; ++i) {
+                const float g = (i & 1) ? -H[T - 1 - i] : H[T - 1 - i];
+                a = fmaf(H[i], v[u + i], a);
+                d = fmaf(g, v[u + i], d);
+            }
+            const size_t oi = var_at<AX>(t, x, p.out_pitch);
+            lo[oi] = a;
+            hi[oi] = d;
+        }
+        return;
+    }
     if (AX == 1 && MODE != VM_SWT) {
         // decimated, along y: the run's outputs k0 .. k0+7 read input rows
         // 2 k0 - (T-2) .. 2 k0 + 15: each loaded once into registers
@@ -145,6 +173,34 @@ __global__ void __launch_bounds__(128) k_var_syn(VarPass p) {
     const float* H = c_var_h[T == 16];
     const int n = p.N;
     const int y0 = blockIdx.y * VAR_RY, y1 = min(y0 + VAR_RY, ey);
+    if (AX == 1 && MODE == VM_SWT) {
+        // undecimated, along y: the polyphase run of k_var_ana; outputs t_u = tb + s u
+        // gather a, d rows tb + s j, j = u + T-1-i in [0, T + 6]
+        const int s_ = p.s, q = blockIdx.y / s_, ph = blockIdx.y - q * s_;
+        const int tb = 8 * s_ * q + ph;
+        if (tb >= p.nout) return;
+        float ca[T + 7], cd[T + 7];
+#pragma unroll
+        for (int j = 0; j < T + 7; ++j) {
+            const size_t at = var_at<AX>(var_mod(tb + s_ * j, n), x, p.in_pitch);
+            ca[j] = A ? __ldg(A + at) : 0.f;
+            cd[j] = __ldg(D + at);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int t = tb + s_ * u;
+            if (t >= p.nout) break;
+            float acc = 0.f;
+#pragma unroll
+            for (int i = 0; i < T; ++i) {
+                const float g = (i & 1) ? -H[T - 1 - i] : H[T - 1 - i];
+                if (A) acc = fmaf(H[i], ca[u + T - 1 - i], acc);
+                acc = fmaf(g, cd[u + T - 1 - i], acc);
+            }
+            out[var_at<AX>(t, x, p.out_pitch)] = 0.5f * acc;
+        }
+        return;
+    }
     if (AX == 1 && MODE != VM_SWT) {
         // decimated, along y: outputs t0 .. t0+7 (t0 even) gather coefficient rows
         // k = t0/2 .. t0/2 + NK - 1: each loaded once into registers (rows outside
@@ -214,7 +270,10 @@ __global__ void __launch_bounds__(128) k_var_syn(VarPass p) {
 template <int T, int MODE>
 static void var_launch(bool syn, int ax, const VarPass& p, int nb, cudaStream_t st) {
     const int ex = ax == 0 ? p.nout : p.other, ey = ax == 0 ? p.other : p.nout;
-    const dim3 grid((unsigned)((ex + 127) / 128), (unsigned)((ey + VAR_RY - 1) / VAR_RY), (unsigned)(nb * p.nplanes));
+    // undecimated column passes: polyphase runs, ceil(ey / (8 s)) blocks of 8 s rows x s phases
+    const unsigned gy = (MODE == VM_SWT && ax == 1) ? (unsigned)(((ey + 8 * p.s - 1) / (8 * p.s)) * p.s)
+                                                    : (unsigned)((ey + VAR_RY - 1) / VAR_RY);
+    const dim3 grid((unsigned)((ex + 127) / 128), gy, (unsigned)(nb * p.nplanes));
     if (syn) {
         if (ax == 0) k_var_syn<T, MODE, 0><<<grid, 128, 0, st>>>(p);
         else k_var_syn<T, MODE, 1><<<grid, 128, 0, st>>>(p);
