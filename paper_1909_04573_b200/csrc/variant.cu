@@ -267,8 +267,140 @@ __global__ void __launch_bounds__(128) k_var_syn(VarPass p) {
     }
 }
 
+// Row (x) passes through shared memory: a CTA stages, for one row at a time, the
+// input span its 512 outputs need (each element loaded once from HBM/L2, index map
+// applied once per element), then every thread computes 4 outputs (t0 + tid + 128 j)
+// from shared memory with consecutive lanes on consecutive addresses.  Decimated
+// analysis stages the span deinterleaved into even / odd samples so the stride-2
+// taps become unit-stride; decimated synthesis stages the coefficient span (lanes
+// 2i, 2i+1 read the same coefficient: broadcast).
+constexpr int VR_OUT = 512;   // outputs per CTA and row
+
+template <int T, int MODE>
+__host__ __device__ inline int var_row_span(bool syn, int s) {   // staged elements per array
+    return MODE == VM_SWT ? VR_OUT + s * (T - 1) : (syn ? VR_OUT / 2 + T / 2 : VR_OUT + T / 2);
+}
+
+template <int T, int MODE>
+__global__ void __launch_bounds__(128) k_var_row_ana(VarPass p) {
+    extern __shared__ float vr_smem[];
+    const int nst = var_row_span<T, MODE>(false, p.s);
+    float* sE = vr_smem;
+    float* sO = vr_smem + nst;
+    const int pl = blockIdx.z % p.nplanes, b = blockIdx.z / p.nplanes;
+    const int tid = threadIdx.x;
+    const int t0 = blockIdx.x * VR_OUT;
+    const float* in = p.in[pl] + (size_t)b * p.in_bstride;
+    float* lo = p.out[2 * pl] + (size_t)b * p.out_bstride;
+    float* hi = p.out[2 * pl + 1] + (size_t)b * p.out_bstride;
+    const float* H = c_var_h[T == 16];
+    const int y0 = blockIdx.y * VAR_RY, y1 = min(y0 + VAR_RY, p.other);
+    // decimated: E[j] = x[base + 2j], O[j] = x[base + 2j + 1], base = 2 t0 - (T-2), j < 512 + T/2
+    // undecimated: E[j] = x[t0 - s (T-1) + j], j < 512 + s (T-1)
+    const int base = MODE == VM_SWT ? t0 - p.s * (T - 1) : 2 * t0 - (T - 2);
+    for (int y = y0; y < y1; ++y) {
+        const float* row = in + (size_t)y * p.in_pitch;
+        __syncthreads();   // the previous row's staging is consumed
+        for (int j = tid; j < nst; j += 128) {
+            if (MODE == VM_SWT) {
+                sE[j] = __ldg(row + var_map<MODE>(base + j, p.N, p.Np));
+            } else {
+                sE[j] = __ldg(row + var_map<MODE>(base + 2 * j, p.N, p.Np));
+                sO[j] = __ldg(row + var_map<MODE>(base + 2 * j + 1, p.N, p.Np));
+            }
+        }
+        __syncthreads();
+        float* lrow = lo + (size_t)y * p.out_pitch;
+        float* hrow = hi + (size_t)y * p.out_pitch;
+#pragma unroll
+        for (int q = 0; q < VR_OUT / 128; ++q) {
+            const int u = tid + 128 * q, k = t0 + u;
+            if (k >= p.nout) break;
+            float a = 0.f, d = 0.f;
+#pragma unroll
+            for (int i = 0; i < T; ++i) {
+                // decimated: x[2k - (T-2) + i] = E/O[u + i/2]; undecimated: x[k - s (T-1-i)] = E[u + s i]
+                const float v = MODE == VM_SWT ? sE[u + p.s * i] : ((i & 1) ? sO[u + i / 2] : sE[u + i / 2]);
+                const float g = (i & 1) ? -H[T - 1 - i] : H[T - 1 - i];
+                a = fmaf(H[i], v, a);
+                d = fmaf(g, v, d);
+            }
+            lrow[k] = a;
+            hrow[k] = d;
+        }
+    }
+}
+
+template <int T, int MODE>
+__global__ void __launch_bounds__(128) k_var_row_syn(VarPass p) {
+    extern __shared__ float vr_smem[];
+    const int nst = var_row_span<T, MODE>(true, p.s);
+    float* sA = vr_smem;
+    float* sD = vr_smem + nst;
+    const int pl = blockIdx.z % p.nplanes, b = blockIdx.z / p.nplanes;
+    const int tid = threadIdx.x;
+    const int t0 = blockIdx.x * VR_OUT;
+    const float* A = p.in[2 * pl] ? p.in[2 * pl] + (size_t)b * p.in_bstride : nullptr;
+    const float* D = p.in[2 * pl + 1] + (size_t)b * p.in_bstride;
+    float* out = p.out[pl] + (size_t)b * p.out_bstride;
+    const float* H = c_var_h[T == 16];
+    const int n = p.N;
+    const int y0 = blockIdx.y * VAR_RY, y1 = min(y0 + VAR_RY, p.other);
+    // decimated: coefficients k = t0/2 + j, j < 256 + T/2 - 1 (dropped outside [0, n) for the
+    // symmetric transform, mod n for the periodic one); undecimated: t0 + j, j < 512 + s (T-1)
+    for (int y = y0; y < y1; ++y) {
+        const float* arow = A ? A + (size_t)y * p.in_pitch : nullptr;
+        const float* drow = D + (size_t)y * p.in_pitch;
+        __syncthreads();
+        for (int j = tid; j < nst; j += 128) {
+            int k = MODE == VM_SWT ? t0 + j : t0 / 2 + j;
+            bool ok = true;
+            if (MODE == VM_SYM) ok = k < n;
+            else k = var_mod(k, n);
+            sA[j] = (ok && arow) ? __ldg(arow + k) : 0.f;
+            sD[j] = ok ? __ldg(drow + k) : 0.f;
+        }
+        __syncthreads();
+        float* orow = out + (size_t)y * p.out_pitch;
+#pragma unroll
+        for (int q = 0; q < VR_OUT / 128; ++q) {
+            const int u = tid + 128 * q, t = t0 + u;
+            if (t >= p.nout) break;
+            float acc = 0.f;
+            if (MODE == VM_SWT) {
+#pragma unroll
+                for (int i = 0; i < T; ++i) {
+                    const float g = (i & 1) ? -H[T - 1 - i] : H[T - 1 - i];
+                    const int j = u + p.s * (T - 1 - i);
+                    acc = fmaf(H[i], sA[j], acc);
+                    acc = fmaf(g, sD[j], acc);
+                }
+                acc *= 0.5f;
+            } else {
+                const int e = u & 1, jb = (u - e) / 2 + (T - 2) / 2;   // k - t0/2 for m = 0
+#pragma unroll
+                for (int m = 0; m < T / 2; ++m) {
+                    const int f = e + 2 * m;
+                    const float g = e ? -H[T - 1 - f] : H[T - 1 - f];
+                    acc = fmaf(H[f], sA[jb - m], acc);
+                    acc = fmaf(g, sD[jb - m], acc);
+                }
+            }
+            orow[t] = acc;
+        }
+    }
+}
+
 template <int T, int MODE>
 static void var_launch(bool syn, int ax, const VarPass& p, int nb, cudaStream_t st) {
+    if (ax == 0) {   // row passes: shared-memory staged
+        const dim3 g((unsigned)((p.nout + VR_OUT - 1) / VR_OUT), (unsigned)((p.other + VAR_RY - 1) / VAR_RY),
+                     (unsigned)(nb * p.nplanes));
+        const size_t sm = 2 * sizeof(float) * var_row_span<T, MODE>(syn, p.s);
+        if (syn) k_var_row_syn<T, MODE><<<g, 128, sm, st>>>(p);
+        else k_var_row_ana<T, MODE><<<g, 128, sm, st>>>(p);
+        return;
+    }
     const int ex = ax == 0 ? p.nout : p.other, ey = ax == 0 ? p.other : p.nout;
     // undecimated column passes: polyphase runs, ceil(ey / (8 s)) blocks of 8 s rows x s phases
     const unsigned gy = (MODE == VM_SWT && ax == 1) ? (unsigned)(((ey + 8 * p.s - 1) / (8 * p.s)) * p.s)
