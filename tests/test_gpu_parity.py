@@ -420,3 +420,18 @@ def test_wdft_fingerprint_fhd(prnu):
     err = np.max(np.abs(Kw.cpu().numpy() - ref)) / float(fp.K.abs().max())
     assert err <= 1e-4, err
     assert prnu.ncc(Kw, v.K.cuda()).item() >= prnu.ncc(fp.K, v.K.cuda()).item() - 0.02
+
+
+@pytest.mark.parametrize("m,H,W,d", [(16, 64, 64, 4), (40, 135, 240, 1), (60, 96, 130, 20)])
+def test_graph_extractor_bit_identical(prnu, m, H, W, d):
+    """The CUDA-graph-captured extraction (GraphExtractor) replays to the same bits as the
+    eager Extractor, across replays and after the static input buffer is rewritten."""
+    fr = _rand_frames(m, H, W, 3 + d)
+    ex = prnu.Extractor(H, W, d, 8)
+    gx = prnu.GraphExtractor(m, H, W, d, 8)
+    a = ex(fr.cuda())
+    b = gx(fr.cuda())
+    assert torch.equal(a.K, b.K) and torch.equal(a.sum_WI, b.sum_WI) and torch.equal(a.sum_I2, b.sum_I2)
+    fr2 = _rand_frames(m, H, W, 99 + d)
+    a2 = ex(fr2.cuda()).K.clone()
+    assert torch.equal(gx(fr2.cuda()).K, a2) and torch.equal(gx().K, a2)
