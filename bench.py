@@ -455,7 +455,25 @@ def main():
             t = timed(lambda: prnu.residual_variant(Ivar, var, out=out), reps=3)
             gb = variant_alg_bytes(H, W, 4, *v) * Ivar.shape[0] / (t / 1000.0) / 1e9
             f3[name] = {"ms_per_frame": t / Ivar.shape[0], "alg_GBps": gb, "frac_hbm": gb / peak_hbm}
-        next_rows = {"f3_variants": f3,
+        # BASELINE config 4 shape (camera identification): 64 fingerprints of 300 frames
+        # 1280x720 at depth 30, then 64 query residuals x 64 fingerprints = 4096 PCEs
+        # (one camera's synthetic frames reused for every camera: throughput only)
+        c4H, c4W, c4n = 720, 1280, 64
+        fr4 = synth.video("drift", 301, c4H, c4W, seed=4, camera=0, device=dev).frames
+        ex4 = prnu.Extractor(c4H, c4W, 30, 10, device=dev)
+        Iq4 = fr4[300:301].expand(c4n, c4H, c4W).contiguous()
+        plan4 = prnu.PcePlan(c4H, c4W, c4n, device=dev)
+
+        def camera_id():
+            Ks4 = [ex4(fr4[:300]).K.clone() for _ in range(c4n)]
+            R4 = prnu.residual(Iq4, zero_mean=True)
+            plan4.set_residual(R4)   # one FFT of the 64 query residuals for all 64 fingerprints
+            for c in range(c4n):
+                plan4.match(prnu.pce_template(Ks4[c], Iq4))
+        t_c4 = timed(camera_id, reps=1)
+        c4 = {"workload": "64 x 300 frames 1280x720, depth 30, 64x64 PCE", "ms": t_c4,
+              "fingerprints_per_s": c4n / (t_c4 / 1000.0), "pce_per_s": c4n * c4n / (t_c4 / 1000.0)}
+        next_rows = {"f3_variants": f3, "c4_camera_id": c4,
                      "f2_wdft_ms_per_fingerprint": t_wdft / len(depths),
                      "f1_block_match_ms": t_blk, "f1_tiles": bplan.n_tiles,
                      "f4_rgb_to_luma_GBps": luma_bytes / (t_luma / 1000.0) / 1e9,

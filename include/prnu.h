@@ -232,6 +232,15 @@ int prnu_pce(void* plan, const float* residual, const float* template_, int batc
              int aligned, double* pce, int* peak_y, int* peak_x, double* peak, void* ws, size_t ws_bytes,
              void* stream);
 int prnu_pce_plan_destroy(void* plan);
+/* Residual-spectrum reuse (camera identification: the same query residuals against
+ * many fingerprints).  prnu_pce_residual_spectrum computes FFT2 of residual
+ * [batch][H][W] into the plan workspace `ws`; prnu_pce_cached then runs prnu_pce
+ * for template_ against that cached spectrum (same arguments as prnu_pce without
+ * `residual`), any number of times, as long as `ws` is not used for another
+ * residual in between.  Results are bit-identical to prnu_pce(residual, template_). */
+int prnu_pce_residual_spectrum(void* plan, const float* residual, void* ws, size_t ws_bytes, void* stream);
+int prnu_pce_cached(void* plan, const float* template_, int batch, int exclusion_half, int aligned, double* pce,
+                    int* peak_y, int* peak_x, double* peak, void* ws, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
  * f2  Wiener filtering of fingerprints in the DFT domain —

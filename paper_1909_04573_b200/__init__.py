@@ -126,6 +126,8 @@ _sig("prnu_pce_template", _i, _vp, _i, _vp, _i, _i, _i, _vp, _vp)
 _sig("prnu_pce_plan_create", _i, _i, _i, _i, ctypes.POINTER(_sz), ctypes.POINTER(_vp))
 _sig("prnu_pce", _i, _vp, _vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _sz, _vp)
 _sig("prnu_pce_plan_destroy", _i, _vp)
+_sig("prnu_pce_residual_spectrum", _i, _vp, _vp, _vp, _sz, _vp)
+_sig("prnu_pce_cached", _i, _vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _sz, _vp)
 _sig("prnu_wdft_plan_create", _i, _i, _i, _i, ctypes.POINTER(_sz), ctypes.POINTER(_vp))
 _sig("prnu_wdft", _i, _vp, _vp, _vp, _vp, _sz, _vp)
 _sig("prnu_wdft_plan_destroy", _i, _vp)
@@ -581,9 +583,32 @@ class PcePlan:
                "prnu_pce")
         return PceResult(o.pce.clone(), o.peak_y.clone(), o.peak_x.clone(), o.peak.clone())
 
+    def set_residual(self, R: torch.Tensor):
+        """Cache FFT2 of the residual batch in the plan's workspace (prnu_pce_residual_spectrum)."""
+        if R.dim() == 2:
+            R = R.unsqueeze(0)
+        _dev(R, torch.float32, "residual", (3,))
+        if R.shape != (self.batch, self.H, self.W):
+            raise ValueError("dimension mismatch with the plan")
+        _check(_lib.prnu_pce_residual_spectrum(self._h, _ptr(R), _ptr(self.ws), self.nbytes, _stream()),
+               "prnu_pce_residual_spectrum")
+
+    def match(self, T: torch.Tensor, exclusion_half: int = 5, aligned: bool = False) -> PceResult:
+        """PCE of the cached residuals (set_residual) against templates T (prnu_pce_cached)."""
+        if T.dim() == 2:
+            T = T.unsqueeze(0)
+        _dev(T, torch.float32, "template", (3,))
+        if T.shape != (self.batch, self.H, self.W):
+            raise ValueError("dimension mismatch with the plan")
+        o = self.out
+        _check(_lib.prnu_pce_cached(self._h, _ptr(T), self.batch, exclusion_half, int(aligned), _ptr(o.pce),
+                                    _ptr(o.peak_y), _ptr(o.peak_x), _ptr(o.peak), _ptr(self.ws), self.nbytes,
+                                    _stream()), "prnu_pce_cached")
+        return PceResult(o.pce.clone(), o.peak_y.clone(), o.peak_x.clone(), o.peak.clone())
+
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and _lib is not None:
             _lib.prnu_pce_plan_destroy(h)
             self._h = None
 
@@ -707,7 +732,7 @@ class BlockPlan:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and _lib is not None:
             _lib.prnu_block_plan_destroy(h)
             self._h = None
 

@@ -643,6 +643,29 @@ int prnu_pce(void* plan, const float* residual, const float* template_, int batc
                    as_stream(stream));
 }
 
+int prnu_pce_residual_spectrum(void* plan, const float* residual, void* ws, size_t ws_bytes, void* stream) {
+    if (!plan || !residual || !ws) return fail(PRNU_INVALID_ARG, "null pointer");
+    int H, W, pb;
+    size_t need;
+    pce_plan_dims(plan, &H, &W, &pb, &need);
+    if (ws_bytes < need) return fail(PRNU_WORKSPACE_TOO_SMALL, "workspace too small");
+    return run_pce(plan, residual, nullptr, 0, 0, nullptr, nullptr, nullptr, nullptr, ws, as_stream(stream));
+}
+
+int prnu_pce_cached(void* plan, const float* template_, int batch, int exclusion_half, int aligned, double* pce,
+                    int* peak_y, int* peak_x, double* peak, void* ws, size_t ws_bytes, void* stream) {
+    if (!plan || !template_ || !pce || !peak_y || !peak_x || !peak || !ws)
+        return fail(PRNU_INVALID_ARG, "null pointer");
+    int H, W, pb;
+    size_t need;
+    pce_plan_dims(plan, &H, &W, &pb, &need);
+    if (batch != pb) return fail(PRNU_DIMENSION_MISMATCH, "batch differs from the plan's batch");
+    if (exclusion_half < 0) return fail(PRNU_BAD_PARAMETER, "exclusion_half must be >= 0");
+    if (ws_bytes < need) return fail(PRNU_WORKSPACE_TOO_SMALL, "workspace too small");
+    return run_pce(plan, nullptr, template_, exclusion_half, aligned, pce, peak_y, peak_x, peak, ws,
+                   as_stream(stream));
+}
+
 int prnu_pce_plan_destroy(void* plan) { return pce_plan_destroy(plan); }
 
 int prnu_wdft_plan_create(int H, int W, int batch, size_t* ws_bytes, void** plan) {

@@ -43,7 +43,9 @@ int launch_pce_template(const float* K, int k_batch, const uint8_t* Iq, int batc
 }
 
 // ---------------------------------------------------------------- spectra
-__global__ void __launch_bounds__(256) k_conj_mul(cufftComplex* __restrict__ R, const cufftComplex* __restrict__ T,
+// T <- R conj(T), in T's storage: the residual spectrum R survives, so one FFT(R)
+// serves every template batch matched against the same residuals (camera ID).
+__global__ void __launch_bounds__(256) k_conj_mul(const cufftComplex* __restrict__ R, cufftComplex* __restrict__ T,
                                                    long long n_per, int batch) {
     long long n = n_per * batch;
     for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += 256LL * gridDim.x) {
@@ -52,7 +54,7 @@ __global__ void __launch_bounds__(256) k_conj_mul(cufftComplex* __restrict__ R, 
         o.x = r.x * t.x + r.y * t.y;       // r * conj(t)
         o.y = r.y * t.x - r.x * t.y;
         if (i % n_per == 0) o.x = o.y = 0.f;   // DC bin: mean removal of both inputs
-        R[i] = o;
+        T[i] = o;
     }
 }
 
@@ -254,8 +256,10 @@ int run_pce(void* plan, const float* R, const float* T, int excl, int aligned, d
     if ((r = cufftSetStream(p->r2c, st)) || (r = cufftSetStream(p->c2r, st)) || (r = cufftSetWorkArea(p->r2c, work)) ||
         (r = cufftSetWorkArea(p->c2r, work)))
         return fail(PRNU_CUDA_ERROR, std::string("cufft setup: ") + cufft_str(r));
-    if ((r = cufftExecR2C(p->r2c, const_cast<float*>(R), Rf)))
+    // R == nullptr: reuse the residual spectrum an earlier call left in this workspace
+    if (R && (r = cufftExecR2C(p->r2c, const_cast<float*>(R), Rf)))
         return fail(PRNU_CUDA_ERROR, std::string("cufftExecR2C: ") + cufft_str(r));
+    if (!T) return PRNU_OK;   // spectrum only
     if ((r = cufftExecR2C(p->r2c, const_cast<float*>(T), Tf)))
         return fail(PRNU_CUDA_ERROR, std::string("cufftExecR2C: ") + cufft_str(r));
     long long n_per = (long long)spectrum_elems(H, W);
@@ -266,7 +270,7 @@ int run_pce(void* plan, const float* R, const float* T, int excl, int aligned, d
     }
     count_launch();
     if (int rc = check_launch("k_conj_mul")) return rc;
-    if ((r = cufftExecC2R(p->c2r, Rf, Cs)))
+    if ((r = cufftExecC2R(p->c2r, Tf, Cs)))
         return fail(PRNU_CUDA_ERROR, std::string("cufftExecC2R: ") + cufft_str(r));
     long long P = (long long)H * W;
     {

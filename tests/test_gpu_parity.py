@@ -435,3 +435,17 @@ def test_graph_extractor_bit_identical(prnu, m, H, W, d):
     fr2 = _rand_frames(m, H, W, 99 + d)
     a2 = ex(fr2.cuda()).K.clone()
     assert torch.equal(gx(fr2.cuda()).K, a2) and torch.equal(gx().K, a2)
+
+
+def test_pce_cached_residual_spectrum_bit_identical(prnu):
+    """prnu_pce_residual_spectrum + prnu_pce_cached (one FFT of the residuals for many
+    template batches) gives the bits of prnu_pce for every template batch."""
+    H, W, b = 96, 130, 3
+    R = torch.from_numpy(_textured(b, H, W, 5) - 128.0).cuda()
+    Ts = [torch.from_numpy(_textured(b, H, W, 10 + k) - 128.0).cuda() for k in range(3)]
+    plan = prnu.PcePlan(H, W, b)
+    ref = [plan(R, T) for T in Ts]
+    plan.set_residual(R)
+    for T, r in zip(Ts, ref):
+        got = plan.match(T)
+        assert torch.equal(got.pce, r.pce) and torch.equal(got.peak_y, r.peak_y) and torch.equal(got.peak, r.peak)

@@ -1,0 +1,47 @@
+"""Camera-identification workload (BASELINE config 4) split: fingerprints vs PCE matrix."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_1909_04573_b200 as prnu
+import synth
+
+H, W, n = 720, 1280, 64
+fr = synth.video("drift", 301, H, W, seed=4, camera=0, device="cuda").frames
+ex = prnu.Extractor(H, W, 30, 10)
+Iq = fr[300:301].expand(n, H, W).contiguous()
+plan = prnu.PcePlan(H, W, n)
+
+
+def timed(fn, reps=3):
+    fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+Ks = [ex(fr[:300]).K.clone() for _ in range(n)]
+R = prnu.residual(Iq, zero_mean=True)
+print("64 fingerprints  %.2f ms" % timed(lambda: [ex(fr[:300]) for _ in range(n)]))
+print("64 query residuals %.2f ms" % timed(lambda: prnu.residual(Iq, zero_mean=True)))
+print("64x64 templates  %.2f ms" % timed(lambda: [prnu.pce_template(Ks[c], Iq) for c in range(n)]))
+T = prnu.pce_template(Ks[0], Iq)
+print("64x64 PCE        %.2f ms" % timed(lambda: [plan(R, T) for c in range(n)]))
+plan.set_residual(R)
+print("64x64 PCE cached %.2f ms" % timed(lambda: [plan.match(T) for c in range(n)]))
+prnu._lib.prnu_profile_begin()
+plan(R, T)
+torch.cuda.synchronize()
+import ctypes
+maxk = 32
+names = ctypes.create_string_buffer(64 * maxk)
+tot = (ctypes.c_double * maxk)()
+cnt = (ctypes.c_int64 * maxk)()
+nk = ctypes.c_int()
+prnu._lib.prnu_profile_end(maxk, names, tot, cnt, ctypes.byref(nk))
+for k in range(nk.value):
+    print("   ", names.raw[64 * k: 64 * k + 64].split(b"\0")[0].decode(), "%.3f ms" % tot[k], cnt[k])
