@@ -460,12 +460,12 @@ def main():
         # (one camera's synthetic frames reused for every camera: throughput only)
         c4H, c4W, c4n = 720, 1280, 64
         fr4 = synth.video("drift", 301, c4H, c4W, seed=4, camera=0, device=dev).frames
-        ex4 = prnu.Extractor(c4H, c4W, 30, 10, device=dev)
+        ex4 = prnu.CameraBatchExtractor(c4H, c4W, 30, 10, streams=8, device=dev)
         Iq4 = fr4[300:301].expand(c4n, c4H, c4W).contiguous()
         plan4 = prnu.PcePlan(c4H, c4W, c4n, device=dev)
 
         def camera_id():
-            Ks4 = [ex4(fr4[:300]).K.clone() for _ in range(c4n)]
+            Ks4 = ex4([fr4[:300]] * c4n)
             R4 = prnu.residual(Iq4, zero_mean=True)
             plan4.set_residual(R4)   # one FFT of the 64 query residuals for all 64 fingerprints
             for c in range(c4n):

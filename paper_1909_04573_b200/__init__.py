@@ -418,6 +418,36 @@ class GraphExtractor:
         return Fingerprint(ex.K, ex.sum_WI, ex.sum_I2, self.n_sda, ex.depth, self.frames.shape[0])
 
 
+class CameraBatchExtractor:
+    """Fingerprints of many independent videos (cameras) of the same size and depth:
+    one Extractor (workspace, accumulators) per stream, cameras dealt round-robin over
+    `streams` CUDA streams so small per-camera waves overlap on the GPU (BASELINE
+    config 4: 64 cameras x 300 frames 1280x720 at depth 30)."""
+
+    def __init__(self, H: int, W: int, depth: int, batch: int = 16, streams: int = 8,
+                 params: DenoiseParams | None = None, device="cuda", eps: float = 1e-6):
+        self.H, self.W = H, W
+        self.exs = [Extractor(H, W, depth, batch, params, device, eps) for _ in range(streams)]
+        self.streams = [torch.cuda.Stream(device=device) for _ in range(streams)]
+        self.device = device
+
+    def __call__(self, videos) -> torch.Tensor:
+        """videos: a sequence of uint8 [m, H, W] device tensors (or a [n, m, H, W] tensor);
+        returns K fp32 [n, H, W]."""
+        n = len(videos)
+        K = torch.empty((n, self.H, self.W), dtype=torch.float32, device=self.device)
+        cur = torch.cuda.current_stream()
+        for s_ in self.streams:
+            s_.wait_stream(cur)
+        for c in range(n):
+            j = c % len(self.streams)
+            with torch.cuda.stream(self.streams[j]):
+                K[c].copy_(self.exs[j](videos[c]).K)
+        for s_ in self.streams:
+            cur.wait_stream(s_)
+        return K
+
+
 class MultiExtractor:
     """Fingerprints at several SDA depths from ONE upload of a host (pinned) frame
     stack [m][H][W]; owns the device workspace (which holds the whole stack)."""

@@ -449,3 +449,11 @@ def test_pce_cached_residual_spectrum_bit_identical(prnu):
     for T, r in zip(Ts, ref):
         got = plan.match(T)
         assert torch.equal(got.pce, r.pce) and torch.equal(got.peak_y, r.peak_y) and torch.equal(got.peak, r.peak)
+
+
+def test_camera_batch_extractor_matches_single(prnu):
+    """Cameras dealt over several streams give each camera's single-stream fingerprint."""
+    vids = [_rand_frames(20, 64, 96, 40 + c).cuda() for c in range(5)]
+    K = prnu.CameraBatchExtractor(64, 96, 4, 3, streams=3)(vids)
+    for c in range(5):
+        assert torch.equal(K[c], prnu.extract_fingerprint(vids[c], 4, batch=3).K)

@@ -25,6 +25,24 @@ def timed(fn, reps=3):
 
 
 Ks = [ex(fr[:300]).K.clone() for _ in range(n)]
+nst = 8
+exs = [prnu.Extractor(H, W, 30, 10) for _ in range(nst)]
+sts = [torch.cuda.Stream() for _ in range(nst)]
+Kout = torch.empty((n, H, W), device="cuda")
+
+
+def fps_streams():
+    cur = torch.cuda.current_stream()
+    for s_ in sts:
+        s_.wait_stream(cur)
+    for c in range(n):
+        with torch.cuda.stream(sts[c % nst]):
+            Kout[c].copy_(exs[c % nst](fr[:300]).K)
+    for s_ in sts:
+        cur.wait_stream(s_)
+
+
+print("64 fingerprints on 8 streams %.2f ms" % timed(fps_streams))
 R = prnu.residual(Iq, zero_mean=True)
 print("64 fingerprints  %.2f ms" % timed(lambda: [ex(fr[:300]) for _ in range(n)]))
 print("64 query residuals %.2f ms" % timed(lambda: prnu.residual(Iq, zero_mean=True)))
