@@ -473,7 +473,24 @@ def main():
         t_c4 = timed(camera_id, reps=1)
         c4 = {"workload": "64 x 300 frames 1280x720, depth 30, 64x64 PCE", "ms": t_c4,
               "fingerprints_per_s": c4n / (t_c4 / 1000.0), "pce_per_s": c4n * c4n / (t_c4 / 1000.0)}
-        next_rows = {"f3_variants": f3, "c4_camera_id": c4,
+        # BASELINE config 5: one 1920x1080 stack of 3600 frames ("shift" model), depths
+        # 1 .. 3600: per depth the fingerprint time, denoised frames/s, % HBM (SDA read +
+        # denoise traffic) and NCC against the true K
+        del fr4, Iq4, plan4, ex4
+        torch.cuda.empty_cache()
+        v5 = synth.video("shift", 3600, H, W, seed=5, device=dev)
+        c5 = {}
+        for d5 in (1, 2, 5, 10, 25, 50, 100, 300, 3600):
+            ex5 = prnu.Extractor(H, W, d5, 225 if d5 == 1 else min(64, 3600 // d5), device=dev)
+            t5 = timed(lambda: ex5(v5.frames), reps=1)
+            n5 = 3600 // d5
+            rho = float(prnu.ncc(ex5(v5.frames).K, v5.K))
+            c5[str(d5)] = {"ms": t5, "denoisings": n5, "denoised_frames_per_s": n5 / (t5 / 1000.0),
+                           "source_frames_per_s": 3600 / (t5 / 1000.0), "ncc_vs_true_K": rho}
+            del ex5
+        del v5
+        torch.cuda.empty_cache()
+        next_rows = {"f3_variants": f3, "c4_camera_id": c4, "c5_depth_sweep": c5,
                      "f2_wdft_ms_per_fingerprint": t_wdft / len(depths),
                      "f1_block_match_ms": t_blk, "f1_tiles": bplan.n_tiles,
                      "f4_rgb_to_luma_GBps": luma_bytes / (t_luma / 1000.0) / 1e9,
