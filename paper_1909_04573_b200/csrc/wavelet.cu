@@ -1302,15 +1302,28 @@ int run_residual(const TIn* in, int nb, int H, int W, const Pyramid& p, const Sh
     s.out = W_out;
     s.out_bstride = (long long)H * W;
     s.out_pitch = W;
-    const int tiles = ((W + ST_X - 1) / ST_X) * ((H + ST_Y - 1) / ST_Y);
-    s.frames_per_cta = std::max(1, std::min(4, tiles * nb / (148 * 6)));
-    dim3 grid((W + ST_X - 1) / ST_X, (H + ST_Y - 1) / ST_Y, (nb + s.frames_per_cta - 1) / s.frames_per_cta);
-    {
+    static const bool synth2 = !(getenv("PRNU_SYNTH2") && getenv("PRNU_SYNTH2")[0] == '0');
+    if (synth2) {   // the v2 pipeline of the levels above (MODE 0: W written, no accumulation)
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_synth_acc2<32, float, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sacc_smem_bytes<32, float, 0>());
+            attr = true;
+        }
+        const int tiles = ((W + ST_X - 1) / ST_X) * ((H + 31) / 32);
+        s.frames_per_cta = std::max(4, std::min(nb, (int)((long long)tiles * nb / (148 * 4 * 4))));
+        dim3 grid((W + ST_X - 1) / ST_X, (H + 31) / 32, (nb + s.frames_per_cta - 1) / s.frames_per_cta);
+        KTimer kt("synthesis_l1", st);
+        k_synth_acc2<32, float, 0><<<grid, 256, sacc_smem_bytes<32, float, 0>(), st>>>(m, CUtensorMap{}, s);
+    } else {
+        const int tiles = ((W + ST_X - 1) / ST_X) * ((H + ST_Y - 1) / ST_Y);
+        s.frames_per_cta = std::max(1, std::min(4, tiles * nb / (148 * 6)));
+        dim3 grid((W + ST_X - 1) / ST_X, (H + ST_Y - 1) / ST_Y, (nb + s.frames_per_cta - 1) / s.frames_per_cta);
         KTimer kt("synthesis_l1", st);
         k_synth_tma<0, float><<<grid, 256, S_SMEM_BYTES, st>>>(m, s);
     }
     count_launch();
-    return check_launch("k_synth_tma(level 1)");
+    return check_launch("k_synth (level 1)");
 }
 
 // acc_wait (optional): event the accumulating launch must wait for (the previous
