@@ -445,7 +445,6 @@ __global__ void __launch_bounds__(SR_NT, MINB) k_analysis_strip(const __grid_con
 #pragma unroll
                 for (int k = 0; k < SR_FIX; ++k) {
                     const float v = fix_dst[k] >= 0 ? stg_at(s, fix_dst[k] >> 9, fix_src[k]) : 0.f;
-                    __syncwarp();
                     if (fix_dst[k] >= 0) stg_put(s, fix_dst[k] >> 9, fix_dst[k] & 511, v);
                 }
                 __syncthreads();
