@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(SR_NT, MINB) k_analysis_strip(const __grid_con
             SPROBE(11);   // TMA wait
             phase ^= 1u << sk;
             prow = inside(i) ? rr : mirror_row(y0_of(i) + rr) - box_y(i);
-            if (edge) {   // (sequential: measured faster than loads-then-stores)
+            if (edge) {   // sources in the plane, destinations outside it: no hazard inside the pass
 #pragma unroll
                 for (int k = 0; k < SR_FIX; ++k) {
                     const float v = fix_dst[k] >= 0 ? stg_at(s, fix_dst[k] >> 9, fix_src[k]) : 0.f;
