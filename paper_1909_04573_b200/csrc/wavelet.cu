@@ -1159,11 +1159,12 @@ static const char* kDwtName[kMaxLevels + 1] = {"", "dwt_l1", "dwt_l2", "dwt_l3",
 static const char* kShrinkName[kMaxLevels + 1] = {"", "shrink_l1", "shrink_l2", "shrink_l3",
                                                   "shrink_l4", "shrink_l5", "shrink_l6"};
 
-// Deepest level analysed by the strip kernel (PRNU_STRIP_MAXL, default 3): the
-// level-4 planes are too small to fill the GPU with the strip kernel's
-// sequential blocks; the tile kernel is faster there (0.51 vs 0.86 ms/step).
+// Deepest level analysed by the strip kernel (PRNU_STRIP_MAXL, default: all).  With
+// the fp32 strips' fill rule (fewer, longer segments; 1 wave) and the direct left
+// mirror, the strip kernel also wins at level 4 (step 22.70 -> 22.55 ms, interleaved
+// A/B); the tile kernel k_analysis_shrink stays as the PRNU_STRIP=0 / A/B path.
 static int strip_max_level() {
-    static const int l = getenv("PRNU_STRIP_MAXL") ? atoi(getenv("PRNU_STRIP_MAXL")) : 3;
+    static const int l = getenv("PRNU_STRIP_MAXL") ? atoi(getenv("PRNU_STRIP_MAXL")) : 6;   // every level
     return l;
 }
 
