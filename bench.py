@@ -39,7 +39,7 @@ def parse():
     ap.add_argument("--width", type=int, default=1920)
     ap.add_argument("--depths", default="1,50")
     ap.add_argument("--batch", type=int, default=0,
-                    help="SDA frames denoised per wave at depth 1 (0: waves of <= 256 frames, equal sizes)")
+                    help="SDA frames denoised per wave at depth 1 (0: waves of <= 360 frames, equal sizes)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
@@ -310,8 +310,8 @@ def main():
     K_true = v.K.contiguous()
     torch.cuda.synchronize()
 
-    if args.batch <= 0:   # equal waves of at most 256 frames (1800 -> 8 waves of 225)
-        nw = -(-m // 256)
+    if args.batch <= 0:   # equal waves of at most 360 frames (1800 -> 5 waves of 360; measured best)
+        nw = -(-m // 360)
         args.batch = -(-m // nw)
     exs = {d: prnu.Extractor(H, W, d, batch=(args.batch if d == 1 else max(1, min(64, m // d))), device=dev)
            for d in depths}

@@ -1,5 +1,5 @@
 """Full-size parity (BASELINE.json configs 2-5) through the C ABI, in the launch
-configuration bench.py times (waves of 225 frames, three streams), against the fp64 oracle on
+configuration bench.py times (waves of 360 frames, three streams), against the fp64 oracle on
 outputs it can compute in seconds, plus properties that hold at any size.
 
 Tolerances as in test_gpu_parity.py."""
@@ -16,7 +16,7 @@ W_TOL = 1e-3
 K_TOL = 1e-3
 NCC_TOL = 1e-5
 PCE_RTOL = 1e-3
-BENCH_BATCH = 225   # bench.py default for 1800 frames: 8 equal waves
+BENCH_BATCH = 360   # bench.py default for 1800 frames: 5 equal waves
 
 
 @pytest.fixture(scope="module")
