@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--e2e-batch", type=int, default=64, help="frames per upload chunk / wave of the e2e run")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the NEXT-row measurements (f1, f2, f4)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the oracle sample")
@@ -503,7 +504,9 @@ def main():
     if not args.no_e2e:
         host = torch.empty((m, H, W), dtype=torch.uint8, pin_memory=True)
         host.copy_(frames)
-        mx = prnu.MultiExtractor(m, H, W, depths, batch=args.batch, device=dev)
+        # upload chunks = waves: smaller waves than the device-resident step's overlap the
+        # PCIe stream better (the first chunk's copy is not hidden)
+        mx = prnu.MultiExtractor(m, H, W, depths, batch=args.e2e_batch, device=dev)
         mx(host)
         torch.cuda.synchronize()
         barrier(world)
