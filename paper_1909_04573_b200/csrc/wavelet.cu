@@ -1270,7 +1270,9 @@ static int denoise_front(const TIn* in, long long in_bstride, int in_pitch, int 
             }
             const int tiles = ((s.NW + ST_X - 1) / ST_X) * ((s.NH + 31) / 32);
             // frames per CTA: enough CTAs for ~4 waves of 4 CTAs/SM, at least 4 frames to amortise the pipeline
-            s.frames_per_cta = std::max(4, std::min(nb, (int)((long long)tiles * nb / (148 * 4 * 4))));
+            static const int waves = getenv("PRNU_SYNTH_WAVES") ? atoi(getenv("PRNU_SYNTH_WAVES")) : 4;
+            static const int fmin = getenv("PRNU_SYNTH_FMIN") ? atoi(getenv("PRNU_SYNTH_FMIN")) : 4;
+            s.frames_per_cta = std::max(fmin, std::min(nb, (int)((long long)tiles * nb / (148 * 4 * waves))));
             dim3 grid((s.NW + ST_X - 1) / ST_X, (s.NH + 31) / 32, (nb + s.frames_per_cta - 1) / s.frames_per_cta);
             KTimer kt(kSynthName[l], st);
             k_synth_acc2<32, float, 0><<<grid, 256, sacc_smem_bytes<32, float, 0>(), st>>>(m, CUtensorMap{}, s);
