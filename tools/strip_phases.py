@@ -4,8 +4,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_1909_04573_b200 as prnu
 import synth
-v = synth.video("drift", 128, 1080, 1920, seed=0, device="cuda")
-ex = prnu.Extractor(1080, 1920, 1, batch=64)
+depth = int(os.environ.get("PHASE_DEPTH", "1"))   # 2: level 1 on the fp32 SDA-frame kernel
+v = synth.video("drift", 128 * depth, 1080, 1920, seed=0, device="cuda")
+ex = prnu.Extractor(1080, 1920, depth, batch=64)
 ex(v.frames); torch.cuda.synchronize()
 buf = (ctypes.c_ulonglong * 16)()
 prnu._lib.prnu_debug_strip_profile(buf, 1)
