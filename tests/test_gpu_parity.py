@@ -190,6 +190,26 @@ def test_extract_depth1_bit_identical_to_conventional(prnu):
     assert torch.equal(fp.sum_WI, num) and torch.equal(fp.sum_I2, den) and torch.equal(fp.K, K)
 
 
+@pytest.mark.parametrize("H,W,d", [(1081, 1919, 1), (270, 481, 3), (33, 1000, 1)])
+def test_extract_odd_sizes_bit_identical_to_conventional(prnu, H, W, d):
+    """Odd widths (u8 rows not 16-byte aligned: no tensor map, thread-loaded staging)
+    and odd heights: the fused extraction equals SDA + residual + accumulate +
+    finalize bit for bit, and matches the oracle's K (R-14)."""
+    m = 2 * d
+    fr = _rand_frames(m, H, W, H + W + d, 20, 236).cuda()
+    fp = prnu.extract_fingerprint(fr, d, batch=2)
+    S = prnu.sda_average(fr, d)
+    Wr = prnu.residual(S if d > 1 else fr)
+    num = torch.zeros((H, W), dtype=torch.float64, device="cuda")
+    den = torch.zeros_like(num)
+    prnu.fingerprint_accumulate(Wr, S, num, den)
+    assert torch.equal(fp.sum_I2, den)
+    assert torch.equal(fp.sum_WI, num) and torch.equal(fp.K, prnu.fingerprint_finalize(num, den))
+    if H * W <= 300_000:
+        K_ref, _, den_ref, n = oracle.extract_fingerprint(fr.cpu().numpy(), d)
+        assert k_metric(fp.K.cpu().numpy(), K_ref, den_ref, n)[0] <= K_TOL
+
+
 def test_extract_deterministic_across_batches(prnu):
     v = synth.video("drift", 40, 64, 128, seed=2)
     fr = v.frames.cuda()
