@@ -386,6 +386,7 @@ def main():
             if by is not None:
                 x["alg_bytes_per_launch"] = by / x["launches_per_step"]
                 x["alg_GBps"] = by / (x["ms_per_step"] / 1000.0) / 1e9
+                x["frac_hbm"] = x["alg_GBps"] / peak
         # dominant kernel = largest share of kernel time
         top = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
         kt = kernels[top]
