@@ -492,7 +492,19 @@ def main():
             del ex5
         del v5
         torch.cuda.empty_cache()
-        next_rows = {"f3_variants": f3, "c4_camera_id": c4, "c5_depth_sweep": c5,
+        # BASELINE config 3: 200 luma stills 4000x3000, depths 1, 5, 10, 20, 50
+        Y3, K3 = synth.stills(200, 3000, 4000, seed=0, device=dev)
+        c3 = {}
+        for d3 in (1, 5, 10, 20, 50):
+            ex3 = prnu.Extractor(3000, 4000, d3, 40 if d3 == 1 else max(1, 200 // d3), device=dev)
+            t3 = timed(lambda: ex3(Y3), reps=1)
+            n3 = 200 // d3
+            c3[str(d3)] = {"ms": t3, "denoisings": n3, "denoised_Mpx_per_s": n3 * 12.0 / (t3 / 1000.0),
+                           "ncc_vs_true_K": float(prnu.ncc(ex3(Y3).K, K3))}
+            del ex3
+        del Y3, K3
+        torch.cuda.empty_cache()
+        next_rows = {"f3_variants": f3, "c4_camera_id": c4, "c5_depth_sweep": c5, "c3_stills": c3,
                      "f2_wdft_ms_per_fingerprint": t_wdft / len(depths),
                      "f1_block_match_ms": t_blk, "f1_tiles": bplan.n_tiles,
                      "f4_rgb_to_luma_GBps": luma_bytes / (t_luma / 1000.0) / 1e9,
