@@ -424,7 +424,7 @@ def main():
     # ---- NEXT rows, measured outside the step: f2 WDFT of the two
     #      fingerprints, f1 500x500 block matching of the query, f4 RGB->luma
     next_rows = None
-    if not args.no_extras:
+    if not args.no_extras and rank == 0:   # measured outside the step, reported by rank 0 only
         def timed(fn, reps=5):
             fn()
             torch.cuda.synchronize()
