@@ -82,23 +82,36 @@ __global__ void __launch_bounds__(256) k_zm_rows(Src src, int H, int W, double* 
     if (threadIdx.x == 0) rowmean[y] = t / W;
 }
 
-// S:135 step 2: column means of the row-centred values.
+// S:135 step 2: column means of the row-centred values, in ZM_CHUNKS row chunks
+// (so the grid fills the GPU) whose partial sums are then added in chunk order:
+// a fixed summation order, independent of launch configuration (deterministic).
+constexpr int ZM_CHUNKS = 16;
 __global__ void __launch_bounds__(256) k_zm_cols(const double* __restrict__ X, const double* __restrict__ rowmean,
-                                                  int H, int W, double* __restrict__ colmean) {
+                                                  int H, int W, double* __restrict__ part) {
     __shared__ double sh[8][33];
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int x = blockIdx.x * 32 + tx;
+    const int y0 = (int)((long long)H * blockIdx.y / ZM_CHUNKS), y1 = (int)((long long)H * (blockIdx.y + 1) / ZM_CHUNKS);
     double s = 0.0;
     if (x < W)
-        for (int y = ty; y < H; y += 8) s += X[(size_t)y * W + x] - rowmean[y];
+        for (int y = y0 + ty; y < y1; y += 8) s += X[(size_t)y * W + x] - rowmean[y];
     sh[ty][tx] = s;
     __syncthreads();
     if (ty == 0 && x < W) {
         double t = 0.0;
 #pragma unroll
         for (int k = 0; k < 8; ++k) t += sh[k][tx];
-        colmean[x] = t / H;
+        part[(size_t)blockIdx.y * W + x] = t;
     }
+}
+__global__ void __launch_bounds__(256) k_zm_cols_final(const double* __restrict__ part, int H, int W,
+                                                        double* __restrict__ colmean) {
+    const int x = blockIdx.x * 256 + threadIdx.x;
+    if (x >= W) return;
+    double t = 0.0;
+#pragma unroll
+    for (int c = 0; c < ZM_CHUNKS; ++c) t += part[(size_t)c * W + x];
+    colmean[x] = t / H;
 }
 
 __global__ void __launch_bounds__(256) k_zm_apply(const double* __restrict__ X, const double* __restrict__ rowmean,
@@ -120,7 +133,7 @@ __global__ void __launch_bounds__(256) k_finalize_plain(FinalizeSrc src, long lo
 
 size_t zm_workspace_bytes(int H, int W) {
     return align_up(sizeof(double) * (size_t)H * W, 256) + align_up(sizeof(double) * H, 256) +
-           align_up(sizeof(double) * W, 256);
+           align_up(sizeof(double) * W, 256) + align_up(sizeof(double) * ZM_CHUNKS * W, 256);
 }
 
 template <class Src>
@@ -131,13 +144,16 @@ static int run_zero_mean(Src src, int H, int W, float* out, void* ws, cudaStream
     double* rm = reinterpret_cast<double*>(p);
     p += align_up(sizeof(double) * H, 256);
     double* cm = reinterpret_cast<double*>(p);
+    p += align_up(sizeof(double) * W, 256);
+    double* part = reinterpret_cast<double*>(p);
     {
         KTimer kt("zm_rows", st);
         k_zm_rows<Src><<<H, 256, 0, st>>>(src, H, W, X, rm);
     }
     {
         KTimer kt("zm_cols", st);
-        k_zm_cols<<<(W + 31) / 32, 256, 0, st>>>(X, rm, H, W, cm);
+        k_zm_cols<<<dim3((W + 31) / 32, ZM_CHUNKS), 256, 0, st>>>(X, rm, H, W, part);
+        k_zm_cols_final<<<(W + 255) / 256, 256, 0, st>>>(part, H, W, cm);
     }
     long long P = (long long)H * W;
     long long blocks = std::min<long long>((P + 255) / 256, 148LL * 16);
@@ -145,7 +161,7 @@ static int run_zero_mean(Src src, int H, int W, float* out, void* ws, cudaStream
         KTimer kt("zm_apply", st);
         k_zm_apply<<<(unsigned)blocks, 256, 0, st>>>(X, rm, cm, H, W, out);
     }
-    count_launch(3);
+    count_launch(4);
     return check_launch("zero_mean");
 }
 
