@@ -20,6 +20,7 @@ if os.environ.get("PRNU_DEBUG"):
     FLAGS.append("-DPRNU_DEBUG")
 for _flag in os.environ.get("PRNU_NVCC_DEFS", "").split():
     FLAGS.append("-D" + _flag)
+FLAGS += os.environ.get("PRNU_NVCC_FLAGS", "").split()   # A/B: extra nvcc flags
 
 
 def _stale(target: str, deps) -> bool:
