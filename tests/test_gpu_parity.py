@@ -477,3 +477,22 @@ def test_camera_batch_extractor_matches_single(prnu):
     K = prnu.CameraBatchExtractor(64, 96, 4, 3, streams=3)(vids)
     for c in range(5):
         assert torch.equal(K[c], prnu.extract_fingerprint(vids[c], 4, batch=3).K)
+
+
+def test_residual_random_shapes(prnu):
+    """24 seeded random plane shapes (16..420 x 16..700), levels 1..4, u8 and fp32
+    input: every output against the oracle (catches staging/segment/strip edge cases)."""
+    g = np.random.default_rng(2024)
+    for case in range(24):
+        H, W = int(g.integers(16, 421)), int(g.integers(16, 701))
+        lv = int(g.integers(1, 5))
+        while H < (1 << lv) or W < (1 << lv):
+            lv -= 1
+        p = prnu.DenoiseParams(levels=lv)
+        fr = torch.from_numpy(g.integers(0, 256, (2, H, W), dtype=np.uint8))
+        src = fr.cuda() if case % 2 == 0 else fr.float().cuda()
+        got = prnu.residual(src, p).cpu().numpy()
+        for i in range(2):
+            ref = oracle.residual(fr[i].numpy().astype(np.float32), levels=lv)
+            err = np.abs(got[i] - ref).max()
+            assert err <= W_TOL, (case, H, W, lv, i, err)
