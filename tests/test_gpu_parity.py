@@ -496,3 +496,20 @@ def test_residual_random_shapes(prnu):
             ref = oracle.residual(fr[i].numpy().astype(np.float32), levels=lv)
             err = np.abs(got[i] - ref).max()
             assert err <= W_TOL, (case, H, W, lv, i, err)
+
+
+def test_extract_random_configs(prnu):
+    """10 seeded random extraction configurations (size, frame count, depth, batch):
+    K against the oracle (R-14), n_sda = floor(m/d), sum_I2 bit-exact."""
+    g = np.random.default_rng(77)
+    for case in range(10):
+        H, W = int(g.integers(16, 201)), int(g.integers(16, 241))
+        m = int(g.integers(2, 41))
+        d = int(g.integers(1, m + 1))
+        batch = int(g.integers(1, 17))
+        fr = torch.from_numpy(g.integers(10, 246, (m, H, W), dtype=np.uint8))
+        fp = prnu.extract_fingerprint(fr.cuda(), d, batch=batch)
+        K_ref, _, den, n = oracle.extract_fingerprint(fr.numpy(), d)
+        assert fp.n_sda == n == m // d, (case, m, d)
+        np.testing.assert_array_equal(fp.sum_I2.cpu().numpy(), den)
+        assert k_metric(fp.K.cpu().numpy(), K_ref, den, n)[0] <= K_TOL, (case, H, W, m, d, batch)
