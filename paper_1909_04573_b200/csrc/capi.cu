@@ -100,7 +100,9 @@ int run_residual(const TIn* in, int nb, int H, int W, const Pyramid& p, const Sh
 template <typename TIn>
 int run_residual_accumulate(const TIn* in, const TIn* I, int nb, int H, int W, const Pyramid& p,
                             const ShrinkParams& sp, double* num, double* den, float* ws_pyr, cudaStream_t st,
-                            cudaEvent_t acc_wait, cudaEvent_t acc_done, long long frame_stride);
+                            cudaEvent_t acc_wait, cudaEvent_t acc_done, long long frame_stride, int in_pitch = 0);
+int launch_pad_rows_u8(const uint8_t* src, long long nb, int H, int W, long long src_stride, uint8_t* dst, int Wp,
+                       cudaStream_t st);
 int launch_accumulate(const float* W, const float* I, int batch, long long P, double* num, double* den,
                       cudaStream_t st);
 size_t zm_workspace_bytes(int H, int W);
@@ -162,9 +164,14 @@ static int extract_streams() {
     return n;
 }
 
+// u8 frames whose rows are not 16-byte multiples cannot be TMA-staged: such waves are
+// first copied to rows of align16(W) bytes (one HBM pass) so both the analysis and the
+// accumulation keep their TMA paths.
+static int pad_pitch_u8(int W) { return (int)align_up((size_t)W, 16); }
 static size_t extract_wave_ws(int H, int W, int batch, int64_t depth, const Pyramid& pyr) {
     size_t s = align_up(sizeof(float) * pyramid_floats_per_frame(pyr) * (size_t)batch, 256);
     if (depth > 1) s += align_up(sizeof(float) * (size_t)H * W * batch, 256);
+    else if (W % 16) s += align_up((size_t)H * pad_pitch_u8(W) * batch, 256);
     return s;
 }
 
@@ -188,9 +195,19 @@ static int extract_chunk(const uint8_t* frames, int64_t nb, int H, int W, int64_
     float* pyr_ws = reinterpret_cast<float*>(ws);
     size_t pyr_bytes = align_up(sizeof(float) * pyramid_floats_per_frame(pyr) * (size_t)nb, 256);
     const long long P = (long long)H * W;
-    if (depth == 1 || depth < 0)
+    if (depth == 1 || depth < 0) {
+        const long long fstride = depth < 0 ? -depth * P : P;
+        if (W % 16) {   // pitched copy (see extract_wave_ws)
+            const int Wp = pad_pitch_u8(W);
+            uint8_t* padded = reinterpret_cast<uint8_t*>(ws + pyr_bytes);
+            int rc = launch_pad_rows_u8(frames, nb, H, W, fstride, padded, Wp, st);
+            if (rc) return rc;
+            return run_residual_accumulate<uint8_t>(padded, padded, (int)nb, H, W, pyr, sp, num, den, pyr_ws, st,
+                                                    acc_wait, acc_done, (long long)H * Wp, Wp);
+        }
         return run_residual_accumulate<uint8_t>(frames, frames, (int)nb, H, W, pyr, sp, num, den, pyr_ws, st,
-                                                acc_wait, acc_done, depth < 0 ? -depth * P : P);
+                                                acc_wait, acc_done, fstride);
+    }
     float* S = reinterpret_cast<float*>(ws + pyr_bytes);
     int rc = launch_sda_average(frames, nb, P, (int)depth, S, st);
     if (rc) return rc;

@@ -82,6 +82,24 @@ __global__ void __launch_bounds__(256) k_sda_average_scalar(const uint8_t* __res
     }
 }
 
+// Pitched copy of u8 frames (rows of W bytes -> rows of Wp bytes, Wp a multiple of 16)
+// so that unaligned frame widths can still be TMA-staged; one CTA per (frame, row).
+__global__ void __launch_bounds__(256) k_pad_rows_u8(const uint8_t* __restrict__ src, int H, int W,
+                                                      long long src_stride, uint8_t* __restrict__ dst, int Wp) {
+    const long long row = blockIdx.x;   // frame * H + y
+    const long long f = row / H, y = row - f * H;
+    const uint8_t* s = src + f * src_stride + y * W;
+    uint8_t* d = dst + row * Wp;
+    for (int x = threadIdx.x; x < Wp; x += 256) d[x] = x < W ? s[x] : 0;
+}
+
+int launch_pad_rows_u8(const uint8_t* src, long long nb, int H, int W, long long src_stride, uint8_t* dst, int Wp,
+                       cudaStream_t st) {
+    k_pad_rows_u8<<<(unsigned)(nb * H), 256, 0, st>>>(src, H, W, src_stride, dst, Wp);
+    count_launch();
+    return check_launch("k_pad_rows_u8");
+}
+
 int launch_sda_average(const uint8_t* frames, long long n_groups, long long P, int d, float* out,
                        cudaStream_t st) {
     if (n_groups <= 0) return PRNU_OK;

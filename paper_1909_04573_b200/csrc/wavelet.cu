@@ -1336,9 +1336,10 @@ int run_residual(const TIn* in, int nb, int H, int W, const Pyramid& p, const Sh
 template <typename TIn>
 int run_residual_accumulate(const TIn* in, const TIn* I, int nb, int H, int W, const Pyramid& p,
                             const ShrinkParams& sp, double* num, double* den, float* ws_pyr, cudaStream_t st,
-                            cudaEvent_t acc_wait, cudaEvent_t acc_done, long long frame_stride) {
+                            cudaEvent_t acc_wait, cudaEvent_t acc_done, long long frame_stride, int in_pitch) {
+    if (in_pitch <= 0) in_pitch = W;   // elements between the rows of `in` and `I`
     PyramidBuffers pb = carve_pyramid(p, ws_pyr, nb);
-    int rc = denoise_front<TIn>(in, frame_stride, W, nb, p, pb, sp, st);
+    int rc = denoise_front<TIn>(in, frame_stride, in_pitch, nb, p, pb, sp, st);
     if (rc) return rc;
     SynthMaps m;
     if ((rc = synth_maps(p, pb, 1, nb, p.levels > 1, &m))) return rc;
@@ -1349,7 +1350,7 @@ int run_residual_accumulate(const TIn* in, const TIn* I, int nb, int H, int W, c
     s.nb = nb;
     s.I = I;
     s.i_bstride = frame_stride;
-    s.i_pitch = W;
+    s.i_pitch = in_pitch;
     s.num = num;
     s.den = den;
     s.acc_pitch = W;
@@ -1370,10 +1371,10 @@ int run_residual_accumulate(const TIn* in, const TIn* I, int nb, int H, int W, c
     CUtensorMap imap;
     SynthMaps m2;
     const size_t es = sizeof(TIn);
-    bool v2 = sacc2 && ((size_t)W * es) % 16 == 0 && ((size_t)frame_stride * es) % 16 == 0 &&
+    bool v2 = sacc2 && ((size_t)in_pitch * es) % 16 == 0 && ((size_t)frame_stride * es) % 16 == 0 &&
               ((uintptr_t)I % 16) == 0 &&
               encode_tensor_map_3d(&imap, sizeof(TIn) == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                                   es, I, (uint64_t)W, (uint64_t)H, (uint64_t)nb, (uint64_t)W * es,
+                                   es, I, (uint64_t)W, (uint64_t)H, (uint64_t)nb, (uint64_t)in_pitch * es,
                                    (uint64_t)frame_stride * es, ST_X, TYsel);
     if (v2) {
         const uint64_t pitch = (uint64_t)p.pitch[1] * 4, plane = (uint64_t)pb.bstride[1] * 4;
@@ -1424,9 +1425,9 @@ template int run_residual<uint8_t>(const uint8_t*, int, int, int, const Pyramid&
                                    float*, cudaStream_t);
 template int run_residual_accumulate<float>(const float*, const float*, int, int, int, const Pyramid&,
                                             const ShrinkParams&, double*, double*, float*, cudaStream_t, cudaEvent_t,
-                                            cudaEvent_t, long long);
+                                            cudaEvent_t, long long, int);
 template int run_residual_accumulate<uint8_t>(const uint8_t*, const uint8_t*, int, int, int, const Pyramid&,
                                               const ShrinkParams&, double*, double*, float*, cudaStream_t,
-                                              cudaEvent_t, cudaEvent_t, long long);
+                                              cudaEvent_t, cudaEvent_t, long long, int);
 
 }  // namespace prnu
