@@ -122,8 +122,13 @@ struct StripStage<uint8_t> {
 };
 template <>
 struct StripStage<float> {
-    static constexpr int BOXW = 136;   // floats (544 B, a 16-B multiple)
-    static constexpr int LOGW = 264;
+#ifndef PRNU_F32_BOXW
+#define PRNU_F32_BOXW 140
+#endif
+    // floats (a 16-B multiple); 140 == 12 mod 32 words: the row pass's LDS.128 over 8 rows
+    // is conflict-free (136 == 8 mod 32 was 2-way)
+    static constexpr int BOXW = PRNU_F32_BOXW;
+    static constexpr int LOGW = 128 + PRNU_F32_BOXW;
 };
 
 template <typename T>
@@ -165,7 +170,7 @@ __device__ __forceinline__ void stg_row22(const uint8_t* s, int r, int g, float 
     constexpr int BW = StripStage<uint8_t>::BOXW;
     const uint8_t* src = s + (g < 8 ? r * BW + 16 * g : SR_IR * BW + r * BW + 16 * g - 128);
     const uint4 w0 = *reinterpret_cast<const uint4*>(src);
-    const uint2 w1 = *reinterpret_cast<const uint2*>(src + 16);
+    const uint2 w1 = *reinterpret_cast<const uint2*>(src + 16);   // (a 16-byte load here: +0.3%)
     const uint32_t w[6] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y};
 #pragma unroll
     for (int k = 0; k < 22; k += 2) {   // exact byte -> float (2^23 trick), two at a time (FADD2)
@@ -359,7 +364,10 @@ __global__ void __launch_bounds__(SR_NT, MINB) k_analysis_strip(const __grid_con
     };
     // every block is staged by TMA (a 16-row box pair at box_y) when the plane has at
     // least 16 rows; otherwise (and without a tensor map) the threads load the rows
-    auto tma_ok = [&](int i) { return a.use_tma && a.NH >= SR_IR; };
+    // planes of 32+ rows: every block's mirrored rows lie in one 16-row window (one
+    // reflection, rows -14 .. NH + 28); shorter planes stage their mirrored blocks by
+    // threads (the mirrored span can wrap through both edges)
+    auto tma_ok = [&](int i) { return a.use_tma && (refl1 || (a.NH >= SR_IR && inside(i))); };
     auto issue = [&](int i) {   // thread 0 only
         const int k = stg_of(i);
         T* s = stg0 + k * STG;

@@ -513,3 +513,15 @@ def test_extract_random_configs(prnu):
         assert fp.n_sda == n == m // d, (case, m, d)
         np.testing.assert_array_equal(fp.sum_I2.cpu().numpy(), den)
         assert k_metric(fp.K.cpu().numpy(), K_ref, den, n)[0] <= K_TOL, (case, H, W, m, d, batch)
+
+
+@pytest.mark.parametrize("H,W", [(100, 256), (100, 336), (120, 512), (70, 400)])
+def test_residual_short_deep_levels(prnu, H, W):
+    """Deep levels with 16..31 input rows (level 4 of H = 100: 18 rows), where a block's
+    mirrored rows can wrap through both plane edges: thread-staged, all outputs vs the oracle."""
+    I = _textured(2, H, W, H + 3 * W)
+    for src in (torch.from_numpy(I).cuda(), torch.from_numpy(np.round(I).astype(np.uint8)).cuda()):
+        got = prnu.residual(src).cpu().numpy()
+        for i in range(2):
+            ref = oracle.residual(src[i].cpu().numpy().astype(np.float32))
+            assert np.abs(got[i] - ref).max() <= W_TOL
