@@ -162,6 +162,7 @@ struct StripArgs {
 template <typename T>
 __device__ __forceinline__ float stg_at(const T* s, int r, int x) {
     constexpr int BW = StripStage<T>::BOXW;
+    PRNU_DCHECK(r >= 0 && r < SR_IR && x >= 0 && x < StripStage<T>::LOGW);
     return x < BW ? (float)s[r * BW + x] : (float)s[SR_IR * BW + r * BW + x - 128];
 }
 
@@ -298,6 +299,7 @@ __global__ void __launch_bounds__(SR_NT, MINB) k_analysis_strip(const __grid_con
     // mirrored halo columns outside the subband read their partner (R-4)
     const int src_t = (gc < 0 || gc >= a.nW) ? min(max(mirror(gc, a.nW) - cx0 + 4, 0), SR_RW - 1) : t;
     const int pos = src_t;   // row-buffer column (plain layout)
+    PRNU_DCHECK(pos >= 0 && pos < SR_RW);
     const bool inner = (t >= 4) && (t < 4 + a.O) && (gc < a.nW);
     // row-pass items of this thread: row rr of groups ga and ga + 8 (skipped when
     // every column of the group lies beyond the subband)
@@ -420,6 +422,7 @@ __global__ void __launch_bounds__(SR_NT, MINB) k_analysis_strip(const __grid_con
     // Row pass (along x) of row rr < nr of the staged rows into the row buffer
     // (regA): lo plane rows [0, 16), hi plane rows [16, 32), columns permuted.
     auto rowpass = [&](const T* s, int prow, int nr) {   // prow: physical staged row of row rr
+        PRNU_DCHECK(rr >= nr || (prow >= 0 && prow < SR_IR));
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int g = ga + 8 * h;
@@ -482,6 +485,7 @@ __global__ void __launch_bounds__(SR_NT, MINB) k_analysis_strip(const __grid_con
             SPROBE(11);   // TMA wait
             phase ^= 1u << sk;
             prow = inside(i) ? rr : mirror_row(y0_of(i) + rr) - box_y(i);
+            PRNU_DCHECK(rr >= (pro ? 6 : SR_IR) || (prow >= 0 && prow < SR_IR));
             if (edge) {   // sources in the plane, destinations outside it: no hazard inside the pass
 #pragma unroll
                 for (int k = 0; k < SR_FIX; ++k) {
