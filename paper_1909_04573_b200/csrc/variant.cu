@@ -320,6 +320,7 @@ __global__ void __launch_bounds__(128) k_var_row_ana(VarPass p) {
 #pragma unroll
             for (int i = 0; i < T; ++i) {
                 // decimated: x[2k - (T-2) + i] = E/O[u + i/2]; undecimated: x[k - s (T-1-i)] = E[u + s i]
+                PRNU_DCHECK((MODE == VM_SWT ? u + p.s * i : u + i / 2) < nst);
                 const float v = MODE == VM_SWT ? sE[u + p.s * i] : ((i & 1) ? sO[u + i / 2] : sE[u + i / 2]);
                 const float g = (i & 1) ? -H[T - 1 - i] : H[T - 1 - i];
                 a = fmaf(H[i], v, a);

@@ -901,6 +901,7 @@ __global__ void __launch_bounds__(256, PRNU_SACC_MINB) k_synth_acc2(const __grid
         // column pass: Lx = synth_y(A, ad), Hx = synth_y(da, dd); item = (coefficient column k, 4 output rows)
         for (int it = tid; it < NITEM; it += 256) {
             const int k = NITEM <= 256 ? ck : item_k(it), sg = NITEM <= 256 ? csg : item_sg(it);
+            PRNU_DCHECK(k < SC_X && 2 * sg + 4 < CY && 4 * sg + 3 < TY);
             float va[5], vda[5], vad[5], vdd[5];
 #pragma unroll
             for (int m = 0; m < 5; ++m) {
