@@ -96,7 +96,7 @@ int launch_rgb_to_luma(const uint8_t* rgb, long long n, long long P, int layout,
 size_t pyramid_floats_per_frame(const Pyramid& p);
 template <typename TIn>
 int run_residual(const TIn* in, int nb, int H, int W, const Pyramid& p, const ShrinkParams& sp, float* W_out,
-                 float* ws_pyr, cudaStream_t st);
+                 float* ws_pyr, cudaStream_t st, int in_pitch = 0);
 template <typename TIn>
 int run_residual_accumulate(const TIn* in, const TIn* I, int nb, int H, int W, const Pyramid& p,
                             const ShrinkParams& sp, double* num, double* den, float* ws_pyr, cudaStream_t st,
@@ -146,8 +146,13 @@ static size_t variant_ws(int batch, int H, int W, const prnu_denoise_params* p, 
            zm_workspace_bytes(H, W);
 }
 
+static int pad_pitch_u8(int W);
+static size_t residual_pad_bytes(int batch, int H, int W) {   // re-pitched u8 planes (unaligned widths)
+    return W % 16 ? align_up((size_t)H * pad_pitch_u8(W) * batch, 256) : 0;
+}
 static size_t residual_ws(int batch, int H, int W, const Pyramid& pyr) {
-    return align_up(sizeof(float) * pyramid_floats_per_frame(pyr) * (size_t)batch, 256) + zm_workspace_bytes(H, W);
+    return align_up(sizeof(float) * pyramid_floats_per_frame(pyr) * (size_t)batch, 256) + zm_workspace_bytes(H, W) +
+           residual_pad_bytes(batch, H, W);
 }
 
 // Waves of SDA frames alternate between kExtractStreams streams (each with its
@@ -227,7 +232,18 @@ static int residual_impl(const TIn* planes, int batch, int H, int W, const prnu_
     if (ws_bytes < residual_ws(batch, H, W, pyr)) return fail(PRNU_WORKSPACE_TOO_SMALL, "workspace too small");
     cudaStream_t st = as_stream(stream);
     float* pyr_ws = reinterpret_cast<float*>(ws);
-    if ((rc = run_residual<TIn>(planes, batch, H, W, pyr, sp, W_out, pyr_ws, st))) return rc;
+    if (sizeof(TIn) == 1 && W % 16) {   // u8 rows that TMA cannot stage: re-pitch them first
+        const int Wp = pad_pitch_u8(W);
+        uint8_t* padded = reinterpret_cast<uint8_t*>(ws) + residual_ws(batch, H, W, pyr) -
+                          residual_pad_bytes(batch, H, W);
+        if ((rc = launch_pad_rows_u8(reinterpret_cast<const uint8_t*>(planes), batch, H, W, (long long)H * W, padded,
+                                     Wp, st)))
+            return rc;
+        if ((rc = run_residual<TIn>(reinterpret_cast<const TIn*>(padded), batch, H, W, pyr, sp, W_out, pyr_ws, st, Wp)))
+            return rc;
+    } else if ((rc = run_residual<TIn>(planes, batch, H, W, pyr, sp, W_out, pyr_ws, st))) {
+        return rc;
+    }
     if (zero_mean) {
         char* zm = reinterpret_cast<char*>(ws) +
                    align_up(sizeof(float) * pyramid_floats_per_frame(pyr) * (size_t)batch, 256);

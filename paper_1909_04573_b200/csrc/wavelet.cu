@@ -1292,9 +1292,10 @@ static int denoise_front(const TIn* in, long long in_bstride, int in_pitch, int 
 
 template <typename TIn>
 int run_residual(const TIn* in, int nb, int H, int W, const Pyramid& p, const ShrinkParams& sp, float* W_out,
-                 float* ws_pyr, cudaStream_t st) {
+                 float* ws_pyr, cudaStream_t st, int in_pitch) {
+    if (in_pitch <= 0) in_pitch = W;
     PyramidBuffers pb = carve_pyramid(p, ws_pyr, nb);
-    int rc = denoise_front<TIn>(in, (long long)H * W, W, nb, p, pb, sp, st);
+    int rc = denoise_front<TIn>(in, (long long)H * in_pitch, in_pitch, nb, p, pb, sp, st);
     if (rc) return rc;
     SynthMaps m;
     if ((rc = synth_maps(p, pb, 1, nb, p.levels > 1, &m))) return rc;
@@ -1421,9 +1422,9 @@ int run_residual_accumulate(const TIn* in, const TIn* I, int nb, int H, int W, c
 }
 
 template int run_residual<float>(const float*, int, int, int, const Pyramid&, const ShrinkParams&, float*, float*,
-                                 cudaStream_t);
+                                 cudaStream_t, int);
 template int run_residual<uint8_t>(const uint8_t*, int, int, int, const Pyramid&, const ShrinkParams&, float*,
-                                   float*, cudaStream_t);
+                                   float*, cudaStream_t, int);
 template int run_residual_accumulate<float>(const float*, const float*, int, int, int, const Pyramid&,
                                             const ShrinkParams&, double*, double*, float*, cudaStream_t, cudaEvent_t,
                                             cudaEvent_t, long long, int);
