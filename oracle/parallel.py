@@ -59,3 +59,50 @@ def sample(frames: np.ndarray, depths, budget_s: float, workers: int | None = No
     finally:
         shm.close()
         shm.unlink()
+
+
+def _chunk(args):
+    import oracle
+    depth, start, stop = args
+    _, num, den, ns = oracle.extract_fingerprint(_FR[start:stop], depth, zero_mean=False)
+    return num, den, ns
+
+
+def extract_fingerprint_chunked(frames: np.ndarray, depth: int, workers: int | None = None,
+                                chunks: int | None = None):
+    """The oracle's fingerprint of a long stack, computed by worker processes.
+
+    The n_s = floor(m/d) SDA groups are split into `chunks` contiguous runs of
+    whole groups (the m mod d remainder is dropped); each worker runs
+    oracle.extract_fingerprint on its run and returns its partial fp64 sums
+    (sum W*I, sum I^2 over its groups, ascending); the partials are added in run
+    order and finalized with oracle.finalize.  This is the oracle's own
+    composition (the MLE numerator and denominator are sums over the
+    SDA frames), only the fp64 additions are regrouped (a relative change of the
+    order of 1e-16, far below every tolerance).  Returns (K, num, den, n_s)."""
+    import oracle
+    frames = np.ascontiguousarray(frames, dtype=np.uint8)
+    m = frames.shape[0]
+    ns = oracle.sda_groups(m, depth)
+    if ns < 0:
+        raise oracle.OracleError(3, "extract_fingerprint_chunked")
+    workers = workers or os.cpu_count() or 1
+    chunks = min(ns, chunks or workers)
+    bounds = [round(ns * k / chunks) for k in range(chunks + 1)]
+    jobs = [(depth, bounds[k] * depth, bounds[k + 1] * depth) for k in range(chunks) if bounds[k + 1] > bounds[k]]
+    shm = shared_memory.SharedMemory(create=True, size=frames.nbytes)
+    try:
+        np.ndarray(frames.shape, dtype=np.uint8, buffer=shm.buf)[:] = frames
+        ctx = mp.get_context("spawn")
+        with ctx.Pool(min(workers, len(jobs)), initializer=_init, initargs=(shm.name, frames.shape)) as pool:
+            parts = pool.map(_chunk, jobs, chunksize=1)
+    finally:
+        shm.close()
+        shm.unlink()
+    num = np.zeros(frames.shape[1:])
+    den = np.zeros(frames.shape[1:])
+    for pn, pd, _ in parts:   # in run order
+        num += pn
+        den += pd
+    assert sum(p[2] for p in parts) == ns
+    return oracle.finalize(num, den), num, den, ns

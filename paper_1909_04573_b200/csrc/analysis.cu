@@ -1,0 +1,831 @@
+// analysis.cu — one DWT analysis level (a2) with the local-variance MAP/Wiener
+// shrink of its three detail subbands fused (a3): the column-streaming strip
+// kernel, with the 8-tap Daubechies filter pair applied as a LIFTING cascade.
+//
+// Operation (R-2, R-4..R-7): for one level,
+//   a[k] = sum_i H_[i] x[2k-6+i],  d[k] = sum_i G_[i] x[2k-6+i]   along rows,
+// then along columns (R-6), on the half-sample symmetric extension of the
+// plane (R-4); the detail subbands da, ad, dd are then shrunk in the noise
+// domain: c - F(c) = c s0 / max(min_w mean_w(c^2), s0) (R-7, R-10).
+//
+// Lifting.  With e[m] = x[2m], o[m] = x[2m+1] (polyphase components), the
+// polyphase matrix of (H_, G_) factors (Daubechies-Sweldens; constants from the
+// factorisation in fp64, tools/lifting.py) into
+//   e1[m] = e[m]  - C1  o[m]
+//   o1[m] = o[m]  + C2A e1[m]   - C2B e1[m+1]
+//   e2[m] = e1[m] + C3A o1[m-1] - C3B o1[m]
+//   o2[m] = o1[m] + C4A e2[m]   + C4B e2[m+1]
+//   e3[m] = e2[m] - C5  o2[m-1]
+//   a[k]  = KA o2[k-2],   d[k] = KD e3[k-1]          (KA KD = 1)
+// i.e. 8 multiply-adds per (a, d) pair instead of 16: the FP32 pipe (not HBM)
+// bounds this kernel, so halving the filter's lane-operations is
+// the lever.  The KA/KD scales are folded: rows store (o2, e3) unscaled; after
+// the column pass aa = KA^2 A.x, da = A.y, ad = D.x, dd = KD^2 D.y (A = column
+// o2, D = column e3), so only LL takes one multiply; the dd scale enters the
+// shrink through per-subband window / sigma constants.
+//
+// Organisation (per CTA of 128 threads = one vertical strip of <= O output
+// coefficient columns plus a 4-column halo each side, one thread per region
+// column, walking down a segment of output rows in blocks of 8 coefficient rows):
+//   * 16 input rows per block arrive by TMA (two boxes, a ring of staging
+//     buffers two blocks ahead); mirrored border rows through a row remap,
+//     out-of-plane columns through an in-smem fix-up (R-4);
+//   * row pass (cooperative; u8: pairs of outputs (k, k+4) through packed
+//     FFMA2 with immediate coefficients, the u8 -> fp32 conversion building the
+//     pairs directly; fp32: scalar lifting) -> row buffer, (k, k+4) adjacent;
+//   * column pass (per thread, streaming): the lifting recurrences along y on
+//     the (lo, hi) pair of the thread's column, carrying 4 pairs of state
+//     between rows; coefficient rows come out in order;
+//   * squares of the details in a 16-row register ring (da scalar, (ad, dd) as
+//     a pair), nested vertical window sums 3/5/7/9 -> shared memory;
+//   * H pass (cooperative, 8 outputs of one row per thread): sliding horizontal
+//     sums ((ad, dd) packed FADD2), window means, Wiener factor, store.
+#include <cstdlib>
+#include <cstring>
+
+#include "common.cuh"
+#include "tma.cuh"
+
+namespace prnu {
+
+// ---- lifting constants (fp64 factorisation of R-2's filter, rounded to fp32)
+#define LF_C1 0.3222758880002811f
+#define LF_C2A 0.29195312600347534f
+#define LF_C2B 1.117123605116217f
+#define LF_C3A 0.5400282834197139f
+#define LF_C3B 1.6889170665560485f
+#define LF_C4A 0.5547946968043377f
+#define LF_C4B 0.006617338010625356f
+#define LF_C5 0.31909219261386207f
+#define LF_KA 2.6337752658977225f
+#define LF_KD 0.3796831160760221f
+#define LF_KA2 6.936772143131393f      // KA^2
+#define LF_KD2 0.14415926620330932f    // KD^2
+#define LF_KD4 0.020781894001587787f   // KD^4
+
+constexpr int AL_NT = 128;   // threads per CTA == region columns
+constexpr int AL_BK = 8;     // coefficient rows per block
+constexpr int AL_IR = 16;    // input rows per block
+constexpr int AL_RBP = 122;  // row-buffer pitch (floats, == 2 mod 4: conflict-free STS.64, lanes over rows)
+
+template <typename T>
+struct AlCfg;
+template <>
+struct AlCfg<uint8_t> {
+    static constexpr int OMAX = 112;   // output columns per strip (region 120)
+    static constexpr int P1 = 124;     // da planes pitch (floats, == 28 mod 32: LDS.128 over 8 rows conflict-free)
+    static constexpr int P2 = 122;     // (ad, dd) planes pitch (float2; 2 P2 == 20 mod 32)
+    static constexpr int NSTG = 3;     // staging buffers (TMA two blocks ahead)
+    static constexpr int BOXW = 144;   // staged bytes per row and box
+    static constexpr int MINB = 3;
+};
+template <>
+struct AlCfg<float> {
+    static constexpr int OMAX = 104;   // region 112
+    static constexpr int P1 = 116;     // == 20 mod 32
+    static constexpr int P2 = 114;     // 2 P2 == 4 mod 32
+    static constexpr int NSTG = 1;
+    static constexpr int BOXW = 140;   // floats (12 mod 32 words)
+    static constexpr int MINB = 3;
+};
+template <typename T>
+__host__ __device__ constexpr int al_logw() { return 128 + AlCfg<T>::BOXW; }
+template <typename T>
+__host__ __device__ constexpr int al_stage_elems() { return 2 * AL_IR * AlCfg<T>::BOXW; }
+template <typename T>
+__host__ __device__ constexpr int al_da_floats() { return 5 * AL_BK * AlCfg<T>::P1; }
+template <typename T>
+__host__ __device__ constexpr int al_pr_floats() { return 2 * 5 * AL_BK * AlCfg<T>::P2; }
+template <typename T>
+constexpr size_t al_smem_bytes() {
+    return AlCfg<T>::NSTG * al_stage_elems<T>() * sizeof(T) + sizeof(float) * (al_da_floats<T>() + al_pr_floats<T>()) +
+           32;
+}
+static_assert(2 * AL_IR * AL_RBP <= 5 * AL_BK * AlCfg<float>::P1, "row buffer inside the da planes");
+static_assert(AlCfg<uint8_t>::OMAX + 8 <= AlCfg<uint8_t>::P2 && AlCfg<float>::OMAX + 8 <= AlCfg<float>::P2, "V planes");
+static_assert(al_smem_bytes<uint8_t>() <= 75 * 1024 && al_smem_bytes<float>() <= 75 * 1024, "3 CTAs per SM");
+
+struct AlArgs {
+    const void* in;
+    long long in_bstride;   // elements between frames
+    int in_pitch;           // elements per row
+    int NH, NW;             // input plane
+    float* ll;              // approximation out (nullable: coarsest level)
+    float* d0;              // da = lo_y(hi_x)
+    float* d1;              // ad = hi_y(lo_x)
+    float* d2;              // dd = hi_y(hi_x)
+    long long out_bstride;
+    int out_pitch;
+    int nH, nW;             // subband
+    ShrinkParams sp;
+    int O;                  // output columns per strip (multiple of 8)
+    int SH;                 // output rows per segment (multiple of 8)
+    int use_tma;
+};
+
+// packed fp32 helpers: {k, k} * b + c with k an immediate (FFMA2 imm form)
+__device__ __forceinline__ float2 lf2(float k, float2 b, float2 c) {
+    unsigned long long rb = *reinterpret_cast<const unsigned long long*>(&b);
+    unsigned long long rc = *reinterpret_cast<const unsigned long long*>(&c);
+    unsigned long long r;
+    asm("{.reg .b64 kk; mov.b64 kk, {%1, %1}; fma.rn.f32x2 %0, kk, %2, %3;}" : "=l"(r) : "f"(k), "l"(rb), "l"(rc));
+    return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+    unsigned long long ra = *reinterpret_cast<const unsigned long long*>(&a);
+    unsigned long long rb = *reinterpret_cast<const unsigned long long*>(&b);
+    unsigned long long r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(ra), "l"(rb));
+    return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+    unsigned long long ra = *reinterpret_cast<const unsigned long long*>(&a);
+    unsigned long long rb = *reinterpret_cast<const unsigned long long*>(&b);
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(ra), "l"(rb));
+    return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+    unsigned long long ra = *reinterpret_cast<const unsigned long long*>(&a);
+    unsigned long long rb = *reinterpret_cast<const unsigned long long*>(&b);
+    unsigned long long r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(ra), "l"(rb));
+    return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float al_rcp(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+// per-subband constants of the (ad, dd) pair: window means (1/w^2, KD^4/w^2), sigma (s0, KD^2 s0) set per launch
+__constant__ float2 c_al_w[4] = {{1.0f / 9.0f, LF_KD4 / 9.0f},
+                                 {1.0f / 25.0f, LF_KD4 / 25.0f},
+                                 {1.0f / 49.0f, LF_KD4 / 49.0f},
+                                 {1.0f / 81.0f, LF_KD4 / 81.0f}};
+
+template <typename T>
+__device__ __forceinline__ float al_stg_at(const T* s, int r, int x) {
+    constexpr int BW = AlCfg<T>::BOXW;
+    return x < BW ? (float)s[r * BW + x] : (float)s[AL_IR * BW + r * BW + x - 128];
+}
+__device__ __forceinline__ void al_stg_put(uint8_t* s, int r, int x, float v) {
+    constexpr int BW = AlCfg<uint8_t>::BOXW;
+    const uint8_t u = (uint8_t)v;
+    if (x < BW) s[r * BW + x] = u;
+    if (x >= 128) s[AL_IR * BW + r * BW + x - 128] = u;
+}
+__device__ __forceinline__ void al_stg_put(float* s, int r, int x, float v) {
+    constexpr int BW = AlCfg<float>::BOXW;
+    if (x < BW) s[r * BW + x] = v;
+    if (x >= 128) s[AL_IR * BW + r * BW + x - 128] = v;
+}
+
+// ---- row pass of one item (staged row r, group g: region columns 8g .. 8g+7):
+// lo/hi (unscaled o2 / e3) of the 8 coefficient columns as pairs (i, i+4), i < 4.
+// Inputs v[k] = logical staged column 16g + 2 + k (k < 22) = x[2 gc0 - 6 + k].
+__device__ __forceinline__ void al_rowpass(const uint8_t* s, int r, int g, float2 (&L)[4], float2 (&Hh)[4]) {
+    constexpr int BW = AlCfg<uint8_t>::BOXW;
+    const uint8_t* src = s + (g < 8 ? r * BW + 16 * g : AL_IR * BW + r * BW + 16 * g - 128);
+    const uint4 w0 = *reinterpret_cast<const uint4*>(src);
+    const uint2 w1 = *reinterpret_cast<const uint2*>(src + 16);
+    const uint32_t w[6] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y};
+    // byte b (logical 16g + b) -> 2^23 + byte as a float bit pattern
+    auto bf = [&](int b) { return __uint_as_float(__byte_perm(w[b >> 2], 0x4B000000u, 0x7540u | (uint32_t)(b & 3))); };
+    const float2 m23 = make_float2(-8388608.f, -8388608.f);
+    float2 E[7], O[7];
+#pragma unroll
+    for (int j = 0; j < 7; ++j) {   // E[j] = (v[2j], v[2j+8]), O[j] = (v[2j+1], v[2j+9]) exactly
+        E[j] = add2(make_float2(bf(2 * j + 2), bf(2 * j + 10)), m23);
+        O[j] = add2(make_float2(bf(2 * j + 3), bf(2 * j + 11)), m23);
+    }
+    float2 E1[7], O1[6], E2[6], O2[5];
+#pragma unroll
+    for (int j = 0; j < 7; ++j) E1[j] = lf2(-LF_C1, O[j], E[j]);
+#pragma unroll
+    for (int j = 0; j < 6; ++j) O1[j] = lf2(-LF_C2B, E1[j + 1], lf2(LF_C2A, E1[j], O[j]));
+#pragma unroll
+    for (int j = 1; j < 6; ++j) E2[j] = lf2(-LF_C3B, O1[j], lf2(LF_C3A, O1[j - 1], E1[j]));
+#pragma unroll
+    for (int j = 1; j < 5; ++j) O2[j] = lf2(LF_C4B, E2[j + 1], lf2(LF_C4A, E2[j], O1[j]));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        L[i] = O2[i + 1];                          // o2 at k = i, i + 4
+        Hh[i] = lf2(-LF_C5, O2[i + 1], E2[i + 2]);  // e3 at k = i, i + 4 (e3[j] = e2[j] - C5 o2[j-1])
+    }
+}
+__device__ __forceinline__ void al_rowpass(const float* s, int r, int g, float2 (&L)[4], float2 (&Hh)[4]) {
+    constexpr int BW = AlCfg<float>::BOXW;
+    const float* src = s + (g < 8 ? r * BW + 16 * g : AL_IR * BW + r * BW + 16 * g - 128) + 2;
+    float v[22];
+    {
+        const float2 a = *reinterpret_cast<const float2*>(src);
+        v[0] = a.x;
+        v[1] = a.y;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            const float4 b = *reinterpret_cast<const float4*>(src + 2 + 4 * k);
+            v[2 + 4 * k] = b.x;
+            v[3 + 4 * k] = b.y;
+            v[4 + 4 * k] = b.z;
+            v[5 + 4 * k] = b.w;
+        }
+    }
+    float e1[11], o1[10], e2[10], o2[9];
+#pragma unroll
+    for (int j = 0; j < 11; ++j) e1[j] = fmaf(-LF_C1, v[2 * j + 1], v[2 * j]);
+#pragma unroll
+    for (int j = 0; j < 10; ++j) o1[j] = fmaf(-LF_C2B, e1[j + 1], fmaf(LF_C2A, e1[j], v[2 * j + 1]));
+#pragma unroll
+    for (int j = 1; j < 10; ++j) e2[j] = fmaf(-LF_C3B, o1[j], fmaf(LF_C3A, o1[j - 1], e1[j]));
+#pragma unroll
+    for (int j = 1; j < 9; ++j) o2[j] = fmaf(LF_C4B, e2[j + 1], fmaf(LF_C4A, e2[j], o1[j]));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        L[i] = make_float2(o2[i + 1], o2[i + 5]);
+        Hh[i] = make_float2(fmaf(-LF_C5, o2[i + 1], e2[i + 2]), fmaf(-LF_C5, o2[i + 5], e2[i + 6]));
+    }
+}
+
+__device__ __forceinline__ float al_pick16(const float (&q)[16], int sl) {
+    float r = q[0];
+#pragma unroll
+    for (int i = 1; i < 16; ++i) r = (sl == i) ? q[i] : r;
+    return r;
+}
+__device__ __forceinline__ float2 al_pick16(const float2 (&q)[16], int sl) {
+    float2 r = q[0];
+#pragma unroll
+    for (int i = 1; i < 16; ++i) r = (sl == i) ? q[i] : r;
+    return r;
+}
+
+constexpr int AL_FIX = 5;   // edge fix-up slots per thread: ceil(16 rows * 40 columns / 128)
+
+template <typename T, int MINB, bool ALL4>
+__global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_constant__ CUtensorMap map, AlArgs a) {
+    constexpr int BW = AlCfg<T>::BOXW;
+    constexpr int LOGW = al_logw<T>();
+    constexpr int STG = al_stage_elems<T>();
+    constexpr int NSTG = AlCfg<T>::NSTG, P1 = AlCfg<T>::P1, P2 = AlCfg<T>::P2;
+    extern __shared__ __align__(128) unsigned char smem[];
+    T* stg0 = reinterpret_cast<T*>(smem);
+    float* DA = reinterpret_cast<float*>(smem + NSTG * STG * sizeof(T));   // da planes v3 v5 v7 v9 c [8][P1]; row buffer
+    float2* PR = reinterpret_cast<float2*>(DA + al_da_floats<T>());        // (ad, dd) planes [8][P2]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(PR + 5 * AL_BK * P2);
+    float* RBlo = DA;                    // row buffer: lo [16][AL_RBP], hi [16][AL_RBP] (overlaps the da planes)
+    float* RBhi = DA + AL_IR * AL_RBP;
+
+    const int t = threadIdx.x;
+    const int cx0 = blockIdx.x * a.O;
+    const int ky0 = blockIdx.y * a.SH;
+    const int ky1 = min(ky0 + a.SH, a.nH);
+    const int b = blockIdx.z;
+    const int xs = 2 * cx0 - 16;
+    const int K0 = ky0 - 4;
+    const int nblk = 1 + (ky1 - ky0 + AL_BK - 1) / AL_BK;
+    const int ncols = a.O + 8;
+    const int ngroups = ncols / 8;
+    const T* in = reinterpret_cast<const T*>(a.in) + (size_t)b * a.in_bstride;
+    const int gc = cx0 - 4 + t;   // this thread's coefficient column
+    // column-pass source column: in-plane columns read their own row-pass column; mirrored
+    // halo columns outside the subband read their partner's (R-4); idle threads a valid one
+    int src = (gc < 0 || gc >= a.nW) ? mirror(gc, a.nW) - cx0 + 4 : t;
+    src = min(max(src, 0), ncols - 1);
+    const int slot = 8 * (src >> 3) + 2 * (src & 3) + ((src >> 2) & 1);   // (k, k+4) adjacent
+    const bool inner = (t >= 4) && (t < 4 + a.O) && (gc < a.nW);
+    const int rr = t & 15, ga = t >> 4;
+    const bool doA = ga < ngroups && cx0 - 4 + 8 * ga < a.nW;
+    const bool doB = ga + 8 < ngroups && cx0 - 4 + 8 * (ga + 8) < a.nW;
+    const int hj = t & 7, hg = t >> 3;
+    const int hx = cx0 + 8 * hg;
+    const bool hv = (t < a.O) && (hx < a.nW);
+    const bool hfull = hx + 8 <= a.nW;
+
+    if (t == 0) {
+        for (int k = 0; k < NSTG; ++k) mbar_init(&bar[k], 1);
+        fence_mbar_init();
+    }
+    const bool edge = a.use_tma && (xs < 0 || xs + LOGW > a.NW);
+    // edge fix-up (TMA-staged blocks of the first / last strip): out-of-plane logical columns
+    // of the staged rows receive their mirrored in-plane values (R-4).  At most 16 + 24
+    // columns (xs >= -16; input columns NW .. NW+23): thread t handles column slot t % 40
+    // of rows t / 40 + 3k; sources in the plane, destinations outside it (no hazard).
+    int fx = -1, fs = 0;
+    const int fr0 = t / 40;
+    if (edge) {
+        const int nleft = xs < 0 ? min(-xs, LOGW) : 0;
+        const int xr0 = max(a.NW - xs, nleft), xr1 = min(LOGW, a.NW - xs + 24);
+        const int ncnt = nleft + max(xr1 - xr0, 0);
+        const int idx = t - 40 * fr0;
+        if (t < 120 && idx < ncnt) {
+            fx = idx < nleft ? idx : xr0 + idx - nleft;
+            fs = min(max(mirror(xs + fx, a.NW) - xs, 0), LOGW - 1);
+        }
+    }
+    auto fixup = [&](T* s) {
+        if (fx < 0) return;
+        float v[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k)
+            if (fr0 + 3 * k < AL_IR) v[k] = al_stg_at(s, fr0 + 3 * k, fs);
+#pragma unroll
+        for (int k = 0; k < 6; ++k)
+            if (fr0 + 3 * k < AL_IR) al_stg_put(s, fr0 + 3 * k, fx, v[k]);
+    };
+    auto stg_of = [&](int i) { return (i + NSTG) % NSTG; };
+    auto y0_of = [&](int i) { return i < 0 ? 2 * K0 - 6 : 2 * (K0 + AL_BK * i); };
+    const bool refl1 = a.NH >= 32;
+    auto mirror_row = [&](int y) {
+        return refl1 ? (y < 0 ? -1 - y : (y >= a.NH ? 2 * a.NH - 1 - y : y)) : mirror(y, a.NH);
+    };
+    auto inside = [&](int i) { const int y0 = y0_of(i); return y0 >= 0 && y0 + AL_IR <= a.NH; };
+    auto box_y = [&](int i) {
+        const int y0 = y0_of(i);
+        if (inside(i)) return y0;
+        const int y1 = y0 + (i < 0 ? 6 : AL_IR) - 1;
+        int lo = min(mirror_row(y0), mirror_row(y1));
+        if (y0 < 0 && y1 >= 0) lo = 0;
+        return min(lo, a.NH - AL_IR);
+    };
+    auto tma_ok = [&](int i) { return a.use_tma && (refl1 || (a.NH >= AL_IR && inside(i))); };
+    auto issue = [&](int i) {
+        const int k = stg_of(i);
+        T* s = stg0 + k * STG;
+        const int y = box_y(i);
+        mbar_arrive_expect_tx(&bar[k], (uint32_t)(2 * AL_IR * BW * sizeof(T)));
+        tma_load_3d(s, &map, xs, y, b, &bar[k]);
+        tma_load_3d(s + AL_IR * BW, &map, xs + 128, y, b, &bar[k]);
+    };
+    if (t == 0) {
+        for (int i = -1; i < NSTG - 1 && i < nblk; ++i)
+            if (tma_ok(i)) issue(i);
+    }
+    __syncthreads();
+    const bool vec_ok = ((reinterpret_cast<uintptr_t>(in) & 15) == 0) && ((a.in_pitch * sizeof(T)) % 16 == 0);
+    auto manual = [&](T* s, int y0, int nr) {
+        constexpr int CE = 16 / sizeof(T);
+        constexpr int NCH = LOGW / CE;
+        constexpr int PER = (AL_IR * NCH + AL_NT - 1) / AL_NT;
+        uint4 v[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int e = t + k * AL_NT;
+            v[k] = make_uint4(0u, 0u, 0u, 0u);
+            if (e < nr * NCH) {
+                const int r = e / NCH, ch = e - r * NCH;
+                const int gx = xs + ch * CE;
+                const T* row = in + (size_t)mirror(y0 + r, a.NH) * a.in_pitch;
+                if (vec_ok && gx >= 0 && gx + CE <= a.NW) {
+                    v[k] = __ldg(reinterpret_cast<const uint4*>(row + gx));
+                } else {
+                    T tmp[CE];
+#pragma unroll
+                    for (int i = 0; i < CE; ++i) tmp[i] = row[mirror(gx + i, a.NW)];
+                    memcpy(&v[k], tmp, 16);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int e = t + k * AL_NT;
+            if (e < nr * NCH) {
+                const int r = e / NCH, x = (e - r * NCH) * CE;
+                if (x < BW) *reinterpret_cast<uint4*>(s + r * BW + x) = v[k];
+                if (x >= 128) *reinterpret_cast<uint4*>(s + AL_IR * BW + r * BW + x - 128) = v[k];
+            }
+        }
+    };
+    auto rowpass = [&](const T* s, int prow, int nr) {
+        if (rr >= nr) return;
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+            const int g = ga + 8 * h;
+            if (h == 0 ? doA : doB) {
+                float2 L[4], Hh[4];
+                al_rowpass(s, prow, g, L, Hh);
+                float2* dl = reinterpret_cast<float2*>(RBlo + rr * AL_RBP + 8 * g);
+                float2* dh = reinterpret_cast<float2*>(RBhi + rr * AL_RBP + 8 * g);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    dl[i] = L[i];
+                    dh[i] = Hh[i];
+                }
+            }
+        }
+    };
+
+    // column-pass lifting state (pairs over (lo, hi) of this column): o[m-1], e1[m-1], o1[m-2], e2[m-2]
+    float2 so = make_float2(0.f, 0.f), se1 = so, so1 = so, se2 = so;
+    float qd_c[8], cd_c[4];       // da: squares of the last 8 coefficient rows, c of the last 4
+    float2 qp_c[8], cp_c[4];      // (ad, dd) likewise
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        qd_c[k] = 0.f;
+        qp_c[k] = make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        cd_c[k] = 0.f;
+        cp_c[k] = make_float2(0.f, 0.f);
+    }
+    const float s0 = a.sp.sigma0_sq;
+    const float2 s0p = make_float2(s0, s0 * LF_KD2);
+    const int wm = a.sp.wmask;
+    uint32_t phase = 0;
+    const long long ll_off = (long long)b * a.out_bstride + gc;   // LL element offset of row 0 (a.ll may be null)
+    const size_t dst_off = (size_t)b * a.out_bstride + hx;
+
+#pragma unroll 1
+    for (int i = -1; i < nblk; ++i) {
+        const bool pro = i < 0;
+        const int K = K0 + AL_BK * i;
+        const int sk = stg_of(i);
+        T* s = stg0 + sk * STG;
+        int prow;
+        if (tma_ok(i)) {
+            mbar_wait(&bar[sk], (phase >> sk) & 1);
+            phase ^= 1u << sk;
+            prow = inside(i) ? rr : mirror_row(y0_of(i) + rr) - box_y(i);
+            if (edge) {
+                fixup(s);
+                __syncthreads();
+            }
+        } else {
+            manual(s, pro ? 2 * K0 - 6 : 2 * K, pro ? 6 : AL_IR);
+            prow = rr;
+            __syncthreads();
+        }
+        rowpass(s, prow, pro ? 6 : AL_IR);
+        fence_proxy_async();
+        __syncthreads();   // B1: row buffer complete, staging buffer s consumed
+        if (t == 0 && i + NSTG < nblk && tma_ok(i + NSTG)) issue(i + NSTG);
+
+        // ---- column pass: (e, o) row pairs j of the block = coefficient rows m = K + j;
+        // squares straight into the ring (slots 8..15), LL stored as it comes out
+        auto lift_y = [&](int j, float2& o2, float2& e3) {
+            const float2 pe = make_float2(RBlo[(2 * j) * AL_RBP + slot], RBhi[(2 * j) * AL_RBP + slot]);
+            const float2 po = make_float2(RBlo[(2 * j + 1) * AL_RBP + slot], RBhi[(2 * j + 1) * AL_RBP + slot]);
+            const float2 e1 = lf2(-LF_C1, po, pe);                              // e1[m]
+            const float2 o1 = lf2(-LF_C2B, e1, lf2(LF_C2A, se1, so));           // o1[m-1]
+            const float2 e2 = lf2(-LF_C3B, o1, lf2(LF_C3A, so1, se1));          // e2[m-1]
+            o2 = lf2(LF_C4B, e2, lf2(LF_C4A, se2, so1));                        // o2[m-2] = a[m] / KA
+            e3 = lf2(-LF_C5, o2, e2);                                           // e3[m-1] = d[m] / KD
+            so = po;
+            se1 = e1;
+            so1 = o1;
+            se2 = e2;
+        };
+        if (pro) {   // input rows 2K0-6 .. 2K0-1: lifting state only
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                float2 o2, e3;
+                lift_y(j, o2, e3);
+            }
+            __syncthreads();   // row buffer free for block 0
+            continue;
+        }
+        float qd[16], cn[8];
+        float2 qp[16], cpn[8];
+        // LL rows of this block inside the segment (bit j: row K + j), interior columns only
+        const uint32_t llmask = (a.ll != nullptr && inner)
+                                    ? ((0xFFu >> (8 - min(max(ky1 - K, 0), 8))) & (0xFFu << min(max(ky0 - K, 0), 8)))
+                                    : 0u;
+        float* llp = a.ll + ll_off + K * a.out_pitch;
+#pragma unroll
+        for (int j = 0; j < AL_BK; ++j) {
+            float2 o2, e3;
+            lift_y(j, o2, e3);
+            const float llv = LF_KA2 * o2.x;
+            if (llmask & (1u << j)) *llp = llv;
+            llp += a.out_pitch;
+            cn[j] = o2.y;                  // da
+            cpn[j] = e3;                   // (ad, dd / KD^2)
+            qd[8 + j] = __fmul_rn(o2.y, o2.y);
+            qp[8 + j] = mul2(e3, e3);
+        }
+        float cd[8];
+        float2 cp[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            qd[k] = qd_c[k];
+            qp[k] = qp_c[k];
+        }
+        // rows beyond the subband are mirrored copies (R-4): row r >= nH <- 2nH-1-r
+        if (K + AL_BK > a.nH) {
+#pragma unroll
+            for (int k = 0; k < AL_BK; ++k) {
+                const int row = K + k;
+                if (row >= a.nH) {
+                    const int sl = (2 * a.nH - 1 - row) - K + 8;
+                    qd[8 + k] = al_pick16(qd, sl);
+                    qp[8 + k] = al_pick16(qp, sl);
+                }
+            }
+        }
+        if (K < 0) {   // rows -4..-1 (top segment) <- rows 3..0
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                qd[8 + k] = qd[15 - k];
+                qp[8 + k] = qp[15 - k];
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {   // c of output rows K-4 .. K+3
+            cd[j] = j < 4 ? cd_c[j] : cn[j - 4];
+            cp[j] = j < 4 ? cp_c[j] : cpn[j - 4];
+        }
+        if (i > 0) {
+            // output rows K-4 .. K+3: nested vertical sums over ring rows j .. j+8
+            if (t < ncols) {
+#pragma unroll
+                for (int j = 0; j < AL_BK; ++j) {
+                    const float2 v3 = add2(add2(qp[j + 3], qp[j + 4]), qp[j + 5]);
+                    const float2 v5 = add2(v3, add2(qp[j + 2], qp[j + 6]));
+                    const float2 v7 = add2(v5, add2(qp[j + 1], qp[j + 7]));
+                    const float2 v9 = add2(v7, add2(qp[j], qp[j + 8]));
+                    PR[(0 * AL_BK + j) * P2 + t] = v3;
+                    PR[(1 * AL_BK + j) * P2 + t] = v5;
+                    PR[(2 * AL_BK + j) * P2 + t] = v7;
+                    PR[(3 * AL_BK + j) * P2 + t] = v9;
+                    PR[(4 * AL_BK + j) * P2 + t] = cp[j];
+                }
+            }
+            __syncthreads();   // B2: every thread is done reading the row buffer (overlaps the da planes)
+            if (t < ncols) {
+#pragma unroll
+                for (int j = 0; j < AL_BK; ++j) {
+                    const float v3 = qd[j + 3] + qd[j + 4] + qd[j + 5];
+                    const float v5 = v3 + qd[j + 2] + qd[j + 6];
+                    const float v7 = v5 + qd[j + 1] + qd[j + 7];
+                    const float v9 = v7 + qd[j] + qd[j + 8];
+                    DA[(0 * AL_BK + j) * P1 + t] = v3;
+                    DA[(1 * AL_BK + j) * P1 + t] = v5;
+                    DA[(2 * AL_BK + j) * P1 + t] = v7;
+                    DA[(3 * AL_BK + j) * P1 + t] = v9;
+                    DA[(4 * AL_BK + j) * P1 + t] = cd[j];
+                }
+            }
+            __syncthreads();   // B3: V/c of all three subbands ready
+            if (hv && K - 4 + hj < ky1) {
+                const size_t roff = dst_off + (size_t)(K - 4 + hj) * a.out_pitch;
+                // ---- da: region columns 8hg .. 8hg+15 of row hj
+                {
+                    const float* base = DA + hj * P1 + 8 * hg;
+                    float m[8];
+                    {
+                        float u[16];
+#pragma unroll
+                        for (int q4 = 0; q4 < 4; ++q4) {
+                            const float4 x = *reinterpret_cast<const float4*>(base + 0 * AL_BK * P1 + 4 * q4);
+                            u[4 * q4] = x.x; u[4 * q4 + 1] = x.y; u[4 * q4 + 2] = x.z; u[4 * q4 + 3] = x.w;
+                        }
+                        float s3 = u[3] + u[4] + u[5];
+#pragma unroll
+                        for (int x = 0; x < 8; ++x) {
+                            if (x > 0) s3 += u[x + 5] - u[x + 2];
+                            m[x] = (ALL4 || (wm & 1)) ? s3 * (1.0f / 9.0f) : 3.402823466e38f;
+                        }
+                    }
+                    {
+                        float u[16];
+#pragma unroll
+                        for (int q4 = 0; q4 < 4; ++q4) {
+                            const float4 x = *reinterpret_cast<const float4*>(base + 1 * AL_BK * P1 + 4 * q4);
+                            u[4 * q4] = x.x; u[4 * q4 + 1] = x.y; u[4 * q4 + 2] = x.z; u[4 * q4 + 3] = x.w;
+                        }
+                        float s5 = u[2] + u[3] + u[4] + u[5] + u[6];
+#pragma unroll
+                        for (int x = 0; x < 8; ++x) {
+                            if (x > 0) s5 += u[x + 6] - u[x + 1];
+                            if (ALL4 || (wm & 2)) m[x] = fminf(m[x], s5 * (1.0f / 25.0f));
+                        }
+                    }
+                    {
+                        float u[16];
+#pragma unroll
+                        for (int q4 = 0; q4 < 4; ++q4) {
+                            const float4 x = *reinterpret_cast<const float4*>(base + 2 * AL_BK * P1 + 4 * q4);
+                            u[4 * q4] = x.x; u[4 * q4 + 1] = x.y; u[4 * q4 + 2] = x.z; u[4 * q4 + 3] = x.w;
+                        }
+                        float s7 = u[1] + u[2] + u[3] + u[4] + u[5] + u[6] + u[7];
+#pragma unroll
+                        for (int x = 0; x < 8; ++x) {
+                            if (x > 0) s7 += u[x + 7] - u[x];
+                            if (ALL4 || (wm & 4)) m[x] = fminf(m[x], s7 * (1.0f / 49.0f));
+                        }
+                    }
+                    {
+                        float u[16];
+#pragma unroll
+                        for (int q4 = 0; q4 < 4; ++q4) {
+                            const float4 x = *reinterpret_cast<const float4*>(base + 3 * AL_BK * P1 + 4 * q4);
+                            u[4 * q4] = x.x; u[4 * q4 + 1] = x.y; u[4 * q4 + 2] = x.z; u[4 * q4 + 3] = x.w;
+                        }
+                        float s9 = u[0] + u[1] + u[2] + u[3] + u[4] + u[5] + u[6] + u[7] + u[8];
+#pragma unroll
+                        for (int x = 0; x < 8; ++x) {
+                            if (x > 0) s9 += u[x + 8] - u[x - 1];
+                            if (ALL4 || (wm & 8)) m[x] = fminf(m[x], s9 * (1.0f / 81.0f));
+                        }
+                    }
+                    const float4 c0 = *reinterpret_cast<const float4*>(base + 4 * AL_BK * P1 + 4);
+                    const float4 c1 = *reinterpret_cast<const float4*>(base + 4 * AL_BK * P1 + 8);
+                    const float cv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+                    float o[8];
+#pragma unroll
+                    for (int x = 0; x < 8; ++x) o[x] = (cv[x] * s0) * al_rcp(fmaxf(m[x], s0));
+                    float* drow = a.d0 + roff;
+                    if (hfull) {
+                        reinterpret_cast<float4*>(drow)[0] = make_float4(o[0], o[1], o[2], o[3]);
+                        reinterpret_cast<float4*>(drow)[1] = make_float4(o[4], o[5], o[6], o[7]);
+                    } else {
+#pragma unroll
+                        for (int x = 0; x < 8; ++x)
+                            if (hx + x < a.nW) drow[x] = o[x];
+                    }
+                }
+                // ---- (ad, dd): float2 region columns 8hg .. 8hg+15 of row hj
+                {
+                    const float2* base = PR + hj * P2 + 8 * hg;
+                    float2 m[8];
+                    {
+                        float2 u[12];   // columns 2 .. 13
+#pragma unroll
+                        for (int q2 = 0; q2 < 6; ++q2) {
+                            const float4 x = *reinterpret_cast<const float4*>(base + 0 * AL_BK * P2 + 2 + 2 * q2);
+                            u[2 * q2] = make_float2(x.x, x.y);
+                            u[2 * q2 + 1] = make_float2(x.z, x.w);
+                        }
+                        float2 s3 = add2(add2(u[1], u[2]), u[3]);
+#pragma unroll
+                        for (int x = 0; x < 8; ++x) {
+                            if (x > 0) s3 = add2(s3, sub2(u[x + 3], u[x]));
+                            m[x] = (ALL4 || (wm & 1)) ? mul2(s3, c_al_w[0]) : make_float2(3.402823466e38f, 3.402823466e38f);
+                        }
+                    }
+                    {
+                        float2 u[12];   // columns 2 .. 13
+#pragma unroll
+                        for (int q2 = 0; q2 < 6; ++q2) {
+                            const float4 x = *reinterpret_cast<const float4*>(base + 1 * AL_BK * P2 + 2 + 2 * q2);
+                            u[2 * q2] = make_float2(x.x, x.y);
+                            u[2 * q2 + 1] = make_float2(x.z, x.w);
+                        }
+                        float2 s5 = add2(add2(add2(u[0], u[1]), add2(u[2], u[3])), u[4]);
+#pragma unroll
+                        for (int x = 0; x < 8; ++x) {
+                            if (x > 0) s5 = add2(s5, sub2(u[x + 4], u[x - 1]));
+                            if (ALL4 || (wm & 2)) {
+                                const float2 r = mul2(s5, c_al_w[1]);
+                                m[x] = make_float2(fminf(m[x].x, r.x), fminf(m[x].y, r.y));
+                            }
+                        }
+                    }
+                    {
+                        float2 u[16];   // columns 0 .. 15
+#pragma unroll
+                        for (int q2 = 0; q2 < 8; ++q2) {
+                            const float4 x = *reinterpret_cast<const float4*>(base + 2 * AL_BK * P2 + 2 * q2);
+                            u[2 * q2] = make_float2(x.x, x.y);
+                            u[2 * q2 + 1] = make_float2(x.z, x.w);
+                        }
+                        float2 s7 = add2(add2(add2(u[1], u[2]), add2(u[3], u[4])), add2(add2(u[5], u[6]), u[7]));
+#pragma unroll
+                        for (int x = 0; x < 8; ++x) {
+                            if (x > 0) s7 = add2(s7, sub2(u[x + 7], u[x]));
+                            if (ALL4 || (wm & 4)) {
+                                const float2 r = mul2(s7, c_al_w[2]);
+                                m[x] = make_float2(fminf(m[x].x, r.x), fminf(m[x].y, r.y));
+                            }
+                        }
+                    }
+                    {
+                        float2 u[16];   // columns 0 .. 15
+#pragma unroll
+                        for (int q2 = 0; q2 < 8; ++q2) {
+                            const float4 x = *reinterpret_cast<const float4*>(base + 3 * AL_BK * P2 + 2 * q2);
+                            u[2 * q2] = make_float2(x.x, x.y);
+                            u[2 * q2 + 1] = make_float2(x.z, x.w);
+                        }
+                        float2 s9 = add2(add2(add2(add2(u[0], u[1]), add2(u[2], u[3])), add2(add2(u[4], u[5]), add2(u[6], u[7]))), u[8]);
+#pragma unroll
+                        for (int x = 0; x < 8; ++x) {
+                            if (x > 0) s9 = add2(s9, sub2(u[x + 8], u[x - 1]));
+                            if (ALL4 || (wm & 8)) {
+                                const float2 r = mul2(s9, c_al_w[3]);
+                                m[x] = make_float2(fminf(m[x].x, r.x), fminf(m[x].y, r.y));
+                            }
+                        }
+                    }
+                    float oa[8], od[8];
+#pragma unroll
+                    for (int q2 = 0; q2 < 4; ++q2) {
+                        const float4 x = *reinterpret_cast<const float4*>(base + 4 * AL_BK * P2 + 4 + 2 * q2);
+                        const float2 c0 = mul2(make_float2(x.x, x.y), s0p), c1 = mul2(make_float2(x.z, x.w), s0p);
+                        oa[2 * q2] = c0.x * al_rcp(fmaxf(m[2 * q2].x, s0));
+                        od[2 * q2] = c0.y * al_rcp(fmaxf(m[2 * q2].y, s0));
+                        oa[2 * q2 + 1] = c1.x * al_rcp(fmaxf(m[2 * q2 + 1].x, s0));
+                        od[2 * q2 + 1] = c1.y * al_rcp(fmaxf(m[2 * q2 + 1].y, s0));
+                    }
+                    float* arow = a.d1 + roff;
+                    float* drow = a.d2 + roff;
+                    if (hfull) {
+                        reinterpret_cast<float4*>(arow)[0] = make_float4(oa[0], oa[1], oa[2], oa[3]);
+                        reinterpret_cast<float4*>(arow)[1] = make_float4(oa[4], oa[5], oa[6], oa[7]);
+                        reinterpret_cast<float4*>(drow)[0] = make_float4(od[0], od[1], od[2], od[3]);
+                        reinterpret_cast<float4*>(drow)[1] = make_float4(od[4], od[5], od[6], od[7]);
+                    } else {
+#pragma unroll
+                        for (int x = 0; x < 8; ++x)
+                            if (hx + x < a.nW) {
+                                arow[x] = oa[x];
+                                drow[x] = od[x];
+                            }
+                    }
+                }
+            }
+        }
+        __syncthreads();   // B4: V buffers and the row buffer free for the next block
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            qd_c[k] = qd[8 + k];
+            qp_c[k] = qp[8 + k];
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {   // c of rows K+4 .. K+7 (output rows of the next block)
+            cd_c[k] = cn[4 + k];
+            cp_c[k] = cpn[4 + k];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ host
+bool encode_tensor_map_3d(CUtensorMap* map, CUtensorMapDataType dt, size_t elem_bytes, const void* base, uint64_t cols,
+                          uint64_t rows, uint64_t depth, uint64_t pitch_bytes, uint64_t plane_bytes, uint32_t box_w,
+                          uint32_t box_h);
+
+template <typename T>
+static int lift_launch(const T* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll, float* d0,
+                       float* d1, float* d2, long long out_bstride, int out_pitch, int nH, int nW,
+                       const ShrinkParams& sp, int nb, cudaStream_t st) {
+    static DeviceFlags done[2];
+    int rc;
+    if ((rc = set_smem_attr((const void*)k_analysis_lift<T, AlCfg<T>::MINB, true>, al_smem_bytes<T>(), done[0])))
+        return rc;
+    if ((rc = set_smem_attr((const void*)k_analysis_lift<T, AlCfg<T>::MINB, false>, al_smem_bytes<T>(), done[1])))
+        return rc;
+    if (nb > 65535) return fail(PRNU_INVALID_ARG, "analysis: more than 65535 planes in one launch");
+    AlArgs a{};
+    a.in = in;
+    a.in_bstride = in_bstride;
+    a.in_pitch = in_pitch;
+    a.NH = NH;
+    a.NW = NW;
+    a.ll = ll;
+    a.d0 = d0;
+    a.d1 = d1;
+    a.d2 = d2;
+    a.out_bstride = out_bstride;
+    a.out_pitch = out_pitch;
+    a.nH = nH;
+    a.nW = nW;
+    a.sp = sp;
+    const int S0 = (nW + AlCfg<T>::OMAX - 1) / AlCfg<T>::OMAX;
+    a.O = (int)align_up((size_t)((nW + S0 - 1) / S0), 8);
+    const int S = (nW + a.O - 1) / a.O;
+    // segments of <= 300 rows (prologue overhead <= 3%), more of them while the grid holds
+    // fewer than 6 (u8, level 1) / 1 (fp32) waves of MINB CTAs per SM
+    const long long waves = sizeof(T) == 1 ? 6 : 1;
+    const long long slots = (long long)device_sm_count() * AlCfg<T>::MINB;
+    int nseg = (nH + 299) / 300;
+    while ((long long)S * nseg * nb < waves * slots && (nH + nseg) / (nseg + 1) >= 32) ++nseg;
+    a.SH = (int)align_up((size_t)((nH + nseg - 1) / nseg), 8);
+    nseg = (nH + a.SH - 1) / a.SH;
+    CUtensorMap map{};
+    const size_t es = sizeof(T);
+    const CUtensorMapDataType dt = sizeof(T) == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    a.use_tma = ((in_pitch * es) % 16 == 0) && ((in_bstride * es) % 16 == 0) && ((uintptr_t)in % 16 == 0) &&
+                encode_tensor_map_3d(&map, dt, es, in, (uint64_t)NW, (uint64_t)NH, (uint64_t)nb, (uint64_t)in_pitch * es,
+                                     (uint64_t)in_bstride * es, AlCfg<T>::BOXW, AL_IR);
+    dim3 grid(S, nseg, nb);
+    if (sp.wmask == 15)
+        k_analysis_lift<T, AlCfg<T>::MINB, true><<<grid, AL_NT, al_smem_bytes<T>(), st>>>(map, a);
+    else
+        k_analysis_lift<T, AlCfg<T>::MINB, false><<<grid, AL_NT, al_smem_bytes<T>(), st>>>(map, a);
+    return PRNU_OK;
+}
+
+int launch_analysis_lift_u8(const uint8_t* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll,
+                            float* d0, float* d1, float* d2, long long out_bstride, int out_pitch, int nH, int nW,
+                            const ShrinkParams& sp, int nb, cudaStream_t st) {
+    return lift_launch<uint8_t>(in, in_bstride, in_pitch, NH, NW, ll, d0, d1, d2, out_bstride, out_pitch, nH, nW, sp,
+                                nb, st);
+}
+int launch_analysis_lift_f32(const float* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll,
+                             float* d0, float* d1, float* d2, long long out_bstride, int out_pitch, int nH, int nW,
+                             const ShrinkParams& sp, int nb, cudaStream_t st) {
+    return lift_launch<float>(in, in_bstride, in_pitch, NH, NW, ll, d0, d1, d2, out_bstride, out_pitch, nH, nW, sp,
+                              nb, st);
+}
+
+}  // namespace prnu

@@ -27,6 +27,35 @@ int check_launch(const char* what) {
     return PRNU_OK;
 }
 
+static int current_device(int* dev) {
+    cudaError_t e = cudaGetDevice(dev);
+    if (e != cudaSuccess) return fail(PRNU_CUDA_ERROR, std::string("cudaGetDevice: ") + cudaGetErrorString(e));
+    if (*dev < 0 || *dev >= 64) return fail(PRNU_CUDA_ERROR, "device ordinal beyond 63");
+    return PRNU_OK;
+}
+
+int set_smem_attr(const void* fn, size_t bytes, DeviceFlags& done) {
+    int dev = 0, rc = current_device(&dev);
+    if (rc) return rc;
+    const uint64_t bit = 1ull << dev;
+    if (done.bits.load(std::memory_order_acquire) & bit) return PRNU_OK;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return fail(PRNU_CUDA_ERROR, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    done.bits.fetch_or(bit, std::memory_order_acq_rel);
+    return PRNU_OK;
+}
+
+int device_sm_count() {
+    static std::atomic<int> cache[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+    int n = cache[dev].load(std::memory_order_relaxed);
+    if (n > 0) return n;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 1;
+    cache[dev].store(n, std::memory_order_relaxed);
+    return n;
+}
+
 // ---------------------------------------------------------------- profiler
 struct ProfRec {
     const char* name;

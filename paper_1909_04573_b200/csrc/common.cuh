@@ -48,6 +48,17 @@ struct KTimer {
 
 bool profiling_active();
 
+// Per-device "done" flags (bit d = device d), for one-time per-device setup such
+// as cudaFuncSetAttribute, which applies to the current device only.
+struct DeviceFlags {
+    std::atomic<uint64_t> bits{0};
+};
+// Raise fn's dynamic shared-memory limit to `bytes` on the current device, once
+// per device (a failed call is reported and retried on the next launch).
+int set_smem_attr(const void* fn, size_t bytes, DeviceFlags& done);
+// Streaming multiprocessors of the current device (cudaDevAttrMultiProcessorCount, cached per device).
+int device_sm_count();
+
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -142,5 +153,13 @@ int launch_analysis_strip_u8(const uint8_t* in, long long in_bstride, int in_pit
 int launch_analysis_strip_f32(const float* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll,
                               float* d0, float* d1, float* d2, long long out_bstride, int out_pitch, int nH, int nW,
                               const ShrinkParams& sp, int nb, cudaStream_t st);
+
+// analysis.cu: column-streaming analysis (lifting) + shrink of one level
+int launch_analysis_lift_u8(const uint8_t* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll,
+                            float* d0, float* d1, float* d2, long long out_bstride, int out_pitch, int nH, int nW,
+                            const ShrinkParams& sp, int nb, cudaStream_t st);
+int launch_analysis_lift_f32(const float* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll,
+                             float* d0, float* d1, float* d2, long long out_bstride, int out_pitch, int nH, int nW,
+                             const ShrinkParams& sp, int nb, cudaStream_t st);
 
 }  // namespace prnu

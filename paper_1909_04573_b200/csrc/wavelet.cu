@@ -1164,6 +1164,11 @@ static const char* kShrinkName[kMaxLevels + 1] = {"", "shrink_l1", "shrink_l2", 
 // the fp32 strips' fill rule (fewer, longer segments; 1 wave) and the direct left
 // mirror, the strip kernel also wins at level 4 (step 22.70 -> 22.55 ms, interleaved
 // A/B); the tile kernel k_analysis_shrink stays as the PRNU_STRIP=0 / A/B path.
+// A/B during development: PRNU_ANALYSIS=strip selects the direct-filter strip kernel
+static bool use_lift() {
+    static const bool on = !(getenv("PRNU_ANALYSIS") && std::string(getenv("PRNU_ANALYSIS")) == "strip");
+    return on;
+}
 static int strip_max_level() {
     static const int l = getenv("PRNU_STRIP_MAXL") ? atoi(getenv("PRNU_STRIP_MAXL")) : 6;   // every level
     return l;
@@ -1223,7 +1228,16 @@ static int denoise_front(const TIn* in, long long in_bstride, int in_pitch, int 
             a.in = in;
             a.in_bstride = in_bstride;
             a.in_pitch = in_pitch;
-            if (use_strip()) {
+            if (use_lift()) {
+                rc = sizeof(TIn) == 1
+                         ? launch_analysis_lift_u8(reinterpret_cast<const uint8_t*>(in), in_bstride, in_pitch, a.NH,
+                                                   a.NW, a.ll, a.d0, a.d1, a.d2, a.out_bstride, a.out_pitch, a.nH,
+                                                   a.nW, sp, nb, st)
+                         : launch_analysis_lift_f32(reinterpret_cast<const float*>(in), in_bstride, in_pitch, a.NH,
+                                                    a.NW, a.ll, a.d0, a.d1, a.d2, a.out_bstride, a.out_pitch, a.nH,
+                                                    a.nW, sp, nb, st);
+                if (rc) return rc;
+            } else if (use_strip()) {
                 rc = sizeof(TIn) == 1
                          ? launch_analysis_strip_u8(reinterpret_cast<const uint8_t*>(in), in_bstride, in_pitch, a.NH,
                                                     a.NW, a.ll, a.d0, a.d1, a.d2, a.out_bstride, a.out_pitch, a.nH,
@@ -1239,7 +1253,11 @@ static int denoise_front(const TIn* in, long long in_bstride, int in_pitch, int 
             a.in = pb.approx[l - 1];
             a.in_bstride = (long long)pb.bstride[l - 1];
             a.in_pitch = p.pitch[l - 1];
-            if (use_strip() && l <= strip_max_level()) {
+            if (use_lift()) {
+                rc = launch_analysis_lift_f32(pb.approx[l - 1], a.in_bstride, a.in_pitch, a.NH, a.NW, a.ll, a.d0,
+                                              a.d1, a.d2, a.out_bstride, a.out_pitch, a.nH, a.nW, sp, nb, st);
+                if (rc) return rc;
+            } else if (use_strip() && l <= strip_max_level()) {
                 rc = launch_analysis_strip_f32(pb.approx[l - 1], a.in_bstride, a.in_pitch, a.NH, a.NW, a.ll, a.d0,
                                                a.d1, a.d2, a.out_bstride, a.out_pitch, a.nH, a.nW, sp, nb, st);
                 if (rc) return rc;

@@ -48,16 +48,27 @@ def test_c2_depth50_full_oracle(prnu, video_c2):
     K_ref, num, den, ns = oracle.extract_fingerprint(fr.cpu().numpy(), 50)
     assert fp.n_sda == ns == 36
     np.testing.assert_array_equal(fp.sum_I2.cpu().numpy(), den)      # exact: same fp32 SDA frames, same order
-    assert k_metric(fp.K.cpu().numpy(), K_ref, den, ns) <= K_TOL
+    Kg = fp.K.cpu().numpy()
+    prim = k_metric(Kg, K_ref, den, ns)
     rho = prnu.ncc(fp.K, video_c2.K).item()
-    assert abs(rho - oracle.ncc(K_ref, video_c2.K.cpu().numpy())) <= NCC_TOL
+    d_ncc = abs(rho - oracle.ncc(K_ref, video_c2.K.cpu().numpy()))
+    print(f"\nC2 d=50: R-14 primary {prim:.3e}, secondary 255*max|dK| "
+          f"{255.0 * float(np.abs(Kg.astype(np.float64) - K_ref).max()):.3e}, |dNCC| {d_ncc:.2e}")
+    assert prim <= K_TOL
+    assert d_ncc <= NCC_TOL
     assert rho > 0.9
 
 
-def test_c2_depth1_sampled(prnu, video_c2):
-    """Config 2, conventional (1800 denoisings) in the bench configuration:
-    sum_I2 equals the exact integer sum of squares; residuals of sampled frames
-    match the oracle; the first 32 frames' accumulator matches the oracle's."""
+def test_c2_depth1_full_oracle(prnu, video_c2):
+    """Config 2, conventional (1800 denoisings), in the bench configuration (waves
+    of 360 frames over the library's three streams): the WHOLE 1800-frame
+    fingerprint against the oracle ("SDA-1 is the same as conventional",
+    P:413).  The oracle's fingerprint is computed by worker processes on every
+    host core (oracle.parallel.extract_fingerprint_chunked: partial sums of
+    contiguous frame runs, added in order; ~1 min on 16 cores).  Also: sum_I2
+    equals the exact integer sum of squares, sampled residuals match, and the
+    R-14 secondary metric 255 max|dK| is reported."""
+    from oracle import parallel
     fr = video_c2.frames[:1800]
     fp = prnu.extract_fingerprint(fr, 1, batch=BENCH_BATCH)
     assert fp.n_sda == 1800
@@ -72,12 +83,20 @@ def test_c2_depth1_sampled(prnu, video_c2):
     for j, i in enumerate(idx):
         Wr = oracle.residual(fr[i].cpu().numpy().astype(np.float32))
         assert np.abs(Wg[j] - Wr).max() <= W_TOL
-    # one whole wave: the fingerprint of the first 32 frames against the oracle
-    sub = fr[:32].contiguous()
-    fp32 = prnu.extract_fingerprint(sub, 1, batch=BENCH_BATCH)
-    K_ref, num, den, ns = oracle.extract_fingerprint(sub.cpu().numpy(), 1)
-    assert k_metric(fp32.K.cpu().numpy(), K_ref, den, ns) <= K_TOL
-    assert prnu.ncc(fp.K, video_c2.K).item() > 0.9
+    host = fr.cpu().numpy()
+    K_ref, num, den, ns = parallel.extract_fingerprint_chunked(host, 1)
+    assert ns == 1800
+    np.testing.assert_array_equal(fp.sum_I2.cpu().numpy(), den)
+    Kg = fp.K.cpu().numpy()
+    prim = k_metric(Kg, K_ref, den, ns)
+    sec = 255.0 * float(np.abs(Kg.astype(np.float64) - K_ref).max())
+    rho = prnu.ncc(fp.K, video_c2.K).item()
+    d_ncc = abs(rho - oracle.ncc(K_ref, video_c2.K.cpu().numpy()))
+    print(f"\nC2 d=1 full 1800 frames: R-14 primary {prim:.3e}, secondary 255*max|dK| {sec:.3e}, "
+          f"|dNCC| {d_ncc:.2e}, NCC(K, K_true) {rho:.4f}")
+    assert prim <= K_TOL
+    assert d_ncc <= NCC_TOL
+    assert rho > 0.9
 
 
 def test_c2_query_pce(prnu, video_c2):

@@ -1,6 +1,7 @@
 """Pins for the oracle's MLE accumulation (a5), finalize + zero-mean (a6) and the
 composed fingerprint path: Eq. (2) P:151-155."""
 import numpy as np
+import pytest
 import torch
 
 import oracle
@@ -86,3 +87,75 @@ def test_synth_is_deterministic():
     a = synth.video("drift", 3, 24, 40, seed=5).frames
     b = synth.video("drift", 3, 24, 40, seed=5).frames
     assert torch.equal(a, b)
+
+
+def _groups_by_hand(fr, d):
+    """SDA frames of the disjoint groups [i d, (i+1) d), i < floor(m/d) (P:124,
+    P:170-175), written out with numpy: the exact integer sum of the
+    group's frames over d, rounded once to fp32 (R-11; test_oracle_sda pins this
+    rounding against IEEE fp32 division)."""
+    m = fr.shape[0]
+    out = []
+    for i in range(m // d):
+        s = fr[i * d:(i + 1) * d].astype(np.int64).sum(axis=0)
+        out.append((s.astype(np.float64) / d).astype(np.float32))
+    return out
+
+
+@pytest.mark.parametrize("m,d", [(11, 3), (16, 4), (9, 2), (7, 7), (5, 1)])
+def test_extract_fingerprint_groups_pinned(m, d):
+    """oracle_extract_fingerprint at depth d > 1 with a remainder (m mod d frames
+    dropped) equals, bit for bit, an explicit loop over the disjoint groups
+    [i d, (i+1) d): hand-computed SDA frame -> residual -> MLE accumulate in
+    ascending i -> finalize.  A wrong group stride
+    (overlapping or shifted groups), a wrong group count or the remainder frames
+    leaking in would change the sums."""
+    v = synth.video("shift", m, 24, 40, seed=7)
+    fr = v.frames.numpy()
+    K, num, den, ns = oracle.extract_fingerprint(fr, d)
+    assert ns == m // d
+    n2, d2 = np.zeros((24, 40)), np.zeros((24, 40))
+    for S in _groups_by_hand(fr, d):
+        oracle.mle_accumulate(oracle.residual(S), S, n2, d2)
+    assert np.array_equal(num, n2) and np.array_equal(den, d2)
+    assert np.array_equal(K, oracle.finalize(n2, d2))
+    # the m mod d remainder does not enter: overwrite it, same result
+    if m % d:
+        fr2 = fr.copy()
+        fr2[ns * d:] = 255 - fr2[ns * d:]
+        K2, num2, den2, _ = oracle.extract_fingerprint(fr2, d)
+        assert np.array_equal(num2, num) and np.array_equal(den2, den)
+    # every frame of every group does enter: perturb the last frame of the last group
+    fr3 = fr.copy()
+    fr3[ns * d - 1] ^= 1
+    _, _, den3, _ = oracle.extract_fingerprint(fr3, d)
+    assert not np.array_equal(den3, den)
+
+
+def test_extract_fingerprint_overlap_detected():
+    """The pin above distinguishes disjoint from overlapping groups: groups of the
+    same depth at stride 1 give different sums (so the equality is not vacuous)."""
+    v = synth.video("shift", 8, 24, 40, seed=8)
+    fr = v.frames.numpy()
+    _, num, den, _ = oracle.extract_fingerprint(fr, 4)
+    n2, d2 = np.zeros((24, 40)), np.zeros((24, 40))
+    for i in range(2):   # overlapping: frames [i, i + 4)
+        S = (fr[i:i + 4].astype(np.int64).sum(0) / 4.0).astype(np.float32)
+        oracle.mle_accumulate(oracle.residual(S), S, n2, d2)
+    assert not np.array_equal(den, d2)
+
+
+def test_extract_fingerprint_chunked_matches():
+    """oracle.parallel.extract_fingerprint_chunked (partial sums of contiguous runs
+    of groups in worker processes, added in order) equals the sequential oracle up
+    to the regrouping of fp64 additions."""
+    from oracle import parallel
+    v = synth.video("shift", 23, 32, 48, seed=9)
+    fr = v.frames.numpy()
+    for d in (1, 3):
+        K, num, den, ns = oracle.extract_fingerprint(fr, d)
+        K2, num2, den2, ns2 = parallel.extract_fingerprint_chunked(fr, d, workers=2, chunks=3)
+        assert ns2 == ns
+        np.testing.assert_allclose(num2, num, rtol=1e-13, atol=1e-12)
+        np.testing.assert_allclose(den2, den, rtol=1e-14)
+        np.testing.assert_allclose(K2, K, rtol=1e-10, atol=1e-14)

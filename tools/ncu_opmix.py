@@ -1,28 +1,41 @@
-"""Opcode mix of one kernel launch from an ncu report's SASS source page."""
+"""Dynamic SASS opcode mix of one kernel from an ncu report (source page):
+   python tools/ncu_opmix.py report.ncu-rep [kernel-regex] [positions]
+Prints warp-instructions per opcode (and per position if given) with shared-memory
+wavefronts and stall samples."""
+import collections
 import csv
+import io
 import re
 import subprocess
 import sys
-from collections import defaultdict
 
-rep, idx = sys.argv[1], sys.argv[2]
-txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "--launch-skip", idx,
-                      "--launch-count", "1"], capture_output=True, text=True).stdout
-rows = list(csv.reader(txt.splitlines()))
-hdr = next(r for r in rows if r and r[0] == "Address")
-ie = hdr.index("Instructions Executed")
-mix = defaultdict(float)
-for r in rows:
-    if len(r) <= ie or not r[0].startswith("0x"):
+rep = sys.argv[1]
+kern = sys.argv[2] if len(sys.argv) > 2 else None
+npos = float(sys.argv[3]) if len(sys.argv) > 3 else 0.0
+cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"]
+if kern:
+    cmd += ["-k", "regex:" + kern]
+out = subprocess.run(cmd, capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(out)))
+hdr = next(r for r in rows if "Source" in r and "Instructions Executed" in r)
+i0 = rows.index(hdr)
+data = [r for r in rows[i0 + 1:] if len(r) == len(hdr)]
+iS, iE = hdr.index("Source"), hdr.index("Instructions Executed")
+iW, iSm = hdr.index("L1 Wavefronts Shared"), hdr.index("Warp Stall Sampling (All Samples)")
+tot, wf, st = collections.Counter(), collections.Counter(), collections.Counter()
+T = 0
+for r in data:
+    m = re.match(r"\s*(@!?U?P\w+\s+)?([A-Z0-9_]+)(\.\S+)?", r[iS])
+    if not m:
         continue
-    ins = r[1].strip()
-    ins = re.sub(r"^@!?U?P\w+\s+", "", ins)
-    op = ins.split()[0] if ins else "?"
-    try:
-        mix[op] += float(r[ie] or 0)
-    except ValueError:
-        pass
-tot = sum(mix.values())
-print(f"total warp-level instructions {tot:.0f}")
-for op, v in sorted(mix.items(), key=lambda x: -x[1])[:40]:
-    print(f"{op:28s} {v:14.0f} {100*v/tot:5.1f}%")
+    op = m.group(2)
+    key = op + (m.group(3) or "") if op in ("LDS", "STS", "LDG", "STG") else op
+    n = int(r[iE] or 0)
+    T += n
+    tot[key] += n
+    wf[key] += int(r[iW] or 0)
+    st[key] += int(r[iSm] or 0)
+print(f"total warp-instructions {T}" + (f"  per position (thread-instr) {T * 32 / npos:.1f}" if npos else ""))
+for k, v in tot.most_common(45):
+    per = f" {v * 32 / npos:7.2f}/pos" if npos else ""
+    print(f"{k:16s} {v:12d} {v / T * 100:5.1f}%{per}  wf {wf[k]:10d}  stall {st[k]}")
