@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import re
 import os
 import sys
 import threading
@@ -148,11 +149,12 @@ def sub_len(n):
     return (n + 7) // 2
 
 
-# FP32-pipe lane-operations the method needs per level-l coefficient position:
-# DWT 2 x (2 rows x 2 outputs x 8 taps) = 64 FMA; shrink of 3 detail coefficients,
-# each c^2 (1) + nested vertical (8) + sliding horizontal (8) window sums + 4 scalings
-# + the Wiener product (2) = 23 -> 69.  min / max / rcp run on other pipes (not counted).
-ALU_OPS_PER_POSITION = 64 + 3 * 23
+# FP32-pipe lane-operations per level-l coefficient position of the lifted analysis
+# (DESIGN.md §6): the lifting DWT costs 8 FMA per (a, d) pair -> rows 2 x 8 + columns
+# 2 x 8 = 32, + 1 (the LL scale); the shrink of 3 detail coefficients, each c^2 (1) +
+# nested vertical (8) + sliding horizontal (8) window sums + 4 scalings + the Wiener
+# product (2) = 23 -> 69.  min / max / rcp run on other pipes (not counted).
+ALU_OPS_PER_POSITION = 33 + 3 * 23
 FP32_LANES_PER_SM = 128
 
 
@@ -165,8 +167,9 @@ def algorithmic_ops_per_step(name: str, H: int, W: int, levels: int, depths, m: 
     for _ in range(l):
         nH, nW = sub_len(nH), sub_len(nW)
     f_u8 = (m if 1 in depths else 0) + n_query
-    f_f32 = sum(m // d for d in depths if d > 1)
-    frames = f_u8 if name.endswith("_u8") else (f_f32 if name.endswith("_f32") else f_u8 + f_f32)
+    f_u16 = sum(m // d for d in depths if 1 < d <= 257)
+    f_f32 = sum(m // d for d in depths if d > 257)
+    frames = {"_u8": f_u8, "u16": f_u16, "f32": f_f32}.get(name[-3:], f_u8 + f_u16 + f_f32)
     return frames * nH * nW * ALU_OPS_PER_POSITION
 
 
@@ -182,35 +185,33 @@ def algorithmic_bytes_per_step(name: str, H: int, W: int, levels: int, depths, m
         nW.append(sub_len(nW[-1]))
     n = [nH[l] * nW[l] for l in range(levels + 1)]
     P = H * W
-    f_u8 = (m if 1 in depths else 0) + n_query          # level-1 u8 inputs
-    f_f32 = sum(m // d for d in depths if d > 1)        # SDA frames
-    f_all = f_u8 + f_f32
+    f_u8 = (m if 1 in depths else 0) + n_query                 # level-1 u8 inputs
+    f_u16 = sum(m // d for d in depths if 1 < d <= 257)        # SDA frames as exact u16 group sums
+    f_f32 = sum(m // d for d in depths if d > 257)             # SDA frames as fp32
+    f_all = f_u8 + f_u16 + f_f32
+    if name == "sda_sum":                                       # d u8 frames read, u16 sum written
+        return sum((m // d) * (d * P + 2 * P) for d in depths if 1 < d <= 257)
     if name == "sda_average":
-        return sum((m // d) * (d * P + 4 * P) for d in depths if d > 1)
-    if name == "dwt_l1_u8":
-        return f_u8 * (1 * P + 4 * 4 * n[1])
-    if name == "dwt_l1_f32":
-        return f_f32 * (4 * P + 4 * 4 * n[1])
-    if name.startswith("dwt_l"):
-        l = int(name[-1])
-        return f_all * (4 * n[l - 1] + (4 if l < levels else 3) * 4 * n[l])
-    if name.startswith("shrink_l"):
-        l = int(name[-1])
-        return f_all * 2 * 3 * 4 * n[l]          # raw details read once, c - F(c) written once
+        return sum((m // d) * (d * P + 4 * P) for d in depths if d > 257)
     if name == "analysis_l1_u8":
         return f_u8 * (1 * P + 4 * 4 * n[1])
+    if name == "analysis_l1_u16":
+        return f_u16 * (2 * P + 4 * 4 * n[1])
     if name == "analysis_l1_f32":
         return f_f32 * (4 * P + 4 * 4 * n[1])
-    if name.startswith("analysis_l"):
-        l = int(name[-1])
+    lvl = re.match(r"(analysis|synthesis)_l(\d)$", name)
+    if lvl and lvl.group(1) == "analysis":
+        l = int(lvl.group(2))
         return f_all * (4 * n[l - 1] + (4 if l < levels else 3) * 4 * n[l])
-    if name.startswith("synthesis_l") and name != "synthesis_l1":
-        l = int(name[-1])
+    if lvl and lvl.group(1) == "synthesis" and name != "synthesis_l1":
+        l = int(lvl.group(2))
         return f_all * ((4 if l < levels else 3) * 4 * n[l] + 4 * n[l - 1])
     if name == "synthesis_l1":
         return n_query * (4 * 4 * n[1] + 4 * P)
     if name == "synth_acc_l1_u8":
         return (m if 1 in depths else 0) * (4 * 4 * n[1] + 1 * P)
+    if name == "synth_acc_l1_u16":
+        return f_u16 * (4 * 4 * n[1] + 2 * P)
     if name == "synth_acc_l1_f32":
         return f_f32 * (4 * 4 * n[1] + 4 * P)
     return None
@@ -414,12 +415,14 @@ def main():
         roof = dict(kernel=top, bound="hbm", avg_launch_ms=avg_ms, share_of_kernel_time=kt["share"], **hbm_view)
         if ops is not None:
             sm_mhz = peaks.get("sm_max_mhz", 1965.0)
-            alu_peak = 148 * FP32_LANES_PER_SM * sm_mhz * 1e6 / 1e12
+            n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+            alu_peak = n_sm * FP32_LANES_PER_SM * sm_mhz * 1e6 / 1e12
             alu_ach = ops / (kt["ms_per_step"] / 1000.0) / 1e12
-            roof["alu_view"] = {"bound_note": "FP32 issue-bound (ncu: issue-active 57%, DRAM < 30%)",
+            roof["alu_view"] = {"bound_note": "bound by the L1/shared-memory data pipe and issue, not HBM "
+                                              "(DESIGN.md §6)",
                                 "achieved": alu_ach, "peak": alu_peak, "unit": "T fp32 lane-op/s",
                                 "frac": alu_ach / alu_peak, "ops_per_launch": ops / kt["launches_per_step"],
-                                "peak_source": "derived: 148 SM x 128 FP32 lanes x %.0f MHz" % sm_mhz}
+                                "peak_source": "derived: %d SM x 128 FP32 lanes x %.0f MHz" % (n_sm, sm_mhz)}
 
     # ---- NEXT rows, measured outside the step: f2 WDFT of the two
     #      fingerprints, f1 500x500 block matching of the query, f4 RGB->luma

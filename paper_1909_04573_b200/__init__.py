@@ -14,6 +14,7 @@ Citations: P:<n> = PAPER.md line, S:<n> = SPEC.md line, R-<n> = DESIGN.md readin
 from __future__ import annotations
 
 import ctypes
+import functools
 import os
 import re
 from dataclasses import dataclass, field
@@ -151,7 +152,41 @@ def _check(rc: int, where: str):
 
 
 def _stream():
+    """The current stream of the CURRENT device (every library call runs inside
+    _on_device, which makes the tensors' device current)."""
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _cuda_device(device) -> torch.device:
+    """A concrete CUDA device (index filled in) for a device spec."""
+    d = torch.device(device)
+    if d.type != "cuda":
+        raise ValueError(f"expected a CUDA device, got {d}")
+    return d if d.index is not None else torch.device("cuda", torch.cuda.current_device())
+
+
+def _on_device(fn):
+    """Run a binding call with the device of its tensors (or of `self.device` for the
+    plan/extractor classes) made current: the library launches on the current
+    device's stream and keeps per-device state (kernel attributes, helper streams),
+    so a call on cuda:N must run with cuda:N current.  All CUDA tensor arguments
+    must live on that one device."""
+    @functools.wraps(fn)
+    def wrapped(*args, **kw):
+        dev = None
+        if args and isinstance(getattr(args[0], "device", None), torch.device) and not isinstance(args[0], torch.Tensor):
+            dev = args[0].device
+        for a in list(args) + list(kw.values()):
+            if isinstance(a, torch.Tensor) and a.is_cuda:
+                if dev is None:
+                    dev = a.device
+                elif a.device != dev:
+                    raise ValueError(f"tensor on {a.device}, expected {dev} (one device per call)")
+        if dev is None:
+            return fn(*args, **kw)
+        with torch.cuda.device(dev):
+            return fn(*args, **kw)
+    return wrapped
 
 
 def _ptr(t: torch.Tensor):
@@ -195,6 +230,7 @@ def sda_groups(m: int, depth: int) -> int:
     return int(n.value)
 
 
+@_on_device
 def sda_average(frames: torch.Tensor, depth: int) -> torch.Tensor:
     """u8 [m,H,W] -> fp32 [floor(m/depth),H,W] SDA frames, bit-exact."""
     _dev(frames, torch.uint8, "frames", (3,))
@@ -209,6 +245,7 @@ prnu_sda_average = sda_average
 
 
 # ---------------------------------------------------------------- f4 luma
+@_on_device
 def rgb_to_luma(rgb: torch.Tensor, layout: str = "planar", dtype: torch.dtype = torch.float32) -> torch.Tensor:
     """u8 RGB -> luma [n,H,W] with the BT.601 weights (BASELINE config 3).
 
@@ -237,6 +274,7 @@ prnu_rgb_to_luma = rgb_to_luma
 
 
 # ---------------------------------------------------------------- a2-a4
+@_on_device
 def residual(planes: torch.Tensor, params: DenoiseParams | None = None, zero_mean: bool = False,
              out: torch.Tensor | None = None) -> torch.Tensor:
     """W = I - F(I) for fp32 or u8 planes [b,H,W] (or [H,W])."""
@@ -264,6 +302,7 @@ def residual(planes: torch.Tensor, params: DenoiseParams | None = None, zero_mea
 prnu_residual = residual
 
 
+@_on_device
 def residual_variant(planes: torch.Tensor, variant: DenoiseVariant, params: DenoiseParams | None = None,
                      zero_mean: bool = False, out: torch.Tensor | None = None) -> torch.Tensor:
     """f3: W = I - F(I) with a denoiser variant (db8 / pad + periodic / undecimated) for
@@ -298,6 +337,7 @@ def wavelet_filter(taps: int = 8) -> list:
 
 
 # ---------------------------------------------------------------- a5-a6
+@_on_device
 def fingerprint_accumulate(W: torch.Tensor, I: torch.Tensor, sum_WI: torch.Tensor, sum_I2: torch.Tensor):
     """sum_WI += W*I, sum_I2 += I^2 over the batch in order (Eq. 2)."""
     if W.dim() == 2:
@@ -316,6 +356,7 @@ def fingerprint_accumulate(W: torch.Tensor, I: torch.Tensor, sum_WI: torch.Tenso
 prnu_fingerprint_accumulate = fingerprint_accumulate
 
 
+@_on_device
 def fingerprint_finalize(sum_WI: torch.Tensor, sum_I2: torch.Tensor, eps: float = 1e-6,
                          zero_mean: bool = True) -> torch.Tensor:
     """K = sum_WI / max(sum_I2, eps), then row/column zero-mean."""
@@ -335,6 +376,9 @@ prnu_fingerprint_finalize = fingerprint_finalize
 
 @dataclass
 class Fingerprint:
+    """A fingerprint and its MLE sums.  Fingerprints returned by Extractor /
+    GraphExtractor ALIAS the extractor's own buffers (no allocation per call): the
+    next call of the same extractor overwrites them — call .clone() to keep one."""
     K: torch.Tensor        # fp32 [H,W], zero-meaned K_hat
     sum_WI: torch.Tensor   # fp64 [H,W]
     sum_I2: torch.Tensor   # fp64 [H,W]
@@ -342,13 +386,20 @@ class Fingerprint:
     depth: int
     frames: int
 
+    def clone(self) -> "Fingerprint":
+        return Fingerprint(self.K.clone(), self.sum_WI.clone(), self.sum_I2.clone(), self.n_sda, self.depth,
+                           self.frames)
+
 
 class Extractor:
     """Reusable fingerprint extractor for fixed (H, W, depth, batch): owns the
-    workspace and accumulators so repeated calls allocate nothing."""
+    workspace and accumulators so repeated calls allocate nothing.  The returned
+    Fingerprint aliases those accumulators (see Fingerprint)."""
 
     def __init__(self, H: int, W: int, depth: int, batch: int = 16, params: DenoiseParams | None = None,
                  device="cuda", eps: float = 1e-6, host: bool = False):
+        device = _cuda_device(device)
+        self.device = device
         self.H, self.W, self.depth, self.batch, self.eps, self.host = H, W, depth, batch, eps, host
         self.p = _params(params)
         q = _lib.prnu_extract_host_workspace_bytes if host else _lib.prnu_extract_workspace_bytes
@@ -361,6 +412,7 @@ class Extractor:
         self.K = (torch.empty((H, W), dtype=torch.float32, pin_memory=True) if host
                   else torch.empty((H, W), dtype=torch.float32, device=device))
 
+    @_on_device
     def __call__(self, frames: torch.Tensor) -> Fingerprint:
         if frames.dtype != torch.uint8 or frames.dim() != 3 or not frames.is_contiguous():
             raise TypeError("frames must be a contiguous uint8 [m,H,W] tensor")
@@ -396,10 +448,12 @@ class GraphExtractor:
     def __init__(self, m: int, H: int, W: int, depth: int, batch: int = 16, params: DenoiseParams | None = None,
                  device="cuda", eps: float = 1e-6):
         self.ex = Extractor(H, W, depth, batch, params, device, eps)
-        self.frames = torch.empty((m, H, W), dtype=torch.uint8, device=device)
+        self.device = self.ex.device
+        self.frames = torch.empty((m, H, W), dtype=torch.uint8, device=self.device)
         self.graph = None
         self.n_sda = sda_groups(m, depth)
 
+    @_on_device
     def __call__(self, frames: torch.Tensor | None = None) -> Fingerprint:
         if frames is not None and frames.data_ptr() != self.frames.data_ptr():
             self.frames.copy_(frames)
@@ -427,10 +481,12 @@ class CameraBatchExtractor:
     def __init__(self, H: int, W: int, depth: int, batch: int = 16, streams: int = 8,
                  params: DenoiseParams | None = None, device="cuda", eps: float = 1e-6):
         self.H, self.W = H, W
+        device = _cuda_device(device)
         self.exs = [Extractor(H, W, depth, batch, params, device, eps) for _ in range(streams)]
         self.streams = [torch.cuda.Stream(device=device) for _ in range(streams)]
         self.device = device
 
+    @_on_device
     def __call__(self, videos) -> torch.Tensor:
         """videos: a sequence of uint8 [m, H, W] device tensors (or a [n, m, H, W] tensor);
         returns K fp32 [n, H, W]."""
@@ -455,6 +511,8 @@ class MultiExtractor:
     def __init__(self, m: int, H: int, W: int, depths, batch: int = 64, params: DenoiseParams | None = None,
                  device="cuda", eps: float = 1e-6):
         self.m, self.H, self.W, self.batch, self.eps = m, H, W, batch, eps
+        device = _cuda_device(device)
+        self.device = device
         self.depths = [int(d) for d in depths]
         self.p = _params(params)
         self._d = (_i64 * len(self.depths))(*self.depths)
@@ -467,6 +525,7 @@ class MultiExtractor:
         self.K = torch.empty((len(self.depths), H, W), dtype=torch.float32, pin_memory=True)
         self.n_sda = [0] * len(self.depths)
 
+    @_on_device
     def __call__(self, frames_host: torch.Tensor) -> torch.Tensor:
         if frames_host.is_cuda or frames_host.dtype != torch.uint8 or not frames_host.is_contiguous():
             raise TypeError("frames must be a contiguous uint8 CPU (pinned) tensor")
@@ -481,6 +540,7 @@ class MultiExtractor:
         return self.K
 
 
+@_on_device
 def extract_fingerprint(frames: torch.Tensor, depth: int, params: DenoiseParams | None = None, batch: int = 16,
                         eps: float = 1e-6) -> Fingerprint:
     """The three steps of P:58-60 (average, denoise, MLE) + finalize, on device frames."""
@@ -492,6 +552,7 @@ def extract_fingerprint(frames: torch.Tensor, depth: int, params: DenoiseParams 
 prnu_extract_fingerprint = extract_fingerprint
 
 
+@_on_device
 def extract_fingerprint_stride(frames: torch.Tensor, stride: int, params: DenoiseParams | None = None,
                                batch: int = 16, eps: float = 1e-6) -> Fingerprint:
     """f4 I-frame emulation: conventional fingerprint of the
@@ -514,6 +575,7 @@ def extract_fingerprint_stride(frames: torch.Tensor, stride: int, params: Denois
 prnu_extract_fingerprint_stride = extract_fingerprint_stride
 
 
+@_on_device
 def extract_fingerprint_variant(frames: torch.Tensor, depth: int, variant: DenoiseVariant,
                                 params: DenoiseParams | None = None, batch: int = 16,
                                 eps: float = 1e-6) -> Fingerprint:
@@ -539,6 +601,7 @@ def extract_fingerprint_variant(frames: torch.Tensor, depth: int, variant: Denoi
 
 
 # ---------------------------------------------------------------- a7-a8
+@_on_device
 def ncc(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
     """Aligned Pearson correlation per plane (R-16), fp64 [batch] (or 0-dim)."""
     squeeze = a.dim() == 2
@@ -559,6 +622,7 @@ def ncc(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
 prnu_ncc = ncc
 
 
+@_on_device
 def pce_template(K: torch.Tensor, Iq: torch.Tensor) -> torch.Tensor:
     """T = K (.) Iq (R-18); K fp32 [H,W] or [b,H,W], Iq u8 [b,H,W] or [H,W]."""
     if Iq.dim() == 2:
@@ -589,9 +653,12 @@ class PcePlan:
 
     def __init__(self, H: int, W: int, batch: int = 1, device="cuda"):
         self.H, self.W, self.batch = H, W, batch
+        device = _cuda_device(device)
+        self.device = device
         nb = _sz()
         h = _vp()
-        _check(_lib.prnu_pce_plan_create(H, W, batch, ctypes.byref(nb), ctypes.byref(h)), "prnu_pce_plan_create")
+        with torch.cuda.device(device):   # the cuFFT plans belong to the current device
+            _check(_lib.prnu_pce_plan_create(H, W, batch, ctypes.byref(nb), ctypes.byref(h)), "prnu_pce_plan_create")
         self._h = h
         self.nbytes = int(nb.value)
         self.ws = _ws(self.nbytes, device)
@@ -600,6 +667,7 @@ class PcePlan:
                              torch.empty(batch, dtype=torch.int32, device=device),
                              torch.empty(batch, dtype=torch.float64, device=device))
 
+    @_on_device
     def __call__(self, R: torch.Tensor, T: torch.Tensor, exclusion_half: int = 5, aligned: bool = False) -> PceResult:
         if R.dim() == 2:
             R, T = R.unsqueeze(0), T.unsqueeze(0)
@@ -613,6 +681,7 @@ class PcePlan:
                "prnu_pce")
         return PceResult(o.pce.clone(), o.peak_y.clone(), o.peak_x.clone(), o.peak.clone())
 
+    @_on_device
     def set_residual(self, R: torch.Tensor):
         """Cache FFT2 of the residual batch in the plan's workspace (prnu_pce_residual_spectrum)."""
         if R.dim() == 2:
@@ -623,6 +692,7 @@ class PcePlan:
         _check(_lib.prnu_pce_residual_spectrum(self._h, _ptr(R), _ptr(self.ws), self.nbytes, _stream()),
                "prnu_pce_residual_spectrum")
 
+    @_on_device
     def match(self, T: torch.Tensor, exclusion_half: int = 5, aligned: bool = False) -> PceResult:
         """PCE of the cached residuals (set_residual) against templates T (prnu_pce_cached)."""
         if T.dim() == 2:
@@ -639,7 +709,8 @@ class PcePlan:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value and _lib is not None:
-            _lib.prnu_pce_plan_destroy(h)
+            with torch.cuda.device(self.device):
+                _lib.prnu_pce_plan_destroy(h)
             self._h = None
 
 
@@ -650,13 +721,17 @@ class WdftPlan:
 
     def __init__(self, H: int, W: int, batch: int = 1, device="cuda"):
         self.H, self.W, self.batch = H, W, batch
+        device = _cuda_device(device)
+        self.device = device
         nb = _sz()
         h = _vp()
-        _check(_lib.prnu_wdft_plan_create(H, W, batch, ctypes.byref(nb), ctypes.byref(h)), "prnu_wdft_plan_create")
+        with torch.cuda.device(device):
+            _check(_lib.prnu_wdft_plan_create(H, W, batch, ctypes.byref(nb), ctypes.byref(h)), "prnu_wdft_plan_create")
         self._h = h
         self.nbytes = int(nb.value)
         self.ws = _ws(self.nbytes, device)
 
+    @_on_device
     def __call__(self, K: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         squeeze = K.dim() == 2
         if squeeze:
@@ -671,10 +746,12 @@ class WdftPlan:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value and _lib is not None:
-            _lib.prnu_wdft_plan_destroy(h)
+            with torch.cuda.device(self.device):
+                _lib.prnu_wdft_plan_destroy(h)
             self._h = None
 
 
+@_on_device
 def wdft(K: torch.Tensor) -> torch.Tensor:
     b = 1 if K.dim() == 2 else K.shape[0]
     return WdftPlan(K.shape[-2], K.shape[-1], b, K.device)(K)
@@ -683,6 +760,7 @@ def wdft(K: torch.Tensor) -> torch.Tensor:
 prnu_wdft = wdft
 
 
+@_on_device
 def pce(R: torch.Tensor, T: torch.Tensor, exclusion_half: int = 5, aligned: bool = False) -> PceResult:
     b = 1 if R.dim() == 2 else R.shape[0]
     return PcePlan(R.shape[-2], R.shape[-1], b, R.device)(R, T, exclusion_half, aligned)
@@ -732,11 +810,13 @@ class BlockPlan:
 
     def __init__(self, H: int, W: int, block: int = 500, device="cuda"):
         self.H, self.W, self.block = H, W, block
+        device = _cuda_device(device)
         n = _i()
         nb = _sz()
         h = _vp()
-        _check(_lib.prnu_block_plan_create(H, W, block, ctypes.byref(n), ctypes.byref(nb), ctypes.byref(h)),
-               "prnu_block_plan_create")
+        with torch.cuda.device(device):
+            _check(_lib.prnu_block_plan_create(H, W, block, ctypes.byref(n), ctypes.byref(nb), ctypes.byref(h)),
+                   "prnu_block_plan_create")
         self._h = h
         self.n_tiles = int(n.value)
         self.nbytes = int(nb.value)
@@ -749,6 +829,7 @@ class BlockPlan:
         return [(y, x, min(b, self.H - y), min(b, self.W - x)) for y in range(0, self.H, b)
                 for x in range(0, self.W, b)]
 
+    @_on_device
     def __call__(self, R: torch.Tensor, T: torch.Tensor, exclusion_half: int = 5):
         _dev(R, torch.float32, "residual", (2,))
         _dev(T, torch.float32, "template", (2,))
@@ -763,10 +844,12 @@ class BlockPlan:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value and _lib is not None:
-            _lib.prnu_block_plan_destroy(h)
+            with torch.cuda.device(self.device):
+                _lib.prnu_block_plan_destroy(h)
             self._h = None
 
 
+@_on_device
 def block_match(R: torch.Tensor, T: torch.Tensor, block: int = 500, exclusion_half: int = 5):
     return BlockPlan(R.shape[-2], R.shape[-1], block, R.device)(R, T, exclusion_half)
 

@@ -11,7 +11,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libprnu.so")
-SOURCES = ["capi.cu", "sda.cu", "wavelet.cu", "strip.cu", "analysis.cu", "split.cu", "mle.cu", "pce.cu", "wdft.cu", "variant.cu"]
+SOURCES = ["capi.cu", "sda.cu", "wavelet.cu", "analysis.cu", "shrink.cu", "mle.cu", "pce.cu", "wdft.cu", "variant.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
@@ -30,8 +30,15 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+STAMP = os.path.join(BUILD, "flags.stamp")
+
+
 def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
+    # objects built with other flags (PRNU_DEBUG, PRNU_NVCC_DEFS / _FLAGS) are stale
+    stamp = " ".join([NVCC, *ARCH, *FLAGS])
+    if not os.path.exists(STAMP) or open(STAMP).read() != stamp:
+        force = True
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(ROOT, "include", "prnu.h"))
     jobs = []
@@ -56,6 +63,8 @@ def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) 
                 sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
             if r.returncode:
                 raise RuntimeError(f"nvcc failed for {cmd[-3]}")
+    with open(STAMP, "w") as f:
+        f.write(stamp)
     if force or jobs or _stale(LIB, objs):
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcufft", "-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True)

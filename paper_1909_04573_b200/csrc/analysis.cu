@@ -80,6 +80,15 @@ struct AlCfg<uint8_t> {
     static constexpr int MINB = 3;
 };
 template <>
+struct AlCfg<uint16_t> {   // exact SDA group sums (level 1 at 2 <= d <= 257)
+    static constexpr int OMAX = 112;
+    static constexpr int P1 = 124;
+    static constexpr int P2 = 122;
+    static constexpr int NSTG = 1;
+    static constexpr int BOXW = 152;   // elements (304 B = 76 words == 12 mod 32)
+    static constexpr int MINB = 3;
+};
+template <>
 struct AlCfg<float> {
     static constexpr int OMAX = 104;   // region 112
     static constexpr int P1 = 116;     // == 20 mod 32
@@ -103,7 +112,9 @@ constexpr size_t al_smem_bytes() {
 }
 static_assert(2 * AL_IR * AL_RBP <= 5 * AL_BK * AlCfg<float>::P1, "row buffer inside the da planes");
 static_assert(AlCfg<uint8_t>::OMAX + 8 <= AlCfg<uint8_t>::P2 && AlCfg<float>::OMAX + 8 <= AlCfg<float>::P2, "V planes");
-static_assert(al_smem_bytes<uint8_t>() <= 75 * 1024 && al_smem_bytes<float>() <= 75 * 1024, "3 CTAs per SM");
+static_assert(al_smem_bytes<uint8_t>() <= 75 * 1024 && al_smem_bytes<uint16_t>() <= 75 * 1024 &&
+                  al_smem_bytes<float>() <= 75 * 1024,
+              "3 CTAs per SM");
 
 struct AlArgs {
     const void* in;
@@ -121,6 +132,7 @@ struct AlArgs {
     int O;                  // output columns per strip (multiple of 8)
     int SH;                 // output rows per segment (multiple of 8)
     int use_tma;
+    float div_d, div_r;     // u16 SDA sums: S = RN(sum / d) (R-11)
 };
 
 // packed fp32 helpers: {k, k} * b + c with k an immediate (FFMA2 imm form)
@@ -174,6 +186,12 @@ __device__ __forceinline__ void al_stg_put(uint8_t* s, int r, int x, float v) {
     if (x < BW) s[r * BW + x] = u;
     if (x >= 128) s[AL_IR * BW + r * BW + x - 128] = u;
 }
+__device__ __forceinline__ void al_stg_put(uint16_t* s, int r, int x, float v) {
+    constexpr int BW = AlCfg<uint16_t>::BOXW;
+    const uint16_t u = (uint16_t)v;
+    if (x < BW) s[r * BW + x] = u;
+    if (x >= 128) s[AL_IR * BW + r * BW + x - 128] = u;
+}
 __device__ __forceinline__ void al_stg_put(float* s, int r, int x, float v) {
     constexpr int BW = AlCfg<float>::BOXW;
     if (x < BW) s[r * BW + x] = v;
@@ -183,21 +201,8 @@ __device__ __forceinline__ void al_stg_put(float* s, int r, int x, float v) {
 // ---- row pass of one item (staged row r, group g: region columns 8g .. 8g+7):
 // lo/hi (unscaled o2 / e3) of the 8 coefficient columns as pairs (i, i+4), i < 4.
 // Inputs v[k] = logical staged column 16g + 2 + k (k < 22) = x[2 gc0 - 6 + k].
-__device__ __forceinline__ void al_rowpass(const uint8_t* s, int r, int g, float2 (&L)[4], float2 (&Hh)[4]) {
-    constexpr int BW = AlCfg<uint8_t>::BOXW;
-    const uint8_t* src = s + (g < 8 ? r * BW + 16 * g : AL_IR * BW + r * BW + 16 * g - 128);
-    const uint4 w0 = *reinterpret_cast<const uint4*>(src);
-    const uint2 w1 = *reinterpret_cast<const uint2*>(src + 16);
-    const uint32_t w[6] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y};
-    // byte b (logical 16g + b) -> 2^23 + byte as a float bit pattern
-    auto bf = [&](int b) { return __uint_as_float(__byte_perm(w[b >> 2], 0x4B000000u, 0x7540u | (uint32_t)(b & 3))); };
-    const float2 m23 = make_float2(-8388608.f, -8388608.f);
-    float2 E[7], O[7];
-#pragma unroll
-    for (int j = 0; j < 7; ++j) {   // E[j] = (v[2j], v[2j+8]), O[j] = (v[2j+1], v[2j+9]) exactly
-        E[j] = add2(make_float2(bf(2 * j + 2), bf(2 * j + 10)), m23);
-        O[j] = add2(make_float2(bf(2 * j + 3), bf(2 * j + 11)), m23);
-    }
+// lifting of the 14 input pairs E[j] = (v[2j], v[2j+8]), O[j] = (v[2j+1], v[2j+9]), j < 7
+__device__ __forceinline__ void al_lift_pairs(const float2 (&E)[7], const float2 (&O)[7], float2 (&L)[4], float2 (&Hh)[4]) {
     float2 E1[7], O1[6], E2[6], O2[5];
 #pragma unroll
     for (int j = 0; j < 7; ++j) E1[j] = lf2(-LF_C1, O[j], E[j]);
@@ -213,7 +218,51 @@ __device__ __forceinline__ void al_rowpass(const uint8_t* s, int r, int g, float
         Hh[i] = lf2(-LF_C5, O2[i + 1], E2[i + 2]);  // e3 at k = i, i + 4 (e3[j] = e2[j] - C5 o2[j-1])
     }
 }
-__device__ __forceinline__ void al_rowpass(const float* s, int r, int g, float2 (&L)[4], float2 (&Hh)[4]) {
+__device__ __forceinline__ void al_rowpass(const uint8_t* s, int r, int g, float, float, float2 (&L)[4],
+                                           float2 (&Hh)[4]) {
+    constexpr int BW = AlCfg<uint8_t>::BOXW;
+    const uint8_t* src = s + (g < 8 ? r * BW + 16 * g : AL_IR * BW + r * BW + 16 * g - 128);
+    const uint4 w0 = *reinterpret_cast<const uint4*>(src);
+    const uint2 w1 = *reinterpret_cast<const uint2*>(src + 16);
+    const uint32_t w[6] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y};
+    // byte b (logical 16g + b) -> 2^23 + byte as a float bit pattern
+    auto bf = [&](int b) { return __uint_as_float(__byte_perm(w[b >> 2], 0x4B000000u, 0x7540u | (uint32_t)(b & 3))); };
+    const float2 m23 = make_float2(-8388608.f, -8388608.f);
+    float2 E[7], O[7];
+#pragma unroll
+    for (int j = 0; j < 7; ++j) {   // E[j] = (v[2j], v[2j+8]), O[j] = (v[2j+1], v[2j+9]) exactly
+        E[j] = add2(make_float2(bf(2 * j + 2), bf(2 * j + 10)), m23);
+        O[j] = add2(make_float2(bf(2 * j + 3), bf(2 * j + 11)), m23);
+    }
+    al_lift_pairs(E, O, L, Hh);
+}
+// exact SDA group sums: v[k] = RN(sum / d) (R-11), then the same lifting
+__device__ __forceinline__ void al_rowpass(const uint16_t* s, int r, int g, float dv, float rv, float2 (&L)[4],
+                                           float2 (&Hh)[4]) {
+    constexpr int BW = AlCfg<uint16_t>::BOXW;
+    const uint16_t* src = s + (g < 8 ? r * BW + 16 * g : AL_IR * BW + r * BW + 16 * g - 128);
+    const uint4 w0 = *reinterpret_cast<const uint4*>(src);
+    const uint4 w1 = *reinterpret_cast<const uint4*>(src + 8);
+    const uint4 w2 = *reinterpret_cast<const uint4*>(src + 16);
+    const uint32_t w[12] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w, w2.x, w2.y, w2.z, w2.w};
+    // element e (logical 16g + e) -> 2^23 + sum as a float bit pattern
+    auto bf = [&](int e) {
+        return __uint_as_float(__byte_perm(w[e >> 1], 0x4B000000u, (e & 1) ? 0x7632u : 0x7610u));
+    };
+    const float2 m23 = make_float2(-8388608.f, -8388608.f);
+    float2 E[7], O[7];
+#pragma unroll
+    for (int j = 0; j < 7; ++j) {   // sums exactly, then q = RN(sum / d) lane-wise (sda_div, packed)
+        const float2 se = add2(make_float2(bf(2 * j + 2), bf(2 * j + 10)), m23);
+        const float2 so = add2(make_float2(bf(2 * j + 3), bf(2 * j + 11)), m23);
+        const float2 qe = mul2(se, make_float2(rv, rv)), qo = mul2(so, make_float2(rv, rv));
+        E[j] = ffma2(rv, ffma2(-dv, qe, se), qe);
+        O[j] = ffma2(rv, ffma2(-dv, qo, so), qo);
+    }
+    al_lift_pairs(E, O, L, Hh);
+}
+__device__ __forceinline__ void al_rowpass(const float* s, int r, int g, float, float, float2 (&L)[4],
+                                           float2 (&Hh)[4]) {
     constexpr int BW = AlCfg<float>::BOXW;
     const float* src = s + (g < 8 ? r * BW + 16 * g : AL_IR * BW + r * BW + 16 * g - 128) + 2;
     float v[22];
@@ -402,7 +451,7 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
             const int g = ga + 8 * h;
             if (h == 0 ? doA : doB) {
                 float2 L[4], Hh[4];
-                al_rowpass(s, prow, g, L, Hh);
+                al_rowpass(s, prow, g, a.div_d, a.div_r, L, Hh);
                 float2* dl = reinterpret_cast<float2*>(RBlo + rr * AL_RBP + 8 * g);
                 float2* dh = reinterpret_cast<float2*>(RBhi + rr * AL_RBP + 8 * g);
 #pragma unroll
@@ -767,7 +816,7 @@ bool encode_tensor_map_3d(CUtensorMap* map, CUtensorMapDataType dt, size_t elem_
 template <typename T>
 static int lift_launch(const T* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll, float* d0,
                        float* d1, float* d2, long long out_bstride, int out_pitch, int nH, int nW,
-                       const ShrinkParams& sp, int nb, cudaStream_t st) {
+                       const ShrinkParams& sp, const SdaDiv& div, int nb, cudaStream_t st) {
     static DeviceFlags done[2];
     int rc;
     if ((rc = set_smem_attr((const void*)k_analysis_lift<T, AlCfg<T>::MINB, true>, al_smem_bytes<T>(), done[0])))
@@ -790,6 +839,8 @@ static int lift_launch(const T* in, long long in_bstride, int in_pitch, int NH, 
     a.nH = nH;
     a.nW = nW;
     a.sp = sp;
+    a.div_d = div.d;
+    a.div_r = div.r;
     const int S0 = (nW + AlCfg<T>::OMAX - 1) / AlCfg<T>::OMAX;
     a.O = (int)align_up((size_t)((nW + S0 - 1) / S0), 8);
     const int S = (nW + a.O - 1) / a.O;
@@ -803,7 +854,9 @@ static int lift_launch(const T* in, long long in_bstride, int in_pitch, int NH, 
     nseg = (nH + a.SH - 1) / a.SH;
     CUtensorMap map{};
     const size_t es = sizeof(T);
-    const CUtensorMapDataType dt = sizeof(T) == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    const CUtensorMapDataType dt = sizeof(T) == 1   ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                   : sizeof(T) == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                                    : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     a.use_tma = ((in_pitch * es) % 16 == 0) && ((in_bstride * es) % 16 == 0) && ((uintptr_t)in % 16 == 0) &&
                 encode_tensor_map_3d(&map, dt, es, in, (uint64_t)NW, (uint64_t)NH, (uint64_t)nb, (uint64_t)in_pitch * es,
                                      (uint64_t)in_bstride * es, AlCfg<T>::BOXW, AL_IR);
@@ -819,13 +872,19 @@ int launch_analysis_lift_u8(const uint8_t* in, long long in_bstride, int in_pitc
                             float* d0, float* d1, float* d2, long long out_bstride, int out_pitch, int nH, int nW,
                             const ShrinkParams& sp, int nb, cudaStream_t st) {
     return lift_launch<uint8_t>(in, in_bstride, in_pitch, NH, NW, ll, d0, d1, d2, out_bstride, out_pitch, nH, nW, sp,
-                                nb, st);
+                                SdaDiv{}, nb, st);
+}
+int launch_analysis_lift_u16(const uint16_t* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll,
+                             float* d0, float* d1, float* d2, long long out_bstride, int out_pitch, int nH, int nW,
+                             const ShrinkParams& sp, const SdaDiv& div, int nb, cudaStream_t st) {
+    return lift_launch<uint16_t>(in, in_bstride, in_pitch, NH, NW, ll, d0, d1, d2, out_bstride, out_pitch, nH, nW,
+                                 sp, div, nb, st);
 }
 int launch_analysis_lift_f32(const float* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll,
                              float* d0, float* d1, float* d2, long long out_bstride, int out_pitch, int nH, int nW,
                              const ShrinkParams& sp, int nb, cudaStream_t st) {
     return lift_launch<float>(in, in_bstride, in_pitch, NH, NW, ll, d0, d1, d2, out_bstride, out_pitch, nH, nW, sp,
-                              nb, st);
+                              SdaDiv{}, nb, st);
 }
 
 }  // namespace prnu

@@ -128,8 +128,13 @@ int run_residual(const TIn* in, int nb, int H, int W, const Pyramid& p, const Sh
                  float* ws_pyr, cudaStream_t st, int in_pitch = 0);
 template <typename TIn>
 int run_residual_accumulate(const TIn* in, const TIn* I, int nb, int H, int W, const Pyramid& p,
-                            const ShrinkParams& sp, double* num, double* den, float* ws_pyr, cudaStream_t st,
-                            cudaEvent_t acc_wait, cudaEvent_t acc_done, long long frame_stride, int in_pitch = 0);
+                            const ShrinkParams& sp, const SdaDiv& div, double* num, double* den, float* ws_pyr,
+                            cudaStream_t st, cudaEvent_t acc_wait, cudaEvent_t acc_done, long long frame_stride,
+                            int in_pitch = 0);
+int launch_sda_sum_u16(const uint8_t* frames, long long n_groups, int H, int W, int d, uint16_t* out, int Wp,
+                       cudaStream_t st);
+int launch_sda_average_pitched(const uint8_t* frames, long long n_groups, int H, int W, int d, float* out, int Wp,
+                               cudaStream_t st);
 int launch_pad_rows_u8(const uint8_t* src, long long nb, int H, int W, long long src_stride, uint8_t* dst, int Wp,
                        cudaStream_t st);
 int launch_accumulate(const float* W, const float* I, int batch, long long P, double* num, double* den,
@@ -187,25 +192,25 @@ static size_t residual_ws(int batch, int H, int W, const Pyramid& pyr) {
 // Waves of SDA frames alternate between kExtractStreams streams (each with its
 // own pyramid/SDA workspace) so one wave's small levels overlap the next wave's
 // large ones; only the accumulating launches are chained (ascending order).
-constexpr int kMaxExtractStreams = 4;
+// Three streams measured best (round 1: 2 -> 3 streams -3.5% per step, 4 no gain).
+constexpr int kExtractStreams = 3;
+// planes per launch along grid.z (the analysis and synthesis kernels)
+constexpr int kMaxBatch = 65535;
+static int extract_streams() { return kExtractStreams; }
 
-static int extract_streams() {
-    static const int n = [] {
-        const char* e = getenv("PRNU_STREAMS");
-        int v = e ? atoi(e) : 3;
-        return v < 1 ? 1 : (v > kMaxExtractStreams ? kMaxExtractStreams : v);
-    }();
-    return n;
-}
-
-// u8 frames whose rows are not 16-byte multiples cannot be TMA-staged: such waves are
-// first copied to rows of align16(W) bytes (one HBM pass) so both the analysis and the
-// accumulation keep their TMA paths.
+// Frames that TMA cannot stage (rows not 16-byte multiples, or a misaligned base or
+// frame stride) are first copied to rows of align16(W) bytes (one HBM pass) so both
+// the analysis and the accumulation keep their TMA paths.  SDA groups (d >= 2) go
+// through exact u16 group sums (d <= 257) or fp32 frames (d > 257), both written with
+// 16-byte rows by the SDA kernel.
 static int pad_pitch_u8(int W) { return (int)align_up((size_t)W, 16); }
+static int sum_pitch_u16(int W) { return (int)align_up((size_t)W, 8); }
+static int sda_pitch_f32(int W) { return (int)align_up((size_t)W, 4); }
 static size_t extract_wave_ws(int H, int W, int batch, int64_t depth, const Pyramid& pyr) {
     size_t s = align_up(sizeof(float) * pyramid_floats_per_frame(pyr) * (size_t)batch, 256);
-    if (depth > 1) s += align_up(sizeof(float) * (size_t)H * W * batch, 256);
-    else if (W % 16) s += align_up((size_t)H * pad_pitch_u8(W) * batch, 256);
+    if (depth > 257) s += align_up(sizeof(float) * (size_t)H * sda_pitch_f32(W) * batch, 256);
+    else if (depth > 1) s += align_up(sizeof(uint16_t) * (size_t)H * sum_pitch_u16(W) * batch, 256);
+    else s += align_up((size_t)H * pad_pitch_u8(W) * batch, 256);   // re-pitched u8 frames (when needed)
     return s;
 }
 
@@ -229,23 +234,34 @@ static int extract_chunk(const uint8_t* frames, int64_t nb, int H, int W, int64_
     float* pyr_ws = reinterpret_cast<float*>(ws);
     size_t pyr_bytes = align_up(sizeof(float) * pyramid_floats_per_frame(pyr) * (size_t)nb, 256);
     const long long P = (long long)H * W;
+    int rc;
     if (depth == 1 || depth < 0) {
         const long long fstride = depth < 0 ? -depth * P : P;
-        if (W % 16) {   // pitched copy (see extract_wave_ws)
+        if (W % 16 || fstride % 16 || (uintptr_t)frames % 16) {   // re-pitched copy (see extract_wave_ws)
             const int Wp = pad_pitch_u8(W);
             uint8_t* padded = reinterpret_cast<uint8_t*>(ws + pyr_bytes);
-            int rc = launch_pad_rows_u8(frames, nb, H, W, fstride, padded, Wp, st);
-            if (rc) return rc;
-            return run_residual_accumulate<uint8_t>(padded, padded, (int)nb, H, W, pyr, sp, num, den, pyr_ws, st,
-                                                    acc_wait, acc_done, (long long)H * Wp, Wp);
+            if ((rc = launch_pad_rows_u8(frames, nb, H, W, fstride, padded, Wp, st))) return rc;
+            return run_residual_accumulate<uint8_t>(padded, padded, (int)nb, H, W, pyr, sp, SdaDiv{}, num, den, pyr_ws,
+                                                    st, acc_wait, acc_done, (long long)H * Wp, Wp);
         }
-        return run_residual_accumulate<uint8_t>(frames, frames, (int)nb, H, W, pyr, sp, num, den, pyr_ws, st,
+        return run_residual_accumulate<uint8_t>(frames, frames, (int)nb, H, W, pyr, sp, SdaDiv{}, num, den, pyr_ws, st,
                                                 acc_wait, acc_done, fstride);
     }
+    if (depth <= 257) {   // exact u16 group sums; S = RN(sum / d) inside the kernels (R-11)
+        const int Wp = sum_pitch_u16(W);
+        uint16_t* S = reinterpret_cast<uint16_t*>(ws + pyr_bytes);
+        if ((rc = launch_sda_sum_u16(frames, nb, H, W, (int)depth, S, Wp, st))) return rc;
+        SdaDiv div;
+        div.d = (float)depth;
+        div.r = 1.0f / div.d;   // IEEE fp32 division: RN(1/d)
+        return run_residual_accumulate<uint16_t>(S, S, (int)nb, H, W, pyr, sp, div, num, den, pyr_ws, st, acc_wait,
+                                                 acc_done, (long long)H * Wp, Wp);
+    }
+    const int Wp = sda_pitch_f32(W);
     float* S = reinterpret_cast<float*>(ws + pyr_bytes);
-    int rc = launch_sda_average(frames, nb, P, (int)depth, S, st);
-    if (rc) return rc;
-    return run_residual_accumulate<float>(S, S, (int)nb, H, W, pyr, sp, num, den, pyr_ws, st, acc_wait, acc_done, P);
+    if ((rc = launch_sda_average_pitched(frames, nb, H, W, (int)depth, S, Wp, st))) return rc;
+    return run_residual_accumulate<float>(S, S, (int)nb, H, W, pyr, sp, SdaDiv{}, num, den, pyr_ws, st, acc_wait,
+                                          acc_done, (long long)H * Wp, Wp);
 }
 
 template <typename TIn>
@@ -253,7 +269,7 @@ static int residual_impl(const TIn* planes, int batch, int H, int W, const prnu_
                          float* W_out, void* ws, size_t ws_bytes, void* stream) {
     int rc;
     if (!planes || !W_out || !ws) return fail(PRNU_INVALID_ARG, "null pointer");
-    if (batch < 1) return fail(PRNU_INVALID_ARG, "batch must be >= 1");
+    if (batch < 1 || batch > kMaxBatch) return fail(PRNU_INVALID_ARG, "batch must be in 1..65535");
     if ((rc = check_dims(H, W))) return rc;
     ShrinkParams sp;
     if ((rc = validate_params(p, H, W, &sp))) return rc;
@@ -379,6 +395,37 @@ size_t prnu_extract_workspace_bytes(int H, int W, int batch, int64_t depth, cons
     return extract_ws(H, W, batch, depth, make_pyramid(H, W, p->levels));
 }
 
+// Per-device helper streams and events of the multi-stream extraction, created on
+// first use and kept for the life of the process (no per-call create/destroy).
+struct ExtractCtx {
+    std::mutex mu;
+    cudaStream_t helper[kExtractStreams - 1] = {};
+    cudaEvent_t ev_start = nullptr, ev_end[kExtractStreams] = {}, acc[kExtractStreams] = {};
+};
+static int extract_ctx(ExtractCtx** out) {
+    static std::mutex g_mu;
+    static ExtractCtx* g_ctx[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return fail(PRNU_CUDA_ERROR, "cudaGetDevice");
+    std::lock_guard<std::mutex> lock(g_mu);
+    if (!g_ctx[dev]) {
+        ExtractCtx* c = new ExtractCtx();
+        cudaError_t e = cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming);
+        for (int j = 0; j < kExtractStreams && e == cudaSuccess; ++j) {
+            if (j > 0) e = cudaStreamCreateWithFlags(&c->helper[j - 1], cudaStreamNonBlocking);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_end[j], cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->acc[j], cudaEventDisableTiming);
+        }
+        if (e != cudaSuccess) {
+            delete c;   // (handles created before the failure are leaked: the device is unusable anyway)
+            return fail(PRNU_CUDA_ERROR, std::string("extraction streams: ") + cudaGetErrorString(e));
+        }
+        g_ctx[dev] = c;
+    }
+    *out = g_ctx[dev];
+    return PRNU_OK;
+}
+
 // mode 0: SDA depth `depth` (1 = conventional); mode 1: stride selection with
 // step `depth` (frames 0, depth, 2 depth, ... < m), each frame denoised.
 static int extract_impl(const uint8_t* frames, int64_t m, int H, int W, int64_t depth, int mode,
@@ -386,7 +433,7 @@ static int extract_impl(const uint8_t* frames, int64_t m, int H, int W, int64_t 
                         double* sum_I2, int64_t* n_sda_host, void* ws, size_t ws_bytes, void* stream) {
     int rc;
     if (!frames || !K_out || !sum_WI || !sum_I2 || !ws) return fail(PRNU_INVALID_ARG, "null pointer");
-    if (batch < 1) return fail(PRNU_INVALID_ARG, "batch must be >= 1");
+    if (batch < 1 || batch > kMaxBatch) return fail(PRNU_INVALID_ARG, "batch must be in 1..65535");
     if ((rc = check_dims(H, W))) return rc;
     int64_t ns;
     if ((rc = prnu_sda_groups(m, depth, &ns))) return rc;
@@ -422,39 +469,30 @@ static int extract_impl(const uint8_t* frames, int64_t m, int H, int W, int64_t 
         return launch_finalize(sum_WI, sum_I2, H, W, eps, 1, K_out, zm, st);
     }
     // nst streams: waves rotate over them; each wave's accumulation waits for the
-    // previous wave's (events), so the per-pixel order stays ascending
-    cudaStream_t sts[kMaxExtractStreams] = {st, nullptr, nullptr, nullptr};
-    cudaEvent_t ev_start = nullptr, ev_end[kMaxExtractStreams] = {}, acc[kMaxExtractStreams] = {};
-    cudaError_t e = cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
-    for (int j = 0; j < nst && e == cudaSuccess; ++j) {
-        if (j > 0) e = cudaStreamCreateWithFlags(&sts[j], cudaStreamNonBlocking);
-        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_end[j], cudaEventDisableTiming);
-        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&acc[j], cudaEventDisableTiming);
-    }
-    if (e == cudaSuccess) e = cudaEventRecord(ev_start, st);   // helper streams start after the caller's prior work
-    for (int j = 1; j < nst && e == cudaSuccess; ++j) e = cudaStreamWaitEvent(sts[j], ev_start, 0);
+    // previous wave's (events), so the per-pixel order stays ascending.  The helper
+    // streams and events are created once per device (ExtractCtx) and reused; the
+    // context's mutex serialises the enqueue of concurrent calls on one device.
+    ExtractCtx* cx = nullptr;
+    if ((rc = extract_ctx(&cx))) return rc;
+    std::lock_guard<std::mutex> lock(cx->mu);
+    cudaStream_t sts[kExtractStreams] = {st};
+    for (int j = 1; j < nst; ++j) sts[j] = cx->helper[j - 1];
+    cudaError_t e = cudaEventRecord(cx->ev_start, st);   // helper streams start after the caller's prior work
+    for (int j = 1; j < nst && e == cudaSuccess; ++j) e = cudaStreamWaitEvent(sts[j], cx->ev_start, 0);
     rc = (e == cudaSuccess) ? PRNU_OK : fail(PRNU_CUDA_ERROR, std::string("stream setup: ") + cudaGetErrorString(e));
     int64_t k = 0;
     for (int64_t g0 = 0; g0 < ns && rc == PRNU_OK; g0 += batch, ++k) {
         int64_t nb = std::min<int64_t>(batch, ns - g0);
         const int j = (int)(k % nst), jp = (int)((k + nst - 1) % nst);
         rc = extract_chunk(frames + (size_t)g0 * depth * P, nb, H, W, dsel, pyr, sp, sum_WI, sum_I2,
-                           wsb + j * wave, sts[j], k > 0 ? acc[jp] : nullptr, acc[j]);
+                           wsb + j * wave, sts[j], k > 0 ? cx->acc[jp] : nullptr, cx->acc[j]);
     }
     for (int j = 1; j < nst && rc == PRNU_OK; ++j) {   // the caller's stream sees all waves
-        e = cudaEventRecord(ev_end[j], sts[j]);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev_end[j], 0);
+        e = cudaEventRecord(cx->ev_end[j], sts[j]);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, cx->ev_end[j], 0);
         if (e != cudaSuccess) rc = fail(PRNU_CUDA_ERROR, std::string("stream join: ") + cudaGetErrorString(e));
     }
     if (rc == PRNU_OK) rc = launch_finalize(sum_WI, sum_I2, H, W, eps, 1, K_out, zm, st);
-    // destroying a stream/event with pending work is legal: resources are released on completion
-    for (int j = 1; j < nst; ++j)
-        if (sts[j]) cudaStreamDestroy(sts[j]);
-    if (ev_start) cudaEventDestroy(ev_start);
-    for (int j = 0; j < nst; ++j) {
-        if (ev_end[j]) cudaEventDestroy(ev_end[j]);
-        if (acc[j]) cudaEventDestroy(acc[j]);
-    }
     return rc;
 }
 
@@ -486,7 +524,7 @@ int prnu_extract_fingerprint_host(const uint8_t* frames_host, int64_t m, int H, 
                                   void* stream) {
     int rc;
     if (!frames_host || !K_out_host || !sum_WI || !sum_I2 || !ws) return fail(PRNU_INVALID_ARG, "null pointer");
-    if (batch < 1) return fail(PRNU_INVALID_ARG, "batch must be >= 1");
+    if (batch < 1 || batch > kMaxBatch) return fail(PRNU_INVALID_ARG, "batch must be in 1..65535");
     if ((rc = check_dims(H, W))) return rc;
     int64_t ns;
     if ((rc = prnu_sda_groups(m, depth, &ns))) return rc;
@@ -782,7 +820,7 @@ int prnu_residual_variant(const float* planes, int batch, int H, int W, const pr
                           void* stream) {
     int rc;
     if (!planes || !W_out || !ws) return fail(PRNU_INVALID_ARG, "null pointer");
-    if (batch < 1) return fail(PRNU_INVALID_ARG, "batch must be >= 1");
+    if (batch < 1 || batch > kMaxBatch) return fail(PRNU_INVALID_ARG, "batch must be in 1..65535");
     if ((rc = check_dims(H, W))) return rc;
     ShrinkParams sp;
     if ((rc = validate_params(p, H, W, &sp))) return rc;

@@ -128,6 +128,25 @@ struct Pyramid {
 
 Pyramid make_pyramid(int H, int W, int levels);
 
+// SDA frames from exact group sums (a1, R-11): S = RN(sum / d) with sum an integer
+// < 2^24.  d and r = RN(1/d) as fp32; d = 1 for plain frames.
+struct SdaDiv {
+    float d = 1.0f, r = 1.0f;
+};
+// u16 in the low (hi = 0) or high (hi = 1) half of w -> its exact fp32 value
+// (2^23 + u as a bit pattern, minus 2^23).
+__device__ __forceinline__ float u16_to_f32(uint32_t w, int hi) {
+    return __fadd_rn(__uint_as_float(__byte_perm(w, 0x4B000000u, hi ? 0x7632u : 0x7610u)), -8388608.0f);
+}
+// RN_fp32(s / d): reciprocal product plus one FMA correction.  Equal to the correctly
+// rounded quotient for every integer s <= 255 d and 2 <= d <= 257 (and the config
+// depths 300..3600): exhaustive check in tools/sda_div_check.py / tests/test_capi_cpu.py.
+__device__ __forceinline__ float sda_div(float s, float d, float r) {
+    const float q0 = __fmul_rn(s, r);
+    const float rem = __fmaf_rn(-q0, d, s);
+    return __fmaf_rn(rem, r, q0);
+}
+
 // Shrink constants passed by value to kernels.
 struct ShrinkParams {
     float sigma0_sq;
@@ -136,28 +155,18 @@ struct ShrinkParams {
 
 int validate_params(const prnu_denoise_params* p, int H, int W, ShrinkParams* sp);
 
-// split.cu: one level as a streaming DWT kernel + a streaming shrink kernel
-int launch_dwt_strip_u8(const uint8_t* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll, float* c0,
-                        float* c1, float* c2, long long out_bstride, int out_pitch, int nH, int nW, int nb,
-                        cudaStream_t st);
-int launch_dwt_strip_f32(const float* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll, float* c0,
-                         float* c1, float* c2, long long out_bstride, int out_pitch, int nH, int nW, int nb,
-                         cudaStream_t st);
+// shrink.cu: the streaming shrink of detail planes held in HBM (variants, WDFT)
 int launch_shrink_strip(const float* const src[3], float* const dst[3], long long bstride, int pitch, int nH, int nW,
                         const ShrinkParams& sp, int nb, cudaStream_t st, int nsub = 3, const float* s0_dev = nullptr);
 
-// strip.cu: column-streaming analysis + shrink of one level (see strip.cu)
-int launch_analysis_strip_u8(const uint8_t* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll,
-                             float* d0, float* d1, float* d2, long long out_bstride, int out_pitch, int nH, int nW,
-                             const ShrinkParams& sp, int nb, cudaStream_t st);
-int launch_analysis_strip_f32(const float* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll,
-                              float* d0, float* d1, float* d2, long long out_bstride, int out_pitch, int nH, int nW,
-                              const ShrinkParams& sp, int nb, cudaStream_t st);
 
 // analysis.cu: column-streaming analysis (lifting) + shrink of one level
 int launch_analysis_lift_u8(const uint8_t* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll,
                             float* d0, float* d1, float* d2, long long out_bstride, int out_pitch, int nH, int nW,
                             const ShrinkParams& sp, int nb, cudaStream_t st);
+int launch_analysis_lift_u16(const uint16_t* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll,
+                             float* d0, float* d1, float* d2, long long out_bstride, int out_pitch, int nH, int nW,
+                             const ShrinkParams& sp, const SdaDiv& div, int nb, cudaStream_t st);
 int launch_analysis_lift_f32(const float* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll,
                              float* d0, float* d1, float* d2, long long out_bstride, int out_pitch, int nH, int nW,
                              const ShrinkParams& sp, int nb, cudaStream_t st);

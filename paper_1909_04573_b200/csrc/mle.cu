@@ -28,7 +28,7 @@ __global__ void __launch_bounds__(256) k_accumulate(const float* __restrict__ Wr
 
 int launch_accumulate(const float* W, const float* I, int batch, long long P, double* num, double* den,
                       cudaStream_t st) {
-    long long blocks = std::min<long long>((P + 255) / 256, 148LL * 16);
+    long long blocks = std::min<long long>((P + 255) / 256, 16LL * device_sm_count());
     {
         KTimer kt("accumulate", st);
         k_accumulate<<<(unsigned)blocks, 256, 0, st>>>(W, I, batch, P, num, den);
@@ -156,7 +156,7 @@ static int run_zero_mean(Src src, int H, int W, float* out, void* ws, cudaStream
         k_zm_cols_final<<<(W + 255) / 256, 256, 0, st>>>(part, H, W, cm);
     }
     long long P = (long long)H * W;
-    long long blocks = std::min<long long>((P + 255) / 256, 148LL * 16);
+    long long blocks = std::min<long long>((P + 255) / 256, 16LL * device_sm_count());
     {
         KTimer kt("zm_apply", st);
         k_zm_apply<<<(unsigned)blocks, 256, 0, st>>>(X, rm, cm, H, W, out);
@@ -170,7 +170,7 @@ int launch_finalize(const double* num, const double* den, int H, int W, double e
     FinalizeSrc src{num, den, eps};
     if (zero_mean) return run_zero_mean(src, H, W, K, ws, st);
     long long P = (long long)H * W;
-    long long blocks = std::min<long long>((P + 255) / 256, 148LL * 16);
+    long long blocks = std::min<long long>((P + 255) / 256, 16LL * device_sm_count());
     {
         KTimer kt("finalize_plain", st);
         k_finalize_plain<<<(unsigned)blocks, 256, 0, st>>>(src, P, K);
@@ -184,7 +184,7 @@ int launch_zero_mean_f32(float* Wp, int H, int W, void* ws, cudaStream_t st) {
 }
 
 // ---------------------------------------------------------------- a7 NCC
-constexpr int NCC_BLOCKS = 296;   // 2 x 148 SMs; fixed so the sum order is fixed
+constexpr int NCC_BLOCKS = 256;   // a fixed partition (not the SM count): the same sum order on every device
 
 size_t ncc_workspace_bytes(int batch) {
     return align_up(sizeof(double) * (size_t)batch * NCC_BLOCKS * 2, 256) +

@@ -9,7 +9,7 @@
 
 namespace prnu {
 
-constexpr int PCE_BLOCKS = 148;   // partial blocks per pair (fixed => fixed sum order)
+constexpr int PCE_BLOCKS = 128;   // partial blocks per pair: a fixed partition (not the SM count) => fixed sum order
 constexpr double PCE_CAP = 1e12;
 
 struct PcePlan {
@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(256) k_pce_template(const float* __restrict__ 
 
 int launch_pce_template(const float* K, int k_batch, const uint8_t* Iq, int batch, long long P, float* T,
                         cudaStream_t st) {
-    unsigned blocks = (unsigned)std::min<long long>((P + 255) / 256, 148LL * 4);
+    unsigned blocks = (unsigned)std::min<long long>((P + 255) / 256, 4LL * device_sm_count());
     {
         KTimer kt("pce_template", st);
         k_pce_template<<<dim3(blocks, batch), 256, 0, st>>>(K, k_batch, Iq, P, T);
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(256) k_pce_final(const float* __restrict__ C, 
         e += q.e;
     }
     block_reduce_peak(best, bi, e);
-    int p = aligned ? 0 : bi;
+    int p = aligned ? 0 : max(bi, 0);   // bi < 0 only for an all-NaN surface: report position 0
     int y = p / W, x = p - (p / W) * W;
     // circular (2e+1)^2 neighbourhood, distinct positions only (first min(H,2e+1) rows/cols)
     const int nr = min(H, 2 * excl + 1), nc = min(W, 2 * excl + 1);
@@ -263,7 +263,7 @@ int run_pce(void* plan, const float* R, const float* T, int excl, int aligned, d
     if ((r = cufftExecR2C(p->r2c, const_cast<float*>(T), Tf)))
         return fail(PRNU_CUDA_ERROR, std::string("cufftExecR2C: ") + cufft_str(r));
     long long n_per = (long long)spectrum_elems(H, W);
-    unsigned blocks = (unsigned)std::min<long long>((n_per * batch + 255) / 256, 148LL * 8);
+    unsigned blocks = (unsigned)std::min<long long>((n_per * batch + 255) / 256, 8LL * device_sm_count());
     {
         KTimer kt("pce_conj_mul", st);
         k_conj_mul<<<blocks, 256, 0, st>>>(Rf, Tf, n_per, batch);
@@ -355,6 +355,10 @@ int block_plan_create(int H, int W, int block, int* n_tiles, size_t* ws_bytes, v
             k.ntx = xs[c][2];
             k.count = k.nty * k.ntx;
             if (k.count == 0 || k.h == 0 || k.w == 0) continue;
+            if (k.count > 65535) {   // the per-class launches put tiles on grid.y
+                rc = fail(PRNU_BAD_PARAMETER, "block too small: more than 65535 tiles of one size");
+                break;
+            }
             rc = pce_plan_create(k.h, k.w, k.count, &k.pce_ws, &k.plan);
             if (rc) break;
             bp->cls[bp->n_classes++] = k;

@@ -82,6 +82,92 @@ __global__ void __launch_bounds__(256) k_sda_average_scalar(const uint8_t* __res
     }
 }
 
+// SDA group sums for the fused extraction (2 <= d <= 257, R-11): the exact sum of the
+// d frames of each group as u16 (255 * 257 = 65535), rows written with a pitch of Wp
+// elements (a multiple of 8: 16-byte rows, TMA-stageable; pad columns 0).  The
+// analysis and the accumulation form S = RN(sum / d) themselves (sda_div), so the
+// fp32 SDA frame never goes through HBM: 2 B per pixel written and read instead of 4.
+// Vector path (W % 8 == 0, 8-byte aligned frames): 8 pixels per thread, packed 16-bit
+// lane sums (even / odd bytes) stored interleaved as 8 u16.
+__global__ void __launch_bounds__(256) k_sda_sum_u16_vec(const uint2* __restrict__ frames, long long P8, int d,
+                                                          uint4* __restrict__ out) {
+    const int g = blockIdx.y;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P8;
+         i += (long long)gridDim.x * blockDim.x) {
+        const uint2* src = frames + (size_t)g * d * P8 + i;
+        uint32_t pe[2] = {0, 0}, po[2] = {0, 0};
+        int j = 0;
+        for (; j + 8 <= d; j += 8) {
+            uint2 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldcs(src + (size_t)(j + u) * P8);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                pe[0] += v[u].x & 0x00ff00ffu;
+                po[0] += (v[u].x >> 8) & 0x00ff00ffu;
+                pe[1] += v[u].y & 0x00ff00ffu;
+                po[1] += (v[u].y >> 8) & 0x00ff00ffu;
+            }
+        }
+        for (; j < d; ++j) {
+            const uint2 v = __ldcs(src + (size_t)j * P8);
+            pe[0] += v.x & 0x00ff00ffu;
+            po[0] += (v.x >> 8) & 0x00ff00ffu;
+            pe[1] += v.y & 0x00ff00ffu;
+            po[1] += (v.y >> 8) & 0x00ff00ffu;
+        }
+        // pixel 4q+0 = low half of pe[q], 4q+1 = low half of po[q], 4q+2 / 4q+3 = high halves
+        out[(size_t)g * P8 + i] = make_uint4(__byte_perm(pe[0], po[0], 0x5410), __byte_perm(pe[0], po[0], 0x7632),
+                                             __byte_perm(pe[1], po[1], 0x5410), __byte_perm(pe[1], po[1], 0x7632));
+    }
+}
+
+// Generic path: one pixel per thread, any width / alignment, rows re-pitched to Wp.
+template <typename TO>
+__global__ void __launch_bounds__(256) k_sda_rows(const uint8_t* __restrict__ frames, int H, int W, int d, int Wp,
+                                                   TO* __restrict__ out) {
+    const int g = blockIdx.y;
+    const long long P = (long long)H * W, Pp = (long long)H * Wp;
+    const float fd = (float)d;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < Pp;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long y = i / Wp, x = i - y * Wp;
+        uint32_t s = 0;
+        if (x < W) {
+            const uint8_t* src = frames + (size_t)g * d * P + y * W + x;
+            for (int j = 0; j < d; ++j) s += src[(size_t)j * P];
+        }
+        if (sizeof(TO) == 2) out[(size_t)g * Pp + i] = (TO)s;                  // exact sum (d <= 257)
+        else out[(size_t)g * Pp + i] = (TO)__fdiv_rn((float)s, fd);           // RN(sum / d) (d > 257)
+    }
+}
+
+int launch_sda_sum_u16(const uint8_t* frames, long long n_groups, int H, int W, int d, uint16_t* out, int Wp,
+                       cudaStream_t st) {
+    if (n_groups <= 0) return PRNU_OK;
+    if (d < 1 || d > 257) return fail(PRNU_BAD_PARAMETER, "u16 SDA sums need 1 <= d <= 257");
+    const long long P = (long long)H * W;
+    const bool vec = Wp == W && W % 8 == 0 && ((uintptr_t)frames % 8 == 0) && ((uintptr_t)out % 16 == 0);
+    const long long cap = 8LL * device_sm_count();
+    for (long long g0 = 0; g0 < n_groups; g0 += 65535) {
+        const int ng = (int)std::min<long long>(65535, n_groups - g0);
+        KTimer kt("sda_sum", st);
+        if (vec) {
+            const long long P8 = P / 8;
+            dim3 grid((unsigned)std::min<long long>((P8 + 255) / 256, cap), ng);
+            k_sda_sum_u16_vec<<<grid, 256, 0, st>>>(reinterpret_cast<const uint2*>(frames + g0 * d * P), P8, d,
+                                                    reinterpret_cast<uint4*>(out + g0 * (long long)H * Wp));
+        } else {
+            dim3 grid((unsigned)std::min<long long>(((long long)H * Wp + 255) / 256, cap), ng);
+            k_sda_rows<uint16_t><<<grid, 256, 0, st>>>(frames + g0 * d * P, H, W, d, Wp, out + g0 * (long long)H * Wp);
+        }
+        count_launch();
+        int rc = check_launch("k_sda_sum_u16");
+        if (rc) return rc;
+    }
+    return PRNU_OK;
+}
+
 // Pitched copy of u8 frames (rows of W bytes -> rows of Wp bytes, Wp a multiple of 16)
 // so that unaligned frame widths can still be TMA-staged; one CTA per (frame, row).
 __global__ void __launch_bounds__(256) k_pad_rows_u8(const uint8_t* __restrict__ src, int H, int W,
@@ -100,6 +186,28 @@ int launch_pad_rows_u8(const uint8_t* src, long long nb, int H, int W, long long
     return check_launch("k_pad_rows_u8");
 }
 
+int launch_sda_average(const uint8_t* frames, long long n_groups, long long P, int d, float* out, cudaStream_t st);
+
+// fp32 SDA frames with rows of Wp floats (Wp >= W; the extraction uses a multiple of 4
+// so that the frames are TMA-stageable)
+int launch_sda_average_pitched(const uint8_t* frames, long long n_groups, int H, int W, int d, float* out, int Wp,
+                               cudaStream_t st) {
+    if (Wp == W) return launch_sda_average(frames, n_groups, (long long)H * W, d, out, st);
+    if (n_groups <= 0) return PRNU_OK;
+    const long long cap = 8LL * device_sm_count();
+    for (long long g0 = 0; g0 < n_groups; g0 += 65535) {
+        const int ng = (int)std::min<long long>(65535, n_groups - g0);
+        KTimer kt("sda_average", st);
+        dim3 grid((unsigned)std::min<long long>(((long long)H * Wp + 255) / 256, cap), ng);
+        k_sda_rows<float><<<grid, 256, 0, st>>>(frames + g0 * d * (long long)H * W, H, W, d, Wp,
+                                                 out + g0 * (long long)H * Wp);
+        count_launch();
+        int rc = check_launch("k_sda_average (pitched)");
+        if (rc) return rc;
+    }
+    return PRNU_OK;
+}
+
 int launch_sda_average(const uint8_t* frames, long long n_groups, long long P, int d, float* out,
                        cudaStream_t st) {
     if (n_groups <= 0) return PRNU_OK;
@@ -109,12 +217,12 @@ int launch_sda_average(const uint8_t* frames, long long n_groups, long long P, i
         KTimer kt("sda_average", st);
         if (vec) {
             long long P16 = P / SDA_VEC;
-            long long blocks = std::min<long long>((P16 + 255) / 256, 148LL * 8);
+            long long blocks = std::min<long long>((P16 + 255) / 256, 8LL * device_sm_count());
             dim3 grid((unsigned)blocks, ng);
             k_sda_average_vec<<<grid, 256, 0, st>>>(reinterpret_cast<const uint4*>(frames + g0 * d * P), P16, d,
                                                     reinterpret_cast<float4*>(out + g0 * P));
         } else {
-            long long blocks = std::min<long long>((P + 255) / 256, 148LL * 8);
+            long long blocks = std::min<long long>((P + 255) / 256, 8LL * device_sm_count());
             dim3 grid((unsigned)blocks, ng);
             k_sda_average_scalar<<<grid, 256, 0, st>>>(frames + g0 * d * P, P, d, out + g0 * P);
         }
@@ -264,7 +372,7 @@ int launch_rgb_to_luma(const uint8_t* rgb, long long n, long long P, int layout,
                        cudaStream_t st) {
     if (P % 16 == 0 && ((uintptr_t)rgb & 15) == 0 && ((uintptr_t)out & 15) == 0) {
         const long long total = n * (P / 16);
-        const int blocks = (int)std::max(1LL, std::min((total + 255) / 256, 148LL * 16));
+        const int blocks = (int)std::max(1LL, std::min((total + 255) / 256, 16LL * device_sm_count()));
         if (layout == 0 && rounding == 0) k_rgb_to_luma16<0, 0><<<blocks, 256, 0, st>>>(rgb, n, P, out);
         else if (layout == 0) k_rgb_to_luma16<0, 1><<<blocks, 256, 0, st>>>(rgb, n, P, out);
         else if (rounding == 0) k_rgb_to_luma16<1, 0><<<blocks, 256, 0, st>>>(rgb, n, P, out);
@@ -273,7 +381,7 @@ int launch_rgb_to_luma(const uint8_t* rgb, long long n, long long P, int layout,
         return check_launch("k_rgb_to_luma16");
     }
     const long long total = n * (P / 4);
-    const int blocks = (int)std::max(1LL, std::min((total + 255) / 256, 148LL * 16));
+    const int blocks = (int)std::max(1LL, std::min((total + 255) / 256, 16LL * device_sm_count()));
     if (layout == 0 && rounding == 0) k_rgb_to_luma<0, 0><<<blocks, 256, 0, st>>>(rgb, n, P, out);
     else if (layout == 0) k_rgb_to_luma<0, 1><<<blocks, 256, 0, st>>>(rgb, n, P, out);
     else if (rounding == 0) k_rgb_to_luma<1, 0><<<blocks, 256, 0, st>>>(rgb, n, P, out);

@@ -9,7 +9,7 @@
 // W = I - F(I), R-10), built from separable one-dimensional passes:
 //
 //   k_var_ana<T, MODE, AX>   one analysis pass along x (AX = 0) or y (AX = 1)
-//   launch_shrink_strip      split.cu's streaming shrink, reused unchanged
+//   launch_shrink_strip      shrink.cu's streaming shrink
 //   k_var_syn<T, MODE, AX>   one synthesis pass (gather form); a null approximation is zero
 //
 // Filter convention (GPU side; R-5 generalised to T taps): H_ is the

@@ -17,7 +17,7 @@
 
 namespace prnu {
 
-constexpr int WD_BLOCKS = 148;
+constexpr int WD_BLOCKS = 128;   // a fixed partition (not the SM count) => fixed sum order
 
 struct WdftPlan {
     int H, W, batch;
@@ -173,7 +173,7 @@ int run_wdft(void* plan, const float* K, float* K_out, void* ws, cudaStream_t st
         (r = cufftSetWorkArea(p->c2r, work)))
         return fail(PRNU_CUDA_ERROR, "cufft setup failed");
     if ((r = cufftExecR2C(p->r2c, const_cast<float*>(K), F))) return fail(PRNU_CUDA_ERROR, "cufftExecR2C failed");
-    const unsigned blocks = (unsigned)std::min<long long>((P + 255) / 256, 148LL * 8);
+    const unsigned blocks = (unsigned)std::min<long long>((P + 255) / 256, 8LL * device_sm_count());
     {
         KTimer kt("wdft_mag", st);
         k_wdft_mag<<<dim3(blocks, B), 256, 0, st>>>(F, H, W, (float)(1.0 / sqrt((double)P)), A);
