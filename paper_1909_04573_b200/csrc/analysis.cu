@@ -341,6 +341,7 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
     int src = (gc < 0 || gc >= a.nW) ? mirror(gc, a.nW) - cx0 + 4 : t;
     src = min(max(src, 0), ncols - 1);
     const int slot = 8 * (src >> 3) + 2 * (src & 3) + ((src >> 2) & 1);   // (k, k+4) adjacent
+    PRNU_DCHECK(slot >= 0 && slot < AL_RBP && ncols <= P2 && ncols <= P1 && (ncols & 7) == 0);
     const bool inner = (t >= 4) && (t < 4 + a.O) && (gc < a.nW);
     const int rr = t & 15, ga = t >> 4;
     const bool doA = ga < ngroups && cx0 - 4 + 8 * ga < a.nW;
@@ -401,6 +402,7 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
         const int k = stg_of(i);
         T* s = stg0 + k * STG;
         const int y = box_y(i);
+        PRNU_DCHECK(y >= 0 && y + AL_IR <= a.NH);
         mbar_arrive_expect_tx(&bar[k], (uint32_t)(2 * AL_IR * BW * sizeof(T)));
         tma_load_3d(s, &map, xs, y, b, &bar[k]);
         tma_load_3d(s + AL_IR * BW, &map, xs + 128, y, b, &bar[k]);
@@ -452,6 +454,7 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
             if (h == 0 ? doA : doB) {
                 float2 L[4], Hh[4];
                 al_rowpass(s, prow, g, a.div_d, a.div_r, L, Hh);
+                PRNU_DCHECK(rr < AL_IR && 8 * g + 8 <= AL_RBP && prow >= 0 && prow < AL_IR);
                 float2* dl = reinterpret_cast<float2*>(RBlo + rr * AL_RBP + 8 * g);
                 float2* dh = reinterpret_cast<float2*>(RBhi + rr * AL_RBP + 8 * g);
 #pragma unroll
@@ -491,6 +494,7 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
         const int sk = stg_of(i);
         T* s = stg0 + sk * STG;
         int prow;
+        PRNU_STRESS(1);
         if (tma_ok(i)) {
             mbar_wait(&bar[sk], (phase >> sk) & 1);
             phase ^= 1u << sk;
@@ -507,6 +511,7 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
         rowpass(s, prow, pro ? 6 : AL_IR);
         fence_proxy_async();
         __syncthreads();   // B1: row buffer complete, staging buffer s consumed
+        PRNU_STRESS(2);
         if (t == 0 && i + NSTG < nblk && tma_ok(i + NSTG)) issue(i + NSTG);
 
         // ---- column pass: (e, o) row pairs j of the block = coefficient rows m = K + j;
@@ -545,6 +550,7 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
             float2 o2, e3;
             lift_y(j, o2, e3);
             const float llv = LF_KA2 * o2.x;
+            PRNU_DCHECK(!(llmask & (1u << j)) || (K + j >= 0 && K + j < a.nH && gc >= 0 && gc < a.nW));
             if (llmask & (1u << j)) *llp = llv;
             llp += a.out_pitch;
             cn[j] = o2.y;                  // da
@@ -600,6 +606,7 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
                 }
             }
             __syncthreads();   // B2: every thread is done reading the row buffer (overlaps the da planes)
+            PRNU_STRESS(3);
             if (t < ncols) {
 #pragma unroll
                 for (int j = 0; j < AL_BK; ++j) {
@@ -615,7 +622,10 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
                 }
             }
             __syncthreads();   // B3: V/c of all three subbands ready
+            PRNU_STRESS(4);
             if (hv && K - 4 + hj < ky1) {
+                PRNU_DCHECK(K - 4 + hj >= 0 && K - 4 + hj < a.nH && hx < a.nW && 8 * hg + 16 <= P2 &&
+                            (!hfull || hx + 8 <= a.out_pitch));
                 const size_t roff = dst_off + (size_t)(K - 4 + hj) * a.out_pitch;
                 // ---- da: region columns 8hg .. 8hg+15 of row hj
                 {
@@ -795,6 +805,7 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
             }
         }
         __syncthreads();   // B4: V buffers and the row buffer free for the next block
+        PRNU_STRESS(5);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             qd_c[k] = qd[8 + k];

@@ -897,6 +897,15 @@ const char* prnu_last_error(void) { return t_err.c_str(); }
 
 uint64_t prnu_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
-const char* prnu_version(void) { return "prnu-b200 0.1.0 (sm_100a)"; }
+const char* prnu_version(void) {
+    return "prnu-b200 0.2.0 (sm_100a)"
+#ifdef PRNU_DEBUG
+           " +debug"
+#endif
+#ifdef PRNU_RACE_STRESS
+           " +race-stress"
+#endif
+        ;
+}
 
 }  // extern "C"

@@ -29,6 +29,27 @@
     } while (0)
 #endif
 
+// Race stress (debug builds: PRNU_NVCC_DEFS=PRNU_RACE_STRESS): at the phase boundaries
+// of the shared-memory kernels a pseudo-random quarter of the warps sleeps up to ~4 us,
+// reshuffling the interleaving of warps; a missing barrier or mbarrier wait then changes
+// the results, which tools/gpu_race_stress.sh compares bit for bit with the release
+// build (compute-sanitizer is not available on the GPU pool).
+#ifdef PRNU_RACE_STRESS
+__device__ __forceinline__ void prnu_race_stress(uint32_t tag) {
+    uint32_t h = (blockIdx.x * 73856093u) ^ (blockIdx.y * 19349663u) ^ (blockIdx.z * 83492791u) ^
+                 ((threadIdx.x >> 5) * 2654435761u) ^ (tag * 40503u);
+    h ^= h >> 13;
+    h *= 0x5bd1e995u;
+    h ^= h >> 15;
+    if ((h & 3u) == 0u) __nanosleep(64u + (h >> 20) % 4096u);
+}
+#define PRNU_STRESS(tag) prnu_race_stress(tag)
+#else
+#define PRNU_STRESS(tag) \
+    do {                 \
+    } while (0)
+#endif
+
 namespace prnu {
 
 // ---------------------------------------------------------------- errors

@@ -123,7 +123,8 @@ __global__ void __launch_bounds__(NT, 4) k_shrink_hfirst(ShrinkArgs a) {
             pf[k] = pf2[k];
         }
         if (i + 2 < nblk) load_block(i + 2, pf2);
-        __syncthreads();   // squares of rows K .. K+7 visible (the other plane is free)
+        __syncthreads();
+        PRNU_STRESS(21);   // squares of rows K .. K+7 visible (the other plane is free)
         if (!outc) continue;
         // nested horizontal sums of this column, rows K .. K+7 -> ring slots 8 .. 15
 #pragma unroll

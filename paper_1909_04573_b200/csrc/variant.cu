@@ -300,7 +300,8 @@ __global__ void __launch_bounds__(128) k_var_row_ana(VarPass p) {
     const int base = MODE == VM_SWT ? t0 - p.s * (T - 1) : 2 * t0 - (T - 2);
     for (int y = y0; y < y1; ++y) {
         const float* row = in + (size_t)y * p.in_pitch;
-        __syncthreads();   // the previous row's staging is consumed
+        __syncthreads();
+    PRNU_STRESS(31);   // the previous row's staging is consumed
         for (int j = tid; j < nst; j += 128) {
             if (MODE == VM_SWT) {
                 sE[j] = __ldg(row + var_map<MODE>(base + j, p.N, p.Np));
@@ -310,6 +311,7 @@ __global__ void __launch_bounds__(128) k_var_row_ana(VarPass p) {
             }
         }
         __syncthreads();
+    PRNU_STRESS(31);
         float* lrow = lo + (size_t)y * p.out_pitch;
         float* hrow = hi + (size_t)y * p.out_pitch;
 #pragma unroll
@@ -353,6 +355,7 @@ __global__ void __launch_bounds__(128) k_var_row_syn(VarPass p) {
         const float* arow = A ? A + (size_t)y * p.in_pitch : nullptr;
         const float* drow = D + (size_t)y * p.in_pitch;
         __syncthreads();
+    PRNU_STRESS(31);
         for (int j = tid; j < nst; j += 128) {
             int k = MODE == VM_SWT ? t0 + j : t0 / 2 + j;
             bool ok = true;
@@ -362,6 +365,7 @@ __global__ void __launch_bounds__(128) k_var_row_syn(VarPass p) {
             sD[j] = ok ? __ldg(drow + k) : 0.f;
         }
         __syncthreads();
+    PRNU_STRESS(31);
         float* orow = out + (size_t)y * p.out_pitch;
 #pragma unroll
         for (int q = 0; q < VR_OUT / 128; ++q) {

@@ -163,6 +163,7 @@ __global__ void __launch_bounds__(256, 4) k_synth_acc2(const __grid_constant__ S
 
     for (int f = 0; f < nb; ++f) {
         const int st = f & 1;
+        PRNU_STRESS(11);
         mbar_wait(&bar[st], (f >> 1) & 1);
         const float* c = coef0 + st * SA_STAGE_COEF;
         float* sLo = sL0 + (f & 1) * 2 * TY * SA_LP;
@@ -200,6 +201,7 @@ __global__ void __launch_bounds__(256, 4) k_synth_acc2(const __grid_constant__ S
             }
         }
         __syncthreads();   // L/H planes of frame f complete; every thread is past frame f-1
+        PRNU_STRESS(12);
         if (tid == 0 && f + 2 < nb) {
             fence_proxy_async();
             issue(f + 2);   // coefficient stage of frame f, I stage of frame f-1: both consumed
@@ -274,6 +276,7 @@ __global__ void __launch_bounds__(256, 4) k_synth_acc2(const __grid_constant__ S
             }
         }
     }
+    PRNU_DCHECK(!rowok || (gy >= 0 && gy < a.NH));
     if (MODE && rowok) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
