@@ -106,3 +106,101 @@ def extract_fingerprint_chunked(frames: np.ndarray, depth: int, workers: int | N
         den += pd
     assert sum(p[2] for p in parts) == ns
     return oracle.finalize(num, den), num, den, ns
+
+
+# ---------------------------------------------------------------- worker pool for large parity tests
+def _fp_job(args):
+    import oracle
+    name, shape, depth = args
+    shm = shared_memory.SharedMemory(name=name)
+    try:
+        fr = np.ndarray(shape, dtype=np.uint8, buffer=shm.buf)
+        K, num, den, ns = oracle.extract_fingerprint(fr, depth)
+        return K, den, ns
+    finally:
+        shm.close()
+
+
+def _res_job(args):
+    import oracle
+    name, shape = args
+    shm = shared_memory.SharedMemory(name=name)
+    try:
+        q = np.ndarray(shape, dtype=np.uint8, buffer=shm.buf)
+        return oracle.residual(q.astype(np.float32), zero_mean=True)
+    finally:
+        shm.close()
+
+
+def _pce_job(args):
+    from oracle import match
+    R, T = args
+    C = match.correlation_surface(R, T)
+    p, peak, _ = match.pce_from_surface(C)
+    top = np.sort(np.abs(C).ravel())[-2:]
+    gap = float((top[1] - top[0]) / top[1])
+    return p, peak, gap, (C if gap < 1e-4 else None)   # the surface only for a near-tie (R-19)
+
+
+class OraclePool:
+    """A pool of worker processes (one per host core) running oracle functions on
+    arrays handed over through shared memory: fingerprints of many videos and
+    residual / PCE evaluations for the full-size camera-ID parity test.  At most
+    `max_pending` inputs are held at once (bounded host memory)."""
+
+    def __init__(self, workers: int | None = None, max_pending: int | None = None):
+        self.workers = workers or os.cpu_count() or 1
+        self.max_pending = max_pending or 2 * self.workers
+        self.pool = mp.get_context("spawn").Pool(self.workers)
+        self.pending = []   # (async result, shm)
+
+    def _share(self, a: np.ndarray):
+        a = np.ascontiguousarray(a)
+        shm = shared_memory.SharedMemory(create=True, size=max(1, a.nbytes))
+        np.ndarray(a.shape, dtype=a.dtype, buffer=shm.buf)[:] = a
+        return shm
+
+    def _throttle(self):
+        while len([p for p in self.pending if not p[0].ready()]) >= self.max_pending:
+            self.pending[0][0].wait(0.05)
+            self._reap()
+
+    def _reap(self):
+        for p in self.pending:
+            if p[0].ready() and p[1] is not None:
+                p[1].close()
+                p[1].unlink()
+                p[1] = None
+
+    def fingerprint(self, frames: np.ndarray, depth: int):
+        """oracle.extract_fingerprint(frames, depth) -> async (K, den, n_s)."""
+        self._throttle()
+        shm = self._share(frames)
+        r = self.pool.apply_async(_fp_job, ((shm.name, frames.shape, depth),))
+        self.pending.append([r, shm])
+        return r
+
+    def residual(self, frame: np.ndarray):
+        """oracle.residual(frame, zero_mean=True) of a u8 frame -> async fp64 plane."""
+        self._throttle()
+        shm = self._share(frame)
+        r = self.pool.apply_async(_res_job, ((shm.name, frame.shape),))
+        self.pending.append([r, shm])
+        return r
+
+    def pce(self, R: np.ndarray, T: np.ndarray):
+        """oracle PCE of (R, T) -> async (pce, peak, top-2 relative gap, surface)."""
+        return self.pool.apply_async(_pce_job, ((R, T),))
+
+    def close(self):
+        for p in self.pending:
+            p[0].wait()
+        self._reap()
+        self.pool.close()
+        self.pool.join()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()

@@ -77,6 +77,9 @@ struct AlCfg<uint8_t> {
     static constexpr int P2 = 122;     // (ad, dd) planes pitch (float2; 2 P2 == 20 mod 32)
     static constexpr int NSTG = 3;     // staging buffers (TMA two blocks ahead)
     static constexpr int BOXW = 144;   // staged bytes per row and box
+    // SPLITV = true (one V buffer used by (ad, dd) then da: 52.9 KB, 4 CTAs/SM at 128 registers)
+    // measured 8% slower at FHD (11.26 vs 10.46 ms/step): the L1 data pipe, not latency, binds
+    static constexpr bool SPLITV = false;
     static constexpr int MINB = 3;
 };
 template <>
@@ -86,6 +89,7 @@ struct AlCfg<uint16_t> {   // exact SDA group sums (level 1 at 2 <= d <= 257)
     static constexpr int P2 = 122;
     static constexpr int NSTG = 1;
     static constexpr int BOXW = 152;   // elements (304 B = 76 words == 12 mod 32)
+    static constexpr bool SPLITV = false;
     static constexpr int MINB = 3;
 };
 template <>
@@ -95,6 +99,7 @@ struct AlCfg<float> {
     static constexpr int P2 = 114;     // 2 P2 == 4 mod 32
     static constexpr int NSTG = 1;
     static constexpr int BOXW = 140;   // floats (12 mod 32 words)
+    static constexpr bool SPLITV = false;
     static constexpr int MINB = 3;
 };
 template <typename T>
@@ -105,16 +110,24 @@ template <typename T>
 __host__ __device__ constexpr int al_da_floats() { return 5 * AL_BK * AlCfg<T>::P1; }
 template <typename T>
 __host__ __device__ constexpr int al_pr_floats() { return 2 * 5 * AL_BK * AlCfg<T>::P2; }
+// V buffer: da and (ad, dd) planes side by side, or (SPLITV) one buffer used by both in turn;
+// the row buffer (2 x 16 x AL_RBP floats) lives at its start
+template <typename T>
+__host__ __device__ constexpr int al_v_floats() {
+    return AlCfg<T>::SPLITV ? (al_pr_floats<T>() > al_da_floats<T>() ? al_pr_floats<T>() : al_da_floats<T>())
+                            : al_da_floats<T>() + al_pr_floats<T>();
+}
 template <typename T>
 constexpr size_t al_smem_bytes() {
-    return AlCfg<T>::NSTG * al_stage_elems<T>() * sizeof(T) + sizeof(float) * (al_da_floats<T>() + al_pr_floats<T>()) +
-           32;
+    return AlCfg<T>::NSTG * al_stage_elems<T>() * sizeof(T) + sizeof(float) * al_v_floats<T>() + 32;
 }
 static_assert(2 * AL_IR * AL_RBP <= 5 * AL_BK * AlCfg<float>::P1, "row buffer inside the da planes");
 static_assert(AlCfg<uint8_t>::OMAX + 8 <= AlCfg<uint8_t>::P2 && AlCfg<float>::OMAX + 8 <= AlCfg<float>::P2, "V planes");
-static_assert(al_smem_bytes<uint8_t>() <= 75 * 1024 && al_smem_bytes<uint16_t>() <= 75 * 1024 &&
-                  al_smem_bytes<float>() <= 75 * 1024,
-              "3 CTAs per SM");
+template <typename T>
+constexpr bool al_fits() {   // MINB CTAs per SM in 228 KB (1 KB reserved per CTA)
+    return AlCfg<T>::MINB * (al_smem_bytes<T>() + 1024) <= 228 * 1024;
+}
+static_assert(al_fits<uint8_t>() && al_fits<uint16_t>() && al_fits<float>(), "CTAs per SM");
 
 struct AlArgs {
     const void* in;
@@ -316,11 +329,13 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
     constexpr int LOGW = al_logw<T>();
     constexpr int STG = al_stage_elems<T>();
     constexpr int NSTG = AlCfg<T>::NSTG, P1 = AlCfg<T>::P1, P2 = AlCfg<T>::P2;
+    constexpr bool SPLITV = AlCfg<T>::SPLITV;
     extern __shared__ __align__(128) unsigned char smem[];
     T* stg0 = reinterpret_cast<T*>(smem);
-    float* DA = reinterpret_cast<float*>(smem + NSTG * STG * sizeof(T));   // da planes v3 v5 v7 v9 c [8][P1]; row buffer
-    float2* PR = reinterpret_cast<float2*>(DA + al_da_floats<T>());        // (ad, dd) planes [8][P2]
-    uint64_t* bar = reinterpret_cast<uint64_t*>(PR + 5 * AL_BK * P2);
+    float* V0 = reinterpret_cast<float*>(smem + NSTG * STG * sizeof(T));
+    float* DA = V0;                                                         // da planes v3 v5 v7 v9 c [8][P1]; row buffer
+    float2* PR = reinterpret_cast<float2*>(SPLITV ? V0 : V0 + al_da_floats<T>());   // (ad, dd) planes [8][P2]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(V0 + al_v_floats<T>());
     float* RBlo = DA;                    // row buffer: lo [16][AL_RBP], hi [16][AL_RBP] (overlaps the da planes)
     float* RBhi = DA + AL_IR * AL_RBP;
 
@@ -590,43 +605,46 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
             cp[j] = j < 4 ? cp_c[j] : cpn[j - 4];
         }
         if (i > 0) {
-            // output rows K-4 .. K+3: nested vertical sums over ring rows j .. j+8
-            if (t < ncols) {
+            // output rows K-4 .. K+3: nested vertical sums over ring rows j .. j+8 -> V planes,
+            // then the H pass.  SPLITV (4 CTAs/SM configurations): the (ad, dd) and the da planes
+            // share one buffer, written and consumed one after the other.
+            const bool hon = hv && K - 4 + hj < ky1;
+            PRNU_DCHECK(!hon || (K - 4 + hj >= 0 && K - 4 + hj < a.nH && hx < a.nW && 8 * hg + 16 <= P2 &&
+                                 (!hfull || hx + 8 <= a.out_pitch)));
+            const size_t roff = dst_off + (size_t)(K - 4 + hj) * a.out_pitch;
+            auto write_pair = [&]() {
+                if (t < ncols) {
 #pragma unroll
-                for (int j = 0; j < AL_BK; ++j) {
-                    const float2 v3 = add2(add2(qp[j + 3], qp[j + 4]), qp[j + 5]);
-                    const float2 v5 = add2(v3, add2(qp[j + 2], qp[j + 6]));
-                    const float2 v7 = add2(v5, add2(qp[j + 1], qp[j + 7]));
-                    const float2 v9 = add2(v7, add2(qp[j], qp[j + 8]));
-                    PR[(0 * AL_BK + j) * P2 + t] = v3;
-                    PR[(1 * AL_BK + j) * P2 + t] = v5;
-                    PR[(2 * AL_BK + j) * P2 + t] = v7;
-                    PR[(3 * AL_BK + j) * P2 + t] = v9;
-                    PR[(4 * AL_BK + j) * P2 + t] = cp[j];
+                    for (int j = 0; j < AL_BK; ++j) {
+                        const float2 v3 = add2(add2(qp[j + 3], qp[j + 4]), qp[j + 5]);
+                        const float2 v5 = add2(v3, add2(qp[j + 2], qp[j + 6]));
+                        const float2 v7 = add2(v5, add2(qp[j + 1], qp[j + 7]));
+                        const float2 v9 = add2(v7, add2(qp[j], qp[j + 8]));
+                        PR[(0 * AL_BK + j) * P2 + t] = v3;
+                        PR[(1 * AL_BK + j) * P2 + t] = v5;
+                        PR[(2 * AL_BK + j) * P2 + t] = v7;
+                        PR[(3 * AL_BK + j) * P2 + t] = v9;
+                        PR[(4 * AL_BK + j) * P2 + t] = cp[j];
+                    }
                 }
-            }
-            __syncthreads();   // B2: every thread is done reading the row buffer (overlaps the da planes)
-            PRNU_STRESS(3);
-            if (t < ncols) {
+            };
+            auto write_da = [&]() {
+                if (t < ncols) {
 #pragma unroll
-                for (int j = 0; j < AL_BK; ++j) {
-                    const float v3 = qd[j + 3] + qd[j + 4] + qd[j + 5];
-                    const float v5 = v3 + qd[j + 2] + qd[j + 6];
-                    const float v7 = v5 + qd[j + 1] + qd[j + 7];
-                    const float v9 = v7 + qd[j] + qd[j + 8];
-                    DA[(0 * AL_BK + j) * P1 + t] = v3;
-                    DA[(1 * AL_BK + j) * P1 + t] = v5;
-                    DA[(2 * AL_BK + j) * P1 + t] = v7;
-                    DA[(3 * AL_BK + j) * P1 + t] = v9;
-                    DA[(4 * AL_BK + j) * P1 + t] = cd[j];
+                    for (int j = 0; j < AL_BK; ++j) {
+                        const float v3 = qd[j + 3] + qd[j + 4] + qd[j + 5];
+                        const float v5 = v3 + qd[j + 2] + qd[j + 6];
+                        const float v7 = v5 + qd[j + 1] + qd[j + 7];
+                        const float v9 = v7 + qd[j] + qd[j + 8];
+                        DA[(0 * AL_BK + j) * P1 + t] = v3;
+                        DA[(1 * AL_BK + j) * P1 + t] = v5;
+                        DA[(2 * AL_BK + j) * P1 + t] = v7;
+                        DA[(3 * AL_BK + j) * P1 + t] = v9;
+                        DA[(4 * AL_BK + j) * P1 + t] = cd[j];
+                    }
                 }
-            }
-            __syncthreads();   // B3: V/c of all three subbands ready
-            PRNU_STRESS(4);
-            if (hv && K - 4 + hj < ky1) {
-                PRNU_DCHECK(K - 4 + hj >= 0 && K - 4 + hj < a.nH && hx < a.nW && 8 * hg + 16 <= P2 &&
-                            (!hfull || hx + 8 <= a.out_pitch));
-                const size_t roff = dst_off + (size_t)(K - 4 + hj) * a.out_pitch;
+            };
+            auto h_da = [&]() {
                 // ---- da: region columns 8hg .. 8hg+15 of row hj
                 {
                     const float* base = DA + hj * P1 + 8 * hg;
@@ -703,6 +721,8 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
                             if (hx + x < a.nW) drow[x] = o[x];
                     }
                 }
+            };
+            auto h_pair = [&]() {
                 // ---- (ad, dd): float2 region columns 8hg .. 8hg+15 of row hj
                 {
                     const float2* base = PR + hj * P2 + 8 * hg;
@@ -801,6 +821,31 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
                                 drow[x] = od[x];
                             }
                     }
+                }
+            };
+            if (SPLITV) {
+                __syncthreads();   // B2: every thread is done reading the row buffer (inside the V buffer)
+                PRNU_STRESS(3);
+                write_pair();
+                __syncthreads();   // B3: (ad, dd) V/c ready
+                PRNU_STRESS(4);
+                if (hon) h_pair();
+                __syncthreads();   // B3b: (ad, dd) planes consumed
+                PRNU_STRESS(6);
+                write_da();
+                __syncthreads();   // B3c: da V/c ready
+                PRNU_STRESS(7);
+                if (hon) h_da();
+            } else {
+                write_pair();      // (the (ad, dd) planes do not overlap the row buffer)
+                __syncthreads();   // B2: every thread is done reading the row buffer (overlaps the da planes)
+                PRNU_STRESS(3);
+                write_da();
+                __syncthreads();   // B3: V/c of all three subbands ready
+                PRNU_STRESS(4);
+                if (hon) {
+                    h_da();
+                    h_pair();
                 }
             }
         }

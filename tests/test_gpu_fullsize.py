@@ -149,43 +149,64 @@ def test_c3_stills_sampled(prnu):
         assert prnu.extract_fingerprint(Y, d, batch=BENCH_BATCH if d == 1 else 20).n_sda == 200 // d
 
 
-def test_c4_camera_id_sampled(prnu):
+def test_c4_camera_id_full(prnu):
     """Config 4: 64 cameras x 300 frames 1280x720, depth 30, 64 query residuals
-    against 64 fingerprints (4096 PCEs).  Diagonal > 60 > off-diagonal
-    (directional); sampled entries against the oracle."""
+    against 64 fingerprints (4096 PCEs).  Against the oracle (worker processes on
+    every host core): all 64 fingerprints (R-14, sum_I2 bit-exact), all 64 query
+    residuals, and a full column and row of the PCE matrix (query q vs camera 0,
+    query 0 vs camera c: 127 pairs; R-19 tie rule).  Directional: diagonal > 60,
+    off-diagonal FPR < 1%."""
+    from oracle import parallel
     H, W, n = 720, 1280, 64
-    Ks, queries, cams = [], [], {}
-    for c in range(n):
-        v = synth.video("drift", 301, H, W, seed=4, camera=c, device="cuda")
-        Ks.append(prnu.extract_fingerprint(v.frames[:300], 30, batch=10).K.clone())
-        queries.append(v.frames[300])
-        if c < 2:
-            cams[c] = v.frames.cpu().numpy()
-    Iq = torch.stack(queries)
-    R = prnu.residual(Iq, zero_mean=True)
-    plan = prnu.PcePlan(H, W, n)
-    M = np.zeros((n, n))
-    PY = np.zeros((n, n), dtype=np.int64)
-    PX = np.zeros((n, n), dtype=np.int64)
-    for c in range(n):
-        res = plan(R, prnu.pce_template(Ks[c], Iq))
-        M[:, c] = res.pce.cpu().numpy()
-        PY[:, c] = res.peak_y.cpu().numpy()
-        PX[:, c] = res.peak_x.cpu().numpy()
+    Ks, queries = [], []
+    with parallel.OraclePool() as pool:
+        fps, dens = [], []
+        for c in range(n):
+            v = synth.video("drift", 301, H, W, seed=4, camera=c, device="cuda")
+            fp = prnu.extract_fingerprint(v.frames[:300], 30, batch=10)
+            Ks.append(fp.K.clone())
+            dens.append(fp.sum_I2.cpu().numpy())
+            queries.append(v.frames[300].clone())
+            fps.append(pool.fingerprint(v.frames[:300].cpu().numpy(), 30))
+        Iq = torch.stack(queries)
+        R = prnu.residual(Iq, zero_mean=True)
+        qn = Iq.cpu().numpy()
+        rres = [pool.residual(qn[q]) for q in range(n)]
+        K_ref = []
+        for c in range(n):
+            Kr, den, ns = fps[c].get()
+            assert ns == 10
+            np.testing.assert_array_equal(dens[c], den)
+            assert k_metric(Ks[c].cpu().numpy(), Kr, den, ns) <= K_TOL, c
+            K_ref.append(Kr)
+        R_ref = [r.get() for r in rres]
+        Rg = R.cpu().numpy()
+        for q in range(n):
+            assert np.abs(Rg[q] - R_ref[q]).max() <= W_TOL, q
+        plan = prnu.PcePlan(H, W, n)
+        plan.set_residual(R)
+        M = np.zeros((n, n))
+        PY = np.zeros((n, n), dtype=np.int64)
+        PX = np.zeros((n, n), dtype=np.int64)
+        for c in range(n):
+            res = plan.match(prnu.pce_template(Ks[c], Iq))
+            M[:, c] = res.pce.cpu().numpy()
+            PY[:, c] = res.peak_y.cpu().numpy()
+            PX[:, c] = res.peak_x.cpu().numpy()
+        pairs = [(q, 0) for q in range(n)] + [(0, c) for c in range(1, n)]
+        jobs = [pool.pce(R_ref[q], oracle.pce_template(K_ref[c], qn[q])) for q, c in pairs]
+        worst = 0.0
+        for (q, c), j in zip(pairs, jobs):
+            p_ref, peak_ref, gap, C = j.get()
+            gpk = (int(PY[q, c]), int(PX[q, c]))
+            if gpk != peak_ref:
+                assert gap < 1e-4, (q, c, gpk, peak_ref)
+                p_ref = oracle.match.pce_from_surface(C, peak=gpk)[0]
+            rel = abs(M[q, c] - p_ref) / (abs(p_ref) + 1e-3)
+            worst = max(worst, rel)
+            assert abs(M[q, c] - p_ref) <= PCE_RTOL * abs(p_ref) + 1e-3, (q, c, M[q, c], p_ref)
+    print(f"\nC4: 64 fingerprints, 64 residuals and {len(pairs)} PCE pairs vs the oracle; "
+          f"worst PCE relative difference {worst:.2e}")
     off = M[~np.eye(n, dtype=bool)]
     assert np.all(np.diag(M) > 60)
     assert np.mean(off > 60) < 0.01
-    # oracle on sampled pairs: cameras 0 and 1 against queries 0, 1, 2 (R-19 tie rule)
-    for c in (0, 1):
-        K_ref, _, _, _ = oracle.extract_fingerprint(cams[c][:300], 30)
-        for q in (0, 1, 2):
-            qn = queries[q].cpu().numpy()
-            C = oracle.correlation_surface(oracle.residual(qn.astype(np.float32), zero_mean=True),
-                                           oracle.pce_template(K_ref, qn))
-            p_ref, peak_ref, _ = oracle.match.pce_from_surface(C)
-            gpk = (int(PY[q, c]), int(PX[q, c]))
-            if gpk != peak_ref:
-                top = np.sort(np.abs(C).ravel())[-2:]
-                assert (top[1] - top[0]) / top[1] < 1e-4, (q, c, gpk, peak_ref)
-                p_ref = oracle.match.pce_from_surface(C, peak=gpk)[0]
-            assert abs(M[q, c] - p_ref) <= PCE_RTOL * abs(p_ref) + 1e-3, (q, c, M[q, c], p_ref)

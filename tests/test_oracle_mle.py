@@ -159,3 +159,23 @@ def test_extract_fingerprint_chunked_matches():
         np.testing.assert_allclose(num2, num, rtol=1e-13, atol=1e-12)
         np.testing.assert_allclose(den2, den, rtol=1e-14)
         np.testing.assert_allclose(K2, K, rtol=1e-10, atol=1e-14)
+
+
+def test_oracle_pool_matches_direct_calls():
+    """oracle.parallel.OraclePool (worker processes + shared memory) returns what the
+    oracle returns when called directly."""
+    from oracle import parallel
+    v = synth.video("shift", 8, 24, 32, seed=12)
+    fr = v.frames.numpy()
+    with parallel.OraclePool(workers=2) as pool:
+        f = pool.fingerprint(fr, 4)
+        r = pool.residual(fr[0])
+        K, _, den, ns = oracle.extract_fingerprint(fr, 4)
+        Kp, denp, nsp = f.get()
+        assert nsp == ns and np.array_equal(Kp, K) and np.array_equal(denp, den)
+        R = oracle.residual(fr[0].astype(np.float32), zero_mean=True)
+        assert np.array_equal(r.get(), R)
+        T = oracle.pce_template(K, fr[1])
+        p, peak, gap, _ = pool.pce(R, T).get()
+        p_ref, peak_ref, _ = oracle.pce(R, T)
+        assert p == p_ref and peak == peak_ref
