@@ -59,9 +59,9 @@ namespace prnu {
 #define LF_C5 0.31909219261386207f
 #define LF_KA 2.6337752658977225f
 #define LF_KD 0.3796831160760221f
-#define LF_KA2 6.936772143131393f      // KA^2
-#define LF_KD2 0.14415926620330932f    // KD^2
-#define LF_KD4 0.020781894001587787f   // KD^4
+#define LF_KA2 6.936772151254619f      // KA^2
+#define LF_KD2 0.14415926863319808f    // KD^2
+#define LF_KD4 0.02078189473285857f    // KD^4
 
 constexpr int AL_NT = 128;   // threads per CTA == region columns
 constexpr int AL_BK = 8;     // coefficient rows per block

@@ -1,10 +1,15 @@
 """The C-ABI library loads and exports every symbol include/prnu.h declares;
 host-side validation and workspace queries work without a GPU (no compute)."""
 import ctypes
+import os
+
+import numpy as np
 
 import pytest
 
 import paper_1909_04573_b200 as prnu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def test_library_exports_every_header_symbol():
@@ -91,3 +96,40 @@ def test_variant_validation_host():
         vv = prnu.DenoiseVariant(*v).c()
         n = prnu._lib.prnu_residual_variant_workspace_bytes(2, 64, 96, ctypes.byref(p), ctypes.byref(vv))
         assert (n > 0) == ok, v
+
+
+def test_lifting_constants_reproduce_the_filter():
+    """R-27: the lifting constants compiled into analysis.cu (LF_*) are those of the
+    factorisation in tools/lifting.py (to fp32 precision) and, used in fp64, the
+    cascade reproduces R-2's direct analysis filter pair to rounding."""
+    import importlib.util
+    import re
+    src = open(os.path.join(ROOT, "paper_1909_04573_b200", "csrc", "analysis.cu")).read()
+    lf = {m.group(1): float(m.group(2)) for m in re.finditer(r"#define (LF_\w+) ([-0-9.e]+)f", src)}
+    spec = importlib.util.spec_from_file_location("lifting", os.path.join(ROOT, "tools", "lifting.py"))
+    L = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(L)
+    M, steps = L.factor()
+    q1, q2, q3, q4 = [s_[2] for s_ in steps]
+    KA, KD = M[0][1][1][0], M[1][0][1][0]
+    want = {"LF_C1": q1[1][0], "LF_C2A": -q2[1][0], "LF_C2B": q2[1][1], "LF_C3A": -q3[1][0], "LF_C3B": q3[1][1],
+            "LF_C4A": -q4[1][0], "LF_C4B": -q4[1][1], "LF_C5": -M[1][1][1][0] / KD, "LF_KA": KA, "LF_KD": KD,
+            "LF_KA2": KA * KA, "LF_KD2": KD * KD, "LF_KD4": KD ** 4}
+    for k, v in want.items():
+        assert np.float32(lf[k]) == np.float32(v), (k, lf[k], v)
+    x = np.random.default_rng(3).uniform(0, 255, 256)
+    c = [lf[k] for k in ("LF_C1", "LF_C2A", "LF_C2B", "LF_C3A", "LF_C3B", "LF_C4A", "LF_C4B", "LF_C5", "LF_KA",
+                         "LF_KD")]
+    assert np.abs(L.lift(x, *c, np.float64) - L.direct(x, np.float64)).max() < 1e-11
+
+
+def test_sda_division_sequence_exact():
+    """R-28: q = RN(q0 + RN(s - q0 d) r), q0 = RN(s r), r = RN(1/d) equals the correctly
+    rounded fp32 quotient s/d for every integer s <= 255 d (a subset of depths here;
+    tools/sda_div_check.py runs every d <= 257 and the config depths)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("sda_div_check", os.path.join(ROOT, "tools", "sda_div_check.py"))
+    D = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(D)
+    for d in (2, 3, 5, 7, 10, 25, 30, 50, 100, 255, 256, 257):
+        assert D.check(d) == 0, d

@@ -10,9 +10,11 @@ python tools/launch_summary.py $O/ncu_launches.csv > $O/ncu_launches_summary.txt
 gzip -f $O/ncu_launches.csv
 python tools/profile_extract.py 64 64 > /dev/null 2>&1
 timeout 1200 ncu --set full --clock-control none --import-source on \
-  -k "regex:k_analysis_strip|k_synth_acc2|k_analysis_shrink|k_synth_tma|k_dwt_strip|k_shrink_hfirst" -c 9 -f -o $O/full \
+  -k "regex:k_analysis_lift|k_synth_acc2|k_sda_sum" -c 9 -f -o $O/full \
   python tools/profile_extract.py 64 64 > $O/ncu_full_run.log 2>&1; echo "ncu full rc $?"
 python tools/ncu_summary.py $O/full.ncu-rep > $O/ncu_full_summary.txt
-python tools/ncu_traffic.py $O/full.ncu-rep "k_analysis_strip<unsigned char" analysis_l1_u8 64 1080 1920 \
-  "profiles/r01/full.ncu-rep launch 0: k_analysis_strip<u8> (analysis_l1_u8), FHD, 64 frames per launch" > $O/traffic.json
+python tools/ncu_traffic.py $O/full.ncu-rep "k_analysis_lift<unsigned char" analysis_l1_u8 64 1080 1920 \
+  "profiles/r02/full.ncu-rep: k_analysis_lift<u8> (analysis_l1_u8), FHD, 64 frames per launch" > $O/traffic.json
+python tools/ncu_opmix.py $O/full.ncu-rep "k_analysis_lift<unsigned char" 33466176 > $O/ncu_opmix_analysis_l1.txt
+python tools/ncu_lines.py $O/full.ncu-rep "k_analysis_lift<unsigned char" 40 > $O/ncu_lines_analysis_l1.txt
 echo done

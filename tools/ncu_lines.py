@@ -23,6 +23,8 @@ for r in rows:
         fname = r[1].split("/")[-1]
         continue
     if len(r) > 3 and r[0] == "Line No":
+        if hdr is not None and T > 0 and len(sys.argv) > 4:
+            break
         hdr = r
         continue
     if hdr is None or len(r) != len(hdr):

@@ -19,7 +19,12 @@ out = subprocess.run(cmd, capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = next(r for r in rows if "Source" in r and "Instructions Executed" in r)
 i0 = rows.index(hdr)
-data = [r for r in rows[i0 + 1:] if len(r) == len(hdr)]
+data = []
+for r in rows[i0 + 1:]:   # the first kernel's section only (a report can hold several)
+    if len(r) == len(hdr) and r[0] == hdr[0]:
+        break
+    if len(r) == len(hdr):
+        data.append(r)
 iS, iE = hdr.index("Source"), hdr.index("Instructions Executed")
 iW, iSm = hdr.index("L1 Wavefronts Shared"), hdr.index("Warp Stall Sampling (All Samples)")
 tot, wf, st = collections.Counter(), collections.Counter(), collections.Counter()
@@ -30,11 +35,11 @@ for r in data:
         continue
     op = m.group(2)
     key = op + (m.group(3) or "") if op in ("LDS", "STS", "LDG", "STG") else op
-    n = int(r[iE] or 0)
+    n = int(r[iE]) if r[iE].isdigit() else 0
     T += n
     tot[key] += n
-    wf[key] += int(r[iW] or 0)
-    st[key] += int(r[iSm] or 0)
+    wf[key] += int(r[iW]) if r[iW].isdigit() else 0
+    st[key] += int(r[iSm]) if r[iSm].isdigit() else 0
 print(f"total warp-instructions {T}" + (f"  per position (thread-instr) {T * 32 / npos:.1f}" if npos else ""))
 for k, v in tot.most_common(45):
     per = f" {v * 32 / npos:7.2f}/pos" if npos else ""
