@@ -525,3 +525,15 @@ def test_residual_short_deep_levels(prnu, H, W):
         for i in range(2):
             ref = oracle.residual(src[i].cpu().numpy().astype(np.float32))
             assert np.abs(got[i] - ref).max() <= W_TOL
+
+
+@pytest.mark.parametrize("H,W", [(45, 60), (27, 54), (125, 250), (64, 2), (2, 16), (48, 40)])
+def test_pce_fft235_sizes_match_oracle(prnu, H, W):
+    """PCE at plane sizes whose factors are 3 and 5 only, powers of two, and tiny / flat
+    planes, against the oracle's FFT-based surface (R-17, R-19): shifted, null and
+    affine pairs."""
+    g = np.random.default_rng(H * 7 + W)
+    T = g.normal(0, 1, (3, H, W)).astype(np.float32)
+    R = np.stack([np.roll(T[0], (1, 3 % W), axis=(0, 1)) + g.normal(0, 0.5, (H, W)),
+                  g.normal(0, 1, (H, W)), T[2] * 2.0 + 1.0]).astype(np.float32)
+    _pce_check(prnu, R, T, excl=min(5, (min(H, W) - 1) // 2))
