@@ -321,7 +321,6 @@ __device__ __forceinline__ float2 al_pick16(const float2 (&q)[16], int sl) {
     return r;
 }
 
-constexpr int AL_FIX = 5;   // edge fix-up slots per thread: ceil(16 rows * 40 columns / 128)
 
 template <typename T, int MINB, bool ALL4>
 __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_constant__ CUtensorMap map, AlArgs a) {

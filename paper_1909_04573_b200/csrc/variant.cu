@@ -45,12 +45,17 @@ __constant__ float c_var_h[2][16] = {
 enum VarMode { VM_SYM = 0, VM_PER = 1, VM_SWT = 2 };
 
 __device__ __forceinline__ int var_mod(int i, int n) {
+    if (i >= 0 && i < n) return i;           // the common case: no division
+    if (i >= n && i < 2 * n) return i - n;   // one wrap
     const int r = i % n;
     return r < 0 ? r + n : r;
 }
-// where analysis input sample i of a length-N axis comes from (R-4, R-24, R-25)
+// where analysis input sample i of a length-N axis comes from (R-4, R-24, R-25).
+// Interior samples (almost all) return at once: the integer modulo of the general
+// maps made the passes instruction-bound (8 FHD frames, db4 periodic: see DESIGN §6).
 template <int MODE>
 __device__ __forceinline__ int var_map(int i, int N, int Np) {
+    if (i >= 0 && i < N) return i;
     if (MODE == VM_SYM) return mirror(i, N);
     if (MODE == VM_PER) {
         const int r = var_mod(i, Np);       // periodic over the padded length Np ...

@@ -39,7 +39,6 @@ constexpr int SC_Y = ST_Y / 2 + 3;      // 19 coefficient rows
 constexpr int SC_X = ST_X / 2 + 3;      // 35 coefficient cols
 constexpr int SC_BW = 36;               // TMA box width (144 B, multiple of 16)
 constexpr int SC_PS = 704;              // plane stride in floats (>= 19*36, 128-B multiple)
-constexpr int SC_TILE = 4 * SC_PS;      // one frame's 4 planes (128-B multiple)
 static_assert(SC_Y * SC_BW <= SC_PS && (SC_PS * 4) % 128 == 0, "TMA plane tile layout");
 
 struct SynthMaps {
