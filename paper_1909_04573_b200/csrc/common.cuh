@@ -84,6 +84,38 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// ---------------------------------------------------------------- reductions
+// Deterministic warp-shuffle sums (the fingerprint / NCC / PCE / WDFT block
+// reductions): an xor butterfly inside each warp (lane i and lane i^o add the
+// same two operands, so every lane ends with the same bits), then every thread
+// adds the NW warp totals in warp order.  A fixed shape => bit-reproducible.
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+// Sums N values per thread across the block (NW = blockDim.x / 32 warps);
+// sh holds N * NW doubles.  Result in v[] on every thread.
+template <int N, int NW = 8>
+__device__ __forceinline__ void block_sum(double (&v)[N], double* sh) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int j = 0; j < N; ++j) v[j] = warp_sum(v[j]);
+    if (lane == 0) {
+#pragma unroll
+        for (int j = 0; j < N; ++j) sh[j * NW + w] = v[j];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        double t = sh[j * NW];
+#pragma unroll
+        for (int k = 1; k < NW; ++k) t += sh[j * NW + k];
+        v[j] = t;
+    }
+    __syncthreads();   // sh may be reused at once
+}
+
 // ---------------------------------------------------------------- wavelet
 // 8-tap Daubechies (4 vanishing moments) in minimum-phase order (R-2, R-5):
 // analysis   a[c] = sum_i H_[i] x[2c-6+i],   d[c] = sum_i G_[i] x[2c-6+i]

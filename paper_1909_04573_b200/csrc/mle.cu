@@ -38,20 +38,6 @@ int launch_accumulate(const float* W, const float* I, int batch, long long P, do
 }
 
 // ---------------------------------------------------------------- a6
-// Deterministic block sum of one double per thread (blockDim.x == 256).
-__device__ __forceinline__ double block_sum_256(double v, double* sh) {
-    sh[threadIdx.x] = v;
-    __syncthreads();
-#pragma unroll
-    for (int s = 128; s > 0; s >>= 1) {
-        if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
-        __syncthreads();
-    }
-    double r = sh[0];
-    __syncthreads();
-    return r;
-}
-
 struct FinalizeSrc {   // K = sum_WI / max(sum_I2, eps)
     const double* num;
     const double* den;
@@ -70,7 +56,7 @@ struct FloatSrc {      // a residual plane to be zero-meaned
 template <class Src>
 __global__ void __launch_bounds__(256) k_zm_rows(Src src, int H, int W, double* __restrict__ X,
                                                   double* __restrict__ rowmean) {
-    __shared__ double sh[256];
+    __shared__ double sh[8];
     const int y = blockIdx.x;
     double s = 0.0;
     for (int x = threadIdx.x; x < W; x += 256) {
@@ -78,8 +64,9 @@ __global__ void __launch_bounds__(256) k_zm_rows(Src src, int H, int W, double* 
         X[(size_t)y * W + x] = v;
         s += v;
     }
-    double t = block_sum_256(s, sh);
-    if (threadIdx.x == 0) rowmean[y] = t / W;
+    double t[1] = {s};
+    block_sum(t, sh);
+    if (threadIdx.x == 0) rowmean[y] = t[0] / W;
 }
 
 // S:135 step 2: column means of the row-centred values, in ZM_CHUNKS row chunks
@@ -193,7 +180,7 @@ size_t ncc_workspace_bytes(int batch) {
 
 __global__ void __launch_bounds__(256) k_ncc_pass1(const float* __restrict__ a, const float* __restrict__ b,
                                                     long long P, double* __restrict__ part) {
-    __shared__ double sh[256];
+    __shared__ double sh[16];
     const int pb = blockIdx.y;
     const float* A = a + (size_t)pb * P;
     const float* B = b + (size_t)pb * P;
@@ -202,11 +189,11 @@ __global__ void __launch_bounds__(256) k_ncc_pass1(const float* __restrict__ a, 
         sa += (double)A[i];
         sb += (double)B[i];
     }
-    sa = block_sum_256(sa, sh);
-    sb = block_sum_256(sb, sh);
+    double t[2] = {sa, sb};
+    block_sum(t, sh);
     if (threadIdx.x == 0) {
-        part[((size_t)pb * NCC_BLOCKS + blockIdx.x) * 2 + 0] = sa;
-        part[((size_t)pb * NCC_BLOCKS + blockIdx.x) * 2 + 1] = sb;
+        part[((size_t)pb * NCC_BLOCKS + blockIdx.x) * 2 + 0] = t[0];
+        part[((size_t)pb * NCC_BLOCKS + blockIdx.x) * 2 + 1] = t[1];
     }
 }
 
@@ -217,14 +204,16 @@ __device__ __forceinline__ void ncc_means(const double* part1, int pb, long long
         sa += part1[((size_t)pb * NCC_BLOCKS + k) * 2 + 0];
         sb += part1[((size_t)pb * NCC_BLOCKS + k) * 2 + 1];
     }
-    *ma = block_sum_256(sa, sh) / (double)P;
-    *mb = block_sum_256(sb, sh) / (double)P;
+    double t[2] = {sa, sb};
+    block_sum(t, sh);
+    *ma = t[0] / (double)P;
+    *mb = t[1] / (double)P;
 }
 
 __global__ void __launch_bounds__(256) k_ncc_pass2(const float* __restrict__ a, const float* __restrict__ b,
                                                     long long P, const double* __restrict__ part1,
                                                     double* __restrict__ part2) {
-    __shared__ double sh[256];
+    __shared__ double sh[24];
     const int pb = blockIdx.y;
     double ma, mb;
     ncc_means(part1, pb, P, &ma, &mb, sh);
@@ -237,27 +226,24 @@ __global__ void __launch_bounds__(256) k_ncc_pass2(const float* __restrict__ a, 
         saa += da * da;
         sbb += db * db;
     }
-    sab = block_sum_256(sab, sh);
-    saa = block_sum_256(saa, sh);
-    sbb = block_sum_256(sbb, sh);
+    double t[3] = {sab, saa, sbb};
+    block_sum(t, sh);
     if (threadIdx.x == 0) {
         double* o = part2 + ((size_t)pb * NCC_BLOCKS + blockIdx.x) * 3;
-        o[0] = sab;
-        o[1] = saa;
-        o[2] = sbb;
+        o[0] = t[0];
+        o[1] = t[1];
+        o[2] = t[2];
     }
 }
 
 __global__ void __launch_bounds__(256) k_ncc_final(const double* __restrict__ part2, double* __restrict__ out) {
-    __shared__ double sh[256];
+    __shared__ double sh[24];
     const int pb = blockIdx.x;
     double s[3] = {0.0, 0.0, 0.0};
     for (int k = threadIdx.x; k < NCC_BLOCKS; k += 256)
         for (int j = 0; j < 3; ++j) s[j] += part2[((size_t)pb * NCC_BLOCKS + k) * 3 + j];
-    double sab = block_sum_256(s[0], sh);
-    double saa = block_sum_256(s[1], sh);
-    double sbb = block_sum_256(s[2], sh);
-    if (threadIdx.x == 0) out[pb] = sab / sqrt(saa * sbb);   // NaN for a constant input
+    block_sum(s, sh);
+    if (threadIdx.x == 0) out[pb] = s[0] / sqrt(s[1] * s[2]);   // NaN for a constant input
 }
 
 int launch_ncc(const float* a, const float* b, int batch, long long P, double* out, void* ws, cudaStream_t st) {

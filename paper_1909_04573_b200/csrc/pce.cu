@@ -72,28 +72,42 @@ __device__ __forceinline__ bool better(float a1, int i1, float a2, int i2) {
     return a1 > a2 || (a1 == a2 && i1 < i2);
 }
 
+// Warp-shuffle reduction of (|C| peak, index, energy): the xor butterfly picks the
+// same winner on both lanes of every exchange (better() is a total order on the
+// candidates; NaN never becomes one, k_pce_partial skips it), then
+// every thread folds the 8 warp results in warp order.  Fixed shape, deterministic.
 __device__ void block_reduce_peak(float& a, int& idx, double& e) {
-    __shared__ float sa[256];
-    __shared__ int si[256];
-    __shared__ double se[256];
-    sa[threadIdx.x] = a;
-    si[threadIdx.x] = idx;
-    se[threadIdx.x] = e;
-    __syncthreads();
-    for (int s = 128; s > 0; s >>= 1) {
-        if (threadIdx.x < s) {
-            int o = threadIdx.x + s;
-            if (better(sa[o], si[o], sa[threadIdx.x], si[threadIdx.x])) {
-                sa[threadIdx.x] = sa[o];
-                si[threadIdx.x] = si[o];
-            }
-            se[threadIdx.x] += se[o];
+    __shared__ float sa[8];
+    __shared__ int si[8];
+    __shared__ double se[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        float a2 = __shfl_xor_sync(0xffffffffu, a, o);
+        int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
+        if (better(a2, i2, a, idx)) {
+            a = a2;
+            idx = i2;
         }
-        __syncthreads();
     }
+    e = warp_sum(e);
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        sa[w] = a;
+        si[w] = idx;
+        se[w] = e;
+    }
+    __syncthreads();
     a = sa[0];
     idx = si[0];
     e = se[0];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) {
+        if (better(sa[k], si[k], a, idx)) {
+            a = sa[k];
+            idx = si[k];
+        }
+        e += se[k];
+    }
     __syncthreads();
 }
 
@@ -147,18 +161,14 @@ __global__ void __launch_bounds__(256) k_pce_final(const float* __restrict__ C, 
         double v = (double)Cb[(size_t)yy * W + xx];
         en += v * v;
     }
-    __shared__ double sh[256];
-    sh[threadIdx.x] = en;
-    __syncthreads();
-    for (int s = 128; s > 0; s >>= 1) {
-        if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
-        __syncthreads();
-    }
+    __shared__ double sh[8];
+    double ent[1] = {en};
+    block_sum(ent, sh);
     if (threadIdx.x == 0) {
         double v = (double)Cb[p];
         double n_out = (double)(P - (long long)nr * nc);
         double r;
-        double bg = n_out > 0 ? (e - sh[0]) / n_out : 0.0;
+        double bg = n_out > 0 ? (e - ent[0]) / n_out : 0.0;
         if (!(n_out > 0) || !(bg > 0.0)) r = (v >= 0.0) ? PCE_CAP : -PCE_CAP;
         else r = (v >= 0.0 ? 1.0 : -1.0) * v * v / bg;   // scale-invariant ratio
         pce[b] = r;

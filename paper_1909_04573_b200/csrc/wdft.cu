@@ -35,14 +35,10 @@ __global__ void __launch_bounds__(256) k_wdft_energy(const float* __restrict__ K
         const double v = Kb[i];
         acc = fma(v, v, acc);
     }
-    __shared__ double sh[256];
-    sh[threadIdx.x] = acc;
-    __syncthreads();
-    for (int s = 128; s > 0; s >>= 1) {
-        if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) part[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = sh[0];
+    __shared__ double sh[8];
+    double t[1] = {acc};
+    block_sum(t, sh);
+    if (threadIdx.x == 0) part[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = t[0];
 }
 
 __global__ void k_wdft_energy_final(const double* part, int nblk, long long P, float* s2) {

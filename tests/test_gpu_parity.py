@@ -430,6 +430,26 @@ def test_wdft_matches_oracle(prnu, B, H, W):
 
 
 @pytest.mark.gpu
+def test_wdft_closed_form_gpu(prnu):
+    """The GPU path against R-23's closed form (tests/test_oracle_match.py): an isolated
+    strong line is scaled by s2/(c1^2 HW/324), a weak one passes with gain 1, and a line
+    in spectrum row 1 (mirror window folds it in twice) is scaled by 81/(HW)."""
+    def cos(H, W, c, fy, fx):
+        y, x = np.mgrid[0:H, 0:W]
+        return c * np.cos(2 * np.pi * (fy * y / H + fx * x / W))
+    H, W = 64, 48
+    K1, K2 = cos(H, W, 1.0, 9, 13), cos(H, W, 0.05, 25, 6)
+    s2 = (1.0 + 0.05 ** 2) / 2
+    want_a = (s2 / (H * W / 324)) * K1 + K2
+    H2, W2 = 40, 72
+    K3 = cos(H2, W2, 0.3, 1, 20)
+    want_b = (81.0 / (H2 * W2)) * K3
+    for K, want in ((K1 + K2, want_a), (K3, want_b)):
+        got = prnu.wdft(torch.from_numpy(K.astype(np.float32)).cuda()).cpu().numpy()
+        assert np.max(np.abs(got - want)) <= 1e-5 * np.max(np.abs(K)), np.max(np.abs(got - want))
+
+
+@pytest.mark.gpu
 def test_wdft_fingerprint_fhd(prnu):
     """On a real (synthetic-camera) fingerprint at FHD: parity and it keeps the PRNU
     (NCC with the true K does not drop)."""

@@ -200,3 +200,37 @@ def test_wdft_gain_matches_brute_force_windows():
         m = np.minimum(m, box)
     ref = np.real(np.fft.ifft2(F * (s2 / np.maximum(m, s2))))
     assert np.max(np.abs(oracle.wiener_dft(K) - ref)) < 1e-12
+
+
+def _cos(H, W, c, fy, fx):
+    y, x = np.mgrid[0:H, 0:W]
+    return c * np.cos(2 * np.pi * (fy * y / H + fx * x / W))
+
+
+def test_wdft_closed_form_isolated_cosines():
+    """R-23 in closed form, without the oracle's FFT: a cosine c cos(2pi(fy y/H + fx x/W))
+    has two spectral lines |F| = c HW/2, so A^2 = c^2 HW/4 there and 0 elsewhere.  With
+    every other line outside the 9x9 box, the box means at a line are A^2/w^2 and the
+    minimum is the w = 9 one, A^2/81; s2 = sum c_i^2/2 (Parseval).  Hence each component
+    is scaled by g_i = s2 / max(c_i^2 HW/324, s2): a strong line is attenuated, a weak
+    one (box mean below s2) passes with gain exactly 1."""
+    H, W = 64, 48
+    c1, c2 = 1.0, 0.05
+    K1, K2 = _cos(H, W, c1, 9, 13), _cos(H, W, c2, 25, 6)
+    s2 = (c1 * c1 + c2 * c2) / 2
+    g1 = s2 / max(c1 * c1 * H * W / 324, s2)
+    g2 = s2 / max(c2 * c2 * H * W / 324, s2)
+    assert g1 < 0.06 and g2 == 1.0
+    out = oracle.wiener_dft(K1 + K2)
+    assert np.max(np.abs(out - (g1 * K1 + g2 * K2))) < 1e-12
+
+
+def test_wdft_closed_form_mirror_window_at_the_edge():
+    """The mirror (e_N) extension of R-7 on the spectrum array: for a line in row 1
+    (and its partner in row H-1) the 7- and 9-wide windows fold the line in twice,
+    so the box means are A^2/9, A^2/25, 2A^2/49, 2A^2/81 and the minimum is 2A^2/81:
+    gain = s2 / (2 A^2/81) = (c^2/2) / (c^2 HW/162) = 81/(HW)."""
+    H, W = 40, 72
+    K = _cos(H, W, 0.3, 1, 20)
+    out = oracle.wiener_dft(K)
+    assert np.max(np.abs(out - (81.0 / (H * W)) * K)) < 1e-12
