@@ -11,7 +11,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libprnu.so")
-SOURCES = ["capi.cu", "sda.cu", "wavelet.cu", "analysis.cu", "shrink.cu", "mle.cu", "pce.cu", "wdft.cu", "variant.cu"]
+SOURCES = ["capi.cu", "sda.cu", "wavelet.cu", "analysis.cu", "shrink.cu", "mle.cu", "pce.cu", "pcefft.cu", "wdft.cu", "variant.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",

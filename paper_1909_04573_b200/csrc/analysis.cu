@@ -148,35 +148,6 @@ struct AlArgs {
     float div_d, div_r;     // u16 SDA sums: S = RN(sum / d) (R-11)
 };
 
-// packed fp32 helpers: {k, k} * b + c with k an immediate (FFMA2 imm form)
-__device__ __forceinline__ float2 lf2(float k, float2 b, float2 c) {
-    unsigned long long rb = *reinterpret_cast<const unsigned long long*>(&b);
-    unsigned long long rc = *reinterpret_cast<const unsigned long long*>(&c);
-    unsigned long long r;
-    asm("{.reg .b64 kk; mov.b64 kk, {%1, %1}; fma.rn.f32x2 %0, kk, %2, %3;}" : "=l"(r) : "f"(k), "l"(rb), "l"(rc));
-    return *reinterpret_cast<float2*>(&r);
-}
-__device__ __forceinline__ float2 add2(float2 a, float2 b) {
-    unsigned long long ra = *reinterpret_cast<const unsigned long long*>(&a);
-    unsigned long long rb = *reinterpret_cast<const unsigned long long*>(&b);
-    unsigned long long r;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(ra), "l"(rb));
-    return *reinterpret_cast<float2*>(&r);
-}
-__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
-    unsigned long long ra = *reinterpret_cast<const unsigned long long*>(&a);
-    unsigned long long rb = *reinterpret_cast<const unsigned long long*>(&b);
-    unsigned long long r;
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(ra), "l"(rb));
-    return *reinterpret_cast<float2*>(&r);
-}
-__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
-    unsigned long long ra = *reinterpret_cast<const unsigned long long*>(&a);
-    unsigned long long rb = *reinterpret_cast<const unsigned long long*>(&b);
-    unsigned long long r;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(ra), "l"(rb));
-    return *reinterpret_cast<float2*>(&r);
-}
 __device__ __forceinline__ float al_rcp(float x) {
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -218,17 +189,17 @@ __device__ __forceinline__ void al_stg_put(float* s, int r, int x, float v) {
 __device__ __forceinline__ void al_lift_pairs(const float2 (&E)[7], const float2 (&O)[7], float2 (&L)[4], float2 (&Hh)[4]) {
     float2 E1[7], O1[6], E2[6], O2[5];
 #pragma unroll
-    for (int j = 0; j < 7; ++j) E1[j] = lf2(-LF_C1, O[j], E[j]);
+    for (int j = 0; j < 7; ++j) E1[j] = ffma2(-LF_C1, O[j], E[j]);
 #pragma unroll
-    for (int j = 0; j < 6; ++j) O1[j] = lf2(-LF_C2B, E1[j + 1], lf2(LF_C2A, E1[j], O[j]));
+    for (int j = 0; j < 6; ++j) O1[j] = ffma2(-LF_C2B, E1[j + 1], ffma2(LF_C2A, E1[j], O[j]));
 #pragma unroll
-    for (int j = 1; j < 6; ++j) E2[j] = lf2(-LF_C3B, O1[j], lf2(LF_C3A, O1[j - 1], E1[j]));
+    for (int j = 1; j < 6; ++j) E2[j] = ffma2(-LF_C3B, O1[j], ffma2(LF_C3A, O1[j - 1], E1[j]));
 #pragma unroll
-    for (int j = 1; j < 5; ++j) O2[j] = lf2(LF_C4B, E2[j + 1], lf2(LF_C4A, E2[j], O1[j]));
+    for (int j = 1; j < 5; ++j) O2[j] = ffma2(LF_C4B, E2[j + 1], ffma2(LF_C4A, E2[j], O1[j]));
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         L[i] = O2[i + 1];                          // o2 at k = i, i + 4
-        Hh[i] = lf2(-LF_C5, O2[i + 1], E2[i + 2]);  // e3 at k = i, i + 4 (e3[j] = e2[j] - C5 o2[j-1])
+        Hh[i] = ffma2(-LF_C5, O2[i + 1], E2[i + 2]);  // e3 at k = i, i + 4 (e3[j] = e2[j] - C5 o2[j-1])
     }
 }
 __device__ __forceinline__ void al_rowpass(const uint8_t* s, int r, int g, float, float, float2 (&L)[4],
@@ -533,11 +504,11 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
         auto lift_y = [&](int j, float2& o2, float2& e3) {
             const float2 pe = make_float2(RBlo[(2 * j) * AL_RBP + slot], RBhi[(2 * j) * AL_RBP + slot]);
             const float2 po = make_float2(RBlo[(2 * j + 1) * AL_RBP + slot], RBhi[(2 * j + 1) * AL_RBP + slot]);
-            const float2 e1 = lf2(-LF_C1, po, pe);                              // e1[m]
-            const float2 o1 = lf2(-LF_C2B, e1, lf2(LF_C2A, se1, so));           // o1[m-1]
-            const float2 e2 = lf2(-LF_C3B, o1, lf2(LF_C3A, so1, se1));          // e2[m-1]
-            o2 = lf2(LF_C4B, e2, lf2(LF_C4A, se2, so1));                        // o2[m-2] = a[m] / KA
-            e3 = lf2(-LF_C5, o2, e2);                                           // e3[m-1] = d[m] / KD
+            const float2 e1 = ffma2(-LF_C1, po, pe);                              // e1[m]
+            const float2 o1 = ffma2(-LF_C2B, e1, ffma2(LF_C2A, se1, so));           // o1[m-1]
+            const float2 e2 = ffma2(-LF_C3B, o1, ffma2(LF_C3A, so1, se1));          // e2[m-1]
+            o2 = ffma2(LF_C4B, e2, ffma2(LF_C4A, se2, so1));                        // o2[m-2] = a[m] / KA
+            e3 = ffma2(-LF_C5, o2, e2);                                           // e3[m-1] = d[m] / KD
             so = po;
             se1 = e1;
             so1 = o1;

@@ -84,6 +84,40 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// ---------------------------------------------------------------- packed fp32 (f32x2)
+// Two fp32 lanes per instruction (FADD2 / FMUL2 / FFMA2): half the issue slots of
+// the scalar forms at the same lane throughput (broadcast-scalar forms: ffma2 /
+// fmul2s below).
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+    unsigned long long ra = *reinterpret_cast<const unsigned long long*>(&a);
+    unsigned long long rb = *reinterpret_cast<const unsigned long long*>(&b);
+    unsigned long long r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(ra), "l"(rb));
+    return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+    unsigned long long ra = *reinterpret_cast<const unsigned long long*>(&a);
+    unsigned long long rb = *reinterpret_cast<const unsigned long long*>(&b);
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(ra), "l"(rb));
+    return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+    unsigned long long ra = *reinterpret_cast<const unsigned long long*>(&a);
+    unsigned long long rb = *reinterpret_cast<const unsigned long long*>(&b);
+    unsigned long long r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(ra), "l"(rb));
+    return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {   // a * b + c
+    unsigned long long ra = *reinterpret_cast<const unsigned long long*>(&a);
+    unsigned long long rb = *reinterpret_cast<const unsigned long long*>(&b);
+    unsigned long long rc = *reinterpret_cast<const unsigned long long*>(&c);
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(ra), "l"(rb), "l"(rc));
+    return *reinterpret_cast<float2*>(&r);
+}
+
 // ---------------------------------------------------------------- reductions
 // Deterministic warp-shuffle sums (the fingerprint / NCC / PCE / WDFT block
 // reductions): an xor butterfly inside each warp (lane i and lane i^o add the

@@ -12,14 +12,19 @@ namespace prnu {
 constexpr int PCE_BLOCKS = 128;   // partial blocks per pair: a fixed partition (not the SM count) => fixed sum order
 constexpr double PCE_CAP = 1e12;
 
+// Two paths: `cols` (H has a radix plan in pcefft.cu, W even): cuFFT 1-D C2C rows
+// of the packed real planes + the fused column kernel; otherwise 2-D R2C/C2R.
 struct PcePlan {
     int H, W, batch;
-    cufftHandle r2c, c2r;
+    bool cols;
+    cufftHandle r2c, c2r, c2c;
     size_t work;       // bytes of cuFFT work area
     size_t ws_bytes;   // total workspace prnu_pce needs
 };
 
 static size_t spectrum_elems(int H, int W) { return (size_t)H * (W / 2 + 1); }
+bool pce_cols_supported(int H);
+int launch_pce_cols(int mode, const void* Z, const void* Rs, void* out, int H, int W, int batch, cudaStream_t st);
 
 // ---------------------------------------------------------------- template
 __global__ void __launch_bounds__(256) k_pce_template(const float* __restrict__ K, int k_batch,
@@ -198,25 +203,41 @@ int pce_plan_create(int H, int W, int batch, size_t* ws_bytes, void** out) {
     p->H = H;
     p->W = W;
     p->batch = batch;
-    int n[2] = {H, W};
+    p->cols = W % 2 == 0 && pce_cols_supported(H);
     size_t w1 = 0, w2 = 0;
     cufftResult r;
-    if ((r = cufftCreate(&p->r2c)) || (r = cufftCreate(&p->c2r))) {
-        delete p;
-        return fail(PRNU_CUDA_ERROR, std::string("cufftCreate: ") + cufft_str(r));
-    }
-    cufftSetAutoAllocation(p->r2c, 0);
-    cufftSetAutoAllocation(p->c2r, 0);
-    int nf = W / 2 + 1;
-    int inembed_r[2] = {H, W}, onembed_c[2] = {H, nf};
-    r = cufftMakePlanMany(p->r2c, 2, n, inembed_r, 1, H * W, onembed_c, 1, H * nf, CUFFT_R2C, batch, &w1);
-    if (r == CUFFT_SUCCESS)
-        r = cufftMakePlanMany(p->c2r, 2, n, onembed_c, 1, H * nf, inembed_r, 1, H * W, CUFFT_C2R, batch, &w2);
-    if (r != CUFFT_SUCCESS) {
-        cufftDestroy(p->r2c);
-        cufftDestroy(p->c2r);
-        delete p;
-        return fail(PRNU_CUDA_ERROR, std::string("cufftMakePlanMany: ") + cufft_str(r));
+    if (p->cols) {
+        if ((r = cufftCreate(&p->c2c))) {
+            delete p;
+            return fail(PRNU_CUDA_ERROR, std::string("cufftCreate: ") + cufft_str(r));
+        }
+        cufftSetAutoAllocation(p->c2c, 0);
+        long long m[1] = {W / 2};
+        r = cufftMakePlanMany64(p->c2c, 1, m, m, 1, W / 2, m, 1, W / 2, CUFFT_C2C, (long long)H * batch, &w1);
+        if (r != CUFFT_SUCCESS) {
+            cufftDestroy(p->c2c);
+            delete p;
+            return fail(PRNU_CUDA_ERROR, std::string("cufftMakePlanMany64: ") + cufft_str(r));
+        }
+    } else {
+        int n[2] = {H, W};
+        if ((r = cufftCreate(&p->r2c)) || (r = cufftCreate(&p->c2r))) {
+            delete p;
+            return fail(PRNU_CUDA_ERROR, std::string("cufftCreate: ") + cufft_str(r));
+        }
+        cufftSetAutoAllocation(p->r2c, 0);
+        cufftSetAutoAllocation(p->c2r, 0);
+        int nf = W / 2 + 1;
+        int inembed_r[2] = {H, W}, onembed_c[2] = {H, nf};
+        r = cufftMakePlanMany(p->r2c, 2, n, inembed_r, 1, H * W, onembed_c, 1, H * nf, CUFFT_R2C, batch, &w1);
+        if (r == CUFFT_SUCCESS)
+            r = cufftMakePlanMany(p->c2r, 2, n, onembed_c, 1, H * nf, inembed_r, 1, H * W, CUFFT_C2R, batch, &w2);
+        if (r != CUFFT_SUCCESS) {
+            cufftDestroy(p->r2c);
+            cufftDestroy(p->c2r);
+            delete p;
+            return fail(PRNU_CUDA_ERROR, std::string("cufftMakePlanMany: ") + cufft_str(r));
+        }
     }
     p->work = std::max(w1, w2);
     size_t spec = sizeof(cufftComplex) * spectrum_elems(H, W) * batch;
@@ -231,8 +252,12 @@ int pce_plan_create(int H, int W, int batch, size_t* ws_bytes, void** out) {
 int pce_plan_destroy(void* plan) {
     PcePlan* p = reinterpret_cast<PcePlan*>(plan);
     if (!p) return PRNU_OK;
-    cufftDestroy(p->r2c);
-    cufftDestroy(p->c2r);
+    if (p->cols) {
+        cufftDestroy(p->c2c);
+    } else {
+        cufftDestroy(p->r2c);
+        cufftDestroy(p->c2r);
+    }
     delete p;
     return PRNU_OK;
 }
@@ -263,25 +288,52 @@ int run_pce(void* plan, const float* R, const float* T, int excl, int aligned, d
     PeakE* part = reinterpret_cast<PeakE*>(c);
 
     cufftResult r;
-    if ((r = cufftSetStream(p->r2c, st)) || (r = cufftSetStream(p->c2r, st)) || (r = cufftSetWorkArea(p->r2c, work)) ||
-        (r = cufftSetWorkArea(p->c2r, work)))
-        return fail(PRNU_CUDA_ERROR, std::string("cufft setup: ") + cufft_str(r));
-    // R == nullptr: reuse the residual spectrum an earlier call left in this workspace
-    if (R && (r = cufftExecR2C(p->r2c, const_cast<float*>(R), Rf)))
-        return fail(PRNU_CUDA_ERROR, std::string("cufftExecR2C: ") + cufft_str(r));
-    if (!T) return PRNU_OK;   // spectrum only
-    if ((r = cufftExecR2C(p->r2c, const_cast<float*>(T), Tf)))
-        return fail(PRNU_CUDA_ERROR, std::string("cufftExecR2C: ") + cufft_str(r));
-    long long n_per = (long long)spectrum_elems(H, W);
-    unsigned blocks = (unsigned)std::min<long long>((n_per * batch + 255) / 256, 8LL * device_sm_count());
-    {
-        KTimer kt("pce_conj_mul", st);
-        k_conj_mul<<<blocks, 256, 0, st>>>(Rf, Tf, n_per, batch);
+    if (p->cols) {
+        // rows: the real planes as packed complex rows (8-byte aligned views; a
+        // misaligned input is staged through Cs first)
+        if ((r = cufftSetStream(p->c2c, st)) || (r = cufftSetWorkArea(p->c2c, work)))
+            return fail(PRNU_CUDA_ERROR, std::string("cufft setup: ") + cufft_str(r));
+        const size_t plane_bytes = sizeof(float) * (size_t)H * W * batch;
+        auto rows = [&](const float* X, cufftComplex* dst) -> int {
+            if (reinterpret_cast<uintptr_t>(X) % 8) {
+                cudaMemcpyAsync(Cs, X, plane_bytes, cudaMemcpyDeviceToDevice, st);
+                X = Cs;
+            }
+            cufftComplex* src = reinterpret_cast<cufftComplex*>(const_cast<float*>(X));
+            if ((r = cufftExecC2C(p->c2c, src, dst, CUFFT_FORWARD)))
+                return fail(PRNU_CUDA_ERROR, std::string("cufftExecC2C: ") + cufft_str(r));
+            return PRNU_OK;
+        };
+        if (R) {
+            if (int rc = rows(R, Rf)) return rc;
+            if (int rc = launch_pce_cols(0, Rf, nullptr, Rf, H, W, batch, st)) return rc;
+        }
+        if (!T) return PRNU_OK;
+        if (int rc = rows(T, Tf)) return rc;
+        if (int rc = launch_pce_cols(1, Tf, Rf, Tf, H, W, batch, st)) return rc;
+        if ((r = cufftExecC2C(p->c2c, Tf, reinterpret_cast<cufftComplex*>(Cs), CUFFT_INVERSE)))
+            return fail(PRNU_CUDA_ERROR, std::string("cufftExecC2C: ") + cufft_str(r));
+    } else {
+        if ((r = cufftSetStream(p->r2c, st)) || (r = cufftSetStream(p->c2r, st)) ||
+            (r = cufftSetWorkArea(p->r2c, work)) || (r = cufftSetWorkArea(p->c2r, work)))
+            return fail(PRNU_CUDA_ERROR, std::string("cufft setup: ") + cufft_str(r));
+        // R == nullptr: reuse the residual spectrum an earlier call left in this workspace
+        if (R && (r = cufftExecR2C(p->r2c, const_cast<float*>(R), Rf)))
+            return fail(PRNU_CUDA_ERROR, std::string("cufftExecR2C: ") + cufft_str(r));
+        if (!T) return PRNU_OK;   // spectrum only
+        if ((r = cufftExecR2C(p->r2c, const_cast<float*>(T), Tf)))
+            return fail(PRNU_CUDA_ERROR, std::string("cufftExecR2C: ") + cufft_str(r));
+        long long n_per = (long long)spectrum_elems(H, W);
+        unsigned blocks = (unsigned)std::min<long long>((n_per * batch + 255) / 256, 8LL * device_sm_count());
+        {
+            KTimer kt("pce_conj_mul", st);
+            k_conj_mul<<<blocks, 256, 0, st>>>(Rf, Tf, n_per, batch);
+        }
+        count_launch();
+        if (int rc = check_launch("k_conj_mul")) return rc;
+        if ((r = cufftExecC2R(p->c2r, Tf, Cs)))
+            return fail(PRNU_CUDA_ERROR, std::string("cufftExecC2R: ") + cufft_str(r));
     }
-    count_launch();
-    if (int rc = check_launch("k_conj_mul")) return rc;
-    if ((r = cufftExecC2R(p->c2r, Tf, Cs)))
-        return fail(PRNU_CUDA_ERROR, std::string("cufftExecC2R: ") + cufft_str(r));
     long long P = (long long)H * W;
     {
         KTimer kt("pce_partial", st);

@@ -547,7 +547,8 @@ def test_residual_short_deep_levels(prnu, H, W):
             assert np.abs(got[i] - ref).max() <= W_TOL
 
 
-@pytest.mark.parametrize("H,W", [(45, 60), (27, 54), (125, 250), (64, 2), (2, 16), (48, 40)])
+@pytest.mark.parametrize("H,W", [(45, 60), (27, 54), (125, 250), (64, 2), (2, 16), (48, 40), (48, 54), (45, 62),
+                                 (720, 1280), (64, 6), (27, 4)])
 def test_pce_fft235_sizes_match_oracle(prnu, H, W):
     """PCE at plane sizes whose factors are 3 and 5 only, powers of two, and tiny / flat
     planes, against the oracle's FFT-based surface (R-17, R-19): shifted, null and
