@@ -224,113 +224,159 @@ constexpr int threads() {
     int t = (4 * N / r + 31) / 32 * 32;
     return t < 128 ? 128 : t;
 }
-// Shared memory: A = the transform buffer, two planes (re, im) of [N][NCOL] floats
-// (a column pair's value at row y is one 8-byte word: a half-warp of a pass touches
-// 4 rows x 4 pairs = 128 contiguous bytes; the first pass stores with row stride
-// R1, conflict-free because every radix plan starts with an odd radix).
-// B = the cached spectrum tile R^[y][pair s: (k, M-k)] (match) fetched by
-// cp.async at kernel start, so its DRAM latency hides behind the forward FFT.
-// tw = exp(2 pi i m / N).
-template <int N>
-constexpr size_t smem_bytes() {
-    return sizeof(float) * 4 * (size_t)NCOL * N + sizeof(float2) * N;
-}
-
-// One Stockham pass of radix R, in place over the 4 column pairs: L = product of
-// the radices already applied.  Twiddle exp(S 2 pi i j k / (L R)) = tw[j k N/(L R)].
-template <int N, int R, int L, int S, int NT>
-__device__ __forceinline__ void pass(float* __restrict__ re, float* __restrict__ im, const float2* __restrict__ tw) {
-    constexpr int NTASK = N / R;
-    static_assert(4 * NTASK <= NT, "one task per thread");
-    const int tau = threadIdx.x, pp = 2 * (tau & 3), t = tau >> 2;
-    const bool act = tau < 4 * NTASK;
-    Cp v[R];
-    if (act) {
-        sfor<0, R>([&](auto j) {
-            const int o = (t + decltype(j)::value * NTASK) * NCOL + pp;
-            v[j] = {*reinterpret_cast<const float2*>(re + o), *reinterpret_cast<const float2*>(im + o)};
-        });
-    }
-    __syncthreads();
-    if (act) {
-        if constexpr (L > 1) {
-            const int step = (t % L) * (N / (L * R));
-            sfor<1, R>([&](auto j) {
-                const float2 w = tw[decltype(j)::value * step];
-                v[j] = pcmul(v[j], w.x, S * w.y);
-            });
-        }
-        Dft<R, S>::run(v);
-        const int base = (t / L) * L * R + (t % L);
-        sfor<0, R>([&](auto r) {
-            const int o = (base + decltype(r)::value * L) * NCOL + pp;
-            *reinterpret_cast<float2*>(re + o) = v[r].re;
-            *reinterpret_cast<float2*>(im + o) = v[r].im;
-        });
-    }
-    __syncthreads();
-}
-
-template <int N, int R1, int R2, int R3, int S, int NT>
-__device__ __forceinline__ void fft3(float* re, float* im, const float2* tw) {
-    pass<N, R1, 1, S, NT>(re, im, tw);
-    pass<N, R2, R1, S, NT>(re, im, tw);
-    pass<N, R3, R1 * R2, S, NT>(re, im, tw);
-}
-
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
 }
 
-// MODE 0: Z (rows FFT of R) -> spectrum out;  MODE 1: Z (rows FFT of T), spectrum Rs
-// -> packed rows of P = R^ conj(T^) after the inverse column FFT, written to out.
-// grid (ncta_main + 1, batch): CTA a < ncta_main owns the pairs k = 4a+1 .. 4a+4,
-// pair s in columns 2s (k) and 2s+1 (M-k), so the global phases move a pair as one
-// 8-byte word per plane; CTA ncta_main owns column 0.  The global phases map
-// task = 4 y + s and issue all of a thread's loads before using them.
+// ---------------------------------------------------------------- fused kernel (all pairs but column 0)
+// Pair layout: one float4 per (row, pair s) = (re_k, re_{M-k}, im_k, im_{M-k}), a
+// row of 4 pairs = 64 bytes; a quarter-warp's LDS.128 / STS.128 covers 2 rows.
+// Shared-memory round trips per element: 5 (the untangle is fused into the first
+// forward pass, which reads Z from global; the conjugate product into the last
+// forward pass; the re-tangle and the global store into the last inverse pass).
+__device__ __forceinline__ Cp ld4(const float4* A, int i) {
+    const float4 q = A[i];
+    return {make_float2(q.x, q.y), make_float2(q.z, q.w)};
+}
+__device__ __forceinline__ void st4(float4* A, int i, Cp v) { A[i] = make_float4(v.re.x, v.re.y, v.im.x, v.im.y); }
+
+template <int N, int R, int L, int S>
+__device__ __forceinline__ void twiddle(Cp* v, int t, const float2* __restrict__ tw) {
+    if constexpr (L > 1) {
+        const int step = (t % L) * (N / (L * R));
+        sfor<1, R>([&](auto j) {
+            const float2 w = tw[decltype(j)::value * step];
+            v[j] = pcmul(v[j], w.x, S * w.y);
+        });
+    }
+}
+
+// in-place Stockham pass over the float4 pair layout
+template <int N, int R, int L, int S, int NT>
+__device__ __forceinline__ void pass4(float4* __restrict__ A, const float2* __restrict__ tw) {
+    constexpr int NTASK = N / R;
+    static_assert(4 * NTASK <= NT, "one task per thread");
+    const int tau = threadIdx.x, s = tau & 3, t = tau >> 2;
+    const bool act = tau < 4 * NTASK;
+    Cp v[R];
+    if (act) sfor<0, R>([&](auto j) { v[j] = ld4(A, (t + decltype(j)::value * NTASK) * 4 + s); });
+    __syncthreads();
+    if (act) {
+        twiddle<N, R, L, S>(v, t, tw);
+        Dft<R, S>::run(v);
+        const int base = (t / L) * L * R + (t % L);
+        sfor<0, R>([&](auto r) { st4(A, (base + decltype(r)::value * L) * 4 + s, v[r]); });
+    }
+    __syncthreads();
+}
+
+// out-of-place variant (no barrier between the loads and the stores)
+template <int N, int R, int L, int S, int NT>
+__device__ __forceinline__ void pass4o(const float4* __restrict__ A, float4* __restrict__ B,
+                                       const float2* __restrict__ tw) {
+    constexpr int NTASK = N / R;
+    static_assert(4 * NTASK <= NT, "one task per thread");
+    const int tau = threadIdx.x, s = tau & 3, t = tau >> 2;
+    if (tau < 4 * NTASK) {
+        Cp v[R];
+        sfor<0, R>([&](auto j) { v[j] = ld4(A, (t + decltype(j)::value * NTASK) * 4 + s); });
+        twiddle<N, R, L, S>(v, t, tw);
+        Dft<R, S>::run(v);
+        const int base = (t / L) * L * R + (t % L);
+        sfor<0, R>([&](auto r) { st4(B, (base + decltype(r)::value * L) * 4 + s, v[r]); });
+    }
+    __syncthreads();
+}
+
+template <int N>
+constexpr size_t smem_bytes_f(int mode) {
+    return sizeof(float4) * 4 * (size_t)N + sizeof(float2) * ((N + 1) & ~1) +
+           (mode ? sizeof(float2) * NCOL * (size_t)N : 0);
+}
+
+// Column 0 (the packed X[0] + i X[M]): lane k of pair 0, the other lanes zero; its
+// conjugate product separates the two Hermitian halves, which needs rows v and -v:
+// F(X0)[v] = (C[v] + conj C[-v])/2, F(XM)[v] = -(i/2)(C[v] - conj C[-v]);
+// P = PA + i PB with PA[0] = 0 (the DC bin).
+template <int N, int R1, int R2, int R3, int MODE, int NT>
+__device__ __forceinline__ void packed_column(const float2* __restrict__ Zb, const float2* __restrict__ Bt,
+                                              float2* __restrict__ Ob, int M, float4* A, const float2* tw) {
+    const int tid = threadIdx.x;
+    for (int y = tid; y < N; y += NT) {
+        const float2 z0 = Zb[(size_t)y * M];
+        A[y * 4] = make_float4(z0.x + z0.y, 0.f, z0.x - z0.y, 0.f);
+        A[y * 4 + 1] = A[y * 4 + 2] = A[y * 4 + 3] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncthreads();
+    pass4<N, R1, 1, -1, NT>(A, tw);
+    pass4<N, R2, R1, -1, NT>(A, tw);
+    pass4<N, R3, R1 * R2, -1, NT>(A, tw);
+    if constexpr (MODE == 0) {
+        for (int y = tid; y < N; y += NT) Ob[(size_t)y * M] = make_float2(A[y * 4].x, A[y * 4].z);
+        return;
+    } else {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+        constexpr int KP = (N + NT - 1) / NT;
+        float2 pv[KP];
+#pragma unroll
+        for (int q = 0; q < KP; ++q) {
+            const int y = tid + q * NT;
+            if (y < N) {
+                const int ym = y ? N - y : 0;
+                const float2 t = make_float2(A[y * 4].x, A[y * 4].z), tm = make_float2(A[ym * 4].x, -A[ym * 4].z);
+                const float2 r = Bt[y * NCOL], rm = conjf2(Bt[ym * NCOL]);
+                const float2 ta = cadd(t, tm), tb = muli<-1>(csub(t, tm));
+                const float2 ra = cadd(r, rm), rb = muli<-1>(csub(r, rm));
+                float2 pa = cmul(ra, conjf2(ta)), pb = cmul(rb, conjf2(tb));
+                if (y == 0) pa = make_float2(0.f, 0.f);
+                const float2 p = cadd(pa, muli<1>(pb));
+                pv[q] = make_float2(0.25f * p.x, 0.25f * p.y);
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < KP; ++q) {
+            const int y = tid + q * NT;
+            if (y < N) A[y * 4] = make_float4(pv[q].x, 0.f, pv[q].y, 0.f);
+        }
+        __syncthreads();
+        pass4<N, R1, 1, 1, NT>(A, tw);
+        pass4<N, R2, R1, 1, NT>(A, tw);
+        pass4<N, R3, R1 * R2, 1, NT>(A, tw);
+        for (int y = tid; y < N; y += NT) {
+            const float x0 = A[y * 4].x, xm = A[y * 4].z;   // X0 + i XM, both real
+            Ob[(size_t)y * M] = make_float2(x0 + xm, x0 - xm);
+        }
+    }
+}
+
+// grid (ncta_main + 1, batch): CTA a < ncta_main owns the pairs k = 4a+1 .. 4a+4
+// (k <= M/2) and their mirrors M-k; the last CTA owns column 0.
 template <int N, int R1, int R2, int R3, int MODE, int NT>
 __global__ void __launch_bounds__(NT, (NT <= 384 ? 2 : 1))
-    k_pce_cols(const float2* __restrict__ Z, const float2* __restrict__ Rs, float2* __restrict__ out, int M, int W,
-               int ncta_main) {
+    k_pce_cols_f(const float2* __restrict__ Z, const float2* __restrict__ Rs, float2* __restrict__ out, int M,
+                 int W) {
     static_assert(R1 * R2 * R3 == N, "radix plan");
     static_assert(R1 % 2 == 1 || (R1 & (R1 - 1)) == 0, "first radix odd (or a power-of-two plan)");
-    constexpr int KQ = (4 * N + NT - 1) / NT;   // (y, pair) tasks per thread
-    constexpr int KP = (N + NT - 1) / NT;       // column-0 tasks per thread
-    constexpr int PL = NCOL * N;                // floats per plane
-    extern __shared__ float sm[];
-    float *Ar = sm, *Ai = sm + PL;
-    float2* Bt = reinterpret_cast<float2*>(sm + 2 * PL);   // [N][NCOL] complex
-    float2* tw = reinterpret_cast<float2*>(sm + 4 * PL);
-    __shared__ float2 wk[4];   // exp(-2 pi i k / W) of the 4 pairs
+    extern __shared__ float4 sm4[];
+    float4* A = sm4;                                          // [N][4 pairs]
+    float2* tw = reinterpret_cast<float2*>(sm4 + 4 * N);      // exp(2 pi i m / N)
+    float2* Bt = tw + ((N + 1) & ~1);                         // [N][8]: R^ (k, M-k) of pair s at 2s, 2s+1 (16-B aligned)
+    __shared__ float2 wk[4];                                  // exp(-2 pi i k / W) of the 4 pairs
     const int tid = threadIdx.x;
     const size_t plane = (size_t)N * M;
     const float2* Zb = Z + (size_t)blockIdx.y * plane;
     float2* Ob = out + (size_t)blockIdx.y * plane;
-    const bool packed = (int)blockIdx.x == ncta_main;
     const int npair = M / 2, k0 = 4 * blockIdx.x + 1;
-    // pair access: (value at k, value at M-k) of pair s, row y
-    auto put2 = [&](int y, int s, float2 vk, float2 vm) {
-        *reinterpret_cast<float2*>(Ar + y * NCOL + 2 * s) = make_float2(vk.x, vm.x);
-        *reinterpret_cast<float2*>(Ai + y * NCOL + 2 * s) = make_float2(vk.y, vm.y);
-    };
-    auto get2 = [&](int y, int s, float2& vk, float2& vm) {
-        const float2 r = *reinterpret_cast<const float2*>(Ar + y * NCOL + 2 * s);
-        const float2 i = *reinterpret_cast<const float2*>(Ai + y * NCOL + 2 * s);
-        vk = make_float2(r.x, i.x);
-        vm = make_float2(r.y, i.y);
-    };
-    auto put0 = [&](int y, float2 v) {
-        Ar[y * NCOL] = v.x;
-        Ai[y * NCOL] = v.y;
-    };
-    auto get0 = [&](int y) { return make_float2(Ar[y * NCOL], Ai[y * NCOL]); };
+    const bool packed = blockIdx.x == gridDim.x - 1;
 
-    if constexpr (MODE == 1) {   // prefetch the R^ tile: Bt[y][2s] = R^[y][k], Bt[y][2s+1] = R^[y][M-k]
+    if constexpr (MODE == 1) {   // prefetch the R^ tile; waited for before the conjugate product
         const float2* Rb = Rs + (size_t)blockIdx.y * plane;
         if (!packed) {
             for (int task = tid; task < 8 * N; task += NT) {
-                const int c = task & 7, y = task >> 3, s = c >> 1, k = k0 + s;
+                const int c = task & 7, y = task >> 3, k = k0 + (c >> 1);
                 if (k <= npair) cp_async8(Bt + y * NCOL + c, Rb + (size_t)y * M + ((c & 1) ? M - k : k));
             }
         } else {
@@ -339,133 +385,109 @@ __global__ void __launch_bounds__(NT, (NT <= 384 ? 2 : 1))
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
     for (int m = tid; m < N; m += NT) tw[m] = kTw<N>.v[m];
-
-    // untangle: X[k] = (Z[k] + conj Z[M-k])/2 - (i/2) w_k (Z[k] - conj Z[M-k]),
-    // X[M-k] likewise with w_{M-k} = -conj(w_k); X[0], X[M] packed as X[0] + i X[M]
-    if (!packed) {
-        float2 zk[KQ], zm[KQ];
-#pragma unroll
-        for (int q = 0; q < KQ; ++q) {
-            const int task = tid + q * NT, s = task & 3, y = task >> 2, k = k0 + s;
-            zk[q] = zm[q] = make_float2(0.f, 0.f);
-            if (task < 4 * N && k <= npair) {
-                zk[q] = Zb[(size_t)y * M + k];
-                zm[q] = Zb[(size_t)y * M + (M - k)];
-            }
-        }
-        if (tid < 4) {
-            double sn, cs;
-            sincospi(-2.0 * (k0 + tid) / W, &sn, &cs);
-            wk[tid] = make_float2((float)cs, (float)sn);
-        }
-        __syncthreads();
-#pragma unroll
-        for (int q = 0; q < KQ; ++q) {
-            const int task = tid + q * NT, s = task & 3, y = task >> 2;
-            if (task < 4 * N) {
-                const float2 w = wk[s], wm = make_float2(-w.x, w.y);
-                const float2 sk = cadd(zk[q], conjf2(zm[q])), dk = csub(zk[q], conjf2(zm[q]));
-                const float2 sm_ = cadd(zm[q], conjf2(zk[q])), dm = csub(zm[q], conjf2(zk[q]));
-                const float2 ek = muli<-1>(cmul(w, dk)), em = muli<-1>(cmul(wm, dm));
-                put2(y, s, make_float2(0.5f * (sk.x + ek.x), 0.5f * (sk.y + ek.y)),
-                     make_float2(0.5f * (sm_.x + em.x), 0.5f * (sm_.y + em.y)));
-            }
-        }
-    } else {
-        float2 z0[KP];
-#pragma unroll
-        for (int q = 0; q < KP; ++q) {
-            const int y = tid + q * NT;
-            if (y < N) z0[q] = Zb[(size_t)y * M];
-        }
-#pragma unroll
-        for (int q = 0; q < KP; ++q) {
-            const int y = tid + q * NT;
-            if (y < N) put0(y, make_float2(z0[q].x + z0[q].y, z0[q].x - z0[q].y));
-        }
+    if (packed) {
+        packed_column<N, R1, R2, R3, MODE, NT>(Zb, Bt, Ob, M, A, tw);
+        return;
+    }
+    if (tid < 4) {
+        double sn, cs;
+        sincospi(-2.0 * (k0 + tid) / W, &sn, &cs);
+        wk[tid] = make_float2((float)cs, (float)sn);
     }
     __syncthreads();
-    fft3<N, R1, R2, R3, -1, NT>(Ar, Ai, tw);
 
-    if constexpr (MODE == 0) {
-        if (!packed) {
-#pragma unroll 4
-            for (int task = tid; task < 4 * N; task += NT) {
-                const int s = task & 3, y = task >> 2, k = k0 + s;
-                if (k > npair) continue;
-                float2 vk, vm;
-                get2(y, s, vk, vm);
-                Ob[(size_t)y * M + k] = vk;
-                if (M - k != k) Ob[(size_t)y * M + (M - k)] = vm;
-            }
-        } else {
-            for (int y = tid; y < N; y += NT) Ob[(size_t)y * M] = get0(y);
+    const int s = tid & 3, k = k0 + s;
+    const bool kv = k <= npair;
+    // forward pass 1 + untangle: X[k] = (Z[k] + conj Z[M-k])/2 - (i/2) w_k (Z[k] - conj Z[M-k]),
+    // X[M-k] likewise with w_{M-k} = -conj(w_k)
+    {
+        constexpr int NTASK = N / R1;
+        static_assert(4 * NTASK <= NT, "one task per thread");
+        const int t = tid >> 2;
+        const bool act = tid < 4 * NTASK;
+        float2 zk[R1], zm[R1];
+        if (act) {
+            sfor<0, R1>([&](auto j) {
+                const int y = t + decltype(j)::value * NTASK;
+                zk[j] = kv ? Zb[(size_t)y * M + k] : make_float2(0.f, 0.f);
+                zm[j] = kv ? Zb[(size_t)y * M + (M - k)] : make_float2(0.f, 0.f);
+            });
+            const float2 w = wk[s], wm = make_float2(-w.x, w.y);
+            Cp v[R1];
+            sfor<0, R1>([&](auto j) {
+                const float2 sk = cadd(zk[j], conjf2(zm[j])), dk = csub(zk[j], conjf2(zm[j]));
+                const float2 sm_ = cadd(zm[j], conjf2(zk[j])), dm = csub(zm[j], conjf2(zk[j]));
+                const float2 ek = muli<-1>(cmul(w, dk)), em = muli<-1>(cmul(wm, dm));
+                v[j] = {make_float2(0.5f * (sk.x + ek.x), 0.5f * (sm_.x + em.x)),
+                        make_float2(0.5f * (sk.y + ek.y), 0.5f * (sm_.y + em.y))};
+            });
+            Dft<R1, -1>::run(v);
+            sfor<0, R1>([&](auto r) { st4(A, (t * R1 + decltype(r)::value) * 4 + s, v[r]); });
         }
-        return;
-    } else {
-        asm volatile("cp.async.wait_all;" ::: "memory");
         __syncthreads();
-        if (!packed) {
-#pragma unroll 4
-            for (int task = tid; task < 4 * N; task += NT) {
-                const int s = task & 3, y = task >> 2;
-                if (k0 + s > npair) continue;
-                const float4 r = *reinterpret_cast<const float4*>(Bt + y * NCOL + 2 * s);
-                float2 tk, tm;
-                get2(y, s, tk, tm);
-                put2(y, s, cmul(make_float2(r.x, r.y), conjf2(tk)), cmul(make_float2(r.z, r.w), conjf2(tm)));
-            }
-            __syncthreads();
-        } else {
-            // the packed column C = F(X0) + i F(XM): F(X0)[v] = (C[v] + conj C[-v])/2,
-            // F(XM)[v] = -(i/2)(C[v] - conj C[-v]); P = PA + i PB, PA[0] = 0 (DC).
-            // Reads A[y] and A[-y]: all reads before any write.
-            float2 pv[KP];
-#pragma unroll
-            for (int q = 0; q < KP; ++q) {
-                const int y = tid + q * NT;
-                if (y < N) {
-                    const int ym = y ? N - y : 0;
-                    const float2 t = get0(y), tm = conjf2(get0(ym));
-                    const float2 r = Bt[y * NCOL], rm = conjf2(Bt[ym * NCOL]);
-                    const float2 ta = cadd(t, tm), tb = muli<-1>(csub(t, tm));
-                    const float2 ra = cadd(r, rm), rb = muli<-1>(csub(r, rm));
-                    float2 pa = cmul(ra, conjf2(ta)), pb = cmul(rb, conjf2(tb));
-                    if (y == 0) pa = make_float2(0.f, 0.f);
-                    const float2 p = cadd(pa, muli<1>(pb));
-                    pv[q] = make_float2(0.25f * p.x, 0.25f * p.y);
+    }
+    pass4<N, R2, R1, -1, NT>(A, tw);
+    // forward pass 3 + (MODE 0) spectrum store / (MODE 1) P = R^ conj(T^), natural order
+    {
+        constexpr int NTASK = N / R3, L = R1 * R2;
+        static_assert(4 * NTASK <= NT, "one task per thread");
+        const int t = tid >> 2;
+        const bool act = tid < 4 * NTASK;
+        Cp v[R3];
+        if (act) sfor<0, R3>([&](auto j) { v[j] = ld4(A, (t + decltype(j)::value * NTASK) * 4 + s); });
+        if constexpr (MODE == 1) asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+        if (act) {
+            twiddle<N, R3, L, -1>(v, t, tw);
+            Dft<R3, -1>::run(v);
+            const int base = (t / L) * L * R3 + (t % L);
+            if constexpr (MODE == 0) {
+                if (kv) {
+                    sfor<0, R3>([&](auto r) {
+                        const int y = base + decltype(r)::value * L;
+                        Ob[(size_t)y * M + k] = make_float2(v[r].re.x, v[r].im.x);
+                        if (M - k != k) Ob[(size_t)y * M + (M - k)] = make_float2(v[r].re.y, v[r].im.y);
+                    });
                 }
+            } else {
+                sfor<0, R3>([&](auto r) {
+                    const int y = base + decltype(r)::value * L;
+                    const float4 q = *reinterpret_cast<const float4*>(Bt + y * NCOL + 2 * s);
+                    const float2 pk = cmul(make_float2(q.x, q.y), make_float2(v[r].re.x, -v[r].im.x));
+                    const float2 pm = cmul(make_float2(q.z, q.w), make_float2(v[r].re.y, -v[r].im.y));
+                    st4(A, y * 4 + s, Cp{make_float2(pk.x, pm.x), make_float2(pk.y, pm.y)});
+                });
             }
-            __syncthreads();
-#pragma unroll
-            for (int q = 0; q < KP; ++q) {
-                const int y = tid + q * NT;
-                if (y < N) put0(y, pv[q]);
-            }
-            __syncthreads();
         }
-        fft3<N, R1, R2, R3, 1, NT>(Ar, Ai, tw);
-        // re-tangle: Z'[k] = (X[k] + conj X[M-k]) + i e_k (X[k] - conj X[M-k]),
-        // e_k = exp(2 pi i k / W) = conj(w_k), e_{M-k} = -w_k
-        if (!packed) {
-#pragma unroll 4
-            for (int task = tid; task < 4 * N; task += NT) {
-                const int s = task & 3, y = task >> 2, k = k0 + s;
-                if (k > npair) continue;
-                float2 xk, xm;
-                get2(y, s, xk, xm);
-                const float2 w = wk[s], ek = conjf2(w), em = make_float2(-w.x, -w.y);
-                const float2 zk = cadd(cadd(xk, conjf2(xm)), muli<1>(cmul(ek, csub(xk, conjf2(xm)))));
-                Ob[(size_t)y * M + k] = zk;
-                if (M - k != k) {
-                    const float2 zm = cadd(cadd(xm, conjf2(xk)), muli<1>(cmul(em, csub(xm, conjf2(xk)))));
-                    Ob[(size_t)y * M + (M - k)] = zm;
-                }
-            }
-        } else {
-            for (int y = tid; y < N; y += NT) {
-                const float2 x = get0(y);   // X0 + i XM, both real
-                Ob[(size_t)y * M] = make_float2(x.x + x.y, x.x - x.y);
+        if constexpr (MODE == 0) return;
+        __syncthreads();
+    }
+    // inverse passes 1, 2 ping-pong through the (consumed) R^ tile: A -> Bt -> A
+    float4* B4 = reinterpret_cast<float4*>(Bt);
+    pass4o<N, R1, 1, 1, NT>(A, B4, tw);
+    pass4o<N, R2, R1, 1, NT>(B4, A, tw);
+    // inverse pass 3 + re-tangle + global store:
+    // Z'[k] = (X[k] + conj X[M-k]) + i e_k (X[k] - conj X[M-k]), e_k = conj(w_k), e_{M-k} = -w_k
+    {
+        constexpr int NTASK = N / R3, L = R1 * R2;
+        const int t = tid >> 2;
+        const bool act = tid < 4 * NTASK;
+        if (act) {
+            Cp v[R3];
+            sfor<0, R3>([&](auto j) { v[j] = ld4(A, (t + decltype(j)::value * NTASK) * 4 + s); });
+            twiddle<N, R3, L, 1>(v, t, tw);
+            Dft<R3, 1>::run(v);
+            const int base = (t / L) * L * R3 + (t % L);
+            const float2 w = wk[s], ek = conjf2(w), em = make_float2(-w.x, -w.y);
+            if (kv) {
+                sfor<0, R3>([&](auto r) {
+                    const int y = base + decltype(r)::value * L;
+                    const float2 xk = make_float2(v[r].re.x, v[r].im.x), xm = make_float2(v[r].re.y, v[r].im.y);
+                    Ob[(size_t)y * M + k] = cadd(cadd(xk, conjf2(xm)), muli<1>(cmul(ek, csub(xk, conjf2(xm)))));
+                    if (M - k != k)
+                        Ob[(size_t)y * M + (M - k)] =
+                            cadd(cadd(xm, conjf2(xk)), muli<1>(cmul(em, csub(xm, conjf2(xk)))));
+                });
             }
         }
     }
@@ -476,17 +498,17 @@ static int launch_cols(int mode, const float2* Z, const float2* Rs, float2* out,
                        cudaStream_t st) {
     constexpr int NT = threads<N, R1, R2, R3>();
     static DeviceFlags done0, done1;
-    const size_t sm = smem_bytes<N>();
-    const void* fn = mode ? (const void*)k_pce_cols<N, R1, R2, R3, 1, NT> : (const void*)k_pce_cols<N, R1, R2, R3, 0, NT>;
+    const size_t sm = smem_bytes_f<N>(mode);
+    const void* fn =
+        mode ? (const void*)k_pce_cols_f<N, R1, R2, R3, 1, NT> : (const void*)k_pce_cols_f<N, R1, R2, R3, 0, NT>;
     if (int rc = set_smem_attr(fn, sm, mode ? done1 : done0)) return rc;
-    const int ncta_main = (M / 2 + 3) / 4;
-    dim3 grid(ncta_main + 1, batch);
+    dim3 grid((M / 2 + 3) / 4 + 1, batch);
     {
         KTimer kt(mode ? "pce_cols_match" : "pce_cols_fwd", st);
         if (mode)
-            k_pce_cols<N, R1, R2, R3, 1, NT><<<grid, NT, sm, st>>>(Z, Rs, out, M, 2 * M, ncta_main);
+            k_pce_cols_f<N, R1, R2, R3, 1, NT><<<grid, NT, sm, st>>>(Z, Rs, out, M, 2 * M);
         else
-            k_pce_cols<N, R1, R2, R3, 0, NT><<<grid, NT, sm, st>>>(Z, Rs, out, M, 2 * M, ncta_main);
+            k_pce_cols_f<N, R1, R2, R3, 0, NT><<<grid, NT, sm, st>>>(Z, Rs, out, M, 2 * M);
     }
     count_launch();
     return check_launch("k_pce_cols");
