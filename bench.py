@@ -474,7 +474,7 @@ def main():
             R4 = prnu.residual(Iq4, zero_mean=True)
             plan4.set_residual(R4)   # one FFT of the 64 query residuals for all 64 fingerprints
             for c in range(c4n):
-                plan4.match(prnu.pce_template(Ks4[c], Iq4))
+                plan4.match_template(Ks4[c], Iq4)   # template K (.) Iq formed inside the row FFT
         t_c4 = timed(camera_id, reps=1)
         c4 = {"workload": "64 x 300 frames 1280x720, depth 30, 64x64 PCE", "ms": t_c4,
               "fingerprints_per_s": c4n / (t_c4 / 1000.0), "pce_per_s": c4n * c4n / (t_c4 / 1000.0)}

@@ -213,15 +213,18 @@ int prnu_ncc(const float* a, const float* b, int batch, int H, int W, double* nc
  *   K fp32 [k_batch][H][W] with k_batch in {1, batch}, Iq u8 [batch][H][W].
  * prnu_pce: for each pair b, C = circular cross-correlation of the
  *   mean-removed residual[b] and template[b] (C[dy,dx] = sum R0[y,x]
- *   T0[y-dy, x-dx], via cuFFT R2C/C2R, fp32; mean removal = zeroing the DC
- *   bin), peak p* = argmax |C| (ties: smallest row-major index) or (0,0) if
+ *   T0[y-dy, x-dx], fp32; mean removal = zeroing the DC bin): for heights and
+ *   widths with a compiled radix plan (720, 1080, 500, ... x 1280, 1920, 500,
+ *   ...) the library's row and column FFT kernels, else cuFFT 1-D rows + the
+ *   column kernel, else cuFFT R2C/C2R), peak p* = argmax |C| (ties: smallest row-major index) or (0,0) if
  *   aligned != 0; PCE = sign(C[p*]) C[p*]^2 / mean of C^2 outside the circular
  *   (2e+1)^2 neighbourhood of p* (e = exclusion_half, default 5), energies in
  *   fp64; zero background energy -> +-1e12.  Outputs (device,
  *   [batch]): pce fp64, peak_y/peak_x int32 (the shift (dy,dx)), peak fp64
  *   (C[p*] in the units of the definition above).  The decision is pce > 60
  *   (strict).
- * prnu_pce_plan_create: cuFFT plans for [batch][H][W] (no auto-allocation);
+ * prnu_pce_plan_create: the plan (and cuFFT plans where used, no
+ *   auto-allocation) for [batch][H][W];
  *   *ws_bytes receives the workspace prnu_pce needs.  *plan is opaque, freed
  *   by prnu_pce_plan_destroy.
  * ------------------------------------------------------------------------- */
@@ -241,6 +244,16 @@ int prnu_pce_plan_destroy(void* plan);
 int prnu_pce_residual_spectrum(void* plan, const float* residual, void* ws, size_t ws_bytes, void* stream);
 int prnu_pce_cached(void* plan, const float* template_, int batch, int exclusion_half, int aligned, double* pce,
                     int* peak_y, int* peak_x, double* peak, void* ws, size_t ws_bytes, void* stream);
+/* prnu_pce_cached_template: prnu_pce_cached for the template K[b or 0] (.) (float)Iq[b]
+ * of prnu_pce_template (R-18) without materialising it: the product is
+ * formed inside the row transform when the plan has a fused row plan, else by
+ * prnu_pce_template into the workspace.  K fp32 [k_batch][H][W] (k_batch in {1,
+ * batch}), Iq u8 [batch][H][W] (device).  Results are bit-identical to
+ * prnu_pce_cached(prnu_pce_template(K, Iq)).  Errors as prnu_pce_cached, plus
+ * PRNU_DIMENSION_MISMATCH for another k_batch. */
+int prnu_pce_cached_template(void* plan, const float* K, int k_batch, const uint8_t* Iq, int batch,
+                             int exclusion_half, int aligned, double* pce, int* peak_y, int* peak_x, double* peak,
+                             void* ws, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
  * f2  Wiener filtering of fingerprints in the DFT domain —

@@ -129,6 +129,7 @@ _sig("prnu_pce", _i, _vp, _vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _sz, _v
 _sig("prnu_pce_plan_destroy", _i, _vp)
 _sig("prnu_pce_residual_spectrum", _i, _vp, _vp, _vp, _sz, _vp)
 _sig("prnu_pce_cached", _i, _vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _sz, _vp)
+_sig("prnu_pce_cached_template", _i, _vp, _vp, _i, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _sz, _vp)
 _sig("prnu_wdft_plan_create", _i, _i, _i, _i, ctypes.POINTER(_sz), ctypes.POINTER(_vp))
 _sig("prnu_wdft", _i, _vp, _vp, _vp, _vp, _sz, _vp)
 _sig("prnu_wdft_plan_destroy", _i, _vp)
@@ -704,6 +705,25 @@ class PcePlan:
         _check(_lib.prnu_pce_cached(self._h, _ptr(T), self.batch, exclusion_half, int(aligned), _ptr(o.pce),
                                     _ptr(o.peak_y), _ptr(o.peak_x), _ptr(o.peak), _ptr(self.ws), self.nbytes,
                                     _stream()), "prnu_pce_cached")
+        return PceResult(o.pce.clone(), o.peak_y.clone(), o.peak_x.clone(), o.peak.clone())
+
+    @_on_device
+    def match_template(self, K: torch.Tensor, Iq: torch.Tensor, exclusion_half: int = 5,
+                       aligned: bool = False) -> PceResult:
+        """PCE of the cached residuals against the templates K (.) Iq (prnu_pce_cached_template):
+        the same result as match(pce_template(K, Iq)) without materialising the templates."""
+        Kb = K.unsqueeze(0) if K.dim() == 2 else K
+        if Iq.dim() == 2:
+            Iq = Iq.unsqueeze(0)
+        _dev(Kb, torch.float32, "K", (3,))
+        _dev(Iq, torch.uint8, "Iq", (3,))
+        if Iq.shape != (self.batch, self.H, self.W) or Kb.shape[1:] != (self.H, self.W):
+            raise ValueError("dimension mismatch with the plan")
+        o = self.out
+        _check(_lib.prnu_pce_cached_template(self._h, _ptr(Kb), Kb.shape[0], _ptr(Iq), self.batch, exclusion_half,
+                                             int(aligned), _ptr(o.pce), _ptr(o.peak_y), _ptr(o.peak_x),
+                                             _ptr(o.peak), _ptr(self.ws), self.nbytes, _stream()),
+               "prnu_pce_cached_template")
         return PceResult(o.pce.clone(), o.peak_y.clone(), o.peak_x.clone(), o.peak.clone())
 
     def __del__(self):

@@ -154,7 +154,8 @@ int wdft_plan_dims(void* plan, int* H, int* W, int* batch, size_t* ws_bytes);
 int run_wdft(void* plan, const float* K, float* K_out, void* ws, cudaStream_t st);
 int pce_plan_destroy(void* plan);
 int pce_plan_dims(void* plan, int* H, int* W, int* batch, size_t* ws_bytes);
-int run_pce(void* plan, const float* R, const float* T, int excl, int aligned, double* pce, int* py, int* px,
+int run_pce(void* plan, const float* R, const float* T, const float* K, int k_batch, const uint8_t* Iq, int excl,
+            int aligned, double* pce, int* py, int* px,
             double* peak, void* ws, cudaStream_t st);
 int block_plan_create(int H, int W, int block, int* n_tiles, size_t* ws_bytes, void** out);
 int block_plan_destroy(void* plan);
@@ -739,7 +740,7 @@ int prnu_pce(void* plan, const float* residual, const float* template_, int batc
     if (batch != pb) return fail(PRNU_DIMENSION_MISMATCH, "batch differs from the plan's batch");
     if (exclusion_half < 0) return fail(PRNU_BAD_PARAMETER, "exclusion_half must be >= 0");
     if (ws_bytes < need) return fail(PRNU_WORKSPACE_TOO_SMALL, "workspace too small");
-    return run_pce(plan, residual, template_, exclusion_half, aligned, pce, peak_y, peak_x, peak, ws,
+    return run_pce(plan, residual, template_, nullptr, 0, nullptr, exclusion_half, aligned, pce, peak_y, peak_x, peak, ws,
                    as_stream(stream));
 }
 
@@ -749,7 +750,8 @@ int prnu_pce_residual_spectrum(void* plan, const float* residual, void* ws, size
     size_t need;
     pce_plan_dims(plan, &H, &W, &pb, &need);
     if (ws_bytes < need) return fail(PRNU_WORKSPACE_TOO_SMALL, "workspace too small");
-    return run_pce(plan, residual, nullptr, 0, 0, nullptr, nullptr, nullptr, nullptr, ws, as_stream(stream));
+    return run_pce(plan, residual, nullptr, nullptr, 0, nullptr, 0, 0, nullptr, nullptr, nullptr, nullptr, ws,
+                   as_stream(stream));
 }
 
 int prnu_pce_cached(void* plan, const float* template_, int batch, int exclusion_half, int aligned, double* pce,
@@ -762,7 +764,23 @@ int prnu_pce_cached(void* plan, const float* template_, int batch, int exclusion
     if (batch != pb) return fail(PRNU_DIMENSION_MISMATCH, "batch differs from the plan's batch");
     if (exclusion_half < 0) return fail(PRNU_BAD_PARAMETER, "exclusion_half must be >= 0");
     if (ws_bytes < need) return fail(PRNU_WORKSPACE_TOO_SMALL, "workspace too small");
-    return run_pce(plan, nullptr, template_, exclusion_half, aligned, pce, peak_y, peak_x, peak, ws,
+    return run_pce(plan, nullptr, template_, nullptr, 0, nullptr, exclusion_half, aligned, pce, peak_y, peak_x, peak,
+                   ws, as_stream(stream));
+}
+
+int prnu_pce_cached_template(void* plan, const float* K, int k_batch, const uint8_t* Iq, int batch,
+                             int exclusion_half, int aligned, double* pce, int* peak_y, int* peak_x, double* peak,
+                             void* ws, size_t ws_bytes, void* stream) {
+    if (!plan || !K || !Iq || !pce || !peak_y || !peak_x || !peak || !ws)
+        return fail(PRNU_INVALID_ARG, "null pointer");
+    int H, W, pb;
+    size_t need;
+    pce_plan_dims(plan, &H, &W, &pb, &need);
+    if (batch != pb) return fail(PRNU_DIMENSION_MISMATCH, "batch differs from the plan's batch");
+    if (k_batch != 1 && k_batch != batch) return fail(PRNU_DIMENSION_MISMATCH, "k_batch must be 1 or batch");
+    if (exclusion_half < 0) return fail(PRNU_BAD_PARAMETER, "exclusion_half must be >= 0");
+    if (ws_bytes < need) return fail(PRNU_WORKSPACE_TOO_SMALL, "workspace too small");
+    return run_pce(plan, nullptr, nullptr, K, k_batch, Iq, exclusion_half, aligned, pce, peak_y, peak_x, peak, ws,
                    as_stream(stream));
 }
 

@@ -6,17 +6,21 @@
 #include <cufft.h>
 
 #include "common.cuh"
+#include "pce.cuh"
 
 namespace prnu {
 
 constexpr int PCE_BLOCKS = 128;   // partial blocks per pair: a fixed partition (not the SM count) => fixed sum order
 constexpr double PCE_CAP = 1e12;
 
-// Two paths: `cols` (H has a radix plan in pcefft.cu, W even): cuFFT 1-D C2C rows
-// of the packed real planes + the fused column kernel; otherwise 2-D R2C/C2R.
+// Three paths.  `cols` (H has a radix plan in pcefft.cu, W even): the rows as 1-D
+// transforms of the packed real planes + the fused column kernel, the rows either
+// by pcefft.cu's row kernel (`rows`: W/2 has a radix plan; the template product
+// and the peak/energy partials fused in) or by cuFFT 1-D C2C; otherwise cuFFT
+// 2-D R2C/C2R.
 struct PcePlan {
     int H, W, batch;
-    bool cols;
+    bool cols, rows;
     cufftHandle r2c, c2r, c2c;
     size_t work;       // bytes of cuFFT work area
     size_t ws_bytes;   // total workspace prnu_pce needs
@@ -24,6 +28,10 @@ struct PcePlan {
 
 static size_t spectrum_elems(int H, int W) { return (size_t)H * (W / 2 + 1); }
 bool pce_cols_supported(int H);
+bool pce_rows_supported(int W);
+int pce_rows_nparts(int H);
+int launch_pce_rows(int mode, const float* X, const float* K, int k_batch, const uint8_t* Iq, const void* Zin,
+                    void* Zout, float* C, void* part, int H, int W, int batch, cudaStream_t st);
 int launch_pce_cols(int mode, const void* Z, const void* Rs, void* out, int H, int W, int batch, cudaStream_t st);
 
 // ---------------------------------------------------------------- template
@@ -35,13 +43,34 @@ __global__ void __launch_bounds__(256) k_pce_template(const float* __restrict__ 
     for (long long i = blockIdx.x * 256LL + threadIdx.x; i < P; i += 256LL * gridDim.x)
         T[(size_t)b * P + i] = Kb[i] * (float)Iq[(size_t)b * P + i];
 }
+// 4 pixels per thread (P % 4 == 0, 16-byte aligned K / T, 4-byte aligned Iq): one
+// 16-byte K load, one 4-byte Iq load and one 16-byte streaming T store per thread
+__global__ void __launch_bounds__(256) k_pce_template4(const float4* __restrict__ K, int k_batch,
+                                                        const uchar4* __restrict__ Iq, long long P4,
+                                                        float4* __restrict__ T) {
+    const int b = blockIdx.y;
+    const float4* Kb = K + (size_t)(k_batch == 1 ? 0 : b) * P4;
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < P4; i += 256LL * gridDim.x) {
+        const float4 k = Kb[i];
+        const uchar4 q = Iq[(size_t)b * P4 + i];
+        __stcs(T + (size_t)b * P4 + i, make_float4(k.x * (float)q.x, k.y * (float)q.y, k.z * (float)q.z, k.w * (float)q.w));
+    }
+}
 
 int launch_pce_template(const float* K, int k_batch, const uint8_t* Iq, int batch, long long P, float* T,
                         cudaStream_t st) {
-    unsigned blocks = (unsigned)std::min<long long>((P + 255) / 256, 4LL * device_sm_count());
+    const bool vec = P % 4 == 0 && reinterpret_cast<uintptr_t>(K) % 16 == 0 && reinterpret_cast<uintptr_t>(T) % 16 == 0 &&
+                     reinterpret_cast<uintptr_t>(Iq) % 4 == 0;
+    const long long n = vec ? P / 4 : P;
+    unsigned blocks = (unsigned)std::min<long long>((n + 255) / 256, 8LL * device_sm_count());
     {
         KTimer kt("pce_template", st);
-        k_pce_template<<<dim3(blocks, batch), 256, 0, st>>>(K, k_batch, Iq, P, T);
+        if (vec)
+            k_pce_template4<<<dim3(blocks, batch), 256, 0, st>>>(reinterpret_cast<const float4*>(K), k_batch,
+                                                                 reinterpret_cast<const uchar4*>(Iq), n,
+                                                                 reinterpret_cast<float4*>(T));
+        else
+            k_pce_template<<<dim3(blocks, batch), 256, 0, st>>>(K, k_batch, Iq, P, T);
     }
     count_launch();
     return check_launch("k_pce_template");
@@ -64,19 +93,6 @@ __global__ void __launch_bounds__(256) k_conj_mul(const cufftComplex* __restrict
 }
 
 // ---------------------------------------------------------------- reductions
-struct PeakE {
-    float a;      // |C| of the best candidate
-    int idx;      // its linear index (-1 = none)
-    double e;     // partial energy
-};
-
-__device__ __forceinline__ bool better(float a1, int i1, float a2, int i2) {
-    // larger |C| wins; ties -> smaller index; idx -1 always loses
-    if (i2 < 0) return i1 >= 0;
-    if (i1 < 0) return false;
-    return a1 > a2 || (a1 == a2 && i1 < i2);
-}
-
 // Warp-shuffle reduction of (|C| peak, index, energy): the xor butterfly picks the
 // same winner on both lanes of every exchange (better() is a total order on the
 // candidates; NaN never becomes one, k_pce_partial skips it), then
@@ -136,7 +152,7 @@ __global__ void __launch_bounds__(256) k_pce_partial(const float* __restrict__ C
 }
 
 __global__ void __launch_bounds__(256) k_pce_final(const float* __restrict__ C, const PeakE* __restrict__ part,
-                                                    int H, int W, int excl, int aligned, double scale,
+                                                    int nparts, int H, int W, int excl, int aligned, double scale,
                                                     double* __restrict__ pce, int* __restrict__ py,
                                                     int* __restrict__ px, double* __restrict__ peak) {
     const int b = blockIdx.x;
@@ -145,8 +161,8 @@ __global__ void __launch_bounds__(256) k_pce_final(const float* __restrict__ C, 
     float best = -1.f;
     int bi = -1;
     double e = 0.0;
-    for (int k = threadIdx.x; k < PCE_BLOCKS; k += 256) {
-        PeakE q = part[(size_t)b * PCE_BLOCKS + k];
+    for (int k = threadIdx.x; k < nparts; k += 256) {
+        PeakE q = part[(size_t)b * nparts + k];
         if (better(q.a, q.idx, best, bi)) {
             best = q.a;
             bi = q.idx;
@@ -204,9 +220,12 @@ int pce_plan_create(int H, int W, int batch, size_t* ws_bytes, void** out) {
     p->W = W;
     p->batch = batch;
     p->cols = W % 2 == 0 && pce_cols_supported(H);
+    p->rows = p->cols && pce_rows_supported(W);
     size_t w1 = 0, w2 = 0;
     cufftResult r;
-    if (p->cols) {
+    if (p->rows) {
+        // no cuFFT plan
+    } else if (p->cols) {
         if ((r = cufftCreate(&p->c2c))) {
             delete p;
             return fail(PRNU_CUDA_ERROR, std::string("cufftCreate: ") + cufft_str(r));
@@ -243,7 +262,7 @@ int pce_plan_create(int H, int W, int batch, size_t* ws_bytes, void** out) {
     size_t spec = sizeof(cufftComplex) * spectrum_elems(H, W) * batch;
     p->ws_bytes = align_up(p->work, 256) + 2 * align_up(spec, 256) +
                   align_up(sizeof(float) * (size_t)H * W * batch, 256) +
-                  align_up(sizeof(PeakE) * (size_t)PCE_BLOCKS * batch, 256);
+                  align_up(sizeof(PeakE) * (size_t)std::max(PCE_BLOCKS, pce_rows_nparts(H)) * batch, 256);
     *ws_bytes = p->ws_bytes;
     *out = p;
     return PRNU_OK;
@@ -252,7 +271,8 @@ int pce_plan_create(int H, int W, int batch, size_t* ws_bytes, void** out) {
 int pce_plan_destroy(void* plan) {
     PcePlan* p = reinterpret_cast<PcePlan*>(plan);
     if (!p) return PRNU_OK;
-    if (p->cols) {
+    if (p->rows) {
+    } else if (p->cols) {
         cufftDestroy(p->c2c);
     } else {
         cufftDestroy(p->r2c);
@@ -271,8 +291,10 @@ int pce_plan_dims(void* plan, int* H, int* W, int* batch, size_t* ws_bytes) {
     return PRNU_OK;
 }
 
-int run_pce(void* plan, const float* R, const float* T, int excl, int aligned, double* pce, int* py, int* px,
-            double* peak, void* ws, cudaStream_t st) {
+// T == nullptr && K != nullptr: the template K[b or 0] (.) (float)Iq[b] (prnu_pce_template)
+// formed inside the row transform (or by prnu_pce_template into Cs on the cuFFT paths).
+int run_pce(void* plan, const float* R, const float* T, const float* K, int k_batch, const uint8_t* Iq, int excl,
+            int aligned, double* pce, int* py, int* px, double* peak, void* ws, cudaStream_t st) {
     PcePlan* p = reinterpret_cast<PcePlan*>(plan);
     const int H = p->H, W = p->W, batch = p->batch;
     char* c = reinterpret_cast<char*>(ws);
@@ -288,12 +310,41 @@ int run_pce(void* plan, const float* R, const float* T, int excl, int aligned, d
     PeakE* part = reinterpret_cast<PeakE*>(c);
 
     cufftResult r;
-    if (p->cols) {
+    const long long P = (long long)H * W;
+    const size_t plane_bytes = sizeof(float) * (size_t)P * batch;
+    int nparts = PCE_BLOCKS;
+    auto mis = [](const void* x, uintptr_t a) { return reinterpret_cast<uintptr_t>(x) % a != 0; };
+    if (R && K) return fail(PRNU_INVALID_ARG, "run_pce: template mode needs the cached residual spectrum");
+    if (!T && K && (!p->rows || mis(K, 8) || mis(Iq, 2))) {   // template into Cs, then as an explicit T
+        if (int rc = launch_pce_template(K, k_batch, Iq, batch, P, Cs, st)) return rc;
+        T = Cs;
+    }
+    if (p->rows) {
+        auto fwd_real = [&](const float* X, cufftComplex* dst) -> int {
+            if (mis(X, 8)) {
+                cudaMemcpyAsync(Cs, X, plane_bytes, cudaMemcpyDeviceToDevice, st);
+                X = Cs;
+            }
+            return launch_pce_rows(0, X, nullptr, 0, nullptr, nullptr, dst, nullptr, nullptr, H, W, batch, st);
+        };
+        if (R) {
+            if (int rc = fwd_real(R, Rf)) return rc;
+            if (int rc = launch_pce_cols(0, Rf, nullptr, Rf, H, W, batch, st)) return rc;
+        }
+        if (!T && !K) return PRNU_OK;
+        if (T) {
+            if (int rc = fwd_real(T, Tf)) return rc;
+        } else if (int rc = launch_pce_rows(1, nullptr, K, k_batch, Iq, nullptr, Tf, nullptr, nullptr, H, W, batch, st)) {
+            return rc;
+        }
+        if (int rc = launch_pce_cols(1, Tf, Rf, Tf, H, W, batch, st)) return rc;
+        if (int rc = launch_pce_rows(2, nullptr, nullptr, 0, nullptr, Tf, nullptr, Cs, part, H, W, batch, st)) return rc;
+        nparts = pce_rows_nparts(H);
+    } else if (p->cols) {
         // rows: the real planes as packed complex rows (8-byte aligned views; a
         // misaligned input is staged through Cs first)
         if ((r = cufftSetStream(p->c2c, st)) || (r = cufftSetWorkArea(p->c2c, work)))
             return fail(PRNU_CUDA_ERROR, std::string("cufft setup: ") + cufft_str(r));
-        const size_t plane_bytes = sizeof(float) * (size_t)H * W * batch;
         auto rows = [&](const float* X, cufftComplex* dst) -> int {
             if (reinterpret_cast<uintptr_t>(X) % 8) {
                 cudaMemcpyAsync(Cs, X, plane_bytes, cudaMemcpyDeviceToDevice, st);
@@ -334,16 +385,18 @@ int run_pce(void* plan, const float* R, const float* T, int excl, int aligned, d
         if ((r = cufftExecC2R(p->c2r, Tf, Cs)))
             return fail(PRNU_CUDA_ERROR, std::string("cufftExecC2R: ") + cufft_str(r));
     }
-    long long P = (long long)H * W;
-    {
-        KTimer kt("pce_partial", st);
-        k_pce_partial<<<dim3(PCE_BLOCKS, batch), 256, 0, st>>>(Cs, P, part);
+    if (!p->rows) {
+        {
+            KTimer kt("pce_partial", st);
+            k_pce_partial<<<dim3(PCE_BLOCKS, batch), 256, 0, st>>>(Cs, P, part);
+        }
+        count_launch();
     }
     {
         KTimer kt("pce_final", st);
-        k_pce_final<<<batch, 256, 0, st>>>(Cs, part, H, W, excl, aligned, 1.0 / (double)P, pce, py, px, peak);
+        k_pce_final<<<batch, 256, 0, st>>>(Cs, part, nparts, H, W, excl, aligned, 1.0 / (double)P, pce, py, px, peak);
     }
-    count_launch(2);
+    count_launch();
     return check_launch("pce reductions");
 }
 
@@ -490,7 +543,7 @@ int run_block_match(void* plan, const float* R, const float* T, int excl, double
         }
         count_launch(2);
         if ((rc = check_launch("k_gather_tiles"))) return rc;
-        if ((rc = run_pce(k.plan, Rg, Tg, excl, 1, pc, py, px, pk, pce_ws, st))) return rc;
+        if ((rc = run_pce(k.plan, Rg, Tg, nullptr, 0, nullptr, excl, 1, pc, py, px, pk, pce_ws, st))) return rc;
         if ((rc = launch_ncc(Rg, Tg, k.count, P, nc, ncc_ws, st))) return rc;
         {
             KTimer kt("block_scatter", st);

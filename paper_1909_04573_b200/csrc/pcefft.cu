@@ -17,6 +17,7 @@
 // and the reductions as before).  Spectrum layout (the cached residual
 // spectrum): [b][v][m], m = 0..M-1, column 0 = X[.][0] + i X[.][M] transformed.
 #include "common.cuh"
+#include "pce.cuh"
 
 
 namespace prnu {
@@ -217,11 +218,11 @@ __device__ const TwTable<N> kTw = TwTable<N>();
 constexpr int NCOL = 8;      // columns per CTA: 4 (k, M-k) pairs = 4 SIMD column pairs
 // Threads per CTA: every pass has 4 N / R tasks and each thread holds at most one
 // (the passes run in place: load, barrier, store), so NT >= 4 N / min(R).
+// Threads per CTA: the in-place pass (forward pass 2) needs one task per thread,
+// 4 N / R2 tasks; every other pass loops.  Plans put their largest radix second.
 template <int N, int R1, int R2, int R3>
 constexpr int threads() {
-    int r = R1 < R2 ? R1 : R2;
-    r = r < R3 ? r : R3;
-    int t = (4 * N / r + 31) / 32 * 32;
+    int t = (4 * N / R2 + 31) / 32 * 32;
     return t < 128 ? 128 : t;
 }
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
@@ -276,9 +277,8 @@ template <int N, int R, int L, int S, int NT>
 __device__ __forceinline__ void pass4o(const float4* __restrict__ A, float4* __restrict__ B,
                                        const float2* __restrict__ tw) {
     constexpr int NTASK = N / R;
-    static_assert(4 * NTASK <= NT, "one task per thread");
-    const int tau = threadIdx.x, s = tau & 3, t = tau >> 2;
-    if (tau < 4 * NTASK) {
+    for (int tau = threadIdx.x; tau < 4 * NTASK; tau += NT) {
+        const int s = tau & 3, t = tau >> 2;
         Cp v[R];
         sfor<0, R>([&](auto j) { v[j] = ld4(A, (t + decltype(j)::value * NTASK) * 4 + s); });
         twiddle<N, R, L, S>(v, t, tw);
@@ -290,9 +290,8 @@ __device__ __forceinline__ void pass4o(const float4* __restrict__ A, float4* __r
 }
 
 template <int N>
-constexpr size_t smem_bytes_f(int mode) {
-    return sizeof(float4) * 4 * (size_t)N + sizeof(float2) * ((N + 1) & ~1) +
-           (mode ? sizeof(float2) * NCOL * (size_t)N : 0);
+constexpr size_t smem_bytes_f() {
+    return sizeof(float4) * 8 * (size_t)N + sizeof(float2) * ((N + 1) & ~1);
 }
 
 // Column 0 (the packed X[0] + i X[M]): lane k of pair 0, the other lanes zero; its
@@ -300,8 +299,9 @@ constexpr size_t smem_bytes_f(int mode) {
 // F(X0)[v] = (C[v] + conj C[-v])/2, F(XM)[v] = -(i/2)(C[v] - conj C[-v]);
 // P = PA + i PB with PA[0] = 0 (the DC bin).
 template <int N, int R1, int R2, int R3, int MODE, int NT>
-__device__ __forceinline__ void packed_column(const float2* __restrict__ Zb, const float2* __restrict__ Bt,
-                                              float2* __restrict__ Ob, int M, float4* A, const float2* tw) {
+__device__ __forceinline__ void packed_column(const float2* __restrict__ Zb, const float2* __restrict__ Rb,
+                                              float2* __restrict__ Ob, int M, float4* A, float4* B,
+                                              const float2* tw) {
     const int tid = threadIdx.x;
     for (int y = tid; y < N; y += NT) {
         const float2 z0 = Zb[(size_t)y * M];
@@ -309,44 +309,31 @@ __device__ __forceinline__ void packed_column(const float2* __restrict__ Zb, con
         A[y * 4 + 1] = A[y * 4 + 2] = A[y * 4 + 3] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     __syncthreads();
-    pass4<N, R1, 1, -1, NT>(A, tw);
-    pass4<N, R2, R1, -1, NT>(A, tw);
-    pass4<N, R3, R1 * R2, -1, NT>(A, tw);
+    pass4o<N, R1, 1, -1, NT>(A, B, tw);
+    pass4o<N, R2, R1, -1, NT>(B, A, tw);
+    pass4o<N, R3, R1 * R2, -1, NT>(A, B, tw);
     if constexpr (MODE == 0) {
-        for (int y = tid; y < N; y += NT) Ob[(size_t)y * M] = make_float2(A[y * 4].x, A[y * 4].z);
+        for (int y = tid; y < N; y += NT) Ob[(size_t)y * M] = make_float2(B[y * 4].x, B[y * 4].z);
         return;
     } else {
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        __syncthreads();
-        constexpr int KP = (N + NT - 1) / NT;
-        float2 pv[KP];
-#pragma unroll
-        for (int q = 0; q < KP; ++q) {
-            const int y = tid + q * NT;
-            if (y < N) {
-                const int ym = y ? N - y : 0;
-                const float2 t = make_float2(A[y * 4].x, A[y * 4].z), tm = make_float2(A[ym * 4].x, -A[ym * 4].z);
-                const float2 r = Bt[y * NCOL], rm = conjf2(Bt[ym * NCOL]);
-                const float2 ta = cadd(t, tm), tb = muli<-1>(csub(t, tm));
-                const float2 ra = cadd(r, rm), rb = muli<-1>(csub(r, rm));
-                float2 pa = cmul(ra, conjf2(ta)), pb = cmul(rb, conjf2(tb));
-                if (y == 0) pa = make_float2(0.f, 0.f);
-                const float2 p = cadd(pa, muli<1>(pb));
-                pv[q] = make_float2(0.25f * p.x, 0.25f * p.y);
-            }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int q = 0; q < KP; ++q) {
-            const int y = tid + q * NT;
-            if (y < N) A[y * 4] = make_float4(pv[q].x, 0.f, pv[q].y, 0.f);
-        }
-        __syncthreads();
-        pass4<N, R1, 1, 1, NT>(A, tw);
-        pass4<N, R2, R1, 1, NT>(A, tw);
-        pass4<N, R3, R1 * R2, 1, NT>(A, tw);
         for (int y = tid; y < N; y += NT) {
-            const float x0 = A[y * 4].x, xm = A[y * 4].z;   // X0 + i XM, both real
+            const int ym = y ? N - y : 0;
+            const float2 t = make_float2(B[y * 4].x, B[y * 4].z), tm = make_float2(B[ym * 4].x, -B[ym * 4].z);
+            const float2 r = Rb[(size_t)y * M], rm = conjf2(Rb[(size_t)ym * M]);
+            const float2 ta = cadd(t, tm), tb = muli<-1>(csub(t, tm));
+            const float2 ra = cadd(r, rm), rb = muli<-1>(csub(r, rm));
+            float2 pa = cmul(ra, conjf2(ta)), pb = cmul(rb, conjf2(tb));
+            if (y == 0) pa = make_float2(0.f, 0.f);
+            const float2 p = cadd(pa, muli<1>(pb));
+            A[y * 4] = make_float4(0.25f * p.x, 0.f, 0.25f * p.y, 0.f);
+            A[y * 4 + 1] = A[y * 4 + 2] = A[y * 4 + 3] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        __syncthreads();
+        pass4o<N, R1, 1, 1, NT>(A, B, tw);
+        pass4o<N, R2, R1, 1, NT>(B, A, tw);
+        pass4o<N, R3, R1 * R2, 1, NT>(A, B, tw);
+        for (int y = tid; y < N; y += NT) {
+            const float x0 = B[y * 4].x, xm = B[y * 4].z;   // X0 + i XM, both real
             Ob[(size_t)y * M] = make_float2(x0 + xm, x0 - xm);
         }
     }
@@ -362,31 +349,30 @@ __global__ void __launch_bounds__(NT, (NT <= 384 ? 2 : 1))
     static_assert(R1 % 2 == 1 || (R1 & (R1 - 1)) == 0, "first radix odd (or a power-of-two plan)");
     extern __shared__ float4 sm4[];
     float4* A = sm4;                                          // [N][4 pairs]
-    float2* tw = reinterpret_cast<float2*>(sm4 + 4 * N);      // exp(2 pi i m / N)
-    float2* Bt = tw + ((N + 1) & ~1);                         // [N][8]: R^ (k, M-k) of pair s at 2s, 2s+1 (16-B aligned)
+    float4* B4 = sm4 + 4 * N;                                 // [N][4 pairs]: the R^ tile, then the P / inverse buffer
+    float2* Bt = reinterpret_cast<float2*>(B4);               // R^ (k, M-k) of pair s at [y][2s], [y][2s+1]
+    float2* tw = reinterpret_cast<float2*>(sm4 + 8 * N);      // exp(2 pi i m / N)
     __shared__ float2 wk[4];                                  // exp(-2 pi i k / W) of the 4 pairs
     const int tid = threadIdx.x;
     const size_t plane = (size_t)N * M;
     const float2* Zb = Z + (size_t)blockIdx.y * plane;
+    const float2* Rb = Rs + (size_t)blockIdx.y * plane;
     float2* Ob = out + (size_t)blockIdx.y * plane;
     const int npair = M / 2, k0 = 4 * blockIdx.x + 1;
     const bool packed = blockIdx.x == gridDim.x - 1;
 
     if constexpr (MODE == 1) {   // prefetch the R^ tile; waited for before the conjugate product
-        const float2* Rb = Rs + (size_t)blockIdx.y * plane;
         if (!packed) {
             for (int task = tid; task < 8 * N; task += NT) {
                 const int c = task & 7, y = task >> 3, k = k0 + (c >> 1);
                 if (k <= npair) cp_async8(Bt + y * NCOL + c, Rb + (size_t)y * M + ((c & 1) ? M - k : k));
             }
-        } else {
-            for (int y = tid; y < N; y += NT) cp_async8(Bt + y * NCOL, Rb + (size_t)y * M);
+            asm volatile("cp.async.commit_group;" ::: "memory");
         }
-        asm volatile("cp.async.commit_group;" ::: "memory");
     }
     for (int m = tid; m < N; m += NT) tw[m] = kTw<N>.v[m];
     if (packed) {
-        packed_column<N, R1, R2, R3, MODE, NT>(Zb, Bt, Ob, M, A, tw);
+        packed_column<N, R1, R2, R3, MODE, NT>(Zb, Rb, Ob, M, A, B4, tw);
         return;
     }
     if (tid < 4) {
@@ -396,48 +382,56 @@ __global__ void __launch_bounds__(NT, (NT <= 384 ? 2 : 1))
     }
     __syncthreads();
 
-    const int s = tid & 3, k = k0 + s;
+    const int s = tid & 3, k = k0 + s;   // NT % 4 == 0: a thread keeps its pair in every pass
     const bool kv = k <= npair;
     // forward pass 1 + untangle: X[k] = (Z[k] + conj Z[M-k])/2 - (i/2) w_k (Z[k] - conj Z[M-k]),
-    // X[M-k] likewise with w_{M-k} = -conj(w_k)
+    // X[M-k] likewise with w_{M-k} = -conj(w_k).  All of a thread's loads are issued first.
     {
-        constexpr int NTASK = N / R1;
-        static_assert(4 * NTASK <= NT, "one task per thread");
-        const int t = tid >> 2;
-        const bool act = tid < 4 * NTASK;
-        float2 zk[R1], zm[R1];
-        if (act) {
+        constexpr int NTASK = N / R1, KT = (4 * NTASK + NT - 1) / NT;
+        float2 zk[KT][R1], zm[KT][R1];
+#pragma unroll
+        for (int q = 0; q < KT; ++q) {
+            const int tau = tid + q * NT, t = tau >> 2;
+            const bool ld = kv && tau < 4 * NTASK;
             sfor<0, R1>([&](auto j) {
                 const int y = t + decltype(j)::value * NTASK;
-                zk[j] = kv ? Zb[(size_t)y * M + k] : make_float2(0.f, 0.f);
-                zm[j] = kv ? Zb[(size_t)y * M + (M - k)] : make_float2(0.f, 0.f);
+                zk[q][j] = ld ? Zb[(size_t)y * M + k] : make_float2(0.f, 0.f);
+                zm[q][j] = ld ? Zb[(size_t)y * M + (M - k)] : make_float2(0.f, 0.f);
             });
-            const float2 w = wk[s], wm = make_float2(-w.x, w.y);
-            Cp v[R1];
-            sfor<0, R1>([&](auto j) {
-                const float2 sk = cadd(zk[j], conjf2(zm[j])), dk = csub(zk[j], conjf2(zm[j]));
-                const float2 sm_ = cadd(zm[j], conjf2(zk[j])), dm = csub(zm[j], conjf2(zk[j]));
-                const float2 ek = muli<-1>(cmul(w, dk)), em = muli<-1>(cmul(wm, dm));
-                v[j] = {make_float2(0.5f * (sk.x + ek.x), 0.5f * (sm_.x + em.x)),
-                        make_float2(0.5f * (sk.y + ek.y), 0.5f * (sm_.y + em.y))};
-            });
-            Dft<R1, -1>::run(v);
-            sfor<0, R1>([&](auto r) { st4(A, (t * R1 + decltype(r)::value) * 4 + s, v[r]); });
+        }
+        const float2 w = wk[s], wm = make_float2(-w.x, w.y);
+#pragma unroll
+        for (int q = 0; q < KT; ++q) {
+            const int tau = tid + q * NT, t = tau >> 2;
+            if (tau < 4 * NTASK) {
+                Cp v[R1];
+                sfor<0, R1>([&](auto j) {
+                    const float2 a = zk[q][j], c = zm[q][j];
+                    const float2 sk = cadd(a, conjf2(c)), dk = csub(a, conjf2(c));
+                    const float2 sm_ = cadd(c, conjf2(a)), dm = csub(c, conjf2(a));
+                    const float2 ek = muli<-1>(cmul(w, dk)), em = muli<-1>(cmul(wm, dm));
+                    v[j] = {make_float2(0.5f * (sk.x + ek.x), 0.5f * (sm_.x + em.x)),
+                            make_float2(0.5f * (sk.y + ek.y), 0.5f * (sm_.y + em.y))};
+                });
+                Dft<R1, -1>::run(v);
+                sfor<0, R1>([&](auto r) { st4(A, (t * R1 + decltype(r)::value) * 4 + s, v[r]); });
+            }
         }
         __syncthreads();
     }
     pass4<N, R2, R1, -1, NT>(A, tw);
-    // forward pass 3 + (MODE 0) spectrum store / (MODE 1) P = R^ conj(T^), natural order
+    // forward pass 3 + (MODE 0) the spectrum store / (MODE 1) P = R^ conj(T^) in natural
+    // order, written over the R^ tile (each (row, pair) read and written by one thread)
     {
         constexpr int NTASK = N / R3, L = R1 * R2;
-        static_assert(4 * NTASK <= NT, "one task per thread");
-        const int t = tid >> 2;
-        const bool act = tid < 4 * NTASK;
-        Cp v[R3];
-        if (act) sfor<0, R3>([&](auto j) { v[j] = ld4(A, (t + decltype(j)::value * NTASK) * 4 + s); });
-        if constexpr (MODE == 1) asm volatile("cp.async.wait_all;" ::: "memory");
-        __syncthreads();
-        if (act) {
+        if constexpr (MODE == 1) {
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncthreads();
+        }
+        for (int tau = tid; tau < 4 * NTASK; tau += NT) {
+            const int t = tau >> 2;
+            Cp v[R3];
+            sfor<0, R3>([&](auto j) { v[j] = ld4(A, (t + decltype(j)::value * NTASK) * 4 + s); });
             twiddle<N, R3, L, -1>(v, t, tw);
             Dft<R3, -1>::run(v);
             const int base = (t / L) * L * R3 + (t % L);
@@ -452,33 +446,31 @@ __global__ void __launch_bounds__(NT, (NT <= 384 ? 2 : 1))
             } else {
                 sfor<0, R3>([&](auto r) {
                     const int y = base + decltype(r)::value * L;
-                    const float4 q = *reinterpret_cast<const float4*>(Bt + y * NCOL + 2 * s);
+                    const float4 q = B4[y * 4 + s];   // (R^k, R^{M-k})
                     const float2 pk = cmul(make_float2(q.x, q.y), make_float2(v[r].re.x, -v[r].im.x));
                     const float2 pm = cmul(make_float2(q.z, q.w), make_float2(v[r].re.y, -v[r].im.y));
-                    st4(A, y * 4 + s, Cp{make_float2(pk.x, pm.x), make_float2(pk.y, pm.y)});
+                    st4(B4, y * 4 + s, Cp{make_float2(pk.x, pm.x), make_float2(pk.y, pm.y)});
                 });
             }
         }
         if constexpr (MODE == 0) return;
         __syncthreads();
     }
-    // inverse passes 1, 2 ping-pong through the (consumed) R^ tile: A -> Bt -> A
-    float4* B4 = reinterpret_cast<float4*>(Bt);
-    pass4o<N, R1, 1, 1, NT>(A, B4, tw);
-    pass4o<N, R2, R1, 1, NT>(B4, A, tw);
+    // inverse passes 1, 2 out of place: B4 -> A -> B4
+    pass4o<N, R1, 1, 1, NT>(B4, A, tw);
+    pass4o<N, R2, R1, 1, NT>(A, B4, tw);
     // inverse pass 3 + re-tangle + global store:
     // Z'[k] = (X[k] + conj X[M-k]) + i e_k (X[k] - conj X[M-k]), e_k = conj(w_k), e_{M-k} = -w_k
     {
         constexpr int NTASK = N / R3, L = R1 * R2;
-        const int t = tid >> 2;
-        const bool act = tid < 4 * NTASK;
-        if (act) {
+        const float2 w = wk[s], ek = conjf2(w), em = make_float2(-w.x, -w.y);
+        for (int tau = tid; tau < 4 * NTASK; tau += NT) {
+            const int t = tau >> 2;
             Cp v[R3];
-            sfor<0, R3>([&](auto j) { v[j] = ld4(A, (t + decltype(j)::value * NTASK) * 4 + s); });
+            sfor<0, R3>([&](auto j) { v[j] = ld4(B4, (t + decltype(j)::value * NTASK) * 4 + s); });
             twiddle<N, R3, L, 1>(v, t, tw);
             Dft<R3, 1>::run(v);
             const int base = (t / L) * L * R3 + (t % L);
-            const float2 w = wk[s], ek = conjf2(w), em = make_float2(-w.x, -w.y);
             if (kv) {
                 sfor<0, R3>([&](auto r) {
                     const int y = base + decltype(r)::value * L;
@@ -493,12 +485,220 @@ __global__ void __launch_bounds__(NT, (NT <= 384 ? 2 : 1))
     }
 }
 
+// ---------------------------------------------------------------- row kernel
+// The row transforms of length M = W/2 (complex) over packed real rows.  CTA: 8
+// rows as 4 row pairs (the SIMD pairs), in the same [n][4 pairs] float4 layout
+// as the column kernel.  Pass 1 reads global memory (and may loop over tasks),
+// pass 2 runs in place (one task per thread), pass 3 writes global memory.
+//   ROW_FWD_REAL  X [b][H][W] real        -> Z [b][H][M] = FFT_M(x[2m] + i x[2m+1])
+//   ROW_FWD_TPL   K (.) Iq, formed on load (the template of S:305 / R-18, the same
+//                 single fp32 product as prnu_pce_template) -> Z
+//   ROW_INV_PEAK  Z' [b][H][M] -> C [b][H][W] (unnormalised inverse) and the peak /
+//                 energy partials of the CTA's rows: part[b][blockIdx.x]
+enum { ROW_FWD_REAL = 0, ROW_FWD_TPL = 1, ROW_INV_PEAK = 2 };
+struct RowArgs {
+    const float* X;
+    const float* K;
+    int k_batch;
+    const uint8_t* Iq;
+    const float2* Zin;
+    float2* Zout;
+    float* C;
+    PeakE* part;
+    int H, nparts;
+};
+constexpr int ROWS = 8;   // rows per CTA
+
+template <int M, int R1, int R2, int R3>
+constexpr int row_threads() {
+    int t = (4 * M / R2 + 31) / 32 * 32;
+    return t < 128 ? 128 : t;
+}
+template <int M>
+constexpr size_t row_smem_bytes() {
+    return sizeof(float4) * 4 * (size_t)M + sizeof(float2) * ((M + 1) & ~1);
+}
+
+template <int M, int R1, int R2, int R3, int MODE, int NT>
+__global__ void __launch_bounds__(NT, (NT <= 384 ? 2 : 1)) k_pce_rows(RowArgs a) {
+    static_assert(R1 * R2 * R3 == M, "radix plan");
+    static_assert(4 * (M / R2) <= NT, "pass 2: one task per thread");
+    constexpr int S = MODE == ROW_INV_PEAK ? 1 : -1;
+    constexpr int W = 2 * M;
+    extern __shared__ float4 sm4[];
+    float4* A = sm4;
+    float2* tw = reinterpret_cast<float2*>(sm4 + 4 * M);
+    const int tid = threadIdx.x, b = blockIdx.y, H = a.H;
+    for (int m = tid; m < M; m += NT) tw[m] = kTw<M>.v[m];
+    __syncthreads();
+
+    // pass 1 (+ the load): task = 4 t + s, rows ra = r0 + 2s, rb = ra + 1; a thread's
+    // KT tasks issue all their global loads before any is used
+    {
+        constexpr int NTASK = M / R1, KT = (4 * NTASK + NT - 1) / NT;
+        Cp v[KT][R1];
+#pragma unroll
+        for (int q = 0; q < KT; ++q) {
+            const int tau = tid + q * NT, s = tau & 3, t = tau >> 2;
+            const int ra = ROWS * blockIdx.x + 2 * s, rb = ra + 1;
+            const bool va = ra < H && tau < 4 * NTASK, vb = rb < H && tau < 4 * NTASK;
+            sfor<0, R1>([&](auto j) {
+                const int n = t + decltype(j)::value * NTASK;
+                float2 za = make_float2(0.f, 0.f), zb = za;
+                if constexpr (MODE == ROW_FWD_REAL) {
+                    const float* Xb = a.X + (size_t)b * H * W;
+                    if (va) za = *reinterpret_cast<const float2*>(Xb + (size_t)ra * W + 2 * n);
+                    if (vb) zb = *reinterpret_cast<const float2*>(Xb + (size_t)rb * W + 2 * n);
+                } else if constexpr (MODE == ROW_FWD_TPL) {
+                    const float* Kb = a.K + (a.k_batch == 1 ? 0 : (size_t)b * H * W);
+                    const uint8_t* Ib = a.Iq + (size_t)b * H * W;
+                    if (va) {
+                        const float2 k = *reinterpret_cast<const float2*>(Kb + (size_t)ra * W + 2 * n);
+                        const uchar2 c = *reinterpret_cast<const uchar2*>(Ib + (size_t)ra * W + 2 * n);
+                        za = make_float2(k.x * (float)c.x, k.y * (float)c.y);
+                    }
+                    if (vb) {
+                        const float2 k = *reinterpret_cast<const float2*>(Kb + (size_t)rb * W + 2 * n);
+                        const uchar2 c = *reinterpret_cast<const uchar2*>(Ib + (size_t)rb * W + 2 * n);
+                        zb = make_float2(k.x * (float)c.x, k.y * (float)c.y);
+                    }
+                } else {
+                    const float2* Zb = a.Zin + (size_t)b * H * M;
+                    if (va) za = Zb[(size_t)ra * M + n];
+                    if (vb) zb = Zb[(size_t)rb * M + n];
+                }
+                v[q][j] = {make_float2(za.x, zb.x), make_float2(za.y, zb.y)};
+            });
+        }
+#pragma unroll
+        for (int q = 0; q < KT; ++q) {
+            const int tau = tid + q * NT, s = tau & 3, t = tau >> 2;
+            if (tau < 4 * NTASK) {
+                Dft<R1, S>::run(v[q]);
+                sfor<0, R1>([&](auto r) { st4(A, (t * R1 + decltype(r)::value) * 4 + s, v[q][r]); });
+            }
+        }
+        __syncthreads();
+    }
+    pass4<M, R2, R1, S, NT>(A, tw);
+    // pass 3 (+ the store / the peak and energy partials)
+    {
+        constexpr int NTASK = M / R3, L = R1 * R2;
+        // per-thread candidates: one running max per row of the pair (its indices
+        // increase with n, so strict > keeps the smallest index), energy in fp32 pairs
+        float besta = -1.f, bestb = -1.f;
+        int bia = -1, bib = -1;
+        float2 ea = make_float2(0.f, 0.f), eb = ea;
+        for (int tau = tid; tau < 4 * NTASK; tau += NT) {
+            const int s = tau & 3, t = tau >> 2;
+            const int ra = ROWS * blockIdx.x + 2 * s, rb = ra + 1;
+            const bool va = ra < H, vb = rb < H;
+            Cp v[R3];
+            sfor<0, R3>([&](auto j) { v[j] = ld4(A, (t + decltype(j)::value * NTASK) * 4 + s); });
+            twiddle<M, R3, L, S>(v, t, tw);
+            Dft<R3, S>::run(v);
+            const int base = (t / L) * L * R3 + (t % L);
+            sfor<0, R3>([&](auto r) {
+                const int n = base + decltype(r)::value * L;
+                const float2 ca = make_float2(v[r].re.x, v[r].im.x), cb = make_float2(v[r].re.y, v[r].im.y);
+                if constexpr (MODE == ROW_INV_PEAK) {
+                    float* Cb = a.C + (size_t)b * H * W;
+                    if (va) {
+                        *reinterpret_cast<float2*>(Cb + (size_t)ra * W + 2 * n) = ca;
+                        const float m0 = fabsf(ca.x), m1 = fabsf(ca.y);
+                        if (m0 > besta) { besta = m0; bia = ra * W + 2 * n; }
+                        if (m1 > besta) { besta = m1; bia = ra * W + 2 * n + 1; }
+                        ea = fma2(ca, ca, ea);
+                    }
+                    if (vb) {
+                        *reinterpret_cast<float2*>(Cb + (size_t)rb * W + 2 * n) = cb;
+                        const float m0 = fabsf(cb.x), m1 = fabsf(cb.y);
+                        if (m0 > bestb) { bestb = m0; bib = rb * W + 2 * n; }
+                        if (m1 > bestb) { bestb = m1; bib = rb * W + 2 * n + 1; }
+                        eb = fma2(cb, cb, eb);
+                    }
+                } else {
+                    float2* Zb = a.Zout + (size_t)b * H * M;
+                    if (va) Zb[(size_t)ra * M + n] = ca;
+                    if (vb) Zb[(size_t)rb * M + n] = cb;
+                }
+            });
+        }
+        float best = besta;
+        int bi = bia;
+        if (better(bestb, bib, best, bi)) {
+            best = bestb;
+            bi = bib;
+        }
+        double e = ((double)ea.x + (double)ea.y) + ((double)eb.x + (double)eb.y);
+        if constexpr (MODE == ROW_INV_PEAK) {
+            // fixed-shape warp-shuffle reduction, then the NT/32 warp results in warp order
+            constexpr int NW = NT / 32;
+            __shared__ float sa[NW];
+            __shared__ int si[NW];
+            __shared__ double se[NW];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const float a2 = __shfl_xor_sync(0xffffffffu, best, o);
+                const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (better(a2, i2, best, bi)) {
+                    best = a2;
+                    bi = i2;
+                }
+            }
+            e = warp_sum(e);
+            if ((tid & 31) == 0) {
+                sa[tid >> 5] = best;
+                si[tid >> 5] = bi;
+                se[tid >> 5] = e;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                float bb = sa[0];
+                int ii = si[0];
+                double ee = se[0];
+                for (int k = 1; k < NW; ++k) {
+                    if (better(sa[k], si[k], bb, ii)) {
+                        bb = sa[k];
+                        ii = si[k];
+                    }
+                    ee += se[k];
+                }
+                a.part[(size_t)b * a.nparts + blockIdx.x] = PeakE{bb, ii, ee};
+            }
+        }
+    }
+}
+
+template <int M, int R1, int R2, int R3>
+static int launch_rows_t(int mode, const RowArgs& a, int batch, cudaStream_t st) {
+    constexpr int NT = row_threads<M, R1, R2, R3>();
+    static DeviceFlags d0, d1, d2;
+    const size_t sm = row_smem_bytes<M>();
+    dim3 grid((a.H + ROWS - 1) / ROWS, batch);
+    const void* fn = mode == ROW_FWD_REAL ? (const void*)k_pce_rows<M, R1, R2, R3, ROW_FWD_REAL, NT>
+                     : mode == ROW_FWD_TPL ? (const void*)k_pce_rows<M, R1, R2, R3, ROW_FWD_TPL, NT>
+                                           : (const void*)k_pce_rows<M, R1, R2, R3, ROW_INV_PEAK, NT>;
+    if (int rc = set_smem_attr(fn, sm, mode == ROW_FWD_REAL ? d0 : mode == ROW_FWD_TPL ? d1 : d2)) return rc;
+    {
+        KTimer kt(mode == ROW_INV_PEAK ? "pce_rows_inv" : "pce_rows_fwd", st);
+        if (mode == ROW_FWD_REAL)
+            k_pce_rows<M, R1, R2, R3, ROW_FWD_REAL, NT><<<grid, NT, sm, st>>>(a);
+        else if (mode == ROW_FWD_TPL)
+            k_pce_rows<M, R1, R2, R3, ROW_FWD_TPL, NT><<<grid, NT, sm, st>>>(a);
+        else
+            k_pce_rows<M, R1, R2, R3, ROW_INV_PEAK, NT><<<grid, NT, sm, st>>>(a);
+    }
+    count_launch();
+    return check_launch("k_pce_rows");
+}
+
 template <int N, int R1, int R2, int R3>
 static int launch_cols(int mode, const float2* Z, const float2* Rs, float2* out, int M, int W, int batch,
                        cudaStream_t st) {
     constexpr int NT = threads<N, R1, R2, R3>();
     static DeviceFlags done0, done1;
-    const size_t sm = smem_bytes_f<N>(mode);
+    const size_t sm = smem_bytes_f<N>();
     const void* fn =
         mode ? (const void*)k_pce_cols_f<N, R1, R2, R3, 1, NT> : (const void*)k_pce_cols_f<N, R1, R2, R3, 0, NT>;
     if (int rc = set_smem_attr(fn, sm, mode ? done1 : done0)) return rc;
@@ -519,16 +719,51 @@ static int launch_cols(int mode, const float2* Z, const float2* Rs, float2* out,
 // Heights with a compiled radix plan (the PCE plan uses the 2-D cuFFT path otherwise).
 #define PRNU_PCE_COL_PLANS(X) \
     X(720, 9, 8, 10)          \
-    X(1080, 15, 8, 9)         \
+    X(1080, 9, 15, 8)         \
     X(500, 5, 10, 10)         \
-    X(480, 5, 6, 16)          \
+    X(480, 5, 16, 6)          \
     X(128, 8, 4, 4)           \
     X(125, 5, 5, 5)           \
-    X(96, 3, 4, 8)            \
+    X(96, 3, 8, 4)            \
     X(64, 4, 4, 4)            \
     X(48, 3, 4, 4)            \
     X(45, 3, 3, 5)            \
     X(27, 3, 3, 3)
+
+// Row lengths M = W/2 with a compiled radix plan (first radix odd: stride-R1 stores).
+#define PRNU_PCE_ROW_PLANS(X) \
+    X(640, 5, 16, 8)          \
+    X(960, 15, 8, 8)          \
+    X(250, 5, 5, 10)          \
+    X(125, 5, 5, 5)           \
+    X(96, 3, 4, 8)            \
+    X(80, 5, 4, 4)            \
+    X(30, 3, 2, 5)            \
+    X(27, 3, 3, 3)            \
+    X(20, 5, 2, 2)
+
+bool pce_rows_supported(int W) {
+    if (W % 2) return false;
+#define PRNU_X(n, a, b, c) \
+    if (W / 2 == n) return true;
+    PRNU_PCE_ROW_PLANS(PRNU_X)
+#undef PRNU_X
+    return false;
+}
+
+int pce_rows_nparts(int H) { return (H + fft::ROWS - 1) / fft::ROWS; }
+
+// mode 0: X -> Z;  1: K (.) Iq -> Z;  2: Z -> C + partials
+int launch_pce_rows(int mode, const float* X, const float* K, int k_batch, const uint8_t* Iq, const void* Zin,
+                    void* Zout, float* C, void* part, int H, int W, int batch, cudaStream_t st) {
+    fft::RowArgs a{X, K, k_batch, Iq, reinterpret_cast<const float2*>(Zin), reinterpret_cast<float2*>(Zout), C,
+                   reinterpret_cast<PeakE*>(part), H, pce_rows_nparts(H)};
+#define PRNU_X(n, r1, r2, r3) \
+    if (W / 2 == n) return fft::launch_rows_t<n, r1, r2, r3>(mode, a, batch, st);
+    PRNU_PCE_ROW_PLANS(PRNU_X)
+#undef PRNU_X
+    return fail(PRNU_INVALID_ARG, "pce rows: no radix plan for this width");
+}
 
 bool pce_cols_supported(int H) {
 #define PRNU_X(n, a, b, c) \

@@ -491,6 +491,29 @@ def test_pce_cached_residual_spectrum_bit_identical(prnu):
         assert torch.equal(got.pce, r.pce) and torch.equal(got.peak_y, r.peak_y) and torch.equal(got.peak, r.peak)
 
 
+@pytest.mark.parametrize("H,W", [(720, 1280), (96, 160), (45, 62), (27, 53)])
+def test_pce_cached_template_bit_identical(prnu, H, W):
+    """prnu_pce_cached_template (the template K (.) Iq formed inside the row transform,
+    or staged on the cuFFT paths) gives the bits of prnu_pce_cached(prnu_pce_template);
+    both agree with the oracle.  Sizes: fused rows + columns, cuFFT rows + columns,
+    2-D cuFFT (odd W)."""
+    b = 2
+    g = np.random.default_rng(H + W)
+    I = torch.from_numpy(g.integers(0, 256, (b, H, W), dtype=np.uint8)).cuda()
+    K = torch.from_numpy(g.normal(0, 0.02, (H, W)).astype(np.float32)).cuda()
+    R = prnu.residual(I, zero_mean=True)
+    plan = prnu.PcePlan(H, W, b)
+    plan.set_residual(R)
+    ref = plan.match(prnu.pce_template(K, I))
+    got = plan.match_template(K, I)
+    assert torch.equal(got.pce, ref.pce) and torch.equal(got.peak_y, ref.peak_y) and torch.equal(got.peak, ref.peak)
+    if H * W <= 96 * 160:
+        for i in range(b):
+            Tn = oracle.pce_template(K.cpu().numpy(), I[i].cpu().numpy())
+            p_ref = oracle.pce(R[i].cpu().numpy().astype(np.float64), Tn)[0]
+            assert abs(got.pce[i].item() - p_ref) <= PCE_RTOL * abs(p_ref) + 1e-6
+
+
 def test_camera_batch_extractor_matches_single(prnu):
     """Cameras dealt over several streams give each camera's single-stream fingerprint."""
     vids = [_rand_frames(20, 64, 96, 40 + c).cuda() for c in range(5)]
@@ -545,6 +568,18 @@ def test_residual_short_deep_levels(prnu, H, W):
         for i in range(2):
             ref = oracle.residual(src[i].cpu().numpy().astype(np.float32))
             assert np.abs(got[i] - ref).max() <= W_TOL
+
+
+@pytest.mark.parametrize("B,H,W,kb", [(3, 720, 1280, 1), (2, 45, 62, 2), (2, 7, 9, 1)])
+def test_pce_template_bit_exact(prnu, B, H, W, kb):
+    """S:305 / R-18: T = K (.) (float)Iq, one fp32 product per pixel: bit-exact against
+    numpy for the 4-pixel vector path (P % 4 == 0) and the scalar path (odd P)."""
+    g = np.random.default_rng(H + W)
+    K = g.normal(0, 0.01, (kb, H, W)).astype(np.float32)
+    I = g.integers(0, 256, (B, H, W), dtype=np.uint8)
+    got = prnu.pce_template(torch.from_numpy(K[0] if kb == 1 else K).cuda(), torch.from_numpy(I).cuda()).cpu().numpy()
+    want = (K if kb > 1 else K[[0] * B]) * I.astype(np.float32)
+    assert got.shape == (B, H, W) and np.array_equal(got.view(np.uint32), want.view(np.uint32))
 
 
 @pytest.mark.parametrize("H,W", [(45, 60), (27, 54), (125, 250), (64, 2), (2, 16), (48, 40), (48, 54), (45, 62),

@@ -51,6 +51,7 @@ T = prnu.pce_template(Ks[0], Iq)
 print("64x64 PCE        %.2f ms" % timed(lambda: [plan(R, T) for c in range(n)]))
 plan.set_residual(R)
 print("64x64 PCE cached %.2f ms" % timed(lambda: [plan.match(T) for c in range(n)]))
+print("64x64 PCE cached, fused templates %.2f ms" % timed(lambda: [plan.match_template(Ks[c], Iq) for c in range(n)]))
 prnu._lib.prnu_profile_begin()
 plan(R, T)
 torch.cuda.synchronize()
