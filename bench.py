@@ -467,21 +467,20 @@ def main():
         fr4 = synth.video("drift", 301, c4H, c4W, seed=4, camera=0, device=dev).frames
         ex4 = prnu.CameraBatchExtractor(c4H, c4W, 30, 10, streams=8, device=dev)
         Iq4 = fr4[300:301].expand(c4n, c4H, c4W).contiguous()
-        plan4 = prnu.PcePlan(c4H, c4W, c4n, device=dev)
+        pm4 = prnu.PceMatrix(c4H, c4W, c4n, streams=4, device=dev)
 
         def camera_id():
             Ks4 = ex4([fr4[:300]] * c4n)
             R4 = prnu.residual(Iq4, zero_mean=True)
-            plan4.set_residual(R4)   # one FFT of the 64 query residuals for all 64 fingerprints
-            for c in range(c4n):
-                plan4.match_template(Ks4[c], Iq4)   # template K (.) Iq formed inside the row FFT
+            pm4.set_queries(R4, Iq4)   # one FFT of the 64 query residuals per stream plan
+            pm4(Ks4)                   # 64 x 64 PCEs, templates K (.) Iq formed inside the row FFT
         t_c4 = timed(camera_id, reps=1)
         c4 = {"workload": "64 x 300 frames 1280x720, depth 30, 64x64 PCE", "ms": t_c4,
               "fingerprints_per_s": c4n / (t_c4 / 1000.0), "pce_per_s": c4n * c4n / (t_c4 / 1000.0)}
         # BASELINE config 5: one 1920x1080 stack of 3600 frames ("shift" model), depths
         # 1 .. 3600: per depth the fingerprint time, denoised frames/s, % HBM (SDA read +
         # denoise traffic) and NCC against the true K
-        del fr4, Iq4, plan4, ex4
+        del fr4, Iq4, pm4, ex4
         torch.cuda.empty_cache()
         v5 = synth.video("shift", 3600, H, W, seed=5, device=dev)
         c5 = {}

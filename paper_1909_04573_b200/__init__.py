@@ -650,7 +650,8 @@ class PceResult:
 
 
 class PcePlan:
-    """cuFFT plans + workspace for [batch][H][W] residual/template pairs."""
+    """PCE plan (the library's row / column FFT kernels, or cuFFT where a size has no
+    radix plan) + workspace for [batch][H][W] residual/template pairs."""
 
     def __init__(self, H: int, W: int, batch: int = 1, device="cuda"):
         self.H, self.W, self.batch = H, W, batch
@@ -732,6 +733,46 @@ class PcePlan:
             with torch.cuda.device(self.device):
                 _lib.prnu_pce_plan_destroy(h)
             self._h = None
+
+
+class PceMatrix:
+    """Camera identification (BASELINE config 4): the PCE of `batch` query residuals
+    against the templates K_c (.) Iq of many fingerprints K_c.  One PcePlan per stream,
+    each holding the cached query-residual spectrum; fingerprints are dealt
+    round-robin over the streams so consecutive fingerprints' kernels overlap."""
+
+    def __init__(self, H: int, W: int, batch: int, streams: int = 4, device="cuda"):
+        device = _cuda_device(device)
+        self.H, self.W, self.batch, self.device = H, W, batch, device
+        self.plans = [PcePlan(H, W, batch, device) for _ in range(streams)]
+        self.streams = [torch.cuda.Stream(device=device) for _ in range(streams)]
+        self.Iq = None
+
+    @_on_device
+    def set_queries(self, R: torch.Tensor, Iq: torch.Tensor):
+        """R: zero-mean query residuals fp32 [batch][H][W]; Iq: the query frames u8."""
+        for p in self.plans:
+            p.set_residual(R)
+        self.Iq = Iq
+
+    @_on_device
+    def __call__(self, Ks, exclusion_half: int = 5) -> PceResult:
+        """Ks: a sequence of fp32 [H][W] fingerprints (or [n][H][W]); returns PceResult
+        fields of shape [n][batch] (row c: fingerprint c against every query)."""
+        if self.Iq is None:
+            raise RuntimeError("set_queries first")
+        cur = torch.cuda.current_stream()
+        for s_ in self.streams:
+            s_.wait_stream(cur)
+        res = []
+        for c in range(len(Ks)):
+            j = c % len(self.plans)
+            with torch.cuda.stream(self.streams[j]):
+                res.append(self.plans[j].match_template(Ks[c], self.Iq, exclusion_half))
+        for s_ in self.streams:
+            cur.wait_stream(s_)
+        return PceResult(torch.stack([r.pce for r in res]), torch.stack([r.peak_y for r in res]),
+                         torch.stack([r.peak_x for r in res]), torch.stack([r.peak for r in res]))
 
 
 class WdftPlan:

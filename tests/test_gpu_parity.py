@@ -514,6 +514,25 @@ def test_pce_cached_template_bit_identical(prnu, H, W):
             assert abs(got.pce[i].item() - p_ref) <= PCE_RTOL * abs(p_ref) + 1e-6
 
 
+def test_pce_matrix_matches_single_plan(prnu):
+    """PceMatrix (plans dealt over streams) gives, row by row, the bits of one plan's
+    match_template for each fingerprint."""
+    H, W, b, n = 96, 160, 3, 5
+    g = np.random.default_rng(11)
+    I = torch.from_numpy(g.integers(0, 256, (b, H, W), dtype=np.uint8)).cuda()
+    Ks = torch.from_numpy(g.normal(0, 0.02, (n, H, W)).astype(np.float32)).cuda()
+    R = prnu.residual(I, zero_mean=True)
+    pm = prnu.PceMatrix(H, W, b, streams=3)
+    pm.set_queries(R, I)
+    got = pm(Ks)
+    plan = prnu.PcePlan(H, W, b)
+    plan.set_residual(R)
+    for c in range(n):
+        ref = plan.match_template(Ks[c], I)
+        assert torch.equal(got.pce[c], ref.pce) and torch.equal(got.peak_y[c], ref.peak_y)
+        assert torch.equal(got.peak[c], ref.peak)
+
+
 def test_camera_batch_extractor_matches_single(prnu):
     """Cameras dealt over several streams give each camera's single-stream fingerprint."""
     vids = [_rand_frames(20, 64, 96, 40 + c).cuda() for c in range(5)]

@@ -64,3 +64,22 @@ nk = ctypes.c_int()
 prnu._lib.prnu_profile_end(maxk, names, tot, cnt, ctypes.byref(nk))
 for k in range(nk.value):
     print("   ", names.raw[64 * k: 64 * k + 64].split(b"\0")[0].decode(), "%.3f ms" % tot[k], cnt[k])
+
+# concurrent plans: cameras dealt over streams, one plan (and cached residual spectrum) per stream
+for nst in (2, 3, 4):
+    plans = [prnu.PcePlan(H, W, n) for _ in range(nst)]
+    for p_ in plans:
+        p_.set_residual(R)
+    streams = [torch.cuda.Stream() for _ in range(nst)]
+
+    def multi():
+        cur = torch.cuda.current_stream()
+        for s_ in streams:
+            s_.wait_stream(cur)
+        for c in range(n):
+            with torch.cuda.stream(streams[c % nst]):
+                plans[c % nst].match_template(Ks[c], Iq)
+        for s_ in streams:
+            cur.wait_stream(s_)
+    print("64x64 PCE cached, fused templates, %d streams %.2f ms" % (nst, timed(multi)))
+    del plans
