@@ -361,17 +361,21 @@ __global__ void __launch_bounds__(NT, (NT <= 384 ? 2 : 1))
     const int npair = M / 2, k0 = 4 * blockIdx.x + 1;
     const bool packed = blockIdx.x == gridDim.x - 1;
 
-    if constexpr (MODE == 1) {   // prefetch the R^ tile; waited for before the conjugate product
+    // async copies: group 0 = the twiddle table (waited for before forward pass 2),
+    // group 1 = the R^ tile (match; waited for before the conjugate product)
+    for (int m = tid; m < N; m += NT) cp_async8(tw + m, &kTw<N>.v[m]);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    if constexpr (MODE == 1) {
         if (!packed) {
             for (int task = tid; task < 8 * N; task += NT) {
                 const int c = task & 7, y = task >> 3, k = k0 + (c >> 1);
                 if (k <= npair) cp_async8(Bt + y * NCOL + c, Rb + (size_t)y * M + ((c & 1) ? M - k : k));
             }
-            asm volatile("cp.async.commit_group;" ::: "memory");
         }
+        asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    for (int m = tid; m < N; m += NT) tw[m] = kTw<N>.v[m];
     if (packed) {
+        asm volatile("cp.async.wait_all;" ::: "memory");
         packed_column<N, R1, R2, R3, MODE, NT>(Zb, Rb, Ob, M, A, B4, tw);
         return;
     }
@@ -417,6 +421,10 @@ __global__ void __launch_bounds__(NT, (NT <= 384 ? 2 : 1))
                 sfor<0, R1>([&](auto r) { st4(A, (t * R1 + decltype(r)::value) * 4 + s, v[r]); });
             }
         }
+        if constexpr (MODE == 1)
+            asm volatile("cp.async.wait_group 1;" ::: "memory");   // the twiddles (the R^ tile may still fly)
+        else
+            asm volatile("cp.async.wait_all;" ::: "memory");
         __syncthreads();
     }
     pass4<N, R2, R1, -1, NT>(A, tw);
@@ -529,8 +537,8 @@ __global__ void __launch_bounds__(NT, (NT <= 384 ? 2 : 1)) k_pce_rows(RowArgs a)
     float4* A = sm4;
     float2* tw = reinterpret_cast<float2*>(sm4 + 4 * M);
     const int tid = threadIdx.x, b = blockIdx.y, H = a.H;
-    for (int m = tid; m < M; m += NT) tw[m] = kTw<M>.v[m];
-    __syncthreads();
+    for (int m = tid; m < M; m += NT) cp_async8(tw + m, &kTw<M>.v[m]);   // waited for before pass 2
+    asm volatile("cp.async.commit_group;" ::: "memory");
 
     // pass 1 (+ the load): task = 4 t + s, rows ra = r0 + 2s, rb = ra + 1; a thread's
     // KT tasks issue all their global loads before any is used
@@ -578,6 +586,7 @@ __global__ void __launch_bounds__(NT, (NT <= 384 ? 2 : 1)) k_pce_rows(RowArgs a)
                 sfor<0, R1>([&](auto r) { st4(A, (t * R1 + decltype(r)::value) * 4 + s, v[q][r]); });
             }
         }
+        asm volatile("cp.async.wait_all;" ::: "memory");
         __syncthreads();
     }
     pass4<M, R2, R1, S, NT>(A, tw);
