@@ -77,9 +77,12 @@ struct SynthArgs {
 // exact sequence as the analysis (sda_div), so both kernels see the oracle's fp32 S.
 // Per-pixel order is ascending frame order.
 constexpr int SA_STAGE_COEF = 4 * SC_PS;           // floats per stage (4 planes)
-// L/H plane pitch: 40 == 8 mod 32 makes the row pass's LDS.128 (8 lanes: rows 4w+(l&3),
-// columns 4 (l>>2)) conflict-free; the column pass stores consecutive columns (any pitch)
-constexpr int SA_LP = 40;
+// L/H plane pitch.  The row pass maps lane l to row 4w + (l >> 3), column group l & 7, so
+// its LDS.128 (8 lanes: one row, 128 contiguous bytes) and the I-tile loads (a half-warp:
+// two 64-byte rows) are conflict-free at any pitch; 36 (== 4 mod 32) spreads the column
+// pass's halo items (coefficient columns 32 .. 35 of 4-row groups sg, one warp: banks
+// 16 sg + k) over 8 banks (4-way) where 40 put them on 4 (7-way).
+constexpr int SA_LP = 36;
 template <int TY, typename TI, int MODE = 1>
 constexpr size_t sacc_smem_bytes() {
     return 2 * SA_STAGE_COEF * sizeof(float) + (MODE ? 3 * TY * ST_X * sizeof(TI) : 0) +
@@ -134,9 +137,9 @@ __global__ void __launch_bounds__(256, 4) k_synth_acc2(const __grid_constant__ S
         if (nb > 1) issue(1);
     }
 
-    // row pass / accumulate mapping: warp w rows 4w .. 4w+3, lane -> (row 4w + (lane & 3), 8 columns at 8 (lane >> 2))
+    // row pass / accumulate mapping: warp w rows 4w .. 4w+3, lane -> (row 4w + (lane >> 3), 8 columns at 8 (lane & 7))
     const int lane = tid & 31, warp = tid >> 5;
-    const int rt = 4 * warp + (lane & 3), rg = lane >> 2;
+    const int rt = 4 * warp + (lane >> 3), rg = lane & 7;
     const int gy = ty0 + rt, gx = tx0 + 8 * rg;
     const bool rowact = rt < TY;            // warp-uniform: the last warp idles in the row pass when TY = 28
     const bool rowok = rowact && gy < a.NH;
