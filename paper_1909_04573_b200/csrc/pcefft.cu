@@ -262,14 +262,14 @@ __device__ __forceinline__ void pass4(float4* __restrict__ A, const float2* __re
     const bool act = tau < 4 * NTASK;
     Cp v[R];
     if (act) sfor<0, R>([&](auto j) { v[j] = ld4(A, (t + decltype(j)::value * NTASK) * 4 + s); });
-    __syncthreads();
+    __syncthreads(); PRNU_STRESS(41);
     if (act) {
         twiddle<N, R, L, S>(v, t, tw);
         Dft<R, S>::run(v);
         const int base = (t / L) * L * R + (t % L);
         sfor<0, R>([&](auto r) { st4(A, (base + decltype(r)::value * L) * 4 + s, v[r]); });
     }
-    __syncthreads();
+    __syncthreads(); PRNU_STRESS(42);
 }
 
 // out-of-place variant (no barrier between the loads and the stores)
@@ -286,7 +286,7 @@ __device__ __forceinline__ void pass4o(const float4* __restrict__ A, float4* __r
         const int base = (t / L) * L * R + (t % L);
         sfor<0, R>([&](auto r) { st4(B, (base + decltype(r)::value * L) * 4 + s, v[r]); });
     }
-    __syncthreads();
+    __syncthreads(); PRNU_STRESS(43);
 }
 
 template <int N>
@@ -308,7 +308,7 @@ __device__ __forceinline__ void packed_column(const float2* __restrict__ Zb, con
         A[y * 4] = make_float4(z0.x + z0.y, 0.f, z0.x - z0.y, 0.f);
         A[y * 4 + 1] = A[y * 4 + 2] = A[y * 4 + 3] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    __syncthreads();
+    __syncthreads(); PRNU_STRESS(44);
     pass4o<N, R1, 1, -1, NT>(A, B, tw);
     pass4o<N, R2, R1, -1, NT>(B, A, tw);
     pass4o<N, R3, R1 * R2, -1, NT>(A, B, tw);
@@ -328,7 +328,7 @@ __device__ __forceinline__ void packed_column(const float2* __restrict__ Zb, con
             A[y * 4] = make_float4(0.25f * p.x, 0.f, 0.25f * p.y, 0.f);
             A[y * 4 + 1] = A[y * 4 + 2] = A[y * 4 + 3] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        __syncthreads();
+        __syncthreads(); PRNU_STRESS(45);
         pass4o<N, R1, 1, 1, NT>(A, B, tw);
         pass4o<N, R2, R1, 1, NT>(B, A, tw);
         pass4o<N, R3, R1 * R2, 1, NT>(A, B, tw);
@@ -384,7 +384,7 @@ __global__ void __launch_bounds__(NT, (NT <= 384 ? 2 : 1))
         sincospi(-2.0 * (k0 + tid) / W, &sn, &cs);
         wk[tid] = make_float2((float)cs, (float)sn);
     }
-    __syncthreads();
+    __syncthreads(); PRNU_STRESS(46);
 
     const int s = tid & 3, k = k0 + s;   // NT % 4 == 0: a thread keeps its pair in every pass
     const bool kv = k <= npair;
@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(NT, (NT <= 384 ? 2 : 1))
             asm volatile("cp.async.wait_group 1;" ::: "memory");   // the twiddles (the R^ tile may still fly)
         else
             asm volatile("cp.async.wait_all;" ::: "memory");
-        __syncthreads();
+        __syncthreads(); PRNU_STRESS(47);
     }
     pass4<N, R2, R1, -1, NT>(A, tw);
     // forward pass 3 + (MODE 0) the spectrum store / (MODE 1) P = R^ conj(T^) in natural
@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(NT, (NT <= 384 ? 2 : 1))
         constexpr int NTASK = N / R3, L = R1 * R2;
         if constexpr (MODE == 1) {
             asm volatile("cp.async.wait_all;" ::: "memory");
-            __syncthreads();
+            __syncthreads(); PRNU_STRESS(48);
         }
         for (int tau = tid; tau < 4 * NTASK; tau += NT) {
             const int t = tau >> 2;
@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(NT, (NT <= 384 ? 2 : 1))
             }
         }
         if constexpr (MODE == 0) return;
-        __syncthreads();
+        __syncthreads(); PRNU_STRESS(49);
     }
     // inverse passes 1, 2 out of place: B4 -> A -> B4
     pass4o<N, R1, 1, 1, NT>(B4, A, tw);
@@ -587,7 +587,7 @@ __global__ void __launch_bounds__(NT, (NT <= 384 ? 2 : 1)) k_pce_rows(RowArgs a)
             }
         }
         asm volatile("cp.async.wait_all;" ::: "memory");
-        __syncthreads();
+        __syncthreads(); PRNU_STRESS(50);
     }
     pass4<M, R2, R1, S, NT>(A, tw);
     // pass 3 (+ the store / the peak and energy partials)
@@ -661,7 +661,7 @@ __global__ void __launch_bounds__(NT, (NT <= 384 ? 2 : 1)) k_pce_rows(RowArgs a)
                 si[tid >> 5] = bi;
                 se[tid >> 5] = e;
             }
-            __syncthreads();
+            __syncthreads(); PRNU_STRESS(51);
             if (tid == 0) {
                 float bb = sa[0];
                 int ii = si[0];

@@ -51,6 +51,27 @@ r = prnu.pce(R, T)
 out["pce"], out["pce_y"], out["pce_x"] = r.pce, r.peak_y, r.peak_x
 pb, nb = prnu.block_match(R[0], T[0], 100)
 out["blk_pce"], out["blk_ncc"] = pb, nb
+# the PCE row / column FFT kernels (pcefft.cu): 720p cached + fused templates, H = 96 with
+# a row plan, H = 45 with cuFFT rows, 500 x 500 block tiles
+Iq = u8(3, 720, 1280)
+Kq = torch.randn(720, 1280, device=dev, generator=g) * 0.02
+Rq = prnu.residual(Iq, zero_mean=True)
+plan = prnu.PcePlan(720, 1280, 3)
+plan.set_residual(Rq)
+r = plan.match_template(Kq, Iq)
+out["pce720_t"], out["pce720_t_peak"] = r.pce, r.peak
+r = plan.match(prnu.pce_template(Kq, Iq))
+out["pce720_c"] = r.peak
+for (H2, W2) in ((96, 160), (45, 60)):
+    I2 = u8(2, H2, W2)
+    R2 = prnu.residual(I2.float(), zero_mean=True)
+    r = prnu.pce(R2, prnu.pce_template(Kq[:H2, :W2].contiguous(), I2))
+    out[f"pce_{H2}x{W2}"] = r.peak
+Ib = u8(1, 1000, 1000)
+Rb = prnu.residual(Ib, zero_mean=True)[0]
+Kb = torch.randn(1000, 1000, device=dev, generator=g) * 0.02
+pb, nb = prnu.block_match(Rb, prnu.pce_template(Kb, Ib)[0], 500)
+out["blk500_pce"], out["blk500_ncc"] = pb, nb
 out["wdft"] = prnu.wdft(torch.stack([out["fp_d3_K"], out["fp_d1_K"]]))
 for taps, bnd, tr in ((16, 0, 0), (8, 1, 0), (8, 1, 1)):
     out[f"var_{taps}_{bnd}_{tr}"] = prnu.residual_variant(u8(2, 40, 52).float(), prnu.DenoiseVariant(taps, bnd, tr))
