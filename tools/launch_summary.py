@@ -16,10 +16,10 @@ for r in rows[1:]:
     v = float(r[vi].replace(",", ""))
     scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
     name = r[ki]
-    if "prnu::" not in name and "splitk::" not in name:
+    if not any(t in name for t in ("prnu::", "splitk::", "fft::k_pce")):   # ncu prints prnu::fft:: as fft::
         other += v * scale
         continue
-    short = name.split("(")[0].replace("void ", "").replace("prnu::", "").replace("splitk::", "")
+    short = name.split("(")[0].replace("void ", "").replace("prnu::", "").replace("splitk::", "").replace("fft::", "")
     tot[short] += v * scale
     cnt[short] += 1
 T = sum(tot.values())

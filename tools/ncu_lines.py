@@ -18,13 +18,18 @@ ops = collections.defaultdict(collections.Counter)
 src = {}
 hdr = None
 T = 0
+fn = None
+cur = None
 for r in rows:
+    if len(r) >= 2 and r[0] == "Function Name":   # the first kernel only (a report can hold several)
+        if fn is not None and r[1] != fn:
+            break
+        fn = r[1]
+        continue
     if len(r) >= 2 and r[0] == "File Path":
         fname = r[1].split("/")[-1]
         continue
     if len(r) > 3 and r[0] == "Line No":
-        if hdr is not None and T > 0 and len(sys.argv) > 4:
-            break
         hdr = r
         continue
     if hdr is None or len(r) != len(hdr):
@@ -39,7 +44,7 @@ for r in rows:
         T += n
         continue
     m = re.match(r"\s*(@!?U?P\w+\s+)?([A-Z0-9_]+)", sass)
-    if m:
+    if m and cur is not None:
         ops[cur][m.group(2)] += n
 print("total", T)
 for key, n in cnt.most_common(top):
