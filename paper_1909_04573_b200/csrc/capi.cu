@@ -140,9 +140,10 @@ int launch_pad_rows_u8(const uint8_t* src, long long nb, int H, int W, long long
 int launch_accumulate(const float* W, const float* I, int batch, long long P, double* num, double* den,
                       cudaStream_t st);
 size_t zm_workspace_bytes(int H, int W);
+size_t zm_workspace_bytes(int H, int W, int batch);
 int launch_finalize(const double* num, const double* den, int H, int W, double eps, int zero_mean, float* K,
                     void* ws, cudaStream_t st);
-int launch_zero_mean_f32(float* Wp, int H, int W, void* ws, cudaStream_t st);
+int launch_zero_mean_f32(float* Wp, int batch, int H, int W, void* ws, cudaStream_t st);
 size_t ncc_workspace_bytes(int batch);
 int launch_ncc(const float* a, const float* b, int batch, long long P, double* out, void* ws, cudaStream_t st);
 int launch_pce_template(const float* K, int k_batch, const uint8_t* Iq, int batch, long long P, float* T,
@@ -178,7 +179,7 @@ static int validate_variant(const prnu_denoise_variant* v) {
 }
 static size_t variant_ws(int batch, int H, int W, const prnu_denoise_params* p, const prnu_denoise_variant* v) {
     return variant_workspace_bytes(batch, H, W, p->levels, v->taps, v->boundary, v->transform) +
-           zm_workspace_bytes(H, W);
+           zm_workspace_bytes(H, W, batch);
 }
 
 static int pad_pitch_u8(int W);
@@ -186,8 +187,8 @@ static size_t residual_pad_bytes(int batch, int H, int W) {   // re-pitched u8 p
     return W % 16 ? align_up((size_t)H * pad_pitch_u8(W) * batch, 256) : 0;
 }
 static size_t residual_ws(int batch, int H, int W, const Pyramid& pyr) {
-    return align_up(sizeof(float) * pyramid_floats_per_frame(pyr) * (size_t)batch, 256) + zm_workspace_bytes(H, W) +
-           residual_pad_bytes(batch, H, W);
+    return align_up(sizeof(float) * pyramid_floats_per_frame(pyr) * (size_t)batch, 256) +
+           zm_workspace_bytes(H, W, batch) + residual_pad_bytes(batch, H, W);
 }
 
 // Waves of SDA frames alternate between kExtractStreams streams (each with its
@@ -293,8 +294,7 @@ static int residual_impl(const TIn* planes, int batch, int H, int W, const prnu_
     if (zero_mean) {
         char* zm = reinterpret_cast<char*>(ws) +
                    align_up(sizeof(float) * pyramid_floats_per_frame(pyr) * (size_t)batch, 256);
-        for (int b = 0; b < batch; ++b)
-            if ((rc = launch_zero_mean_f32(W_out + (size_t)b * H * W, H, W, zm, st))) return rc;
+        if ((rc = launch_zero_mean_f32(W_out, batch, H, W, zm, st))) return rc;
     }
     return PRNU_OK;
 }
@@ -851,8 +851,7 @@ int prnu_residual_variant(const float* planes, int batch, int H, int W, const pr
     if (zero_mean) {
         char* zm = reinterpret_cast<char*>(ws) +
                    variant_workspace_bytes(batch, H, W, p->levels, v->taps, v->boundary, v->transform);
-        for (int b = 0; b < batch; ++b)
-            if ((rc = launch_zero_mean_f32(W_out + (size_t)b * H * W, H, W, zm, st))) return rc;
+        if ((rc = launch_zero_mean_f32(W_out, batch, H, W, zm, st))) return rc;
     }
     return PRNU_OK;
 }

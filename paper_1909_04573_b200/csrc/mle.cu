@@ -38,115 +38,118 @@ int launch_accumulate(const float* W, const float* I, int batch, long long P, do
 }
 
 // ---------------------------------------------------------------- a6
-struct FinalizeSrc {   // K = sum_WI / max(sum_I2, eps)
+struct FinalizeSrc {   // K = sum_WI / max(sum_I2, eps); one plane
     const double* num;
     const double* den;
     double eps;
-    __device__ __forceinline__ double operator()(size_t i) const {
+    __device__ __forceinline__ double operator()(int, size_t i) const {
         double d = den[i];
         return num[i] / (d > eps ? d : eps);
     }
 };
-struct FloatSrc {      // a residual plane to be zero-meaned
+struct FloatSrc {      // residual planes [b][H][W] to be zero-meaned (in place)
     const float* w;
-    __device__ __forceinline__ double operator()(size_t i) const { return (double)w[i]; }
+    long long P;
+    __device__ __forceinline__ double operator()(int b, size_t i) const { return (double)w[(size_t)b * P + i]; }
 };
 
-// S:135 step 1: materialise x (fp64) and each row's mean.
+// Row / column zero-mean (R-9) of `batch` planes, one launch per step with
+// the plane index in the grid.  The source is re-evaluated in every step (the same
+// fp64 value each time) instead of being materialised, and every sum keeps a fixed
+// order (deterministic, independent of the batch).
+// S:135 step 1: each row's mean.
 template <class Src>
-__global__ void __launch_bounds__(256) k_zm_rows(Src src, int H, int W, double* __restrict__ X,
-                                                  double* __restrict__ rowmean) {
+__global__ void __launch_bounds__(256) k_zm_rows(Src src, int H, int W, double* __restrict__ rowmean) {
     __shared__ double sh[8];
-    const int y = blockIdx.x;
+    const int y = blockIdx.x, b = blockIdx.y;
     double s = 0.0;
-    for (int x = threadIdx.x; x < W; x += 256) {
-        double v = src((size_t)y * W + x);
-        X[(size_t)y * W + x] = v;
-        s += v;
-    }
+    for (int x = threadIdx.x; x < W; x += 256) s += src(b, (size_t)y * W + x);
     double t[1] = {s};
     block_sum(t, sh);
-    if (threadIdx.x == 0) rowmean[y] = t[0] / W;
+    if (threadIdx.x == 0) rowmean[(size_t)b * H + y] = t[0] / W;
 }
 
 // S:135 step 2: column means of the row-centred values, in ZM_CHUNKS row chunks
 // (so the grid fills the GPU) whose partial sums are then added in chunk order:
 // a fixed summation order, independent of launch configuration (deterministic).
 constexpr int ZM_CHUNKS = 16;
-__global__ void __launch_bounds__(256) k_zm_cols(const double* __restrict__ X, const double* __restrict__ rowmean,
-                                                  int H, int W, double* __restrict__ part) {
+template <class Src>
+__global__ void __launch_bounds__(256) k_zm_cols(Src src, const double* __restrict__ rowmean, int H, int W,
+                                                  double* __restrict__ part) {
     __shared__ double sh[8][33];
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, b = blockIdx.z;
     const int x = blockIdx.x * 32 + tx;
     const int y0 = (int)((long long)H * blockIdx.y / ZM_CHUNKS), y1 = (int)((long long)H * (blockIdx.y + 1) / ZM_CHUNKS);
+    const double* rm = rowmean + (size_t)b * H;
     double s = 0.0;
     if (x < W)
-        for (int y = y0 + ty; y < y1; y += 8) s += X[(size_t)y * W + x] - rowmean[y];
+        for (int y = y0 + ty; y < y1; y += 8) s += src(b, (size_t)y * W + x) - rm[y];
     sh[ty][tx] = s;
     __syncthreads();
     if (ty == 0 && x < W) {
         double t = 0.0;
 #pragma unroll
         for (int k = 0; k < 8; ++k) t += sh[k][tx];
-        part[(size_t)blockIdx.y * W + x] = t;
+        part[((size_t)b * ZM_CHUNKS + blockIdx.y) * W + x] = t;
     }
 }
 __global__ void __launch_bounds__(256) k_zm_cols_final(const double* __restrict__ part, int H, int W,
                                                         double* __restrict__ colmean) {
-    const int x = blockIdx.x * 256 + threadIdx.x;
+    const int x = blockIdx.x * 256 + threadIdx.x, b = blockIdx.y;
     if (x >= W) return;
     double t = 0.0;
 #pragma unroll
-    for (int c = 0; c < ZM_CHUNKS; ++c) t += part[(size_t)c * W + x];
-    colmean[x] = t / H;
+    for (int c = 0; c < ZM_CHUNKS; ++c) t += part[((size_t)b * ZM_CHUNKS + c) * W + x];
+    colmean[(size_t)b * W + x] = t / H;
 }
 
-__global__ void __launch_bounds__(256) k_zm_apply(const double* __restrict__ X, const double* __restrict__ rowmean,
+template <class Src>
+__global__ void __launch_bounds__(256) k_zm_apply(Src src, const double* __restrict__ rowmean,
                                                    const double* __restrict__ colmean, int H, int W,
                                                    float* __restrict__ out) {
-    long long P = (long long)H * W;
+    const long long P = (long long)H * W;
+    const int b = blockIdx.y;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P;
          i += (long long)gridDim.x * blockDim.x) {
         int y = (int)(i / W), x = (int)(i - (long long)y * W);
-        out[i] = (float)((X[i] - rowmean[y]) - colmean[x]);
+        out[(size_t)b * P + i] = (float)((src(b, (size_t)i) - rowmean[(size_t)b * H + y]) - colmean[(size_t)b * W + x]);
     }
 }
 
 __global__ void __launch_bounds__(256) k_finalize_plain(FinalizeSrc src, long long P, float* __restrict__ out) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P;
          i += (long long)gridDim.x * blockDim.x)
-        out[i] = (float)src((size_t)i);
+        out[i] = (float)src(0, (size_t)i);
 }
 
-size_t zm_workspace_bytes(int H, int W) {
-    return align_up(sizeof(double) * (size_t)H * W, 256) + align_up(sizeof(double) * H, 256) +
-           align_up(sizeof(double) * W, 256) + align_up(sizeof(double) * ZM_CHUNKS * W, 256);
+size_t zm_workspace_bytes(int H, int W, int batch) {
+    return align_up(sizeof(double) * (size_t)batch * H, 256) + align_up(sizeof(double) * (size_t)batch * W, 256) +
+           align_up(sizeof(double) * (size_t)batch * ZM_CHUNKS * W, 256);
 }
+size_t zm_workspace_bytes(int H, int W) { return zm_workspace_bytes(H, W, 1); }
 
 template <class Src>
-static int run_zero_mean(Src src, int H, int W, float* out, void* ws, cudaStream_t st) {
+static int run_zero_mean(Src src, int batch, int H, int W, float* out, void* ws, cudaStream_t st) {
     char* p = reinterpret_cast<char*>(ws);
-    double* X = reinterpret_cast<double*>(p);
-    p += align_up(sizeof(double) * (size_t)H * W, 256);
     double* rm = reinterpret_cast<double*>(p);
-    p += align_up(sizeof(double) * H, 256);
+    p += align_up(sizeof(double) * (size_t)batch * H, 256);
     double* cm = reinterpret_cast<double*>(p);
-    p += align_up(sizeof(double) * W, 256);
+    p += align_up(sizeof(double) * (size_t)batch * W, 256);
     double* part = reinterpret_cast<double*>(p);
     {
         KTimer kt("zm_rows", st);
-        k_zm_rows<Src><<<H, 256, 0, st>>>(src, H, W, X, rm);
+        k_zm_rows<Src><<<dim3(H, batch), 256, 0, st>>>(src, H, W, rm);
     }
     {
         KTimer kt("zm_cols", st);
-        k_zm_cols<<<dim3((W + 31) / 32, ZM_CHUNKS), 256, 0, st>>>(X, rm, H, W, part);
-        k_zm_cols_final<<<(W + 255) / 256, 256, 0, st>>>(part, H, W, cm);
+        k_zm_cols<Src><<<dim3((W + 31) / 32, ZM_CHUNKS, batch), 256, 0, st>>>(src, rm, H, W, part);
+        k_zm_cols_final<<<dim3((W + 255) / 256, batch), 256, 0, st>>>(part, H, W, cm);
     }
     long long P = (long long)H * W;
-    long long blocks = std::min<long long>((P + 255) / 256, 16LL * device_sm_count());
+    long long blocks = std::max<long long>(1, std::min<long long>((P + 255) / 256, 16LL * device_sm_count() / batch));
     {
         KTimer kt("zm_apply", st);
-        k_zm_apply<<<(unsigned)blocks, 256, 0, st>>>(X, rm, cm, H, W, out);
+        k_zm_apply<Src><<<dim3((unsigned)blocks, batch), 256, 0, st>>>(src, rm, cm, H, W, out);
     }
     count_launch(4);
     return check_launch("zero_mean");
@@ -155,7 +158,7 @@ static int run_zero_mean(Src src, int H, int W, float* out, void* ws, cudaStream
 int launch_finalize(const double* num, const double* den, int H, int W, double eps, int zero_mean, float* K,
                     void* ws, cudaStream_t st) {
     FinalizeSrc src{num, den, eps};
-    if (zero_mean) return run_zero_mean(src, H, W, K, ws, st);
+    if (zero_mean) return run_zero_mean(src, 1, H, W, K, ws, st);
     long long P = (long long)H * W;
     long long blocks = std::min<long long>((P + 255) / 256, 16LL * device_sm_count());
     {
@@ -166,8 +169,10 @@ int launch_finalize(const double* num, const double* den, int H, int W, double e
     return check_launch("k_finalize_plain");
 }
 
-int launch_zero_mean_f32(float* Wp, int H, int W, void* ws, cudaStream_t st) {
-    return run_zero_mean(FloatSrc{Wp}, H, W, Wp, ws, st);
+// in place over batch planes [b][H][W]; ws: zm_workspace_bytes(H, W, batch)
+int launch_zero_mean_f32(float* Wp, int batch, int H, int W, void* ws, cudaStream_t st) {
+    if (batch > 65535) return fail(PRNU_INVALID_ARG, "zero mean: batch too large");
+    return run_zero_mean(FloatSrc{Wp, (long long)H * W}, batch, H, W, Wp, ws, st);
 }
 
 // ---------------------------------------------------------------- a7 NCC
