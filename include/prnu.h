@@ -322,6 +322,22 @@ size_t prnu_residual_variant_workspace_bytes(int batch, int H, int W, const prnu
 int prnu_residual_variant(const float* planes, int batch, int H, int W, const prnu_denoise_params* p,
                           const prnu_denoise_variant* v, int zero_mean, float* W_out, void* ws, size_t ws_bytes,
                           void* stream);
+/* prnu_extract_fingerprint_variant: the extraction of P:58-60 (SDA average, denoise,
+ * MLE, finalize; as prnu_extract_fingerprint) with denoiser variant v (R-24 ..
+ * R-26): waves of `batch` fp32 SDA frames (R-11) through prnu_residual_variant's
+ * passes, accumulated in ascending group order, finalized with zero-mean.  Arguments,
+ * outputs and errors as prnu_extract_fingerprint (frames u8 [m][H][W] device; K_out fp32
+ * [H][W]; sum_WI / sum_I2 fp64 [H][W], zeroed by the call), plus the variant checks of
+ * prnu_residual_variant; the workspace is
+ * prnu_extract_variant_workspace_bytes(H, W, batch, p, v) (0 for invalid arguments).
+ * Bit-identical to prnu_sda_average -> prnu_residual_variant ->
+ * prnu_fingerprint_accumulate -> prnu_fingerprint_finalize over the same waves. */
+size_t prnu_extract_variant_workspace_bytes(int H, int W, int batch, const prnu_denoise_params* p,
+                                            const prnu_denoise_variant* v);
+int prnu_extract_fingerprint_variant(const uint8_t* frames, int64_t m, int H, int W, int64_t depth,
+                                     const prnu_denoise_params* p, const prnu_denoise_variant* v, int batch,
+                                     double eps, float* K_out, double* sum_WI, double* sum_I2, int64_t* n_sda_host,
+                                     void* ws, size_t ws_bytes, void* stream);
 int prnu_wavelet_filter(int taps, double* h_out);
 
 /* ---------------------------------------------------------------------------

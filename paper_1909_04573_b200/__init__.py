@@ -139,6 +139,9 @@ _sig("prnu_block_plan_destroy", _i, _vp)
 _VP = ctypes.POINTER(_Variant)
 _sig("prnu_residual_variant_workspace_bytes", _sz, _i, _i, _i, _P, _VP)
 _sig("prnu_residual_variant", _i, _vp, _i, _i, _i, _P, _VP, _i, _vp, _vp, _sz, _vp)
+_sig("prnu_extract_variant_workspace_bytes", _sz, _i, _i, _i, _P, _VP)
+_sig("prnu_extract_fingerprint_variant", _i, _vp, _i64, _i, _i, _i64, _P, _VP, _i, _d, _vp, _vp, _vp,
+     ctypes.POINTER(_i64), _vp, _sz, _vp)
 _sig("prnu_wavelet_filter", _i, _i, ctypes.POINTER(_d))
 _sig("prnu_profile_begin", _i)
 _sig("prnu_profile_end", _i, _i, ctypes.c_char_p, ctypes.POINTER(_d), ctypes.POINTER(_i64), ctypes.POINTER(_i))
@@ -581,24 +584,27 @@ def extract_fingerprint_variant(frames: torch.Tensor, depth: int, variant: Denoi
                                 params: DenoiseParams | None = None, batch: int = 16,
                                 eps: float = 1e-6) -> Fingerprint:
     """f3: the fingerprint pipeline (SDA average, denoise, MLE, finalize) with a
-    denoiser variant, composed from the C-ABI calls prnu_sda_average ->
-    prnu_residual_variant -> prnu_fingerprint_accumulate (ascending group order) ->
-    prnu_fingerprint_finalize, one wave of `batch` SDA frames at a time."""
+    denoiser variant (prnu_extract_fingerprint_variant: waves of `batch` SDA frames
+    through the variant passes, accumulated in ascending group order)."""
     _dev(frames, torch.uint8, "frames", (3,))
     m, H, W = frames.shape
-    n_s = sda_groups(m, depth)
-    s_wi = torch.zeros((H, W), dtype=torch.float64, device=frames.device)
-    s_i2 = torch.zeros_like(s_wi)
-    Wbuf = None
-    for g0 in range(0, n_s, batch):
-        g1 = min(g0 + batch, n_s)
-        S = sda_average(frames[g0 * depth: g1 * depth], depth)
-        if Wbuf is None or Wbuf.shape[0] != S.shape[0]:
-            Wbuf = torch.empty_like(S)
-        residual_variant(S, variant, params, out=Wbuf)
-        fingerprint_accumulate(Wbuf, S, s_wi, s_i2)
-    K = fingerprint_finalize(s_wi, s_i2, eps)
-    return Fingerprint(K, s_wi, s_i2, n_s, depth, m)
+    p = _params(params)
+    v = variant.c()
+    nbytes = _lib.prnu_extract_variant_workspace_bytes(H, W, batch, ctypes.byref(p), ctypes.byref(v))
+    if nbytes == 0:
+        raise PrnuError(4, "invalid arguments for the variant extraction")
+    ws = _ws(nbytes, frames.device)
+    s_wi = torch.empty((H, W), dtype=torch.float64, device=frames.device)
+    s_i2 = torch.empty_like(s_wi)
+    K = torch.empty((H, W), dtype=torch.float32, device=frames.device)
+    n = _i64()
+    _check(_lib.prnu_extract_fingerprint_variant(_ptr(frames), m, H, W, depth, ctypes.byref(p), ctypes.byref(v),
+                                                 batch, eps, _ptr(K), _ptr(s_wi), _ptr(s_i2), ctypes.byref(n),
+                                                 _ptr(ws), nbytes, _stream()), "prnu_extract_fingerprint_variant")
+    return Fingerprint(K, s_wi, s_i2, int(n.value), depth, m)
+
+
+prnu_extract_fingerprint_variant = extract_fingerprint_variant
 
 
 # ---------------------------------------------------------------- a7-a8

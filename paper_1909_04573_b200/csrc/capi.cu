@@ -856,6 +856,60 @@ int prnu_residual_variant(const float* planes, int batch, int H, int W, const pr
     return PRNU_OK;
 }
 
+// f3 inside the extraction: SDA average (fp32 S, R-11) -> variant residual -> MLE
+// accumulation in ascending group order -> finalize, one wave of `batch` SDA frames at a
+// time (the composition prnu_sda_average -> prnu_residual_variant ->
+// prnu_fingerprint_accumulate -> prnu_fingerprint_finalize, bit-identical to it).
+static size_t extract_variant_ws(int H, int W, int batch, const prnu_denoise_params* p, const prnu_denoise_variant* v) {
+    const size_t plane = sizeof(float) * (size_t)batch * H * W;
+    return 2 * align_up(plane, 256) + align_up(variant_ws(batch, H, W, p, v), 256) + zm_workspace_bytes(H, W);
+}
+
+size_t prnu_extract_variant_workspace_bytes(int H, int W, int batch, const prnu_denoise_params* p,
+                                            const prnu_denoise_variant* v) {
+    if (batch < 1 || batch > kMaxBatch || H <= 0 || W <= 0 || validate_params(p, H, W, nullptr) ||
+        validate_variant(v))
+        return 0;
+    return extract_variant_ws(H, W, batch, p, v);
+}
+
+int prnu_extract_fingerprint_variant(const uint8_t* frames, int64_t m, int H, int W, int64_t depth,
+                                     const prnu_denoise_params* p, const prnu_denoise_variant* v, int batch,
+                                     double eps, float* K_out, double* sum_WI, double* sum_I2, int64_t* n_sda_host,
+                                     void* ws, size_t ws_bytes, void* stream) {
+    int rc;
+    if (!frames || !K_out || !sum_WI || !sum_I2 || !ws || !p || !v) return fail(PRNU_INVALID_ARG, "null pointer");
+    if (batch < 1 || batch > kMaxBatch) return fail(PRNU_INVALID_ARG, "batch must be in 1..65535");
+    if ((rc = check_dims(H, W))) return rc;
+    int64_t ns;
+    if ((rc = prnu_sda_groups(m, depth, &ns))) return rc;
+    if (depth > 65793) return fail(PRNU_BAD_PARAMETER, "depth > 65793 (sum would exceed 2^24)");
+    if (!(eps > 0.0)) return fail(PRNU_BAD_PARAMETER, "eps must be > 0");
+    ShrinkParams sp;
+    if ((rc = validate_params(p, H, W, &sp))) return rc;
+    if ((rc = validate_variant(v))) return rc;
+    if (ws_bytes < extract_variant_ws(H, W, batch, p, v)) return fail(PRNU_WORKSPACE_TOO_SMALL, "workspace too small");
+    if (n_sda_host) *n_sda_host = ns;
+    cudaStream_t st = as_stream(stream);
+    const size_t P = (size_t)H * W;
+    char* wsb = reinterpret_cast<char*>(ws);
+    float* S = reinterpret_cast<float*>(wsb);
+    float* Wr = reinterpret_cast<float*>(wsb + align_up(sizeof(float) * (size_t)batch * P, 256));
+    float* vws = reinterpret_cast<float*>(wsb + 2 * align_up(sizeof(float) * (size_t)batch * P, 256));
+    char* zm = wsb + 2 * align_up(sizeof(float) * (size_t)batch * P, 256) + align_up(variant_ws(batch, H, W, p, v), 256);
+    if (cudaMemsetAsync(sum_WI, 0, sizeof(double) * P, st) != cudaSuccess ||
+        cudaMemsetAsync(sum_I2, 0, sizeof(double) * P, st) != cudaSuccess)
+        return fail(PRNU_CUDA_ERROR, "cudaMemsetAsync");
+    for (int64_t g0 = 0; g0 < ns; g0 += batch) {
+        const int nb = (int)std::min<int64_t>(batch, ns - g0);
+        if ((rc = launch_sda_average(frames + (size_t)g0 * depth * P, nb, (long long)P, (int)depth, S, st))) return rc;
+        if ((rc = run_residual_variant(S, nb, H, W, p->levels, v->taps, v->boundary, v->transform, sp, Wr, vws, st)))
+            return rc;
+        if ((rc = launch_accumulate(Wr, S, nb, (long long)P, sum_WI, sum_I2, st))) return rc;
+    }
+    return launch_finalize(sum_WI, sum_I2, H, W, eps, 1, K_out, zm, st);
+}
+
 int prnu_wavelet_filter(int taps, double* h_out) {
     if (!h_out) return fail(PRNU_INVALID_ARG, "null pointer");
     return variant_filter(taps, h_out);

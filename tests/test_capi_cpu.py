@@ -133,3 +133,16 @@ def test_sda_division_sequence_exact():
     spec.loader.exec_module(D)
     for d in (2, 3, 5, 7, 10, 25, 30, 50, 100, 255, 256, 257):
         assert D.check(d) == 0, d
+
+
+def test_extract_variant_workspace_validation():
+    """prnu_extract_variant_workspace_bytes: > 0 for valid arguments, 0 for a bad
+    variant, batch or plane (validated on the host before any launch)."""
+    p = prnu.DenoiseParams().c()
+    L = prnu._lib
+    ok = prnu.DenoiseVariant(16, 0, 0).c()
+    bad = prnu.DenoiseVariant(12, 0, 0).c()
+    assert L.prnu_extract_variant_workspace_bytes(64, 96, 4, ctypes.byref(p), ctypes.byref(ok)) > 0
+    assert L.prnu_extract_variant_workspace_bytes(64, 96, 4, ctypes.byref(p), ctypes.byref(bad)) == 0
+    assert L.prnu_extract_variant_workspace_bytes(64, 96, 0, ctypes.byref(p), ctypes.byref(ok)) == 0
+    assert L.prnu_extract_variant_workspace_bytes(0, 96, 4, ctypes.byref(p), ctypes.byref(ok)) == 0

@@ -130,3 +130,26 @@ def test_variant_fingerprint_matches_oracle(prnu, v, kw, depth):
     np.testing.assert_array_equal(fp.sum_I2.cpu().numpy(), den)     # exact fp64 sums of exact products
     d = np.abs(fp.K.cpu().numpy().astype(np.float64) - K)
     assert float((d * np.sqrt(den / S.shape[0])).max()) <= W_TOL
+
+
+@pytest.mark.parametrize("v", [(16, 0, 0), (8, 1, 0), (8, 1, 1)])
+@pytest.mark.parametrize("m,depth,batch", [(16, 4, 3), (23, 2, 5)])
+def test_variant_extraction_is_the_composition(prnu, v, m, depth, batch):
+    """prnu_extract_fingerprint_variant (native waves) is bit-identical to composing
+    prnu_sda_average -> prnu_residual_variant -> prnu_fingerprint_accumulate ->
+    prnu_fingerprint_finalize over the same waves (remainder frames dropped)."""
+    g = torch.Generator().manual_seed(m + depth)
+    fr = torch.randint(0, 256, (m, 48, 72), generator=g, dtype=torch.uint8).cuda()
+    var = prnu.DenoiseVariant(*v)
+    fp = prnu.extract_fingerprint_variant(fr, depth, var, batch=batch)
+    ns = m // depth
+    s_wi = torch.zeros((48, 72), dtype=torch.float64, device="cuda")
+    s_i2 = torch.zeros_like(s_wi)
+    for g0 in range(0, ns, batch):
+        g1 = min(g0 + batch, ns)
+        S = prnu.sda_average(fr[g0 * depth: g1 * depth], depth)
+        Wr = prnu.residual_variant(S, var)
+        prnu.fingerprint_accumulate(Wr, S, s_wi, s_i2)
+    K = prnu.fingerprint_finalize(s_wi, s_i2, 1e-6)
+    assert fp.n_sda == ns
+    assert torch.equal(fp.sum_WI, s_wi) and torch.equal(fp.sum_I2, s_i2) and torch.equal(fp.K, K)
