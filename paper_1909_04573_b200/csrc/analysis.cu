@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
     const int hj = t & 7, hg = t >> 3;
     const int hx = cx0 + 8 * hg;
     const bool hv = (t < a.O) && (hx < a.nW);
-    const bool hfull = hx + 8 <= a.nW;
+    const bool hfull = hx + 8 <= a.nW;   // 8 outputs in the plane: one 256-bit store (32-byte aligned, host-checked)
 
     if (t == 0) {
         for (int k = 0; k < NSTG; ++k) mbar_init(&bar[k], 1);
@@ -683,8 +683,7 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
                     for (int x = 0; x < 8; ++x) o[x] = (cv[x] * s0) * al_rcp(fmaxf(m[x], s0));
                     float* drow = a.d0 + roff;
                     if (hfull) {
-                        reinterpret_cast<float4*>(drow)[0] = make_float4(o[0], o[1], o[2], o[3]);
-                        reinterpret_cast<float4*>(drow)[1] = make_float4(o[4], o[5], o[6], o[7]);
+                        st_global_v8(drow, o);
                     } else {
 #pragma unroll
                         for (int x = 0; x < 8; ++x)
@@ -779,10 +778,8 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
                     float* arow = a.d1 + roff;
                     float* drow = a.d2 + roff;
                     if (hfull) {
-                        reinterpret_cast<float4*>(arow)[0] = make_float4(oa[0], oa[1], oa[2], oa[3]);
-                        reinterpret_cast<float4*>(arow)[1] = make_float4(oa[4], oa[5], oa[6], oa[7]);
-                        reinterpret_cast<float4*>(drow)[0] = make_float4(od[0], od[1], od[2], od[3]);
-                        reinterpret_cast<float4*>(drow)[1] = make_float4(od[4], od[5], od[6], od[7]);
+                        st_global_v8(arow, oa);
+                        st_global_v8(drow, od);
                     } else {
 #pragma unroll
                         for (int x = 0; x < 8; ++x)
@@ -850,6 +847,9 @@ static int lift_launch(const T* in, long long in_bstride, int in_pitch, int NH, 
     if ((rc = set_smem_attr((const void*)k_analysis_lift<T, AlCfg<T>::MINB, false>, al_smem_bytes<T>(), done[1])))
         return rc;
     if (nb > 65535) return fail(PRNU_INVALID_ARG, "analysis: more than 65535 planes in one launch");
+    // the H pass stores 8 outputs per thread with one 256-bit store: 32-byte aligned subband rows
+    if ((((uintptr_t)d0 | (uintptr_t)d1 | (uintptr_t)d2) & 31) || (out_pitch & 7) || (out_bstride & 7))
+        return fail(PRNU_INVALID_ARG, "analysis: subband planes must have 32-byte aligned rows");
     AlArgs a{};
     a.in = in;
     a.in_bstride = in_bstride;

@@ -118,6 +118,15 @@ __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {   // a * 
     return *reinterpret_cast<float2*>(&r);
 }
 
+// 8 consecutive floats with one 256-bit store (STG.E.256, sm_100; p 32-byte aligned).
+// The L1 data pipe spends one wavefront per 32-byte sector a store instruction touches:
+// two STG.128 of a lane's 8 outputs touch its sector twice, one STG.256 once.
+__device__ __forceinline__ void st_global_v8(float* p, const float (&v)[8]) {
+    asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(v[0]), "f"(v[1]),
+                 "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+                 : "memory");
+}
+
 // ---------------------------------------------------------------- reductions
 // Deterministic warp-shuffle sums (the fingerprint / NCC / PCE / WDFT block
 // reductions): an xor butterfly inside each warp (lane i and lane i^o add the

@@ -53,6 +53,7 @@ struct SynthArgs {
     float* out;                  // MODE 0 output [nb][NH][out_pitch]
     long long out_bstride;
     int out_pitch;
+    int out_v8;                  // MODE 0: out, out_pitch, out_bstride allow 32-byte aligned 8-float stores
     const void* I;               // MODE 1: frames the residuals come from (u8, u16 SDA sums, fp32)
     long long i_bstride;
     int i_pitch;
@@ -234,7 +235,9 @@ __global__ void __launch_bounds__(256, 4) k_synth_acc2(const __grid_constant__ S
         if (MODE == 0) {   // plain inverse level: write this thread's 8 outputs
             if (rowok) {
                 float* orow = a.out + (size_t)(f0 + f) * a.out_bstride + (size_t)gy * a.out_pitch + gx;
-                if (gx + 8 <= a.NW && ((a.out_pitch & 3) == 0)) {
+                if (gx + 8 <= a.NW && a.out_v8) {   // one 256-bit store per thread (whole sectors)
+                    st_global_v8(orow, w);
+                } else if (gx + 8 <= a.NW && ((a.out_pitch & 3) == 0)) {
                     reinterpret_cast<float4*>(orow)[0] = make_float4(w[0], w[1], w[2], w[3]);
                     reinterpret_cast<float4*>(orow)[1] = make_float4(w[4], w[5], w[6], w[7]);
                 } else {
@@ -402,6 +405,7 @@ static int synth_level(const Pyramid& p, const PyramidBuffers& pb, int l, int nb
     s.out = out;
     s.out_bstride = out_bstride;
     s.out_pitch = out_pitch;
+    s.out_v8 = ((uintptr_t)out % 32 == 0) && (out_pitch % 8 == 0) && (out_bstride % 8 == 0);
     const long long tiles = (long long)((s.NW + ST_X - 1) / ST_X) * ((s.NH + 31) / 32);
     const long long slots = 4LL * device_sm_count();
     s.frames_per_cta = (int)std::max<long long>(4, std::min<long long>(nb, tiles * nb / (slots * 4)));
