@@ -25,3 +25,23 @@ def cuda_available():
         return torch.cuda.is_available()
     except Exception:
         return False
+
+
+# Parity numbers worth keeping in the log of a -q run (the full-size R-14 metrics):
+# tests append lines through the `parity_report` fixture, the terminal summary prints them.
+_PARITY_LINES = []
+
+
+@pytest.fixture
+def parity_report():
+    def add(line):
+        print("\n" + line)
+        _PARITY_LINES.append(line)
+    return add
+
+
+def pytest_terminal_summary(terminalreporter):
+    if _PARITY_LINES:
+        terminalreporter.section("parity report")
+        for line in _PARITY_LINES:
+            terminalreporter.write_line(line)

@@ -41,7 +41,7 @@ def video_c2():
     return v
 
 
-def test_c2_depth50_full_oracle(prnu, video_c2):
+def test_c2_depth50_full_oracle(prnu, video_c2, parity_report):
     """Config 2, SDA depth 50: the whole 36-frame fingerprint against the oracle."""
     fr = video_c2.frames[:1800]
     fp = prnu.extract_fingerprint(fr, 50, batch=36)
@@ -52,14 +52,14 @@ def test_c2_depth50_full_oracle(prnu, video_c2):
     prim = k_metric(Kg, K_ref, den, ns)
     rho = prnu.ncc(fp.K, video_c2.K).item()
     d_ncc = abs(rho - oracle.ncc(K_ref, video_c2.K.cpu().numpy()))
-    print(f"\nC2 d=50: R-14 primary {prim:.3e}, secondary 255*max|dK| "
+    parity_report(f"C2 d=50: R-14 primary {prim:.3e}, secondary 255*max|dK| "
           f"{255.0 * float(np.abs(Kg.astype(np.float64) - K_ref).max()):.3e}, |dNCC| {d_ncc:.2e}")
     assert prim <= K_TOL
     assert d_ncc <= NCC_TOL
     assert rho > 0.9
 
 
-def test_c2_depth1_full_oracle(prnu, video_c2):
+def test_c2_depth1_full_oracle(prnu, video_c2, parity_report):
     """Config 2, conventional (1800 denoisings), in the bench configuration (waves
     of 360 frames over the library's three streams): the WHOLE 1800-frame
     fingerprint against the oracle ("SDA-1 is the same as conventional",
@@ -92,7 +92,7 @@ def test_c2_depth1_full_oracle(prnu, video_c2):
     sec = 255.0 * float(np.abs(Kg.astype(np.float64) - K_ref).max())
     rho = prnu.ncc(fp.K, video_c2.K).item()
     d_ncc = abs(rho - oracle.ncc(K_ref, video_c2.K.cpu().numpy()))
-    print(f"\nC2 d=1 full 1800 frames: R-14 primary {prim:.3e}, secondary 255*max|dK| {sec:.3e}, "
+    parity_report(f"C2 d=1 full 1800 frames: R-14 primary {prim:.3e}, secondary 255*max|dK| {sec:.3e}, "
           f"|dNCC| {d_ncc:.2e}, NCC(K, K_true) {rho:.4f}")
     assert prim <= K_TOL
     assert d_ncc <= NCC_TOL
