@@ -167,9 +167,10 @@ def algorithmic_ops_per_step(name: str, H: int, W: int, levels: int, depths, m: 
     for _ in range(l):
         nH, nW = sub_len(nH), sub_len(nW)
     f_u8 = (m if 1 in depths else 0) + n_query
-    f_u16 = sum(m // d for d in depths if 1 < d <= 257)
+    f_pair = sum(m // d for d in depths if d == 2)
+    f_u16 = sum(m // d for d in depths if 2 < d <= 257)
     f_f32 = sum(m // d for d in depths if d > 257)
-    frames = {"_u8": f_u8, "u16": f_u16, "f32": f_f32}.get(name[-3:], f_u8 + f_u16 + f_f32)
+    frames = {"_u8": f_u8, "u16": f_u16, "f32": f_f32, "air": f_pair}.get(name[-3:], f_u8 + f_pair + f_u16 + f_f32)
     return frames * nH * nW * ALU_OPS_PER_POSITION
 
 
@@ -186,17 +187,20 @@ def algorithmic_bytes_per_step(name: str, H: int, W: int, levels: int, depths, m
     n = [nH[l] * nW[l] for l in range(levels + 1)]
     P = H * W
     f_u8 = (m if 1 in depths else 0) + n_query                 # level-1 u8 inputs
-    f_u16 = sum(m // d for d in depths if 1 < d <= 257)        # SDA frames as exact u16 group sums
+    f_pair = sum(m // d for d in depths if d == 2)             # SDA pairs: both u8 frames staged by the kernels
+    f_u16 = sum(m // d for d in depths if 2 < d <= 257)        # SDA frames as exact u16 group sums
     f_f32 = sum(m // d for d in depths if d > 257)             # SDA frames as fp32
-    f_all = f_u8 + f_u16 + f_f32
+    f_all = f_u8 + f_pair + f_u16 + f_f32
     if name == "sda_sum":                                       # d u8 frames read, u16 sum written
-        return sum((m // d) * (d * P + 2 * P) for d in depths if 1 < d <= 257)
+        return sum((m // d) * (d * P + 2 * P) for d in depths if 2 < d <= 257)
     if name == "sda_average":
         return sum((m // d) * (d * P + 4 * P) for d in depths if d > 257)
     if name == "analysis_l1_u8":
         return f_u8 * (1 * P + 4 * 4 * n[1])
     if name == "analysis_l1_u16":
         return f_u16 * (2 * P + 4 * 4 * n[1])
+    if name == "analysis_l1_pair":
+        return f_pair * (2 * P + 4 * 4 * n[1])
     if name == "analysis_l1_f32":
         return f_f32 * (4 * P + 4 * 4 * n[1])
     lvl = re.match(r"(analysis|synthesis)_l(\d)$", name)
@@ -212,9 +216,17 @@ def algorithmic_bytes_per_step(name: str, H: int, W: int, levels: int, depths, m
         return (m if 1 in depths else 0) * (4 * 4 * n[1] + 1 * P)
     if name == "synth_acc_l1_u16":
         return f_u16 * (4 * 4 * n[1] + 2 * P)
+    if name == "synth_acc_l1_pair":
+        return f_pair * (4 * 4 * n[1] + 2 * P)
     if name == "synth_acc_l1_f32":
         return f_f32 * (4 * 4 * n[1] + 4 * P)
     return None
+
+
+def sda_batch(n: int) -> int:
+    """SDA frames per wave: equal waves of at most 360 (as the depth-1 default)."""
+    nw = -(-n // 360)
+    return max(1, -(-n // nw))
 
 
 # ------------------------------------------------------------------ reference arm / cpu baseline
@@ -315,7 +327,7 @@ def main():
     if args.batch <= 0:   # equal waves of at most 360 frames (1800 -> 5 waves of 360; measured best)
         nw = -(-m // 360)
         args.batch = -(-m // nw)
-    exs = {d: prnu.Extractor(H, W, d, batch=(args.batch if d == 1 else max(1, min(64, m // d))), device=dev)
+    exs = {d: prnu.Extractor(H, W, d, batch=(args.batch if d == 1 else sda_batch(m // d)), device=dev)
            for d in depths}
     n_sda = {d: m // d for d in depths}
     plan = prnu.PcePlan(H, W, len(depths), device=dev)
@@ -485,7 +497,7 @@ def main():
         v5 = synth.video("shift", 3600, H, W, seed=5, device=dev)
         c5 = {}
         for d5 in (1, 2, 5, 10, 25, 50, 100, 300, 3600):
-            ex5 = prnu.Extractor(H, W, d5, 225 if d5 == 1 else min(64, 3600 // d5), device=dev)
+            ex5 = prnu.Extractor(H, W, d5, 225 if d5 == 1 else sda_batch(3600 // d5), device=dev)
             t5 = timed(lambda: ex5(v5.frames), reps=1)
             n5 = 3600 // d5
             rho = float(prnu.ncc(ex5(v5.frames).K, v5.K))

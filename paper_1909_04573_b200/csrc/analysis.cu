@@ -72,6 +72,8 @@ template <typename T>
 struct AlCfg;
 template <>
 struct AlCfg<uint8_t> {
+    using E = uint8_t;                 // staged element
+    static constexpr int DEP = 1;      // frames per staged box (u8pair: 2)
     static constexpr int OMAX = 112;   // output columns per strip (region 120)
     static constexpr int P1 = 124;     // da planes pitch (floats, == 28 mod 32: LDS.128 over 8 rows conflict-free)
     static constexpr int P2 = 122;     // (ad, dd) planes pitch (float2; 2 P2 == 20 mod 32)
@@ -83,7 +85,9 @@ struct AlCfg<uint8_t> {
     static constexpr int MINB = 3;
 };
 template <>
-struct AlCfg<uint16_t> {   // exact SDA group sums (level 1 at 2 <= d <= 257)
+struct AlCfg<uint16_t> {   // exact SDA group sums (level 1 at 3 <= d <= 257)
+    using E = uint16_t;
+    static constexpr int DEP = 1;
     static constexpr int OMAX = 112;
     static constexpr int P1 = 124;
     static constexpr int P2 = 122;
@@ -94,6 +98,8 @@ struct AlCfg<uint16_t> {   // exact SDA group sums (level 1 at 2 <= d <= 257)
 };
 template <>
 struct AlCfg<float> {
+    using E = float;
+    static constexpr int DEP = 1;
     static constexpr int OMAX = 104;   // region 112
     static constexpr int P1 = 116;     // == 20 mod 32
     static constexpr int P2 = 114;     // 2 P2 == 4 mod 32
@@ -102,10 +108,25 @@ struct AlCfg<float> {
     static constexpr bool SPLITV = false;
     static constexpr int MINB = 3;
 };
+template <>
+struct AlCfg<u8pair> {   // SDA pairs (level 1 at d = 2): both u8 frames of a group in one depth-2 box
+    using E = uint8_t;
+    static constexpr int DEP = 2;
+    static constexpr int OMAX = 112;
+    static constexpr int P1 = 124;
+    static constexpr int P2 = 122;
+    // a stage holds 2 boxes x 2 frames x 16 rows (9.2 KB, as the u16 sums); measured: 2 stages at
+    // 104-column strips (to fit 3 CTAs/SM) 5.37 vs 5.11 ms per 900 FHD pairs, slower
+    static constexpr int NSTG = 1;
+    static constexpr int BOXW = 144;
+    static constexpr bool SPLITV = false;
+    static constexpr int MINB = 3;
+};
 template <typename T>
 __host__ __device__ constexpr int al_logw() { return 128 + AlCfg<T>::BOXW; }
+// staged elements per stage: [box 0: DEP frames x 16 rows x BOXW][box 1: likewise]
 template <typename T>
-__host__ __device__ constexpr int al_stage_elems() { return 2 * AL_IR * AlCfg<T>::BOXW; }
+__host__ __device__ constexpr int al_stage_elems() { return 2 * AlCfg<T>::DEP * AL_IR * AlCfg<T>::BOXW; }
 template <typename T>
 __host__ __device__ constexpr int al_da_floats() { return 5 * AL_BK * AlCfg<T>::P1; }
 template <typename T>
@@ -119,7 +140,7 @@ __host__ __device__ constexpr int al_v_floats() {
 }
 template <typename T>
 constexpr size_t al_smem_bytes() {
-    return AlCfg<T>::NSTG * al_stage_elems<T>() * sizeof(T) + sizeof(float) * al_v_floats<T>() + 32;
+    return AlCfg<T>::NSTG * al_stage_elems<T>() * sizeof(typename AlCfg<T>::E) + sizeof(float) * al_v_floats<T>() + 32;
 }
 static_assert(2 * AL_IR * AL_RBP <= 5 * AL_BK * AlCfg<float>::P1, "row buffer inside the da planes");
 static_assert(AlCfg<uint8_t>::OMAX + 8 <= AlCfg<uint8_t>::P2 && AlCfg<float>::OMAX + 8 <= AlCfg<float>::P2, "V planes");
@@ -127,7 +148,7 @@ template <typename T>
 constexpr bool al_fits() {   // MINB CTAs per SM in 228 KB (1 KB reserved per CTA)
     return AlCfg<T>::MINB * (al_smem_bytes<T>() + 1024) <= 228 * 1024;
 }
-static_assert(al_fits<uint8_t>() && al_fits<uint16_t>() && al_fits<float>(), "CTAs per SM");
+static_assert(al_fits<uint8_t>() && al_fits<uint16_t>() && al_fits<float>() && al_fits<u8pair>(), "CTAs per SM");
 
 struct AlArgs {
     const void* in;
@@ -159,27 +180,17 @@ __constant__ float2 c_al_w[4] = {{1.0f / 9.0f, LF_KD4 / 9.0f},
                                  {1.0f / 49.0f, LF_KD4 / 49.0f},
                                  {1.0f / 81.0f, LF_KD4 / 81.0f}};
 
+// staged row r (< DEP * 16: frame r / 16, row r % 16), logical column x (box 0: x < BOXW, box 1: x >= 128)
 template <typename T>
-__device__ __forceinline__ float al_stg_at(const T* s, int r, int x) {
-    constexpr int BW = AlCfg<T>::BOXW;
-    return x < BW ? (float)s[r * BW + x] : (float)s[AL_IR * BW + r * BW + x - 128];
+__device__ __forceinline__ typename AlCfg<T>::E al_stg_at(const typename AlCfg<T>::E* s, int r, int x) {
+    constexpr int BW = AlCfg<T>::BOXW, BOFF = AlCfg<T>::DEP * AL_IR * BW;
+    return x < BW ? s[r * BW + x] : s[BOFF + r * BW + x - 128];
 }
-__device__ __forceinline__ void al_stg_put(uint8_t* s, int r, int x, float v) {
-    constexpr int BW = AlCfg<uint8_t>::BOXW;
-    const uint8_t u = (uint8_t)v;
-    if (x < BW) s[r * BW + x] = u;
-    if (x >= 128) s[AL_IR * BW + r * BW + x - 128] = u;
-}
-__device__ __forceinline__ void al_stg_put(uint16_t* s, int r, int x, float v) {
-    constexpr int BW = AlCfg<uint16_t>::BOXW;
-    const uint16_t u = (uint16_t)v;
-    if (x < BW) s[r * BW + x] = u;
-    if (x >= 128) s[AL_IR * BW + r * BW + x - 128] = u;
-}
-__device__ __forceinline__ void al_stg_put(float* s, int r, int x, float v) {
-    constexpr int BW = AlCfg<float>::BOXW;
+template <typename T>
+__device__ __forceinline__ void al_stg_put(typename AlCfg<T>::E* s, int r, int x, typename AlCfg<T>::E v) {
+    constexpr int BW = AlCfg<T>::BOXW, BOFF = AlCfg<T>::DEP * AL_IR * BW;
     if (x < BW) s[r * BW + x] = v;
-    if (x >= 128) s[AL_IR * BW + r * BW + x - 128] = v;
+    if (x >= 128) s[BOFF + r * BW + x - 128] = v;
 }
 
 // ---- row pass of one item (staged row r, group g: region columns 8g .. 8g+7):
@@ -245,6 +256,31 @@ __device__ __forceinline__ void al_rowpass(const uint16_t* s, int r, int g, floa
     }
     al_lift_pairs(E, O, L, Hh);
 }
+// SDA pairs (d = 2): S = (b0 + b1) / 2 exactly (u8_half_bias, R-11), then the same lifting
+__device__ __forceinline__ void al_rowpass_pair(const uint8_t* s, int r, int g, float2 (&L)[4], float2 (&Hh)[4]) {
+    constexpr int BW = AlCfg<u8pair>::BOXW;
+    const uint8_t* src = s + (g < 8 ? r * BW + 16 * g : 2 * AL_IR * BW + r * BW + 16 * g - 128);
+    const uint8_t* src1 = src + AL_IR * BW;   // the group's second frame, same row
+    const uint4 a0 = *reinterpret_cast<const uint4*>(src);
+    const uint2 a1 = *reinterpret_cast<const uint2*>(src + 16);
+    const uint4 b0 = *reinterpret_cast<const uint4*>(src1);
+    const uint2 b1 = *reinterpret_cast<const uint2*>(src1 + 16);
+    const uint32_t wa[6] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y};
+    const uint32_t wb[6] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y};
+    auto ha = [&](int b) { return u8_half_bias(wa[b >> 2], b & 3); };
+    auto hb = [&](int b) { return u8_half_bias(wb[b >> 2], b & 3); };
+    const float2 m22 = make_float2(-4194304.f, -4194304.f);
+    auto sv = [&](int b0_, int b1_) {   // (S[b0_], S[b1_]) = ((h(a) - 2^22) + h(b)) - 2^22, exact
+        return add2(add2(add2(make_float2(ha(b0_), ha(b1_)), m22), make_float2(hb(b0_), hb(b1_))), m22);
+    };
+    float2 E[7], O[7];
+#pragma unroll
+    for (int j = 0; j < 7; ++j) {
+        E[j] = sv(2 * j + 2, 2 * j + 10);
+        O[j] = sv(2 * j + 3, 2 * j + 11);
+    }
+    al_lift_pairs(E, O, L, Hh);
+}
 __device__ __forceinline__ void al_rowpass(const float* s, int r, int g, float, float, float2 (&L)[4],
                                            float2 (&Hh)[4]) {
     constexpr int BW = AlCfg<float>::BOXW;
@@ -300,9 +336,11 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
     constexpr int STG = al_stage_elems<T>();
     constexpr int NSTG = AlCfg<T>::NSTG, P1 = AlCfg<T>::P1, P2 = AlCfg<T>::P2;
     constexpr bool SPLITV = AlCfg<T>::SPLITV;
+    constexpr int DEP = AlCfg<T>::DEP;
+    using E = typename AlCfg<T>::E;
     extern __shared__ __align__(128) unsigned char smem[];
-    T* stg0 = reinterpret_cast<T*>(smem);
-    float* V0 = reinterpret_cast<float*>(smem + NSTG * STG * sizeof(T));
+    E* stg0 = reinterpret_cast<E*>(smem);
+    float* V0 = reinterpret_cast<float*>(smem + NSTG * STG * sizeof(E));
     float* DA = V0;                                                         // da planes v3 v5 v7 v9 c [8][P1]; row buffer
     float2* PR = reinterpret_cast<float2*>(SPLITV ? V0 : V0 + al_da_floats<T>());   // (ad, dd) planes [8][P2]
     uint64_t* bar = reinterpret_cast<uint64_t*>(V0 + al_v_floats<T>());
@@ -319,7 +357,7 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
     const int nblk = 1 + (ky1 - ky0 + AL_BK - 1) / AL_BK;
     const int ncols = a.O + 8;
     const int ngroups = ncols / 8;
-    const T* in = reinterpret_cast<const T*>(a.in) + (size_t)b * a.in_bstride;
+    const E* in = reinterpret_cast<const E*>(a.in) + (size_t)b * a.in_bstride;
     const int gc = cx0 - 4 + t;   // this thread's coefficient column
     // column-pass source column: in-plane columns read their own row-pass column; mirrored
     // halo columns outside the subband read their partner's (R-4); idle threads a valid one
@@ -344,7 +382,8 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
     // edge fix-up (TMA-staged blocks of the first / last strip): out-of-plane logical columns
     // of the staged rows receive their mirrored in-plane values (R-4).  At most 16 + 24
     // columns (xs >= -16; input columns NW .. NW+23): thread t handles column slot t % 40
-    // of rows t / 40 + 3k; sources in the plane, destinations outside it (no hazard).
+    // of staged rows t / 40 + 3k (DEP x 16 rows); sources in the plane, destinations outside
+    // it (no hazard).
     int fx = -1, fs = 0;
     const int fr0 = t / 40;
     if (edge) {
@@ -357,15 +396,16 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
             fs = min(max(mirror(xs + fx, a.NW) - xs, 0), LOGW - 1);
         }
     }
-    auto fixup = [&](T* s) {
+    auto fixup = [&](E* s) {
         if (fx < 0) return;
-        float v[6];
+        constexpr int FR = (DEP * AL_IR + 2) / 3;
+        E v[FR];
 #pragma unroll
-        for (int k = 0; k < 6; ++k)
-            if (fr0 + 3 * k < AL_IR) v[k] = al_stg_at(s, fr0 + 3 * k, fs);
+        for (int k = 0; k < FR; ++k)
+            if (fr0 + 3 * k < DEP * AL_IR) v[k] = al_stg_at<T>(s, fr0 + 3 * k, fs);
 #pragma unroll
-        for (int k = 0; k < 6; ++k)
-            if (fr0 + 3 * k < AL_IR) al_stg_put(s, fr0 + 3 * k, fx, v[k]);
+        for (int k = 0; k < FR; ++k)
+            if (fr0 + 3 * k < DEP * AL_IR) al_stg_put<T>(s, fr0 + 3 * k, fx, v[k]);
     };
     auto stg_of = [&](int i) { return (i + NSTG) % NSTG; };
     auto y0_of = [&](int i) { return i < 0 ? 2 * K0 - 6 : 2 * (K0 + AL_BK * i); };
@@ -382,24 +422,29 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
         if (y0 < 0 && y1 >= 0) lo = 0;
         return min(lo, a.NH - AL_IR);
     };
+    // (u8pair: TMA only; the host takes the u16-sum path where the pair boxes do not apply)
     auto tma_ok = [&](int i) { return a.use_tma && (refl1 || (a.NH >= AL_IR && inside(i))); };
     auto issue = [&](int i) {
         const int k = stg_of(i);
-        T* s = stg0 + k * STG;
+        E* s = stg0 + k * STG;
         const int y = box_y(i);
         PRNU_DCHECK(y >= 0 && y + AL_IR <= a.NH);
-        mbar_arrive_expect_tx(&bar[k], (uint32_t)(2 * AL_IR * BW * sizeof(T)));
-        tma_load_3d(s, &map, xs, y, b, &bar[k]);
-        tma_load_3d(s + AL_IR * BW, &map, xs + 128, y, b, &bar[k]);
+        mbar_arrive_expect_tx(&bar[k], (uint32_t)(2 * DEP * AL_IR * BW * sizeof(E)));
+        tma_load_3d(s, &map, xs, y, DEP * b, &bar[k]);
+        tma_load_3d(s + DEP * AL_IR * BW, &map, xs + 128, y, DEP * b, &bar[k]);
     };
     if (t == 0) {
         for (int i = -1; i < NSTG - 1 && i < nblk; ++i)
             if (tma_ok(i)) issue(i);
     }
     __syncthreads();
-    const bool vec_ok = ((reinterpret_cast<uintptr_t>(in) & 15) == 0) && ((a.in_pitch * sizeof(T)) % 16 == 0);
-    auto manual = [&](T* s, int y0, int nr) {
-        constexpr int CE = 16 / sizeof(T);
+    const bool vec_ok = ((reinterpret_cast<uintptr_t>(in) & 15) == 0) && ((a.in_pitch * sizeof(E)) % 16 == 0);
+    auto manual = [&](E* s, int y0, int nr) {
+        if (DEP != 1) {   // unreachable: pairs are staged by TMA only
+            __trap();
+            return;
+        }
+        constexpr int CE = 16 / sizeof(E);
         constexpr int NCH = LOGW / CE;
         constexpr int PER = (AL_IR * NCH + AL_NT - 1) / AL_NT;
         uint4 v[PER];
@@ -410,11 +455,11 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
             if (e < nr * NCH) {
                 const int r = e / NCH, ch = e - r * NCH;
                 const int gx = xs + ch * CE;
-                const T* row = in + (size_t)mirror(y0 + r, a.NH) * a.in_pitch;
+                const E* row = in + (size_t)mirror(y0 + r, a.NH) * a.in_pitch;
                 if (vec_ok && gx >= 0 && gx + CE <= a.NW) {
                     v[k] = __ldg(reinterpret_cast<const uint4*>(row + gx));
                 } else {
-                    T tmp[CE];
+                    E tmp[CE];
 #pragma unroll
                     for (int i = 0; i < CE; ++i) tmp[i] = row[mirror(gx + i, a.NW)];
                     memcpy(&v[k], tmp, 16);
@@ -431,14 +476,17 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
             }
         }
     };
-    auto rowpass = [&](const T* s, int prow, int nr) {
+    auto rowpass = [&](const E* s, int prow, int nr) {
         if (rr >= nr) return;
 #pragma unroll 1
         for (int h = 0; h < 2; ++h) {
             const int g = ga + 8 * h;
             if (h == 0 ? doA : doB) {
                 float2 L[4], Hh[4];
-                al_rowpass(s, prow, g, a.div_d, a.div_r, L, Hh);
+                if constexpr (DEP == 2)
+                    al_rowpass_pair(s, prow, g, L, Hh);
+                else
+                    al_rowpass(s, prow, g, a.div_d, a.div_r, L, Hh);
                 PRNU_DCHECK(rr < AL_IR && 8 * g + 8 <= AL_RBP && prow >= 0 && prow < AL_IR);
                 float2* dl = reinterpret_cast<float2*>(RBlo + rr * AL_RBP + 8 * g);
                 float2* dh = reinterpret_cast<float2*>(RBhi + rr * AL_RBP + 8 * g);
@@ -477,7 +525,7 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
         const bool pro = i < 0;
         const int K = K0 + AL_BK * i;
         const int sk = stg_of(i);
-        T* s = stg0 + sk * STG;
+        E* s = stg0 + sk * STG;
         int prow;
         PRNU_STRESS(1);
         if (tma_ok(i)) {
@@ -832,12 +880,9 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
 }
 
 // ------------------------------------------------------------------ host
-bool encode_tensor_map_3d(CUtensorMap* map, CUtensorMapDataType dt, size_t elem_bytes, const void* base, uint64_t cols,
-                          uint64_t rows, uint64_t depth, uint64_t pitch_bytes, uint64_t plane_bytes, uint32_t box_w,
-                          uint32_t box_h);
 
 template <typename T>
-static int lift_launch(const T* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll, float* d0,
+static int lift_launch(const typename AlCfg<T>::E* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll, float* d0,
                        float* d1, float* d2, long long out_bstride, int out_pitch, int nH, int nW,
                        const ShrinkParams& sp, const SdaDiv& div, int nb, cudaStream_t st) {
     static DeviceFlags done[2];
@@ -872,20 +917,23 @@ static int lift_launch(const T* in, long long in_bstride, int in_pitch, int NH, 
     const int S = (nW + a.O - 1) / a.O;
     // segments of <= 300 rows (prologue overhead <= 3%), more of them while the grid holds
     // fewer than 6 (u8, level 1) / 1 (fp32) waves of MINB CTAs per SM
-    const long long waves = sizeof(T) == 1 ? 6 : 1;
+    const long long waves = sizeof(typename AlCfg<T>::E) == 1 ? 6 : 1;
     const long long slots = (long long)device_sm_count() * AlCfg<T>::MINB;
     int nseg = (nH + 299) / 300;
     while ((long long)S * nseg * nb < waves * slots && (nH + nseg) / (nseg + 1) >= 32) ++nseg;
     a.SH = (int)align_up((size_t)((nH + nseg - 1) / nseg), 8);
     nseg = (nH + a.SH - 1) / a.SH;
     CUtensorMap map{};
-    const size_t es = sizeof(T);
-    const CUtensorMapDataType dt = sizeof(T) == 1   ? CU_TENSOR_MAP_DATA_TYPE_UINT8
-                                   : sizeof(T) == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+    constexpr int DEP = AlCfg<T>::DEP;
+    const size_t es = sizeof(typename AlCfg<T>::E);
+    const CUtensorMapDataType dt = es == 1   ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                   : es == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
                                                     : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     a.use_tma = ((in_pitch * es) % 16 == 0) && ((in_bstride * es) % 16 == 0) && ((uintptr_t)in % 16 == 0) &&
-                encode_tensor_map_3d(&map, dt, es, in, (uint64_t)NW, (uint64_t)NH, (uint64_t)nb, (uint64_t)in_pitch * es,
-                                     (uint64_t)in_bstride * es, AlCfg<T>::BOXW, AL_IR);
+                encode_tensor_map_3d(&map, dt, es, in, (uint64_t)NW, (uint64_t)NH, (uint64_t)nb * DEP,
+                                     (uint64_t)in_pitch * es, (uint64_t)in_bstride * es, AlCfg<T>::BOXW, AL_IR, DEP);
+    // pairs: in_bstride is the frame stride, group b = frames DEP b, DEP b + 1 (TMA only, >= 32 rows)
+    if (DEP != 1 && (!a.use_tma || NH < 32)) return fail(PRNU_INVALID_ARG, "analysis: SDA pairs need TMA-stageable frames");
     dim3 grid(S, nseg, nb);
     if (sp.wmask == 15)
         k_analysis_lift<T, AlCfg<T>::MINB, true><<<grid, AL_NT, al_smem_bytes<T>(), st>>>(map, a);
@@ -905,6 +953,12 @@ int launch_analysis_lift_u16(const uint16_t* in, long long in_bstride, int in_pi
                              const ShrinkParams& sp, const SdaDiv& div, int nb, cudaStream_t st) {
     return lift_launch<uint16_t>(in, in_bstride, in_pitch, NH, NW, ll, d0, d1, d2, out_bstride, out_pitch, nH, nW,
                                  sp, div, nb, st);
+}
+int launch_analysis_lift_pair(const uint8_t* in, long long frame_stride, int in_pitch, int NH, int NW, float* ll,
+                              float* d0, float* d1, float* d2, long long out_bstride, int out_pitch, int nH, int nW,
+                              const ShrinkParams& sp, int nb, cudaStream_t st) {
+    return lift_launch<u8pair>(in, frame_stride, in_pitch, NH, NW, ll, d0, d1, d2, out_bstride, out_pitch, nH, nW, sp,
+                               SdaDiv{}, nb, st);
 }
 int launch_analysis_lift_f32(const float* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll,
                              float* d0, float* d1, float* d2, long long out_bstride, int out_pitch, int nH, int nW,

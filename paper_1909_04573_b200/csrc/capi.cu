@@ -249,6 +249,13 @@ static int extract_chunk(const uint8_t* frames, int64_t nb, int H, int W, int64_
         return run_residual_accumulate<uint8_t>(frames, frames, (int)nb, H, W, pyr, sp, SdaDiv{}, num, den, pyr_ws, st,
                                                 acc_wait, acc_done, fstride);
     }
+    if (depth == 2 && W % 16 == 0 && P % 16 == 0 && (uintptr_t)frames % 16 == 0 && H >= 32) {
+        // SDA pairs: both frames of a group staged by one depth-2 TMA box in the analysis and
+        // the accumulation, S = (b0 + b1) / 2 formed there (exact, R-11): no sum pass
+        const u8pair* F = reinterpret_cast<const u8pair*>(frames);
+        return run_residual_accumulate<u8pair>(F, F, (int)nb, H, W, pyr, sp, SdaDiv{}, num, den, pyr_ws, st, acc_wait,
+                                               acc_done, P);
+    }
     if (depth <= 257) {   // exact u16 group sums; S = RN(sum / d) inside the kernels (R-11)
         const int Wp = sum_pitch_u16(W);
         uint16_t* S = reinterpret_cast<uint16_t*>(ws + pyr_bytes);

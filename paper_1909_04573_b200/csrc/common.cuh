@@ -234,6 +234,18 @@ struct SdaDiv {
 __device__ __forceinline__ float u16_to_f32(uint32_t w, int hi) {
     return __fadd_rn(__uint_as_float(__byte_perm(w, 0x4B000000u, hi ? 0x7632u : 0x7610u)), -8388608.0f);
 }
+// SDA pairs (depth d = 2, R-11): the two u8 frames of a group staged together by one
+// TMA box of depth 2 ([frame][row][x] in shared memory), S = (b0 + b1) / 2 formed where
+// it is consumed (exact in fp32: no sum pass, no u16 plane).  A tag type: 2 bytes per
+// pixel, like the u16 sums it replaces at d = 2.
+struct u8pair {
+    uint8_t b[2];
+};
+// (2^22 + b/2) as a float bit pattern from byte b (ulp 0.5 at 2^22): the half of a u8
+// exactly, so S = ((h(b0) - 2^22) + h(b1)) - 2^22 = (b0 + b1) / 2 with two exact adds.
+__device__ __forceinline__ float u8_half_bias(uint32_t w, int byte) {
+    return __uint_as_float(__byte_perm(w, 0x4A800000u, 0x7640u | (uint32_t)byte));
+}
 // RN_fp32(s / d): reciprocal product plus one FMA correction.  Equal to the correctly
 // rounded quotient for every integer s <= 255 d and 2 <= d <= 257 (and the config
 // depths 300..3600): exhaustive check in tools/sda_div_check.py / tests/test_capi_cpu.py.
@@ -263,6 +275,10 @@ int launch_analysis_lift_u8(const uint8_t* in, long long in_bstride, int in_pitc
 int launch_analysis_lift_u16(const uint16_t* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll,
                              float* d0, float* d1, float* d2, long long out_bstride, int out_pitch, int nH, int nW,
                              const ShrinkParams& sp, const SdaDiv& div, int nb, cudaStream_t st);
+// SDA pairs (d = 2): groups of two u8 frames (frame_stride apart; group b = frames 2b, 2b+1)
+int launch_analysis_lift_pair(const uint8_t* in, long long frame_stride, int in_pitch, int NH, int NW, float* ll,
+                              float* d0, float* d1, float* d2, long long out_bstride, int out_pitch, int nH, int nW,
+                              const ShrinkParams& sp, int nb, cudaStream_t st);
 int launch_analysis_lift_f32(const float* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll,
                              float* d0, float* d1, float* d2, long long out_bstride, int out_pitch, int nH, int nW,
                              const ShrinkParams& sp, int nb, cudaStream_t st);

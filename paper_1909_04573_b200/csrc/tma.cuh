@@ -57,10 +57,10 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
 
 // ---------------------------------------------------------------- host
 // Encode a rank-3 map over [depth][rows][cols] elements with the given row
-// pitch and plane stride (bytes) and a box of (box_w, box_h, 1).  Returns
+// pitch and plane stride (bytes) and a box of (box_w, box_h, box_d).  Returns
 // false if the driver entry point is unavailable or the encoding fails.
 bool encode_tensor_map_3d(CUtensorMap* map, CUtensorMapDataType dt, size_t elem_bytes, const void* base, uint64_t cols,
                           uint64_t rows, uint64_t depth, uint64_t pitch_bytes, uint64_t plane_bytes, uint32_t box_w,
-                          uint32_t box_h);
+                          uint32_t box_h, uint32_t box_d = 1);
 
 }  // namespace prnu

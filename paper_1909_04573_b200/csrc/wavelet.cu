@@ -17,6 +17,7 @@
 // Filters are compile-time immediates (FFMA-imm).  fp32 arithmetic; the
 // accumulators are fp64.
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "tma.cuh"
@@ -97,6 +98,9 @@ __global__ void __launch_bounds__(256, 4) k_synth_acc2(const __grid_constant__ S
                                                        const __grid_constant__ CUtensorMap imap, SynthArgs a) {
     constexpr int CY = TY / 2 + 3;   // coefficient rows of a TY-row tile
     static_assert(TY % 4 == 0 && TY <= 32, "tile height");
+    // SDA pairs (d = 2): the I tile is both frames of the group, [2][TY][ST_X] bytes (one depth-2 box)
+    constexpr bool PAIR = std::is_same<TI, u8pair>::value;
+    constexpr int IDEP = PAIR ? 2 : 1;
     extern __shared__ __align__(128) float smem[];
     // coefficient ring of 2 stages (frame f in stage f & 1, released after its
     // column pass), I-tile ring of 3 (frame f in f % 3, released after its row
@@ -131,7 +135,7 @@ __global__ void __launch_bounds__(256, 4) k_synth_acc2(const __grid_constant__ S
         tma_load_3d(c + 1 * SC_PS, &maps.d0, kx0, ky0, f0 + f, &bar[st]);
         tma_load_3d(c + 2 * SC_PS, &maps.d1, kx0, ky0, f0 + f, &bar[st]);
         tma_load_3d(c + 3 * SC_PS, &maps.d2, kx0, ky0, f0 + f, &bar[st]);
-        if (MODE) tma_load_3d(itile0 + (f % 3) * TY * ST_X, &imap, tx0, ty0, f, &bar[st]);
+        if (MODE) tma_load_3d(itile0 + (f % 3) * TY * ST_X, &imap, tx0, ty0, IDEP * f, &bar[st]);
     };
     if (tid == 0) {
         if (nb > 0) issue(0);
@@ -153,7 +157,7 @@ __global__ void __launch_bounds__(256, 4) k_synth_acc2(const __grid_constant__ S
         den_i[k] = 0u;
         den_d[k] = 0.0;
     }
-    if (MODE && sizeof(TI) != 1) {
+    if (MODE && sizeof(TI) != 1) {   // u16 / fp32 / pairs: the fp64 accumulator in registers
 #pragma unroll
         for (int k = 0; k < 8; ++k) den_d[k] = (rowok && gx + k < a.NW) ? a.den[(size_t)gy * a.acc_pitch + gx + k] : 0.0;
     }
@@ -249,7 +253,26 @@ __global__ void __launch_bounds__(256, 4) k_synth_acc2(const __grid_constant__ S
             continue;
         }
         const TI* irow = itile0 + (f % 3) * TY * ST_X + rt * ST_X + 8 * rg;
-        if (sizeof(TI) == 1) {
+        if constexpr (PAIR) {   // S = (b0 + b1) / 2 exactly; I^2 = s^2 / 4 summed as the integer s^2
+            const uint8_t* ib = reinterpret_cast<const uint8_t*>(itile0 + (f % 3) * TY * ST_X) + rt * ST_X + 8 * rg;
+            const uint2 i0 = *reinterpret_cast<const uint2*>(ib);
+            const uint2 i1 = *reinterpret_cast<const uint2*>(ib + TY * ST_X);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t sb = __byte_perm(k < 4 ? i0.x : i0.y, 0, 0x4440u | (uint32_t)(k & 3)) +
+                                    __byte_perm(k < 4 ? i1.x : i1.y, 0, 0x4440u | (uint32_t)(k & 3));
+                den_i[k] += sb * sb;   // <= 8192 groups between flushes: < 2^32
+                const double xd = 0.5 * (__hiloint2double(0x43300000, (int)sb) - 4503599627370496.0);
+                num[k] = fma((double)w[k], xd, num[k]);   // exact product, one fp64 rounding
+            }
+            if ((f & 8191) == 8191) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    den_d[k] += 0.25 * (double)den_i[k];   // exact (multiples of 1/4 below 2^51)
+                    den_i[k] = 0u;
+                }
+            }
+        } else if (sizeof(TI) == 1) {
             const uint2 iv = *reinterpret_cast<const uint2*>(irow);
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
@@ -288,7 +311,7 @@ __global__ void __launch_bounds__(256, 4) k_synth_acc2(const __grid_constant__ S
             if (gx + k < a.NW) {
                 a.num[(size_t)gy * a.acc_pitch + gx + k] = num[k];
                 double* dp = a.den + (size_t)gy * a.acc_pitch + gx + k;
-                *dp = sizeof(TI) == 1 ? *dp + (double)den_i[k] : den_d[k];
+                *dp = PAIR ? den_d[k] + 0.25 * (double)den_i[k] : sizeof(TI) == 1 ? *dp + (double)den_i[k] : den_d[k];
             }
         }
     }
@@ -347,7 +370,7 @@ static const char* kSynthName[kMaxLevels + 1] = {"", "synthesis_l1", "synthesis_
 
 bool encode_tensor_map_3d(CUtensorMap* map, CUtensorMapDataType dt, size_t elem_bytes, const void* base, uint64_t cols,
                           uint64_t rows, uint64_t depth, uint64_t pitch_bytes, uint64_t plane_bytes, uint32_t box_w,
-                          uint32_t box_h) {
+                          uint32_t box_h, uint32_t box_d) {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     if (!fn) {
         cudaDriverEntryPointQueryResult q;
@@ -360,7 +383,7 @@ bool encode_tensor_map_3d(CUtensorMap* map, CUtensorMapDataType dt, size_t elem_
     (void)elem_bytes;
     cuuint64_t dims[3] = {cols, rows, depth};
     cuuint64_t strides[2] = {pitch_bytes, plane_bytes};
-    cuuint32_t box[3] = {box_w, box_h, 1};
+    cuuint32_t box[3] = {box_w, box_h, box_d};
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = fn(map, dt, 3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -430,10 +453,16 @@ static int denoise_front(const TIn* in, long long in_bstride, int in_pitch, int 
         float* ll = (l < L) ? pb.approx[l] : nullptr;
         const long long ob = (long long)pb.bstride[l];
         {
-            KTimer kt(l == 1 ? (sizeof(TIn) == 1 ? "analysis_l1_u8" : sizeof(TIn) == 2 ? "analysis_l1_u16" : "analysis_l1_f32")
+            constexpr bool PAIR = std::is_same<TIn, u8pair>::value;
+            KTimer kt(l == 1 ? (PAIR ? "analysis_l1_pair" : sizeof(TIn) == 1 ? "analysis_l1_u8"
+                                : sizeof(TIn) == 2 ? "analysis_l1_u16" : "analysis_l1_f32")
                              : kAnalysisName[l],
                       st);
-            if (l == 1 && sizeof(TIn) == 1)
+            if (l == 1 && PAIR)
+                rc = launch_analysis_lift_pair(reinterpret_cast<const uint8_t*>(in), in_bstride, in_pitch, p.nH[0],
+                                               p.nW[0], ll, pb.det[1][0], pb.det[1][1], pb.det[1][2], ob, p.pitch[1],
+                                               p.nH[1], p.nW[1], sp, nb, st);
+            else if (l == 1 && sizeof(TIn) == 1)
                 rc = launch_analysis_lift_u8(reinterpret_cast<const uint8_t*>(in), in_bstride, in_pitch, p.nH[0],
                                              p.nW[0], ll, pb.det[1][0], pb.det[1][1], pb.det[1][2], ob, p.pitch[1],
                                              p.nH[1], p.nW[1], sp, nb, st);
@@ -441,6 +470,8 @@ static int denoise_front(const TIn* in, long long in_bstride, int in_pitch, int 
                 rc = launch_analysis_lift_u16(reinterpret_cast<const uint16_t*>(in), in_bstride, in_pitch, p.nH[0],
                                               p.nW[0], ll, pb.det[1][0], pb.det[1][1], pb.det[1][2], ob, p.pitch[1],
                                               p.nH[1], p.nW[1], sp, div, nb, st);
+            else if (l == 1 && sizeof(TIn) != 4)
+                rc = fail(PRNU_INVALID_ARG, "denoise: unsupported level-1 input");
             else
                 rc = launch_analysis_lift_f32(l == 1 ? reinterpret_cast<const float*>(in) : pb.approx[l - 1],
                                               l == 1 ? in_bstride : (long long)pb.bstride[l - 1],
@@ -511,18 +542,21 @@ int run_residual_accumulate(const TIn* in, const TIn* I, int nb, int H, int W, c
     const int TY = waste(28) < waste(32) - 1e-9 ? 28 : 32;
     CUtensorMap imap;
     SynthMaps m2;
-    const size_t es = sizeof(TIn);
+    // pairs (d = 2): u8 frames frame_stride apart, group f = frames 2f, 2f+1 in one depth-2 box
+    constexpr bool PAIR = std::is_same<TIn, u8pair>::value;
+    constexpr int IDEP = PAIR ? 2 : 1;
+    const size_t es = PAIR ? 1 : sizeof(TIn);
     const CUtensorMapDataType dt = es == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
                                    : es == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     if (((size_t)in_pitch * es) % 16 || ((size_t)frame_stride * es) % 16 || ((uintptr_t)I % 16) ||
-        !encode_tensor_map_3d(&imap, dt, es, I, (uint64_t)W, (uint64_t)H, (uint64_t)nb, (uint64_t)in_pitch * es,
-                              (uint64_t)frame_stride * es, ST_X, TY))
+        !encode_tensor_map_3d(&imap, dt, es, I, (uint64_t)W, (uint64_t)H, (uint64_t)nb * IDEP,
+                              (uint64_t)in_pitch * es, (uint64_t)frame_stride * es, ST_X, TY, IDEP))
         return fail(PRNU_CUDA_ERROR, "accumulation: frames not TMA-stageable (16-byte pitch / stride / base)");
     if ((rc = synth_maps(p, pb, 1, nb, s.has_A, TY / 2 + 3, &m2))) return rc;
     if ((H + TY - 1) / TY > 65535) return fail(PRNU_INVALID_ARG, "accumulation grid too large");
     static DeviceFlags attr[2];
     {
-        KTimer kt(es == 1 ? "synth_acc_l1_u8" : es == 2 ? "synth_acc_l1_u16" : "synth_acc_l1_f32", st);
+        KTimer kt(PAIR ? "synth_acc_l1_pair" : es == 1 ? "synth_acc_l1_u8" : es == 2 ? "synth_acc_l1_u16" : "synth_acc_l1_f32", st);
         dim3 g2((W + ST_X - 1) / ST_X, (H + TY - 1) / TY, 1);
         if (TY == 28) {
             if ((rc = set_smem_attr((const void*)k_synth_acc2<28, TIn>, sacc_smem_bytes<28, TIn>(), attr[0]))) return rc;
@@ -548,6 +582,9 @@ template int run_residual_accumulate<float>(const float*, const float*, int, int
 template int run_residual_accumulate<uint16_t>(const uint16_t*, const uint16_t*, int, int, int, const Pyramid&,
                                                const ShrinkParams&, const SdaDiv&, double*, double*, float*,
                                                cudaStream_t, cudaEvent_t, cudaEvent_t, long long, int);
+template int run_residual_accumulate<u8pair>(const u8pair*, const u8pair*, int, int, int, const Pyramid&,
+                                             const ShrinkParams&, const SdaDiv&, double*, double*, float*,
+                                             cudaStream_t, cudaEvent_t, cudaEvent_t, long long, int);
 template int run_residual_accumulate<uint8_t>(const uint8_t*, const uint8_t*, int, int, int, const Pyramid&,
                                               const ShrinkParams&, const SdaDiv&, double*, double*, float*,
                                               cudaStream_t, cudaEvent_t, cudaEvent_t, long long, int);

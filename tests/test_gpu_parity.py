@@ -210,6 +210,37 @@ def test_extract_odd_sizes_bit_identical_to_conventional(prnu, H, W, d):
         assert k_metric(fp.K.cpu().numpy(), K_ref, den_ref, n)[0] <= K_TOL
 
 
+@pytest.mark.parametrize("H,W,m,batch", [(64, 128, 10, 2), (33, 1024, 6, 3), (270, 480, 8, 4), (1080, 1920, 4, 2)])
+def test_extract_depth2_pairs(prnu, H, W, m, batch):
+    """d = 2 on TMA-stageable frames (W % 16 == 0, >= 32 rows): both frames of a group are
+    staged by one depth-2 box in the analysis and the accumulation (S = (b0 + b1) / 2, R-11).
+    Bit-identical to the u16-sum path (same frames at a base not 16-byte aligned) and to
+    SDA average + residual + accumulate + finalize; K against the oracle (R-14); the
+    extreme values 0 and 255 in both frames of a pair."""
+    fr = _rand_frames(m, H, W, H + 7 * W + m, 0, 256).cuda()
+    fr[0, :5] = 255
+    fr[1, :5] = 255
+    fr[0, 5:9] = 0
+    fp = prnu.extract_fingerprint(fr, 2, batch=batch)
+    raw = torch.empty(m * H * W + 16, dtype=torch.uint8, device="cuda")
+    fr_u = raw[1:1 + m * H * W].view(m, H, W)   # misaligned base: the u16-sum path
+    fr_u.copy_(fr)
+    fu = prnu.extract_fingerprint(fr_u, 2, batch=batch)
+    assert torch.equal(fp.sum_I2, fu.sum_I2) and torch.equal(fp.sum_WI, fu.sum_WI) and torch.equal(fp.K, fu.K)
+    S = prnu.sda_average(fr, 2)
+    Wr = prnu.residual(S)
+    num = torch.zeros((H, W), dtype=torch.float64, device="cuda")
+    den = torch.zeros_like(num)
+    prnu.fingerprint_accumulate(Wr, S, num, den)
+    assert torch.equal(fp.sum_I2, den) and torch.equal(fp.sum_WI, num)
+    assert torch.equal(fp.K, prnu.fingerprint_finalize(num, den))
+    if H * W <= 300_000:
+        K_ref, _, den_ref, n = oracle.extract_fingerprint(fr.cpu().numpy(), 2)
+        assert fp.n_sda == n == m // 2
+        np.testing.assert_array_equal(fp.sum_I2.cpu().numpy(), den_ref)
+        assert k_metric(fp.K.cpu().numpy(), K_ref, den_ref, n)[0] <= K_TOL
+
+
 def test_extract_deterministic_across_batches(prnu):
     v = synth.video("drift", 40, 64, 128, seed=2)
     fr = v.frames.cuda()
