@@ -127,6 +127,15 @@ __device__ __forceinline__ void st_global_v8(float* p, const float (&v)[8]) {
                  : "memory");
 }
 
+// 4 consecutive doubles with one 256-bit load / store (p 32-byte aligned): whole sectors.
+__device__ __forceinline__ void ld_global_v4d(const double* p, double (&v)[4]) {
+    asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+}
+__device__ __forceinline__ void st_global_v4d(double* p, const double (&v)[4]) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
+                 : "memory");
+}
+
 // ---------------------------------------------------------------- reductions
 // Deterministic warp-shuffle sums (the fingerprint / NCC / PCE / WDFT block
 // reductions): an xor butterfly inside each warp (lane i and lane i^o add the

@@ -61,6 +61,7 @@ struct SynthArgs {
     double* num;                 // MODE 1: fp64 accumulators [NH][acc_pitch]
     double* den;
     int acc_pitch;
+    int acc_v4;                  // num, den and acc_pitch allow 32-byte aligned 4-double accesses
     float div_d, div_r;          // u16 SDA sums: S = RN(sum / d), d and RN(1/d) (R-11)
 };
 
@@ -151,15 +152,41 @@ __global__ void __launch_bounds__(256, 4) k_synth_acc2(const __grid_constant__ S
     double num[8];
     uint32_t den_i[8];
     double den_d[8];
+    // NUM / DEN rows of this thread's 8 pixels: two 256-bit accesses each when 32-byte aligned
+    // (scalar fp64 accesses at a 64-byte lane stride touch every sector 4 times)
+    const bool acc_v = MODE && rowok && gx + 8 <= a.NW && a.acc_v4;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-        num[k] = (MODE && rowok && gx + k < a.NW) ? a.num[(size_t)gy * a.acc_pitch + gx + k] : 0.0;
+        num[k] = 0.0;
         den_i[k] = 0u;
         den_d[k] = 0.0;
     }
-    if (MODE && sizeof(TI) != 1) {   // u16 / fp32 / pairs: the fp64 accumulator in registers
+    if (acc_v) {
+        const double* np = a.num + (size_t)gy * a.acc_pitch + gx;
+        double t0[4], t1[4];
+        ld_global_v4d(np, t0);
+        ld_global_v4d(np + 4, t1);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) den_d[k] = (rowok && gx + k < a.NW) ? a.den[(size_t)gy * a.acc_pitch + gx + k] : 0.0;
+        for (int k = 0; k < 4; ++k) {
+            num[k] = t0[k];
+            num[k + 4] = t1[k];
+        }
+        if (sizeof(TI) != 1) {   // u16 / fp32 / pairs: the fp64 DEN accumulator in registers
+            const double* dp = a.den + (size_t)gy * a.acc_pitch + gx;
+            ld_global_v4d(dp, t0);
+            ld_global_v4d(dp + 4, t1);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                den_d[k] = t0[k];
+                den_d[k + 4] = t1[k];
+            }
+        }
+    } else if (MODE) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            num[k] = (rowok && gx + k < a.NW) ? a.num[(size_t)gy * a.acc_pitch + gx + k] : 0.0;
+            if (sizeof(TI) != 1) den_d[k] = (rowok && gx + k < a.NW) ? a.den[(size_t)gy * a.acc_pitch + gx + k] : 0.0;
+        }
     }
     // column-pass items (frame-invariant): item it = (coefficient column k, output rows 4 sg .. 4 sg + 3);
     // with at most one item per thread (TY <= 28) it is computed once here
@@ -306,12 +333,43 @@ __global__ void __launch_bounds__(256, 4) k_synth_acc2(const __grid_constant__ S
     }
     PRNU_DCHECK(!rowok || (gy >= 0 && gy < a.NH));
     if (MODE && rowok) {
+        double dv[8];
+        if (sizeof(TI) == 1 && !PAIR) {   // u8: DEN += the wave's exact integer sum (read here, once)
+            if (acc_v) {
+                double t0[4], t1[4];
+                const double* dp = a.den + (size_t)gy * a.acc_pitch + gx;
+                ld_global_v4d(dp, t0);
+                ld_global_v4d(dp + 4, t1);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            if (gx + k < a.NW) {
-                a.num[(size_t)gy * a.acc_pitch + gx + k] = num[k];
-                double* dp = a.den + (size_t)gy * a.acc_pitch + gx + k;
-                *dp = PAIR ? den_d[k] + 0.25 * (double)den_i[k] : sizeof(TI) == 1 ? *dp + (double)den_i[k] : den_d[k];
+                for (int k = 0; k < 4; ++k) {
+                    dv[k] = t0[k] + (double)den_i[k];
+                    dv[k + 4] = t1[k] + (double)den_i[k + 4];
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    dv[k] = gx + k < a.NW ? a.den[(size_t)gy * a.acc_pitch + gx + k] + (double)den_i[k] : 0.0;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) dv[k] = PAIR ? den_d[k] + 0.25 * (double)den_i[k] : den_d[k];
+        }
+        if (acc_v) {
+            double* np = a.num + (size_t)gy * a.acc_pitch + gx;
+            double* dp = a.den + (size_t)gy * a.acc_pitch + gx;
+            const double n0[4] = {num[0], num[1], num[2], num[3]}, n1[4] = {num[4], num[5], num[6], num[7]};
+            const double d0[4] = {dv[0], dv[1], dv[2], dv[3]}, d1[4] = {dv[4], dv[5], dv[6], dv[7]};
+            st_global_v4d(np, n0);
+            st_global_v4d(np + 4, n1);
+            st_global_v4d(dp, d0);
+            st_global_v4d(dp + 4, d1);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                if (gx + k < a.NW) {
+                    a.num[(size_t)gy * a.acc_pitch + gx + k] = num[k];
+                    a.den[(size_t)gy * a.acc_pitch + gx + k] = dv[k];
+                }
             }
         }
     }
@@ -529,6 +587,7 @@ int run_residual_accumulate(const TIn* in, const TIn* I, int nb, int H, int W, c
     s.num = num;
     s.den = den;
     s.acc_pitch = W;
+    s.acc_v4 = ((uintptr_t)num % 32 == 0) && ((uintptr_t)den % 32 == 0) && (W % 4 == 0);
     s.div_d = div.d;
     s.div_r = div.r;
     if (acc_wait && cudaStreamWaitEvent(st, acc_wait, 0) != cudaSuccess)
