@@ -401,6 +401,326 @@ __global__ void __launch_bounds__(128) k_var_row_syn(VarPass p) {
     }
 }
 
+// ------------------------------------------------------------------ fused 2-D tile passes
+// Decimated variants (symmetric / periodic): one kernel per analysis level (rows and
+// columns of a tile through shared memory: input read once, the four subbands written
+// once) and one per synthesis level (four coefficient tiles in, the level's output out),
+// instead of two separable passes with an HBM round trip in between.  Same arithmetic
+// in the same order as k_var_ana / k_var_row_ana and k_var_syn / k_var_row_syn (every
+// output bit-identical to the separable passes).
+constexpr int VT_Y = 32, VT_X = 32;   // analysis: coefficient positions per tile
+constexpr int VS_Y = 32, VS_X = 64;   // synthesis: output pixels per tile
+
+struct VarTile {
+    const float* in;          // analysis: the level's input plane;  synthesis: unused
+    const float* c[4];        // synthesis: A (null: zero approximation), ad, da, dd
+    float* out[4];            // analysis: A, ad, da, dd;  synthesis: out[0]
+    long long in_bstride, out_bstride;
+    int in_pitch, out_pitch;
+    int N_y, Np_y, N_x, Np_x; // analysis: real / periodic input extents
+    int nH, nW;               // analysis: subband extent;  synthesis: coefficient extent
+    int oH, oW;               // synthesis: output extent
+};
+
+// analysis tile layout: even / odd input columns [IR][ECP] (ECP: a row pass item reads NLD
+// float4 from column 4 u4), the odd array offset so even / odd staging lanes hit distinct banks
+template <int T>
+struct VaLayout {
+    static constexpr int IR = 2 * VT_Y + T - 2;               // input rows of the tile
+    static constexpr int EC = VT_X + T / 2 - 1;               // even / odd input columns used
+    static constexpr int NLD = (T / 2 + 3 + 3) / 4;           // float4 per row pass item and array
+    static constexpr int ECP = VT_X - 4 + 4 * NLD;            // row pitch (>= EC, multiple of 4)
+    static constexpr int OFF = ((16 - (IR * ECP) % 32) + 32) % 32;
+    static constexpr size_t floats = 2 * (size_t)IR * ECP + OFF + 2 * (size_t)IR * VT_X;
+};
+template <int T>
+__host__ __device__ constexpr size_t var_ana2d_smem() {
+    return sizeof(float) * VaLayout<T>::floats;
+}
+template <int T>
+__host__ __device__ constexpr int var_syn_nld() { return (T / 2 + 3 + 3) / 4; }   // float4 per x-pass item
+template <int T>
+__host__ __device__ constexpr int var_syn_kxp() { return VS_X / 2 - 4 + 4 * var_syn_nld<T>(); }   // X pitch
+template <int T>
+__host__ __device__ constexpr size_t var_syn2d_smem() {
+    return sizeof(float) * (4 * (size_t)(VS_Y / 2 + T / 2 - 1) * (VS_X / 2 + T / 2 - 1) +
+                            2 * (size_t)VS_Y * var_syn_kxp<T>());
+}
+
+template <int T, int MODE>
+__global__ void __launch_bounds__(256, 2) k_var_ana2d(VarTile p) {
+    using LY = VaLayout<T>;
+    constexpr int IR = LY::IR, EC = LY::EC, ECP = LY::ECP, NLD = LY::NLD;
+    extern __shared__ __align__(16) float va_smem[];
+    float* sE = va_smem;                          // [IR][ECP] x[.][base + 2j]
+    float* sO = sE + IR * ECP + LY::OFF;          // [IR][ECP] x[.][base + 2j + 1]
+    float* sL = sO + IR * ECP;                    // [IR][VT_X] lo_x
+    float* sH = sL + IR * VT_X;                   // [IR][VT_X] hi_x
+    const int tid = threadIdx.x;
+    const int b = blockIdx.z;
+    const int ky0 = blockIdx.y * VT_Y, kx0 = blockIdx.x * VT_X;
+    const int yb = 2 * ky0 - (T - 2), xb = 2 * kx0 - (T - 2);
+    const float* in = p.in + (size_t)b * p.in_bstride;
+    const float* H = c_var_h[T == 16];
+    // stage: consecutive threads on consecutive input columns (coalesced), boundary map once per
+    // element; all of a thread's loads issued before the first store (memory-level parallelism)
+    {   // thread = (input column c, row group rg): the column map once, rows rg, rg + NRG, ...
+        constexpr int CW = 2 * EC, NRG = 256 / CW, NI = (IR + NRG - 1) / NRG;
+        const int c = tid % CW, rg = tid / CW;
+        // tiles whose input region lies inside the plane (almost all): no index maps
+        const bool interior = yb >= 0 && yb + IR <= p.N_y && xb >= 0 && xb + CW <= p.N_x;
+        if (rg < NRG) {
+            const int x = interior ? xb + c : var_map<MODE>(xb + c, p.N_x, p.Np_x);
+            float* dst = (c & 1 ? sO : sE) + (c >> 1);
+            float v[NI];
+            if (interior) {
+                const float* src = in + (size_t)(yb + rg) * p.in_pitch + x;
+                const size_t step = (size_t)NRG * p.in_pitch;
+#pragma unroll
+                for (int k = 0; k < NI; ++k)
+                    if (rg + NRG * k < IR) v[k] = __ldg(src + k * step);
+            } else {
+#pragma unroll
+                for (int k = 0; k < NI; ++k) {
+                    const int r = rg + NRG * k;
+                    if (r < IR) v[k] = __ldg(in + (size_t)var_map<MODE>(yb + r, p.N_y, p.Np_y) * p.in_pitch + x);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < NI; ++k) {
+                const int r = rg + NRG * k;
+                if (r < IR) dst[r * ECP] = v[k];
+            }
+        }
+    }
+    __syncthreads();
+    PRNU_STRESS(41);
+    // (lo, hi) as one packed pair: FFMA2 of the sample with (H_[i], G_[i]), lane-wise the fmaf chain
+    float2 hg[T];
+#pragma unroll
+    for (int i = 0; i < T; ++i) hg[i] = make_float2(H[i], (i & 1) ? -H[T - 1 - i] : H[T - 1 - i]);
+    // rows: item = (staged row r, coefficient columns 4 u4 .. 4 u4 + 3), inputs by float4
+    for (int e = tid; e < IR * (VT_X / 4); e += 256) {
+        const int r = e / (VT_X / 4), u4 = e - r * (VT_X / 4);
+        float ev[4 * NLD], ov[4 * NLD];
+#pragma unroll
+        for (int k = 0; k < NLD; ++k) {
+            const float4 a = *reinterpret_cast<const float4*>(sE + r * ECP + 4 * u4 + 4 * k);
+            const float4 c = *reinterpret_cast<const float4*>(sO + r * ECP + 4 * u4 + 4 * k);
+            ev[4 * k] = a.x; ev[4 * k + 1] = a.y; ev[4 * k + 2] = a.z; ev[4 * k + 3] = a.w;
+            ov[4 * k] = c.x; ov[4 * k + 1] = c.y; ov[4 * k + 2] = c.z; ov[4 * k + 3] = c.w;
+        }
+        float2 acc[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            acc[q] = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int i = 0; i < T; ++i) acc[q] = ffma2((i & 1) ? ov[q + i / 2] : ev[q + i / 2], hg[i], acc[q]);
+        }
+        *reinterpret_cast<float4*>(sL + r * VT_X + 4 * u4) = make_float4(acc[0].x, acc[1].x, acc[2].x, acc[3].x);
+        *reinterpret_cast<float4*>(sH + r * VT_X + 4 * u4) = make_float4(acc[0].y, acc[1].y, acc[2].y, acc[3].y);
+    }
+    __syncthreads();
+    PRNU_STRESS(42);
+    // columns: item = (coefficient rows 4 q4 .. 4 q4 + 3, column u); (aa, ad) from lo_x, (da, dd) from hi_x
+    const size_t ob = (size_t)b * p.out_bstride;
+    for (int e = tid; e < (VT_Y / 4) * VT_X; e += 256) {
+        const int q4 = e / VT_X, u = e - q4 * VT_X;
+        const int gx = kx0 + u;
+        float lv[T + 6], hv[T + 6];
+#pragma unroll
+        for (int j = 0; j < T + 6; ++j) {
+            lv[j] = sL[(8 * q4 + j) * VT_X + u];
+            hv[j] = sH[(8 * q4 + j) * VT_X + u];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int gy = ky0 + 4 * q4 + q;
+            float2 la = make_float2(0.f, 0.f), ha = la;   // (aa, ad), (da, dd)
+#pragma unroll
+            for (int i = 0; i < T; ++i) {
+                la = ffma2(lv[2 * q + i], hg[i], la);
+                ha = ffma2(hv[2 * q + i], hg[i], ha);
+            }
+            if (gy < p.nH && gx < p.nW) {
+                const size_t o = ob + (size_t)gy * p.out_pitch + gx;
+                p.out[0][o] = la.x;
+                p.out[1][o] = la.y;
+                p.out[2][o] = ha.x;
+                p.out[3][o] = ha.y;
+            }
+        }
+    }
+}
+
+template <int T, int MODE>
+__global__ void __launch_bounds__(256, 2) k_var_syn2d(VarTile p) {
+    constexpr int KY = VS_Y / 2 + T / 2 - 1, KX = VS_X / 2 + T / 2 - 1;   // coefficient rows / columns
+    constexpr int KXP = var_syn_kxp<T>(), NLD = var_syn_nld<T>();
+    extern __shared__ __align__(16) float vs_smem[];
+    float* sC = vs_smem;                 // [4][KY][KX]: A, ad, da, dd
+    float* sX0 = sC + 4 * KY * KX;       // [VS_Y][KXP] synthesis along y of (A, ad)
+    float* sX1 = sX0 + VS_Y * KXP;       // [VS_Y][KXP] of (da, dd)
+    const int tid = threadIdx.x;
+    const int b = blockIdx.z;
+    const int ty0 = blockIdx.y * VS_Y, tx0 = blockIdx.x * VS_X;
+    const int k0y = ty0 / 2, k0x = tx0 / 2;
+    const int n_y = p.nH, n_x = p.nW;
+    const size_t cb = (size_t)b * p.in_bstride;
+    const float* H = c_var_h[T == 16];
+    // coefficients k = k0 + j: dropped outside [0, n) (symmetric), mod n (periodic)
+    {   // thread = (coefficient column i, row group rg): the column map once, then rows
+        // rg, rg + NRG, ... of the four planes; all loads before the first store
+        constexpr int NRG = 256 / KX, NJ = (KY + NRG - 1) / NRG;
+        const int i = tid % KX, rg = tid / KX;
+        if (rg < NRG) {
+            int kx = k0x + i;
+            bool okx = true;
+            if (MODE == VM_SYM) okx = kx < n_x;
+            else kx = var_mod(kx, n_x);
+            // tiles whose coefficient region lies inside the planes (almost all): no index maps
+            const bool interior = k0y + KY <= n_y && k0x + KX <= n_x;
+            float v[4][NJ];
+#pragma unroll
+            for (int pl = 0; pl < 4; ++pl) {
+                // (no dynamic index into the parameter struct: it would copy it to local memory)
+                const float* src = p.c[pl];
+                if (interior) {
+                    const float* q = src ? src + cb + (size_t)(k0y + rg) * p.in_pitch + kx : nullptr;
+                    const size_t step = (size_t)NRG * p.in_pitch;
+#pragma unroll
+                    for (int k = 0; k < NJ; ++k)
+                        v[pl][k] = (q && rg + NRG * k < KY) ? __ldg(q + k * step) : 0.f;
+                    continue;
+                }
+#pragma unroll
+                for (int k = 0; k < NJ; ++k) {
+                    const int j = rg + NRG * k;
+                    int ky = k0y + j;
+                    bool ok = okx && j < KY && src != nullptr;
+                    if (MODE == VM_SYM) ok = ok && ky < n_y;
+                    else ky = var_mod(ky, n_y);
+                    v[pl][k] = ok ? __ldg(src + cb + (size_t)ky * p.in_pitch + kx) : 0.f;
+                }
+            }
+#pragma unroll
+            for (int pl = 0; pl < 4; ++pl)
+#pragma unroll
+                for (int k = 0; k < NJ; ++k) {
+                    const int j = rg + NRG * k;
+                    if (j < KY) sC[(pl * KY + j) * KX + i] = v[pl][k];
+                }
+        }
+    }
+    __syncthreads();
+    PRNU_STRESS(43);
+    const float* sA = sC;
+    const float* sAD = sC + KY * KX;
+    const float* sDA = sC + 2 * KY * KX;
+    const float* sDD = sC + 3 * KY * KX;
+    // synthesis taps of the (even, odd) output pair: (H_[2m], H_[2m+1]) and (G_[2m], G_[2m+1])
+    float2 hp[T / 2], gp[T / 2];
+#pragma unroll
+    for (int m = 0; m < T / 2; ++m) {
+        hp[m] = make_float2(H[2 * m], H[2 * m + 1]);
+        gp[m] = make_float2(H[T - 1 - 2 * m], -H[T - 2 - 2 * m]);
+    }
+    // along y: item = output rows 4 q2 .. 4 q2 + 3 (pairs q = 2 q2, 2 q2 + 1) of coefficient column i;
+    // pair q: x[2q + e] = sum_m H_[e + 2m] a[q + (T-2)/2 - m] + G_[e + 2m] d[...] (compile-time taps),
+    // coefficient rows 2 q2 .. 2 q2 + T/2 loaded once
+    for (int e = tid; e < (VS_Y / 4) * KX; e += 256) {
+        const int q2 = e / KX, i = e - q2 * KX;
+        float ca[T / 2 + 1], cad[T / 2 + 1], cda[T / 2 + 1], cdd[T / 2 + 1];
+#pragma unroll
+        for (int j = 0; j <= T / 2; ++j) {
+            const int o = (2 * q2 + j) * KX + i;
+            ca[j] = sA[o];
+            cad[j] = sAD[o];
+            cda[j] = sDA[o];
+            cdd[j] = sDD[o];
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {   // q = 2 q2 + h: rows j = h + (T-2)/2 - m relative to 2 q2
+            float2 x0 = make_float2(0.f, 0.f), x1 = x0;   // (even, odd) output rows
+#pragma unroll
+            for (int m = 0; m < T / 2; ++m) {
+                const int j = h + (T - 2) / 2 - m;
+                x0 = ffma2(ca[j], hp[m], x0);
+                x0 = ffma2(cad[j], gp[m], x0);
+                x1 = ffma2(cda[j], hp[m], x1);
+                x1 = ffma2(cdd[j], gp[m], x1);
+            }
+            const int r = 4 * q2 + 2 * h;
+            sX0[r * KXP + i] = x0.x;
+            sX0[(r + 1) * KXP + i] = x0.y;
+            sX1[r * KXP + i] = x1.x;
+            sX1[(r + 1) * KXP + i] = x1.y;
+        }
+    }
+    __syncthreads();
+    PRNU_STRESS(44);
+    // along x: item = 8 output pixels 8 q4 .. 8 q4 + 7 (pairs q = 4 q4 + h) of row u; X columns
+    // 4 q4 .. 4 q4 + T/2 + 2 by float4; lanes on consecutive items
+    float* out = p.out[0] + (size_t)b * p.out_bstride;
+    const bool v4 = (p.out_pitch % 4 == 0) && ((uintptr_t)out % 16 == 0);
+    for (int e = tid; e < VS_Y * (VS_X / 8); e += 256) {
+        const int u = e / (VS_X / 8), q4 = e - u * (VS_X / 8);
+        const int gy = ty0 + u, gx = tx0 + 8 * q4;
+        if (gy >= p.oH || gx >= p.oW) continue;
+        float x0[4 * NLD], x1[4 * NLD];
+#pragma unroll
+        for (int k = 0; k < NLD; ++k) {
+            const float4 a = *reinterpret_cast<const float4*>(sX0 + u * KXP + 4 * q4 + 4 * k);
+            const float4 c = *reinterpret_cast<const float4*>(sX1 + u * KXP + 4 * q4 + 4 * k);
+            x0[4 * k] = a.x; x0[4 * k + 1] = a.y; x0[4 * k + 2] = a.z; x0[4 * k + 3] = a.w;
+            x1[4 * k] = c.x; x1[4 * k + 1] = c.y; x1[4 * k + 2] = c.z; x1[4 * k + 3] = c.w;
+        }
+        float o8[8];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {   // pair q = 4 q4 + h: X columns h + (T-2)/2 - m relative to 4 q4
+            float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int m = 0; m < T / 2; ++m) {
+                acc = ffma2(x0[h + (T - 2) / 2 - m], hp[m], acc);
+                acc = ffma2(x1[h + (T - 2) / 2 - m], gp[m], acc);
+            }
+            o8[2 * h] = acc.x;
+            o8[2 * h + 1] = acc.y;
+        }
+        float* o = out + (size_t)gy * p.out_pitch + gx;
+        if (v4 && gx + 8 <= p.oW) {
+            reinterpret_cast<float4*>(o)[0] = make_float4(o8[0], o8[1], o8[2], o8[3]);
+            reinterpret_cast<float4*>(o)[1] = make_float4(o8[4], o8[5], o8[6], o8[7]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (gx + k < p.oW) o[k] = o8[k];
+        }
+    }
+}
+
+template <int T, int MODE>
+static int var_tile_launch(bool syn, const VarTile& p, int nb, cudaStream_t st) {
+    static DeviceFlags attr[2];
+    int rc;
+    if (syn) {
+        if ((rc = set_smem_attr((const void*)k_var_syn2d<T, MODE>, var_syn2d_smem<T>(), attr[1]))) return rc;
+        const dim3 g((unsigned)((p.oW + VS_X - 1) / VS_X), (unsigned)((p.oH + VS_Y - 1) / VS_Y), (unsigned)nb);
+        k_var_syn2d<T, MODE><<<g, 256, var_syn2d_smem<T>(), st>>>(p);
+    } else {
+        if ((rc = set_smem_attr((const void*)k_var_ana2d<T, MODE>, var_ana2d_smem<T>(), attr[0]))) return rc;
+        const dim3 g((unsigned)((p.nW + VT_X - 1) / VT_X), (unsigned)((p.nH + VT_Y - 1) / VT_Y), (unsigned)nb);
+        k_var_ana2d<T, MODE><<<g, 256, var_ana2d_smem<T>(), st>>>(p);
+    }
+    return PRNU_OK;
+}
+
+static int var_tile_dispatch(int taps, int mode, bool syn, const VarTile& p, int nb, cudaStream_t st) {
+    if (nb > 65535) return fail(PRNU_INVALID_ARG, "variant: more than 65535 frames in one launch");
+    if (taps == 8) return mode == VM_SYM ? var_tile_launch<8, VM_SYM>(syn, p, nb, st) : var_tile_launch<8, VM_PER>(syn, p, nb, st);
+    return mode == VM_SYM ? var_tile_launch<16, VM_SYM>(syn, p, nb, st) : var_tile_launch<16, VM_PER>(syn, p, nb, st);
+}
+
 template <int T, int MODE>
 static void var_launch(bool syn, int ax, const VarPass& p, int nb, cudaStream_t st) {
     // row passes: shared-memory staged, except the 8-tap decimated analysis, for which the
@@ -513,6 +833,78 @@ int variant_filter(int taps, double* h) {
     return fail(PRNU_BAD_PARAMETER, "taps must be 8 or 16");
 }
 
+// Decimated variants through the fused tile kernels: per level one analysis launch
+// (input -> A, ad, da, dd), the shrink, and per level one synthesis launch.
+template <typename NoiseFn>
+static int run_residual_variant_tiles(const VarGeom& g, const float* in, int nb, int H, int W, const ShrinkParams& sp,
+                                      float* W_out, float* const (&A)[2], float* const (&R)[3], NoiseFn noise,
+                                      cudaStream_t st) {
+    int rc;
+    const float* cur = in;
+    long long cur_bs = (long long)H * W;
+    int cur_pitch = W;
+    for (int l = 1; l <= g.L; ++l) {
+        const int nHl = g.nH[l], nWl = g.nW[l];
+        {
+            VarTile p{};
+            p.in = cur;
+            p.out[0] = A[l & 1];
+            p.out[1] = R[1];   // ad = hi_y(lo_x)
+            p.out[2] = R[0];   // da = lo_y(hi_x)
+            p.out[3] = R[2];   // dd
+            p.in_bstride = cur_bs;
+            p.in_pitch = cur_pitch;
+            p.out_bstride = (long long)nHl * nWl;
+            p.out_pitch = nWl;
+            p.N_y = g.inH[l];
+            p.Np_y = g.perH[l];
+            p.N_x = g.inW[l];
+            p.Np_x = g.perW[l];
+            p.nH = nHl;
+            p.nW = nWl;
+            KTimer kt("variant_ana", st);
+            if ((rc = var_tile_dispatch(g.T, g.mode, false, p, nb, st))) return rc;
+        }
+        count_launch();
+        if ((rc = check_launch("k_var_ana2d"))) return rc;
+        {
+            const float* src[3] = {R[0], R[1], R[2]};
+            float* dst[3] = {noise(l, 0), noise(l, 1), noise(l, 2)};
+            KTimer kt("variant_shrink", st);
+            if ((rc = launch_shrink_strip(src, dst, (long long)nHl * nWl, nWl, nHl, nWl, sp, nb, st))) return rc;
+        }
+        count_launch();
+        if ((rc = check_launch("k_shrink (variant)"))) return rc;
+        cur = A[l & 1];
+        cur_bs = (long long)nHl * nWl;
+        cur_pitch = nWl;
+    }
+    for (int l = g.L; l >= 1; --l) {
+        const int nHl = g.nH[l], nWl = g.nW[l];
+        VarTile p{};
+        p.c[0] = l == g.L ? nullptr : A[l & 1];
+        p.c[1] = noise(l, 1);
+        p.c[2] = noise(l, 0);
+        p.c[3] = noise(l, 2);
+        p.out[0] = l == 1 ? W_out : A[(l - 1) & 1];
+        p.in_bstride = (long long)nHl * nWl;
+        p.in_pitch = nWl;
+        p.nH = nHl;
+        p.nW = nWl;
+        p.oH = l == 1 ? H : g.inH[l];
+        p.oW = l == 1 ? W : g.inW[l];
+        p.out_bstride = (long long)p.oH * p.oW;
+        p.out_pitch = p.oW;
+        {
+            KTimer kt("variant_syn", st);
+            if ((rc = var_tile_dispatch(g.T, g.mode, true, p, nb, st))) return rc;
+        }
+        count_launch();
+        if ((rc = check_launch("k_var_syn2d"))) return rc;
+    }
+    return PRNU_OK;
+}
+
 int run_residual_variant(const float* in, int nb, int H, int W, int levels, int taps, int boundary, int transform,
                          const ShrinkParams& sp, float* W_out, float* ws, cudaStream_t st) {
     const VarGeom g = var_geom(H, W, levels, taps, boundary, transform);
@@ -524,6 +916,7 @@ int run_residual_variant(const float* in, int nb, int H, int W, int levels, int 
     float* NZ = A[1] + 4 * g.approx * nb;
     auto noise = [&](int l, int k) { return NZ + (g.sub_off[l] + (size_t)k * g.nH[l] * g.nW[l]) * nb; };
     int rc;
+    if (g.mode != VM_SWT) return run_residual_variant_tiles(g, in, nb, H, W, sp, W_out, A, R, noise, st);
     const float* cur = in;
     long long cur_bs = (long long)H * W;
     int cur_pitch = W;

@@ -1,10 +1,11 @@
-"""Per-pass times of the f3 variant residual (KTimer names of csrc/variant.cu), 8 FHD frames."""
+"""Per-pass times of the f3 variant residual (KTimer names of csrc/variant.cu), NB (argv[1], default 8) FHD frames."""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_1909_04573_b200 as prnu
 
-I = torch.rand((8, 1080, 1920), device="cuda") * 255
+NB = int(sys.argv[1]) if len(sys.argv) > 1 else 8
+I = torch.rand((NB, 1080, 1920), device="cuda") * 255
 for v in ((8, 0, 0), (16, 0, 0), (8, 1, 0), (8, 1, 1), (16, 1, 1)):
     var = prnu.DenoiseVariant(*v)
     out = torch.empty_like(I)
@@ -25,6 +26,6 @@ for v in ((8, 0, 0), (16, 0, 0), (8, 1, 0), (8, 1, 1), (16, 1, 1)):
         nm = names.raw[64 * k: 64 * k + 64].split(b"\0")[0].decode()
         rows.append((tot[k] / 3, cnt[k] / 3, nm))
     s = sum(r[0] for r in rows)
-    print(f"== {v}: {s:.3f} ms per call ({s / 8:.4f} ms/frame)")
+    print(f"== {v}: {s:.3f} ms per call of {NB} frames ({s / NB:.4f} ms/frame)")
     for t, c, nm in sorted(rows, reverse=True):
         print(f"   {nm:20s} {t:8.3f} ms  {c:5.1f} launches")
