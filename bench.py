@@ -272,8 +272,11 @@ def run_reference(args, rank, world):
 
 # ------------------------------------------------------------------ main arm
 def variant_alg_bytes(H, W, levels, taps, boundary, transform):
-    """Algorithmic HBM bytes of one f3 variant residual (csrc/variant.cu): every pass reads
-    its input planes once and writes its outputs once (fp32)."""
+    """Algorithmic HBM bytes of one f3 variant residual (csrc/variant.cu), fp32: decimated
+    variants (fused tile kernels) read each level's input and write its four subbands once,
+    the shrink reads and writes three planes, each synthesis level reads four (three at the
+    coarsest) subbands and writes its output; undecimated variants (separable passes) also
+    move the row-pass intermediates."""
     m = 1 << levels
     h, w = H, W
     tot = 0
@@ -288,14 +291,16 @@ def variant_alg_bytes(H, W, levels, taps, boundary, transform):
         else:
             nh, nw = (h + taps - 1) // 2, (w + taps - 1) // 2
         dims.append((h, w, nh, nw))
-        tot += h * w + 2 * h * nw            # rows pass
-        tot += 2 * h * nw + 4 * nh * nw      # columns pass
+        tot += h * w + 4 * nh * nw           # analysis in, four subbands out
+        if transform:
+            tot += 4 * h * nw                # row-pass intermediates (lo, hi) written + read
         tot += 6 * nh * nw                   # shrink (3 in, 3 out)
         h, w = nh, nw
     for l in range(levels, 0, -1):
         ih, iw, nh, nw = dims[l - 1]
-        tot += (3 if l == levels else 4) * nh * nw + 2 * ih * nw   # synthesis columns
-        tot += 2 * ih * nw + ih * iw                               # synthesis rows
+        tot += (3 if l == levels else 4) * nh * nw + ih * iw       # synthesis in / out
+        if transform:
+            tot += 4 * ih * nw                                     # column-pass intermediates
     return 4 * tot
 
 
@@ -462,8 +467,8 @@ def main():
         luma_bytes = 16 * H * W * (3 + 4)
         pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
         peak_hbm = json.load(open(pk)).get("hbm_gbs", 6650.0) if os.path.exists(pk) else 6650.0
-        # f3 denoiser variants: residual of 8 FHD SDA-like fp32 frames per call
-        Ivar = frames[:8].float()
+        # f3 denoiser variants: residual of 64 FHD SDA-like fp32 frames per call
+        Ivar = frames[:64].float()
         f3 = {}
         for name, v in (("db8_sym", (16, 0, 0)), ("db4_per", (8, 1, 0)), ("db8_per", (16, 1, 0)),
                         ("db4_swt", (8, 1, 1)), ("db8_swt", (16, 1, 1))):
@@ -471,7 +476,8 @@ def main():
             out = torch.empty_like(Ivar)
             t = timed(lambda: prnu.residual_variant(Ivar, var, out=out), reps=3)
             gb = variant_alg_bytes(H, W, 4, *v) * Ivar.shape[0] / (t / 1000.0) / 1e9
-            f3[name] = {"ms_per_frame": t / Ivar.shape[0], "alg_GBps": gb, "frac_hbm": gb / peak_hbm}
+            f3[name] = {"ms_per_frame": t / Ivar.shape[0], "alg_GBps": gb, "frac_hbm": gb / peak_hbm,
+                        "x_default": (t / Ivar.shape[0]) / (ms_step / denoise_per_step)}
         # BASELINE config 4 shape (camera identification): 64 fingerprints of 300 frames
         # 1280x720 at depth 30, then 64 query residuals x 64 fingerprints = 4096 PCEs
         # (one camera's synthetic frames reused for every camera: throughput only)

@@ -766,6 +766,7 @@ struct VarGeom {
     int inH[8], inW[8];     // real input extent of level l (l = 1..L)
     int perH[8], perW[8];   // period of the level's input (== real except padded level 1)
     int nH[8], nW[8];       // subband extent of level l
+    int P[8];               // row pitch of level l's planes (the tile path: a multiple of 8 floats)
     size_t sub_off[8];      // offset of level l's three noise planes (floats, per frame)
     size_t scratch, approx, noise;   // floats per frame: one scratch plane, one approximation plane, all noise
 };
@@ -795,8 +796,10 @@ static VarGeom var_geom(int H, int W, int levels, int taps, int boundary, int tr
             g.nH[l] = (h + taps - 1) / 2;
             g.nW[l] = (w + taps - 1) / 2;
         }
+        // 32-byte rows for the tile kernels' vector accesses; dense for the separable (SWT) passes
+        g.P[l] = g.mode == VM_SWT ? g.nW[l] : (int)align_up((size_t)g.nW[l], 8);
         g.sub_off[l] = off;
-        off += 3 * (size_t)g.nH[l] * g.nW[l];
+        off += 3 * (size_t)g.nH[l] * g.P[l];
         h = g.nH[l];
         w = g.nW[l];
     }
@@ -804,7 +807,7 @@ static VarGeom var_geom(int H, int W, int levels, int taps, int boundary, int tr
     size_t sc = 0, ap = 0;
     for (int l = 1; l <= levels; ++l) {
         sc = std::max(sc, (size_t)std::max(g.inH[l], g.perH[l]) * g.nW[l]);
-        ap = std::max(ap, (size_t)g.nH[l] * g.nW[l]);
+        ap = std::max(ap, (size_t)g.nH[l] * g.P[l]);
     }
     g.scratch = align_up(sc, 64);
     g.approx = align_up(ap, 64);
@@ -844,7 +847,7 @@ static int run_residual_variant_tiles(const VarGeom& g, const float* in, int nb,
     long long cur_bs = (long long)H * W;
     int cur_pitch = W;
     for (int l = 1; l <= g.L; ++l) {
-        const int nHl = g.nH[l], nWl = g.nW[l];
+        const int nHl = g.nH[l], nWl = g.nW[l], Pl = g.P[l];
         {
             VarTile p{};
             p.in = cur;
@@ -854,8 +857,8 @@ static int run_residual_variant_tiles(const VarGeom& g, const float* in, int nb,
             p.out[3] = R[2];   // dd
             p.in_bstride = cur_bs;
             p.in_pitch = cur_pitch;
-            p.out_bstride = (long long)nHl * nWl;
-            p.out_pitch = nWl;
+            p.out_bstride = (long long)nHl * Pl;
+            p.out_pitch = Pl;
             p.N_y = g.inH[l];
             p.Np_y = g.perH[l];
             p.N_x = g.inW[l];
@@ -871,30 +874,30 @@ static int run_residual_variant_tiles(const VarGeom& g, const float* in, int nb,
             const float* src[3] = {R[0], R[1], R[2]};
             float* dst[3] = {noise(l, 0), noise(l, 1), noise(l, 2)};
             KTimer kt("variant_shrink", st);
-            if ((rc = launch_shrink_strip(src, dst, (long long)nHl * nWl, nWl, nHl, nWl, sp, nb, st))) return rc;
+            if ((rc = launch_shrink_strip(src, dst, (long long)nHl * Pl, Pl, nHl, nWl, sp, nb, st))) return rc;
         }
         count_launch();
         if ((rc = check_launch("k_shrink (variant)"))) return rc;
         cur = A[l & 1];
-        cur_bs = (long long)nHl * nWl;
-        cur_pitch = nWl;
+        cur_bs = (long long)nHl * Pl;
+        cur_pitch = Pl;
     }
     for (int l = g.L; l >= 1; --l) {
-        const int nHl = g.nH[l], nWl = g.nW[l];
+        const int nHl = g.nH[l], nWl = g.nW[l], Pl = g.P[l];
         VarTile p{};
         p.c[0] = l == g.L ? nullptr : A[l & 1];
         p.c[1] = noise(l, 1);
         p.c[2] = noise(l, 0);
         p.c[3] = noise(l, 2);
         p.out[0] = l == 1 ? W_out : A[(l - 1) & 1];
-        p.in_bstride = (long long)nHl * nWl;
-        p.in_pitch = nWl;
+        p.in_bstride = (long long)nHl * Pl;
+        p.in_pitch = Pl;
         p.nH = nHl;
         p.nW = nWl;
         p.oH = l == 1 ? H : g.inH[l];
         p.oW = l == 1 ? W : g.inW[l];
-        p.out_bstride = (long long)p.oH * p.oW;
-        p.out_pitch = p.oW;
+        p.out_pitch = l == 1 ? W : g.P[l - 1];   // the level l-1 approximation plane (pitched)
+        p.out_bstride = (long long)p.oH * p.out_pitch;
         {
             KTimer kt("variant_syn", st);
             if ((rc = var_tile_dispatch(g.T, g.mode, true, p, nb, st))) return rc;
@@ -914,7 +917,7 @@ int run_residual_variant(const float* in, int nb, int H, int W, int levels, int 
     float* A[2] = {ws + 2 * g.scratch * nb, ws + (2 * g.scratch + g.approx) * nb};
     float* R[3] = {A[1] + g.approx * nb, A[1] + 2 * g.approx * nb, A[1] + 3 * g.approx * nb};
     float* NZ = A[1] + 4 * g.approx * nb;
-    auto noise = [&](int l, int k) { return NZ + (g.sub_off[l] + (size_t)k * g.nH[l] * g.nW[l]) * nb; };
+    auto noise = [&](int l, int k) { return NZ + (g.sub_off[l] + (size_t)k * g.nH[l] * g.P[l]) * nb; };
     int rc;
     if (g.mode != VM_SWT) return run_residual_variant_tiles(g, in, nb, H, W, sp, W_out, A, R, noise, st);
     const float* cur = in;
