@@ -75,6 +75,8 @@ out["blk500_pce"], out["blk500_ncc"] = pb, nb
 out["wdft"] = prnu.wdft(torch.stack([out["fp_d3_K"], out["fp_d1_K"]]))
 for taps, bnd, tr in ((16, 0, 0), (8, 1, 0), (8, 1, 1)):
     out[f"var_{taps}_{bnd}_{tr}"] = prnu.residual_variant(u8(2, 40, 52).float(), prnu.DenoiseVariant(taps, bnd, tr))
+for taps, bnd in ((16, 0), (8, 1)):   # the tile kernels with interior tiles
+    out[f"var_{taps}_{bnd}_0_270x480"] = prnu.residual_variant(u8(3, 270, 480).float(), prnu.DenoiseVariant(taps, bnd, 0))
 torch.cuda.synchronize()
 print(f"workload {time.perf_counter() - t0:.2f} s")
 out = {k: t.cpu() for k, t in out.items()}
