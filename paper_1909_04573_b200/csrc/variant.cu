@@ -6,11 +6,15 @@
 //
 // Same method as the default path (decomposition, local-variance Wiener shrink of
 // every detail subband with mirror windows, noise-domain reconstruction
-// W = I - F(I), R-10), built from separable one-dimensional passes:
+// W = I - F(I), R-10):
 //
-//   k_var_ana<T, MODE, AX>   one analysis pass along x (AX = 0) or y (AX = 1)
-//   launch_shrink_strip      shrink.cu's streaming shrink
-//   k_var_syn<T, MODE, AX>   one synthesis pass (gather form); a null approximation is zero
+//   decimated variants (db4 / db8, symmetric or pad + periodic): fused 2-D tile kernels,
+//     k_var_ana2d<T, MODE> (one launch per analysis level: rows and columns of a tile in
+//     shared memory, the four subbands written once) and k_var_syn2d<T, MODE> (one launch
+//     per synthesis level);
+//   undecimated variants: separable passes k_var_row_ana / k_var_ana_col and
+//     k_var_row_syn / k_var_syn_col (circular, dilation s);
+//   launch_shrink_strip (shrink.cu) between analysis and synthesis.
 //
 // Filter convention (GPU side; R-5 generalised to T taps): H_ is the
 // minimum-phase lowpass in common.cuh's order (PRNU_H0..7 for T = 8),
@@ -22,8 +26,6 @@
 //                        synthesis is the transpose of its orthogonal analysis)
 //   undecimated          a[t] = sum_i H_[i] x[(t - s (T-1-i)) mod N],
 //                        x[t] = 1/2 sum_i H_[i] a[(t + s (T-1-i)) mod N] + G_[i] d[...]
-// The passes are gathers, one thread per output, coalesced along x; they are
-// HBM/L2-bound (algorithmic bytes in DESIGN.md §6).
 #include "common.cuh"
 
 namespace prnu {
@@ -64,234 +66,111 @@ __device__ __forceinline__ int var_map(int i, int N, int Np) {
     return var_mod(i, N);
 }
 
+// ------------------------------------------------------------------ separable passes (undecimated)
+// The undecimated variants (R-25) run as separable 1-D passes with circular indexing at
+// dilation s = 2^(l-1): a[t] = sum_i H_[i] x[(t - s (T-1-i)) mod N] (d with G_), and the
+// synthesis x[t] = 1/2 sum_i H_[i] a[(t + s (T-1-i)) mod N] + G_[i] d[...].
 struct VarPass {
     const float* in[4];   // analysis: plane pl reads in[pl]; synthesis: (in[2pl], in[2pl+1]) = (a, d)
     float* out[4];        // analysis: plane pl writes (out[2pl], out[2pl+1]) = (lo, hi); synthesis: out[pl]
     long long in_bstride, out_bstride;   // floats between frames
     int in_pitch, out_pitch;             // floats between rows
-    int N, Np;     // analysis: real / periodic length of the input axis; synthesis: n (coefficients)
-    int nout;      // outputs along the axis
+    int N;         // length of the axis the pass filters (circular)
+    int nout;      // outputs along the axis (== N)
     int other;     // extent along the other axis
-    int s;         // undecimated dilation 2^(l-1)
+    int s;         // dilation 2^(l-1)
     int nplanes;
 };
 
-template <int AX>
-__device__ __forceinline__ size_t var_at(int k, int o, int pitch) {
-    return AX == 0 ? (size_t)o * pitch + k : (size_t)k * pitch + o;
-}
-
-// grid: x over the x extent (128 threads per CTA), y over the y extent in runs of
-// VAR_RY rows per thread (amortises the index set-up and the CTA launch; the rows
-// a run shares hit L1), z = frame * nplanes + plane
+// column passes: grid x over the columns (128 threads per CTA), y over runs of 8 outputs of
+// one polyphase component, z = frame * nplanes + plane
 constexpr int VAR_RY = 8;
 
-template <int T, int MODE, int AX>
-__global__ void __launch_bounds__(128) k_var_ana(VarPass p) {
+template <int T>
+__global__ void __launch_bounds__(128) k_var_ana_col(VarPass p) {
     const int pl = blockIdx.z % p.nplanes, b = blockIdx.z / p.nplanes;
     const int x = blockIdx.x * 128 + threadIdx.x;
-    const int ey = AX == 0 ? p.other : p.nout;
-    if (x >= (AX == 0 ? p.nout : p.other)) return;
+    if (x >= p.other) return;
     const float* in = p.in[pl] + (size_t)b * p.in_bstride;
     float* lo = p.out[2 * pl] + (size_t)b * p.out_bstride;
     float* hi = p.out[2 * pl + 1] + (size_t)b * p.out_bstride;
     const float* H = c_var_h[T == 16];
-    const int y0 = blockIdx.y * VAR_RY, y1 = min(y0 + VAR_RY, ey);
-    if (AX == 1 && MODE == VM_SWT) {
-        // undecimated, along y, dilation s: run r = q s + ph holds the outputs
-        // t_u = 8 s q + ph + s u (one polyphase component), which read input rows
-        // 8 s q + ph + s j, j = u + i - (T-1): T + 7 rows, each loaded once
-        const int s_ = p.s, q = blockIdx.y / s_, ph = blockIdx.y - q * s_;
-        const int tb = 8 * s_ * q + ph;
-        if (tb >= p.nout) return;
-        float v[T + 7];
+    // run r = q s + ph holds the outputs t_u = 8 s q + ph + s u (one polyphase component),
+    // which read input rows 8 s q + ph + s j, j = u + i - (T-1): T + 7 rows, each loaded once
+    const int s_ = p.s, q = blockIdx.y / s_, ph = blockIdx.y - q * s_;
+    const int tb = 8 * s_ * q + ph;
+    if (tb >= p.nout) return;
+    float v[T + 7];
 #pragma unroll
-        for (int j = 0; j < T + 7; ++j)
-            v[j] = __ldg(in + var_at<AX>(var_mod(tb + s_ * (j - (T - 1)), p.N), x, p.in_pitch));
+    for (int j = 0; j < T + 7; ++j)
+        v[j] = __ldg(in + (size_t)var_mod(tb + s_ * (j - (T - 1)), p.N) * p.in_pitch + x);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int t = tb + s_ * u;
-            if (t >= p.nout) break;
-            float a = 0.f, d = 0.f;
-#pragma unroll
-            for (int i = 0; i < T; ++i) {
-                const float g = (i & 1) ? -H[T - 1 - i] : H[T - 1 - i];
-                a = fmaf(H[i], v[u + i], a);
-                d = fmaf(g, v[u + i], d);
-            }
-            const size_t oi = var_at<AX>(t, x, p.out_pitch);
-            lo[oi] = a;
-            hi[oi] = d;
-        }
-        return;
-    }
-    if (AX == 1 && MODE != VM_SWT) {
-        // decimated, along y: the run's outputs k0 .. k0+7 read input rows
-        // 2 k0 - (T-2) .. 2 k0 + 15: each loaded once into registers
-        constexpr int NR = 2 * VAR_RY + T - 2;
-        float v[NR];
-#pragma unroll
-        for (int j = 0; j < NR; ++j)
-            v[j] = __ldg(in + var_at<AX>(var_map<MODE>(2 * y0 - (T - 2) + j, p.N, p.Np), x, p.in_pitch));
-#pragma unroll
-        for (int r = 0; r < VAR_RY; ++r) {
-            if (y0 + r >= y1) break;
-            float a = 0.f, d = 0.f;
-#pragma unroll
-            for (int i = 0; i < T; ++i) {
-                const float g = (i & 1) ? -H[T - 1 - i] : H[T - 1 - i];
-                a = fmaf(H[i], v[2 * r + i], a);
-                d = fmaf(g, v[2 * r + i], d);
-            }
-            const size_t oi = var_at<AX>(y0 + r, x, p.out_pitch);
-            lo[oi] = a;
-            hi[oi] = d;
-        }
-        return;
-    }
-    for (int y = y0; y < y1; ++y) {
-        const int k = AX == 0 ? x : y, o = AX == 0 ? y : x;
+    for (int u = 0; u < 8; ++u) {
+        const int t = tb + s_ * u;
+        if (t >= p.nout) break;
         float a = 0.f, d = 0.f;
 #pragma unroll
         for (int i = 0; i < T; ++i) {
-            const int src = MODE == VM_SWT ? k - p.s * (T - 1 - i) : 2 * k - (T - 2) + i;
-            const float v = __ldg(in + var_at<AX>(var_map<MODE>(src, p.N, p.Np), o, p.in_pitch));
             const float g = (i & 1) ? -H[T - 1 - i] : H[T - 1 - i];
-            a = fmaf(H[i], v, a);
-            d = fmaf(g, v, d);
+            a = fmaf(H[i], v[u + i], a);
+            d = fmaf(g, v[u + i], d);
         }
-        const size_t oi = var_at<AX>(k, o, p.out_pitch);
+        const size_t oi = (size_t)t * p.out_pitch + x;
         lo[oi] = a;
         hi[oi] = d;
     }
 }
 
-template <int T, int MODE, int AX>
-__global__ void __launch_bounds__(128) k_var_syn(VarPass p) {
+template <int T>
+__global__ void __launch_bounds__(128) k_var_syn_col(VarPass p) {
     const int pl = blockIdx.z % p.nplanes, b = blockIdx.z / p.nplanes;
     const int x = blockIdx.x * 128 + threadIdx.x;
-    const int ey = AX == 0 ? p.other : p.nout;
-    if (x >= (AX == 0 ? p.nout : p.other)) return;
+    if (x >= p.other) return;
     const float* A = p.in[2 * pl] ? p.in[2 * pl] + (size_t)b * p.in_bstride : nullptr;   // null: zero approximation
     const float* D = p.in[2 * pl + 1] + (size_t)b * p.in_bstride;
     float* out = p.out[pl] + (size_t)b * p.out_bstride;
     const float* H = c_var_h[T == 16];
-    const int n = p.N;
-    const int y0 = blockIdx.y * VAR_RY, y1 = min(y0 + VAR_RY, ey);
-    if (AX == 1 && MODE == VM_SWT) {
-        // undecimated, along y: the polyphase run of k_var_ana; outputs t_u = tb + s u
-        // gather a, d rows tb + s j, j = u + T-1-i in [0, T + 6]
-        const int s_ = p.s, q = blockIdx.y / s_, ph = blockIdx.y - q * s_;
-        const int tb = 8 * s_ * q + ph;
-        if (tb >= p.nout) return;
-        float ca[T + 7], cd[T + 7];
+    // the polyphase run of k_var_ana_col; outputs t_u = tb + s u gather a, d rows tb + s j,
+    // j = u + T-1-i in [0, T + 6]
+    const int s_ = p.s, q = blockIdx.y / s_, ph = blockIdx.y - q * s_;
+    const int tb = 8 * s_ * q + ph;
+    if (tb >= p.nout) return;
+    float ca[T + 7], cd[T + 7];
 #pragma unroll
-        for (int j = 0; j < T + 7; ++j) {
-            const size_t at = var_at<AX>(var_mod(tb + s_ * j, n), x, p.in_pitch);
-            ca[j] = A ? __ldg(A + at) : 0.f;
-            cd[j] = __ldg(D + at);
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int t = tb + s_ * u;
-            if (t >= p.nout) break;
-            float acc = 0.f;
-#pragma unroll
-            for (int i = 0; i < T; ++i) {
-                const float g = (i & 1) ? -H[T - 1 - i] : H[T - 1 - i];
-                if (A) acc = fmaf(H[i], ca[u + T - 1 - i], acc);
-                acc = fmaf(g, cd[u + T - 1 - i], acc);
-            }
-            out[var_at<AX>(t, x, p.out_pitch)] = 0.5f * acc;
-        }
-        return;
+    for (int j = 0; j < T + 7; ++j) {
+        const size_t at = (size_t)var_mod(tb + s_ * j, p.N) * p.in_pitch + x;
+        ca[j] = A ? __ldg(A + at) : 0.f;
+        cd[j] = __ldg(D + at);
     }
-    if (AX == 1 && MODE != VM_SWT) {
-        // decimated, along y: outputs t0 .. t0+7 (t0 even) gather coefficient rows
-        // k = t0/2 .. t0/2 + NK - 1: each loaded once into registers (rows outside
-        // [0, n) are dropped for the symmetric transform, wrapped for the periodic one)
-        constexpr int NK = VAR_RY / 2 + T / 2 - 1;
-        float ca[NK], cd[NK];
 #pragma unroll
-        for (int j = 0; j < NK; ++j) {
-            int k = y0 / 2 + j;
-            bool ok = true;
-            if (MODE == VM_SYM) ok = k < n;
-            else k = var_mod(k, n);
-            const size_t at = var_at<AX>(ok ? k : 0, x, p.in_pitch);
-            ca[j] = (ok && A) ? __ldg(A + at) : 0.f;
-            cd[j] = ok ? __ldg(D + at) : 0.f;
-        }
-#pragma unroll
-        for (int u = 0; u < VAR_RY; ++u) {
-            if (y0 + u >= y1) break;
-            const int e = u & 1;
-            float acc = 0.f;
-#pragma unroll
-            for (int m = 0; m < T / 2; ++m) {
-                const int j = (u - e) / 2 + (T - 2) / 2 - m;   // k - t0/2
-                const int f = e + 2 * m;
-                const float g = e ? -H[T - 1 - f] : H[T - 1 - f];
-                acc = fmaf(H[f], ca[j], acc);
-                acc = fmaf(g, cd[j], acc);
-            }
-            out[var_at<AX>(y0 + u, x, p.out_pitch)] = acc;
-        }
-        return;
-    }
-    for (int y = y0; y < y1; ++y) {
-    const int t = AX == 0 ? x : y, o = AX == 0 ? y : x;
-    float acc = 0.f;
-    if (MODE == VM_SWT) {
+    for (int u = 0; u < 8; ++u) {
+        const int t = tb + s_ * u;
+        if (t >= p.nout) break;
+        float acc = 0.f;
 #pragma unroll
         for (int i = 0; i < T; ++i) {
-            const size_t at = var_at<AX>(var_mod(t + p.s * (T - 1 - i), n), o, p.in_pitch);
             const float g = (i & 1) ? -H[T - 1 - i] : H[T - 1 - i];
-            if (A) acc = fmaf(H[i], __ldg(A + at), acc);
-            acc = fmaf(g, __ldg(D + at), acc);
+            if (A) acc = fmaf(H[i], ca[u + T - 1 - i], acc);
+            acc = fmaf(g, cd[u + T - 1 - i], acc);
         }
-        acc *= 0.5f;
-    } else {
-        const int e = t & 1, base = (t - e) / 2 + (T - 2) / 2;
-#pragma unroll
-        for (int m = 0; m < T / 2; ++m) {
-            int k = base - m;
-            if (MODE == VM_SYM) {
-                if (k < 0 || k >= n) continue;
-            } else {
-                k = var_mod(k, n);
-            }
-            const int f = e + 2 * m;
-            const float g = e ? -H[T - 1 - f] : H[T - 1 - f];
-            const size_t at = var_at<AX>(k, o, p.in_pitch);
-            if (A) acc = fmaf(H[f], __ldg(A + at), acc);
-            acc = fmaf(g, __ldg(D + at), acc);
-        }
-    }
-    out[var_at<AX>(t, o, p.out_pitch)] = acc;
+        out[(size_t)t * p.out_pitch + x] = 0.5f * acc;
     }
 }
 
-// Row (x) passes through shared memory: a CTA stages, for one row at a time, the
-// input span its 512 outputs need (each element loaded once from HBM/L2, index map
-// applied once per element), then every thread computes 4 outputs (t0 + tid + 128 j)
-// from shared memory with consecutive lanes on consecutive addresses.  Decimated
-// analysis stages the span deinterleaved into even / odd samples so the stride-2
-// taps become unit-stride; decimated synthesis stages the coefficient span (lanes
-// 2i, 2i+1 read the same coefficient: broadcast).
+// Row (x) passes through shared memory: a CTA stages, for one row at a time, the input
+// span its 512 outputs need (each element loaded once, index map applied once per
+// element), then every thread computes 4 outputs (t0 + tid + 128 j) from shared memory
+// with consecutive lanes on consecutive addresses.
 constexpr int VR_OUT = 512;   // outputs per CTA and row
 
-template <int T, int MODE>
-__host__ __device__ inline int var_row_span(bool syn, int s) {   // staged elements per array
-    return MODE == VM_SWT ? VR_OUT + s * (T - 1) : (syn ? VR_OUT / 2 + T / 2 : VR_OUT + T / 2);
-}
+template <int T>
+__host__ __device__ inline int var_row_span(int s) { return VR_OUT + s * (T - 1); }   // staged elements per array
 
-template <int T, int MODE>
+template <int T>
 __global__ void __launch_bounds__(128) k_var_row_ana(VarPass p) {
     extern __shared__ float vr_smem[];
-    const int nst = var_row_span<T, MODE>(false, p.s);
+    const int nst = var_row_span<T>(p.s);
     float* sE = vr_smem;
-    float* sO = vr_smem + nst;
     const int pl = blockIdx.z % p.nplanes, b = blockIdx.z / p.nplanes;
     const int tid = threadIdx.x;
     const int t0 = blockIdx.x * VR_OUT;
@@ -300,23 +179,14 @@ __global__ void __launch_bounds__(128) k_var_row_ana(VarPass p) {
     float* hi = p.out[2 * pl + 1] + (size_t)b * p.out_bstride;
     const float* H = c_var_h[T == 16];
     const int y0 = blockIdx.y * VAR_RY, y1 = min(y0 + VAR_RY, p.other);
-    // decimated: E[j] = x[base + 2j], O[j] = x[base + 2j + 1], base = 2 t0 - (T-2), j < 512 + T/2
-    // undecimated: E[j] = x[t0 - s (T-1) + j], j < 512 + s (T-1)
-    const int base = MODE == VM_SWT ? t0 - p.s * (T - 1) : 2 * t0 - (T - 2);
+    const int base = t0 - p.s * (T - 1);   // E[j] = x[base + j]
     for (int y = y0; y < y1; ++y) {
         const float* row = in + (size_t)y * p.in_pitch;
         __syncthreads();
-    PRNU_STRESS(31);   // the previous row's staging is consumed
-        for (int j = tid; j < nst; j += 128) {
-            if (MODE == VM_SWT) {
-                sE[j] = __ldg(row + var_map<MODE>(base + j, p.N, p.Np));
-            } else {
-                sE[j] = __ldg(row + var_map<MODE>(base + 2 * j, p.N, p.Np));
-                sO[j] = __ldg(row + var_map<MODE>(base + 2 * j + 1, p.N, p.Np));
-            }
-        }
+        PRNU_STRESS(31);   // the previous row's staging is consumed
+        for (int j = tid; j < nst; j += 128) sE[j] = __ldg(row + var_mod(base + j, p.N));
         __syncthreads();
-    PRNU_STRESS(31);
+        PRNU_STRESS(31);
         float* lrow = lo + (size_t)y * p.out_pitch;
         float* hrow = hi + (size_t)y * p.out_pitch;
 #pragma unroll
@@ -325,10 +195,9 @@ __global__ void __launch_bounds__(128) k_var_row_ana(VarPass p) {
             if (k >= p.nout) break;
             float a = 0.f, d = 0.f;
 #pragma unroll
-            for (int i = 0; i < T; ++i) {
-                // decimated: x[2k - (T-2) + i] = E/O[u + i/2]; undecimated: x[k - s (T-1-i)] = E[u + s i]
-                PRNU_DCHECK((MODE == VM_SWT ? u + p.s * i : u + i / 2) < nst);
-                const float v = MODE == VM_SWT ? sE[u + p.s * i] : ((i & 1) ? sO[u + i / 2] : sE[u + i / 2]);
+            for (int i = 0; i < T; ++i) {   // x[k - s (T-1-i)] = E[u + s i]
+                PRNU_DCHECK(u + p.s * i < nst);
+                const float v = sE[u + p.s * i];
                 const float g = (i & 1) ? -H[T - 1 - i] : H[T - 1 - i];
                 a = fmaf(H[i], v, a);
                 d = fmaf(g, v, d);
@@ -339,10 +208,10 @@ __global__ void __launch_bounds__(128) k_var_row_ana(VarPass p) {
     }
 }
 
-template <int T, int MODE>
+template <int T>
 __global__ void __launch_bounds__(128) k_var_row_syn(VarPass p) {
     extern __shared__ float vr_smem[];
-    const int nst = var_row_span<T, MODE>(true, p.s);
+    const int nst = var_row_span<T>(p.s);
     float* sA = vr_smem;
     float* sD = vr_smem + nst;
     const int pl = blockIdx.z % p.nplanes, b = blockIdx.z / p.nplanes;
@@ -352,51 +221,33 @@ __global__ void __launch_bounds__(128) k_var_row_syn(VarPass p) {
     const float* D = p.in[2 * pl + 1] + (size_t)b * p.in_bstride;
     float* out = p.out[pl] + (size_t)b * p.out_bstride;
     const float* H = c_var_h[T == 16];
-    const int n = p.N;
     const int y0 = blockIdx.y * VAR_RY, y1 = min(y0 + VAR_RY, p.other);
-    // decimated: coefficients k = t0/2 + j, j < 256 + T/2 - 1 (dropped outside [0, n) for the
-    // symmetric transform, mod n for the periodic one); undecimated: t0 + j, j < 512 + s (T-1)
-    for (int y = y0; y < y1; ++y) {
+    for (int y = y0; y < y1; ++y) {   // coefficients t0 + j (mod n), j < 512 + s (T-1)
         const float* arow = A ? A + (size_t)y * p.in_pitch : nullptr;
         const float* drow = D + (size_t)y * p.in_pitch;
         __syncthreads();
-    PRNU_STRESS(31);
+        PRNU_STRESS(31);
         for (int j = tid; j < nst; j += 128) {
-            int k = MODE == VM_SWT ? t0 + j : t0 / 2 + j;
-            bool ok = true;
-            if (MODE == VM_SYM) ok = k < n;
-            else k = var_mod(k, n);
-            sA[j] = (ok && arow) ? __ldg(arow + k) : 0.f;
-            sD[j] = ok ? __ldg(drow + k) : 0.f;
+            const int k = var_mod(t0 + j, p.N);
+            sA[j] = arow ? __ldg(arow + k) : 0.f;
+            sD[j] = __ldg(drow + k);
         }
         __syncthreads();
-    PRNU_STRESS(31);
+        PRNU_STRESS(31);
         float* orow = out + (size_t)y * p.out_pitch;
 #pragma unroll
         for (int q = 0; q < VR_OUT / 128; ++q) {
             const int u = tid + 128 * q, t = t0 + u;
             if (t >= p.nout) break;
             float acc = 0.f;
-            if (MODE == VM_SWT) {
 #pragma unroll
-                for (int i = 0; i < T; ++i) {
-                    const float g = (i & 1) ? -H[T - 1 - i] : H[T - 1 - i];
-                    const int j = u + p.s * (T - 1 - i);
-                    acc = fmaf(H[i], sA[j], acc);
-                    acc = fmaf(g, sD[j], acc);
-                }
-                acc *= 0.5f;
-            } else {
-                const int e = u & 1, jb = (u - e) / 2 + (T - 2) / 2;   // k - t0/2 for m = 0
-#pragma unroll
-                for (int m = 0; m < T / 2; ++m) {
-                    const int f = e + 2 * m;
-                    const float g = e ? -H[T - 1 - f] : H[T - 1 - f];
-                    acc = fmaf(H[f], sA[jb - m], acc);
-                    acc = fmaf(g, sD[jb - m], acc);
-                }
+            for (int i = 0; i < T; ++i) {
+                const float g = (i & 1) ? -H[T - 1 - i] : H[T - 1 - i];
+                const int j = u + p.s * (T - 1 - i);
+                acc = fmaf(H[i], sA[j], acc);
+                acc = fmaf(g, sD[j], acc);
             }
-            orow[t] = acc;
+            orow[t] = 0.5f * acc;
         }
     }
 }
@@ -722,42 +573,26 @@ static int var_tile_dispatch(int taps, int mode, bool syn, const VarTile& p, int
     return mode == VM_SYM ? var_tile_launch<16, VM_SYM>(syn, p, nb, st) : var_tile_launch<16, VM_PER>(syn, p, nb, st);
 }
 
-template <int T, int MODE>
+template <int T>
 static void var_launch(bool syn, int ax, const VarPass& p, int nb, cudaStream_t st) {
-    // row passes: shared-memory staged, except the 8-tap decimated analysis, for which the
-    // direct stride-2 gather through L1 measured faster (8 FHD frames: 0.097 vs 0.126 ms)
-    if (ax == 0 && !(T == 8 && MODE != VM_SWT && !syn)) {
+    if (ax == 0) {   // rows: shared-memory staged
         const dim3 g((unsigned)((p.nout + VR_OUT - 1) / VR_OUT), (unsigned)((p.other + VAR_RY - 1) / VAR_RY),
                      (unsigned)(nb * p.nplanes));
-        const size_t sm = 2 * sizeof(float) * var_row_span<T, MODE>(syn, p.s);
-        if (syn) k_var_row_syn<T, MODE><<<g, 128, sm, st>>>(p);
-        else k_var_row_ana<T, MODE><<<g, 128, sm, st>>>(p);
+        const size_t sm = 2 * sizeof(float) * var_row_span<T>(p.s);
+        if (syn) k_var_row_syn<T><<<g, 128, sm, st>>>(p);
+        else k_var_row_ana<T><<<g, 128, sm, st>>>(p);
         return;
     }
-    const int ex = ax == 0 ? p.nout : p.other, ey = ax == 0 ? p.other : p.nout;
-    // undecimated column passes: polyphase runs, ceil(ey / (8 s)) blocks of 8 s rows x s phases
-    const unsigned gy = (MODE == VM_SWT && ax == 1) ? (unsigned)(((ey + 8 * p.s - 1) / (8 * p.s)) * p.s)
-                                                    : (unsigned)((ey + VAR_RY - 1) / VAR_RY);
-    const dim3 grid((unsigned)((ex + 127) / 128), gy, (unsigned)(nb * p.nplanes));
-    if (syn) {
-        if (ax == 0) k_var_syn<T, MODE, 0><<<grid, 128, 0, st>>>(p);
-        else k_var_syn<T, MODE, 1><<<grid, 128, 0, st>>>(p);
-    } else {
-        if (ax == 0) k_var_ana<T, MODE, 0><<<grid, 128, 0, st>>>(p);
-        else k_var_ana<T, MODE, 1><<<grid, 128, 0, st>>>(p);
-    }
+    // columns: polyphase runs, ceil(nout / (8 s)) blocks of 8 s rows x s phases
+    const dim3 grid((unsigned)((p.other + 127) / 128), (unsigned)(((p.nout + 8 * p.s - 1) / (8 * p.s)) * p.s),
+                    (unsigned)(nb * p.nplanes));
+    if (syn) k_var_syn_col<T><<<grid, 128, 0, st>>>(p);
+    else k_var_ana_col<T><<<grid, 128, 0, st>>>(p);
 }
 
-static void var_dispatch(int taps, int mode, bool syn, int ax, const VarPass& p, int nb, cudaStream_t st) {
-    if (taps == 8) {
-        if (mode == VM_SYM) var_launch<8, VM_SYM>(syn, ax, p, nb, st);
-        else if (mode == VM_PER) var_launch<8, VM_PER>(syn, ax, p, nb, st);
-        else var_launch<8, VM_SWT>(syn, ax, p, nb, st);
-    } else {
-        if (mode == VM_SYM) var_launch<16, VM_SYM>(syn, ax, p, nb, st);
-        else if (mode == VM_PER) var_launch<16, VM_PER>(syn, ax, p, nb, st);
-        else var_launch<16, VM_SWT>(syn, ax, p, nb, st);
-    }
+static void var_dispatch(int taps, bool syn, int ax, const VarPass& p, int nb, cudaStream_t st) {
+    if (taps == 8) var_launch<8>(syn, ax, p, nb, st);
+    else var_launch<16>(syn, ax, p, nb, st);
 }
 
 // ------------------------------------------------------------------ geometry / workspace
@@ -937,13 +772,12 @@ int run_residual_variant(const float* in, int nb, int H, int W, int levels, int 
             p.out_bstride = (long long)g.scratch;
             p.out_pitch = nWl;
             p.N = g.inW[l];
-            p.Np = g.perW[l];
             p.nout = nWl;
             p.other = g.inH[l];
             p.s = s;
             p.nplanes = 1;
             KTimer kt("variant_ana_x", st);
-            var_dispatch(taps, g.mode, false, 0, p, nb, st);
+            var_dispatch(taps, false, 0, p, nb, st);
         }
         count_launch();
         if ((rc = check_launch("k_var_ana (x)"))) return rc;
@@ -960,13 +794,12 @@ int run_residual_variant(const float* in, int nb, int H, int W, int levels, int 
             p.out_bstride = (long long)nHl * nWl;
             p.out_pitch = nWl;
             p.N = g.inH[l];
-            p.Np = g.perH[l];
             p.nout = nHl;
             p.other = nWl;
             p.s = s;
             p.nplanes = 2;
             KTimer kt("variant_ana_y", st);
-            var_dispatch(taps, g.mode, false, 1, p, nb, st);
+            var_dispatch(taps, false, 1, p, nb, st);
         }
         count_launch();
         if ((rc = check_launch("k_var_ana (y)"))) return rc;
@@ -1005,7 +838,7 @@ int run_residual_variant(const float* in, int nb, int H, int W, int levels, int 
             p.s = s;
             p.nplanes = 2;
             KTimer kt("variant_syn_y", st);
-            var_dispatch(taps, g.mode, true, 1, p, nb, st);
+            var_dispatch(taps, true, 1, p, nb, st);
         }
         count_launch();
         if ((rc = check_launch("k_var_syn (y)"))) return rc;
@@ -1024,7 +857,7 @@ int run_residual_variant(const float* in, int nb, int H, int W, int levels, int 
             p.s = s;
             p.nplanes = 1;
             KTimer kt("variant_syn_x", st);
-            var_dispatch(taps, g.mode, true, 0, p, nb, st);
+            var_dispatch(taps, true, 0, p, nb, st);
         }
         count_launch();
         if ((rc = check_launch("k_var_syn (x)"))) return rc;
