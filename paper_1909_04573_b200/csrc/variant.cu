@@ -256,10 +256,8 @@ __global__ void __launch_bounds__(128) k_var_row_syn(VarPass p) {
 // Decimated variants (symmetric / periodic): one kernel per analysis level (rows and
 // columns of a tile through shared memory: input read once, the four subbands written
 // once) and one per synthesis level (four coefficient tiles in, the level's output out),
-// instead of two separable passes with an HBM round trip in between.  Same arithmetic
-// in the same order as the separable passes k_var_ana / k_var_row_ana and k_var_syn /
-// k_var_row_syn (still used by the undecimated variants); parity against the oracle in
-// tests/test_gpu_variants.py.
+// instead of two separable passes with an HBM round trip in between (round 1; the same
+// arithmetic in the same order); parity against the oracle in tests/test_gpu_variants.py.
 constexpr int VT_Y = 32, VT_X = 32;   // analysis: coefficient positions per tile
 constexpr int VS_Y = 32, VS_X = 64;   // synthesis: output pixels per tile
 
