@@ -258,8 +258,11 @@ __global__ void __launch_bounds__(128) k_var_row_syn(VarPass p) {
 // once) and one per synthesis level (four coefficient tiles in, the level's output out),
 // instead of two separable passes with an HBM round trip in between (round 1; the same
 // arithmetic in the same order); parity against the oracle in tests/test_gpu_variants.py.
-constexpr int VT_Y = 32, VT_X = 32;   // analysis: coefficient positions per tile
-constexpr int VS_Y = 32, VS_X = 64;   // synthesis: output pixels per tile
+constexpr int VT_Y = 32, VT_X = 32;   // analysis: coefficient positions per tile (64-row tiles at T = 16: slower)
+constexpr int VS_X = 64;   // synthesis: output pixels per tile row
+// output rows per synthesis tile: 64 for the 16-tap filter (its coefficient halo is T/2 - 1 rows)
+template <int T>
+__host__ __device__ constexpr int var_vs_y() { return T == 16 ? 64 : 32; }
 
 struct VarTile {
     const float* in;          // analysis: the level's input plane;  synthesis: unused
@@ -293,8 +296,8 @@ template <int T>
 __host__ __device__ constexpr int var_syn_kxp() { return VS_X / 2 - 4 + 4 * var_syn_nld<T>(); }   // X pitch
 template <int T>
 __host__ __device__ constexpr size_t var_syn2d_smem() {
-    return sizeof(float) * (4 * (size_t)(VS_Y / 2 + T / 2 - 1) * (VS_X / 2 + T / 2 - 1) +
-                            2 * (size_t)VS_Y * var_syn_kxp<T>());
+    return sizeof(float) * (4 * (size_t)(var_vs_y<T>() / 2 + T / 2 - 1) * (VS_X / 2 + T / 2 - 1) +
+                            2 * (size_t)var_vs_y<T>() * var_syn_kxp<T>());
 }
 
 template <int T, int MODE>
@@ -405,6 +408,7 @@ __global__ void __launch_bounds__(256, 2) k_var_ana2d(VarTile p) {
 
 template <int T, int MODE>
 __global__ void __launch_bounds__(256, 2) k_var_syn2d(VarTile p) {
+    constexpr int VS_Y = var_vs_y<T>();
     constexpr int KY = VS_Y / 2 + T / 2 - 1, KX = VS_X / 2 + T / 2 - 1;   // coefficient rows / columns
     constexpr int KXP = var_syn_kxp<T>(), NLD = var_syn_nld<T>();
     extern __shared__ __align__(16) float vs_smem[];
@@ -555,7 +559,8 @@ static int var_tile_launch(bool syn, const VarTile& p, int nb, cudaStream_t st) 
     int rc;
     if (syn) {
         if ((rc = set_smem_attr((const void*)k_var_syn2d<T, MODE>, var_syn2d_smem<T>(), attr[1]))) return rc;
-        const dim3 g((unsigned)((p.oW + VS_X - 1) / VS_X), (unsigned)((p.oH + VS_Y - 1) / VS_Y), (unsigned)nb);
+        const dim3 g((unsigned)((p.oW + VS_X - 1) / VS_X), (unsigned)((p.oH + var_vs_y<T>() - 1) / var_vs_y<T>()),
+                     (unsigned)nb);
         k_var_syn2d<T, MODE><<<g, 256, var_syn2d_smem<T>(), st>>>(p);
     } else {
         if ((rc = set_smem_attr((const void*)k_var_ana2d<T, MODE>, var_ana2d_smem<T>(), attr[0]))) return rc;
