@@ -9,7 +9,8 @@
  *  - Every pointer is a DEVICE pointer owned by the caller unless the argument
  *    name ends in `_host`.  The library never allocates or frees caller memory;
  *    scratch space is the caller-owned `ws` of at least the size the matching
- *    `*_workspace_bytes` query returns (256-byte aligned).
+ *    `*_workspace_bytes` query returns (256-byte aligned; the denoising entry
+ *    points reject a misaligned `ws` with PRNU_INVALID_ARG).
  *  - Planes are row-major and contiguous: `[batch][H][W]`, H rows of W columns,
  *    frames/batch outermost.  "1920x1080" means W = 1920, H = 1080.
  *  - Calls are asynchronous on `stream` (a `cudaStream_t` passed as void*;

@@ -220,6 +220,13 @@ static size_t extract_ws(int H, int W, int batch, int64_t depth, const Pyramid& 
     return extract_streams() * extract_wave_ws(H, W, batch, depth, pyr) + zm_workspace_bytes(H, W);
 }
 
+// The workspace contract (include/prnu.h): 256-byte aligned.  The denoiser's pyramid planes
+// are carved from it with 128-byte rows and written with 32-byte (256-bit) stores.
+static int check_ws_align(const void* ws) {
+    if (reinterpret_cast<uintptr_t>(ws) % 256) return fail(PRNU_INVALID_ARG, "workspace must be 256-byte aligned");
+    return PRNU_OK;
+}
+
 static int check_dims(int H, int W) {
     if (H <= 0 || W <= 0) return fail(PRNU_INVALID_ARG, "H and W must be positive");
     if ((long long)H * W > (1LL << 31) - 1) return fail(PRNU_INVALID_ARG, "H*W must fit in int32");
@@ -284,6 +291,7 @@ static int residual_impl(const TIn* planes, int batch, int H, int W, const prnu_
     if ((rc = validate_params(p, H, W, &sp))) return rc;
     Pyramid pyr = make_pyramid(H, W, p->levels);
     if (ws_bytes < residual_ws(batch, H, W, pyr)) return fail(PRNU_WORKSPACE_TOO_SMALL, "workspace too small");
+    if ((rc = check_ws_align(ws))) return rc;
     cudaStream_t st = as_stream(stream);
     float* pyr_ws = reinterpret_cast<float*>(ws);
     if (sizeof(TIn) == 1 && W % 16) {   // u8 rows that TMA cannot stage: re-pitch them first
@@ -454,6 +462,7 @@ static int extract_impl(const uint8_t* frames, int64_t m, int H, int W, int64_t 
     if ((rc = validate_params(p, H, W, &sp))) return rc;
     Pyramid pyr = make_pyramid(H, W, p->levels);
     if (ws_bytes < extract_ws(H, W, batch, unit, pyr)) return fail(PRNU_WORKSPACE_TOO_SMALL, "workspace too small");
+    if ((rc = check_ws_align(ws))) return rc;
     if (n_sda_host) *n_sda_host = ns;
     cudaStream_t st = as_stream(stream);
     const size_t P = (size_t)H * W;
@@ -542,6 +551,7 @@ int prnu_extract_fingerprint_host(const uint8_t* frames_host, int64_t m, int H, 
     if ((rc = validate_params(p, H, W, &sp))) return rc;
     if (ws_bytes < prnu_extract_host_workspace_bytes(H, W, batch, depth, p))
         return fail(PRNU_WORKSPACE_TOO_SMALL, "workspace too small");
+    if ((rc = check_ws_align(ws))) return rc;
     if (n_sda_host) *n_sda_host = ns;
     Pyramid pyr = make_pyramid(H, W, p->levels);
     const size_t P = (size_t)H * W;
@@ -649,6 +659,7 @@ int prnu_extract_multi_host(const uint8_t* frames_host, int64_t m, int H, int W,
     size_t off_w, off_K, off_zm;
     if (ws_bytes < multi_layout(m, H, W, batch, depths_host, n_depths, pyr, &off_w, &off_K, &off_zm))
         return fail(PRNU_WORKSPACE_TOO_SMALL, "workspace too small");
+    if ((rc = check_ws_align(ws))) return rc;
     const size_t P = (size_t)H * W;
     char* wsb = reinterpret_cast<char*>(ws);
     uint8_t* fdev = reinterpret_cast<uint8_t*>(wsb);
@@ -851,6 +862,7 @@ int prnu_residual_variant(const float* planes, int batch, int H, int W, const pr
     if ((rc = validate_params(p, H, W, &sp))) return rc;
     if ((rc = validate_variant(v))) return rc;
     if (ws_bytes < variant_ws(batch, H, W, p, v)) return fail(PRNU_WORKSPACE_TOO_SMALL, "workspace too small");
+    if ((rc = check_ws_align(ws))) return rc;
     cudaStream_t st = as_stream(stream);
     if ((rc = run_residual_variant(planes, batch, H, W, p->levels, v->taps, v->boundary, v->transform, sp, W_out,
                                    reinterpret_cast<float*>(ws), st)))
@@ -896,6 +908,7 @@ int prnu_extract_fingerprint_variant(const uint8_t* frames, int64_t m, int H, in
     if ((rc = validate_params(p, H, W, &sp))) return rc;
     if ((rc = validate_variant(v))) return rc;
     if (ws_bytes < extract_variant_ws(H, W, batch, p, v)) return fail(PRNU_WORKSPACE_TOO_SMALL, "workspace too small");
+    if ((rc = check_ws_align(ws))) return rc;
     if (n_sda_host) *n_sda_host = ns;
     cudaStream_t st = as_stream(stream);
     const size_t P = (size_t)H * W;

@@ -58,6 +58,12 @@ def test_validation_is_synchronous_and_precedes_launch():
     assert L.prnu_residual(dummy, 1, 64, 64, ctypes.byref(bad), 0, dummy, dummy, 1 << 30, None) == 4
     # workspace too small
     assert L.prnu_residual(dummy, 1, 64, 64, ctypes.byref(p), 0, dummy, dummy, 16, None) == 9
+    # workspace not 256-byte aligned (the header's contract; the pyramid is written with 256-bit stores)
+    off = ctypes.c_void_p((1 << 20) + 16)
+    assert L.prnu_residual(dummy, 1, 64, 64, ctypes.byref(p), 0, dummy, off, 1 << 30, None) == 1
+    K = ctypes.c_void_p(1 << 21)
+    assert L.prnu_extract_fingerprint(dummy, 16, 64, 64, 4, ctypes.byref(p), 4, ctypes.c_double(1e-6), K, K, K, None,
+                                      off, ctypes.c_size_t(1 << 30), None) == 1
     # depth exceeds frames
     assert L.prnu_sda_average(dummy, 10, 8, 8, 11, dummy, None, None) == 3
     assert "depth" in L.prnu_last_error().decode()
