@@ -338,7 +338,8 @@ def main():
     n_sda = {d: m // d for d in depths}
     plan = prnu.PcePlan(H, W, len(depths), device=dev)
 
-    side = torch.cuda.Stream(device=dev)
+    side = torch.cuda.Stream(device=dev)                # least priority: fills the gaps
+    main_hp = torch.cuda.Stream(device=dev, priority=-1)   # depth 1 (the library's wave streams inherit it)
 
     def step(concurrent=True):
         # The depths are independent fingerprints of the same frames, and the query residual
@@ -350,11 +351,14 @@ def main():
         cur = torch.cuda.current_stream()
         if concurrent and not args.serial_depths:
             side.wait_stream(cur)   # also: the previous step's readers of the side outputs are done
+            main_hp.wait_stream(cur)
             with torch.cuda.stream(side):
                 Rq = prnu.residual(query, zero_mean=True)
                 for k in range(1, len(depths)):
                     Ks[k] = exs[depths[k]](frames).K
-            Ks[0] = exs[depths[0]](frames).K
+            with torch.cuda.stream(main_hp):
+                Ks[0] = exs[depths[0]](frames).K
+            cur.wait_stream(main_hp)
             cur.wait_stream(side)
         else:
             for k, d in enumerate(depths):

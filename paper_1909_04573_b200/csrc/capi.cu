@@ -418,17 +418,24 @@ struct ExtractCtx {
     cudaStream_t helper[kExtractStreams - 1] = {};
     cudaEvent_t ev_start = nullptr, ev_end[kExtractStreams] = {}, acc[kExtractStreams] = {};
 };
-static int extract_ctx(ExtractCtx** out) {
+// One context per (device, stream priority): the helper streams run the waves at the
+// priority of the caller's stream, so a caller can rank an extraction against its other work.
+static int extract_ctx(ExtractCtx** out, cudaStream_t caller) {
     static std::mutex g_mu;
-    static ExtractCtx* g_ctx[64] = {};
+    constexpr int kPrio = 8;   // priority levels kept apart (CUDA has 6 on sm_100; clamped)
+    static ExtractCtx* g_ctx[64][kPrio] = {};
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return fail(PRNU_CUDA_ERROR, "cudaGetDevice");
+    int prio = 0, lo = 0, hi = 0;
+    if (cudaStreamGetPriority(caller, &prio) != cudaSuccess || cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess)
+        return fail(PRNU_CUDA_ERROR, "stream priority query");
+    const int pi = std::min(std::max(lo - prio, 0), kPrio - 1);   // 0 = the least priority
     std::lock_guard<std::mutex> lock(g_mu);
-    if (!g_ctx[dev]) {
+    if (!g_ctx[dev][pi]) {
         ExtractCtx* c = new ExtractCtx();
         cudaError_t e = cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming);
         for (int j = 0; j < kExtractStreams && e == cudaSuccess; ++j) {
-            if (j > 0) e = cudaStreamCreateWithFlags(&c->helper[j - 1], cudaStreamNonBlocking);
+            if (j > 0) e = cudaStreamCreateWithPriority(&c->helper[j - 1], cudaStreamNonBlocking, lo - pi);
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_end[j], cudaEventDisableTiming);
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->acc[j], cudaEventDisableTiming);
         }
@@ -436,9 +443,9 @@ static int extract_ctx(ExtractCtx** out) {
             delete c;   // (handles created before the failure are leaked: the device is unusable anyway)
             return fail(PRNU_CUDA_ERROR, std::string("extraction streams: ") + cudaGetErrorString(e));
         }
-        g_ctx[dev] = c;
+        g_ctx[dev][pi] = c;
     }
-    *out = g_ctx[dev];
+    *out = g_ctx[dev][pi];
     return PRNU_OK;
 }
 
@@ -490,7 +497,7 @@ static int extract_impl(const uint8_t* frames, int64_t m, int H, int W, int64_t 
     // streams and events are created once per device (ExtractCtx) and reused; the
     // context's mutex serialises the enqueue of concurrent calls on one device.
     ExtractCtx* cx = nullptr;
-    if ((rc = extract_ctx(&cx))) return rc;
+    if ((rc = extract_ctx(&cx, st))) return rc;
     std::lock_guard<std::mutex> lock(cx->mu);
     cudaStream_t sts[kExtractStreams] = {st};
     for (int j = 1; j < nst; ++j) sts[j] = cx->helper[j - 1];
