@@ -241,6 +241,21 @@ def test_extract_depth2_pairs(prnu, H, W, m, batch):
         assert k_metric(fp.K.cpu().numpy(), K_ref, den_ref, n)[0] <= K_TOL
 
 
+def test_extract_on_high_priority_stream_bit_identical(prnu):
+    """The wave streams of an extraction inherit the caller stream's priority (their own
+    context per priority); results do not depend on it."""
+    v = synth.video("drift", 24, 64, 128, seed=3)
+    fr = v.frames.cuda()
+    ref = prnu.extract_fingerprint(fr, 1, batch=5)
+    ref_K, ref_den = ref.K.clone(), ref.sum_I2.clone()
+    hp = torch.cuda.Stream(priority=-1)
+    hp.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(hp):
+        fp = prnu.extract_fingerprint(fr, 1, batch=5)
+    torch.cuda.current_stream().wait_stream(hp)
+    assert torch.equal(fp.K, ref_K) and torch.equal(fp.sum_I2, ref_den)
+
+
 def test_extract_deterministic_across_batches(prnu):
     v = synth.video("drift", 40, 64, 128, seed=2)
     fr = v.frames.cuda()
