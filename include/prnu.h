@@ -42,10 +42,9 @@ enum {
     PRNU_BAD_PARAMETER = 4,        /* sigma0_sq <= 0, levels outside 1..6, window not in
                                       {3,5,7,9}, exclusion_half < 0        [S:110]        */
     PRNU_DIMENSION_MISMATCH = 5,   /*                                        [S:198, S:207] */
-    PRNU_EMPTY_ACCUMULATOR = 6,    /* reserved (finalize cannot inspect device data
-                                      synchronously; see prnu_fingerprint_finalize) [S:216] */
-    PRNU_CONSTANT_INPUT = 7,       /* reserved (see prnu_ncc)                [S:288]        */
-    PRNU_DEGENERATE_SURFACE = 8,   /* reserved (see prnu_pce)                [S:297]        */
+    PRNU_EMPTY_ACCUMULATOR = 6,    /* prnu_check_results on sum_I2           [S:216]        */
+    PRNU_CONSTANT_INPUT = 7,       /* prnu_check_results on NCC values       [S:288]        */
+    PRNU_DEGENERATE_SURFACE = 8,   /* prnu_check_results on PCE peaks        [S:297]        */
     PRNU_WORKSPACE_TOO_SMALL = 9,
     PRNU_CUDA_ERROR = 10           /* a launch / cuFFT call failed; see prnu_last_error() */
 };
@@ -135,8 +134,8 @@ int prnu_fingerprint_accumulate(const float* W, const float* I, int batch, int H
  * a6  Finalize — S:212-220: K = sum_WI / max(sum_I2, eps) element-wise, then
  * (zero_mean != 0) the row/column zero-mean of S:135 computed in fp64
  * (K - rowmean - colmean + totalmean, R-13); K_out fp32 [H][W].
- * An all-zero accumulator yields K = 0 (EMPTY_ACCUMULATOR cannot be detected
- * without a device->host sync; the host wrapper tracks contribution counts).
+ * An all-zero accumulator yields K = 0 in-band (this call stays asynchronous);
+ * prnu_check_results(2, sum_I2, H*W, ...) reports it as EMPTY_ACCUMULATOR.
  * ------------------------------------------------------------------------- */
 size_t prnu_finalize_workspace_bytes(int H, int W);
 int prnu_fingerprint_finalize(const double* sum_WI, const double* sum_I2, int H, int W, double eps,
@@ -199,12 +198,26 @@ int prnu_extract_multi_host(const uint8_t* frames_host, int64_t m, int H, int W,
  * correlation over all pixels at shift (0,0),
  * rho = sum (a-abar)(b-bbar) / sqrt(sum (a-abar)^2 sum (b-bbar)^2),
  * two-pass, fp64 sums, fixed reduction order.  a, b fp32 [batch][H][W];
- * ncc_out fp64 [batch] (device).  A constant input yields NaN (ConstantInput,
- * S:288, is reported in-band because detection would need a sync).
+ * ncc_out fp64 [batch] (device).  A constant input yields NaN in-band (this call
+ * stays asynchronous); prnu_check_results(0, ncc_out, batch, ...) reports it as
+ * CONSTANT_INPUT.
  * ------------------------------------------------------------------------- */
 size_t prnu_ncc_workspace_bytes(int batch, int H, int W);
 int prnu_ncc(const float* a, const float* b, int batch, int H, int W, double* ncc_out, void* ws,
              size_t ws_bytes, void* stream);
+
+/* prnu_check_results: the data-dependent error kinds of SPEC, which the
+ * asynchronous calls report in-band, as a status.  SYNCHRONOUS: waits for `stream`, then
+ * inspects `n` fp64 values (device) the earlier calls wrote:
+ *   kind 0  NCC values (prnu_ncc)               -> PRNU_CONSTANT_INPUT if any is NaN
+ *           (an operand with zero variance);
+ *   kind 1  PCE peak values C[p*] (`peak` of prnu_pce*) -> PRNU_DEGENERATE_SURFACE if any
+ *           is 0 (all values of the mean-removed surface equal; a zero background
+ *           alone is not degenerate: that PCE is the +-1e12 cap);
+ *   kind 2  sum_I2 of a fingerprint (H*W values) -> PRNU_EMPTY_ACCUMULATOR if every value
+ *           is 0 (no frame contributed).
+ * PRNU_OK otherwise.  Errors: INVALID_ARG (null, n < 1, unknown kind), CUDA_ERROR.         */
+int prnu_check_results(int kind, const double* values, int64_t n, void* stream);
 
 /* ---------------------------------------------------------------------------
  * a8  PCE — P:259 ("PCE ... A preset threshold of 60 ... Values higher than

@@ -123,6 +123,7 @@ _sig("prnu_extract_fingerprint_host", _i, _vp, _i64, _i, _i, _i64, _P, _i, _d, _
      ctypes.POINTER(_i64), _vp, _sz, _vp)
 _sig("prnu_ncc_workspace_bytes", _sz, _i, _i, _i)
 _sig("prnu_ncc", _i, _vp, _vp, _i, _i, _i, _vp, _vp, _sz, _vp)
+_sig("prnu_check_results", _i, _i, _vp, _i64, _vp)
 _sig("prnu_pce_template", _i, _vp, _i, _vp, _i, _i, _i, _vp, _vp)
 _sig("prnu_pce_plan_create", _i, _i, _i, _i, ctypes.POINTER(_sz), ctypes.POINTER(_vp))
 _sig("prnu_pce", _i, _vp, _vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _sz, _vp)
@@ -608,9 +609,23 @@ prnu_extract_fingerprint_variant = extract_fingerprint_variant
 
 
 # ---------------------------------------------------------------- a7-a8
+CHECK_NCC, CHECK_PCE, CHECK_SUM_I2 = 0, 1, 2
+
+
 @_on_device
-def ncc(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
-    """Aligned Pearson correlation per plane (R-16), fp64 [batch] (or 0-dim)."""
+def check_results(kind: int, values: torch.Tensor) -> None:
+    """prnu_check_results: raise PrnuError 7 (ConstantInput) for NaN NCC values,
+    8 (DegenerateSurface) for a zero PCE peak (the surface is constant), 6
+    (EmptyAccumulator) for an all-zero sum_I2.  Synchronous (waits for the current
+    stream)."""
+    _dev(values, torch.float64, "values", (1, 2, 3))
+    _check(_lib.prnu_check_results(int(kind), _ptr(values), values.numel(), _stream()), "prnu_check_results")
+
+
+@_on_device
+def ncc(a: torch.Tensor, b: torch.Tensor, check: bool = False) -> torch.Tensor:
+    """Aligned Pearson correlation per plane (R-16), fp64 [batch] (or 0-dim).  A constant
+    operand gives NaN in-band; check=True raises PrnuError 7 instead (synchronous)."""
     squeeze = a.dim() == 2
     if squeeze:
         a, b = a.unsqueeze(0), b.unsqueeze(0)
@@ -623,6 +638,8 @@ def ncc(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
     ws = _ws(nbytes, a.device)
     out = torch.empty((n,), dtype=torch.float64, device=a.device)
     _check(_lib.prnu_ncc(_ptr(a), _ptr(b), n, H, W, _ptr(out), _ptr(ws), nbytes, _stream()), "prnu_ncc")
+    if check:
+        check_results(CHECK_NCC, out)
     return out[0] if squeeze else out
 
 
@@ -828,9 +845,15 @@ prnu_wdft = wdft
 
 
 @_on_device
-def pce(R: torch.Tensor, T: torch.Tensor, exclusion_half: int = 5, aligned: bool = False) -> PceResult:
+def pce(R: torch.Tensor, T: torch.Tensor, exclusion_half: int = 5, aligned: bool = False,
+        check: bool = False) -> PceResult:
+    """PCE per pair (prnu_pce).  A degenerate (constant) surface is reported in-band (peak 0,
+    PCE at the cap); check=True raises PrnuError 8 instead (synchronous)."""
     b = 1 if R.dim() == 2 else R.shape[0]
-    return PcePlan(R.shape[-2], R.shape[-1], b, R.device)(R, T, exclusion_half, aligned)
+    res = PcePlan(R.shape[-2], R.shape[-1], b, R.device)(R, T, exclusion_half, aligned)
+    if check:
+        check_results(CHECK_PCE, res.peak.reshape(-1))
+    return res
 
 
 prnu_pce = pce

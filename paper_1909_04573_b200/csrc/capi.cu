@@ -737,6 +737,13 @@ int prnu_ncc(const float* a, const float* b, int batch, int H, int W, double* nc
     return launch_ncc(a, b, batch, (long long)H * W, ncc_out, ws, as_stream(stream));
 }
 
+int prnu_check_results(int kind, const double* values, int64_t n, void* stream) {
+    if (!values) return fail(PRNU_INVALID_ARG, "null pointer");
+    if (n < 1) return fail(PRNU_INVALID_ARG, "n must be positive");
+    if (kind < 0 || kind > 2) return fail(PRNU_INVALID_ARG, "kind must be 0 (NCC), 1 (PCE) or 2 (sum_I2)");
+    return prnu::check_results(kind, values, (long long)n, as_stream(stream));
+}
+
 int prnu_pce_template(const float* K, int k_batch, const uint8_t* Iq, int batch, int H, int W, float* T_out,
                       void* stream) {
     int rc;

@@ -284,6 +284,8 @@ int launch_analysis_lift_u8(const uint8_t* in, long long in_bstride, int in_pitc
 int launch_analysis_lift_u16(const uint16_t* in, long long in_bstride, int in_pitch, int NH, int NW, float* ll,
                              float* d0, float* d1, float* d2, long long out_bstride, int out_pitch, int nH, int nW,
                              const ShrinkParams& sp, const SdaDiv& div, int nb, cudaStream_t st);
+// prnu_check_results (mle.cu): synchronous status of results already written on st
+int check_results(int kind, const double* v, long long n, cudaStream_t st);
 // SDA pairs (d = 2): groups of two u8 frames (frame_stride apart; group b = frames 2b, 2b+1)
 int launch_analysis_lift_pair(const uint8_t* in, long long frame_stride, int in_pitch, int NH, int NW, float* ll,
                               float* d0, float* d1, float* d2, long long out_bstride, int out_pitch, int nH, int nW,

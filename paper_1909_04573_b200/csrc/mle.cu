@@ -273,4 +273,41 @@ int launch_ncc(const float* a, const float* b, int batch, long long P, double* o
     return check_launch("ncc");
 }
 
+// ---------------------------------------------------------------- result checks
+// Flags the data-dependent error kinds (prnu_check_results): bit 0 = some NaN, bit 1 = some
+// zero, bit 2 = some non-zero.  An idempotent OR into one word (the result does not
+// depend on the order of the atomics).
+__global__ void k_check_results(const double* __restrict__ v, long long n, unsigned* __restrict__ flags) {
+    unsigned f = 0u;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double x = v[i];
+        if (isnan(x)) f |= 1u;
+        if (x == 0.0) f |= 2u;
+        if (x != 0.0) f |= 4u;
+    }
+    f = __reduce_or_sync(0xffffffffu, f);
+    if ((threadIdx.x & 31) == 0 && f) atomicOr(flags, f);
+}
+
+int check_results(int kind, const double* v, long long n, cudaStream_t st) {
+    unsigned* flags = nullptr;
+    unsigned h = 0u;
+    if (cudaMallocAsync(&flags, sizeof(unsigned), st) != cudaSuccess) return fail(PRNU_CUDA_ERROR, "cudaMallocAsync");
+    cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(unsigned), st);
+    if (e == cudaSuccess) {
+        const long long blocks = std::min<long long>((n + 255) / 256, 4LL * device_sm_count());
+        k_check_results<<<(unsigned)std::max<long long>(blocks, 1), 256, 0, st>>>(v, n, flags);
+        count_launch();
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&h, flags, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(flags, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return fail(PRNU_CUDA_ERROR, std::string("check_results: ") + cudaGetErrorString(e));
+    if (kind == 0 && (h & 1u)) return fail(PRNU_CONSTANT_INPUT, "NCC of an operand with zero variance (NaN)");
+    if (kind == 1 && (h & 2u)) return fail(PRNU_DEGENERATE_SURFACE, "PCE of a surface with all values equal (peak 0)");
+    if (kind == 2 && !(h & 4u)) return fail(PRNU_EMPTY_ACCUMULATOR, "sum_I2 is zero everywhere: no frame accumulated");
+    return PRNU_OK;
+}
+
 }  // namespace prnu

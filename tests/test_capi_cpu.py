@@ -58,6 +58,10 @@ def test_validation_is_synchronous_and_precedes_launch():
     assert L.prnu_residual(dummy, 1, 64, 64, ctypes.byref(bad), 0, dummy, dummy, 1 << 30, None) == 4
     # workspace too small
     assert L.prnu_residual(dummy, 1, 64, 64, ctypes.byref(p), 0, dummy, dummy, 16, None) == 9
+    # prnu_check_results: argument validation before any device work
+    assert L.prnu_check_results(3, dummy, 10, None) == 1
+    assert L.prnu_check_results(0, dummy, 0, None) == 1
+    assert L.prnu_check_results(0, None, 10, None) == 1
     # workspace not 256-byte aligned (the header's contract; the pyramid is written with 256-bit stores)
     off = ctypes.c_void_p((1 << 20) + 16)
     assert L.prnu_residual(dummy, 1, 64, 64, ctypes.byref(p), 0, dummy, off, 1 << 30, None) == 1

@@ -256,6 +256,32 @@ def test_extract_on_high_priority_stream_bit_identical(prnu):
     assert torch.equal(fp.K, ref_K) and torch.equal(fp.sum_I2, ref_den)
 
 
+def test_check_results_error_kinds(prnu):
+    """SPEC's data-dependent error kinds (S:216 EmptyAccumulator, S:288 ConstantInput,
+    S:297 DegenerateSurface) through the synchronous prnu_check_results; the asynchronous
+    calls report them in-band (NaN / non-finite / zero)."""
+    g = torch.Generator(device="cpu").manual_seed(5)
+    a = torch.full((2, 32, 48), 3.0, device="cuda")             # zero variance
+    b = torch.randn((2, 32, 48), generator=g).cuda()
+    assert torch.isnan(prnu.ncc(a, b)).all()
+    with pytest.raises(prnu.PrnuError) as e:
+        prnu.ncc(a, b, check=True)
+    assert e.value.code == 7
+    prnu.ncc(b, b + 1.0, check=True)                            # a valid pair passes
+    R = torch.randn((1, 64, 64), generator=g).cuda()
+    res = prnu.pce(R, torch.zeros((1, 64, 64), device="cuda"))  # a constant (zero) surface
+    assert (res.peak == 0).all()
+    with pytest.raises(prnu.PrnuError) as e:
+        prnu.pce(R, torch.zeros((1, 64, 64), device="cuda"), check=True)
+    assert e.value.code == 8
+    prnu.pce(R, R.clone(), check=True)
+    with pytest.raises(prnu.PrnuError) as e:
+        prnu.check_results(prnu.CHECK_SUM_I2, torch.zeros((64, 64), dtype=torch.float64, device="cuda"))
+    assert e.value.code == 6
+    fp = prnu.extract_fingerprint(synth.video("shift", 8, 64, 64, seed=1).frames.cuda(), 2, batch=2)
+    prnu.check_results(prnu.CHECK_SUM_I2, fp.sum_I2)
+
+
 def test_extract_deterministic_across_batches(prnu):
     v = synth.video("drift", 40, 64, 128, seed=2)
     fr = v.frames.cuda()
