@@ -492,6 +492,13 @@ def main():
         # f3 denoiser variants: residual of 64 FHD SDA-like fp32 frames per call
         Ivar = frames[:64].float()
         f3 = {}
+        # the default denoiser (db4, symmetric) through the same residual call on the same fp32
+        # frames: the like-for-like denominator (x_default divides by the fused u8 extraction's
+        # per-denoise time, which reads 1 B/px and writes no residual)
+        out_def = torch.empty_like(Ivar)
+        t_def = timed(lambda: prnu.residual(Ivar, out=out_def), reps=3)
+        f3["db4_sym_default"] = {"ms_per_frame": t_def / Ivar.shape[0],
+                                 "x_default": (t_def / Ivar.shape[0]) / (ms_step / denoise_per_step)}
         for name, v in (("db8_sym", (16, 0, 0)), ("db4_per", (8, 1, 0)), ("db8_per", (16, 1, 0)),
                         ("db4_swt", (8, 1, 1)), ("db8_swt", (16, 1, 1))):
             var = prnu.DenoiseVariant(*v)
@@ -499,7 +506,8 @@ def main():
             t = timed(lambda: prnu.residual_variant(Ivar, var, out=out), reps=3)
             gb = variant_alg_bytes(H, W, 4, *v) * Ivar.shape[0] / (t / 1000.0) / 1e9
             f3[name] = {"ms_per_frame": t / Ivar.shape[0], "alg_GBps": gb, "frac_hbm": gb / peak_hbm,
-                        "x_default": (t / Ivar.shape[0]) / (ms_step / denoise_per_step)}
+                        "x_default": (t / Ivar.shape[0]) / (ms_step / denoise_per_step),
+                        "x_default_residual": t / t_def}
         # BASELINE config 4 shape (camera identification): 64 fingerprints of 300 frames
         # 1280x720 at depth 30, then 64 query residuals x 64 fingerprints = 4096 PCEs
         # (one camera's synthetic frames reused for every camera: throughput only)
