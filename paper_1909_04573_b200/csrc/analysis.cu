@@ -515,6 +515,16 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
     }
     const float s0 = a.sp.sigma0_sq;
     const float2 s0p = make_float2(s0, s0 * LF_KD2);
+    // ALL4 (windows 3, 5, 7, 9): the window means are kept scaled by 81 (the 9x9 sum needs no
+    // multiply; the 7 and 9 minima go through one 3-input min), and the Wiener factor
+    // c s0 / max(m, s0) = c (81 s0) / max(81 m, 81 s0) takes the scaled thresholds; for the
+    // (ad, dd) pair the dd lane's KD^4 / KD^2 factors move from the window weights into them
+    const float t81 = 81.0f * s0;
+    const float2 t81p = make_float2(t81, t81 / LF_KD4);   // thresholds (da / ad lane, dd lane)
+    const float2 c81p = make_float2(t81, t81 / LF_KD2);   // numerators
+    // the 7x7 term kept live for a 3-input min only where it does not spill (fp32 levels;
+    // measured: the u8 / u16 / pair instances spill at the 168-register cap and run slower)
+    constexpr bool MIN3 = ALL4 && std::is_same<T, float>::value;
     const int wm = a.sp.wmask;
     uint32_t phase = 0;
     const long long ll_off = (long long)b * a.out_bstride + gc;   // LL element offset of row 0 (a.ll may be null)
@@ -666,7 +676,7 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
                 // ---- da: region columns 8hg .. 8hg+15 of row hj
                 {
                     const float* base = DA + hj * P1 + 8 * hg;
-                    float m[8];
+                    float m[8], r7[8];
                     {
                         float u[16];
 #pragma unroll
@@ -678,7 +688,7 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
 #pragma unroll
                         for (int x = 0; x < 8; ++x) {
                             if (x > 0) s3 += u[x + 5] - u[x + 2];
-                            m[x] = (ALL4 || (wm & 1)) ? s3 * (1.0f / 9.0f) : 3.402823466e38f;
+                            m[x] = ALL4 ? s3 * 9.0f : (wm & 1) ? s3 * (1.0f / 9.0f) : 3.402823466e38f;
                         }
                     }
                     {
@@ -692,7 +702,7 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
 #pragma unroll
                         for (int x = 0; x < 8; ++x) {
                             if (x > 0) s5 += u[x + 6] - u[x + 1];
-                            if (ALL4 || (wm & 2)) m[x] = fminf(m[x], s5 * (1.0f / 25.0f));
+                            if (ALL4 || (wm & 2)) m[x] = fminf(m[x], s5 * (ALL4 ? 3.24f : 1.0f / 25.0f));
                         }
                     }
                     {
@@ -706,7 +716,9 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
 #pragma unroll
                         for (int x = 0; x < 8; ++x) {
                             if (x > 0) s7 += u[x + 7] - u[x];
-                            if (ALL4 || (wm & 4)) m[x] = fminf(m[x], s7 * (1.0f / 49.0f));
+                            if (MIN3) r7[x] = s7 * (81.0f / 49.0f);
+                            else if (ALL4) m[x] = fminf(m[x], s7 * (81.0f / 49.0f));
+                            else if (wm & 4) m[x] = fminf(m[x], s7 * (1.0f / 49.0f));
                         }
                     }
                     {
@@ -720,7 +732,9 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
 #pragma unroll
                         for (int x = 0; x < 8; ++x) {
                             if (x > 0) s9 += u[x + 8] - u[x - 1];
-                            if (ALL4 || (wm & 8)) m[x] = fminf(m[x], s9 * (1.0f / 81.0f));
+                            if (MIN3) m[x] = fminf(fminf(m[x], r7[x]), s9);   // FMNMX3
+                            else if (ALL4) m[x] = fminf(m[x], s9);
+                            else if (wm & 8) m[x] = fminf(m[x], s9 * (1.0f / 81.0f));
                         }
                     }
                     const float4 c0 = *reinterpret_cast<const float4*>(base + 4 * AL_BK * P1 + 4);
@@ -728,7 +742,8 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
                     const float cv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
                     float o[8];
 #pragma unroll
-                    for (int x = 0; x < 8; ++x) o[x] = (cv[x] * s0) * al_rcp(fmaxf(m[x], s0));
+                    for (int x = 0; x < 8; ++x)
+                        o[x] = ALL4 ? (cv[x] * t81) * al_rcp(fmaxf(m[x], t81)) : (cv[x] * s0) * al_rcp(fmaxf(m[x], s0));
                     float* drow = a.d0 + roff;
                     if (hfull) {
                         st_global_v8(drow, o);
@@ -743,7 +758,7 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
                 // ---- (ad, dd): float2 region columns 8hg .. 8hg+15 of row hj
                 {
                     const float2* base = PR + hj * P2 + 8 * hg;
-                    float2 m[8];
+                    float2 m[8], r7[8];
                     {
                         float2 u[12];   // columns 2 .. 13
 #pragma unroll
@@ -756,7 +771,8 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
 #pragma unroll
                         for (int x = 0; x < 8; ++x) {
                             if (x > 0) s3 = add2(s3, sub2(u[x + 3], u[x]));
-                            m[x] = (ALL4 || (wm & 1)) ? mul2(s3, c_al_w[0]) : make_float2(3.402823466e38f, 3.402823466e38f);
+                            m[x] = ALL4 ? mul2(s3, make_float2(9.0f, 9.0f))
+                                   : (wm & 1) ? mul2(s3, c_al_w[0]) : make_float2(3.402823466e38f, 3.402823466e38f);
                         }
                     }
                     {
@@ -772,7 +788,7 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
                         for (int x = 0; x < 8; ++x) {
                             if (x > 0) s5 = add2(s5, sub2(u[x + 4], u[x - 1]));
                             if (ALL4 || (wm & 2)) {
-                                const float2 r = mul2(s5, c_al_w[1]);
+                                const float2 r = ALL4 ? mul2(s5, make_float2(3.24f, 3.24f)) : mul2(s5, c_al_w[1]);
                                 m[x] = make_float2(fminf(m[x].x, r.x), fminf(m[x].y, r.y));
                             }
                         }
@@ -789,7 +805,12 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
 #pragma unroll
                         for (int x = 0; x < 8; ++x) {
                             if (x > 0) s7 = add2(s7, sub2(u[x + 7], u[x]));
-                            if (ALL4 || (wm & 4)) {
+                            if (MIN3) {
+                                r7[x] = mul2(s7, make_float2(81.0f / 49.0f, 81.0f / 49.0f));
+                            } else if (ALL4) {
+                                const float2 r = mul2(s7, make_float2(81.0f / 49.0f, 81.0f / 49.0f));
+                                m[x] = make_float2(fminf(m[x].x, r.x), fminf(m[x].y, r.y));
+                            } else if (wm & 4) {
                                 const float2 r = mul2(s7, c_al_w[2]);
                                 m[x] = make_float2(fminf(m[x].x, r.x), fminf(m[x].y, r.y));
                             }
@@ -807,7 +828,11 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
 #pragma unroll
                         for (int x = 0; x < 8; ++x) {
                             if (x > 0) s9 = add2(s9, sub2(u[x + 8], u[x - 1]));
-                            if (ALL4 || (wm & 8)) {
+                            if (MIN3) {   // FMNMX3 per lane
+                                m[x] = make_float2(fminf(fminf(m[x].x, r7[x].x), s9.x), fminf(fminf(m[x].y, r7[x].y), s9.y));
+                            } else if (ALL4) {
+                                m[x] = make_float2(fminf(m[x].x, s9.x), fminf(m[x].y, s9.y));
+                            } else if (wm & 8) {
                                 const float2 r = mul2(s9, c_al_w[3]);
                                 m[x] = make_float2(fminf(m[x].x, r.x), fminf(m[x].y, r.y));
                             }
@@ -817,11 +842,13 @@ __global__ void __launch_bounds__(AL_NT, MINB) k_analysis_lift(const __grid_cons
 #pragma unroll
                     for (int q2 = 0; q2 < 4; ++q2) {
                         const float4 x = *reinterpret_cast<const float4*>(base + 4 * AL_BK * P2 + 4 + 2 * q2);
-                        const float2 c0 = mul2(make_float2(x.x, x.y), s0p), c1 = mul2(make_float2(x.z, x.w), s0p);
-                        oa[2 * q2] = c0.x * al_rcp(fmaxf(m[2 * q2].x, s0));
-                        od[2 * q2] = c0.y * al_rcp(fmaxf(m[2 * q2].y, s0));
-                        oa[2 * q2 + 1] = c1.x * al_rcp(fmaxf(m[2 * q2 + 1].x, s0));
-                        od[2 * q2 + 1] = c1.y * al_rcp(fmaxf(m[2 * q2 + 1].y, s0));
+                        const float2 cs = ALL4 ? c81p : s0p;
+                        const float2 th = ALL4 ? t81p : make_float2(s0, s0);
+                        const float2 c0 = mul2(make_float2(x.x, x.y), cs), c1 = mul2(make_float2(x.z, x.w), cs);
+                        oa[2 * q2] = c0.x * al_rcp(fmaxf(m[2 * q2].x, th.x));
+                        od[2 * q2] = c0.y * al_rcp(fmaxf(m[2 * q2].y, th.y));
+                        oa[2 * q2 + 1] = c1.x * al_rcp(fmaxf(m[2 * q2 + 1].x, th.x));
+                        od[2 * q2 + 1] = c1.y * al_rcp(fmaxf(m[2 * q2 + 1].y, th.y));
                     }
                     float* arow = a.d1 + roff;
                     float* drow = a.d2 + roff;
