@@ -86,11 +86,26 @@ constexpr int SA_STAGE_COEF = 4 * SC_PS;           // floats per stage (4 planes
 // pass's halo items (coefficient columns 32 .. 35 of 4-row groups sg, one warp: banks
 // 16 sg + k) over 8 banks (4-way) where 40 put them on 4 (7-way).
 constexpr int SA_LP = 36;
+// Swizzled planes (u8 accumulation and the plain inverse levels, where the shared memory
+// for 4 CTAs/SM allows it): pitch 52 (== 20 mod 32) and row t stored 4 ((t >> 3) & 3)
+// columns to the right.  A halo item's row 4 sg + c then sits in bank
+// 16 (sg & 1) + 4 ((sg >> 1) & 3) + 20 c + (k - 32) (mod 32): the 8 row groups on 8
+// distinct bank quads, so the halo warp's stores are conflict-free (4-way at pitch 36);
+// the main items (32 consecutive columns of one row) and the row pass's LDS.128 (8 lanes:
+// 128 contiguous bytes of one row) stay conflict-free, and the shift is a per-thread
+// constant (no instruction per frame).
+constexpr int SA_LP_SWZ = 52;
+template <typename TI, int MODE>
+__host__ __device__ constexpr int sacc_lp() {
+    return (MODE == 0 || (sizeof(TI) == 1 && !std::is_same<TI, u8pair>::value)) ? SA_LP_SWZ : SA_LP;
+}
 template <int TY, typename TI, int MODE = 1>
 constexpr size_t sacc_smem_bytes() {
     return 2 * SA_STAGE_COEF * sizeof(float) + (MODE ? 3 * TY * ST_X * sizeof(TI) : 0) +
-           2 * 2 * TY * SA_LP * sizeof(float) + 2 * sizeof(uint64_t);
+           2 * 2 * TY * sacc_lp<TI, MODE>() * sizeof(float) + 2 * sizeof(uint64_t);
 }
+static_assert(4 * (sacc_smem_bytes<32, uint8_t, 1>() + 1024) <= 228 * 1024 &&
+              4 * (sacc_smem_bytes<32, float, 0>() + 1024) <= 228 * 1024, "4 CTAs/SM with the swizzled planes");
 
 // MODE 1: accumulate (frames 0 .. nb-1, one CTA per tile); MODE 0: plain inverse
 // level written to a.out (frames [z * frames_per_cta, ...) per CTA, no I tiles).
@@ -108,8 +123,10 @@ __global__ void __launch_bounds__(256, 4) k_synth_acc2(const __grid_constant__ S
     // pass): frame f+2 is issued at the barrier of frame f, two frames ahead.
     float* coef0 = smem;                                                      // [2][4][SC_PS]
     TI* itile0 = reinterpret_cast<TI*>(smem + 2 * SA_STAGE_COEF);             // [3][TY][ST_X] (MODE 1)
-    float* sL0 = reinterpret_cast<float*>(itile0 + (MODE ? 3 * TY * ST_X : 0));   // [2][2][TY][SA_LP]
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sL0 + 2 * 2 * TY * SA_LP);
+    constexpr int LP = sacc_lp<TI, MODE>();
+    constexpr bool SWZ = LP == SA_LP_SWZ;
+    float* sL0 = reinterpret_cast<float*>(itile0 + (MODE ? 3 * TY * ST_X : 0));   // [2][2][TY][LP]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sL0 + 2 * 2 * TY * LP);
     const int tid = threadIdx.x;
     const int ty0 = blockIdx.y * TY, tx0 = blockIdx.x * ST_X;
     const int ky0 = ty0 >> 1, kx0 = tx0 >> 1;
@@ -194,22 +211,29 @@ __global__ void __launch_bounds__(256, 4) k_synth_acc2(const __grid_constant__ S
     auto item_k = [](int it) { return it < 32 * (TY / 4) ? (it & 31) : 32 + (it - 32 * (TY / 4)) % (SC_X - 32); };
     auto item_sg = [](int it) { return it < 32 * (TY / 4) ? (it >> 5) : (it - 32 * (TY / 4)) / (SC_X - 32); };
     const int ck = item_k(tid), csg = item_sg(tid);
+    // an item's coefficient-tile load offset (row 2 sg) and plane store offset (row 4 sg, swizzle shift)
+    auto ld_off = [](int k, int sg) { return 2 * sg * SC_BW + k; };
+    auto st_off = [](int k, int sg) { return 4 * sg * LP + k + (SWZ ? 4 * ((sg >> 1) & 3) : 0); };
+    const int cld = ld_off(ck, csg), cst = st_off(ck, csg);
+    // row-pass plane offset of this thread's 8 columns (swizzled planes: row rt shifted 4 ((rt >> 3) & 3))
+    const int roff = rt * LP + (SWZ ? 4 * ((rt >> 3) & 3) : 0) + 4 * rg;
 
     for (int f = 0; f < nb; ++f) {
         const int st = f & 1;
         PRNU_STRESS(11);
         mbar_wait(&bar[st], (f >> 1) & 1);
         const float* c = coef0 + st * SA_STAGE_COEF;
-        float* sLo = sL0 + (f & 1) * 2 * TY * SA_LP;
-        float* sHi = sLo + TY * SA_LP;
+        float* sLo = sL0 + (f & 1) * 2 * TY * LP;
+        float* sHi = sLo + TY * LP;
         // column pass: Lx = synth_y(A, ad), Hx = synth_y(da, dd); item = (coefficient column k, 4 output rows)
         for (int it = tid; it < NITEM; it += 256) {
-            const int k = NITEM <= 256 ? ck : item_k(it), sg = NITEM <= 256 ? csg : item_sg(it);
-            PRNU_DCHECK(k < SC_X && 2 * sg + 4 < CY && 4 * sg + 3 < TY);
+            PRNU_DCHECK(item_k(it) < SC_X && 2 * item_sg(it) + 4 < CY && 4 * item_sg(it) + 3 < TY);
+            const int lo0 = NITEM <= 256 ? cld : ld_off(item_k(it), item_sg(it));
+            const int so0 = NITEM <= 256 ? cst : st_off(item_k(it), item_sg(it));
             float va[5], vda[5], vad[5], vdd[5];
 #pragma unroll
             for (int m = 0; m < 5; ++m) {
-                const int r = (2 * sg + m) * SC_BW + k;
+                const int r = lo0 + m * SC_BW;
                 va[m] = c[0 * SC_PS + r];
                 vda[m] = c[1 * SC_PS + r];
                 vad[m] = c[2 * SC_PS + r];
@@ -227,11 +251,11 @@ __global__ void __launch_bounds__(256, 4) k_synth_acc2(const __grid_constant__ S
                     h = ffma2(vda[q + m], c_sh[m], h);
                     h = ffma2(vdd[q + m], c_sg[m], h);
                 }
-                const int t = 4 * sg + 2 * q;
-                sLo[t * SA_LP + k] = l.x;
-                sLo[(t + 1) * SA_LP + k] = l.y;
-                sHi[t * SA_LP + k] = h.x;
-                sHi[(t + 1) * SA_LP + k] = h.y;
+                const int o = so0 + 2 * q * LP;   // output row 4 sg + 2 q
+                sLo[o] = l.x;
+                sLo[o + LP] = l.y;
+                sHi[o] = h.x;
+                sHi[o + LP] = h.y;
             }
         }
         __syncthreads();   // L/H planes of frame f complete; every thread is past frame f-1
@@ -244,8 +268,8 @@ __global__ void __launch_bounds__(256, 4) k_synth_acc2(const __grid_constant__ S
         // row pass of 8 pixels + accumulation
         float vl[8], vh[8];
         {   // columns 4 rg .. 4 rg + 7 (the 8th unused): two LDS.128 per plane
-            const float4* pl = reinterpret_cast<const float4*>(sLo + rt * SA_LP + 4 * rg);
-            const float4* ph = reinterpret_cast<const float4*>(sHi + rt * SA_LP + 4 * rg);
+            const float4* pl = reinterpret_cast<const float4*>(sLo + roff);
+            const float4* ph = reinterpret_cast<const float4*>(sHi + roff);
             const float4 l0 = pl[0], l1 = pl[1], h0 = ph[0], h1 = ph[1];
             vl[0] = l0.x; vl[1] = l0.y; vl[2] = l0.z; vl[3] = l0.w; vl[4] = l1.x; vl[5] = l1.y; vl[6] = l1.z; vl[7] = l1.w;
             vh[0] = h0.x; vh[1] = h0.y; vh[2] = h0.z; vh[3] = h0.w; vh[4] = h1.x; vh[5] = h1.y; vh[6] = h1.z; vh[7] = h1.w;
